@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Generate tests/golden/*.npz by RUNNING THE REFERENCE ITSELF.
+
+TEST INFRASTRUCTURE ONLY. Run in the build container (where /root/reference is
+mounted read-only); the GPU box never runs this, it only reads the committed
+fixtures:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python oracle/gen_golden.py
+
+Every array saved here is an output of the unmodified reference package
+(`orcasim`, imported from /root/reference/pkg/src) or a seeded input fed to it.
+tests/test_oracle_golden.py pins oracle/orca_oracle.c against these fixtures bit
+for bit; the GPU parity tests then compare the CUDA path both with the fixtures
+directly and with the pinned oracle on larger seeded inputs.
+
+Fixtures (all small, compressed):
+  kat.npz            shuffle permutations, problem seeds, VO exits and LP
+                     known answers (the cases of pkg/tests/test_lp.py:23-100,
+                     122-127 and pkg/tests/test_orca.py:25-50) + random VO/LP.
+  lp_batch_*.npz     K.solve_range over CSR-packed random batches, k in [8,64],
+                     feasible / mixed / infeasible.
+  frame_*.npz        engine._advance on seeded plaza crowds incl. per-agent
+                     cell (ix,iy), ordered neighbour rows, constraints, out_v,
+                     status, failed_at, new state, metrics.
+  chain_1k.npz       config 1: 100 consecutive reference steps of 1,024
+                     pedestrians (each input = previous output rounded to
+                     float32 so an FP32 device state sees identical inputs);
+                     positions/velocities stored for every step.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+REF_SRC = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import orcasim._kernels as K  # noqa: E402
+import orcasim.engine as E  # noqa: E402
+from orcasim.lp import shuffle_order  # noqa: E402
+from orcasim.scenario import ScenarioConfig as RefConfig  # noqa: E402
+
+from paper_2008_11578_b200.synth import lp_batch, plaza_crowd  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def ref_config(**kw) -> RefConfig:
+    from orcasim.orca import AgentClass, ResponsibilityMatrix
+    from orcasim.scenario import DEFAULT_CLASS_PARAMS, ClassParams
+    cfg = RefConfig(regions=[],
+                    class_params={c: ClassParams(*p) for c, p in DEFAULT_CLASS_PARAMS.items()},
+                    responsibility=ResponsibilityMatrix.default())
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+def ref_state(st) -> E.SimState:
+    return E.SimState(frame=st.frame, time=st.time, ids=st.ids, positions=st.positions,
+                      velocities=st.velocities, radii=st.radii, pref_speeds=st.pref_speeds,
+                      max_speeds=st.max_speeds, goals=st.goals, goal_tols=st.goal_tols,
+                      class_codes=st.class_codes, rng_state=None)
+
+
+# ---------------------------------------------------------------------------
+
+def gen_kat():
+    out = {}
+    ks, seeds, perms = [], [], []
+    for k in (0, 1, 2, 5, 16, 33, 64):
+        for seed in (0, 1, 2**63 - 1, 1234567890123456789, 0xDEADBEEFCAFEF00D):
+            perm = np.empty(max(k, 1), dtype=np.int64)
+            K.shuffle_into(perm, k, np.uint64(seed))
+            assert list(perm[:k]) == shuffle_order(k, seed)
+            row = np.full(64, -1, dtype=np.int64)
+            row[:k] = perm[:k]
+            ks.append(k)
+            seeds.append(seed)
+            perms.append(row)
+    out["shuffle_k"] = np.array(ks, dtype=np.int64)
+    out["shuffle_seed"] = np.array(seeds, dtype=np.uint64)
+    out["shuffle_perm"] = np.array(perms)
+
+    fr = np.array([0, 1, 2, 99, 12345, 2**31 - 1], dtype=np.int64)
+    ag = np.array([0, 1, 7, 1023, 2**31 - 1, 2**32 + 5], dtype=np.int64)
+    ps = np.empty((fr.size, ag.size), dtype=np.uint64)
+    for a, f in enumerate(fr):
+        for b, g in enumerate(ag):
+            ps[a, b] = K._problem_seed(np.int64(f), np.int64(g))
+            if g < 2**32:
+                assert int(ps[a, b]) == E.problem_seed(int(g), int(f))
+    out["seed_frames"], out["seed_ids"], out["seed_values"] = fr, ag, ps
+
+    # VO exits: the three known answers of test_orca.py:25-50 then random ones
+    rng = np.random.default_rng(31)
+    cases = [(10.0, 0.0, 0.0, 0.0, 0.5, 2.0, 0.1),
+             (2.0, 0.0, 2.0, 0.0, 1.0, 1.0, 0.1),
+             (0.4, 0.0, 0.0, 0.0, 0.5, 2.0, 0.1),
+             (0.0, 0.0, 1.0, 0.0, 0.5, 2.0, 0.1)]
+    for _ in range(4000):
+        d = 0.05 + 12.0 * rng.random()
+        a = 2 * np.pi * rng.random()
+        comb = 0.2 + 2.2 * rng.random()
+        tau = 0.5 + 3.0 * rng.random()
+        rv = rng.normal(size=2) * 3.0
+        cases.append((d * math.cos(a), d * math.sin(a), rv[0], rv[1], comb, tau, 0.1))
+    cases = f32(np.array(cases))
+    vo = np.empty((cases.shape[0], 5))
+    for i, c in enumerate(cases):
+        ux, uy, nx, ny, ok = K.vo_exit(*c)
+        vo[i] = (ux, uy, nx, ny, float(ok))
+    assert np.allclose(vo[0, :4], [4.75, 0, -1, 0]) and np.allclose(vo[1, :4], [-1, 0, -1, 0])
+    assert np.allclose(vo[2, :4], [-1, 0, -1, 0]) and vo[3, 4] == 0.0
+    out["vo_in"], out["vo_out"] = cases, vo
+
+    # LP known answers (test_lp.py:23-43, 77-100): solve_closest_point / least_penetration
+    from orcasim.lp import (HalfPlaneConstraint, LpProblem, solve_closest_point,
+                            solve_least_penetration)
+
+    def hp(p, n):
+        return HalfPlaneConstraint(np.asarray(p, float), np.asarray(n, float))
+
+    r1 = solve_closest_point(LpProblem([], (1.0, 0.5), 2.0))
+    r2 = solve_closest_point(LpProblem([], (3.0, 4.0), 2.5))
+    r3 = solve_closest_point(LpProblem([hp((0, 1), (0, 1))], (0.7, 0.2), 5.0))
+    out["lp_kat_closest"] = np.array([r1.velocity, r2.velocity, r3.velocity])
+    band_f = [hp((0, -1), (0, 1)), hp((0, 1), (0, -1))]
+    band_e = [hp((0, 1), (0, 1)), hp((0, -1), (0, -1))]
+    tri = []
+    for deg in (90, 210, 330):
+        n = np.array([math.cos(math.radians(deg)), math.sin(math.radians(deg))])
+        tri.append(hp(n, n))
+    out["lp_kat_lpen"] = np.array([
+        solve_least_penetration(band_f, 5.0, 0, (0.3, 2.0)),
+        solve_least_penetration(band_f, 5.0, 0, (-0.2, 0.4)),
+        solve_least_penetration(band_e, 5.0, 0, (0.3, 2.0)),
+        solve_least_penetration(tri, 5.0, 0, (0.4, -0.3))])
+    out["lp_kat_tri_nrm"] = np.array([c.normal for c in tri])
+    np.savez_compressed(os.path.join(OUT, "kat.npz"), **out)
+    print("kat.npz", {k: v.shape for k, v in out.items()})
+
+
+def gen_lp_batches():
+    for name, frac, n, seed in (("feasible", 0.0, 600, 1), ("mixed", 0.5, 600, 2),
+                                ("infeasible", 1.0, 600, 3), ("small_k", 0.3, 1500, 4)):
+        kmin, kmax = (0, 16) if name == "small_k" else (8, 64)
+        coff, cpts, cnrm, tgt, caps, seeds = lp_batch(n, kmin, kmax, frac, seed=seed)
+        out_v = np.empty((n, 2))
+        status = np.empty(n, dtype=np.int64)
+        failed = np.empty(n, dtype=np.int64)
+        K.solve_range(coff, cpts, cnrm, tgt, caps, seeds, out_v, status, failed, 0, n)
+        np.savez_compressed(os.path.join(OUT, f"lp_batch_{name}.npz"), coff=coff,
+                            cpts=cpts.astype(np.float32), cnrm=cnrm.astype(np.float32),
+                            tgt=tgt.astype(np.float32), caps=caps.astype(np.float32),
+                            seeds=seeds, out_v=out_v, status=status.astype(np.int8),
+                            failed=failed.astype(np.int16))
+        print(f"lp_batch_{name}.npz fallback frac {status.mean():.3f}")
+
+
+def frame_debug(state, cfg):
+    """What engine._advance computes before integration, plus the per-agent
+    neighbour rows / constraints (via K._collect_neighbors and K.vo_exit, the
+    same calls frame_solve_range makes, K:515-541)."""
+    n = state.active_count
+    cell = cfg.neighbor_radius
+    reach = int(math.ceil(cfg.neighbor_radius / cell))
+    rad2 = cfg.neighbor_radius * cfg.neighbor_radius
+    order, ukeys, starts = E._grid_arrays(state.positions, cell)
+    ix = np.floor(state.positions[:, 0] / cell).astype(np.int64)
+    iy = np.floor(state.positions[:, 1] / cell).astype(np.int64)
+    max_n = cfg.max_neighbors
+    nb_rows = np.full((n, max(max_n, 1)), -1, dtype=np.int64)
+    nb_cnt = np.zeros(n, dtype=np.int64)
+    nb_d2 = np.empty(max(max_n, 1))
+    nb_id = np.empty(max(max_n, 1), dtype=np.int64)
+    nb_ix = np.empty(max(max_n, 1), dtype=np.int64)
+    cons = np.zeros((n, max(max_n, 1), 4))
+    fmat = cfg.responsibility.as_array()
+    avoid = state.radii + 0.5 * cfg.avoidance_margin
+    for i in range(n):
+        c = 0
+        if max_n > 0:
+            c = K._collect_neighbors(i, state.positions, state.ids, order, ukeys, starts, cell,
+                                     reach, rad2, max_n, nb_d2, nb_id, nb_ix)
+        nb_cnt[i] = c
+        nb_rows[i, :c] = nb_ix[:c]
+        for t in range(c):
+            j = nb_ix[t]
+            rp = state.positions[j] - state.positions[i]
+            rv = state.velocities[i] - state.velocities[j]
+            ux, uy, nx, ny, ok = K.vo_exit(rp[0], rp[1], rv[0], rv[1], avoid[i] + avoid[j],
+                                           cfg.tau, cfg.dt)
+            assert ok
+            f = fmat[state.class_codes[i], state.class_codes[j]]
+            cons[i, t] = (state.velocities[i, 0] + f * ux, state.velocities[i, 1] + f * uy, nx, ny)
+    des = E._desired_velocities(state.positions, state.goals, state.pref_speeds, cfg.dt)
+    out_v = np.empty((n, 2))
+    status = np.empty(n, dtype=np.int64)
+    failed = np.empty(n, dtype=np.int64)
+    err = np.empty(n, dtype=np.int64)
+    K.frame_solve_range(state.positions, state.velocities, avoid, state.max_speeds,
+                        state.class_codes, state.ids, fmat, des, order, ukeys, starts, cell, reach,
+                        rad2, max_n, cfg.tau, cfg.dt, state.frame, out_v, status, failed, err, 0, n)
+    return dict(cell_ix=ix, cell_iy=iy, nb_rows=nb_rows, nb_count=nb_cnt, cons=cons, des=des,
+                out_v=out_v, status=status, failed=failed, err=err)
+
+
+def save_frame(name, state, cfg, extra=None):
+    dbg = frame_debug(state, cfg)
+    new_state, _log, min_sep, coll, fb, removed = E._advance(ref_state(state), cfg, 1, 4096, False)
+    # the fused kernel inside _advance must agree with the composed debug run
+    keep = ~np.isin(state.ids, removed)
+    assert np.array_equal(new_state.velocities, dbg["out_v"][keep])
+    d = dict(
+        frame=np.int64(state.frame), ids=state.ids, positions=state.positions.astype(np.float32),
+        velocities=state.velocities.astype(np.float32), radii=state.radii.astype(np.float32),
+        pref_speeds=state.pref_speeds.astype(np.float32),
+        max_speeds=state.max_speeds.astype(np.float32), goals=state.goals.astype(np.float32),
+        goal_tols=state.goal_tols.astype(np.float32), class_codes=state.class_codes.astype(np.int8),
+        dt=cfg.dt, tau=cfg.tau, neighbor_radius=cfg.neighbor_radius,
+        max_neighbors=np.int64(cfg.max_neighbors), avoidance_margin=cfg.avoidance_margin,
+        fmat=cfg.responsibility.as_array(),
+        cell_ix=dbg["cell_ix"].astype(np.int32), cell_iy=dbg["cell_iy"].astype(np.int32),
+        nb_rows=dbg["nb_rows"].astype(np.int32), nb_count=dbg["nb_count"].astype(np.int8),
+        cons=dbg["cons"], des=dbg["des"], out_v=dbg["out_v"], status=dbg["status"].astype(np.int8),
+        failed=dbg["failed"].astype(np.int8),
+        new_ids=new_state.ids, new_positions=new_state.positions,
+        new_velocities=new_state.velocities, removed_ids=removed,
+        min_separation=np.float64(min_sep), collision_count=np.int64(coll),
+        lp_fallbacks=np.int64(fb))
+    # inputs must be float32-representable (so an FP32 device state is exact)
+    for k in ("positions", "velocities", "radii", "pref_speeds", "max_speeds", "goals",
+              "goal_tols"):
+        assert np.array_equal(d[k].astype(np.float64), getattr(state, k)), k
+    if extra:
+        d.update(extra)
+    np.savez_compressed(os.path.join(OUT, f"frame_{name}.npz"), **d)
+    print(f"frame_{name}.npz n={state.active_count} fallbacks={fb} removed={removed.size} "
+          f"min_sep={min_sep:.4f} coll={coll}")
+
+
+def gen_frames():
+    # mixed plaza, default parameters (config 2 in miniature)
+    st, _ = plaza_crowd(480, 32, density=0.25, seed=11)
+    save_frame("mixed_512", st, ref_config())
+    # dense crowd: most agents take the fallback (config 3 in miniature)
+    st, _ = plaza_crowd(700, 20, density=2.0, seed=12)
+    st.frame = 7
+    save_frame("dense_720", st, ref_config())
+    # small radius / few neighbours, non-default responsibility, agents near their goals
+    from orcasim.orca import AgentClass, ResponsibilityMatrix
+    P, V = AgentClass.PEDESTRIAN, AgentClass.VEHICLE
+    resp = ResponsibilityMatrix({(P, P): 0.5, (V, V): 0.5, (P, V): 0.75, (V, P): 0.25})
+    st, _ = plaza_crowd(300, 60, density=0.6, seed=13, origin=(-20.0, -13.0))
+    rng = np.random.default_rng(5)
+    near = rng.permutation(360)[:60]
+    st.goals[near] = f32(st.positions[near] + rng.normal(size=(60, 2)) * 0.2)
+    st.frame = 3
+    save_frame("odd_360", st, ref_config(neighbor_radius=f32(4.0).item(), max_neighbors=5,
+                                          tau=1.5, dt=0.25, avoidance_margin=0.0,
+                                          responsibility=resp))
+    # sparse: many agents with no / few neighbours, negative coordinates
+    st, _ = plaza_crowd(200, 10, density=0.004, seed=14, origin=(-150.0, -90.0))
+    save_frame("sparse_210", st, ref_config())
+
+
+def gen_chain():
+    st, _ = plaza_crowd(1024, 0, density=0.25, seed=1)
+    cfg = ref_config()
+    state = ref_state(st)
+    n0 = state.active_count
+    steps = 100
+    pos_in = np.full((steps, n0, 2), np.nan, dtype=np.float32)
+    vel_in = np.full((steps, n0, 2), np.nan, dtype=np.float32)
+    out_v = np.full((steps, n0, 2), np.nan)
+    status = np.full((steps, n0), -1, dtype=np.int8)
+    active = np.zeros(steps, dtype=np.int64)
+    fallbacks = np.zeros(steps, dtype=np.int64)
+    min_sep = np.zeros(steps)
+    coll = np.zeros(steps, dtype=np.int64)
+    for s in range(steps):
+        ids = state.ids
+        active[s] = ids.shape[0]
+        pos_in[s, ids] = state.positions
+        vel_in[s, ids] = state.velocities
+        dbg = frame_debug(state, cfg)
+        out_v[s, ids] = dbg["out_v"]
+        status[s, ids] = dbg["status"]
+        new_state, _log, ms, cc, fb, _removed = E._advance(state, cfg, 1, 4096, False)
+        fallbacks[s], min_sep[s], coll[s] = fb, ms, cc
+        # next input = this output rounded to float32 (identical inputs for FP32 device state)
+        new_state.positions = f32(new_state.positions)
+        new_state.velocities = f32(new_state.velocities)
+        state = new_state
+    np.savez_compressed(os.path.join(OUT, "chain_1k.npz"), pos_in=pos_in, vel_in=vel_in,
+                        out_v=out_v, status=status, active=active, fallbacks=fallbacks,
+                        min_sep=min_sep, collisions=coll,
+                        goals=st.goals.astype(np.float32), radii=st.radii.astype(np.float32),
+                        pref_speeds=st.pref_speeds.astype(np.float32),
+                        max_speeds=st.max_speeds.astype(np.float32),
+                        goal_tols=st.goal_tols.astype(np.float32))
+    print("chain_1k.npz active", active[[0, -1]], "fallbacks/step", fallbacks.mean())
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    gen_kat()
+    gen_lp_batches()
+    gen_frames()
+    gen_chain()

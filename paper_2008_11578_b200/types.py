@@ -1,0 +1,167 @@
+"""Host-side mirror of the reference's public types for the steering step.
+
+Same names, fields, defaults and error behaviour as the reference so callers
+can switch imports (reference file:line, paths under pkg/src/orcasim/):
+
+    AgentClass            orca.py:31-45
+    ResponsibilityMatrix  orca.py:76-129   (default(): PP .5, VV .5, PV 1, VP 0)
+    ClassParams           scenario.py:64-68
+    ScenarioConfig        scenario.py:79-114 (hot-path fields only; the YAML
+                          schema / spawn regions are out of scope)
+    SimState              engine.py:55-87
+    FrameMetrics          engine.py:46-52
+
+Objects of the reference's own classes are accepted everywhere these are
+(attribute access only).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+__all__ = ["AgentClass", "ResponsibilityMatrix", "ClassParams", "ScenarioConfig",
+           "SimState", "FrameMetrics", "DEFAULTS", "DEFAULT_CLASS_PARAMS"]
+
+
+class AgentClass(IntEnum):
+    PEDESTRIAN = 0
+    VEHICLE = 1
+
+    @property
+    def label(self) -> str:
+        return self.name.lower()
+
+    @classmethod
+    def from_label(cls, label: str) -> "AgentClass":
+        try:
+            return cls[label.strip().upper()]
+        except KeyError:
+            raise ValueError(f"unknown agent class {label!r}") from None
+
+
+# scenario.py:43-56
+DEFAULT_CLASS_PARAMS = {
+    AgentClass.PEDESTRIAN: (0.25, 1.4, 2.0),
+    AgentClass.VEHICLE: (1.0, 3.0, 5.0),
+}
+
+DEFAULTS = {
+    "dt": 0.1,
+    "tau": 2.0,
+    "neighbor_radius": 15.0,
+    "max_neighbors": 16,
+    "clearance_time": 0.5,
+    "avoidance_margin": 0.1,
+    "seed": 0,
+}
+
+
+@dataclass
+class ResponsibilityMatrix:
+    """Avoidance fractions f[(A, B)]: the share of the exit displacement an
+    agent of class A applies when avoiding class B (orca.py:76-129)."""
+
+    f: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        clean = {}
+        for (a, b), value in self.f.items():
+            value = float(value)
+            if not 0.0 <= value <= 1.0:
+                raise ValueError(f"responsibility f[{a},{b}] = {value} outside [0, 1]")
+            clean[(AgentClass(a), AgentClass(b))] = value
+        self.f = clean
+
+    @classmethod
+    def default(cls) -> "ResponsibilityMatrix":
+        P, V = AgentClass.PEDESTRIAN, AgentClass.VEHICLE
+        return cls({(P, P): 0.5, (V, V): 0.5, (P, V): 1.0, (V, P): 0.0})
+
+    def get(self, a, b) -> float:
+        try:
+            return self.f[(AgentClass(a), AgentClass(b))]
+        except KeyError:
+            raise KeyError(f"responsibility matrix has no entry for ({a}, {b})") from None
+
+    def guarantee_holds(self, a, b) -> bool:
+        return self.get(a, b) + self.get(b, a) >= 1.0
+
+    def as_array(self) -> np.ndarray:
+        n = max(int(c) for c in AgentClass) + 1
+        arr = np.zeros((n, n), dtype=np.float64)
+        for (a, b), value in self.f.items():
+            arr[int(a), int(b)] = value
+        return arr
+
+
+@dataclass
+class ClassParams:
+    radius: float
+    pref_speed: float
+    max_speed: float
+
+
+def _default_class_params():
+    return {c: ClassParams(*p) for c, p in DEFAULT_CLASS_PARAMS.items()}
+
+
+@dataclass
+class ScenarioConfig:
+    """The fields of scenario.ScenarioConfig the per-frame step reads
+    (scenario.py:79-99). `regions` is kept for signature compatibility; spawn
+    sampling itself is outside the accelerated path."""
+
+    regions: list = field(default_factory=list)
+    class_params: dict = field(default_factory=_default_class_params)
+    responsibility: ResponsibilityMatrix = field(default_factory=ResponsibilityMatrix.default)
+    dt: float = DEFAULTS["dt"]
+    tau: float = DEFAULTS["tau"]
+    neighbor_radius: float = DEFAULTS["neighbor_radius"]
+    max_neighbors: int = DEFAULTS["max_neighbors"]
+    goal_tolerance: float | None = None
+    clearance_time: float = DEFAULTS["clearance_time"]
+    avoidance_margin: float = DEFAULTS["avoidance_margin"]
+    seed: int = DEFAULTS["seed"]
+    max_frames: int | None = None
+    warnings: list = field(default_factory=list)
+
+    def goal_tolerance_for(self, agent_class) -> float:
+        if self.goal_tolerance is not None:
+            return self.goal_tolerance
+        return self.class_params[AgentClass(agent_class)].radius
+
+
+@dataclass
+class FrameMetrics:
+    frame: int
+    wall_ms: float
+    min_separation: float
+    collision_count: int
+    active_agents: int
+
+
+@dataclass
+class SimState:
+    """Simulation state after `frame` completed steps (time = frame * dt);
+    field-for-field the reference's engine.SimState (engine.py:55-87)."""
+
+    frame: int
+    time: float
+    ids: np.ndarray
+    positions: np.ndarray
+    velocities: np.ndarray
+    radii: np.ndarray
+    pref_speeds: np.ndarray
+    max_speeds: np.ndarray
+    goals: np.ndarray
+    goal_tols: np.ndarray
+    class_codes: np.ndarray
+    rng_state: object = None
+    lp_fallbacks: int = 0
+
+    @property
+    def active_count(self) -> int:
+        return int(self.ids.shape[0])
