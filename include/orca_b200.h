@@ -1,0 +1,217 @@
+/*
+ * orca_b200.h -- C ABI of the B200-native ORCA steering step (arXiv 2008.11578).
+ *
+ * This is the drop-in boundary for the ONE path this repository accelerates:
+ * the per-frame step of the reference simulator,
+ *
+ *     engine._advance            pkg/src/orcasim/engine.py:194-295
+ *       _grid_arrays             engine.py:149-161
+ *       _desired_velocities      engine.py:133-139
+ *       frame_solve_range        pkg/src/orcasim/_kernels.py:493-556
+ *       new_pos = pos + v*dt     engine.py:249, arrivals engine.py:251-255
+ *       min_sep_range            _kernels.py:559-589 (metrics, engine.py:270-286)
+ *     solve_range                _kernels.py:306-336 (batched LP entry)
+ *
+ * The reference is pure Python + numba and has no FFI layer; the seam a
+ * maintainer would bind is the flat-array signature of frame_solve_range /
+ * solve_range and the SimState arrays of engine.py:55-74. Every entry point
+ * takes plain pointers and sizes (no torch types). Host arrays use the
+ * reference's own dtypes and layouts (float64 / int64, [n,2] row-major) so a
+ * ctypes / cffi binding passes numpy buffers straight through; see
+ * INTEGRATION.md for the stub.
+ *
+ * Conventions
+ *   - Every function returns 0 on success and a negative ORCA_E* code on
+ *     failure; orca_last_error() returns the message of the last failure on
+ *     that handle (or of the last handle-less call on this thread).
+ *   - A handle owns its device buffers and is bound to one CUDA device and one
+ *     stream. A handle is not thread-safe; distinct handles are independent.
+ *   - orca_step / orca_run are asynchronous with respect to the host; errors
+ *     raised by device code (coincident centres, grid range) are sticky and
+ *     surface at the next orca_sync / orca_download / orca_get_info.
+ *   - precision: ORCA_F32 keeps the device state and the LP arithmetic in FP32
+ *     (cell indices and neighbour-ordering keys are always FP64, so bins and
+ *     neighbour lists are bit-exact for float32-representable inputs);
+ *     ORCA_F64 keeps everything in FP64 with no FMA contraction and is
+ *     bit-identical to the reference on any input.
+ */
+#ifndef ORCA_B200_H
+#define ORCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORCA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ORCA_API __attribute__((visibility("default")))
+#else
+#define ORCA_API
+#endif
+
+enum {
+    ORCA_OK = 0,
+    ORCA_EINVAL = -1,      /* bad argument */
+    ORCA_ECUDA = -2,       /* CUDA runtime failure (message has the cudaError) */
+    ORCA_ECOINCIDENT = -3, /* engine.py:239-245: exactly coincident centres */
+    ORCA_ERANGE = -4,      /* engine.py:152-153: position outside the indexable grid */
+    ORCA_ECAPACITY = -5,   /* more agents than the handle was created for */
+    ORCA_EUNSUPPORTED = -6 /* e.g. max_neighbors above ORCA_MAX_NEIGHBORS */
+};
+
+enum { ORCA_F32 = 0, ORCA_F64 = 1 };
+
+#define ORCA_MAX_NEIGHBORS 32
+
+typedef struct orca_sim orca_sim;
+
+/* Parameters the step reads from scenario.ScenarioConfig (scenario.py:79-99)
+ * plus engine-level switches. fmat is ResponsibilityMatrix.as_array()
+ * (orca.py:123-129), row-major f[self_class][other_class]. */
+typedef struct orca_params {
+    double dt;
+    double tau;
+    double neighbor_radius;
+    double avoidance_margin;
+    double fmat[4];
+    int32_t max_neighbors;
+    int32_t remove_arrivals; /* engine.py:251-255,288-294: drop agents within goal_tol */
+    int32_t compute_metrics; /* engine.py:270-286: min_separation / collision_count */
+    int32_t reserved;
+} orca_params;
+
+/* Counters of the most recent completed step (engine.FrameMetrics, engine.py:46-52,
+ * plus SimState.frame / lp_fallbacks, engine.py:62,74). */
+typedef struct orca_info {
+    int64_t frame;           /* frames completed */
+    int64_t active_agents;   /* rows alive after arrival removal */
+    int64_t lp_fallbacks;    /* count_nonzero(out_status) of the last step (engine.py:247) */
+    int64_t removed_agents;  /* arrivals removed by the last step */
+    int64_t collision_count; /* last step; 0 unless compute_metrics */
+    double min_separation;   /* last step; +inf unless compute_metrics */
+    int32_t grid_nx, grid_ny; /* search-grid dimensions used by the last step */
+    double grid_cell;         /* search-grid cell edge (m) */
+} orca_info;
+
+/* ---- lifetime ----------------------------------------------------------- */
+
+ORCA_API int orca_abi_version(void);
+
+/* Create a handle for up to `capacity` agents on CUDA device `device`. */
+ORCA_API int orca_create(orca_sim **out, int device, int64_t capacity, int precision);
+ORCA_API void orca_destroy(orca_sim *sim);
+
+/* Use an existing CUDA stream (cudaStream_t passed as void*; NULL = the
+ * handle's own stream). Lets the caller order the step against its own work. */
+ORCA_API int orca_set_stream(orca_sim *sim, void *cuda_stream);
+
+ORCA_API int orca_set_params(orca_sim *sim, const orca_params *params);
+
+ORCA_API const char *orca_last_error(const orca_sim *sim);
+
+/* ---- state in / out (engine.SimState arrays, engine.py:55-74) ------------ */
+
+/* Host -> device. positions/velocities/goals are [n,2] row-major float64, the
+ * rest [n]. `frame` is SimState.frame (frames completed so far). Pinned host
+ * memory makes the copy asynchronous; pageable memory works too. */
+ORCA_API int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_t *ids,
+                const double *positions, const double *velocities, const double *radii,
+                const double *pref_speeds, const double *max_speeds, const double *goals,
+                const double *goal_tols, const int64_t *class_codes);
+
+/* Device -> host; synchronises. Any pointer may be NULL to skip that array.
+ * Arrays must hold orca_info.active_agents rows (query with orca_get_info).
+ * status / failed_at are the out_status / out_failed of the last step for the
+ * surviving rows (_kernels.py:553-556; failed_at is the neighbour rank). */
+ORCA_API int orca_download(orca_sim *sim, int64_t *ids, double *positions, double *velocities,
+                  double *radii, double *pref_speeds, double *max_speeds, double *goals,
+                  double *goal_tols, int64_t *class_codes);
+
+/* Only positions and velocities (the arrays a step changes). */
+ORCA_API int orca_download_pv(orca_sim *sim, double *positions, double *velocities);
+
+/* Host -> device refresh of positions and velocities only (same n, same rows). */
+ORCA_API int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
+                   const double *velocities);
+
+/* ---- stepping ------------------------------------------------------------ */
+
+/* One frame of engine._advance on the resident state (asynchronous). */
+ORCA_API int orca_step(orca_sim *sim);
+
+/* `steps` consecutive frames without host round trips. */
+ORCA_API int orca_run(orca_sim *sim, int64_t steps);
+
+/* Wait for all queued work and report sticky device errors:
+ * ORCA_ECOINCIDENT with the reference's message
+ *   "frame F: agents A and B have exactly coincident centers; avoidance direction is undefined"
+ * or ORCA_ERANGE with "agent position out of indexable grid range". */
+ORCA_API int orca_sync(orca_sim *sim);
+
+/* Synchronises, then fills `info`. */
+ORCA_API int orca_get_info(orca_sim *sim, orca_info *info);
+
+/* One whole reference step() through host buffers: upload of positions and
+ * velocities, one frame, download of the new positions / velocities and the
+ * per-row solver status (engine.step, engine.py:298-308, with the static agent
+ * attributes already resident from orca_upload). Requires remove_arrivals == 0.
+ * out_status may be NULL. */
+ORCA_API int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
+                   const double *velocities, double *new_positions, double *new_velocities,
+                   int64_t *out_status);
+
+/* ---- parity taps (pre-step snapshot of the LAST step; storage-row order) --- */
+
+/* cell_ix/cell_iy: floor(pos / neighbor_radius) as int64 (engine.py:150-151).
+ * nb_rows [n, max_neighbors] (-1 padded) and nb_count [n]: the ordered
+ * neighbour rows of _collect_neighbors (_kernels.py:450-490).
+ * out_v [n,2], status, failed_at: what frame_solve_range wrote
+ * (_kernels.py:543-556). Valid only when the last step removed no agents or
+ * remove_arrivals == 0; n is the agent count BEFORE that step. Any pointer may
+ * be NULL. */
+ORCA_API int orca_debug_last_step(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_iy,
+                         int64_t *nb_rows, int64_t *nb_count, double *out_v, int64_t *status,
+                         int64_t *failed_at, double *desired_v);
+
+/* ---- batched LP (lp.solve_batch / _kernels.solve_range, CSR layout) -------- */
+
+/* Host arrays in the layout of _kernels.py:306-312: coff int64[n+1], cpts/cnrm
+ * float64[m,2], tgt float64[n,2], caps float64[n], seeds uint64[n]; outputs
+ * out_v float64[n,2], out_status int64[n] (0 feasible, 1 fallback used),
+ * out_failed int64[n] (original constraint index or -1). Synchronous. */
+ORCA_API int orca_lp_solve_batch(int device, int precision, int64_t n, const int64_t *coff,
+                        const double *cpts, const double *cnrm, const double *tgt,
+                        const double *caps, const uint64_t *seeds, double *out_v,
+                        int64_t *out_status, int64_t *out_failed);
+
+/* Resident variant for benchmarking: build once, solve many times on device. */
+typedef struct orca_lp_batch orca_lp_batch;
+ORCA_API int orca_lp_batch_create(orca_lp_batch **out, int device, int precision, int64_t n,
+                         const int64_t *coff, const double *cpts, const double *cnrm,
+                         const double *tgt, const double *caps, const uint64_t *seeds);
+ORCA_API int orca_lp_batch_set_stream(orca_lp_batch *b, void *cuda_stream);
+ORCA_API int orca_lp_batch_solve(orca_lp_batch *b);             /* asynchronous */
+ORCA_API int orca_lp_batch_download(orca_lp_batch *b, double *out_v, int64_t *out_status,
+                           int64_t *out_failed);        /* synchronises */
+ORCA_API void orca_lp_batch_destroy(orca_lp_batch *b);
+
+/* ---- single-op taps for known-answer tests -------------------------------- */
+
+/* vo_exit (_kernels.py:343-419) evaluated on the device for `count` cases;
+ * in7 = (rpx, rpy, rvx, rvy, comb_r, tau, dt) per case, out5 = (ux, uy, nx, ny, ok). */
+ORCA_API int orca_vo_exit_batch(int device, int precision, int64_t count, const double *in7,
+                       double *out5);
+
+/* Fisher-Yates order (_kernels.py:43-54) computed on the device: perm[k]. */
+ORCA_API int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *perm);
+
+/* _problem_seed (_kernels.py:57-61) computed on the device. */
+ORCA_API int orca_problem_seed(int device, int64_t frame, int64_t agent_id, uint64_t *seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORCA_B200_H */

@@ -1,8 +1,18 @@
 """B200-native ORCA steering step (arXiv 2008.11578) behind the reference's
-public simulation API. See DESIGN.md."""
+public simulation API. See DESIGN.md / INTEGRATION.md.
+
+Importing the package does not touch the GPU; the first call into
+`engine` / `lp` loads liborca_b200.so and fails loudly if it (or a CUDA device)
+is missing -- there is no CPU fallback.
+"""
 
 from .types import (AgentClass, ClassParams, FrameMetrics, ResponsibilityMatrix,
                     ScenarioConfig, SimState)
+from .engine import Simulation, desired_velocity, init_state, problem_seed, step
+from .lp import (HalfPlaneConstraint, LpBatch, LpProblem, LpResult, LpStatus, shuffle_order,
+                 solve_batch, solve_closest_point, solve_range)
 
 __all__ = ["AgentClass", "ClassParams", "FrameMetrics", "ResponsibilityMatrix",
-           "ScenarioConfig", "SimState"]
+           "ScenarioConfig", "SimState", "Simulation", "desired_velocity", "init_state",
+           "problem_seed", "step", "HalfPlaneConstraint", "LpBatch", "LpProblem", "LpResult",
+           "LpStatus", "shuffle_order", "solve_batch", "solve_closest_point", "solve_range"]

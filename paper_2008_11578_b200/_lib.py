@@ -1,0 +1,129 @@
+"""ctypes binding of liborca_b200.so (the C ABI in include/orca_b200.h).
+
+There is no CPU fallback: `load()` raises if the shared library has not been
+built (`python -c "import __graft_entry__ as g; g.build()"` or
+`make -C paper_2008_11578_b200/csrc`), and every entry point fails with
+OrcaError if no CUDA device is usable.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liborca_b200.so")
+
+ORCA_F32, ORCA_F64 = 0, 1
+ORCA_MAX_NEIGHBORS = 32
+ORCA_ECOINCIDENT, ORCA_ERANGE = -3, -4
+
+# every symbol include/orca_b200.h declares (checked by tests/test_abi.py)
+SYMBOLS = [
+    "orca_abi_version", "orca_create", "orca_destroy", "orca_set_stream", "orca_set_params",
+    "orca_last_error", "orca_upload", "orca_download", "orca_download_pv", "orca_upload_pv",
+    "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host",
+    "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
+    "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
+    "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
+]
+
+
+class OrcaError(RuntimeError):
+    """A C-ABI call failed; .code is the ORCA_E* value."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[orca_b200 rc={code}] {message}")
+        self.code = code
+        self.message = message
+
+
+class OrcaParams(C.Structure):
+    _fields_ = [("dt", C.c_double), ("tau", C.c_double), ("neighbor_radius", C.c_double),
+                ("avoidance_margin", C.c_double), ("fmat", C.c_double * 4),
+                ("max_neighbors", C.c_int32), ("remove_arrivals", C.c_int32),
+                ("compute_metrics", C.c_int32), ("reserved", C.c_int32)]
+
+
+class OrcaInfo(C.Structure):
+    _fields_ = [("frame", C.c_int64), ("active_agents", C.c_int64), ("lp_fallbacks", C.c_int64),
+                ("removed_agents", C.c_int64), ("collision_count", C.c_int64),
+                ("min_separation", C.c_double), ("grid_nx", C.c_int32), ("grid_ny", C.c_int32),
+                ("grid_cell", C.c_double)]
+
+
+_lib = None
+
+
+def load():
+    """Load liborca_b200.so and declare its prototypes. Raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: the CUDA extension has not been built. Run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (needs nvcc). "
+            "paper_2008_11578_b200 has no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, f64, u64, ci = C.c_void_p, C.c_int64, C.c_double, C.c_uint64, C.c_int
+    P = C.POINTER
+    L.orca_abi_version.restype = ci
+    L.orca_create.argtypes = [P(vp), ci, i64, ci]
+    L.orca_destroy.argtypes = [vp]
+    L.orca_destroy.restype = None
+    L.orca_set_stream.argtypes = [vp, vp]
+    L.orca_set_params.argtypes = [vp, P(OrcaParams)]
+    L.orca_last_error.argtypes = [vp]
+    L.orca_last_error.restype = C.c_char_p
+    L.orca_upload.argtypes = [vp, i64, i64] + [vp] * 9
+    L.orca_download.argtypes = [vp] + [vp] * 9
+    L.orca_download_pv.argtypes = [vp, vp, vp]
+    L.orca_upload_pv.argtypes = [vp, i64, i64, vp, vp]
+    L.orca_step.argtypes = [vp]
+    L.orca_run.argtypes = [vp, i64]
+    L.orca_sync.argtypes = [vp]
+    L.orca_get_info.argtypes = [vp, P(OrcaInfo)]
+    L.orca_step_host.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp]
+    L.orca_debug_last_step.argtypes = [vp, i64] + [vp] * 8
+    L.orca_lp_solve_batch.argtypes = [ci, ci, i64] + [vp] * 9
+    L.orca_lp_batch_create.argtypes = [P(vp), ci, ci, i64] + [vp] * 6
+    L.orca_lp_batch_set_stream.argtypes = [vp, vp]
+    L.orca_lp_batch_solve.argtypes = [vp]
+    L.orca_lp_batch_download.argtypes = [vp, vp, vp, vp]
+    L.orca_lp_batch_destroy.argtypes = [vp]
+    L.orca_lp_batch_destroy.restype = None
+    L.orca_vo_exit_batch.argtypes = [ci, ci, i64, vp, vp]
+    L.orca_shuffle_order.argtypes = [ci, i64, u64, vp]
+    L.orca_problem_seed.argtypes = [ci, i64, i64, P(u64)]
+    for name in SYMBOLS:
+        fn = getattr(L, name)
+        if name not in ("orca_destroy", "orca_last_error", "orca_lp_batch_destroy"):
+            fn.restype = ci
+    _lib = L
+    return L
+
+
+def check(rc: int, handle=None):
+    if rc == 0:
+        return
+    msg = load().orca_last_error(handle)
+    raise OrcaError(rc, msg.decode("utf-8", "replace") if msg else "unknown error")
+
+
+def ptr(a):
+    """void* of a C-contiguous numpy array (or NULL for None)."""
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return C.c_void_p(a.ctypes.data)
+
+
+def precision_code(precision) -> int:
+    if precision in (ORCA_F32, "f32", "float32", np.float32):
+        return ORCA_F32
+    if precision in (ORCA_F64, "f64", "float64", np.float64):
+        return ORCA_F64
+    raise ValueError(f"unknown precision {precision!r} (use 'f32' or 'f64')")

@@ -1,0 +1,1019 @@
+// orca_api.cu -- host side of the C ABI declared in include/orca_b200.h.
+//
+// No CPU fallback lives here: every entry point either launches the sm_100a
+// kernels of orca_kernels.cuh / orca_lp_batch.cuh or fails with an error code.
+#include <cmath>
+#include <cstdarg>
+#include <cstdlib>
+#include <new>
+#include <vector>
+
+#include "orca_kernels.cuh"
+#include "orca_lp_batch.cuh"
+
+using namespace orca;
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+
+struct orca_sim {
+    int device = 0;
+    int precision = ORCA_F32;
+    int64_t capacity = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    orca_params params{};
+    bool have_params = false;
+    bool loaded = false;
+    int64_t frame = 0;   // frames completed (host mirror)
+    int64_t n_bound = 0; // host-side upper bound on resident rows (owned + ghost)
+    int64_t n_pre = 0;   // n_bound before the last step (parity taps)
+
+    // state, storage-row order
+    void *pv[3] = {nullptr, nullptr, nullptr}; // (x, y, vx, vy)
+    int cur = 0;                               // pv[cur] is the current snapshot
+    int pre = 0;                               // pv[pre] is the pre-step snapshot of the last step
+    void *goalpref[2] = {nullptr, nullptr};    // (gx, gy, pref_speed, goal_tol)
+    void *radmax[2] = {nullptr, nullptr};      // (radius, max_speed)
+    i64 *ids[2] = {nullptr, nullptr};
+    u8 *cls[2] = {nullptr, nullptr};
+    i8 *status[2] = {nullptr, nullptr};
+    i8 *failed[2] = {nullptr, nullptr};
+    int acur = 0;
+    u8 *arrived = nullptr;
+    int *keep = nullptr, *dst_idx = nullptr;
+
+    // per-step scratch
+    int max_cells = 0;
+    int *cell_of = nullptr, *rank_of = nullptr, *cell_count = nullptr, *cell_start = nullptr,
+        *block_sums = nullptr;
+    void *s_xy = nullptr, *s_pv = nullptr, *s_dm = nullptr;
+    int *s_row = nullptr, *s_cell = nullptr;
+    u8 *s_cls = nullptr;
+    int *nb = nullptr;
+    u8 *nb_cnt = nullptr;
+    int *fq = nullptr;
+    void *fq_state = nullptr;
+    GridPlan *plan = nullptr;
+    GridPlan *h_plan = nullptr; // pinned mirror
+
+    // float64 staging in the reference's host layout
+    double *stg = nullptr;
+    size_t stg_bytes = 0;
+    double *dbg = nullptr;
+    size_t dbg_bytes = 0;
+
+    int64_t binned_frame = -1; // the sorted arrays describe the state after this many frames
+    char err[512] = {0};
+};
+
+static thread_local char g_err[512] = {0};
+
+static int fail(orca_sim *sim, int code, const char *fmt, ...)
+{
+    char *dst = sim ? sim->err : g_err;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(dst, 512, fmt, ap);
+    va_end(ap);
+    if (sim) memcpy(g_err, sim->err, 512);
+    return code;
+}
+
+#define CK(sim, call)                                                                             \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(sim, ORCA_ECUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_),      \
+                        __FILE__, __LINE__, cudaGetErrorString(e_));                              \
+    } while (0)
+
+#define CKL(sim) CK(sim, cudaGetLastError())
+
+template <typename T> static cudaError_t dalloc(T **p, size_t count)
+{
+    return cudaMalloc(reinterpret_cast<void **>(p), (count ? count : 1) * sizeof(T));
+}
+
+static constexpr int pick_threads(int bytes_per_thread)
+{
+    return bytes_per_thread * 128 <= 72 * 1024 ? 128 : (bytes_per_thread * 64 <= 72 * 1024 ? 64 : 32);
+}
+
+template <typename R, int MAXN> struct KCfg {
+    typedef typename Vec<R>::T4 R4;
+    static constexpr int solve_bpt = (int)sizeof(R4) * MAXN + MAXN;
+    static constexpr int solve_threads = pick_threads(solve_bpt);
+    static constexpr int fb_bpt = 2 * (int)sizeof(R4) * MAXN + 2 * MAXN;
+    static constexpr int fb_threads = pick_threads(fb_bpt);
+};
+
+extern "C" int orca_abi_version(void) { return ORCA_ABI_VERSION; }
+
+extern "C" const char *orca_last_error(const orca_sim *sim) { return sim ? sim->err : g_err; }
+
+// ---------------------------------------------------------------------------
+// create / destroy
+// ---------------------------------------------------------------------------
+
+template <typename R, int MAXN> static cudaError_t set_smem_attrs()
+{
+    typedef KCfg<R, MAXN> C;
+    cudaError_t e = cudaFuncSetAttribute(k_solve<R, MAXN, C::solve_threads>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::solve_bpt * C::solve_threads);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_fallback<R, MAXN, C::fb_threads>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::fb_bpt * C::fb_threads);
+}
+
+extern "C" void orca_destroy(orca_sim *sim)
+{
+    if (!sim) return;
+    cudaSetDevice(sim->device);
+    if (sim->stream) cudaStreamSynchronize(sim->stream);
+    for (int i = 0; i < 3; ++i) cudaFree(sim->pv[i]);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(sim->goalpref[i]);
+        cudaFree(sim->radmax[i]);
+        cudaFree(sim->ids[i]);
+        cudaFree(sim->cls[i]);
+        cudaFree(sim->status[i]);
+        cudaFree(sim->failed[i]);
+    }
+    cudaFree(sim->arrived);
+    cudaFree(sim->keep);
+    cudaFree(sim->dst_idx);
+    cudaFree(sim->cell_of);
+    cudaFree(sim->rank_of);
+    cudaFree(sim->cell_count);
+    cudaFree(sim->cell_start);
+    cudaFree(sim->block_sums);
+    cudaFree(sim->s_xy);
+    cudaFree(sim->s_pv);
+    cudaFree(sim->s_dm);
+    cudaFree(sim->s_row);
+    cudaFree(sim->s_cell);
+    cudaFree(sim->s_cls);
+    cudaFree(sim->nb);
+    cudaFree(sim->nb_cnt);
+    cudaFree(sim->fq);
+    cudaFree(sim->fq_state);
+    cudaFree(sim->plan);
+    cudaFree(sim->stg);
+    cudaFree(sim->dbg);
+    if (sim->h_plan) cudaFreeHost(sim->h_plan);
+    if (sim->own_stream) cudaStreamDestroy(sim->own_stream);
+    delete sim;
+}
+
+extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int precision)
+{
+    if (!out) return fail(nullptr, ORCA_EINVAL, "orca_create: out is NULL");
+    *out = nullptr;
+    if (capacity < 0 || capacity > 0x3FFFFFFF)
+        return fail(nullptr, ORCA_EINVAL, "orca_create: capacity %lld out of range", (long long)capacity);
+    if (precision != ORCA_F32 && precision != ORCA_F64)
+        return fail(nullptr, ORCA_EINVAL, "orca_create: unknown precision %d", precision);
+    int ndev = 0;
+    CK(nullptr, cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(nullptr, ORCA_EINVAL, "orca_create: device %d not available (%d visible)", device, ndev);
+    CK(nullptr, cudaSetDevice(device));
+
+    orca_sim *sim = new (std::nothrow) orca_sim();
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_create: out of host memory");
+    sim->device = device;
+    sim->precision = precision;
+    sim->capacity = capacity;
+    const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
+    const size_t rs = precision == ORCA_F32 ? sizeof(float) : sizeof(double);
+    sim->max_cells = (int)(2 * cap + 1024);
+
+#define CKC(call)                                                                                 \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            int rc_ = fail(nullptr, ORCA_ECUDA, "orca_create: %s: %s", #call, cudaGetErrorString(e_)); \
+            orca_destroy(sim);                                                                    \
+            return rc_;                                                                           \
+        }                                                                                         \
+    } while (0)
+
+    CKC(cudaStreamCreateWithFlags(&sim->own_stream, cudaStreamNonBlocking));
+    sim->stream = sim->own_stream;
+    for (int i = 0; i < 3; ++i) CKC(cudaMalloc(&sim->pv[i], cap * 4 * rs));
+    for (int i = 0; i < 2; ++i) {
+        CKC(cudaMalloc(&sim->goalpref[i], cap * 4 * rs));
+        CKC(cudaMalloc(&sim->radmax[i], cap * 2 * rs));
+        CKC(dalloc(&sim->ids[i], cap));
+        CKC(dalloc(&sim->cls[i], cap));
+        CKC(dalloc(&sim->status[i], cap));
+        CKC(dalloc(&sim->failed[i], cap));
+    }
+    CKC(dalloc(&sim->arrived, cap));
+    CKC(dalloc(&sim->keep, cap + 1));
+    CKC(dalloc(&sim->dst_idx, cap + 1));
+    CKC(dalloc(&sim->cell_of, cap));
+    CKC(dalloc(&sim->rank_of, cap));
+    CKC(dalloc(&sim->cell_count, (size_t)sim->max_cells + 1));
+    CKC(dalloc(&sim->cell_start, (size_t)sim->max_cells + 1));
+    CKC(dalloc(&sim->block_sums, (size_t)sim->max_cells / SCAN_TILE + 2));
+    CKC(cudaMalloc(&sim->s_xy, cap * 2 * rs));
+    CKC(cudaMalloc(&sim->s_pv, cap * 4 * rs));
+    CKC(cudaMalloc(&sim->s_dm, cap * 4 * rs));
+    CKC(dalloc(&sim->s_row, cap));
+    CKC(dalloc(&sim->s_cell, cap));
+    CKC(dalloc(&sim->s_cls, cap));
+    CKC(dalloc(&sim->nb, cap * ORCA_MAX_NEIGHBORS));
+    CKC(dalloc(&sim->nb_cnt, cap));
+    CKC(dalloc(&sim->fq, cap));
+    CKC(cudaMalloc(&sim->fq_state, cap * 4 * rs));
+    CKC(dalloc(&sim->plan, 1));
+    CKC(cudaMallocHost(reinterpret_cast<void **>(&sim->h_plan), sizeof(GridPlan)));
+    sim->stg_bytes = cap * 12 * sizeof(double);
+    CKC(cudaMalloc(reinterpret_cast<void **>(&sim->stg), sim->stg_bytes));
+    CKC(cudaMemset(sim->plan, 0, sizeof(GridPlan)));
+    CKC((set_smem_attrs<float, 16>()));
+    CKC((set_smem_attrs<float, 32>()));
+    CKC((set_smem_attrs<double, 16>()));
+    CKC((set_smem_attrs<double, 32>()));
+#undef CKC
+    *out = sim;
+    return ORCA_OK;
+}
+
+extern "C" int orca_set_stream(orca_sim *sim, void *cuda_stream)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_set_stream: sim is NULL");
+    CK(sim, cudaSetDevice(sim->device));
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    sim->stream = cuda_stream ? reinterpret_cast<cudaStream_t>(cuda_stream) : sim->own_stream;
+    return ORCA_OK;
+}
+
+extern "C" int orca_set_params(orca_sim *sim, const orca_params *p)
+{
+    if (!sim || !p) return fail(sim, ORCA_EINVAL, "orca_set_params: NULL argument");
+    if (!(p->dt > 0.0) || !std::isfinite(p->dt))
+        return fail(sim, ORCA_EINVAL, "dt must be positive, got %g", p->dt);
+    if (!(p->tau > 0.0) || !std::isfinite(p->tau))
+        return fail(sim, ORCA_EINVAL, "tau must be positive, got %g", p->tau);
+    if (!(p->neighbor_radius > 0.0) || !std::isfinite(p->neighbor_radius))
+        return fail(sim, ORCA_EINVAL, "neighbor_radius must be positive, got %g", p->neighbor_radius);
+    if (p->max_neighbors < 0)
+        return fail(sim, ORCA_EINVAL, "max_neighbors must be >= 0, got %d", p->max_neighbors);
+    if (p->max_neighbors > ORCA_MAX_NEIGHBORS)
+        return fail(sim, ORCA_EUNSUPPORTED, "max_neighbors %d exceeds ORCA_MAX_NEIGHBORS (%d)",
+                    p->max_neighbors, ORCA_MAX_NEIGHBORS);
+    sim->params = *p;
+    sim->have_params = true;
+    sim->binned_frame = -1;
+    return ORCA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// upload / download
+// ---------------------------------------------------------------------------
+
+static inline dim3 grid_for(int64_t n, int threads) { return dim3((unsigned)std::max<int64_t>(1, (n + threads - 1) / threads)); }
+
+template <typename R>
+static int upload_pv_impl(orca_sim *sim, int64_t n, const double *positions, const double *velocities)
+{
+    typedef typename Vec<R>::T4 R4;
+    double *d_pos = sim->stg, *d_vel = sim->stg + 2 * n;
+    CK(sim, cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, sim->stream));
+    CK(sim, cudaMemcpyAsync(d_vel, velocities, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, sim->stream));
+    k_import_pv<R><<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, d_pos, d_vel,
+                                                              reinterpret_cast<R4 *>(sim->pv[sim->cur]));
+    CKL(sim);
+    return ORCA_OK;
+}
+
+template <typename R>
+static int upload_attrs_impl(orca_sim *sim, int64_t n, const double *radii, const double *pref,
+                             const double *maxs, const double *goals, const double *gtol,
+                             const int64_t *cls)
+{
+    typedef typename Vec<R>::T4 R4;
+    typedef typename Vec<R>::T2 R2;
+    double *b = sim->stg + 4 * n;
+    double *d_rad = b, *d_pref = b + n, *d_max = b + 2 * n, *d_goal = b + 3 * n, *d_gtol = b + 5 * n;
+    i64 *d_cls = reinterpret_cast<i64 *>(b + 6 * n);
+    cudaStream_t st = sim->stream;
+    CK(sim, cudaMemcpyAsync(d_rad, radii, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(sim, cudaMemcpyAsync(d_pref, pref, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(sim, cudaMemcpyAsync(d_max, maxs, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(sim, cudaMemcpyAsync(d_goal, goals, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
+    CK(sim, cudaMemcpyAsync(d_gtol, gtol, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(sim, cudaMemcpyAsync(d_cls, cls, sizeof(i64) * n, cudaMemcpyHostToDevice, st));
+    k_import_attrs<R><<<grid_for(n, 256), 256, 0, st>>>(
+        (int)n, d_rad, d_pref, d_max, d_goal, d_gtol, d_cls,
+        reinterpret_cast<R4 *>(sim->goalpref[sim->acur]), reinterpret_cast<R2 *>(sim->radmax[sim->acur]),
+        sim->cls[sim->acur]);
+    CKL(sim);
+    return ORCA_OK;
+}
+
+static int reset_plan(orca_sim *sim, int64_t n, int64_t frame)
+{
+    GridPlan h;
+    memset(&h, 0, sizeof(h));
+    h.n = (int)n;
+    h.n_owned = (int)n;
+    h.n_after = (int)n;
+    h.err_pair = ORCA_NO_ERR;
+    h.err_frame = -1;
+    h.frame = frame;
+    h.min_sep_enc = enc_double(INFINITY);
+    *sim->h_plan = h;
+    CK(sim, cudaMemcpyAsync(sim->plan, sim->h_plan, sizeof(GridPlan), cudaMemcpyHostToDevice, sim->stream));
+    // the pinned mirror is reused by later reads; make sure this copy has left it
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    return ORCA_OK;
+}
+
+extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_t *ids,
+                           const double *positions, const double *velocities, const double *radii,
+                           const double *pref_speeds, const double *max_speeds, const double *goals,
+                           const double *goal_tols, const int64_t *class_codes)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_upload: sim is NULL");
+    if (n < 0) return fail(sim, ORCA_EINVAL, "orca_upload: n = %lld", (long long)n);
+    if (n > sim->capacity)
+        return fail(sim, ORCA_ECAPACITY, "orca_upload: %lld agents exceed the handle capacity %lld",
+                    (long long)n, (long long)sim->capacity);
+    if (n > 0 && (!ids || !positions || !velocities || !radii || !pref_speeds || !max_speeds || !goals ||
+                  !goal_tols || !class_codes))
+        return fail(sim, ORCA_EINVAL, "orca_upload: NULL array");
+    CK(sim, cudaSetDevice(sim->device));
+    sim->cur = 0;
+    sim->pre = 0;
+    sim->acur = 0;
+    int rc = reset_plan(sim, n, frame);
+    if (rc) return rc;
+    if (n > 0) {
+        CK(sim, cudaMemcpyAsync(sim->ids[0], ids, sizeof(i64) * n, cudaMemcpyHostToDevice, sim->stream));
+        CK(sim, cudaMemsetAsync(sim->status[0], 0, n, sim->stream));
+        CK(sim, cudaMemsetAsync(sim->failed[0], 0xFF, n, sim->stream));
+        rc = sim->precision == ORCA_F32 ? upload_pv_impl<float>(sim, n, positions, velocities)
+                                        : upload_pv_impl<double>(sim, n, positions, velocities);
+        if (rc) return rc;
+        rc = sim->precision == ORCA_F32
+                 ? upload_attrs_impl<float>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes)
+                 : upload_attrs_impl<double>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes);
+        if (rc) return rc;
+    }
+    sim->frame = frame;
+    sim->n_bound = n;
+    sim->n_pre = n;
+    sim->loaded = true;
+    sim->binned_frame = -1;
+    return ORCA_OK;
+}
+
+extern "C" int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
+                              const double *velocities)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_upload_pv: no resident state");
+    if (n != sim->n_bound)
+        return fail(sim, ORCA_EINVAL, "orca_upload_pv: n = %lld but %lld rows are resident", (long long)n,
+                    (long long)sim->n_bound);
+    if (n > 0 && (!positions || !velocities)) return fail(sim, ORCA_EINVAL, "orca_upload_pv: NULL array");
+    CK(sim, cudaSetDevice(sim->device));
+    sim->frame = frame;
+    sim->binned_frame = -1;
+    if (n == 0) return ORCA_OK;
+    return sim->precision == ORCA_F32 ? upload_pv_impl<float>(sim, n, positions, velocities)
+                                      : upload_pv_impl<double>(sim, n, positions, velocities);
+}
+
+// copy the device plan to the pinned mirror and wait
+static int fetch_plan(orca_sim *sim)
+{
+    CK(sim, cudaSetDevice(sim->device));
+    CK(sim, cudaMemcpyAsync(sim->h_plan, sim->plan, sizeof(GridPlan), cudaMemcpyDeviceToHost, sim->stream));
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    const GridPlan &h = *sim->h_plan;
+    sim->n_bound = h.n;
+    if (h.err_range) return fail(sim, ORCA_ERANGE, "agent position out of indexable grid range");
+    if (h.err_pair != ORCA_NO_ERR)
+        return fail(sim, ORCA_ECOINCIDENT,
+                    "frame %lld: agents %lld and %lld have exactly coincident centers; "
+                    "avoidance direction is undefined",
+                    (long long)h.err_frame, (long long)h.err_id_i, (long long)h.err_id_j);
+    return ORCA_OK;
+}
+
+extern "C" int orca_sync(orca_sim *sim)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_sync: sim is NULL");
+    return fetch_plan(sim);
+}
+
+extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
+{
+    if (!sim || !info) return fail(sim, ORCA_EINVAL, "orca_get_info: NULL argument");
+    int rc = fetch_plan(sim);
+    const GridPlan &h = *sim->h_plan;
+    info->frame = h.frame;
+    info->active_agents = h.n_owned;
+    info->lp_fallbacks = h.fq_count;
+    info->removed_agents = h.removed;
+    info->collision_count = (int64_t)h.collisions;
+    info->min_separation = dec_double(h.min_sep_enc);
+    info->grid_nx = h.nx;
+    info->grid_ny = h.ny;
+    info->grid_cell = h.cell;
+    return rc;
+}
+
+template <typename R> static int download_pv_impl(orca_sim *sim, int64_t n, double *positions, double *velocities)
+{
+    typedef typename Vec<R>::T4 R4;
+    double *d_pos = sim->stg, *d_vel = sim->stg + 2 * n;
+    k_export_pv<R><<<grid_for(n, 256), 256, 0, sim->stream>>>(
+        (int)n, reinterpret_cast<const R4 *>(sim->pv[sim->cur]), d_pos, d_vel);
+    CKL(sim);
+    if (positions)
+        CK(sim, cudaMemcpyAsync(positions, d_pos, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, sim->stream));
+    if (velocities)
+        CK(sim, cudaMemcpyAsync(velocities, d_vel, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, sim->stream));
+    return ORCA_OK;
+}
+
+template <typename R>
+static int download_attrs_impl(orca_sim *sim, int64_t n, double *radii, double *pref, double *maxs,
+                               double *goals, double *gtol, int64_t *cls)
+{
+    typedef typename Vec<R>::T4 R4;
+    typedef typename Vec<R>::T2 R2;
+    double *b = sim->stg + 4 * n;
+    double *d_rad = b, *d_pref = b + n, *d_max = b + 2 * n, *d_goal = b + 3 * n, *d_gtol = b + 5 * n;
+    i64 *d_cls = reinterpret_cast<i64 *>(b + 6 * n);
+    cudaStream_t st = sim->stream;
+    k_export_attrs<R><<<grid_for(n, 256), 256, 0, st>>>(
+        (int)n, reinterpret_cast<const R4 *>(sim->goalpref[sim->acur]),
+        reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], d_rad, d_pref, d_max,
+        d_goal, d_gtol, d_cls);
+    CKL(sim);
+    if (radii) CK(sim, cudaMemcpyAsync(radii, d_rad, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (pref) CK(sim, cudaMemcpyAsync(pref, d_pref, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (maxs) CK(sim, cudaMemcpyAsync(maxs, d_max, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (goals) CK(sim, cudaMemcpyAsync(goals, d_goal, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+    if (gtol) CK(sim, cudaMemcpyAsync(gtol, d_gtol, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (cls) CK(sim, cudaMemcpyAsync(cls, d_cls, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
+    return ORCA_OK;
+}
+
+extern "C" int orca_download(orca_sim *sim, int64_t *ids, double *positions, double *velocities,
+                             double *radii, double *pref_speeds, double *max_speeds, double *goals,
+                             double *goal_tols, int64_t *class_codes)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_download: no resident state");
+    int rc = fetch_plan(sim);
+    if (rc) return rc;
+    const int64_t n = sim->h_plan->n_owned;
+    if (n == 0) return ORCA_OK;
+    if (ids) CK(sim, cudaMemcpyAsync(ids, sim->ids[sim->acur], sizeof(i64) * n, cudaMemcpyDeviceToHost, sim->stream));
+    if (positions || velocities) {
+        rc = sim->precision == ORCA_F32 ? download_pv_impl<float>(sim, n, positions, velocities)
+                                        : download_pv_impl<double>(sim, n, positions, velocities);
+        if (rc) return rc;
+    }
+    if (radii || pref_speeds || max_speeds || goals || goal_tols || class_codes) {
+        rc = sim->precision == ORCA_F32
+                 ? download_attrs_impl<float>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes)
+                 : download_attrs_impl<double>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes);
+        if (rc) return rc;
+    }
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    return ORCA_OK;
+}
+
+extern "C" int orca_download_pv(orca_sim *sim, double *positions, double *velocities)
+{
+    return orca_download(sim, nullptr, positions, velocities, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// the step
+// ---------------------------------------------------------------------------
+
+static StepParams make_params(const orca_sim *sim)
+{
+    StepParams P;
+    const orca_params &p = sim->params;
+    P.dt = p.dt;
+    P.tau = p.tau;
+    P.nr = p.neighbor_radius;
+    P.rad2 = p.neighbor_radius * p.neighbor_radius; // engine.py:213
+    P.half_margin = 0.5 * p.avoidance_margin;       // engine.py:227
+    for (int i = 0; i < 4; ++i) P.fmat[i] = p.fmat[i];
+    P.max_n = p.max_neighbors;
+    P.stride = (int)(sim->capacity > 0 ? sim->capacity : 1);
+    P.frame = sim->frame;
+    P.max_cells = (int)std::min<int64_t>(sim->max_cells, 2 * sim->n_bound + 1024);
+    P.occ_target = 4.0;
+    const char *occ = getenv("ORCA_OCC_TARGET");
+    if (occ) {
+        const double v = atof(occ);
+        if (v > 0.0) P.occ_target = v;
+    }
+    return P;
+}
+
+// K0 + K1: bounding box, plan, histogram, scan, scatter of pv[cur]
+template <typename R> static int bin_build(orca_sim *sim, const StepParams &P)
+{
+    typedef typename Vec<R>::T4 R4;
+    typedef typename Vec<R>::T2 R2;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const R4 *pv = reinterpret_cast<const R4 *>(sim->pv[sim->cur]);
+    k_begin_bins<<<1, 1, 0, st>>>(sim->plan);
+    CK(sim, cudaMemsetAsync(sim->cell_count, 0, sizeof(int) * ((size_t)P.max_cells + 1), st));
+    const int bbox_blocks = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (n + 255) / 256));
+    k_bbox<R><<<bbox_blocks, 256, 0, st>>>(sim->plan, pv);
+    k_plan<<<1, 1, 0, st>>>(sim->plan, P);
+    k_count<R><<<grid_for(n, 256), 256, 0, st>>>(sim->plan, pv, sim->cell_of, sim->rank_of, sim->cell_count, P.nr);
+    const int scan_blocks = (P.max_cells + 1 + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count, sim->block_sums);
+    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->block_sums);
+    k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count,
+                                                       sim->block_sums, sim->cell_start);
+    k_scatter<R><<<grid_for(n, 256), 256, 0, st>>>(
+        sim->plan, P, pv, reinterpret_cast<const R4 *>(sim->goalpref[sim->acur]),
+        reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], sim->cell_of, sim->rank_of,
+        sim->cell_start, reinterpret_cast<R2 *>(sim->s_xy), reinterpret_cast<R4 *>(sim->s_pv),
+        reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell, sim->s_cls);
+    CKL(sim);
+    sim->binned_frame = sim->frame;
+    return ORCA_OK;
+}
+
+template <typename R, int MAXN> static int solve_stage(orca_sim *sim, const StepParams &P, int out_idx)
+{
+    typedef typename Vec<R>::T4 R4;
+    typedef typename Vec<R>::T2 R2;
+    typedef KCfg<R, MAXN> C;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur;
+    k_gather<R, MAXN><<<grid_for(n, 128), 128, 0, st>>>(
+        sim->plan, P, reinterpret_cast<const R2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+        sim->ids[a], sim->nb, sim->nb_cnt);
+    k_solve<R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
+                                         C::solve_bpt * C::solve_threads, st>>>(
+        sim->plan, P, reinterpret_cast<const R4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+        sim->s_cls, sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
+        reinterpret_cast<const R4 *>(sim->goalpref[a]), reinterpret_cast<R4 *>(sim->pv[out_idx]),
+        sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state));
+    const int fb_blocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, (n + C::fb_threads - 1) / C::fb_threads));
+    k_fallback<R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * C::fb_threads, st>>>(
+        sim->plan, P, reinterpret_cast<const R4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+        sim->s_cls, sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
+        reinterpret_cast<const R4 *>(sim->goalpref[a]), reinterpret_cast<R4 *>(sim->pv[out_idx]),
+        sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state));
+    CKL(sim);
+    return ORCA_OK;
+}
+
+__global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids, i64 frame_new)
+{
+    if (plan->err_pair != ORCA_NO_ERR && plan->err_frame < 0) {
+        plan->err_frame = frame_new;
+        plan->err_id_i = ids[(unsigned)(plan->err_pair >> 32)];
+        plan->err_id_j = ids[(unsigned)(plan->err_pair & 0xFFFFFFFFu)];
+    }
+}
+
+template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int dst_pv_idx)
+{
+    typedef typename Vec<R>::T4 R4;
+    typedef typename Vec<R>::T2 R2;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur, b = 1 - a;
+    k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
+                                                       sim->params.remove_arrivals);
+    const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
+    k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums);
+    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
+    k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums,
+                                                       sim->dst_idx);
+    k_compact<R><<<grid_for(n, 256), 256, 0, st>>>(
+        sim->plan, sim->keep, sim->dst_idx, reinterpret_cast<const R4 *>(sim->pv[src_idx]),
+        reinterpret_cast<R4 *>(sim->pv[dst_pv_idx]), reinterpret_cast<const R4 *>(sim->goalpref[a]),
+        reinterpret_cast<R4 *>(sim->goalpref[b]), reinterpret_cast<const R2 *>(sim->radmax[a]),
+        reinterpret_cast<R2 *>(sim->radmax[b]), sim->ids[a], sim->ids[b], sim->cls[a], sim->cls[b],
+        sim->status[a], sim->status[b], sim->failed[a], sim->failed[b]);
+    k_after_compact<<<1, 1, 0, st>>>(sim->plan, sim->dst_idx);
+    CKL(sim);
+    sim->acur = b;
+    return ORCA_OK;
+}
+
+template <typename R> static int metrics_stage(orca_sim *sim, const StepParams &P)
+{
+    typedef typename Vec<R>::T2 R2;
+    const int64_t n = sim->n_bound;
+    k_min_sep<R><<<grid_for(n, 128), 128, 0, sim->stream>>>(
+        sim->plan, P, reinterpret_cast<const R2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+        sim->ids[sim->acur], reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), 1e-6 /* engine.py:36 */);
+    CKL(sim);
+    return ORCA_OK;
+}
+
+template <typename R> static int step_impl(orca_sim *sim)
+{
+    StepParams P = make_params(sim);
+    int rc;
+    const int64_t n = sim->n_bound;
+    sim->n_pre = n;
+    k_begin_step<<<1, 1, 0, sim->stream>>>(sim->plan);
+    if (n == 0) { // engine.py:202-209
+        k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->frame + 1, sim->params.remove_arrivals);
+        CKL(sim);
+        sim->frame += 1;
+        return ORCA_OK;
+    }
+    if (sim->binned_frame != sim->frame) {
+        rc = bin_build<R>(sim, P);
+        if (rc) return rc;
+    }
+    const int out_idx = (sim->cur + 1) % 3;
+    rc = P.max_n <= 16 ? solve_stage<R, 16>(sim, P, out_idx) : solve_stage<R, 32>(sim, P, out_idx);
+    if (rc) return rc;
+    k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur], sim->frame + 1);
+    k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->frame + 1, sim->params.remove_arrivals);
+    CKL(sim);
+    sim->pre = sim->cur;
+    if (sim->params.remove_arrivals) {
+        const int dst = (sim->cur + 2) % 3;
+        rc = compact_stage<R>(sim, out_idx, dst);
+        if (rc) return rc;
+        sim->cur = dst;
+    } else {
+        sim->cur = out_idx;
+    }
+    sim->frame += 1;
+    sim->binned_frame = -1;
+    if (sim->params.compute_metrics) {
+        // engine.py:270-286: metrics of the post-step, post-removal positions. The bin
+        // build it needs is the one the next step would do anyway, so it is kept.
+        StepParams P2 = make_params(sim);
+        rc = bin_build<R>(sim, P2);
+        if (rc) return rc;
+        rc = metrics_stage<R>(sim, P2);
+        if (rc) return rc;
+    }
+    return ORCA_OK;
+}
+
+extern "C" int orca_step(orca_sim *sim)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_step: sim is NULL");
+    if (!sim->loaded) return fail(sim, ORCA_EINVAL, "orca_step: no state uploaded");
+    if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_step: orca_set_params was not called");
+    CK(sim, cudaSetDevice(sim->device));
+    return sim->precision == ORCA_F32 ? step_impl<float>(sim) : step_impl<double>(sim);
+}
+
+extern "C" int orca_run(orca_sim *sim, int64_t steps)
+{
+    for (int64_t i = 0; i < steps; ++i) {
+        int rc = orca_step(sim);
+        if (rc) return rc;
+    }
+    return ORCA_OK;
+}
+
+extern "C" int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
+                              const double *velocities, double *new_positions, double *new_velocities,
+                              int64_t *out_status)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_step_host: no resident state");
+    if (sim->params.remove_arrivals)
+        return fail(sim, ORCA_EINVAL, "orca_step_host requires remove_arrivals == 0");
+    int rc = orca_upload_pv(sim, n, frame, positions, velocities);
+    if (rc) return rc;
+    rc = orca_step(sim);
+    if (rc) return rc;
+    if (n > 0) {
+        rc = sim->precision == ORCA_F32 ? download_pv_impl<float>(sim, n, new_positions, new_velocities)
+                                        : download_pv_impl<double>(sim, n, new_positions, new_velocities);
+        if (rc) return rc;
+        if (out_status) {
+            i64 *d = reinterpret_cast<i64 *>(sim->stg + 4 * n);
+            k_export_i8<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->status[sim->acur], d);
+            CKL(sim);
+            CK(sim, cudaMemcpyAsync(out_status, d, sizeof(i64) * n, cudaMemcpyDeviceToHost, sim->stream));
+        }
+    }
+    return fetch_plan(sim);
+}
+
+// ---------------------------------------------------------------------------
+// parity taps
+// ---------------------------------------------------------------------------
+
+template <typename R>
+static int debug_impl(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_iy, int64_t *nb_rows,
+                      int64_t *nb_count, double *out_v, int64_t *status, int64_t *failed_at,
+                      double *desired_v)
+{
+    typedef typename Vec<R>::T4 R4;
+    StepParams P = make_params(sim);
+    const int max_n = std::max(P.max_n, 1);
+    const size_t need = sizeof(double) * (size_t)n * (size_t)(2 + max_n + 1 + 2 + 2 + 2 + 2);
+    if (need > sim->dbg_bytes) {
+        cudaFree(sim->dbg);
+        sim->dbg = nullptr;
+        sim->dbg_bytes = 0;
+        CK(sim, cudaMalloc(reinterpret_cast<void **>(&sim->dbg), need));
+        sim->dbg_bytes = need;
+    }
+    cudaStream_t st = sim->stream;
+    i64 *d_ix = reinterpret_cast<i64 *>(sim->dbg);
+    i64 *d_iy = d_ix + n;
+    i64 *d_rows = d_iy + n;
+    i64 *d_cnt = d_rows + (size_t)n * max_n;
+    double *d_des = reinterpret_cast<double *>(d_cnt + n);
+    double *d_pos = d_des + 2 * n;
+    double *d_vel = d_pos + 2 * n;
+    i64 *d_st = reinterpret_cast<i64 *>(d_vel + 2 * n);
+    i64 *d_fa = d_st + n;
+    k_debug_rows<R><<<grid_for(n, 256), 256, 0, st>>>(
+        (int)n, P, reinterpret_cast<const R4 *>(sim->pv[sim->pre]), sim->s_row, sim->nb, sim->nb_cnt,
+        reinterpret_cast<const R4 *>(sim->s_dm), d_ix, d_iy, d_rows, d_cnt, d_des);
+    // the un-compacted post-step buffer is pv[(pre+1)%3]
+    k_export_pv<R><<<grid_for(n, 256), 256, 0, st>>>(
+        (int)n, reinterpret_cast<const R4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel);
+    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->status[sim->acur], d_st);
+    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->failed[sim->acur], d_fa);
+    CKL(sim);
+    if (cell_ix) CK(sim, cudaMemcpyAsync(cell_ix, d_ix, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
+    if (cell_iy) CK(sim, cudaMemcpyAsync(cell_iy, d_iy, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
+    if (nb_rows && P.max_n > 0)
+        CK(sim, cudaMemcpyAsync(nb_rows, d_rows, sizeof(i64) * n * P.max_n, cudaMemcpyDeviceToHost, st));
+    if (nb_count) CK(sim, cudaMemcpyAsync(nb_count, d_cnt, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
+    if (out_v) CK(sim, cudaMemcpyAsync(out_v, d_vel, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+    if (status) CK(sim, cudaMemcpyAsync(status, d_st, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
+    if (failed_at) CK(sim, cudaMemcpyAsync(failed_at, d_fa, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
+    if (desired_v) CK(sim, cudaMemcpyAsync(desired_v, d_des, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+    CK(sim, cudaStreamSynchronize(st));
+    return ORCA_OK;
+}
+
+extern "C" int orca_debug_last_step(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_iy,
+                                    int64_t *nb_rows, int64_t *nb_count, double *out_v, int64_t *status,
+                                    int64_t *failed_at, double *desired_v)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_debug_last_step: no resident state");
+    if (sim->params.remove_arrivals || sim->params.compute_metrics)
+        return fail(sim, ORCA_EINVAL,
+                    "orca_debug_last_step needs remove_arrivals == 0 and compute_metrics == 0");
+    if (n != sim->n_pre)
+        return fail(sim, ORCA_EINVAL, "orca_debug_last_step: n = %lld, last step had %lld rows", (long long)n,
+                    (long long)sim->n_pre);
+    CK(sim, cudaSetDevice(sim->device));
+    if (n == 0) return ORCA_OK;
+    return sim->precision == ORCA_F32
+               ? debug_impl<float>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v)
+               : debug_impl<double>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
+}
+
+// ---------------------------------------------------------------------------
+// batched LP
+// ---------------------------------------------------------------------------
+
+struct orca_lp_batch {
+    int device = 0, precision = ORCA_F32;
+    int64_t n = 0, m = 0;
+    cudaStream_t stream = nullptr, own_stream = nullptr;
+    i64 *coff = nullptr;
+    void *cons = nullptr, *prob = nullptr, *proj = nullptr;
+    u64 *seeds = nullptr;
+    int *perm = nullptr;
+    double *out_v = nullptr;
+    i64 *out_status = nullptr, *out_failed = nullptr;
+};
+
+extern "C" void orca_lp_batch_destroy(orca_lp_batch *b)
+{
+    if (!b) return;
+    cudaSetDevice(b->device);
+    if (b->stream) cudaStreamSynchronize(b->stream);
+    cudaFree(b->coff);
+    cudaFree(b->cons);
+    cudaFree(b->prob);
+    cudaFree(b->proj);
+    cudaFree(b->seeds);
+    cudaFree(b->perm);
+    cudaFree(b->out_v);
+    cudaFree(b->out_status);
+    cudaFree(b->out_failed);
+    if (b->own_stream) cudaStreamDestroy(b->own_stream);
+    delete b;
+}
+
+template <typename R>
+static cudaError_t lp_pack(orca_lp_batch *b, const double *cpts, const double *cnrm, const double *tgt,
+                           const double *caps)
+{
+    typedef typename Vec<R>::T4 R4;
+    cudaError_t e;
+    double *tmp = nullptr;
+    const size_t m = (size_t)b->m, n = (size_t)b->n;
+    const size_t words = std::max<size_t>(4 * m, 3 * n);
+    if ((e = cudaMalloc(reinterpret_cast<void **>(&tmp), sizeof(double) * std::max<size_t>(words, 1))) != cudaSuccess) return e;
+    cudaStream_t st = b->stream;
+    if (m) {
+        cudaMemcpyAsync(tmp, cpts, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(tmp + 2 * m, cnrm, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, st);
+        k_lp_pack<R><<<grid_for((int64_t)m, 256), 256, 0, st>>>((i64)m, tmp, tmp + 2 * m,
+                                                               reinterpret_cast<R4 *>(b->cons));
+    }
+    cudaStreamSynchronize(st);
+    if (n) {
+        cudaMemcpyAsync(tmp, tgt, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(tmp + 2 * n, caps, sizeof(double) * n, cudaMemcpyHostToDevice, st);
+        k_lp_pack_problems<R><<<grid_for((int64_t)n, 256), 256, 0, st>>>((i64)n, tmp, tmp + 2 * n,
+                                                                        reinterpret_cast<R4 *>(b->prob));
+    }
+    e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+extern "C" int orca_lp_batch_create(orca_lp_batch **out, int device, int precision, int64_t n,
+                                    const int64_t *coff, const double *cpts, const double *cnrm,
+                                    const double *tgt, const double *caps, const uint64_t *seeds)
+{
+    if (!out) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: out is NULL");
+    *out = nullptr;
+    if (n < 0 || !coff || (n > 0 && (!tgt || !caps || !seeds)))
+        return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: bad arguments");
+    if (precision != ORCA_F32 && precision != ORCA_F64)
+        return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: unknown precision %d", precision);
+    if (coff[0] != 0) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: coff[0] must be 0");
+    for (int64_t i = 0; i < n; ++i)
+        if (coff[i + 1] < coff[i])
+            return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: coff is not non-decreasing at %lld", (long long)i);
+    const int64_t m = coff[n];
+    if (m > 0 && (!cpts || !cnrm)) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: NULL constraints");
+    int ndev = 0;
+    CK(nullptr, cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: device %d not available", device);
+    CK(nullptr, cudaSetDevice(device));
+    orca_lp_batch *b = new (std::nothrow) orca_lp_batch();
+    if (!b) return fail(nullptr, ORCA_EINVAL, "out of host memory");
+    b->device = device;
+    b->precision = precision;
+    b->n = n;
+    b->m = m;
+    const size_t rs = precision == ORCA_F32 ? sizeof(float) : sizeof(double);
+    const size_t nn = (size_t)std::max<int64_t>(n, 1), mm = (size_t)std::max<int64_t>(m, 1);
+#define CKB(call)                                                                                 \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            int rc_ = fail(nullptr, ORCA_ECUDA, "orca_lp_batch_create: %s: %s", #call, cudaGetErrorString(e_)); \
+            orca_lp_batch_destroy(b);                                                             \
+            return rc_;                                                                           \
+        }                                                                                         \
+    } while (0)
+    CKB(cudaStreamCreateWithFlags(&b->own_stream, cudaStreamNonBlocking));
+    b->stream = b->own_stream;
+    CKB(dalloc(&b->coff, nn + 1));
+    CKB(cudaMalloc(&b->cons, mm * 4 * rs));
+    CKB(cudaMalloc(&b->prob, nn * 4 * rs));
+    CKB(cudaMalloc(&b->proj, mm * 4 * rs));
+    CKB(dalloc(&b->seeds, nn));
+    CKB(dalloc(&b->perm, mm));
+    CKB(dalloc(&b->out_v, 2 * nn));
+    CKB(dalloc(&b->out_status, nn));
+    CKB(dalloc(&b->out_failed, nn));
+    CKB(cudaMemcpyAsync(b->coff, coff, sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, b->stream));
+    if (n) CKB(cudaMemcpyAsync(b->seeds, seeds, sizeof(u64) * n, cudaMemcpyHostToDevice, b->stream));
+    CKB(precision == ORCA_F32 ? lp_pack<float>(b, cpts, cnrm, tgt, caps) : lp_pack<double>(b, cpts, cnrm, tgt, caps));
+#undef CKB
+    *out = b;
+    return ORCA_OK;
+}
+
+extern "C" int orca_lp_batch_set_stream(orca_lp_batch *b, void *cuda_stream)
+{
+    if (!b) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_set_stream: NULL batch");
+    CK(nullptr, cudaSetDevice(b->device));
+    CK(nullptr, cudaStreamSynchronize(b->stream));
+    b->stream = cuda_stream ? reinterpret_cast<cudaStream_t>(cuda_stream) : b->own_stream;
+    return ORCA_OK;
+}
+
+extern "C" int orca_lp_batch_solve(orca_lp_batch *b)
+{
+    if (!b) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_solve: NULL batch");
+    CK(nullptr, cudaSetDevice(b->device));
+    if (b->n == 0) return ORCA_OK;
+    if (b->precision == ORCA_F32) {
+        k_lp_batch<float><<<grid_for(b->n, 128), 128, 0, b->stream>>>(
+            b->n, b->coff, reinterpret_cast<const float4 *>(b->cons), reinterpret_cast<const float4 *>(b->prob),
+            b->seeds, b->perm, reinterpret_cast<float4 *>(b->proj), b->out_v, b->out_status, b->out_failed);
+    } else {
+        k_lp_batch<double><<<grid_for(b->n, 128), 128, 0, b->stream>>>(
+            b->n, b->coff, reinterpret_cast<const double4 *>(b->cons), reinterpret_cast<const double4 *>(b->prob),
+            b->seeds, b->perm, reinterpret_cast<double4 *>(b->proj), b->out_v, b->out_status, b->out_failed);
+    }
+    CKL(nullptr);
+    return ORCA_OK;
+}
+
+extern "C" int orca_lp_batch_download(orca_lp_batch *b, double *out_v, int64_t *out_status, int64_t *out_failed)
+{
+    if (!b) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_download: NULL batch");
+    CK(nullptr, cudaSetDevice(b->device));
+    const size_t n = (size_t)b->n;
+    if (n) {
+        if (out_v) CK(nullptr, cudaMemcpyAsync(out_v, b->out_v, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, b->stream));
+        if (out_status) CK(nullptr, cudaMemcpyAsync(out_status, b->out_status, sizeof(i64) * n, cudaMemcpyDeviceToHost, b->stream));
+        if (out_failed) CK(nullptr, cudaMemcpyAsync(out_failed, b->out_failed, sizeof(i64) * n, cudaMemcpyDeviceToHost, b->stream));
+    }
+    CK(nullptr, cudaStreamSynchronize(b->stream));
+    return ORCA_OK;
+}
+
+extern "C" int orca_lp_solve_batch(int device, int precision, int64_t n, const int64_t *coff,
+                                   const double *cpts, const double *cnrm, const double *tgt,
+                                   const double *caps, const uint64_t *seeds, double *out_v,
+                                   int64_t *out_status, int64_t *out_failed)
+{
+    orca_lp_batch *b = nullptr;
+    int rc = orca_lp_batch_create(&b, device, precision, n, coff, cpts, cnrm, tgt, caps, seeds);
+    if (rc) return rc;
+    rc = orca_lp_batch_solve(b);
+    if (!rc) rc = orca_lp_batch_download(b, out_v, out_status, out_failed);
+    orca_lp_batch_destroy(b);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+// single-op taps
+// ---------------------------------------------------------------------------
+
+extern "C" int orca_vo_exit_batch(int device, int precision, int64_t count, const double *in7, double *out5)
+{
+    if (count < 0 || (count > 0 && (!in7 || !out5))) return fail(nullptr, ORCA_EINVAL, "orca_vo_exit_batch: bad arguments");
+    if (count == 0) return ORCA_OK;
+    CK(nullptr, cudaSetDevice(device));
+    double *d_in = nullptr, *d_out = nullptr;
+    CK(nullptr, cudaMalloc(reinterpret_cast<void **>(&d_in), sizeof(double) * 7 * count));
+    CK(nullptr, cudaMalloc(reinterpret_cast<void **>(&d_out), sizeof(double) * 5 * count));
+    CK(nullptr, cudaMemcpy(d_in, in7, sizeof(double) * 7 * count, cudaMemcpyHostToDevice));
+    if (precision == ORCA_F32) k_vo_exit_batch<float><<<grid_for(count, 128), 128>>>(count, d_in, d_out);
+    else k_vo_exit_batch<double><<<grid_for(count, 128), 128>>>(count, d_in, d_out);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out5, d_out, sizeof(double) * 5 * count, cudaMemcpyDeviceToHost);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    CK(nullptr, e);
+    return ORCA_OK;
+}
+
+extern "C" int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *perm)
+{
+    if (k < 0 || (k > 0 && !perm)) return fail(nullptr, ORCA_EINVAL, "orca_shuffle_order: bad arguments");
+    if (k == 0) return ORCA_OK;
+    CK(nullptr, cudaSetDevice(device));
+    i64 *d = nullptr;
+    CK(nullptr, cudaMalloc(reinterpret_cast<void **>(&d), sizeof(i64) * k));
+    // k <= 32 exercises the unrolled shuffle of the step kernels, larger k the batch-LP one
+    if (k <= 32) k_shuffle_tap_smem<<<1, 32>>>((int)k, seed, d);
+    else k_shuffle_tap<<<1, 1>>>((int)k, seed, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(perm, d, sizeof(i64) * k, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CK(nullptr, e);
+    return ORCA_OK;
+}
+
+extern "C" int orca_problem_seed(int device, int64_t frame, int64_t agent_id, uint64_t *seed)
+{
+    if (!seed) return fail(nullptr, ORCA_EINVAL, "orca_problem_seed: seed is NULL");
+    CK(nullptr, cudaSetDevice(device));
+    u64 *d = nullptr;
+    CK(nullptr, cudaMalloc(reinterpret_cast<void **>(&d), sizeof(u64)));
+    k_seed_tap<<<1, 1>>>(frame, agent_id, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(seed, d, sizeof(u64), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CK(nullptr, e);
+    return ORCA_OK;
+}

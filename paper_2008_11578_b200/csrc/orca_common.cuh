@@ -1,0 +1,94 @@
+// orca_common.cuh -- shared device structs, error plumbing and small utilities.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "orca_b200.h"
+#include "orca_math.cuh"
+
+namespace orca {
+
+typedef unsigned char u8;
+typedef signed char i8;
+
+// _kernels.py:426-432 / engine.py:146: |floor(pos/cell)| must stay <= 2^29 - 2
+#define ORCA_CELL_LIMIT ((double)((1LL << 29) - 2))
+
+#define ORCA_NO_ERR 0xFFFFFFFFFFFFFFFFULL
+
+// Device-resident per-step plan and counters. Written by k_plan / k_finish and
+// read by every kernel of the step, so a step needs no host round trip.
+struct GridPlan {
+    // population
+    int n;       // rows in the state arrays (owned + ghost)
+    int n_owned; // rows [0, n_owned) are solved and integrated; the rest are halo ghosts
+    // search grid (rebuilt every step from the bounding box)
+    int nx, ny, ncells, rmax;
+    double x0, y0, cell, inv_cell;
+    // bounding-box accumulators, order-preserving u64 encodings of doubles
+    u64 minx, miny, maxx, maxy;
+    // sticky errors
+    u64 err_pair;   // (row_i << 32 | row_j) of the first coincident pair in row order
+    i64 err_frame;  // frame_new of that step
+    i64 err_id_i, err_id_j;
+    int err_range;  // a position left the reference's indexable grid range
+    // per-step counters
+    int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
+    int removed;   // arrivals removed by this step
+    int n_after;   // rows after arrival removal
+    // metrics
+    u64 min_sep_enc; // order-preserving encoding of the running minimum
+    u64 collisions;
+    // frames completed
+    i64 frame;
+};
+
+struct StepParams {
+    double dt, tau, nr, rad2, half_margin;
+    double fmat[4];
+    int max_n;
+    int stride;  // leading dimension of the slot-major neighbour table
+    i64 frame;   // pre-step frame index (seed input, engine.py:233)
+    int max_cells;
+    double occ_target;
+};
+
+__host__ __device__ __forceinline__ u64 enc_double(double x)
+{
+#ifdef __CUDA_ARCH__
+    u64 b = (u64)__double_as_longlong(x);
+#else
+    u64 b;
+    memcpy(&b, &x, 8);
+#endif
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+__host__ __device__ __forceinline__ double dec_double(u64 e)
+{
+    u64 b = (e >> 63) ? (e & 0x7FFFFFFFFFFFFFFFULL) : ~e;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)b);
+#else
+    double x;
+    memcpy(&x, &b, 8);
+    return x;
+#endif
+}
+
+// vector helpers
+__device__ __forceinline__ float4 mk4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
+__device__ __forceinline__ double4 mk4(double a, double b, double c, double d) { return make_double4(a, b, c, d); }
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
+
+template <typename R> struct Fmt;
+template <> struct Fmt<float> { static constexpr bool is_f32 = true; };
+template <> struct Fmt<double> { static constexpr bool is_f32 = false; };
+
+static inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+} // namespace orca

@@ -1,0 +1,809 @@
+// orca_kernels.cuh -- the kernels of one steering step, sm_100a.
+//
+//   K0  k_bbox / k_plan      bounding box -> dense search grid for this step
+//   K1  k_count              search-cell id per agent + per-cell histogram
+//       k_scan_*             exclusive prefix scan of the histogram (CSR starts)
+//       k_scatter            counting-sort scatter into cell-sorted SoA arrays,
+//                            fused with the desired velocity (engine.py:133-139)
+//   K2  k_gather             exact top-max_n neighbours by (d2, id) within
+//                            neighbor_radius (_kernels.py:450-490), ring search
+//   K3  k_solve              ORCA half-planes (_kernels.py:525-541) + shuffled
+//                            incremental LP (_kernels.py:122-146) + integration
+//       k_fallback           least-penetration stage (_kernels.py:254-283) for the
+//                            agents k_solve queued, + integration
+//   K4  k_finish / k_compact counters, arrival removal (engine.py:251-294)
+//
+// The search grid is NOT the reference's grid (cell = neighbor_radius): it is
+// finer (about occ_target agents per cell) and searched in growing rings, which
+// is legal because the neighbour set is defined geometrically and is invariant
+// under the cell size (pkg/tests/test_grid.py:101). The reference's own cell
+// index floor(pos/neighbor_radius) is still produced bit-exactly (k_ref_cells)
+// and range-checked every step (engine.py:152-153).
+#pragma once
+
+#include "orca_common.cuh"
+
+namespace orca {
+
+// ---------------------------------------------------------------------------
+// K0: bounding box + grid plan
+// ---------------------------------------------------------------------------
+
+// per-step counters (start of every step)
+__global__ void k_begin_step(GridPlan *plan)
+{
+    plan->fq_count = 0;
+    plan->removed = 0;
+    plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
+    plan->collisions = 0;
+}
+
+// bounding-box accumulators (start of every bin build)
+__global__ void k_begin_bins(GridPlan *plan)
+{
+    plan->minx = plan->miny = 0xFFFFFFFFFFFFFFFFULL;
+    plan->maxx = plan->maxy = 0ULL;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_bbox(GridPlan *plan, const typename Vec<R>::T4 *__restrict__ pv)
+{
+    const int n = plan->n;
+    double lox = 1e300, loy = 1e300, hix = -1e300, hiy = -1e300;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const typename Vec<R>::T4 a = pv[i];
+        const double x = (double)a.x, y = (double)a.y;
+        lox = fmin(lox, x);
+        hix = fmax(hix, x);
+        loy = fmin(loy, y);
+        hiy = fmax(hiy, y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lox = fmin(lox, __shfl_xor_sync(0xFFFFFFFFu, lox, o));
+        loy = fmin(loy, __shfl_xor_sync(0xFFFFFFFFu, loy, o));
+        hix = fmax(hix, __shfl_xor_sync(0xFFFFFFFFu, hix, o));
+        hiy = fmax(hiy, __shfl_xor_sync(0xFFFFFFFFu, hiy, o));
+    }
+    if ((threadIdx.x & 31) == 0 && lox <= hix) {
+        atomicMin(&plan->minx, enc_double(lox));
+        atomicMin(&plan->miny, enc_double(loy));
+        atomicMax(&plan->maxx, enc_double(hix));
+        atomicMax(&plan->maxy, enc_double(hiy));
+    }
+}
+
+// One thread: choose the search-cell edge from the mean density, snap it so an
+// integer number of rings covers neighbor_radius, and make the dense grid fit.
+__global__ void k_plan(GridPlan *plan, StepParams P)
+{
+    const int n = plan->n;
+    double x0 = 0.0, y0 = 0.0, w = 0.0, h = 0.0;
+    if (n > 0) {
+        x0 = dec_double(plan->minx);
+        y0 = dec_double(plan->miny);
+        w = dec_double(plan->maxx) - x0;
+        h = dec_double(plan->maxy) - y0;
+    }
+    const double nr = P.nr;
+    const double area = fmax(w, 1e-3 * nr) * fmax(h, 1e-3 * nr);
+    double c = sqrt(P.occ_target * area / fmax((double)n, 1.0));
+    c = fmin(fmax(c, nr / 16.0), nr);
+    // snap: rings * c covers nr with a 1e-6 relative margin, so rmax == rings
+    const double rings = ceil(nr / c);
+    c = nr / rings * (1.0 + 1e-6);
+    while ((floor(w / c) + 1.0) * (floor(h / c) + 1.0) > (double)P.max_cells) c *= 1.25;
+    const int nx = (int)floor(w / c) + 1, ny = (int)floor(h / c) + 1;
+    plan->x0 = x0;
+    plan->y0 = y0;
+    plan->cell = c;
+    plan->inv_cell = 1.0 / c;
+    plan->nx = nx;
+    plan->ny = ny;
+    plan->ncells = nx * ny;
+    plan->rmax = (int)ceil(nr / c * (1.0 + 1e-9));
+}
+
+__device__ __forceinline__ void search_cell(const GridPlan *plan, double x, double y, int &cx, int &cy)
+{
+    // monotone in x and y; the ring-termination bound in k_gather relies on that
+    const double fx = (x - plan->x0) * plan->inv_cell;
+    const double fy = (y - plan->y0) * plan->inv_cell;
+    cx = min(max((int)floor(fx), 0), plan->nx - 1);
+    cy = min(max((int)floor(fy), 0), plan->ny - 1);
+}
+
+// ---------------------------------------------------------------------------
+// K1: count, scan, scatter
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_count(GridPlan *plan, const typename Vec<R>::T4 *__restrict__ pv, int *__restrict__ cell_of,
+        int *__restrict__ rank_of, int *__restrict__ cell_count, double nr)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= plan->n) return;
+    const typename Vec<R>::T4 a = pv[i];
+    const double x = (double)a.x, y = (double)a.y;
+    // engine.py:150-153: the reference's own bin index must stay indexable
+    const double rix = floor(__ddiv_rn(x, nr)), riy = floor(__ddiv_rn(y, nr));
+    if (!(fabs(rix) <= ORCA_CELL_LIMIT) || !(fabs(riy) <= ORCA_CELL_LIMIT)) plan->err_range = 1;
+    int cx, cy;
+    search_cell(plan, x, y, cx, cy);
+    const int c = cx * plan->ny + cy; // column-major: a column's rows are contiguous
+    cell_of[i] = c;
+    rank_of[i] = atomicAdd(&cell_count[c], 1);
+}
+
+// Exclusive scan of `in[0 .. len)` where len = *len_ptr + len_extra (device
+// value). Three phases; tiles of SCAN_TILE elements per block.
+#define SCAN_THREADS 256
+#define SCAN_ITEMS 8
+#define SCAN_TILE (SCAN_THREADS * SCAN_ITEMS)
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *smem_warp, int &block_total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) smem_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < (SCAN_THREADS / 32) ? smem_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, w, o);
+            if (lane >= o) w += t;
+        }
+        smem_warp[32 + lane] = w; // inclusive over warps
+    }
+    __syncthreads();
+    const int warp_off = wid == 0 ? 0 : smem_warp[32 + wid - 1];
+    block_total = smem_warp[32 + SCAN_THREADS / 32 - 1];
+    __syncthreads();
+    return warp_off + inc - v;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_reduce(const int *__restrict__ len_ptr, int len_extra, const int *__restrict__ in,
+              int *__restrict__ block_sums)
+{
+    const int len = *len_ptr + len_extra;
+    const int base = blockIdx.x * SCAN_TILE;
+    if (base >= len) return;
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        const int i = base + k * SCAN_THREADS + threadIdx.x;
+        if (i < len) s += in[i];
+    }
+    __shared__ int sm[64];
+    int total;
+    block_exclusive_scan(s, sm, total);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_top(const int *__restrict__ len_ptr, int len_extra, int *__restrict__ block_sums)
+{
+    const int len = *len_ptr + len_extra;
+    const int nb = (len + SCAN_TILE - 1) / SCAN_TILE;
+    __shared__ int sm[64];
+    int carry = 0;
+    for (int base = 0; base < nb; base += SCAN_THREADS) {
+        const int i = base + threadIdx.x;
+        const int v = i < nb ? block_sums[i] : 0;
+        int total;
+        const int ex = block_exclusive_scan(v, sm, total);
+        if (i < nb) block_sums[i] = carry + ex;
+        carry += total;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_apply(const int *__restrict__ len_ptr, int len_extra, const int *__restrict__ in,
+             const int *__restrict__ block_sums, int *__restrict__ out)
+{
+    const int len = *len_ptr + len_extra;
+    const int base = blockIdx.x * SCAN_TILE;
+    if (base >= len) return;
+    // thread t owns SCAN_ITEMS consecutive elements
+    const int first = base + threadIdx.x * SCAN_ITEMS;
+    int v[SCAN_ITEMS];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        v[k] = (first + k) < len ? in[first + k] : 0;
+        s += v[k];
+    }
+    __shared__ int sm[64];
+    int total;
+    int run = block_sums[blockIdx.x] + block_exclusive_scan(s, sm, total);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+        if ((first + k) < len) out[first + k] = run;
+        run += v[k];
+    }
+}
+
+// Scatter into cell-sorted order. Writes, per sorted slot s:
+//   s_xy  (x, y)                         candidate stream of the neighbour search
+//   s_pv  (x, y, vx, vy)                 pre-step snapshot
+//   s_dm  (des_vx, des_vy, max_speed, avoid_radius)
+//   s_row storage row, s_cell search cell, s_cls class code
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_scatter(const GridPlan *__restrict__ plan, StepParams P,
+          const typename Vec<R>::T4 *__restrict__ pv, const typename Vec<R>::T4 *__restrict__ goalpref,
+          const typename Vec<R>::T2 *__restrict__ radmax, const u8 *__restrict__ cls,
+          const int *__restrict__ cell_of, const int *__restrict__ rank_of,
+          const int *__restrict__ cell_start, typename Vec<R>::T2 *__restrict__ s_xy,
+          typename Vec<R>::T4 *__restrict__ s_pv, typename Vec<R>::T4 *__restrict__ s_dm,
+          int *__restrict__ s_row, int *__restrict__ s_cell, u8 *__restrict__ s_cls)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= plan->n) return;
+    const int c = cell_of[i];
+    const int s = cell_start[c] + rank_of[i];
+    const typename Vec<R>::T4 a = pv[i];
+    const typename Vec<R>::T4 g = goalpref[i]; // gx, gy, pref_speed, goal_tol
+    const typename Vec<R>::T2 rm = radmax[i];  // radius, max_speed
+    // engine.py:133-139
+    const R dx = g.x - a.x, dy = g.y - a.y;
+    const R dist = sqrt_rn<R>(dx * dx + dy * dy);
+    R speed = div_rn<R>(dist, (R)P.dt);
+    if (g.z < speed) speed = g.z;
+    const R scale = dist > R(0) ? div_rn<R>(speed, dist) : R(0);
+    // engine.py:227
+    const R avoid = Fmt<R>::is_f32 ? (R)((double)rm.x + P.half_margin) : (R)(rm.x + (R)P.half_margin);
+    s_xy[s] = mk2(a.x, a.y);
+    s_pv[s] = a;
+    s_dm[s] = mk4(dx * scale, dy * scale, rm.y, avoid);
+    s_row[s] = i;
+    s_cell[s] = c;
+    s_cls[s] = cls[i];
+}
+
+// ---------------------------------------------------------------------------
+// K2: neighbour gather
+// ---------------------------------------------------------------------------
+
+// One thread per agent (cell-sorted order, so a warp shares its candidate
+// stream). The kept list lives in registers, ascending by (d2, id); slots
+// [0, MAXN-max_n) hold -1 sentinels so the admission threshold is always the
+// last register. Keys are FP64 d2 = dx*dx + dy*dy evaluated exactly like
+// _kernels.py:467-469 (no FMA), so the list is bit-identical to the reference's
+// for float32-representable positions; the FP32 build pre-filters with an FP32
+// distance against a slightly inflated threshold before touching FP64.
+template <typename R, int MAXN>
+__global__ void __launch_bounds__(128)
+k_gather(const GridPlan *__restrict__ plan, StepParams P,
+         const typename Vec<R>::T2 *__restrict__ s_xy, const int *__restrict__ cell_start,
+         const int *__restrict__ s_cell, const int *__restrict__ s_row,
+         const i64 *__restrict__ ids, int *__restrict__ nb, u8 *__restrict__ nb_cnt)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= plan->n) return;
+    const int row = s_row[s];
+    if (row >= plan->n_owned || P.max_n == 0) {
+        nb_cnt[s] = 0;
+        return;
+    }
+    const int nx = plan->nx, ny = plan->ny, rmax = plan->rmax;
+    const double cell = plan->cell;
+    const double rad2 = P.rad2;
+    const int max_n = P.max_n;
+    const int off = MAXN - max_n;
+
+    const typename Vec<R>::T2 me = s_xy[s];
+    const double mx = (double)me.x, my = (double)me.y;
+    const int c0 = s_cell[s];
+    const int cx = c0 / ny, cy = c0 - cx * ny;
+
+    double key[MAXN];
+    int idx[MAXN];
+#pragma unroll
+    for (int t = 0; t < MAXN; ++t) {
+        key[t] = t < off ? -1.0 : __longlong_as_double(0x7FF0000000000000LL);
+        idx[t] = -1;
+    }
+    int cnt = 0;
+    float thr_f = __double2float_ru(rad2 * (1.0 + 1e-6));
+
+    auto id_of = [&](int sidx) -> i64 { return ids[s_row[sidx]]; };
+
+    auto scan_range = [&](int a, int b) {
+        for (int s2 = a; s2 < b; ++s2) {
+            const typename Vec<R>::T2 q = s_xy[s2];
+            if (Fmt<R>::is_f32) {
+                const float dxf = (float)q.x - (float)me.x, dyf = (float)q.y - (float)me.y;
+                if (dxf * dxf + dyf * dyf > thr_f) continue;
+            }
+            const double dx = (double)q.x - mx, dy = (double)q.y - my;
+            const double d2 = dx * dx + dy * dy;
+            if (s2 == s || d2 > rad2) continue;
+            // admission against the current last entry, _kernels.py:473-476
+            const double last = key[MAXN - 1];
+            if (d2 > last) continue;
+            i64 my_id = 0;
+            bool have_id = false;
+            if (d2 == last) {
+                my_id = id_of(s2);
+                have_id = true;
+                if (my_id >= id_of(idx[MAXN - 1])) continue;
+            }
+            bool c_next = true;
+#pragma unroll
+            for (int p = MAXN - 1; p >= 1; --p) {
+                bool cp = d2 < key[p - 1];
+                if (d2 == key[p - 1]) {
+                    if (!have_id) {
+                        my_id = id_of(s2);
+                        have_id = true;
+                    }
+                    cp = my_id < id_of(idx[p - 1]);
+                }
+                if (cp) {
+                    key[p] = key[p - 1];
+                    idx[p] = idx[p - 1];
+                } else if (c_next) {
+                    key[p] = d2;
+                    idx[p] = s2;
+                }
+                c_next = cp;
+            }
+            if (c_next) {
+                key[0] = d2;
+                idx[0] = s2;
+            }
+            cnt = min(cnt + 1, max_n);
+            if (Fmt<R>::is_f32) thr_f = __double2float_ru(fmin(key[MAXN - 1], rad2) * (1.0 + 1e-6));
+        }
+    };
+
+    int r_done = -1;
+    int r_next = min(1, rmax);
+    while (true) {
+        const int gx_lo = max(cx - r_next, 0), gx_hi = min(cx + r_next, nx - 1);
+        const int y_lo = max(cy - r_next, 0), y_hi = min(cy + r_next, ny - 1);
+        for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+            const int *cs = cell_start + gx * ny;
+            if (abs(gx - cx) > r_done) {
+                scan_range(cs[y_lo], cs[y_hi + 1]);
+            } else {
+                const int b_hi = cy - r_done - 1;
+                if (b_hi >= y_lo) scan_range(cs[y_lo], cs[b_hi + 1]);
+                const int t_lo = cy + r_done + 1;
+                if (t_lo <= y_hi) scan_range(cs[t_lo], cs[y_hi + 1]);
+            }
+        }
+        r_done = r_next;
+        if (r_done >= rmax) break;
+        if (cnt == max_n) {
+            // Every unscanned agent is farther than r_done*cell (1e-9 margin for the
+            // rounding of the cell index); stop once the kept list is closer than that.
+            const double d_last = key[MAXN - 1];
+            const double reach = (double)r_done * cell;
+            if (d_last < reach * reach * (1.0 - 1e-9)) break;
+            const int need = (int)(sqrt(d_last) / cell * (1.0 + 1e-9)) + 1;
+            r_next = min(rmax, max(r_done + 1, need));
+        } else {
+            r_next = min(rmax, r_done + 1);
+        }
+    }
+
+    nb_cnt[s] = (u8)cnt;
+#pragma unroll
+    for (int t = 0; t < MAXN; ++t) {
+        const int slot = t - off;
+        if (slot >= 0 && slot < cnt) nb[(size_t)slot * P.stride + s] = idx[t];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: constraints + LP
+// ---------------------------------------------------------------------------
+
+template <typename R> struct SmemCons {
+    typename Vec<R>::T4 *base; // already offset by the thread index
+    int stride;
+    __device__ __forceinline__ void get(int pos, R &px, R &py, R &nx, R &ny) const
+    {
+        const typename Vec<R>::T4 c = base[pos * stride];
+        px = c.x;
+        py = c.y;
+        nx = c.z;
+        ny = c.w;
+    }
+    __device__ __forceinline__ void set(int pos, R px, R py, R nx, R ny)
+    {
+        base[pos * stride] = mk4(px, py, nx, ny);
+    }
+};
+
+// identity-order view: original constraint t sits at shuffled position inv[t]
+template <typename R> struct SmemConsIdent {
+    const typename Vec<R>::T4 *base;
+    const u8 *inv;
+    int stride;
+    __device__ __forceinline__ void get(int t, R &px, R &py, R &nx, R &ny) const
+    {
+        const typename Vec<R>::T4 c = base[(int)inv[t * stride] * stride];
+        px = c.x;
+        py = c.y;
+        nx = c.z;
+        ny = c.w;
+    }
+};
+
+// Fisher-Yates order of _kernels.py:43-54 into perm[pos*stride]; MAXN <= 32.
+template <int MAXN>
+__device__ __forceinline__ void shuffle_smem(u8 *perm, int stride, int k, u64 seed)
+{
+    for (int t = 0; t < k; ++t) perm[t * stride] = (u8)t;
+    u64 state = seed;
+#pragma unroll
+    for (int i = MAXN - 1; i > 0; --i) {
+        if (i < k) {
+            state += ORCA_GOLDEN;
+            const int j = (int)(mix64(state) % (u64)(i + 1)); // constant divisor after unrolling
+            const u8 tmp = perm[i * stride];
+            perm[i * stride] = perm[j * stride];
+            perm[j * stride] = tmp;
+        }
+    }
+}
+
+// Build the ORCA half-planes of agent s into `cons` in SHUFFLED order
+// (_kernels.py:525-541). Returns false on exactly coincident centres.
+template <typename R>
+__device__ __forceinline__ bool build_constraints(
+    int s, int cnt, const StepParams &P, const typename Vec<R>::T4 *__restrict__ s_pv,
+    const typename Vec<R>::T4 *__restrict__ s_dm, const u8 *__restrict__ s_cls,
+    const int *__restrict__ nb, const u8 *perm, int stride, SmemCons<R> &cons, int &bad_j)
+{
+    const typename Vec<R>::T4 me = s_pv[s];
+    const R ri = s_dm[s].w;
+    const int ci = s_cls[s];
+    const R tau = (R)P.tau, dt = (R)P.dt;
+    for (int pos = 0; pos < cnt; ++pos) {
+        const int t = perm[pos * stride];
+        const int j = nb[(size_t)t * P.stride + s];
+        const typename Vec<R>::T4 q = s_pv[j];
+        const R rj = s_dm[j].w;
+        const int cj = s_cls[j];
+        R ux, uy, nx, ny;
+        if (!vo_exit<R>(q.x - me.x, q.y - me.y, me.z - q.z, me.w - q.w, ri + rj, tau, dt, ux, uy,
+                        nx, ny)) {
+            // coincident neighbours have d2 == 0 and therefore lead the list; the
+            // reference reports the first one in rank order (_kernels.py:533-536)
+            bad_j = nb[s];
+            return false;
+        }
+        const R f = (R)P.fmat[ci * 2 + cj];
+        cons.set(pos, me.z + f * ux, me.w + f * uy, nx, ny);
+    }
+    return true;
+}
+
+// Integration + arrival test (engine.py:249-253) for storage row `row`.
+template <typename R>
+__device__ __forceinline__ void integrate_row(int row, const typename Vec<R>::T4 &me, R vx, R vy,
+                                              const StepParams &P,
+                                              const typename Vec<R>::T4 *__restrict__ goalpref,
+                                              typename Vec<R>::T4 *__restrict__ pv_out,
+                                              u8 *__restrict__ arrived)
+{
+    const R dt = (R)P.dt;
+    const R nxp = me.x + vx * dt, nyp = me.y + vy * dt;
+    pv_out[row] = mk4(nxp, nyp, vx, vy);
+    const typename Vec<R>::T4 g = goalpref[row];
+    const R gx = g.x - nxp, gy = g.y - nyp;
+    arrived[row] = sqrt_rn<R>(gx * gx + gy * gy) <= g.w ? 1 : 0;
+}
+
+template <typename R, int MAXN, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T4 *__restrict__ s_pv,
+        const typename Vec<R>::T4 *__restrict__ s_dm, const u8 *__restrict__ s_cls,
+        const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
+        const u8 *__restrict__ nb_cnt, const typename Vec<R>::T4 *__restrict__ goalpref,
+        typename Vec<R>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
+        i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
+        typename Vec<R>::T4 *__restrict__ fq_state)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typename Vec<R>::T4 *sm_cons = reinterpret_cast<typename Vec<R>::T4 *>(smem_raw);
+    u8 *sm_perm = smem_raw + sizeof(typename Vec<R>::T4) * MAXN * THREADS;
+
+    const int s = blockIdx.x * THREADS + threadIdx.x;
+    if (s >= plan->n) return;
+    const int row = s_row[s];
+    if (row >= plan->n_owned) return; // halo ghost: searched, never solved
+
+    const int cnt = nb_cnt[s];
+    const typename Vec<R>::T4 me = s_pv[s];
+    const typename Vec<R>::T4 dm = s_dm[s];
+    u8 *perm = sm_perm + threadIdx.x;
+    SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
+
+    shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
+
+    int bad_j = -1;
+    if (!build_constraints<R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j)) {
+        // _kernels.py:542-547 + engine.py:239-245
+        if (plan->err_frame < 0) // sticky: only the first failing frame is reported
+            atomicMin(&plan->err_pair, ((u64)(unsigned)row << 32) | (u64)(unsigned)s_row[bad_j]);
+        status[row] = 0;
+        failed_at[row] = -1;
+        integrate_row<R>(row, me, me.z, me.w, P, goalpref, pv_out, arrived);
+        return;
+    }
+
+    int fail_pos;
+    R vx, vy;
+    if (lp2_target<R, false, SmemCons<R>>(cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy)) {
+        status[row] = 0;
+        failed_at[row] = -1;
+        integrate_row<R>(row, me, vx, vy, P, goalpref, pv_out, arrived);
+        return;
+    }
+    // queue for the least-penetration stage (warp-aggregated by the compiler)
+    status[row] = 1;
+    failed_at[row] = (i8)perm[fail_pos * THREADS];
+    const int q = atomicAdd(&plan->fq_count, 1);
+    fq[q] = s;
+    fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
+}
+
+template <typename R, int MAXN, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+k_fallback(const GridPlan *__restrict__ plan, StepParams P,
+           const typename Vec<R>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
+           const u8 *__restrict__ s_cls, const int *__restrict__ s_row,
+           const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
+           const typename Vec<R>::T4 *__restrict__ goalpref, typename Vec<R>::T4 *__restrict__ pv_out,
+           u8 *__restrict__ arrived, const int *__restrict__ fq,
+           const typename Vec<R>::T4 *__restrict__ fq_state)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typedef typename Vec<R>::T4 R4;
+    R4 *sm_cons = reinterpret_cast<R4 *>(smem_raw);
+    R4 *sm_proj = sm_cons + MAXN * THREADS;
+    u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * THREADS);
+    u8 *sm_inv = sm_perm + MAXN * THREADS;
+
+    const int nq = plan->fq_count;
+    for (int q = blockIdx.x * THREADS + threadIdx.x; q < nq; q += gridDim.x * THREADS) {
+        const int s = fq[q];
+        const R4 st = fq_state[q];
+        const int row = s_row[s];
+        const int cnt = nb_cnt[s];
+        const R4 me = s_pv[s];
+        const R4 dm = s_dm[s];
+        u8 *perm = sm_perm + threadIdx.x;
+        u8 *inv = sm_inv + threadIdx.x;
+        SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
+        SmemCons<R> proj{sm_proj + threadIdx.x, THREADS};
+
+        shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
+        for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * THREADS] * THREADS] = (u8)pos;
+        int bad_j;
+        build_constraints<R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j);
+
+        SmemConsIdent<R> ident{sm_cons + threadIdx.x, inv, THREADS};
+        R rx, ry;
+        least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+            cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry);
+        integrate_row<R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: finish, arrival removal
+// ---------------------------------------------------------------------------
+
+__global__ void k_finish(GridPlan *plan, i64 frame_new, int remove_arrivals)
+{
+    plan->frame = frame_new;
+    if (!remove_arrivals) {
+        plan->removed = 0;
+        plan->n_after = plan->n_owned;
+    }
+}
+
+// keep[i] = 1 for owned rows that have not arrived; ghosts are always dropped.
+__global__ void __launch_bounds__(256)
+k_keep_flags(const GridPlan *__restrict__ plan, const u8 *__restrict__ arrived,
+             int *__restrict__ keep, int remove_arrivals)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = plan->n;
+    if (i > n) return;
+    keep[i] = (i < plan->n_owned && !(remove_arrivals && arrived[i])) ? 1 : 0;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_compact(GridPlan *__restrict__ plan, const int *__restrict__ keep, const int *__restrict__ dst_idx,
+          const typename Vec<R>::T4 *__restrict__ pv, typename Vec<R>::T4 *__restrict__ pv2,
+          const typename Vec<R>::T4 *__restrict__ gp, typename Vec<R>::T4 *__restrict__ gp2,
+          const typename Vec<R>::T2 *__restrict__ rm, typename Vec<R>::T2 *__restrict__ rm2,
+          const i64 *__restrict__ ids, i64 *__restrict__ ids2, const u8 *__restrict__ cls,
+          u8 *__restrict__ cls2, const i8 *__restrict__ st, i8 *__restrict__ st2,
+          const i8 *__restrict__ fa, i8 *__restrict__ fa2)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = plan->n;
+    if (i >= n) return;
+    if (keep[i]) {
+        const int d = dst_idx[i];
+        pv2[d] = pv[i];
+        gp2[d] = gp[i];
+        rm2[d] = rm[i];
+        ids2[d] = ids[i];
+        cls2[d] = cls[i];
+        st2[d] = st[i];
+        fa2[d] = fa[i];
+    }
+}
+
+__global__ void k_after_compact(GridPlan *plan, const int *__restrict__ dst_idx)
+{
+    const int kept = dst_idx[plan->n]; // exclusive scan evaluated one past the end
+    plan->removed = plan->n_owned - kept;
+    plan->n_after = kept;
+    plan->n = kept;
+    plan->n_owned = kept;
+}
+
+// ---------------------------------------------------------------------------
+// metrics: min separation / collision count (_kernels.py:559-589) on the
+// post-step positions, using the grid of the NEXT bin build (same positions).
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void __launch_bounds__(128)
+k_min_sep(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *__restrict__ s_xy,
+          const int *__restrict__ cell_start, const int *__restrict__ s_cell,
+          const int *__restrict__ s_row, const i64 *__restrict__ ids,
+          const typename Vec<R>::T2 *__restrict__ radmax, double coll_tol)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    double best = __longlong_as_double(0x7FF0000000000000LL);
+    unsigned cnt = 0;
+    if (s < plan->n) {
+        const int nx = plan->nx, ny = plan->ny, r = plan->rmax;
+        const typename Vec<R>::T2 me = s_xy[s];
+        const int row = s_row[s];
+        const i64 my_id = ids[row];
+        const double my_r = (double)radmax[row].x;
+        const int c0 = s_cell[s];
+        const int cx = c0 / ny, cy = c0 - cx * ny;
+        const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
+        for (int gx = max(cx - r, 0); gx <= min(cx + r, nx - 1); ++gx) {
+            const int *cs = cell_start + gx * ny;
+            for (int s2 = cs[y_lo]; s2 < cs[y_hi + 1]; ++s2) {
+                const typename Vec<R>::T2 q = s_xy[s2];
+                const double dx = (double)q.x - (double)me.x, dy = (double)q.y - (double)me.y;
+                const double d2 = dx * dx + dy * dy;
+                if (d2 > P.rad2) continue;
+                const int row2 = s_row[s2];
+                if (ids[row2] <= my_id) continue;
+                const double sep = __dsqrt_rn(d2) - (my_r + (double)radmax[row2].x);
+                if (sep < best) best = sep;
+                if (sep < -coll_tol) ++cnt;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        best = fmin(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+        cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&plan->min_sep_enc, enc_double(best));
+        if (cnt) atomicAdd(&plan->collisions, (u64)cnt);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// conversions between the reference's float64 / int64 host layout and the
+// device state
+// ---------------------------------------------------------------------------
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_import_pv(int n, const double *__restrict__ pos, const double *__restrict__ vel,
+            typename Vec<R>::T4 *__restrict__ pv)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    pv[i] = mk4((R)pos[2 * i], (R)pos[2 * i + 1], (R)vel[2 * i], (R)vel[2 * i + 1]);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_import_attrs(int n, const double *__restrict__ radii, const double *__restrict__ pref,
+               const double *__restrict__ maxs, const double *__restrict__ goals,
+               const double *__restrict__ gtol, const i64 *__restrict__ cls_in,
+               typename Vec<R>::T4 *__restrict__ goalpref, typename Vec<R>::T2 *__restrict__ radmax,
+               u8 *__restrict__ cls)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    goalpref[i] = mk4((R)goals[2 * i], (R)goals[2 * i + 1], (R)pref[i], (R)gtol[i]);
+    radmax[i] = mk2((R)radii[i], (R)maxs[i]);
+    cls[i] = (u8)cls_in[i];
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_export_pv(int n, const typename Vec<R>::T4 *__restrict__ pv, double *__restrict__ pos,
+            double *__restrict__ vel)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const typename Vec<R>::T4 a = pv[i];
+    pos[2 * i] = (double)a.x;
+    pos[2 * i + 1] = (double)a.y;
+    vel[2 * i] = (double)a.z;
+    vel[2 * i + 1] = (double)a.w;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_export_attrs(int n, const typename Vec<R>::T4 *__restrict__ goalpref,
+               const typename Vec<R>::T2 *__restrict__ radmax, const u8 *__restrict__ cls,
+               double *__restrict__ radii, double *__restrict__ pref, double *__restrict__ maxs,
+               double *__restrict__ goals, double *__restrict__ gtol, i64 *__restrict__ cls_out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const typename Vec<R>::T4 g = goalpref[i];
+    const typename Vec<R>::T2 rm = radmax[i];
+    goals[2 * i] = (double)g.x;
+    goals[2 * i + 1] = (double)g.y;
+    pref[i] = (double)g.z;
+    gtol[i] = (double)g.w;
+    radii[i] = (double)rm.x;
+    maxs[i] = (double)rm.y;
+    cls_out[i] = (i64)cls[i];
+}
+
+__global__ void __launch_bounds__(256)
+k_export_i8(int n, const i8 *__restrict__ in, i64 *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (i64)in[i];
+}
+
+// parity taps, storage-row order (see orca_debug_last_step)
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_debug_rows(int n, StepParams P, const typename Vec<R>::T4 *__restrict__ pv_pre,
+             const int *__restrict__ s_row, const int *__restrict__ nb,
+             const u8 *__restrict__ nb_cnt, const typename Vec<R>::T4 *__restrict__ s_dm,
+             i64 *__restrict__ cell_ix, i64 *__restrict__ cell_iy, i64 *__restrict__ nb_rows,
+             i64 *__restrict__ nb_count, double *__restrict__ des)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int row = s_row[s];
+    const typename Vec<R>::T4 a = pv_pre[row];
+    cell_ix[row] = (i64)floor(__ddiv_rn((double)a.x, P.nr));
+    cell_iy[row] = (i64)floor(__ddiv_rn((double)a.y, P.nr));
+    const int cnt = nb_cnt[s];
+    nb_count[row] = cnt;
+    for (int t = 0; t < P.max_n; ++t)
+        nb_rows[(size_t)row * P.max_n + t] = t < cnt ? (i64)s_row[nb[(size_t)t * P.stride + s]] : -1;
+    des[2 * row] = (double)s_dm[s].x;
+    des[2 * row + 1] = (double)s_dm[s].y;
+}
+
+} // namespace orca

@@ -1,0 +1,163 @@
+// orca_lp_batch.cuh -- standalone batched LP over CSR-packed problems, the device
+// twin of _kernels.solve_range (pkg/src/orcasim/_kernels.py:306-336), plus the
+// single-op taps used by the known-answer tests.
+#pragma once
+
+#include "orca_common.cuh"
+#include "orca_kernels.cuh"
+
+namespace orca {
+
+template <typename R> struct GlobalShuf {
+    const typename Vec<R>::T4 *cons; // this problem's rows
+    const int *perm;
+    __device__ __forceinline__ void get(int pos, R &px, R &py, R &nx, R &ny) const
+    {
+        const typename Vec<R>::T4 c = cons[perm[pos]];
+        px = c.x;
+        py = c.y;
+        nx = c.z;
+        ny = c.w;
+    }
+};
+
+template <typename R> struct GlobalIdent {
+    const typename Vec<R>::T4 *cons;
+    __device__ __forceinline__ void get(int t, R &px, R &py, R &nx, R &ny) const
+    {
+        const typename Vec<R>::T4 c = cons[t];
+        px = c.x;
+        py = c.y;
+        nx = c.z;
+        ny = c.w;
+    }
+};
+
+template <typename R> struct GlobalProj {
+    typename Vec<R>::T4 *p;
+    __device__ __forceinline__ void get(int m, R &px, R &py, R &nx, R &ny) const
+    {
+        const typename Vec<R>::T4 c = p[m];
+        px = c.x;
+        py = c.y;
+        nx = c.z;
+        ny = c.w;
+    }
+    __device__ __forceinline__ void set(int m, R px, R py, R nx, R ny) { p[m] = mk4(px, py, nx, ny); }
+};
+
+// (point, normal) float64 rows -> packed (px, py, nx, ny) in R
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_lp_pack(i64 m, const double *__restrict__ cpts, const double *__restrict__ cnrm,
+          typename Vec<R>::T4 *__restrict__ cons)
+{
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    cons[i] = mk4((R)cpts[2 * i], (R)cpts[2 * i + 1], (R)cnrm[2 * i], (R)cnrm[2 * i + 1]);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_lp_pack_problems(i64 n, const double *__restrict__ tgt, const double *__restrict__ caps,
+                   typename Vec<R>::T4 *__restrict__ prob)
+{
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    prob[i] = mk4((R)tgt[2 * i], (R)tgt[2 * i + 1], (R)caps[i], R(0));
+}
+
+// One thread per problem; per-problem scratch (order, projected constraints)
+// lives in global memory at the problem's own CSR offsets, so any k works.
+template <typename R>
+__global__ void __launch_bounds__(128)
+k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__restrict__ cons,
+           const typename Vec<R>::T4 *__restrict__ prob, const u64 *__restrict__ seeds,
+           int *__restrict__ perm_scratch, typename Vec<R>::T4 *__restrict__ proj_scratch,
+           double *__restrict__ out_v, i64 *__restrict__ out_status, i64 *__restrict__ out_failed)
+{
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const i64 lo = coff[i];
+    const int k = (int)(coff[i + 1] - lo);
+    const typename Vec<R>::T4 pr = prob[i];
+    int *perm = perm_scratch + lo;
+
+    // _kernels.py:43-54
+    for (int t = 0; t < k; ++t) perm[t] = t;
+    u64 state = seeds[i];
+    for (int t = k - 1; t > 0; --t) {
+        state += ORCA_GOLDEN;
+        const u64 r = mix64(state);
+        const int j = (t + 1) <= 0xFFFF ? (int)mod_small(r, (uint32_t)(t + 1)) : (int)(r % (u64)(t + 1));
+        const int tmp = perm[t];
+        perm[t] = perm[j];
+        perm[j] = tmp;
+    }
+
+    GlobalShuf<R> shuf{cons + lo, perm};
+    int fail_pos;
+    R vx, vy;
+    if (lp2_target<R, false, GlobalShuf<R>>(shuf, k, R(0), pr.z, pr.x, pr.y, fail_pos, vx, vy)) {
+        out_v[2 * i] = (double)vx;
+        out_v[2 * i + 1] = (double)vy;
+        out_status[i] = 0;
+        out_failed[i] = -1;
+        return;
+    }
+    GlobalIdent<R> ident{cons + lo};
+    GlobalProj<R> proj{proj_scratch + lo};
+    R rx, ry;
+    least_penetration<R, GlobalShuf<R>, GlobalIdent<R>, GlobalProj<R>>(shuf, ident, proj, k, fail_pos,
+                                                                     pr.z, vx, vy, rx, ry);
+    out_v[2 * i] = (double)rx;
+    out_v[2 * i + 1] = (double)ry;
+    out_status[i] = 1;
+    out_failed[i] = perm[fail_pos];
+}
+
+// ---- taps -------------------------------------------------------------------
+
+template <typename R>
+__global__ void k_vo_exit_batch(i64 count, const double *__restrict__ in7, double *__restrict__ out5)
+{
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const double *c = in7 + 7 * i;
+    R ux, uy, nx, ny;
+    const bool ok = vo_exit<R>((R)c[0], (R)c[1], (R)c[2], (R)c[3], (R)c[4], (R)c[5], (R)c[6], ux, uy,
+                               nx, ny);
+    out5[5 * i + 0] = (double)ux;
+    out5[5 * i + 1] = (double)uy;
+    out5[5 * i + 2] = (double)nx;
+    out5[5 * i + 3] = (double)ny;
+    out5[5 * i + 4] = ok ? 1.0 : 0.0;
+}
+
+__global__ void k_shuffle_tap(int k, u64 seed, i64 *perm)
+{
+    for (int t = 0; t < k; ++t) perm[t] = t;
+    u64 state = seed;
+    for (int t = k - 1; t > 0; --t) {
+        state += ORCA_GOLDEN;
+        const u64 r = mix64(state);
+        const int j = (t + 1) <= 0xFFFF ? (int)mod_small(r, (uint32_t)(t + 1)) : (int)(r % (u64)(t + 1));
+        const i64 tmp = perm[t];
+        perm[t] = perm[j];
+        perm[j] = tmp;
+    }
+}
+
+// the unrolled constant-divisor shuffle used inside k_solve / k_fallback, k <= 32
+__global__ void k_shuffle_tap_smem(int k, u64 seed, i64 *perm_out)
+{
+    __shared__ u8 perm[32];
+    if (threadIdx.x == 0) {
+        shuffle_smem<32>(perm, 1, k, seed);
+        for (int t = 0; t < k; ++t) perm_out[t] = perm[t];
+    }
+}
+
+__global__ void k_seed_tap(i64 frame, i64 agent_id, u64 *out) { *out = problem_seed(frame, agent_id); }
+
+} // namespace orca

@@ -1,0 +1,385 @@
+// orca_math.cuh -- scalar building blocks of the steering step, templated on the
+// arithmetic type R (float: the FP32 product path; double: bit-exact twin of the
+// float64 reference). Device-only, header-only.
+//
+// Reference behaviour restated here ("K" = pkg/src/orcasim/_kernels.py):
+//   mix64 / problem_seed / Fisher-Yates   K:36-61
+//   vo_exit                                K:343-419
+//   closest-point LP                       K:74-146
+//   direction LP + least penetration       K:153-283
+//
+// The translation unit is compiled with -fmad=false: the reference never fuses a
+// multiply-add (numba/LLVM without fastmath), and the FP64 instantiation relies
+// on that to be bit-identical. Expression trees follow the reference's
+// evaluation order (Python binary operators associate left to right).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace orca {
+
+typedef unsigned long long u64;
+typedef long long i64;
+
+template <typename R> struct Vec;
+template <> struct Vec<float> { typedef float2 T2; typedef float4 T4; };
+template <> struct Vec<double> { typedef double2 T2; typedef double4 T4; };
+
+template <typename R> __device__ __forceinline__ R rsqrt_exact(R x);
+template <> __device__ __forceinline__ float rsqrt_exact<float>(float x) { return __fsqrt_rn(x); }
+template <> __device__ __forceinline__ double rsqrt_exact<double>(double x) { return __dsqrt_rn(x); }
+// correctly rounded square root (np.sqrt)
+template <typename R> __device__ __forceinline__ R sqrt_rn(R x) { return rsqrt_exact<R>(x); }
+
+template <typename R> __device__ __forceinline__ R div_rn(R a, R b);
+template <> __device__ __forceinline__ float div_rn<float>(float a, float b) { return __fdiv_rn(a, b); }
+template <> __device__ __forceinline__ double div_rn<double>(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---------------------------------------------------------------------------
+// splitmix64, per-problem seed, shuffle                                K:36-61
+// ---------------------------------------------------------------------------
+
+__host__ __device__ __forceinline__ u64 mix64(u64 z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// K:57-61 (frame is the PRE-step frame index, engine.py:233)
+__host__ __device__ __forceinline__ u64 problem_seed(i64 frame, i64 agent_id)
+{
+    return mix64(((u64)frame << 32) | ((u64)agent_id & 0xFFFFFFFFULL));
+}
+
+#define ORCA_GOLDEN 0x9E3779B97F4A7C15ULL
+
+// x mod m for 1 <= m <= 2^16 without a 64-bit division
+__device__ __forceinline__ uint32_t mod_small(u64 x, uint32_t m)
+{
+    uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+    uint32_t two32 = (uint32_t)(0xFFFFFFFFu % m) + 1u; // 2^32 mod m, possibly == m
+    if (two32 == m) two32 = 0;
+    uint32_t r = (hi % m) * two32 + (lo % m); // < m*m + m <= 2^32 for m <= 2^16 - 1
+    return r % m;
+}
+
+// ---------------------------------------------------------------------------
+// velocity-obstacle exit                                              K:343-419
+// ---------------------------------------------------------------------------
+
+// Returns false only for exactly coincident centres. (ux,uy) is the shortest
+// displacement of the relative velocity to the VO boundary, (nx,ny) the outward
+// unit normal there.
+template <typename R>
+__device__ __forceinline__ bool vo_exit(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
+                                        R &ux, R &uy, R &nx, R &ny)
+{
+    if (rpx == R(0) && rpy == R(0)) {
+        ux = uy = nx = ny = R(0);
+        return false;
+    }
+    const R d2 = rpx * rpx + rpy * rpy;
+    const R r2 = comb_r * comb_r;
+
+    if (d2 < r2) { // overlapping: disc of the dt horizon, K:357-376
+        const R inv = div_rn<R>(R(1), dt);
+        const R cx = rpx * inv, cy = rpy * inv;
+        const R rr = comb_r * inv;
+        const R wx = rvx - cx, wy = rvy - cy;
+        const R wl2 = wx * wx + wy * wy;
+        R hx, hy, wl;
+        if (wl2 < R(1e-24)) {
+            const R d = sqrt_rn<R>(d2);
+            hx = div_rn<R>(-rpx, d);
+            hy = div_rn<R>(-rpy, d);
+            wl = R(0);
+        } else {
+            wl = sqrt_rn<R>(wl2);
+            hx = div_rn<R>(wx, wl);
+            hy = div_rn<R>(wy, wl);
+        }
+        const R s = rr - wl;
+        ux = s * hx;
+        uy = s * hy;
+        nx = hx;
+        ny = hy;
+        return true;
+    }
+
+    const R inv = div_rn<R>(R(1), tau);
+    const R cx = rpx * inv, cy = rpy * inv;
+    const R rr = comb_r * inv;
+    const R wx = rvx - cx, wy = rvy - cy;
+    const R wl2 = wx * wx + wy * wy;
+    const R dot_wp = wx * rpx + wy * rpy;
+
+    if (wl2 < R(1e-24)) { // at the cut-off disc centre, K:387-393
+        const R d = sqrt_rn<R>(d2);
+        const R hx = div_rn<R>(-rpx, d), hy = div_rn<R>(-rpy, d);
+        ux = rr * hx;
+        uy = rr * hy;
+        nx = hx;
+        ny = hy;
+        return true;
+    }
+
+    if (dot_wp < R(0) && dot_wp * dot_wp > r2 * wl2) { // cut-off arc, K:395-401
+        const R wl = sqrt_rn<R>(wl2);
+        const R hx = div_rn<R>(wx, wl), hy = div_rn<R>(wy, wl);
+        const R s = rr - wl;
+        ux = s * hx;
+        uy = s * hy;
+        nx = hx;
+        ny = hy;
+        return true;
+    }
+
+    // tangent leg, side by the sign of cross(rel_pos, w), K:403-419
+    const R leg = sqrt_rn<R>(d2 - r2);
+    R dx, dy;
+    if (rpx * wy - rpy * wx > R(0)) {
+        dx = div_rn<R>(rpx * leg - rpy * comb_r, d2);
+        dy = div_rn<R>(rpx * comb_r + rpy * leg, d2);
+    } else {
+        dx = div_rn<R>(-(rpx * leg + rpy * comb_r), d2);
+        dy = div_rn<R>(rpx * comb_r - rpy * leg, d2);
+    }
+    const R t = rvx * dx + rvy * dy;
+    ux = t * dx - rvx;
+    uy = t * dy - rvy;
+    R mx = -dy, my = dx;
+    if (mx * rpx + my * rpy > R(0)) {
+        mx = -mx;
+        my = -my;
+    }
+    nx = mx;
+    ny = my;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// LP core, written against a constraint "view" V:
+//     V::get(pos, px, py, nx, ny)   constraint at position `pos` of the order
+//                                   this view walks (shuffled or identity)
+// and a projected-constraint scratch P with get(m, ...)/set(m, ...).
+// ---------------------------------------------------------------------------
+
+#define ORCA_PARALLEL_EPS 1e-12
+
+// K:74-119. `zz` shifts every constraint point by -zz*normal (the z-relaxed set
+// of K:276-278); SHIFT=false compiles the shift out.
+template <typename R, bool SHIFT, typename V>
+__device__ __forceinline__ bool lp1_target(const V &view, int i_pos, R zz, R cap, R tx, R ty,
+                                           R &ox, R &oy)
+{
+    R px, py, nx, ny;
+    view.get(i_pos, px, py, nx, ny);
+    if (SHIFT) {
+        px = px - zz * nx;
+        py = py - zz * ny;
+    }
+    const R dx = -ny, dy = nx;
+    const R pd = px * dx + py * dy;
+    const R disc = pd * pd + cap * cap - (px * px + py * py);
+    if (disc < R(0)) return false;
+    const R sq = sqrt_rn<R>(disc);
+    R t_left = -pd - sq;
+    R t_right = -pd + sq;
+
+    for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
+        R qx, qy, mx, my;
+        view.get(j_pos, qx, qy, mx, my);
+        if (SHIFT) {
+            qx = qx - zz * mx;
+            qy = qy - zz * my;
+        }
+        const R a = dx * mx + dy * my;
+        const R b = (qx - px) * mx + (qy - py) * my;
+        if (R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS)) {
+            if (b > R(0)) return false;
+            continue;
+        }
+        const R t = div_rn<R>(b, a);
+        if (a > R(0)) {
+            if (t > t_left) t_left = t;
+        } else {
+            if (t < t_right) t_right = t;
+        }
+        if (t_left > t_right) return false;
+    }
+    R t = (tx - px) * dx + (ty - py) * dy;
+    if (t < t_left) t = t_left;
+    else if (t > t_right) t = t_right;
+    ox = px + t * dx;
+    oy = py + t * dy;
+    return true;
+}
+
+// K:122-146. Returns true if feasible; otherwise fail_pos is set and (vx,vy) is
+// the last point that satisfied positions [0, fail_pos).
+template <typename R, bool SHIFT, typename V>
+__device__ __forceinline__ bool lp2_target(const V &view, int k, R zz, R cap, R tx, R ty,
+                                           int &fail_pos, R &vx, R &vy)
+{
+    const R t2 = tx * tx + ty * ty;
+    if (t2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(t2));
+        vx = tx * s;
+        vy = ty * s;
+    } else {
+        vx = tx;
+        vy = ty;
+    }
+    for (int i_pos = 0; i_pos < k; ++i_pos) {
+        R px, py, nx, ny;
+        view.get(i_pos, px, py, nx, ny);
+        if (SHIFT) {
+            px = px - zz * nx;
+            py = py - zz * ny;
+        }
+        if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+            R nvx, nvy;
+            if (!lp1_target<R, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy)) {
+                fail_pos = i_pos;
+                return false;
+            }
+            vx = nvx;
+            vy = nvy;
+        }
+    }
+    fail_pos = -1;
+    return true;
+}
+
+// K:153-190, identity order over the projected constraints
+template <typename R, typename P>
+__device__ __forceinline__ bool lp1_dir(const P &proj, int upto, R cap, R ox, R oy, R &rx, R &ry)
+{
+    R px, py, nx, ny;
+    proj.get(upto, px, py, nx, ny);
+    const R dx = -ny, dy = nx;
+    const R pd = px * dx + py * dy;
+    const R disc = pd * pd + cap * cap - (px * px + py * py);
+    if (disc < R(0)) return false;
+    const R sq = sqrt_rn<R>(disc);
+    R t_left = -pd - sq;
+    R t_right = -pd + sq;
+    for (int j = 0; j < upto; ++j) {
+        R qx, qy, mx, my;
+        proj.get(j, qx, qy, mx, my);
+        const R a = dx * mx + dy * my;
+        const R b = (qx - px) * mx + (qy - py) * my;
+        if (R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS)) {
+            if (b > R(0)) return false;
+            continue;
+        }
+        const R t = div_rn<R>(b, a);
+        if (a > R(0)) {
+            if (t > t_left) t_left = t;
+        } else {
+            if (t < t_right) t_right = t;
+        }
+        if (t_left > t_right) return false;
+    }
+    const R t = (dx * ox + dy * oy) > R(0) ? t_right : t_left;
+    rx = px + t * dx;
+    ry = py + t * dy;
+    return true;
+}
+
+// K:193-205
+template <typename R, typename P>
+__device__ __forceinline__ bool lp2_dir(const P &proj, int m, R cap, R ox, R oy, R &rx, R &ry)
+{
+    R vx = cap * ox, vy = cap * oy;
+    for (int i = 0; i < m; ++i) {
+        R px, py, nx, ny;
+        proj.get(i, px, py, nx, ny);
+        if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+            R nvx, nvy;
+            if (!lp1_dir<R, P>(proj, i, cap, ox, oy, nvx, nvy)) {
+                rx = vx;
+                ry = vy;
+                return false;
+            }
+            vx = nvx;
+            vy = nvy;
+        }
+    }
+    rx = vx;
+    ry = vy;
+    return true;
+}
+
+// K:212-251: minimise the maximum (clamped) violation over the shuffled order,
+// starting at position `begin` from (vx,vy).
+template <typename R, typename V, typename P>
+__device__ __forceinline__ void lp3_minmax(const V &view, P &proj, int k, int begin, R cap, R &vx,
+                                           R &vy, R &z)
+{
+    R dist = R(0);
+    for (int i_pos = begin; i_pos < k; ++i_pos) {
+        R cpx, cpy, cnx, cny;
+        view.get(i_pos, cpx, cpy, cnx, cny);
+        const R viol = (cpx - vx) * cnx + (cpy - vy) * cny;
+        if (viol > dist) {
+            int m = 0;
+            for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
+                R jpx, jpy, jnx, jny;
+                view.get(j_pos, jpx, jpy, jnx, jny);
+                const R mx = jnx - cnx;
+                const R my = jny - cny;
+                const R ml2 = mx * mx + my * my;
+                if (ml2 < R(1e-24)) continue;
+                const R rhs = jpx * jnx + jpy * jny - cpx * cnx - cpy * cny;
+                const R ml = sqrt_rn<R>(ml2);
+                proj.set(m, div_rn<R>(mx * rhs, ml2), div_rn<R>(my * rhs, ml2), div_rn<R>(mx, ml),
+                         div_rn<R>(my, ml));
+                ++m;
+            }
+            R nvx, nvy;
+            if (lp2_dir<R, P>(proj, m, cap, cnx, cny, nvx, nvy)) {
+                vx = nvx;
+                vy = nvy;
+            }
+            dist = (cpx - vx) * cnx + (cpy - vy) * cny;
+            if (dist < R(0)) dist = R(0);
+        }
+    }
+    z = dist;
+}
+
+// K:254-283. VS walks the shuffled order (min-max stage), VI the identity order
+// (re-solve toward the warm start on the z-relaxed set).
+template <typename R, typename VS, typename VI, typename P>
+__device__ __forceinline__ void least_penetration(const VS &shuf, const VI &ident, P &proj, int k,
+                                                  int begin, R cap, R wx, R wy, R &rx, R &ry)
+{
+    const R w2 = wx * wx + wy * wy;
+    if (w2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(w2));
+        wx = wx * s;
+        wy = wy * s;
+    }
+    R vx = wx, vy = wy, z;
+    lp3_minmax<R, VS, P>(shuf, proj, k, begin, cap, vx, vy, z);
+
+    R slack = R(0);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const R zz = z + slack;
+        int fail;
+        R qx, qy;
+        if (lp2_target<R, true, VI>(ident, k, zz, cap, wx, wy, fail, qx, qy)) {
+            rx = qx;
+            ry = qy;
+            return;
+        }
+        slack = slack * R(1e3) + R(1e-12) * (R(1) + z);
+    }
+    rx = vx;
+    ry = vy;
+}
+
+} // namespace orca

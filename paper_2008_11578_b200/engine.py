@@ -1,0 +1,317 @@
+"""Drop-in replacement for the reference's per-frame step, running on a B200.
+
+Public surface (same names, arguments and error behaviour as the reference's
+pkg/src/orcasim/engine.py):
+
+    init_state(config[, agents])  engine.py:173-191
+    step(state, config, worker_count=1, work_unit_steps=4096)
+                                  engine.py:298-308 -> (SimState, FrameMetrics)
+    problem_seed(agent_id, frame) engine.py:40-43
+    desired_velocity(agent, dt)   engine.py:118-130
+
+plus `Simulation`, a device-resident stepping handle for runs that do not want
+a host round trip per frame (the reference's run() loop, engine.py:333-346,
+without the Python between frames).
+
+Everything numerical happens in liborca_b200.so (hand-written sm_100a CUDA,
+reached through the C ABI of include/orca_b200.h). There is no CPU fallback:
+without the library or without a CUDA device these functions raise.
+
+`worker_count` / `work_unit_steps` are accepted for signature compatibility and
+ignored: the reference guarantees results independent of both (engine.py:7-8).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import time as _time
+
+import numpy as np
+
+from . import _lib
+from ._lib import OrcaError, OrcaInfo, OrcaParams, check, load, precision_code, ptr
+from .types import AgentClass, FrameMetrics, ScenarioConfig, SimState
+
+__all__ = ["Simulation", "init_state", "step", "problem_seed", "desired_velocity",
+           "DEFAULT_PRECISION", "COLLISION_TOLERANCE", "DEFAULT_WORK_UNIT_STEPS"]
+
+COLLISION_TOLERANCE = 1e-6          # engine.py:36 (applied inside k_min_sep)
+DEFAULT_WORK_UNIT_STEPS = 4096      # engine.py:37
+MASK64 = (1 << 64) - 1
+
+# "f32": FP32 device state and LP arithmetic, FP64 binning / neighbour keys
+# (the product path). "f64": everything FP64, bit-identical to the reference.
+DEFAULT_PRECISION = os.environ.get("ORCA_B200_PRECISION", "f32")
+
+
+def _mix64(z: int) -> int:
+    z &= MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return (z ^ (z >> 31)) & MASK64
+
+
+def problem_seed(agent_id: int, frame: int) -> int:
+    """Shuffle seed of one agent's LP in one frame (engine.py:40-43)."""
+    return _mix64(((frame & 0xFFFFFFFF) << 32) | (agent_id & 0xFFFFFFFF)) & MASK64
+
+
+def desired_velocity(agent, dt: float) -> np.ndarray:
+    """engine.py:118-130 for one AgentState-like object (host-side helper)."""
+    if dt <= 0:
+        raise ValueError(f"dt must be positive, got {dt!r}")
+    dx = agent.goal[0] - agent.position[0]
+    dy = agent.goal[1] - agent.position[1]
+    dist = math.sqrt(dx * dx + dy * dy)
+    if dist == 0.0:
+        return np.zeros(2)
+    speed = min(agent.pref_speed, dist / dt)
+    scale = speed / dist
+    return np.array([dx * scale, dy * scale])
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if shape is None else a.reshape(shape)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _params_from_config(config, remove_arrivals: bool, compute_metrics: bool) -> OrcaParams:
+    p = OrcaParams()
+    p.dt = float(config.dt)
+    p.tau = float(config.tau)
+    p.neighbor_radius = float(config.neighbor_radius)
+    p.avoidance_margin = float(config.avoidance_margin)
+    fm = np.asarray(config.responsibility.as_array(), dtype=np.float64)
+    if fm.shape != (2, 2):
+        raise ValueError(f"responsibility matrix must be 2x2, got {fm.shape}")
+    for i in range(4):
+        p.fmat[i] = float(fm.flat[i])
+    p.max_neighbors = int(config.max_neighbors)
+    p.remove_arrivals = 1 if remove_arrivals else 0
+    p.compute_metrics = 1 if compute_metrics else 0
+    return p
+
+
+class Simulation:
+    """A device-resident crowd: upload once, step many times, read back.
+
+        sim = Simulation(config, capacity=state.active_count)
+        sim.load(state)
+        sim.run(100)                  # 100 frames, no host round trips
+        state = sim.state()           # SimState of numpy float64 / int64 arrays
+
+    remove_arrivals / compute_metrics select the parts of engine._advance that
+    sit next to the steering step proper (arrival removal engine.py:251-255,
+    metrics engine.py:270-286).
+    """
+
+    def __init__(self, config: ScenarioConfig, capacity: int, precision=None, device: int = 0,
+                 remove_arrivals: bool = True, compute_metrics: bool = False, stream=None):
+        self._L = load()
+        self._h = C.c_void_p()
+        self.precision = precision_code(DEFAULT_PRECISION if precision is None else precision)
+        self.capacity = int(capacity)
+        self.device = int(device)
+        check(self._L.orca_create(C.byref(self._h), self.device, self.capacity, self.precision))
+        self._rng_state = None
+        self._dt = float(config.dt)
+        self.set_config(config, remove_arrivals, compute_metrics)
+        if stream is not None:
+            self.set_stream(stream)
+
+    # -- lifetime -----------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h:
+            self._L.orca_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- configuration ------------------------------------------------------
+    def set_config(self, config, remove_arrivals: bool = True, compute_metrics: bool = False):
+        self._params = _params_from_config(config, remove_arrivals, compute_metrics)
+        self._dt = float(config.dt)
+        check(self._L.orca_set_params(self._h, C.byref(self._params)), self._h)
+
+    def set_stream(self, stream):
+        """Run on an existing CUDA stream (an int handle or a torch.cuda.Stream)."""
+        handle = getattr(stream, "cuda_stream", stream)
+        check(self._L.orca_set_stream(self._h, C.c_void_p(int(handle) if handle else None)), self._h)
+
+    # -- state --------------------------------------------------------------
+    def load(self, state: SimState):
+        n = int(np.asarray(state.ids).shape[0])
+        self._keep = (_i64(state.ids), _f64(state.positions, (n, 2)), _f64(state.velocities, (n, 2)),
+                      _f64(state.radii), _f64(state.pref_speeds), _f64(state.max_speeds),
+                      _f64(state.goals, (n, 2)), _f64(state.goal_tols), _i64(state.class_codes))
+        check(self._L.orca_upload(self._h, n, int(state.frame), *[ptr(a) for a in self._keep]), self._h)
+        self._rng_state = getattr(state, "rng_state", None)
+        self._state_type = type(state)
+
+    def load_pv(self, positions, velocities, frame: int):
+        pos, vel = _f64(positions), _f64(velocities)
+        n = pos.shape[0] if pos.ndim == 2 else pos.size // 2
+        self._keep_pv = (pos, vel)
+        check(self._L.orca_upload_pv(self._h, n, int(frame), ptr(pos), ptr(vel)), self._h)
+
+    def step(self):
+        check(self._L.orca_step(self._h), self._h)
+
+    def run(self, steps: int):
+        check(self._L.orca_run(self._h, int(steps)), self._h)
+
+    def sync(self):
+        self._raise_like_reference(self._L.orca_sync(self._h))
+
+    def info(self) -> OrcaInfo:
+        info = OrcaInfo()
+        self._raise_like_reference(self._L.orca_get_info(self._h, C.byref(info)))
+        return info
+
+    def _raise_like_reference(self, rc: int):
+        if rc in (_lib.ORCA_ECOINCIDENT, _lib.ORCA_ERANGE):
+            # engine.py:239-245 / engine.py:152-153 raise plain ValueError with this text
+            raise ValueError(self._L.orca_last_error(self._h).decode())
+        check(rc, self._h)
+
+    def state(self, state_type=None) -> SimState:
+        info = self.info()
+        n = int(info.active_agents)
+        ids = np.empty(n, dtype=np.int64)
+        pos, vel, goals = np.empty((n, 2)), np.empty((n, 2)), np.empty((n, 2))
+        radii, pref, maxs, gtol = np.empty(n), np.empty(n), np.empty(n), np.empty(n)
+        cls = np.empty(n, dtype=np.int64)
+        self._raise_like_reference(self._L.orca_download(
+            self._h, ptr(ids), ptr(pos), ptr(vel), ptr(radii), ptr(pref), ptr(maxs), ptr(goals),
+            ptr(gtol), ptr(cls)))
+        mk = state_type or getattr(self, "_state_type", SimState)
+        frame = int(info.frame)
+        return mk(frame=frame, time=frame * self._dt, ids=ids, positions=pos, velocities=vel,
+                  radii=radii, pref_speeds=pref, max_speeds=maxs, goals=goals, goal_tols=gtol,
+                  class_codes=cls, rng_state=self._rng_state, lp_fallbacks=int(info.lp_fallbacks))
+
+    def positions_velocities(self):
+        n = int(self.info().active_agents)
+        pos, vel = np.empty((n, 2)), np.empty((n, 2))
+        self._raise_like_reference(self._L.orca_download_pv(self._h, ptr(pos), ptr(vel)))
+        return pos, vel
+
+    def step_host(self, positions, velocities, frame: int, out_pos=None, out_vel=None,
+                  out_status=None):
+        """One frame through host buffers (orca_step_host): H2D of positions and
+        velocities, the step, D2H of the results. Needs remove_arrivals=False."""
+        pos, vel = _f64(positions), _f64(velocities)
+        n = pos.shape[0]
+        out_pos = np.empty((n, 2)) if out_pos is None else out_pos
+        out_vel = np.empty((n, 2)) if out_vel is None else out_vel
+        self._raise_like_reference(self._L.orca_step_host(
+            self._h, n, int(frame), ptr(pos), ptr(vel), ptr(out_pos), ptr(out_vel), ptr(out_status)))
+        return out_pos, out_vel
+
+    def debug_last_step(self, n: int, max_neighbors: int):
+        """Parity taps of the last step (orca_debug_last_step), storage-row order."""
+        k = max(int(max_neighbors), 1)
+        out = dict(cell_ix=np.empty(n, dtype=np.int64), cell_iy=np.empty(n, dtype=np.int64),
+                   nb_rows=np.full((n, k), -1, dtype=np.int64), nb_count=np.empty(n, dtype=np.int64),
+                   out_v=np.empty((n, 2)), status=np.empty(n, dtype=np.int64),
+                   failed_at=np.empty(n, dtype=np.int64), des=np.empty((n, 2)))
+        self._raise_like_reference(self._L.orca_debug_last_step(
+            self._h, n, ptr(out["cell_ix"]), ptr(out["cell_iy"]), ptr(out["nb_rows"]),
+            ptr(out["nb_count"]), ptr(out["out_v"]), ptr(out["status"]), ptr(out["failed_at"]),
+            ptr(out["des"])))
+        if max_neighbors == 0:
+            out["nb_rows"] = out["nb_rows"][:, :0]
+        return out
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped functions
+# ---------------------------------------------------------------------------
+
+def init_state(config: ScenarioConfig, agents=None) -> SimState:
+    """Start agents at their desired velocities (engine.py:173-191).
+
+    The reference samples spawn positions from config.regions
+    (scenario.build_agents, out of this package's scope); here the caller hands
+    over the spawned agents as `agents` (objects with id, position, radius,
+    pref_speed, max_speed, goal, agent_class -- e.g. orcasim.AgentState) or as
+    `config.agents`. With neither, the crowd is empty."""
+    if agents is None:
+        agents = getattr(config, "agents", None) or []
+    n = len(agents)
+    ids = np.array([a.id for a in agents], dtype=np.int64)
+    positions = np.array([a.position for a in agents], dtype=np.float64).reshape(n, 2)
+    radii = np.array([a.radius for a in agents], dtype=np.float64)
+    pref = np.array([a.pref_speed for a in agents], dtype=np.float64)
+    maxs = np.array([a.max_speed for a in agents], dtype=np.float64)
+    goals = np.array([a.goal for a in agents], dtype=np.float64).reshape(n, 2)
+    codes = np.array([int(a.agent_class) for a in agents], dtype=np.int64)
+    gtols = np.array([config.goal_tolerance_for(AgentClass(int(a.agent_class))) for a in agents],
+                     dtype=np.float64)
+    # engine.py:133-139 (host-side setup, once per run)
+    d = goals - positions
+    dist = np.sqrt(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1])
+    speed = np.minimum(pref, dist / config.dt)
+    safe = np.where(dist > 0.0, dist, 1.0)
+    scale = np.where(dist > 0.0, speed / safe, 0.0)
+    velocities = d * scale[:, None]
+    return SimState(frame=0, time=0.0, ids=ids, positions=positions, velocities=velocities,
+                    radii=radii, pref_speeds=pref, max_speeds=maxs, goals=goals, goal_tols=gtols,
+                    class_codes=codes, rng_state=np.random.default_rng(config.seed))
+
+
+_handles: dict = {}
+
+
+def _handle_for(config, n: int, precision, device: int) -> Simulation:
+    """step() keeps one device handle per (device, precision) and grows it on demand."""
+    key = (device, precision_code(DEFAULT_PRECISION if precision is None else precision))
+    sim = _handles.get(key)
+    if sim is None or sim.capacity < n:
+        if sim is not None:
+            sim.close()
+        cap = max(1024, int(n * 1.25))
+        sim = Simulation(config, cap, precision=key[1], device=device,
+                         remove_arrivals=True, compute_metrics=True)
+        _handles[key] = sim
+    return sim
+
+
+def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
+         work_unit_steps: int = DEFAULT_WORK_UNIT_STEPS, *, precision=None, device: int = 0):
+    """Advance one frame on the GPU; returns (new_state, FrameMetrics) exactly
+    like the reference's engine.step (engine.py:298-308). `state` is not
+    modified. Raises ValueError with the reference's messages for coincident
+    centres (engine.py:239-245) and out-of-range positions (engine.py:152-153)."""
+    del worker_count, work_unit_steps  # results do not depend on them (engine.py:7-8)
+    t0 = _time.perf_counter()
+    n = int(np.asarray(state.ids).shape[0])
+    sim = _handle_for(config, n, precision, device)
+    sim.set_config(config, remove_arrivals=True, compute_metrics=True)
+    sim.load(state)
+    sim.step()
+    info = sim.info()                       # raises the reference's ValueError on device errors
+    new_state = sim.state(type(state))
+    wall_ms = (_time.perf_counter() - t0) * 1e3
+    n2 = new_state.ids.shape[0]
+    min_sep = float(info.min_separation) if n2 >= 2 else float("inf")
+    metrics = FrameMetrics(frame=new_state.frame, wall_ms=wall_ms, min_separation=min_sep,
+                           collision_count=int(info.collision_count) if n2 >= 2 else 0,
+                           active_agents=int(n2))
+    return new_state, metrics

@@ -1,0 +1,199 @@
+"""Batched closest-point LP on the GPU: the device twin of the reference's
+lp.solve_batch / _kernels.solve_range (pkg/src/orcasim/lp.py:263-291,
+pkg/src/orcasim/_kernels.py:306-336).
+
+    solve_range(coff, cpts, cnrm, tgt, caps, seeds) -> (out_v, status, failed_at)
+        flat CSR arrays exactly as _kernels.solve_range takes them
+    solve_batch(problems)  -> list[LpResult]
+        object-level API with the reference's validation messages
+    LpBatch(...)            resident batch for repeated solves (benchmarks)
+
+No CPU fallback: all three launch liborca_b200.so kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from ._lib import check, load, precision_code, ptr
+
+__all__ = ["HalfPlaneConstraint", "LpProblem", "LpResult", "LpStatus", "LpBatch",
+           "shuffle_order", "solve_range", "solve_batch", "solve_closest_point"]
+
+MASK64 = (1 << 64) - 1
+
+
+class LpStatus(IntEnum):
+    FEASIBLE = 0
+    FALLBACK_USED = 1
+
+
+@dataclass
+class HalfPlaneConstraint:
+    """Velocities v with dot(v - point, normal) >= 0 are permitted (lp.py)."""
+    point: np.ndarray
+    normal: np.ndarray
+
+
+@dataclass
+class LpProblem:
+    constraints: list
+    target: tuple
+    speed_cap: float
+    shuffle_seed: int = 0
+
+
+@dataclass
+class LpResult:
+    velocity: np.ndarray
+    status: LpStatus
+    failed_at: int | None = None
+
+
+def _mix64(z: int) -> int:
+    z &= MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return (z ^ (z >> 31)) & MASK64
+
+
+def shuffle_order(count: int, seed: int) -> list[int]:
+    """Constraint insertion order for a shuffle seed (lp.py:101-112); host-side
+    twin of the in-kernel shuffle, kept in lockstep by tests/test_gpu_kat.py."""
+    perm = list(range(count))
+    state = seed & MASK64
+    for i in range(count - 1, 0, -1):
+        state = (state + 0x9E3779B97F4A7C15) & MASK64
+        j = _mix64(state) % (i + 1)
+        perm[i], perm[j] = perm[j], perm[i]
+    return perm
+
+
+def _prep(coff, cpts, cnrm, tgt, caps, seeds):
+    coff = np.ascontiguousarray(coff, dtype=np.int64)
+    n = coff.shape[0] - 1
+    cpts = np.ascontiguousarray(cpts, dtype=np.float64).reshape(-1, 2)
+    cnrm = np.ascontiguousarray(cnrm, dtype=np.float64).reshape(-1, 2)
+    tgt = np.ascontiguousarray(tgt, dtype=np.float64).reshape(-1, 2)
+    caps = np.ascontiguousarray(caps, dtype=np.float64)
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    if n < 0 or tgt.shape[0] != n or caps.shape[0] != n or seeds.shape[0] != n:
+        raise ValueError("inconsistent batch arrays")
+    if cpts.shape[0] != int(coff[-1]) or cnrm.shape[0] != int(coff[-1]):
+        raise ValueError("constraint arrays do not match coff[-1]")
+    return n, coff, cpts, cnrm, tgt, caps, seeds
+
+
+def solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision="f32", device: int = 0):
+    """_kernels.solve_range over the whole batch on the GPU.
+    Returns (out_v f64[n,2], status i64[n], failed_at i64[n])."""
+    n, coff, cpts, cnrm, tgt, caps, seeds = _prep(coff, cpts, cnrm, tgt, caps, seeds)
+    out_v = np.empty((n, 2))
+    status = np.empty(n, dtype=np.int64)
+    failed = np.empty(n, dtype=np.int64)
+    check(load().orca_lp_solve_batch(device, precision_code(precision), n, ptr(coff), ptr(cpts),
+                                     ptr(cnrm), ptr(tgt), ptr(caps), ptr(seeds), ptr(out_v),
+                                     ptr(status), ptr(failed)))
+    return out_v, status, failed
+
+
+class LpBatch:
+    """A batch resident on the device: build once, solve repeatedly."""
+
+    def __init__(self, coff, cpts, cnrm, tgt, caps, seeds, precision="f32", device: int = 0,
+                 stream=None):
+        self._L = load()
+        self.n, coff, cpts, cnrm, tgt, caps, seeds = _prep(coff, cpts, cnrm, tgt, caps, seeds)
+        self.m = int(coff[-1])
+        self._h = C.c_void_p()
+        check(self._L.orca_lp_batch_create(C.byref(self._h), device, precision_code(precision),
+                                           self.n, ptr(coff), ptr(cpts), ptr(cnrm), ptr(tgt),
+                                           ptr(caps), ptr(seeds)))
+        if stream is not None:
+            handle = getattr(stream, "cuda_stream", stream)
+            check(self._L.orca_lp_batch_set_stream(
+                self._h, C.c_void_p(int(handle) if handle else None)))
+
+    def solve(self):
+        check(self._L.orca_lp_batch_solve(self._h))
+
+    def results(self):
+        out_v = np.empty((self.n, 2))
+        status = np.empty(self.n, dtype=np.int64)
+        failed = np.empty(self.n, dtype=np.int64)
+        check(self._L.orca_lp_batch_download(self._h, ptr(out_v), ptr(status), ptr(failed)))
+        return out_v, status, failed
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h:
+            self._L.orca_lp_batch_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- object-level API (validation text follows lp.py:115-140) -----------------
+
+def _validate_constraints(constraints, label=""):
+    pts = np.empty((len(constraints), 2), dtype=np.float64)
+    nrm = np.empty((len(constraints), 2), dtype=np.float64)
+    for idx, c in enumerate(constraints):
+        p = np.asarray(c.point, dtype=float).reshape(2)
+        n = np.asarray(c.normal, dtype=float).reshape(2)
+        if not np.all(np.isfinite(p)) or not np.all(np.isfinite(n)):
+            raise ValueError(f"{label}constraint {idx}: non-finite point or normal")
+        nn = float(n[0] * n[0] + n[1] * n[1])
+        if abs(nn - 1.0) > 2.1e-9:
+            raise ValueError(
+                f"{label}constraint {idx}: normal must be unit length, got |n|={np.sqrt(nn)!r}")
+        pts[idx] = p
+        nrm[idx] = n
+    return pts, nrm
+
+
+def _validate_problem(problem, label=""):
+    target = np.asarray(problem.target, dtype=float).reshape(2)
+    if not np.all(np.isfinite(target)):
+        raise ValueError(f"{label}target is non-finite")
+    cap = float(problem.speed_cap)
+    if not np.isfinite(cap) or cap <= 0.0:
+        raise ValueError(f"{label}speed_cap must be positive and finite, got {cap!r}")
+    pts, nrm = _validate_constraints(problem.constraints, label)
+    return pts, nrm, target, cap
+
+
+def solve_batch(problems, worker_count: int = 1, work_unit_steps: int = 64, *,
+                precision="f32", device: int = 0):
+    """lp.solve_batch (lp.py:263-291): validate, pack to CSR, solve on the GPU."""
+    del worker_count, work_unit_steps
+    n = len(problems)
+    coff = np.zeros(n + 1, dtype=np.int64)
+    parts = []
+    for i, p in enumerate(problems):
+        parts.append(_validate_problem(p, label=f"problem {i}: "))
+        coff[i + 1] = coff[i] + len(p.constraints)
+    m = int(coff[n])
+    cpts, cnrm = np.empty((m, 2)), np.empty((m, 2))
+    tgt, caps = np.empty((n, 2)), np.empty(n)
+    seeds = np.empty(n, dtype=np.uint64)
+    for i, (pts, nrm, target, cap) in enumerate(parts):
+        cpts[coff[i]:coff[i + 1]] = pts
+        cnrm[coff[i]:coff[i + 1]] = nrm
+        tgt[i], caps[i] = target, cap
+        seeds[i] = np.uint64(problems[i].shuffle_seed & MASK64)
+    out_v, status, failed = solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision, device)
+    return [LpResult(out_v[i].copy(), LpStatus(int(status[i])),
+                     None if status[i] == 0 else int(failed[i])) for i in range(n)]
+
+
+def solve_closest_point(problem, *, precision="f32", device: int = 0) -> LpResult:
+    """lp.solve_closest_point (lp.py:152-165) for one problem."""
+    return solve_batch([problem], precision=precision, device=device)[0]
