@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the ORCA steering step (BASELINE.json: agent-steps/s and ms/step
+at 1M agents).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload plaza_1m] [--precision mixed|f32|f64]
+
+One "step" is one frame of the steering step (bin build, neighbour gather, ORCA
+half-planes, LP + least-penetration fallback, integration) over the whole
+synthetic crowd. Prints ONE JSON line on rank 0.
+
+  value        agent-steps/s with the crowd resident in HBM (orca_step x K)
+  e2e          the same metric through the drop-in call a reference user makes,
+               engine.step(state, config): host SimState in, host SimState +
+               FrameMetrics out (arrival removal and metrics included), with
+               the H2D / D2H copies inside the timed region
+  roofline     the dominant kernel of the step, timed live with CUDA events on
+               the launching stream (orca_profile_stages), against the measured
+               HBM peak of MEASURED_PEAKS.json
+  cpu_baseline oracle/orca_oracle.c (a C port of the reference's step, pinned
+               bit-exactly to the reference) on this box's host cores, on a
+               bounded sample of the same workload
+  --impl reference   times that CPU port as the reference arm (the Python+numba
+               reference itself cannot travel to the GPU box)
+
+Multi-GPU (torchrun, one rank per GPU): the plaza is cut into x-strips, one per
+rank, with per-step halo exchange and migration over NCCL (parallel/strips.py);
+weak scaling: every rank owns `workload` agents.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2008_11578_b200.synth import CONFIGS, plaza_crowd  # noqa: E402
+
+# algorithmic bytes
+STEP_BYTES_PER_AGENT = 64          # read 44 + write 20, FP32 state
+GATHER_BYTES_PER_AGENT = 8 + 4 + 4 * 16 + 1   # read (x,y) + cell id, write 16 neighbour slots + count
+SOLVE_BYTES_PER_AGENT = 16 + 32 + 1 + 4 * 16 + 1 + 16 + 16 + 2 + 1  # sorted snapshot, des/max/avoid, class, lists, goal, out pv, status, arrived
+BINS_BYTES_PER_AGENT = 16 + 4 + 4 + (16 + 16 + 8 + 1 + 8) + (8 + 16 + 32 + 4 + 4 + 1)  # bbox+count pass, scatter reads, scatter writes
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        names = {"hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                 "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                 "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                 "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(int(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+                try:
+                    mask = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self._h))
+                except Exception:
+                    mask = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h))
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def build_workload(name: str, rank: int = 0, world: int = 1):
+    n_ped, n_veh, density = CONFIGS[name]
+    state, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100 + rank)
+    return state, cfg, dict(workload=name, pedestrians=n_ped, vehicles=n_veh, density_per_m2=density,
+                            neighbor_radius=cfg.neighbor_radius, max_neighbors=cfg.max_neighbors,
+                            dt=cfg.dt, tau=cfg.tau)
+
+
+def cpu_port_rate(state, cfg, rows: int, threads: int, repeats: int = 1):
+    """agent-steps/s of the oracle port, from a bounded sample: the whole-crowd part of
+    the step (grid build, desired velocities) is timed in full, the per-agent part
+    (neighbour query, ORCA, LP, integration) on agents [0, rows) and scaled by n/rows.
+    Returns (agent-steps/s of a full step, seconds of CPU wall time spent per repeat)."""
+    from oracle import oracle as O
+    O.lib()
+    n = state.active_count
+    best_full, spent = None, 0.0
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.frame_solve(state, cfg, worker_count=threads, rows=0)
+        t_common = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        fs = O.frame_solve(state, cfg, worker_count=threads, rows=rows)
+        _ = state.positions[:rows] + fs.out_v[:rows] * cfg.dt      # engine.py:249
+        t_rows = max(time.perf_counter() - t0 - t_common, 1e-9)
+        full = t_common + t_rows * (n / rows)
+        spent = t_common * 2 + t_rows
+        best_full = full if best_full is None else min(best_full, full)
+    return n / best_full, spent
+
+
+def run_reference(args):
+    """--impl reference: the CPU port of the reference step on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    state, cfg, wl = build_workload(args.workload)
+    threads = os.cpu_count() or 1
+    n = state.active_count
+    rows = min(n, args.cpu_rows)
+    for _ in range(max(args.warmup, 1)):
+        cpu_port_rate(state, cfg, min(rows, 8192), threads)
+    rates = []
+    for _ in range(args.steps):
+        rate, _spent = cpu_port_rate(state, cfg, rows, threads)
+        rates.append(rate)
+    value = float(np.median(rates))
+    t_step = n / value
+    sample = (f"per step: grid build + desired velocities over all {n} agents, per-agent solve on rows "
+              f"[0,{rows}) scaled by n/rows; oracle/orca_oracle.c with {threads} pthreads")
+    line = {"impl": "reference", "metric": "agent_steps_per_s", "value": value, "unit": "agent-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": wl,
+            "cpu_baseline": {"value": value, "unit": "agent-steps/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": "ms_per_step is the full-crowd step time extrapolated from the bounded sample"}
+    print(json.dumps(line), flush=True)
+
+
+def pinned_like(torch, arr):
+    t = torch.empty(arr.shape, dtype={np.dtype("float64"): torch.float64,
+                                      np.dtype("int64"): torch.int64}[arr.dtype]).pin_memory()
+    out = t.numpy()
+    out[...] = arr
+    return t, out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_11578_b200 import Simulation
+    from paper_2008_11578_b200 import engine as E
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise RuntimeError("bench.py needs a CUDA device; there is no CPU fallback")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2008_11578_b200.parallel import strips
+        return strips.run_bench(args, rank, world, local)
+
+    state, cfg, wl = build_workload(args.workload)
+    n = state.active_count
+    stream = torch.cuda.Stream()
+    hbm_peak, peak_src = load_peaks()
+
+    # ---- resident: K steps of orca_step on the state in HBM -------------------
+    sim = Simulation(cfg, capacity=n, precision=args.precision, device=local, remove_arrivals=False,
+                     compute_metrics=False, stream=stream)
+    sim.load(state)
+    sim.run(max(args.warmup, 3))
+    sim.sync()
+    l0 = sim.info().kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sim.run(args.steps)
+        e1.record(stream)
+        sim.sync()
+        torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    info = sim.info()
+    launches = int(info.kernel_launches - l0)
+    value = n / ms_step * 1e3
+
+    # ---- per-stage timing, second pass (CUDA events at stage boundaries) -------
+    sim.profile_stages(True)
+    sim.run(args.steps)
+    stage_ms, covered = sim.stage_ms()
+    sim.profile_stages(False)
+    stage_ms = {k: v / max(covered, 1) for k, v in stage_ms.items()}
+    stage_bytes = {"bins": BINS_BYTES_PER_AGENT, "gather": GATHER_BYTES_PER_AGENT,
+                   "solve": SOLVE_BYTES_PER_AGENT}
+    dom = max(("bins", "gather", "solve", "fallback"), key=lambda k: stage_ms[k])
+    dom_bytes = stage_bytes.get(dom, SOLVE_BYTES_PER_AGENT) * n
+    achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
+    fallbacks = int(info.lp_fallbacks)
+    sim.close()
+    if args.resident_only:
+        print(json.dumps({"metric": "agent_steps_per_s", "value": value, "ms_per_step": ms_step,
+                          "stages_ms": stage_ms, "gpu_launches": launches, "n": n,
+                          "precision": args.precision, "note": "resident-only run"}), flush=True)
+        return
+
+    # ---- e2e: engine.step(state, config), host in / host out -------------------
+    keep = []
+    pinned = {}
+    for name in ("ids", "positions", "velocities", "radii", "pref_speeds", "max_speeds", "goals",
+                 "goal_tols", "class_codes"):
+        t, arr = pinned_like(torch, np.ascontiguousarray(getattr(state, name)))
+        keep.append(t)
+        pinned[name] = arr
+    host_state = type(state)(frame=0, time=0.0, rng_state=None, lp_fallbacks=0, **pinned)
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    cur = host_state
+    for _ in range(2):
+        E.step(cur, cfg, precision=args.precision, device=local)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cur = host_state
+    h2d = d2h = 0
+    for _ in range(e2e_steps):
+        n_in = cur.active_count
+        cur, metrics = E.step(cur, cfg, precision=args.precision, device=local)
+        h2d += 104 * n_in
+        d2h += 104 * cur.active_count
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    e2e_value = n / e2e_ms * 1e3
+
+    # ---- e2e through the C ABI with pinned buffers (positions/velocities only) ---
+    sim = Simulation(cfg, capacity=n, precision=args.precision, device=local, remove_arrivals=False,
+                     stream=stream)
+    sim.load(state)
+    tp_in, pos_in = pinned_like(torch, state.positions)
+    tv_in, vel_in = pinned_like(torch, state.velocities)
+    tp_out, pos_out = pinned_like(torch, state.positions)
+    tv_out, vel_out = pinned_like(torch, state.velocities)
+    ts_out, st_out = pinned_like(torch, np.zeros(n, dtype=np.int64))
+    for _ in range(2):
+        sim.step_host(pos_in, vel_in, 0, pos_out, vel_out, st_out)
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        sim.step_host(pos_in, vel_in, k, pos_out, vel_out, st_out)
+        pos_in, pos_out = pos_out, pos_in
+        vel_in, vel_out = vel_out, vel_in
+    abi_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    sim.close()
+
+    # ---- CPU baseline: the oracle port on a bounded sample ------------------------
+    threads = os.cpu_count() or 1
+    rows = min(n, args.cpu_rows)
+    cpu_port_rate(state, cfg, min(rows, 8192), threads)          # warm the page cache / threads
+    cpu_value, _ = cpu_port_rate(state, cfg, rows, threads, repeats=2)
+    cpu1_value, _ = cpu_port_rate(state, cfg, max(1024, rows // 32), 1)
+
+    dtype = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision]
+    wl.update(precision=args.precision,
+              cache="state advances every step; per-step working set ~%.0f MB > 126 MB L2, no flush"
+                    % (n * 260 / 1e6),
+              lp_fallbacks_last_step=fallbacks)
+    line = {
+        "metric": "agent_steps_per_s", "value": value, "unit": "agent-steps/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic", "config": wl, "clocks": clocks.summary(),
+        "e2e": {"value": e2e_value, "unit": "agent-steps/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+                "call": "paper_2008_11578_b200.engine.step(state, config) -- full drop-in incl. "
+                        "arrival removal and metrics; input arrays in pinned host memory",
+                "c_abi_step_host": {"value": n / abi_ms * 1e3, "ms_per_step": abi_ms,
+                                    "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 40 * n}},
+        "gpu_launches": launches,
+        "stages_ms": stage_ms,
+        "roofline": {"bound": "hbm", "kernel": {"bins": "k_count+k_scan+k_scatter", "gather": "k_gather",
+                                                "solve": "k_solve", "fallback": "k_fallback"}[dom],
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": dom_bytes,
+                     "step_frac": STEP_BYTES_PER_AGENT * n / (ms_step * 1e-3) / 1e9 / hbm_peak,
+                     "note": "the step is issue/latency bound, not HBM bound (DESIGN.md s5); "
+                             "fractions are reported against the HBM roofline as the contract asks"},
+        "cpu_baseline": {"value": cpu_value, "unit": "agent-steps/s", "cores": threads, "kind": "port",
+                         "sample": f"one step: grid build + desired velocities over all {n} agents, "
+                                   f"per-agent solve on rows [0,{rows}) scaled by n/rows; "
+                                   f"oracle/orca_oracle.c ({threads} pthreads); "
+                                   f"1 thread: {cpu1_value:.3e} agent-steps/s"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="plaza_1m", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "f32", "f64"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-rows", type=int, default=131072)
+    ap.add_argument("--resident-only", action="store_true",
+                    help="only the HBM-resident timing (for runs under ncu)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -29,11 +29,20 @@
  *   - orca_step / orca_run are asynchronous with respect to the host; errors
  *     raised by device code (coincident centres, grid range) are sticky and
  *     surface at the next orca_sync / orca_download / orca_get_info.
- *   - precision: ORCA_F32 keeps the device state and the LP arithmetic in FP32
- *     (cell indices and neighbour-ordering keys are always FP64, so bins and
- *     neighbour lists are bit-exact for float32-representable inputs);
- *     ORCA_F64 keeps everything in FP64 with no FMA contraction and is
- *     bit-identical to the reference on any input.
+ *   - precision (cell indices and neighbour-ordering keys are FP64 in every
+ *     mode, so bins and neighbour lists are bit-exact whenever the inputs are
+ *     representable in the storage type):
+ *       ORCA_MIXED  FP32 device state (float4 SoA), FP64 arithmetic with no FMA
+ *                   contraction for desired velocity, ORCA half-planes, LP and
+ *                   integration. For float32-representable inputs the solver
+ *                   takes exactly the reference's branches and the results are
+ *                   the reference's, rounded once to FP32 on store. Default.
+ *       ORCA_F32    FP32 state and FP32 arithmetic: fastest; velocities agree
+ *                   with the reference to ~1e-7 m/s typically, but ill-conditioned
+ *                   LPs (dense crowds in the fallback stage) can differ by more
+ *                   than 1e-4 m/s -- counted and reported by the parity tests.
+ *       ORCA_F64    FP64 state and arithmetic: bit-identical to the reference on
+ *                   any float64 input.
  */
 #ifndef ORCA_B200_H
 #define ORCA_B200_H
@@ -62,7 +71,7 @@ enum {
     ORCA_EUNSUPPORTED = -6 /* e.g. max_neighbors above ORCA_MAX_NEIGHBORS */
 };
 
-enum { ORCA_F32 = 0, ORCA_F64 = 1 };
+enum { ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2 };
 
 #define ORCA_MAX_NEIGHBORS 32
 
@@ -94,6 +103,7 @@ typedef struct orca_info {
     double min_separation;   /* last step; +inf unless compute_metrics */
     int32_t grid_nx, grid_ny; /* search-grid dimensions used by the last step */
     double grid_cell;         /* search-grid cell edge (m) */
+    int64_t kernel_launches;  /* kernels this handle has launched since orca_create */
 } orca_info;
 
 /* ---- lifetime ----------------------------------------------------------- */
@@ -153,6 +163,22 @@ ORCA_API int orca_sync(orca_sim *sim);
 
 /* Synchronises, then fills `info`. */
 ORCA_API int orca_get_info(orca_sim *sim, orca_info *info);
+
+/* Per-stage device timing for benchmarks. While enabled, every step records CUDA
+ * events on the handle's stream at the stage boundaries; orca_get_stage_ms
+ * synchronises, writes the accumulated milliseconds of each stage since the last
+ * call into ms[ORCA_N_STAGES] and the number of steps covered into *steps. */
+#define ORCA_N_STAGES 6
+enum {
+    ORCA_STAGE_BINS = 0,     /* bounding box, plan, histogram, scan, scatter */
+    ORCA_STAGE_GATHER = 1,   /* neighbour search */
+    ORCA_STAGE_SOLVE = 2,    /* ORCA half-planes + incremental LP + integration */
+    ORCA_STAGE_FALLBACK = 3, /* least-penetration stage + integration */
+    ORCA_STAGE_FINISH = 4,   /* counters, arrival removal */
+    ORCA_STAGE_METRICS = 5   /* post-step bin build + min separation */
+};
+ORCA_API int orca_profile_stages(orca_sim *sim, int enable);
+ORCA_API int orca_get_stage_ms(orca_sim *sim, double *ms, int64_t *steps);
 
 /* One whole reference step() through host buffers: upload of positions and
  * velocities, one frame, download of the new positions / velocities and the

@@ -234,10 +234,13 @@ class FrameSolve:
 
 
 def frame_solve(state, config, worker_count: int = 1,
-                work_unit_steps: int = DEFAULT_WORK_UNIT_STEPS, debug: bool = False) -> FrameSolve:
+                work_unit_steps: int = DEFAULT_WORK_UNIT_STEPS, debug: bool = False,
+                rows: int | None = None) -> FrameSolve:
     """Grid build + desired velocity + K.frame_solve_range over all agents,
     exactly as engine._advance wires them (E:211-237). With debug=True also
-    returns each agent's ordered neighbour rows and ORCA constraints."""
+    returns each agent's ordered neighbour rows and ORCA constraints.
+    rows=R solves only agents [0, R) (grid and desired velocities still cover
+    the whole crowd) -- the bounded sample bench.py times on the host cores."""
     n = int(np.asarray(state.ids).shape[0])
     max_n = int(config.max_neighbors)
     cell_size = float(config.neighbor_radius)                               # E:211
@@ -257,17 +260,19 @@ def frame_solve(state, config, worker_count: int = 1,
     out.err = np.empty(n, dtype=np.int64)
     out.cell_ix, out.cell_iy, out.des = cix, ciy, des
     out.nb_rows = out.nb_count = out.constraints = None
+    n_solved = n if rows is None else min(int(rows), n)
     if debug:
-        out.nb_rows = np.empty((n, max(max_n, 1)), dtype=np.int64)
-        out.nb_count = np.empty(n, dtype=np.int64)
-        out.constraints = np.empty((n, max(max_n, 1), 4))
+        out.nb_rows = np.empty((n_solved, max(max_n, 1)), dtype=np.int64)
+        out.nb_count = np.empty(n_solved, dtype=np.int64)
+        out.constraints = np.empty((n_solved, max(max_n, 1), 4))
     if n == 0:
         return out
     rc = lib().oracle_frame_solve(
         pos, vel, avoid, _f64(state.max_speeds), _i64(state.class_codes), _i64(state.ids), fmat,
         des, _i64(order), ukeys, ukeys.shape[0], starts, cell_size, reach, rad2, max_n,
         float(config.tau), float(config.dt), int(state.frame), out.out_v, out.status,
-        out.failed_at, out.err, n, int(worker_count), int(work_unit_steps),
+        out.failed_at, out.err, n_solved, int(worker_count),
+        int(work_unit_steps),
         _ptr(out.nb_rows), _ptr(out.nb_count), _ptr(out.constraints))
     assert rc == 0
     if debug and max_n == 0:

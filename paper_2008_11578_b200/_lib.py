@@ -16,8 +16,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liborca_b200.so")
 
-ORCA_F32, ORCA_F64 = 0, 1
+ORCA_F32, ORCA_F64, ORCA_MIXED = 0, 1, 2
 ORCA_MAX_NEIGHBORS = 32
+ORCA_N_STAGES = 6
+STAGE_NAMES = ["bins", "gather", "solve", "fallback", "finish", "metrics"]
 ORCA_ECOINCIDENT, ORCA_ERANGE = -3, -4
 
 # every symbol include/orca_b200.h declares (checked by tests/test_abi.py)
@@ -25,6 +27,7 @@ SYMBOLS = [
     "orca_abi_version", "orca_create", "orca_destroy", "orca_set_stream", "orca_set_params",
     "orca_last_error", "orca_upload", "orca_download", "orca_download_pv", "orca_upload_pv",
     "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host",
+    "orca_profile_stages", "orca_get_stage_ms",
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
     "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
@@ -51,7 +54,7 @@ class OrcaInfo(C.Structure):
     _fields_ = [("frame", C.c_int64), ("active_agents", C.c_int64), ("lp_fallbacks", C.c_int64),
                 ("removed_agents", C.c_int64), ("collision_count", C.c_int64),
                 ("min_separation", C.c_double), ("grid_nx", C.c_int32), ("grid_ny", C.c_int32),
-                ("grid_cell", C.c_double)]
+                ("grid_cell", C.c_double), ("kernel_launches", C.c_int64)]
 
 
 _lib = None
@@ -87,6 +90,8 @@ def load():
     L.orca_sync.argtypes = [vp]
     L.orca_get_info.argtypes = [vp, P(OrcaInfo)]
     L.orca_step_host.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp]
+    L.orca_profile_stages.argtypes = [vp, ci]
+    L.orca_get_stage_ms.argtypes = [vp, P(C.c_double), P(i64)]
     L.orca_debug_last_step.argtypes = [vp, i64] + [vp] * 8
     L.orca_lp_solve_batch.argtypes = [ci, ci, i64] + [vp] * 9
     L.orca_lp_batch_create.argtypes = [P(vp), ci, ci, i64] + [vp] * 6
@@ -121,9 +126,17 @@ def ptr(a):
     return C.c_void_p(a.ctypes.data)
 
 
+_PRECISIONS = {"f32": ORCA_F32, "float32": ORCA_F32, "f64": ORCA_F64, "float64": ORCA_F64,
+               "mixed": ORCA_MIXED, ORCA_F32: ORCA_F32, ORCA_F64: ORCA_F64, ORCA_MIXED: ORCA_MIXED}
+
+
 def precision_code(precision) -> int:
-    if precision in (ORCA_F32, "f32", "float32", np.float32):
-        return ORCA_F32
-    if precision in (ORCA_F64, "f64", "float64", np.float64):
-        return ORCA_F64
-    raise ValueError(f"unknown precision {precision!r} (use 'f32' or 'f64')")
+    """'mixed' (FP32 state, FP64 arithmetic; default), 'f32' or 'f64' -> ORCA_* code."""
+    try:
+        return _PRECISIONS[precision]
+    except (KeyError, TypeError):
+        raise ValueError(f"unknown precision {precision!r} (use 'mixed', 'f32' or 'f64')") from None
+
+
+def precision_name(code: int) -> str:
+    return {ORCA_F32: "f32", ORCA_F64: "f64", ORCA_MIXED: "mixed"}[code]

@@ -65,7 +65,24 @@ struct orca_sim {
     size_t dbg_bytes = 0;
 
     int64_t binned_frame = -1; // the sorted arrays describe the state after this many frames
+    int64_t launches = 0;      // kernels launched by this handle since creation
+
+    // optional per-stage timing (orca_profile_stages)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool; // ORCA_N_STAGES + 1 events per profiled step
+    size_t ev_used = 0;
     char err[512] = {0};
+
+    void mark()
+    {
+        if (!profiling) return;
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return;
+            ev_pool.push_back(e);
+        }
+        cudaEventRecord(ev_pool[ev_used++], stream);
+    }
 };
 
 static thread_local char g_err[512] = {0};
@@ -117,14 +134,14 @@ extern "C" const char *orca_last_error(const orca_sim *sim) { return sim ? sim->
 // create / destroy
 // ---------------------------------------------------------------------------
 
-template <typename R, int MAXN> static cudaError_t set_smem_attrs()
+template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
 {
     typedef KCfg<R, MAXN> C;
-    cudaError_t e = cudaFuncSetAttribute(k_solve<R, MAXN, C::solve_threads>,
+    cudaError_t e = cudaFuncSetAttribute(k_solve<S, R, MAXN, C::solve_threads>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::solve_bpt * C::solve_threads);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_fallback<R, MAXN, C::fb_threads>,
+    return cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::fb_bpt * C::fb_threads);
 }
@@ -164,6 +181,7 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->plan);
     cudaFree(sim->stg);
     cudaFree(sim->dbg);
+    for (cudaEvent_t e : sim->ev_pool) cudaEventDestroy(e);
     if (sim->h_plan) cudaFreeHost(sim->h_plan);
     if (sim->own_stream) cudaStreamDestroy(sim->own_stream);
     delete sim;
@@ -175,7 +193,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     *out = nullptr;
     if (capacity < 0 || capacity > 0x3FFFFFFF)
         return fail(nullptr, ORCA_EINVAL, "orca_create: capacity %lld out of range", (long long)capacity);
-    if (precision != ORCA_F32 && precision != ORCA_F64)
+    if (precision != ORCA_F32 && precision != ORCA_F64 && precision != ORCA_MIXED)
         return fail(nullptr, ORCA_EINVAL, "orca_create: unknown precision %d", precision);
     int ndev = 0;
     CK(nullptr, cudaGetDeviceCount(&ndev));
@@ -189,7 +207,8 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     sim->precision = precision;
     sim->capacity = capacity;
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
-    const size_t rs = precision == ORCA_F32 ? sizeof(float) : sizeof(double);
+    const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
+    const size_t as = precision == ORCA_F32 ? sizeof(float) : sizeof(double); // arithmetic type R
     sim->max_cells = (int)(2 * cap + 1024);
 
 #define CKC(call)                                                                                 \
@@ -223,23 +242,25 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->block_sums, (size_t)sim->max_cells / SCAN_TILE + 2));
     CKC(cudaMalloc(&sim->s_xy, cap * 2 * rs));
     CKC(cudaMalloc(&sim->s_pv, cap * 4 * rs));
-    CKC(cudaMalloc(&sim->s_dm, cap * 4 * rs));
+    CKC(cudaMalloc(&sim->s_dm, cap * 4 * as));
     CKC(dalloc(&sim->s_row, cap));
     CKC(dalloc(&sim->s_cell, cap));
     CKC(dalloc(&sim->s_cls, cap));
     CKC(dalloc(&sim->nb, cap * ORCA_MAX_NEIGHBORS));
     CKC(dalloc(&sim->nb_cnt, cap));
     CKC(dalloc(&sim->fq, cap));
-    CKC(cudaMalloc(&sim->fq_state, cap * 4 * rs));
+    CKC(cudaMalloc(&sim->fq_state, cap * 4 * as));
     CKC(dalloc(&sim->plan, 1));
     CKC(cudaMallocHost(reinterpret_cast<void **>(&sim->h_plan), sizeof(GridPlan)));
     sim->stg_bytes = cap * 12 * sizeof(double);
     CKC(cudaMalloc(reinterpret_cast<void **>(&sim->stg), sim->stg_bytes));
     CKC(cudaMemset(sim->plan, 0, sizeof(GridPlan)));
-    CKC((set_smem_attrs<float, 16>()));
-    CKC((set_smem_attrs<float, 32>()));
-    CKC((set_smem_attrs<double, 16>()));
-    CKC((set_smem_attrs<double, 32>()));
+    CKC((set_smem_attrs<float, float, 16>()));
+    CKC((set_smem_attrs<float, float, 32>()));
+    CKC((set_smem_attrs<float, double, 16>()));
+    CKC((set_smem_attrs<float, double, 32>()));
+    CKC((set_smem_attrs<double, double, 16>()));
+    CKC((set_smem_attrs<double, double, 32>()));
 #undef CKC
     *out = sim;
     return ORCA_OK;
@@ -359,11 +380,10 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
         CK(sim, cudaMemcpyAsync(sim->ids[0], ids, sizeof(i64) * n, cudaMemcpyHostToDevice, sim->stream));
         CK(sim, cudaMemsetAsync(sim->status[0], 0, n, sim->stream));
         CK(sim, cudaMemsetAsync(sim->failed[0], 0xFF, n, sim->stream));
-        rc = sim->precision == ORCA_F32 ? upload_pv_impl<float>(sim, n, positions, velocities)
+        rc = sim->precision != ORCA_F64 ? upload_pv_impl<float>(sim, n, positions, velocities)
                                         : upload_pv_impl<double>(sim, n, positions, velocities);
         if (rc) return rc;
-        rc = sim->precision == ORCA_F32
-                 ? upload_attrs_impl<float>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes)
+        rc = sim->precision != ORCA_F64 ? upload_attrs_impl<float>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes)
                  : upload_attrs_impl<double>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes);
         if (rc) return rc;
     }
@@ -387,7 +407,7 @@ extern "C" int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const dou
     sim->frame = frame;
     sim->binned_frame = -1;
     if (n == 0) return ORCA_OK;
-    return sim->precision == ORCA_F32 ? upload_pv_impl<float>(sim, n, positions, velocities)
+    return sim->precision != ORCA_F64 ? upload_pv_impl<float>(sim, n, positions, velocities)
                                       : upload_pv_impl<double>(sim, n, positions, velocities);
 }
 
@@ -428,6 +448,7 @@ extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
     info->grid_nx = h.nx;
     info->grid_ny = h.ny;
     info->grid_cell = h.cell;
+    info->kernel_launches = sim->launches;
     return rc;
 }
 
@@ -480,13 +501,12 @@ extern "C" int orca_download(orca_sim *sim, int64_t *ids, double *positions, dou
     if (n == 0) return ORCA_OK;
     if (ids) CK(sim, cudaMemcpyAsync(ids, sim->ids[sim->acur], sizeof(i64) * n, cudaMemcpyDeviceToHost, sim->stream));
     if (positions || velocities) {
-        rc = sim->precision == ORCA_F32 ? download_pv_impl<float>(sim, n, positions, velocities)
+        rc = sim->precision != ORCA_F64 ? download_pv_impl<float>(sim, n, positions, velocities)
                                         : download_pv_impl<double>(sim, n, positions, velocities);
         if (rc) return rc;
     }
     if (radii || pref_speeds || max_speeds || goals || goal_tols || class_codes) {
-        rc = sim->precision == ORCA_F32
-                 ? download_attrs_impl<float>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes)
+        rc = sim->precision != ORCA_F64 ? download_attrs_impl<float>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes)
                  : download_attrs_impl<double>(sim, n, radii, pref_speeds, max_speeds, goals, goal_tols, class_codes);
         if (rc) return rc;
     }
@@ -528,58 +548,65 @@ static StepParams make_params(const orca_sim *sim)
 }
 
 // K0 + K1: bounding box, plan, histogram, scan, scatter of pv[cur]
-template <typename R> static int bin_build(orca_sim *sim, const StepParams &P)
+template <typename S, typename R> static int bin_build(orca_sim *sim, const StepParams &P)
 {
+    typedef typename Vec<S>::T4 S4;
+    typedef typename Vec<S>::T2 S2;
     typedef typename Vec<R>::T4 R4;
-    typedef typename Vec<R>::T2 R2;
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
-    const R4 *pv = reinterpret_cast<const R4 *>(sim->pv[sim->cur]);
+    const S4 *pv = reinterpret_cast<const S4 *>(sim->pv[sim->cur]);
     k_begin_bins<<<1, 1, 0, st>>>(sim->plan);
     CK(sim, cudaMemsetAsync(sim->cell_count, 0, sizeof(int) * ((size_t)P.max_cells + 1), st));
     const int bbox_blocks = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (n + 255) / 256));
-    k_bbox<R><<<bbox_blocks, 256, 0, st>>>(sim->plan, pv);
+    k_bbox<S><<<bbox_blocks, 256, 0, st>>>(sim->plan, pv);
     k_plan<<<1, 1, 0, st>>>(sim->plan, P);
-    k_count<R><<<grid_for(n, 256), 256, 0, st>>>(sim->plan, pv, sim->cell_of, sim->rank_of, sim->cell_count, P.nr);
+    k_count<S><<<grid_for(n, 256), 256, 0, st>>>(sim->plan, pv, sim->cell_of, sim->rank_of, sim->cell_count, P.nr);
     const int scan_blocks = (P.max_cells + 1 + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count, sim->block_sums);
     k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->block_sums);
     k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count,
                                                        sim->block_sums, sim->cell_start);
-    k_scatter<R><<<grid_for(n, 256), 256, 0, st>>>(
-        sim->plan, P, pv, reinterpret_cast<const R4 *>(sim->goalpref[sim->acur]),
-        reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], sim->cell_of, sim->rank_of,
-        sim->cell_start, reinterpret_cast<R2 *>(sim->s_xy), reinterpret_cast<R4 *>(sim->s_pv),
+    k_scatter<S, R><<<grid_for(n, 256), 256, 0, st>>>(
+        sim->plan, P, pv, reinterpret_cast<const S4 *>(sim->goalpref[sim->acur]),
+        reinterpret_cast<const S2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], sim->cell_of, sim->rank_of,
+        sim->cell_start, reinterpret_cast<S2 *>(sim->s_xy), reinterpret_cast<S4 *>(sim->s_pv),
         reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell, sim->s_cls);
     CKL(sim);
+    sim->launches += 8;
     sim->binned_frame = sim->frame;
     return ORCA_OK;
 }
 
-template <typename R, int MAXN> static int solve_stage(orca_sim *sim, const StepParams &P, int out_idx)
+template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim, const StepParams &P, int out_idx)
 {
+    typedef typename Vec<S>::T4 S4;
+    typedef typename Vec<S>::T2 S2;
     typedef typename Vec<R>::T4 R4;
-    typedef typename Vec<R>::T2 R2;
     typedef KCfg<R, MAXN> C;
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
-    k_gather<R, MAXN><<<grid_for(n, 128), 128, 0, st>>>(
-        sim->plan, P, reinterpret_cast<const R2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+    k_gather<S, MAXN><<<grid_for(n, 128), 128, 0, st>>>(
+        sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
         sim->ids[a], sim->nb, sim->nb_cnt);
-    k_solve<R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
-                                         C::solve_bpt * C::solve_threads, st>>>(
-        sim->plan, P, reinterpret_cast<const R4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+    sim->mark();
+    k_solve<S, R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
+                                            C::solve_bpt * C::solve_threads, st>>>(
+        sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
         sim->s_cls, sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
-        reinterpret_cast<const R4 *>(sim->goalpref[a]), reinterpret_cast<R4 *>(sim->pv[out_idx]),
+        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state));
+    sim->mark();
     const int fb_blocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, (n + C::fb_threads - 1) / C::fb_threads));
-    k_fallback<R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * C::fb_threads, st>>>(
-        sim->plan, P, reinterpret_cast<const R4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+    k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * C::fb_threads, st>>>(
+        sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
         sim->s_cls, sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
-        reinterpret_cast<const R4 *>(sim->goalpref[a]), reinterpret_cast<R4 *>(sim->pv[out_idx]),
+        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
         sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state));
+    sim->mark();
     CKL(sim);
+    sim->launches += 3;
     return ORCA_OK;
 }
 
@@ -614,6 +641,7 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
         sim->status[a], sim->status[b], sim->failed[a], sim->failed[b]);
     k_after_compact<<<1, 1, 0, st>>>(sim->plan, sim->dst_idx);
     CKL(sim);
+    sim->launches += 6;
     sim->acur = b;
     return ORCA_OK;
 }
@@ -626,52 +654,61 @@ template <typename R> static int metrics_stage(orca_sim *sim, const StepParams &
         sim->plan, P, reinterpret_cast<const R2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
         sim->ids[sim->acur], reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), 1e-6 /* engine.py:36 */);
     CKL(sim);
+    sim->launches += 1;
     return ORCA_OK;
 }
 
-template <typename R> static int step_impl(orca_sim *sim)
+template <typename S, typename R> static int step_impl(orca_sim *sim)
 {
     StepParams P = make_params(sim);
     int rc;
     const int64_t n = sim->n_bound;
     sim->n_pre = n;
+    sim->mark(); // stage boundaries: bins | gather | solve | fallback | finish+compact | metrics
     k_begin_step<<<1, 1, 0, sim->stream>>>(sim->plan);
+    sim->launches += 1;
     if (n == 0) { // engine.py:202-209
         k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->frame + 1, sim->params.remove_arrivals);
         CKL(sim);
+        sim->launches += 1;
+        for (int i = 0; i < ORCA_N_STAGES; ++i) sim->mark();
         sim->frame += 1;
         return ORCA_OK;
     }
     if (sim->binned_frame != sim->frame) {
-        rc = bin_build<R>(sim, P);
+        rc = bin_build<S, R>(sim, P);
         if (rc) return rc;
     }
+    sim->mark();
     const int out_idx = (sim->cur + 1) % 3;
-    rc = P.max_n <= 16 ? solve_stage<R, 16>(sim, P, out_idx) : solve_stage<R, 32>(sim, P, out_idx);
+    rc = P.max_n <= 16 ? solve_stage<S, R, 16>(sim, P, out_idx) : solve_stage<S, R, 32>(sim, P, out_idx);
     if (rc) return rc;
     k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur], sim->frame + 1);
     k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->frame + 1, sim->params.remove_arrivals);
     CKL(sim);
+    sim->launches += 2;
     sim->pre = sim->cur;
     if (sim->params.remove_arrivals) {
         const int dst = (sim->cur + 2) % 3;
-        rc = compact_stage<R>(sim, out_idx, dst);
+        rc = compact_stage<S>(sim, out_idx, dst);
         if (rc) return rc;
         sim->cur = dst;
     } else {
         sim->cur = out_idx;
     }
+    sim->mark();
     sim->frame += 1;
     sim->binned_frame = -1;
     if (sim->params.compute_metrics) {
         // engine.py:270-286: metrics of the post-step, post-removal positions. The bin
         // build it needs is the one the next step would do anyway, so it is kept.
         StepParams P2 = make_params(sim);
-        rc = bin_build<R>(sim, P2);
+        rc = bin_build<S, R>(sim, P2);
         if (rc) return rc;
-        rc = metrics_stage<R>(sim, P2);
+        rc = metrics_stage<S>(sim, P2);
         if (rc) return rc;
     }
+    sim->mark();
     return ORCA_OK;
 }
 
@@ -681,7 +718,40 @@ extern "C" int orca_step(orca_sim *sim)
     if (!sim->loaded) return fail(sim, ORCA_EINVAL, "orca_step: no state uploaded");
     if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_step: orca_set_params was not called");
     CK(sim, cudaSetDevice(sim->device));
-    return sim->precision == ORCA_F32 ? step_impl<float>(sim) : step_impl<double>(sim);
+    switch (sim->precision) {
+    case ORCA_F32: return step_impl<float, float>(sim);
+    case ORCA_MIXED: return step_impl<float, double>(sim);
+    default: return step_impl<double, double>(sim);
+    }
+}
+
+extern "C" int orca_profile_stages(orca_sim *sim, int enable)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_profile_stages: sim is NULL");
+    CK(sim, cudaSetDevice(sim->device));
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    sim->profiling = enable != 0;
+    sim->ev_used = 0;
+    return ORCA_OK;
+}
+
+extern "C" int orca_get_stage_ms(orca_sim *sim, double *ms, int64_t *steps)
+{
+    if (!sim || !ms) return fail(sim, ORCA_EINVAL, "orca_get_stage_ms: NULL argument");
+    CK(sim, cudaSetDevice(sim->device));
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    for (int i = 0; i < ORCA_N_STAGES; ++i) ms[i] = 0.0;
+    const size_t per = ORCA_N_STAGES + 1;
+    const size_t nsteps = sim->ev_used / per;
+    for (size_t k = 0; k < nsteps; ++k)
+        for (int i = 0; i < ORCA_N_STAGES; ++i) {
+            float t = 0.f;
+            CK(sim, cudaEventElapsedTime(&t, sim->ev_pool[k * per + i], sim->ev_pool[k * per + i + 1]));
+            ms[i] += (double)t;
+        }
+    if (steps) *steps = (int64_t)nsteps;
+    sim->ev_used = 0;
+    return ORCA_OK;
 }
 
 extern "C" int orca_run(orca_sim *sim, int64_t steps)
@@ -705,7 +775,7 @@ extern "C" int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const dou
     rc = orca_step(sim);
     if (rc) return rc;
     if (n > 0) {
-        rc = sim->precision == ORCA_F32 ? download_pv_impl<float>(sim, n, new_positions, new_velocities)
+        rc = sim->precision != ORCA_F64 ? download_pv_impl<float>(sim, n, new_positions, new_velocities)
                                         : download_pv_impl<double>(sim, n, new_positions, new_velocities);
         if (rc) return rc;
         if (out_status) {
@@ -722,11 +792,12 @@ extern "C" int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const dou
 // parity taps
 // ---------------------------------------------------------------------------
 
-template <typename R>
+template <typename S, typename R>
 static int debug_impl(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_iy, int64_t *nb_rows,
                       int64_t *nb_count, double *out_v, int64_t *status, int64_t *failed_at,
                       double *desired_v)
 {
+    typedef typename Vec<S>::T4 S4;
     typedef typename Vec<R>::T4 R4;
     StepParams P = make_params(sim);
     const int max_n = std::max(P.max_n, 1);
@@ -748,12 +819,12 @@ static int debug_impl(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_
     double *d_vel = d_pos + 2 * n;
     i64 *d_st = reinterpret_cast<i64 *>(d_vel + 2 * n);
     i64 *d_fa = d_st + n;
-    k_debug_rows<R><<<grid_for(n, 256), 256, 0, st>>>(
-        (int)n, P, reinterpret_cast<const R4 *>(sim->pv[sim->pre]), sim->s_row, sim->nb, sim->nb_cnt,
+    k_debug_rows<S, R><<<grid_for(n, 256), 256, 0, st>>>(
+        (int)n, P, reinterpret_cast<const S4 *>(sim->pv[sim->pre]), sim->s_row, sim->nb, sim->nb_cnt,
         reinterpret_cast<const R4 *>(sim->s_dm), d_ix, d_iy, d_rows, d_cnt, d_des);
     // the un-compacted post-step buffer is pv[(pre+1)%3]
-    k_export_pv<R><<<grid_for(n, 256), 256, 0, st>>>(
-        (int)n, reinterpret_cast<const R4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel);
+    k_export_pv<S><<<grid_for(n, 256), 256, 0, st>>>(
+        (int)n, reinterpret_cast<const S4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel);
     k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->status[sim->acur], d_st);
     k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->failed[sim->acur], d_fa);
     CKL(sim);
@@ -783,9 +854,14 @@ extern "C" int orca_debug_last_step(orca_sim *sim, int64_t n, int64_t *cell_ix, 
                     (long long)sim->n_pre);
     CK(sim, cudaSetDevice(sim->device));
     if (n == 0) return ORCA_OK;
-    return sim->precision == ORCA_F32
-               ? debug_impl<float>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v)
-               : debug_impl<double>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
+    switch (sim->precision) {
+    case ORCA_F32:
+        return debug_impl<float, float>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
+    case ORCA_MIXED:
+        return debug_impl<float, double>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
+    default:
+        return debug_impl<double, double>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -861,7 +937,7 @@ extern "C" int orca_lp_batch_create(orca_lp_batch **out, int device, int precisi
     if (n < 0 || !coff || (n > 0 && (!tgt || !caps || !seeds)))
         return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: bad arguments");
     if (precision != ORCA_F32 && precision != ORCA_F64)
-        return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: unknown precision %d", precision);
+        return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: precision must be ORCA_F32 or ORCA_F64, got %d", precision);
     if (coff[0] != 0) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_create: coff[0] must be 0");
     for (int64_t i = 0; i < n; ++i)
         if (coff[i + 1] < coff[i])

@@ -236,34 +236,34 @@ k_scan_apply(const int *__restrict__ len_ptr, int len_extra, const int *__restri
 //   s_pv  (x, y, vx, vy)                 pre-step snapshot
 //   s_dm  (des_vx, des_vy, max_speed, avoid_radius)
 //   s_row storage row, s_cell search cell, s_cls class code
-template <typename R>
+template <typename S, typename R>
 __global__ void __launch_bounds__(256)
 k_scatter(const GridPlan *__restrict__ plan, StepParams P,
-          const typename Vec<R>::T4 *__restrict__ pv, const typename Vec<R>::T4 *__restrict__ goalpref,
-          const typename Vec<R>::T2 *__restrict__ radmax, const u8 *__restrict__ cls,
+          const typename Vec<S>::T4 *__restrict__ pv, const typename Vec<S>::T4 *__restrict__ goalpref,
+          const typename Vec<S>::T2 *__restrict__ radmax, const u8 *__restrict__ cls,
           const int *__restrict__ cell_of, const int *__restrict__ rank_of,
-          const int *__restrict__ cell_start, typename Vec<R>::T2 *__restrict__ s_xy,
-          typename Vec<R>::T4 *__restrict__ s_pv, typename Vec<R>::T4 *__restrict__ s_dm,
+          const int *__restrict__ cell_start, typename Vec<S>::T2 *__restrict__ s_xy,
+          typename Vec<S>::T4 *__restrict__ s_pv, typename Vec<R>::T4 *__restrict__ s_dm,
           int *__restrict__ s_row, int *__restrict__ s_cell, u8 *__restrict__ s_cls)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= plan->n) return;
     const int c = cell_of[i];
     const int s = cell_start[c] + rank_of[i];
-    const typename Vec<R>::T4 a = pv[i];
-    const typename Vec<R>::T4 g = goalpref[i]; // gx, gy, pref_speed, goal_tol
-    const typename Vec<R>::T2 rm = radmax[i];  // radius, max_speed
+    const typename Vec<S>::T4 a = pv[i];
+    const typename Vec<S>::T4 g = goalpref[i]; // gx, gy, pref_speed, goal_tol
+    const typename Vec<S>::T2 rm = radmax[i];  // radius, max_speed
     // engine.py:133-139
-    const R dx = g.x - a.x, dy = g.y - a.y;
+    const R dx = (R)g.x - (R)a.x, dy = (R)g.y - (R)a.y;
     const R dist = sqrt_rn<R>(dx * dx + dy * dy);
     R speed = div_rn<R>(dist, (R)P.dt);
-    if (g.z < speed) speed = g.z;
+    if ((R)g.z < speed) speed = (R)g.z;
     const R scale = dist > R(0) ? div_rn<R>(speed, dist) : R(0);
-    // engine.py:227
-    const R avoid = Fmt<R>::is_f32 ? (R)((double)rm.x + P.half_margin) : (R)(rm.x + (R)P.half_margin);
+    // engine.py:227 (evaluated in FP64, then rounded to R)
+    const R avoid = (R)((double)rm.x + P.half_margin);
     s_xy[s] = mk2(a.x, a.y);
     s_pv[s] = a;
-    s_dm[s] = mk4(dx * scale, dy * scale, rm.y, avoid);
+    s_dm[s] = mk4(dx * scale, dy * scale, (R)rm.y, avoid);
     s_row[s] = i;
     s_cell[s] = c;
     s_cls[s] = cls[i];
@@ -461,59 +461,60 @@ __device__ __forceinline__ void shuffle_smem(u8 *perm, int stride, int k, u64 se
 
 // Build the ORCA half-planes of agent s into `cons` in SHUFFLED order
 // (_kernels.py:525-541). Returns false on exactly coincident centres.
-template <typename R>
+template <typename S, typename R>
 __device__ __forceinline__ bool build_constraints(
-    int s, int cnt, const StepParams &P, const typename Vec<R>::T4 *__restrict__ s_pv,
+    int s, int cnt, const StepParams &P, const typename Vec<S>::T4 *__restrict__ s_pv,
     const typename Vec<R>::T4 *__restrict__ s_dm, const u8 *__restrict__ s_cls,
     const int *__restrict__ nb, const u8 *perm, int stride, SmemCons<R> &cons, int &bad_j)
 {
-    const typename Vec<R>::T4 me = s_pv[s];
+    const typename Vec<S>::T4 me_s = s_pv[s];
+    const R mex = (R)me_s.x, mey = (R)me_s.y, mevx = (R)me_s.z, mevy = (R)me_s.w;
     const R ri = s_dm[s].w;
     const int ci = s_cls[s];
     const R tau = (R)P.tau, dt = (R)P.dt;
     for (int pos = 0; pos < cnt; ++pos) {
         const int t = perm[pos * stride];
         const int j = nb[(size_t)t * P.stride + s];
-        const typename Vec<R>::T4 q = s_pv[j];
+        const typename Vec<S>::T4 q = s_pv[j];
         const R rj = s_dm[j].w;
         const int cj = s_cls[j];
         R ux, uy, nx, ny;
-        if (!vo_exit<R>(q.x - me.x, q.y - me.y, me.z - q.z, me.w - q.w, ri + rj, tau, dt, ux, uy,
-                        nx, ny)) {
+        if (!vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, tau, dt,
+                        ux, uy, nx, ny)) {
             // coincident neighbours have d2 == 0 and therefore lead the list; the
             // reference reports the first one in rank order (_kernels.py:533-536)
             bad_j = nb[s];
             return false;
         }
         const R f = (R)P.fmat[ci * 2 + cj];
-        cons.set(pos, me.z + f * ux, me.w + f * uy, nx, ny);
+        cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
     }
     return true;
 }
 
 // Integration + arrival test (engine.py:249-253) for storage row `row`.
-template <typename R>
-__device__ __forceinline__ void integrate_row(int row, const typename Vec<R>::T4 &me, R vx, R vy,
+template <typename S, typename R>
+__device__ __forceinline__ void integrate_row(int row, const typename Vec<S>::T4 &me, R vx, R vy,
                                               const StepParams &P,
-                                              const typename Vec<R>::T4 *__restrict__ goalpref,
-                                              typename Vec<R>::T4 *__restrict__ pv_out,
+                                              const typename Vec<S>::T4 *__restrict__ goalpref,
+                                              typename Vec<S>::T4 *__restrict__ pv_out,
                                               u8 *__restrict__ arrived)
 {
     const R dt = (R)P.dt;
-    const R nxp = me.x + vx * dt, nyp = me.y + vy * dt;
-    pv_out[row] = mk4(nxp, nyp, vx, vy);
-    const typename Vec<R>::T4 g = goalpref[row];
-    const R gx = g.x - nxp, gy = g.y - nyp;
-    arrived[row] = sqrt_rn<R>(gx * gx + gy * gy) <= g.w ? 1 : 0;
+    const R nxp = (R)me.x + vx * dt, nyp = (R)me.y + vy * dt;
+    pv_out[row] = mk4((S)nxp, (S)nyp, (S)vx, (S)vy);
+    const typename Vec<S>::T4 g = goalpref[row];
+    const R gx = (R)g.x - nxp, gy = (R)g.y - nyp;
+    arrived[row] = sqrt_rn<R>(gx * gx + gy * gy) <= (R)g.w ? 1 : 0;
 }
 
-template <typename R, int MAXN, int THREADS>
+template <typename S, typename R, int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
-k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T4 *__restrict__ s_pv,
+k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__restrict__ s_pv,
         const typename Vec<R>::T4 *__restrict__ s_dm, const u8 *__restrict__ s_cls,
         const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
-        const u8 *__restrict__ nb_cnt, const typename Vec<R>::T4 *__restrict__ goalpref,
-        typename Vec<R>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
+        const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
+        typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
         i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
         typename Vec<R>::T4 *__restrict__ fq_state)
 {
@@ -527,7 +528,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T4 *__
     if (row >= plan->n_owned) return; // halo ghost: searched, never solved
 
     const int cnt = nb_cnt[s];
-    const typename Vec<R>::T4 me = s_pv[s];
+    const typename Vec<S>::T4 me = s_pv[s];
     const typename Vec<R>::T4 dm = s_dm[s];
     u8 *perm = sm_perm + threadIdx.x;
     SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
@@ -535,13 +536,13 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T4 *__
     shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
 
     int bad_j = -1;
-    if (!build_constraints<R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j)) {
+    if (!build_constraints<S, R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j)) {
         // _kernels.py:542-547 + engine.py:239-245
         if (plan->err_frame < 0) // sticky: only the first failing frame is reported
             atomicMin(&plan->err_pair, ((u64)(unsigned)row << 32) | (u64)(unsigned)s_row[bad_j]);
         status[row] = 0;
         failed_at[row] = -1;
-        integrate_row<R>(row, me, me.z, me.w, P, goalpref, pv_out, arrived);
+        integrate_row<S, R>(row, me, (R)me.z, (R)me.w, P, goalpref, pv_out, arrived);
         return;
     }
 
@@ -550,7 +551,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T4 *__
     if (lp2_target<R, false, SmemCons<R>>(cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy)) {
         status[row] = 0;
         failed_at[row] = -1;
-        integrate_row<R>(row, me, vx, vy, P, goalpref, pv_out, arrived);
+        integrate_row<S, R>(row, me, vx, vy, P, goalpref, pv_out, arrived);
         return;
     }
     // queue for the least-penetration stage (warp-aggregated by the compiler)
@@ -561,13 +562,13 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T4 *__
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
 }
 
-template <typename R, int MAXN, int THREADS>
+template <typename S, typename R, int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 k_fallback(const GridPlan *__restrict__ plan, StepParams P,
-           const typename Vec<R>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
+           const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
            const u8 *__restrict__ s_cls, const int *__restrict__ s_row,
            const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
-           const typename Vec<R>::T4 *__restrict__ goalpref, typename Vec<R>::T4 *__restrict__ pv_out,
+           const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
            u8 *__restrict__ arrived, const int *__restrict__ fq,
            const typename Vec<R>::T4 *__restrict__ fq_state)
 {
@@ -584,7 +585,7 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P,
         const R4 st = fq_state[q];
         const int row = s_row[s];
         const int cnt = nb_cnt[s];
-        const R4 me = s_pv[s];
+        const typename Vec<S>::T4 me = s_pv[s];
         const R4 dm = s_dm[s];
         u8 *perm = sm_perm + threadIdx.x;
         u8 *inv = sm_inv + threadIdx.x;
@@ -594,13 +595,13 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P,
         shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
         for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * THREADS] * THREADS] = (u8)pos;
         int bad_j;
-        build_constraints<R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j);
+        build_constraints<S, R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j);
 
         SmemConsIdent<R> ident{sm_cons + threadIdx.x, inv, THREADS};
         R rx, ry;
         least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry);
-        integrate_row<R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
+        integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
     }
 }
 
@@ -784,9 +785,9 @@ k_export_i8(int n, const i8 *__restrict__ in, i64 *__restrict__ out)
 }
 
 // parity taps, storage-row order (see orca_debug_last_step)
-template <typename R>
+template <typename S, typename R>
 __global__ void __launch_bounds__(256)
-k_debug_rows(int n, StepParams P, const typename Vec<R>::T4 *__restrict__ pv_pre,
+k_debug_rows(int n, StepParams P, const typename Vec<S>::T4 *__restrict__ pv_pre,
              const int *__restrict__ s_row, const int *__restrict__ nb,
              const u8 *__restrict__ nb_cnt, const typename Vec<R>::T4 *__restrict__ s_dm,
              i64 *__restrict__ cell_ix, i64 *__restrict__ cell_iy, i64 *__restrict__ nb_rows,
@@ -795,7 +796,7 @@ k_debug_rows(int n, StepParams P, const typename Vec<R>::T4 *__restrict__ pv_pre
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     const int row = s_row[s];
-    const typename Vec<R>::T4 a = pv_pre[row];
+    const typename Vec<S>::T4 a = pv_pre[row];
     cell_ix[row] = (i64)floor(__ddiv_rn((double)a.x, P.nr));
     cell_iy[row] = (i64)floor(__ddiv_rn((double)a.y, P.nr));
     const int cnt = nb_cnt[s];

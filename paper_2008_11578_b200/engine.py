@@ -41,9 +41,12 @@ COLLISION_TOLERANCE = 1e-6          # engine.py:36 (applied inside k_min_sep)
 DEFAULT_WORK_UNIT_STEPS = 4096      # engine.py:37
 MASK64 = (1 << 64) - 1
 
-# "f32": FP32 device state and LP arithmetic, FP64 binning / neighbour keys
-# (the product path). "f64": everything FP64, bit-identical to the reference.
-DEFAULT_PRECISION = os.environ.get("ORCA_B200_PRECISION", "f32")
+# "mixed" (default): FP32 device state, FP64 arithmetic -- the reference's branches and
+#   results for float32-representable inputs, rounded once to FP32 on store.
+# "f32": FP32 state and arithmetic (fastest; ill-conditioned LPs may differ > 1e-4 m/s).
+# "f64": FP64 state and arithmetic, bit-identical to the reference on any input.
+# Binning and neighbour-ordering keys are FP64 in every mode.
+DEFAULT_PRECISION = os.environ.get("ORCA_B200_PRECISION", "mixed")
 
 
 def _mix64(z: int) -> int:
@@ -189,6 +192,17 @@ class Simulation:
             # engine.py:239-245 / engine.py:152-153 raise plain ValueError with this text
             raise ValueError(self._L.orca_last_error(self._h).decode())
         check(rc, self._h)
+
+    def profile_stages(self, enable: bool = True):
+        """Record CUDA events at the stage boundaries of every following step."""
+        check(self._L.orca_profile_stages(self._h, 1 if enable else 0), self._h)
+
+    def stage_ms(self):
+        """-> ({stage name: accumulated ms}, steps covered) since the last call."""
+        ms = (C.c_double * _lib.ORCA_N_STAGES)()
+        steps = C.c_int64()
+        check(self._L.orca_get_stage_ms(self._h, ms, C.byref(steps)), self._h)
+        return {name: float(ms[i]) for i, name in enumerate(_lib.STAGE_NAMES)}, int(steps.value)
 
     def state(self, state_type=None) -> SimState:
         info = self.info()

@@ -19,7 +19,7 @@ from enum import IntEnum
 
 import numpy as np
 
-from ._lib import check, load, precision_code, ptr
+from ._lib import ORCA_F64, ORCA_MIXED, check, load, precision_code, ptr
 
 __all__ = ["HalfPlaneConstraint", "LpProblem", "LpResult", "LpStatus", "LpBatch",
            "shuffle_order", "solve_range", "solve_batch", "solve_closest_point"]
@@ -73,6 +73,13 @@ def shuffle_order(count: int, seed: int) -> list[int]:
     return perm
 
 
+def _lp_precision(precision) -> int:
+    """The LP entry points take arbitrary float64 problems: 'f64' (default, bit-identical
+    to the reference) or 'f32'. 'mixed' has no separate meaning here and maps to 'f64'."""
+    code = precision_code(precision)
+    return ORCA_F64 if code == ORCA_MIXED else code
+
+
 def _prep(coff, cpts, cnrm, tgt, caps, seeds):
     coff = np.ascontiguousarray(coff, dtype=np.int64)
     n = coff.shape[0] - 1
@@ -88,14 +95,14 @@ def _prep(coff, cpts, cnrm, tgt, caps, seeds):
     return n, coff, cpts, cnrm, tgt, caps, seeds
 
 
-def solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision="f32", device: int = 0):
+def solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision="f64", device: int = 0):
     """_kernels.solve_range over the whole batch on the GPU.
     Returns (out_v f64[n,2], status i64[n], failed_at i64[n])."""
     n, coff, cpts, cnrm, tgt, caps, seeds = _prep(coff, cpts, cnrm, tgt, caps, seeds)
     out_v = np.empty((n, 2))
     status = np.empty(n, dtype=np.int64)
     failed = np.empty(n, dtype=np.int64)
-    check(load().orca_lp_solve_batch(device, precision_code(precision), n, ptr(coff), ptr(cpts),
+    check(load().orca_lp_solve_batch(device, _lp_precision(precision), n, ptr(coff), ptr(cpts),
                                      ptr(cnrm), ptr(tgt), ptr(caps), ptr(seeds), ptr(out_v),
                                      ptr(status), ptr(failed)))
     return out_v, status, failed
@@ -104,13 +111,13 @@ def solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision="f32", device: int
 class LpBatch:
     """A batch resident on the device: build once, solve repeatedly."""
 
-    def __init__(self, coff, cpts, cnrm, tgt, caps, seeds, precision="f32", device: int = 0,
+    def __init__(self, coff, cpts, cnrm, tgt, caps, seeds, precision="f64", device: int = 0,
                  stream=None):
         self._L = load()
         self.n, coff, cpts, cnrm, tgt, caps, seeds = _prep(coff, cpts, cnrm, tgt, caps, seeds)
         self.m = int(coff[-1])
         self._h = C.c_void_p()
-        check(self._L.orca_lp_batch_create(C.byref(self._h), device, precision_code(precision),
+        check(self._L.orca_lp_batch_create(C.byref(self._h), device, _lp_precision(precision),
                                            self.n, ptr(coff), ptr(cpts), ptr(cnrm), ptr(tgt),
                                            ptr(caps), ptr(seeds)))
         if stream is not None:
@@ -171,7 +178,7 @@ def _validate_problem(problem, label=""):
 
 
 def solve_batch(problems, worker_count: int = 1, work_unit_steps: int = 64, *,
-                precision="f32", device: int = 0):
+                precision="f64", device: int = 0):
     """lp.solve_batch (lp.py:263-291): validate, pack to CSR, solve on the GPU."""
     del worker_count, work_unit_steps
     n = len(problems)
@@ -194,6 +201,6 @@ def solve_batch(problems, worker_count: int = 1, work_unit_steps: int = 64, *,
                      None if status[i] == 0 else int(failed[i])) for i in range(n)]
 
 
-def solve_closest_point(problem, *, precision="f32", device: int = 0) -> LpResult:
+def solve_closest_point(problem, *, precision="f64", device: int = 0) -> LpResult:
     """lp.solve_closest_point (lp.py:152-165) for one problem."""
     return solve_batch([problem], precision=precision, device=device)[0]
