@@ -40,6 +40,7 @@ struct orca_sim {
     u8 *cls[2] = {nullptr, nullptr};
     i8 *status[2] = {nullptr, nullptr};
     i8 *failed[2] = {nullptr, nullptr};
+    float *hint[2] = {nullptr, nullptr};       // radius that held last step's neighbour list
     int acur = 0;
     u8 *arrived = nullptr;
     int *keep = nullptr, *dst_idx = nullptr;
@@ -50,11 +51,12 @@ struct orca_sim {
         *block_sums = nullptr;
     void *s_xy = nullptr, *s_pv = nullptr, *s_dm = nullptr;
     int *s_row = nullptr, *s_cell = nullptr;
-    u8 *s_cls = nullptr;
+    void *s_rc = nullptr; // (radius, class) in the storage type
     int *nb = nullptr;
     u8 *nb_cnt = nullptr;
     int *fq = nullptr;
     void *fq_state = nullptr;
+    int *gq = nullptr; // agents queued for the exact ring search
     GridPlan *plan = nullptr;
     GridPlan *h_plan = nullptr; // pinned mirror
 
@@ -66,6 +68,10 @@ struct orca_sim {
 
     int64_t binned_frame = -1; // the sorted arrays describe the state after this many frames
     int64_t launches = 0;      // kernels launched by this handle since creation
+    double occ_target = 4.0;   // mean agents per search cell the plan aims for (ORCA_OCC_TARGET)
+    int r0_override = 0;       // ORCA_R0: force the first ring radius (experiments)
+    int fb_lanes = 8;          // ORCA_FB_LANES: lanes per warp that take a fallback agent
+    bool gather_fast = true;   // ORCA_GATHER_FAST=0: exact ring search for every agent
 
     // optional per-stage timing (orca_profile_stages)
     bool profiling = false;
@@ -122,8 +128,8 @@ template <typename R, int MAXN> struct KCfg {
     typedef typename Vec<R>::T4 R4;
     static constexpr int solve_bpt = (int)sizeof(R4) * MAXN + MAXN;
     static constexpr int solve_threads = pick_threads(solve_bpt);
-    static constexpr int fb_bpt = 2 * (int)sizeof(R4) * MAXN + 2 * MAXN;
-    static constexpr int fb_threads = pick_threads(fb_bpt);
+    static constexpr int fb_bpt = 2 * (int)sizeof(R4) * MAXN + 2 * MAXN; // per ACTIVE thread
+    static constexpr int fb_threads = 128;
 };
 
 extern "C" int orca_abi_version(void) { return ORCA_ABI_VERSION; }
@@ -143,7 +149,7 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                C::fb_bpt * C::fb_threads);
+                                C::fb_bpt * (C::fb_threads / 32) * 16);
 }
 
 extern "C" void orca_destroy(orca_sim *sim)
@@ -159,6 +165,7 @@ extern "C" void orca_destroy(orca_sim *sim)
         cudaFree(sim->cls[i]);
         cudaFree(sim->status[i]);
         cudaFree(sim->failed[i]);
+        cudaFree(sim->hint[i]);
     }
     cudaFree(sim->arrived);
     cudaFree(sim->keep);
@@ -173,11 +180,12 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->s_dm);
     cudaFree(sim->s_row);
     cudaFree(sim->s_cell);
-    cudaFree(sim->s_cls);
+    cudaFree(sim->s_rc);
     cudaFree(sim->nb);
     cudaFree(sim->nb_cnt);
     cudaFree(sim->fq);
     cudaFree(sim->fq_state);
+    cudaFree(sim->gq);
     cudaFree(sim->plan);
     cudaFree(sim->stg);
     cudaFree(sim->dbg);
@@ -206,6 +214,13 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     sim->device = device;
     sim->precision = precision;
     sim->capacity = capacity;
+    if (const char *occ = getenv("ORCA_OCC_TARGET")) {
+        const double v = atof(occ);
+        if (v > 0.0) sim->occ_target = v;
+    }
+    if (const char *r0 = getenv("ORCA_R0")) sim->r0_override = atoi(r0);
+    if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
+    if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
     const size_t as = precision == ORCA_F32 ? sizeof(float) : sizeof(double); // arithmetic type R
@@ -231,6 +246,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
         CKC(dalloc(&sim->cls[i], cap));
         CKC(dalloc(&sim->status[i], cap));
         CKC(dalloc(&sim->failed[i], cap));
+        CKC(dalloc(&sim->hint[i], cap));
     }
     CKC(dalloc(&sim->arrived, cap));
     CKC(dalloc(&sim->keep, cap + 1));
@@ -245,11 +261,12 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(cudaMalloc(&sim->s_dm, cap * 4 * as));
     CKC(dalloc(&sim->s_row, cap));
     CKC(dalloc(&sim->s_cell, cap));
-    CKC(dalloc(&sim->s_cls, cap));
+    CKC(cudaMalloc(&sim->s_rc, cap * 2 * rs));
     CKC(dalloc(&sim->nb, cap * ORCA_MAX_NEIGHBORS));
     CKC(dalloc(&sim->nb_cnt, cap));
     CKC(dalloc(&sim->fq, cap));
     CKC(cudaMalloc(&sim->fq_state, cap * 4 * as));
+    CKC(dalloc(&sim->gq, cap));
     CKC(dalloc(&sim->plan, 1));
     CKC(cudaMallocHost(reinterpret_cast<void **>(&sim->h_plan), sizeof(GridPlan)));
     sim->stg_bytes = cap * 12 * sizeof(double);
@@ -334,7 +351,7 @@ static int upload_attrs_impl(orca_sim *sim, int64_t n, const double *radii, cons
     k_import_attrs<R><<<grid_for(n, 256), 256, 0, st>>>(
         (int)n, d_rad, d_pref, d_max, d_goal, d_gtol, d_cls,
         reinterpret_cast<R4 *>(sim->goalpref[sim->acur]), reinterpret_cast<R2 *>(sim->radmax[sim->acur]),
-        sim->cls[sim->acur]);
+        sim->cls[sim->acur], sim->hint[sim->acur], sim->plan);
     CKL(sim);
     return ORCA_OK;
 }
@@ -350,6 +367,7 @@ static int reset_plan(orca_sim *sim, int64_t n, int64_t frame)
     h.err_frame = -1;
     h.frame = frame;
     h.min_sep_enc = enc_double(INFINITY);
+    h.vmax_enc = enc_double(0.0);
     *sim->h_plan = h;
     CK(sim, cudaMemcpyAsync(sim->plan, sim->h_plan, sizeof(GridPlan), cudaMemcpyHostToDevice, sim->stream));
     // the pinned mirror is reused by later reads; make sure this copy has left it
@@ -538,12 +556,8 @@ static StepParams make_params(const orca_sim *sim)
     P.stride = (int)(sim->capacity > 0 ? sim->capacity : 1);
     P.frame = sim->frame;
     P.max_cells = (int)std::min<int64_t>(sim->max_cells, 2 * sim->n_bound + 1024);
-    P.occ_target = 4.0;
-    const char *occ = getenv("ORCA_OCC_TARGET");
-    if (occ) {
-        const double v = atof(occ);
-        if (v > 0.0) P.occ_target = v;
-    }
+    P.occ_target = sim->occ_target;
+    P.r0_override = sim->r0_override;
     return P;
 }
 
@@ -571,7 +585,7 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
         sim->plan, P, pv, reinterpret_cast<const S4 *>(sim->goalpref[sim->acur]),
         reinterpret_cast<const S2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], sim->cell_of, sim->rank_of,
         sim->cell_start, reinterpret_cast<S2 *>(sim->s_xy), reinterpret_cast<S4 *>(sim->s_pv),
-        reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell, sim->s_cls);
+        reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell, reinterpret_cast<S2 *>(sim->s_rc));
     CKL(sim);
     sim->launches += 8;
     sim->binned_frame = sim->frame;
@@ -587,26 +601,36 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
-    k_gather<S, MAXN><<<grid_for(n, 128), 128, 0, st>>>(
+    if (sim->gather_fast)
+        k_gather_fast<S, MAXN, 48><<<grid_for(n, 128), 128, 0, st>>>(
+            sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+            sim->ids[a], reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt,
+            sim->gq);
+    else
+        k_enqueue_all<<<grid_for(n, 256), 256, 0, st>>>(sim->plan, P.max_n, sim->s_row, sim->nb_cnt, sim->gq);
+    const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 127) / 128));
+    k_gather<S, MAXN><<<gq_blocks, 128, 0, st>>>(
         sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-        sim->ids[a], sim->nb, sim->nb_cnt);
+        sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq);
     sim->mark();
     k_solve<S, R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
                                             C::solve_bpt * C::solve_threads, st>>>(
         sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
-        sim->s_cls, sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
+        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state));
     sim->mark();
-    const int fb_blocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, (n + C::fb_threads - 1) / C::fb_threads));
-    k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * C::fb_threads, st>>>(
-        sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
-        sim->s_cls, sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
+    const int lanes = sim->fb_lanes;                          // active lanes per warp (<= 16)
+    const int fb_at = (C::fb_threads / 32) * lanes;           // agents per block per pass
+    const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + fb_at - 1) / fb_at));
+    k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * fb_at, st>>>(
+        sim->plan, P, lanes, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
         sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state));
     sim->mark();
     CKL(sim);
-    sim->launches += 3;
+    sim->launches += 4;
     return ORCA_OK;
 }
 
@@ -638,7 +662,7 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
         reinterpret_cast<R4 *>(sim->pv[dst_pv_idx]), reinterpret_cast<const R4 *>(sim->goalpref[a]),
         reinterpret_cast<R4 *>(sim->goalpref[b]), reinterpret_cast<const R2 *>(sim->radmax[a]),
         reinterpret_cast<R2 *>(sim->radmax[b]), sim->ids[a], sim->ids[b], sim->cls[a], sim->cls[b],
-        sim->status[a], sim->status[b], sim->failed[a], sim->failed[b]);
+        sim->status[a], sim->status[b], sim->failed[a], sim->failed[b], sim->hint[a], sim->hint[b]);
     k_after_compact<<<1, 1, 0, st>>>(sim->plan, sim->dst_idx);
     CKL(sim);
     sim->launches += 6;

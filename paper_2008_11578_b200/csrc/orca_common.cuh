@@ -26,7 +26,7 @@ struct GridPlan {
     int n;       // rows in the state arrays (owned + ghost)
     int n_owned; // rows [0, n_owned) are solved and integrated; the rest are halo ghosts
     // search grid (rebuilt every step from the bounding box)
-    int nx, ny, ncells, rmax;
+    int nx, ny, ncells, rmax, r0;
     double x0, y0, cell, inv_cell;
     // bounding-box accumulators, order-preserving u64 encodings of doubles
     u64 minx, miny, maxx, maxy;
@@ -37,6 +37,9 @@ struct GridPlan {
     int err_range;  // a position left the reference's indexable grid range
     // per-step counters
     int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
+    int gq_count;  // agents queued for the exact ring search (k_gather)
+    u64 vmax_enc;  // order-preserving encoding of the largest max_speed ever uploaded
+    double vmax;
     int removed;   // arrivals removed by this step
     int n_after;   // rows after arrival removal
     // metrics
@@ -53,6 +56,7 @@ struct StepParams {
     int stride;  // leading dimension of the slot-major neighbour table
     i64 frame;   // pre-step frame index (seed input, engine.py:233)
     int max_cells;
+    int r0_override; // > 0: force the first ring radius (experiments)
     double occ_target;
 };
 

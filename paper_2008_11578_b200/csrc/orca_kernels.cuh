@@ -33,6 +33,7 @@ namespace orca {
 __global__ void k_begin_step(GridPlan *plan)
 {
     plan->fq_count = 0;
+    plan->gq_count = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
     plan->collisions = 0;
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(256) k_bbox(GridPlan *plan, const typename Vec
 __global__ void k_plan(GridPlan *plan, StepParams P)
 {
     const int n = plan->n;
+    plan->vmax = fmax(dec_double(plan->vmax_enc), 0.0);
     double x0 = 0.0, y0 = 0.0, w = 0.0, h = 0.0;
     if (n > 0) {
         x0 = dec_double(plan->minx);
@@ -102,6 +104,12 @@ __global__ void k_plan(GridPlan *plan, StepParams P)
     plan->ny = ny;
     plan->ncells = nx * ny;
     plan->rmax = (int)ceil(nr / c * (1.0 + 1e-9));
+    // first ring radius: the smallest block of cells expected to hold ~1.3 * max_n agents
+    // at the mean density (the search still grows ring by ring where that is not enough)
+    const double occ = fmax((double)n, 1.0) * c * c / area;
+    int r0 = (int)ceil((sqrt(1.3 * (double)max(P.max_n, 1) / fmax(occ, 1e-9)) - 1.0) * 0.5);
+    if (P.r0_override > 0) r0 = P.r0_override;
+    plan->r0 = min(max(r0, 1), plan->rmax);
 }
 
 __device__ __forceinline__ void search_cell(const GridPlan *plan, double x, double y, int &cx, int &cy)
@@ -234,8 +242,9 @@ k_scan_apply(const int *__restrict__ len_ptr, int len_extra, const int *__restri
 // Scatter into cell-sorted order. Writes, per sorted slot s:
 //   s_xy  (x, y)                         candidate stream of the neighbour search
 //   s_pv  (x, y, vx, vy)                 pre-step snapshot
-//   s_dm  (des_vx, des_vy, max_speed, avoid_radius)
-//   s_row storage row, s_cell search cell, s_cls class code
+//   s_dm  (des_vx, des_vy, max_speed, avoid_radius)   own LP inputs, arithmetic type
+//   s_rc  (radius, class code)                         what neighbours read of an agent
+//   s_row storage row, s_cell search cell
 template <typename S, typename R>
 __global__ void __launch_bounds__(256)
 k_scatter(const GridPlan *__restrict__ plan, StepParams P,
@@ -244,7 +253,7 @@ k_scatter(const GridPlan *__restrict__ plan, StepParams P,
           const int *__restrict__ cell_of, const int *__restrict__ rank_of,
           const int *__restrict__ cell_start, typename Vec<S>::T2 *__restrict__ s_xy,
           typename Vec<S>::T4 *__restrict__ s_pv, typename Vec<R>::T4 *__restrict__ s_dm,
-          int *__restrict__ s_row, int *__restrict__ s_cell, u8 *__restrict__ s_cls)
+          int *__restrict__ s_row, int *__restrict__ s_cell, typename Vec<S>::T2 *__restrict__ s_rc)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= plan->n) return;
@@ -266,27 +275,116 @@ k_scatter(const GridPlan *__restrict__ plan, StepParams P,
     s_dm[s] = mk4(dx * scale, dy * scale, (R)rm.y, avoid);
     s_row[s] = i;
     s_cell[s] = c;
-    s_cls[s] = cls[i];
+    s_rc[s] = mk2(rm.x, (S)cls[i]); // what a neighbour needs besides s_pv: radius and class
 }
 
 // ---------------------------------------------------------------------------
 // K2: neighbour gather
 // ---------------------------------------------------------------------------
 
-// One thread per agent (cell-sorted order, so a warp shares its candidate
-// stream). The kept list lives in registers, ascending by (d2, id); slots
-// [0, MAXN-max_n) hold -1 sentinels so the admission threshold is always the
-// last register. Keys are FP64 d2 = dx*dx + dy*dy evaluated exactly like
+#define ORCA_INF __longlong_as_double(0x7FF0000000000000LL)
+
+// The kept list of one agent, in registers, ascending by (d2, id). Slots
+// [0, MAXN-max_n) hold -1 sentinels so the admission threshold is always the last
+// register. Keys are FP64 d2 = dx*dx + dy*dy evaluated exactly like
 // _kernels.py:467-469 (no FMA), so the list is bit-identical to the reference's
-// for float32-representable positions; the FP32 build pre-filters with an FP32
-// distance against a slightly inflated threshold before touching FP64.
-template <typename R, int MAXN>
+// whenever the positions are representable in the storage type.
+template <int MAXN> struct TopK {
+    double key[MAXN];
+    int idx[MAXN];
+    int cnt;
+
+    __device__ __forceinline__ void init(int max_n)
+    {
+        const int off = MAXN - max_n;
+#pragma unroll
+        for (int t = 0; t < MAXN; ++t) {
+            key[t] = t < off ? -1.0 : ORCA_INF;
+            idx[t] = -1;
+        }
+        cnt = 0;
+    }
+
+    // _kernels.py:473-489: admit (d2, id) if it precedes the current last entry, then
+    // shift it into place. Returns true if the list changed.
+    __device__ __forceinline__ bool insert(double d2, int s2, int max_n, const int *__restrict__ s_row,
+                                           const i64 *__restrict__ ids)
+    {
+        const double last = key[MAXN - 1];
+        if (d2 > last) return false;
+        i64 my_id = 0;
+        bool have_id = false;
+        if (d2 == last) {
+            my_id = ids[s_row[s2]];
+            have_id = true;
+            if (my_id >= ids[s_row[idx[MAXN - 1]]]) return false;
+        }
+        bool c_next = true;
+#pragma unroll
+        for (int p = MAXN - 1; p >= 1; --p) {
+            bool cp = d2 < key[p - 1];
+            if (d2 == key[p - 1]) {
+                if (!have_id) {
+                    my_id = ids[s_row[s2]];
+                    have_id = true;
+                }
+                cp = my_id < ids[s_row[idx[p - 1]]];
+            }
+            if (cp) {
+                key[p] = key[p - 1];
+                idx[p] = idx[p - 1];
+            } else if (c_next) {
+                key[p] = d2;
+                idx[p] = s2;
+            }
+            c_next = cp;
+        }
+        if (c_next) {
+            key[0] = d2;
+            idx[0] = s2;
+        }
+        cnt = min(cnt + 1, max_n);
+        return true;
+    }
+
+    // slot-major neighbour table + count + next step's radius hint
+    __device__ __forceinline__ void store(int s, int row, int max_n, int stride, int *__restrict__ nb,
+                                          u8 *__restrict__ nb_cnt, float *__restrict__ hint) const
+    {
+        const int off = MAXN - max_n;
+        nb_cnt[s] = (u8)cnt;
+#pragma unroll
+        for (int t = 0; t < MAXN; ++t) {
+            const int slot = t - off;
+            if (slot >= 0 && slot < cnt) nb[(size_t)slot * stride + s] = idx[t];
+        }
+        // radius that held the whole list this step (rounded up); +inf when fewer than
+        // max_n agents are in range, so the next fast pass scans the full radius
+        hint[row] = cnt == max_n ? __double2float_ru(__dsqrt_ru(key[MAXN - 1])) : __int_as_float(0x7F800000);
+    }
+};
+
+// Fast pass, one thread per agent in cell-sorted order. It relies on temporal
+// coherence but never on it for correctness: last step every kept neighbour was within
+// `hint`, and nobody moves faster than its max_speed, so this step at least max_n agents
+// are within  b = hint + (my max_speed + fastest max_speed) * dt.  The thread scans the
+// cells covering b once, appends every candidate passing a cheap (FP32) distance test
+// to a small shared-memory buffer, then inserts the buffered candidates into the
+// register list with exact FP64 keys -- all lanes of a warp insert at the same time,
+// where the ring search below inserts whenever any lane finds a closer candidate.
+// The result is accepted only if it is provably the exact list (full, and its last key
+// <= b*b, or b covers the whole neighbor_radius); otherwise the agent goes to the queue
+// of the exact ring search (k_gather): no hint yet, a removed neighbour, a teleported
+// agent, or more than CAP candidates.
+template <typename R, int MAXN, int CAP>
 __global__ void __launch_bounds__(128)
-k_gather(const GridPlan *__restrict__ plan, StepParams P,
-         const typename Vec<R>::T2 *__restrict__ s_xy, const int *__restrict__ cell_start,
-         const int *__restrict__ s_cell, const int *__restrict__ s_row,
-         const i64 *__restrict__ ids, int *__restrict__ nb, u8 *__restrict__ nb_cnt)
+k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *__restrict__ s_xy,
+              const int *__restrict__ cell_start, const int *__restrict__ s_cell,
+              const int *__restrict__ s_row, const i64 *__restrict__ ids,
+              const typename Vec<R>::T2 *__restrict__ radmax, float *__restrict__ hint,
+              int *__restrict__ nb, u8 *__restrict__ nb_cnt, int *__restrict__ gq)
 {
+    __shared__ int buf[CAP * 128];
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= plan->n) return;
     const int row = s_row[s];
@@ -294,114 +392,155 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
         nb_cnt[s] = 0;
         return;
     }
+    const float h = hint[row];
+    const double rad2 = P.rad2;
+    const int max_n = P.max_n;
+    const typename Vec<R>::T2 me = s_xy[s];
+    const double mx = (double)me.x, my = (double)me.y;
+    // h == +inf (no list yet, or fewer than max_n in range last step): scan the whole radius
+    double b = (double)h + ((double)radmax[row].y + plan->vmax) * P.dt * (1.0 + 1e-6) + 1e-3;
+    const double T = fmin(b * b, rad2); // NaN-safe: fmin(inf*..., rad2) == rad2
+    const float T_f = __double2float_ru(T * (1.0 + 1e-6));
+
+    const int nx = plan->nx, ny = plan->ny;
+    const int c0 = s_cell[s];
+    const int cx = c0 / ny, cy = c0 - cx * ny;
+    const int r = min(plan->rmax, (int)(sqrt(T) * plan->inv_cell * (1.0 + 1e-9)) + 1);
+    const int gx_lo = max(cx - r, 0), gx_hi = min(cx + r, nx - 1);
+    const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
+    int *my_buf = buf + threadIdx.x;
+    int nbuf = 0;
+    for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+        const int *cs = cell_start + gx * ny;
+        const int e = cs[y_hi + 1];
+        for (int s2 = cs[y_lo]; s2 < e; ++s2) {
+            const typename Vec<R>::T2 q = s_xy[s2];
+            bool pass;
+            if (Fmt<R>::is_f32) {
+                const float dxf = (float)q.x - (float)me.x, dyf = (float)q.y - (float)me.y;
+                pass = dxf * dxf + dyf * dyf <= T_f;
+            } else {
+                const double dx = (double)q.x - mx, dy = (double)q.y - my;
+                pass = dx * dx + dy * dy <= T;
+            }
+            if (pass) {
+                if (nbuf < CAP) my_buf[nbuf * 128] = s2;
+                ++nbuf;
+            }
+        }
+    }
+    bool ok = nbuf <= CAP;
+    TopK<MAXN> top;
+    top.init(max_n);
+    if (ok) {
+        for (int e = 0; e < nbuf; ++e) {
+            const int s2 = my_buf[e * 128];
+            const typename Vec<R>::T2 q = s_xy[s2];
+            const double dx = (double)q.x - mx, dy = (double)q.y - my;
+            const double d2 = dx * dx + dy * dy;
+            if (s2 == s || d2 > rad2) continue;
+            top.insert(d2, s2, max_n, s_row, ids);
+        }
+        // exact iff nothing outside the buffer can precede the last kept entry
+        ok = T >= rad2 || (top.cnt == max_n && top.key[MAXN - 1] <= T);
+    }
+    if (ok) {
+        top.store(s, row, max_n, P.stride, nb, nb_cnt, hint);
+    } else {
+        gq[atomicAdd(&plan->gq_count, 1)] = s;
+    }
+}
+
+// every owned agent goes to the exact ring search (fast pass disabled)
+__global__ void __launch_bounds__(256)
+k_enqueue_all(GridPlan *__restrict__ plan, int max_n, const int *__restrict__ s_row,
+              u8 *__restrict__ nb_cnt, int *__restrict__ gq)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= plan->n) return;
+    if (s_row[s] >= plan->n_owned || max_n == 0) {
+        nb_cnt[s] = 0;
+        return;
+    }
+    gq[atomicAdd(&plan->gq_count, 1)] = s;
+}
+
+// Exact ring search for the agents the fast pass queued (all of them on the first step
+// after an upload). The search grid is walked in growing square rings around the
+// agent's cell; it stops as soon as the list is full and every unscanned cell is
+// provably farther than its last entry. The FP32 build pre-filters with an FP32
+// distance against a slightly inflated threshold before touching FP64.
+template <typename R, int MAXN>
+__global__ void __launch_bounds__(128)
+k_gather(const GridPlan *__restrict__ plan, StepParams P,
+         const typename Vec<R>::T2 *__restrict__ s_xy, const int *__restrict__ cell_start,
+         const int *__restrict__ s_cell, const int *__restrict__ s_row,
+         const i64 *__restrict__ ids, float *__restrict__ hint, int *__restrict__ nb,
+         u8 *__restrict__ nb_cnt, const int *__restrict__ gq)
+{
+    const int nq = plan->gq_count;
     const int nx = plan->nx, ny = plan->ny, rmax = plan->rmax;
     const double cell = plan->cell;
     const double rad2 = P.rad2;
     const int max_n = P.max_n;
-    const int off = MAXN - max_n;
+    for (int qi = blockIdx.x * blockDim.x + threadIdx.x; qi < nq; qi += gridDim.x * blockDim.x) {
+        const int s = gq[qi];
+        const int row = s_row[s];
+        const typename Vec<R>::T2 me = s_xy[s];
+        const double mx = (double)me.x, my = (double)me.y;
+        const int c0 = s_cell[s];
+        const int cx = c0 / ny, cy = c0 - cx * ny;
 
-    const typename Vec<R>::T2 me = s_xy[s];
-    const double mx = (double)me.x, my = (double)me.y;
-    const int c0 = s_cell[s];
-    const int cx = c0 / ny, cy = c0 - cx * ny;
+        TopK<MAXN> top;
+        top.init(max_n);
+        float thr_f = __double2float_ru(rad2 * (1.0 + 1e-6));
 
-    double key[MAXN];
-    int idx[MAXN];
-#pragma unroll
-    for (int t = 0; t < MAXN; ++t) {
-        key[t] = t < off ? -1.0 : __longlong_as_double(0x7FF0000000000000LL);
-        idx[t] = -1;
-    }
-    int cnt = 0;
-    float thr_f = __double2float_ru(rad2 * (1.0 + 1e-6));
-
-    auto id_of = [&](int sidx) -> i64 { return ids[s_row[sidx]]; };
-
-    auto scan_range = [&](int a, int b) {
-        for (int s2 = a; s2 < b; ++s2) {
-            const typename Vec<R>::T2 q = s_xy[s2];
-            if (Fmt<R>::is_f32) {
-                const float dxf = (float)q.x - (float)me.x, dyf = (float)q.y - (float)me.y;
-                if (dxf * dxf + dyf * dyf > thr_f) continue;
-            }
-            const double dx = (double)q.x - mx, dy = (double)q.y - my;
-            const double d2 = dx * dx + dy * dy;
-            if (s2 == s || d2 > rad2) continue;
-            // admission against the current last entry, _kernels.py:473-476
-            const double last = key[MAXN - 1];
-            if (d2 > last) continue;
-            i64 my_id = 0;
-            bool have_id = false;
-            if (d2 == last) {
-                my_id = id_of(s2);
-                have_id = true;
-                if (my_id >= id_of(idx[MAXN - 1])) continue;
-            }
-            bool c_next = true;
-#pragma unroll
-            for (int p = MAXN - 1; p >= 1; --p) {
-                bool cp = d2 < key[p - 1];
-                if (d2 == key[p - 1]) {
-                    if (!have_id) {
-                        my_id = id_of(s2);
-                        have_id = true;
-                    }
-                    cp = my_id < id_of(idx[p - 1]);
+        auto scan_range = [&](int a, int b) {
+            for (int s2 = a; s2 < b; ++s2) {
+                const typename Vec<R>::T2 q = s_xy[s2];
+                if (Fmt<R>::is_f32) {
+                    const float dxf = (float)q.x - (float)me.x, dyf = (float)q.y - (float)me.y;
+                    if (dxf * dxf + dyf * dyf > thr_f) continue;
                 }
-                if (cp) {
-                    key[p] = key[p - 1];
-                    idx[p] = idx[p - 1];
-                } else if (c_next) {
-                    key[p] = d2;
-                    idx[p] = s2;
-                }
-                c_next = cp;
+                const double dx = (double)q.x - mx, dy = (double)q.y - my;
+                const double d2 = dx * dx + dy * dy;
+                if (s2 == s || d2 > rad2) continue;
+                if (top.insert(d2, s2, max_n, s_row, ids) && Fmt<R>::is_f32)
+                    thr_f = __double2float_ru(fmin(top.key[MAXN - 1], rad2) * (1.0 + 1e-6));
             }
-            if (c_next) {
-                key[0] = d2;
-                idx[0] = s2;
-            }
-            cnt = min(cnt + 1, max_n);
-            if (Fmt<R>::is_f32) thr_f = __double2float_ru(fmin(key[MAXN - 1], rad2) * (1.0 + 1e-6));
-        }
-    };
+        };
 
-    int r_done = -1;
-    int r_next = min(1, rmax);
-    while (true) {
-        const int gx_lo = max(cx - r_next, 0), gx_hi = min(cx + r_next, nx - 1);
-        const int y_lo = max(cy - r_next, 0), y_hi = min(cy + r_next, ny - 1);
-        for (int gx = gx_lo; gx <= gx_hi; ++gx) {
-            const int *cs = cell_start + gx * ny;
-            if (abs(gx - cx) > r_done) {
-                scan_range(cs[y_lo], cs[y_hi + 1]);
+        int r_done = -1;
+        int r_next = plan->r0;
+        while (true) {
+            const int gx_lo = max(cx - r_next, 0), gx_hi = min(cx + r_next, nx - 1);
+            const int y_lo = max(cy - r_next, 0), y_hi = min(cy + r_next, ny - 1);
+            for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+                const int *cs = cell_start + gx * ny;
+                if (abs(gx - cx) > r_done) {
+                    scan_range(cs[y_lo], cs[y_hi + 1]);
+                } else {
+                    const int b_hi = cy - r_done - 1;
+                    if (b_hi >= y_lo) scan_range(cs[y_lo], cs[b_hi + 1]);
+                    const int t_lo = cy + r_done + 1;
+                    if (t_lo <= y_hi) scan_range(cs[t_lo], cs[y_hi + 1]);
+                }
+            }
+            r_done = r_next;
+            if (r_done >= rmax) break;
+            if (top.cnt == max_n) {
+                // Every unscanned agent is farther than r_done*cell (1e-9 margin for the
+                // rounding of the cell index); stop once the kept list is closer than that.
+                const double d_last = top.key[MAXN - 1];
+                const double reach = (double)r_done * cell;
+                if (d_last < reach * reach * (1.0 - 1e-9)) break;
+                const int need = (int)(sqrt(d_last) / cell * (1.0 + 1e-9)) + 1;
+                r_next = min(rmax, max(r_done + 1, need));
             } else {
-                const int b_hi = cy - r_done - 1;
-                if (b_hi >= y_lo) scan_range(cs[y_lo], cs[b_hi + 1]);
-                const int t_lo = cy + r_done + 1;
-                if (t_lo <= y_hi) scan_range(cs[t_lo], cs[y_hi + 1]);
+                r_next = min(rmax, r_done + 1);
             }
         }
-        r_done = r_next;
-        if (r_done >= rmax) break;
-        if (cnt == max_n) {
-            // Every unscanned agent is farther than r_done*cell (1e-9 margin for the
-            // rounding of the cell index); stop once the kept list is closer than that.
-            const double d_last = key[MAXN - 1];
-            const double reach = (double)r_done * cell;
-            if (d_last < reach * reach * (1.0 - 1e-9)) break;
-            const int need = (int)(sqrt(d_last) / cell * (1.0 + 1e-9)) + 1;
-            r_next = min(rmax, max(r_done + 1, need));
-        } else {
-            r_next = min(rmax, r_done + 1);
-        }
-    }
-
-    nb_cnt[s] = (u8)cnt;
-#pragma unroll
-    for (int t = 0; t < MAXN; ++t) {
-        const int slot = t - off;
-        if (slot >= 0 && slot < cnt) nb[(size_t)slot * P.stride + s] = idx[t];
+        top.store(s, row, max_n, P.stride, nb, nb_cnt, hint);
     }
 }
 
@@ -464,20 +603,22 @@ __device__ __forceinline__ void shuffle_smem(u8 *perm, int stride, int k, u64 se
 template <typename S, typename R>
 __device__ __forceinline__ bool build_constraints(
     int s, int cnt, const StepParams &P, const typename Vec<S>::T4 *__restrict__ s_pv,
-    const typename Vec<R>::T4 *__restrict__ s_dm, const u8 *__restrict__ s_cls,
-    const int *__restrict__ nb, const u8 *perm, int stride, SmemCons<R> &cons, int &bad_j)
+    const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ nb, const u8 *perm,
+    int stride, SmemCons<R> &cons, int &bad_j)
 {
     const typename Vec<S>::T4 me_s = s_pv[s];
     const R mex = (R)me_s.x, mey = (R)me_s.y, mevx = (R)me_s.z, mevy = (R)me_s.w;
-    const R ri = s_dm[s].w;
-    const int ci = s_cls[s];
+    const typename Vec<S>::T2 rc_i = s_rc[s];
+    const R ri = (R)((double)rc_i.x + P.half_margin); // engine.py:227, as in k_scatter
+    const int ci = (int)rc_i.y;
     const R tau = (R)P.tau, dt = (R)P.dt;
+    const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
     for (int pos = 0; pos < cnt; ++pos) {
         const int t = perm[pos * stride];
         const int j = nb[(size_t)t * P.stride + s];
         const typename Vec<S>::T4 q = s_pv[j];
-        const R rj = s_dm[j].w;
-        const int cj = s_cls[j];
+        const typename Vec<S>::T2 rc_j = s_rc[j];
+        const R rj = (R)((double)rc_j.x + P.half_margin);
         R ux, uy, nx, ny;
         if (!vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, tau, dt,
                         ux, uy, nx, ny)) {
@@ -486,7 +627,7 @@ __device__ __forceinline__ bool build_constraints(
             bad_j = nb[s];
             return false;
         }
-        const R f = (R)P.fmat[ci * 2 + cj];
+        const R f = rc_j.y != S(0) ? f1 : f0; // fmat[cls_i, cls_j], _kernels.py:537
         cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
     }
     return true;
@@ -511,7 +652,7 @@ __device__ __forceinline__ void integrate_row(int row, const typename Vec<S>::T4
 template <typename S, typename R, int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__restrict__ s_pv,
-        const typename Vec<R>::T4 *__restrict__ s_dm, const u8 *__restrict__ s_cls,
+        const typename Vec<R>::T4 *__restrict__ s_dm, const typename Vec<S>::T2 *__restrict__ s_rc,
         const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
         const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
         typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
@@ -536,7 +677,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
 
     int bad_j = -1;
-    if (!build_constraints<S, R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j)) {
+    if (!build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, THREADS, cons, bad_j)) {
         // _kernels.py:542-547 + engine.py:239-245
         if (plan->err_frame < 0) // sticky: only the first failing frame is reported
             atomicMin(&plan->err_pair, ((u64)(unsigned)row << 32) | (u64)(unsigned)s_row[bad_j]);
@@ -562,11 +703,17 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
 }
 
+// Least-penetration stage for the agents k_solve queued. The stage is a long chain of
+// dependent FP64 operations whose control flow differs from agent to agent, so a full
+// warp of 32 queued agents would serialise ~32 different paths while the machine sits
+// idle for lack of warps. Only `lanes` lanes of every warp take an agent (8 by default):
+// 4x more warps in flight for the same queue and 4x fewer paths to serialise per warp.
+// Shared memory is sized for the active lanes only.
 template <typename S, typename R, int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
-k_fallback(const GridPlan *__restrict__ plan, StepParams P,
+k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
            const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
-           const u8 *__restrict__ s_cls, const int *__restrict__ s_row,
+           const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ s_row,
            const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
            const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
            u8 *__restrict__ arrived, const int *__restrict__ fq,
@@ -574,30 +721,34 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P,
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef typename Vec<R>::T4 R4;
+    const int lane = threadIdx.x & 31;
+    if (lane >= lanes) return;
+    const int AT = (THREADS / 32) * lanes;             // active threads per block
+    const int at = (threadIdx.x >> 5) * lanes + lane;  // this thread's active index
     R4 *sm_cons = reinterpret_cast<R4 *>(smem_raw);
-    R4 *sm_proj = sm_cons + MAXN * THREADS;
-    u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * THREADS);
-    u8 *sm_inv = sm_perm + MAXN * THREADS;
+    R4 *sm_proj = sm_cons + MAXN * AT;
+    u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * AT);
+    u8 *sm_inv = sm_perm + MAXN * AT;
 
     const int nq = plan->fq_count;
-    for (int q = blockIdx.x * THREADS + threadIdx.x; q < nq; q += gridDim.x * THREADS) {
+    for (int q = blockIdx.x * AT + at; q < nq; q += gridDim.x * AT) {
         const int s = fq[q];
         const R4 st = fq_state[q];
         const int row = s_row[s];
         const int cnt = nb_cnt[s];
         const typename Vec<S>::T4 me = s_pv[s];
         const R4 dm = s_dm[s];
-        u8 *perm = sm_perm + threadIdx.x;
-        u8 *inv = sm_inv + threadIdx.x;
-        SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
-        SmemCons<R> proj{sm_proj + threadIdx.x, THREADS};
+        u8 *perm = sm_perm + at;
+        u8 *inv = sm_inv + at;
+        SmemCons<R> cons{sm_cons + at, AT};
+        SmemCons<R> proj{sm_proj + at, AT};
 
-        shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
-        for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * THREADS] * THREADS] = (u8)pos;
+        shuffle_smem<MAXN>(perm, AT, cnt, problem_seed(P.frame, ids[row]));
+        for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * AT] * AT] = (u8)pos;
         int bad_j;
-        build_constraints<S, R>(s, cnt, P, s_pv, s_dm, s_cls, nb, perm, THREADS, cons, bad_j);
+        build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, AT, cons, bad_j);
 
-        SmemConsIdent<R> ident{sm_cons + threadIdx.x, inv, THREADS};
+        SmemConsIdent<R> ident{sm_cons + at, inv, AT};
         R rx, ry;
         least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry);
@@ -637,7 +788,8 @@ k_compact(GridPlan *__restrict__ plan, const int *__restrict__ keep, const int *
           const typename Vec<R>::T2 *__restrict__ rm, typename Vec<R>::T2 *__restrict__ rm2,
           const i64 *__restrict__ ids, i64 *__restrict__ ids2, const u8 *__restrict__ cls,
           u8 *__restrict__ cls2, const i8 *__restrict__ st, i8 *__restrict__ st2,
-          const i8 *__restrict__ fa, i8 *__restrict__ fa2)
+          const i8 *__restrict__ fa, i8 *__restrict__ fa2, const float *__restrict__ hint,
+          float *__restrict__ hint2)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = plan->n;
@@ -651,6 +803,7 @@ k_compact(GridPlan *__restrict__ plan, const int *__restrict__ keep, const int *
         cls2[d] = cls[i];
         st2[d] = st[i];
         fa2[d] = fa[i];
+        hint2[d] = hint[i];
     }
 }
 
@@ -734,10 +887,12 @@ k_import_attrs(int n, const double *__restrict__ radii, const double *__restrict
                const double *__restrict__ maxs, const double *__restrict__ goals,
                const double *__restrict__ gtol, const i64 *__restrict__ cls_in,
                typename Vec<R>::T4 *__restrict__ goalpref, typename Vec<R>::T2 *__restrict__ radmax,
-               u8 *__restrict__ cls)
+               u8 *__restrict__ cls, float *__restrict__ hint, GridPlan *__restrict__ plan)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    hint[i] = __int_as_float(0x7F800000); // no neighbour list yet
+    atomicMax(&plan->vmax_enc, enc_double(maxs[i]));
     goalpref[i] = mk4((R)goals[2 * i], (R)goals[2 * i + 1], (R)pref[i], (R)gtol[i]);
     radmax[i] = mk2((R)radii[i], (R)maxs[i]);
     cls[i] = (u8)cls_in[i];
