@@ -237,6 +237,48 @@ ORCA_API int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *p
 /* _problem_seed (_kernels.py:57-61) computed on the device. */
 ORCA_API int orca_problem_seed(int device, int64_t frame, int64_t agent_id, uint64_t *seed);
 
+/* ---- multi-GPU strip decomposition (device-pointer level) ------------------
+ *
+ * The reference has no multi-process path; this is the B200-native
+ * addition for crowds larger than one device: the plaza is cut into x-strips, one
+ * handle (one process, one GPU) per strip. Every step each rank
+ *   1. packs its owned agents within neighbor_radius of a strip edge
+ *      (orca_strip_pack, remove = 0) and sends them to that neighbour,
+ *   2. appends what it received as ghosts (orca_strip_append, ghost = 1): ghosts
+ *      take part in the neighbour search of owned agents but are never solved,
+ *      integrated or reported, and the step drops them again,
+ *   3. steps (orca_step),
+ *   4. packs-and-removes the owned agents whose new x left the strip
+ *      (orca_strip_pack, remove = 1), sends them, and appends the arrivals as
+ *      owned rows (ghost = 0).
+ * Per-agent results depend only on the pre-step snapshot of the agents within
+ * neighbor_radius, so they are bit-identical to a single-device run (keyed by id).
+ * The records travel between ranks as raw bytes (NCCL send/recv). */
+
+typedef struct orca_agent_record {
+    double x, y, vx, vy;
+    double radius, pref_speed, max_speed, goal_tol;
+    double goal_x, goal_y;
+    int64_t id;
+    int64_t class_code;
+} orca_agent_record; /* 96 bytes */
+
+/* Select owned rows with x in [x_lo, x_hi), write them to `records` (DEVICE
+ * pointer, room for `cap` records) and return how many were selected in
+ * *count_out (HOST). If more than `cap` were selected the call fails with
+ * ORCA_ECAPACITY and nothing is removed. With remove != 0 the selected rows are
+ * deleted from the handle. Synchronises. */
+ORCA_API int orca_strip_pack(orca_sim *sim, double x_lo, double x_hi, int remove,
+                             orca_agent_record *records, int64_t cap, int64_t *count_out);
+
+/* Append `count` records (DEVICE pointer) after the resident rows, as owned rows
+ * (ghost == 0; not allowed while ghosts are resident) or as ghosts. Asynchronous. */
+ORCA_API int orca_strip_append(orca_sim *sim, const orca_agent_record *records, int64_t count,
+                               int ghost);
+
+/* Forget the ghost rows without stepping. */
+ORCA_API int orca_strip_drop_ghosts(orca_sim *sim);
+
 #ifdef __cplusplus
 }
 #endif

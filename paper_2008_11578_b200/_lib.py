@@ -31,7 +31,13 @@ SYMBOLS = [
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
     "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
+    "orca_strip_pack", "orca_strip_append", "orca_strip_drop_ghosts",
 ]
+
+RECORD_BYTES = 96   # sizeof(orca_agent_record)
+RECORD_DTYPE = np.dtype([("x", "f8"), ("y", "f8"), ("vx", "f8"), ("vy", "f8"), ("radius", "f8"),
+                         ("pref_speed", "f8"), ("max_speed", "f8"), ("goal_tol", "f8"),
+                         ("goal_x", "f8"), ("goal_y", "f8"), ("id", "i8"), ("class_code", "i8")])
 
 
 class OrcaError(RuntimeError):
@@ -103,6 +109,9 @@ def load():
     L.orca_vo_exit_batch.argtypes = [ci, ci, i64, vp, vp]
     L.orca_shuffle_order.argtypes = [ci, i64, u64, vp]
     L.orca_problem_seed.argtypes = [ci, i64, i64, P(u64)]
+    L.orca_strip_pack.argtypes = [vp, f64, f64, ci, vp, i64, P(i64)]
+    L.orca_strip_append.argtypes = [vp, vp, i64, ci]
+    L.orca_strip_drop_ghosts.argtypes = [vp]
     for name in SYMBOLS:
         fn = getattr(L, name)
         if name not in ("orca_destroy", "orca_last_error", "orca_lp_batch_destroy"):

@@ -44,6 +44,8 @@ struct orca_sim {
     int acur = 0;
     u8 *arrived = nullptr;
     int *keep = nullptr, *dst_idx = nullptr;
+    int *sel = nullptr, *sel_idx = nullptr; // strip selection flags and their scan
+    int64_t ghost_bound = 0;                // ghost rows currently appended
 
     // per-step scratch
     int max_cells = 0;
@@ -170,6 +172,8 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->arrived);
     cudaFree(sim->keep);
     cudaFree(sim->dst_idx);
+    cudaFree(sim->sel);
+    cudaFree(sim->sel_idx);
     cudaFree(sim->cell_of);
     cudaFree(sim->rank_of);
     cudaFree(sim->cell_count);
@@ -251,6 +255,8 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->arrived, cap));
     CKC(dalloc(&sim->keep, cap + 1));
     CKC(dalloc(&sim->dst_idx, cap + 1));
+    CKC(dalloc(&sim->sel, cap + 1));
+    CKC(dalloc(&sim->sel_idx, cap + 1));
     CKC(dalloc(&sim->cell_of, cap));
     CKC(dalloc(&sim->rank_of, cap));
     CKC(dalloc(&sim->cell_count, (size_t)sim->max_cells + 1));
@@ -408,6 +414,7 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->frame = frame;
     sim->n_bound = n;
     sim->n_pre = n;
+    sim->ghost_bound = 0;
     sim->loaded = true;
     sim->binned_frame = -1;
     return ORCA_OK;
@@ -643,15 +650,20 @@ __global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids, i64
     }
 }
 
-template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int dst_pv_idx)
+// Order-preserving removal of rows: arrivals and ghosts after a step (from_sel == false)
+// or the rows orca_strip_pack selected (from_sel == true).
+template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int dst_pv_idx, bool from_sel = false)
 {
     typedef typename Vec<R>::T4 R4;
     typedef typename Vec<R>::T2 R2;
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur, b = 1 - a;
-    k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
-                                                       sim->params.remove_arrivals);
+    if (from_sel)
+        k_keep_unselected<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->sel, sim->keep);
+    else
+        k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
+                                                           sim->params.remove_arrivals);
     const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
     k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums);
     k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
@@ -712,11 +724,13 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     CKL(sim);
     sim->launches += 2;
     sim->pre = sim->cur;
-    if (sim->params.remove_arrivals) {
+    if (sim->params.remove_arrivals || sim->ghost_bound > 0) {
         const int dst = (sim->cur + 2) % 3;
         rc = compact_stage<S>(sim, out_idx, dst);
         if (rc) return rc;
         sim->cur = dst;
+        sim->n_bound -= sim->ghost_bound; // ghosts never survive a step
+        sim->ghost_bound = 0;
     } else {
         sim->cur = out_idx;
     }
@@ -810,6 +824,109 @@ extern "C" int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const dou
         }
     }
     return fetch_plan(sim);
+}
+
+// ---------------------------------------------------------------------------
+// strip decomposition
+// ---------------------------------------------------------------------------
+
+template <typename S>
+static int strip_pack_impl(orca_sim *sim, double x_lo, double x_hi, int remove, orca_agent_record *records,
+                           int64_t cap, int64_t *count_out)
+{
+    typedef typename Vec<S>::T4 S4;
+    typedef typename Vec<S>::T2 S2;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur;
+    const S4 *pv = reinterpret_cast<const S4 *>(sim->pv[sim->cur]);
+    k_strip_flags<S><<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, pv, x_lo, x_hi, sim->sel);
+    const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
+    k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->sel, sim->block_sums);
+    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
+    k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->sel, sim->block_sums, sim->sel_idx);
+    k_strip_pack<S><<<grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(
+        sim->plan, sim->sel, sim->sel_idx, pv, reinterpret_cast<const S4 *>(sim->goalpref[a]),
+        reinterpret_cast<const S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], records, cap);
+    CKL(sim);
+    sim->launches += 5;
+    int rc = fetch_plan(sim);
+    if (rc) return rc;
+    const int64_t count = sim->h_plan->pack_count;
+    if (count_out) *count_out = count;
+    if (count > cap)
+        return fail(sim, ORCA_ECAPACITY, "orca_strip_pack: %lld agents selected, buffer holds %lld",
+                    (long long)count, (long long)cap);
+    if (remove && count > 0) {
+        // compaction of the CURRENT snapshot into a spare pv buffer
+        const int dst = (sim->cur + 1) % 3;
+        rc = compact_stage<S>(sim, sim->cur, dst, true);
+        if (rc) return rc;
+        sim->cur = dst;
+        sim->n_bound -= count;
+        sim->binned_frame = -1;
+    }
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_pack(orca_sim *sim, double x_lo, double x_hi, int remove,
+                               orca_agent_record *records, int64_t cap, int64_t *count_out)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_pack: no resident state");
+    if (cap < 0 || (cap > 0 && !records)) return fail(sim, ORCA_EINVAL, "orca_strip_pack: bad buffer");
+    if (remove && sim->ghost_bound > 0)
+        return fail(sim, ORCA_EINVAL, "orca_strip_pack: cannot remove rows while ghosts are resident");
+    CK(sim, cudaSetDevice(sim->device));
+    return sim->precision == ORCA_F64 ? strip_pack_impl<double>(sim, x_lo, x_hi, remove, records, cap, count_out)
+                                      : strip_pack_impl<float>(sim, x_lo, x_hi, remove, records, cap, count_out);
+}
+
+template <typename S> static int strip_append_impl(orca_sim *sim, const orca_agent_record *records, int64_t count, int ghost)
+{
+    typedef typename Vec<S>::T4 S4;
+    typedef typename Vec<S>::T2 S2;
+    const int a = sim->acur;
+    k_strip_append<S><<<grid_for(count, 256), 256, 0, sim->stream>>>(
+        sim->plan, records, (int)count, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
+        reinterpret_cast<S4 *>(sim->goalpref[a]), reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a],
+        sim->cls[a], sim->status[a], sim->failed[a], sim->hint[a]);
+    k_after_append<<<1, 1, 0, sim->stream>>>(sim->plan, (int)count, ghost);
+    CKL(sim);
+    sim->launches += 2;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_append(orca_sim *sim, const orca_agent_record *records, int64_t count, int ghost)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_append: no resident state");
+    if (count < 0 || (count > 0 && !records)) return fail(sim, ORCA_EINVAL, "orca_strip_append: bad arguments");
+    if (!ghost && sim->ghost_bound > 0)
+        return fail(sim, ORCA_EINVAL, "orca_strip_append: owned rows cannot follow ghost rows");
+    if (sim->n_bound + count > sim->capacity)
+        return fail(sim, ORCA_ECAPACITY, "orca_strip_append: %lld + %lld agents exceed the handle capacity %lld",
+                    (long long)sim->n_bound, (long long)count, (long long)sim->capacity);
+    if (count == 0) return ORCA_OK;
+    CK(sim, cudaSetDevice(sim->device));
+    int rc = sim->precision == ORCA_F64 ? strip_append_impl<double>(sim, records, count, ghost)
+                                        : strip_append_impl<float>(sim, records, count, ghost);
+    if (rc) return rc;
+    sim->n_bound += count;
+    if (ghost) sim->ghost_bound += count;
+    sim->binned_frame = -1;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_drop_ghosts(orca_sim *sim)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_drop_ghosts: no resident state");
+    CK(sim, cudaSetDevice(sim->device));
+    k_drop_ghosts<<<1, 1, 0, sim->stream>>>(sim->plan);
+    CKL(sim);
+    sim->launches += 1;
+    sim->n_bound -= sim->ghost_bound;
+    sim->ghost_bound = 0;
+    sim->binned_frame = -1;
+    return ORCA_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -38,6 +38,7 @@ struct GridPlan {
     // per-step counters
     int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
     int gq_count;  // agents queued for the exact ring search (k_gather)
+    int pack_count; // rows selected by the last orca_strip_pack
     u64 vmax_enc;  // order-preserving encoding of the largest max_speed ever uploaded
     double vmax;
     int removed;   // arrivals removed by this step

@@ -817,6 +817,99 @@ __global__ void k_after_compact(GridPlan *plan, const int *__restrict__ dst_idx)
 }
 
 // ---------------------------------------------------------------------------
+// strip decomposition: select / pack / append agent records (multi-GPU halo
+// exchange and migration; the records travel over NCCL, see parallel/strips.py)
+// ---------------------------------------------------------------------------
+
+// sel[i] = 1 for owned rows with x in [x_lo, x_hi); sel[n] = 0 closes the scan
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_flags(const GridPlan *__restrict__ plan, const typename Vec<S>::T4 *__restrict__ pv,
+              double x_lo, double x_hi, int *__restrict__ sel)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > plan->n) return;
+    int f = 0;
+    if (i < plan->n_owned) {
+        const double x = (double)pv[i].x;
+        f = (x >= x_lo && x < x_hi) ? 1 : 0;
+    }
+    sel[i] = f;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_pack(GridPlan *__restrict__ plan, const int *__restrict__ sel, const int *__restrict__ sel_idx,
+             const typename Vec<S>::T4 *__restrict__ pv, const typename Vec<S>::T4 *__restrict__ goalpref,
+             const typename Vec<S>::T2 *__restrict__ radmax, const i64 *__restrict__ ids,
+             const u8 *__restrict__ cls, orca_agent_record *__restrict__ rec, i64 cap)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = plan->n;
+    if (i == 0) plan->pack_count = sel_idx[n];
+    if (i >= n || !sel[i]) return;
+    const int d = sel_idx[i];
+    if (d >= cap) return;
+    const typename Vec<S>::T4 a = pv[i];
+    const typename Vec<S>::T4 g = goalpref[i];
+    const typename Vec<S>::T2 rm = radmax[i];
+    orca_agent_record r;
+    r.x = (double)a.x;
+    r.y = (double)a.y;
+    r.vx = (double)a.z;
+    r.vy = (double)a.w;
+    r.radius = (double)rm.x;
+    r.pref_speed = (double)g.z;
+    r.max_speed = (double)rm.y;
+    r.goal_tol = (double)g.w;
+    r.goal_x = (double)g.x;
+    r.goal_y = (double)g.y;
+    r.id = ids[i];
+    r.class_code = (i64)cls[i];
+    rec[d] = r;
+}
+
+// keep everything owned that was NOT selected (migration removes the packed rows)
+__global__ void __launch_bounds__(256)
+k_keep_unselected(const GridPlan *__restrict__ plan, const int *__restrict__ sel, int *__restrict__ keep)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > plan->n) return;
+    keep[i] = (i < plan->n_owned && !sel[i]) ? 1 : 0;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_append(GridPlan *__restrict__ plan, const orca_agent_record *__restrict__ rec, int count,
+               typename Vec<S>::T4 *__restrict__ pv, typename Vec<S>::T4 *__restrict__ goalpref,
+               typename Vec<S>::T2 *__restrict__ radmax, i64 *__restrict__ ids, u8 *__restrict__ cls,
+               i8 *__restrict__ status, i8 *__restrict__ failed, float *__restrict__ hint)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int row = plan->n + i;
+    const orca_agent_record r = rec[i];
+    pv[row] = mk4((S)r.x, (S)r.y, (S)r.vx, (S)r.vy);
+    goalpref[row] = mk4((S)r.goal_x, (S)r.goal_y, (S)r.pref_speed, (S)r.goal_tol);
+    radmax[row] = mk2((S)r.radius, (S)r.max_speed);
+    ids[row] = r.id;
+    cls[row] = (u8)r.class_code;
+    status[row] = 0;
+    failed[row] = -1;
+    hint[row] = __int_as_float(0x7F800000);
+    atomicMax(&plan->vmax_enc, enc_double(r.max_speed));
+}
+
+__global__ void k_after_append(GridPlan *plan, int count, int ghost)
+{
+    plan->n += count;
+    if (!ghost) plan->n_owned += count;
+    plan->n_after = plan->n_owned;
+}
+
+__global__ void k_drop_ghosts(GridPlan *plan) { plan->n = plan->n_owned; }
+
+// ---------------------------------------------------------------------------
 // metrics: min separation / collision count (_kernels.py:559-589) on the
 // post-step positions, using the grid of the NEXT bin build (same positions).
 // ---------------------------------------------------------------------------
