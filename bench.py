@@ -263,10 +263,11 @@ def run_ours(args):
     cur = host_state
     h2d = d2h = 0
     for _ in range(e2e_steps):
-        n_in = cur.active_count
         cur, metrics = E.step(cur, cfg, precision=args.precision, device=local)
-        h2d += 104 * n_in
-        d2h += 104 * cur.active_count
+        # bytes actually copied: positions + velocities always; the 7 attribute arrays
+        # (72 B/agent) only when not already resident / re-read after arrivals
+        h2d += E.step.last_traffic[0]
+        d2h += E.step.last_traffic[1]
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     e2e_value = n / e2e_ms * 1e3

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liborca_b200.so")
+# ORCA_B200_LIB: load another build of the same ABI (kernel experiments)
+LIB_PATH = os.environ.get("ORCA_B200_LIB") or os.path.join(_HERE, "liborca_b200.so")
 
 ORCA_F32, ORCA_F64, ORCA_MIXED = 0, 1, 2
 ORCA_MAX_NEIGHBORS = 32

@@ -74,6 +74,7 @@ struct orca_sim {
     int r0_override = 0;       // ORCA_R0: force the first ring radius (experiments)
     int fb_lanes = 8;          // ORCA_FB_LANES: lanes per warp that take a fallback agent
     bool gather_fast = true;   // ORCA_GATHER_FAST=0: exact ring search for every agent
+    bool fb_coop = true;       // ORCA_FB_COOP=0: thread-per-agent least-penetration stage
 
     // optional per-stage timing (orca_profile_stages)
     bool profiling = false;
@@ -149,9 +150,13 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::solve_bpt * C::solve_threads);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
+    e = cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::fb_bpt * (C::fb_threads / 32) * 16);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                C::fb_bpt * (C::fb_threads / 32) * 16);
+                                C::fb_bpt * (C::fb_threads / ORCA_GL));
 }
 
 extern "C" void orca_destroy(orca_sim *sim)
@@ -224,6 +229,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     }
     if (const char *r0 = getenv("ORCA_R0")) sim->r0_override = atoi(r0);
     if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
+    if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
     if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
@@ -627,14 +633,25 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state));
     sim->mark();
-    const int lanes = sim->fb_lanes;                          // active lanes per warp (<= 16)
-    const int fb_at = (C::fb_threads / 32) * lanes;           // agents per block per pass
-    const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + fb_at - 1) / fb_at));
-    k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * fb_at, st>>>(
-        sim->plan, P, lanes, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
-        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
-        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
-        sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state));
+    if (sim->fb_coop) {
+        const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
+        const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + ng - 1) / ng));
+        k_fallback_coop<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
+            sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+            reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
+            reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
+            sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state));
+    } else {
+        const int lanes = sim->fb_lanes;                          // active lanes per warp (<= 16)
+        const int fb_at = (C::fb_threads / 32) * lanes;           // agents per block per pass
+        const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + fb_at - 1) / fb_at));
+        k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * fb_at, st>>>(
+            sim->plan, P, lanes, reinterpret_cast<const S4 *>(sim->s_pv),
+            reinterpret_cast<const R4 *>(sim->s_dm), reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row,
+            sim->ids[a], sim->nb, sim->nb_cnt, reinterpret_cast<const S4 *>(sim->goalpref[a]),
+            reinterpret_cast<S4 *>(sim->pv[out_idx]), sim->arrived, sim->fq,
+            reinterpret_cast<const R4 *>(sim->fq_state));
+    }
     sim->mark();
     CKL(sim);
     sim->launches += 4;

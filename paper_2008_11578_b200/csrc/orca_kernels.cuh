@@ -613,6 +613,8 @@ __device__ __forceinline__ bool build_constraints(
     const int ci = (int)rc_i.y;
     const R tau = (R)P.tau, dt = (R)P.dt;
     const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
+    bool ok_all = true;
+#pragma unroll 2
     for (int pos = 0; pos < cnt; ++pos) {
         const int t = perm[pos * stride];
         const int j = nb[(size_t)t * P.stride + s];
@@ -620,15 +622,16 @@ __device__ __forceinline__ bool build_constraints(
         const typename Vec<S>::T2 rc_j = s_rc[j];
         const R rj = (R)((double)rc_j.x + P.half_margin);
         R ux, uy, nx, ny;
-        if (!vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, tau, dt,
-                        ux, uy, nx, ny)) {
-            // coincident neighbours have d2 == 0 and therefore lead the list; the
-            // reference reports the first one in rank order (_kernels.py:533-536)
-            bad_j = nb[s];
-            return false;
-        }
+        ok_all &= vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, tau, dt,
+                             ux, uy, nx, ny);
         const R f = rc_j.y != S(0) ? f1 : f0; // fmat[cls_i, cls_j], _kernels.py:537
         cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
+    }
+    if (!ok_all) {
+        // coincident neighbours have d2 == 0 and therefore lead the list; the reference
+        // reports the first one in rank order (_kernels.py:533-536)
+        bad_j = nb[s];
+        return false;
     }
     return true;
 }
@@ -753,6 +756,80 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
         least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry);
         integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
+    }
+}
+
+// Group-cooperative least-penetration stage: ORCA_GL (8) adjacent lanes per queued agent,
+// four agents per warp. The lanes share the agent's constraints through shared memory,
+// build them in parallel (one vo_exit per lane and round), and split every inner loop of
+// the stage (orca_math.cuh, g_* functions). Against k_fallback this cuts the warp
+// instructions per agent ~3x in dense crowds, where the stage dominates the step.
+template <typename S, typename R, int MAXN, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
+                const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
+                const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ s_row,
+                const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
+                const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
+                u8 *__restrict__ arrived, const int *__restrict__ fq,
+                const typename Vec<R>::T4 *__restrict__ fq_state)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typedef typename Vec<R>::T4 R4;
+    constexpr int NG = THREADS / ORCA_GL;             // agents (groups) per block and pass
+    const int g = threadIdx.x / ORCA_GL;              // group within the block
+    const int gl = threadIdx.x % ORCA_GL;             // lane within the group
+    const int gshift = (threadIdx.x & 31) - gl;       // first lane of the group within its warp
+    const unsigned gmask = ((1u << ORCA_GL) - 1u) << gshift;
+    R4 *sm_cons = reinterpret_cast<R4 *>(smem_raw);
+    R4 *sm_proj = sm_cons + MAXN * NG;
+    u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * NG);
+    u8 *sm_inv = sm_perm + MAXN * NG;
+
+    const int nq = plan->fq_count;
+    for (int q = blockIdx.x * NG + g; q < nq; q += gridDim.x * NG) {
+        const int s = fq[q];
+        const R4 st = fq_state[q];
+        const int row = s_row[s];
+        const int cnt = nb_cnt[s];
+        const typename Vec<S>::T4 me = s_pv[s];
+        const R4 dm = s_dm[s];
+        u8 *perm = sm_perm + g;
+        u8 *inv = sm_inv + g;
+        SmemCons<R> cons{sm_cons + g, NG};
+        SmemCons<R> proj{sm_proj + g, NG};
+
+        if (gl == 0) {
+            shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(P.frame, ids[row]));
+            for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * NG] * NG] = (u8)pos;
+        }
+        __syncwarp(gmask);
+        {   // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
+            const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
+            const typename Vec<S>::T2 rc_i = s_rc[s];
+            const R ri = (R)((double)rc_i.x + P.half_margin);
+            const int ci = (int)rc_i.y;
+            const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
+            for (int pos = gl; pos < cnt; pos += ORCA_GL) {
+                const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
+                const typename Vec<S>::T4 qv = s_pv[j];
+                const typename Vec<S>::T2 rc_j = s_rc[j];
+                const R rj = (R)((double)rc_j.x + P.half_margin);
+                R ux, uy, nx, ny;
+                vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, (R)P.tau,
+                           (R)P.dt, ux, uy, nx, ny);
+                const R f = rc_j.y != S(0) ? f1 : f0;
+                cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
+            }
+        }
+        __syncwarp(gmask);
+
+        SmemConsIdent<R> ident{sm_cons + g, inv, NG};
+        R rx, ry;
+        g_least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+            cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift);
+        if (gl == 0) integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
+        __syncwarp(gmask); // the group's shared memory is reused by the next queue entry
     }
 }
 

@@ -168,6 +168,14 @@ __device__ __forceinline__ bool vo_exit(R rpx, R rpy, R rvx, R rvy, R comb_r, R 
 
 #define ORCA_PARALLEL_EPS 1e-12
 
+// experiment switches (see profiles/): defaults are the measured-best variants
+#ifndef ORCA_LP1DIR_NOEXIT
+#define ORCA_LP1DIR_NOEXIT 0
+#endif
+#ifndef ORCA_PAIRS_UNROLLED
+#define ORCA_PAIRS_UNROLLED 1
+#endif
+
 // K:74-119. `zz` shifts every constraint point by -zz*normal (the z-relaxed set
 // of K:276-278); SHIFT=false compiles the shift out.
 template <typename R, bool SHIFT, typename V>
@@ -188,26 +196,47 @@ __device__ __forceinline__ bool lp1_target(const V &view, int i_pos, R zz, R cap
     R t_left = -pd - sq;
     R t_right = -pd + sq;
 
-    for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
-        R qx, qy, mx, my;
-        view.get(j_pos, qx, qy, mx, my);
-        if (SHIFT) {
+    if (!SHIFT) {
+        // Main LP (k_solve, all 32 lanes busy): no early exit inside the loop. The outcome
+        // does not depend on where the interval first becomes empty (t_left only grows,
+        // t_right only shrinks), and without exits the division chains of successive
+        // iterations overlap.
+        bool bad = false;
+#pragma unroll 4
+        for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
+            R qx, qy, mx, my;
+            view.get(j_pos, qx, qy, mx, my);
+            const R a = dx * mx + dy * my;
+            const R b = (qx - px) * mx + (qy - py) * my;
+            const bool par = R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS);
+            bad = bad || (par && b > R(0));
+            const R t = div_rn<R>(b, a); // unused when par
+            if (!par && a > R(0) && t > t_left) t_left = t;
+            if (!par && !(a > R(0)) && t < t_right) t_right = t;
+        }
+        if (bad || t_left > t_right) return false;
+    } else {
+        // Re-solve on the z-relaxed set (k_fallback, few lanes per warp): infeasibility is
+        // common here, so leaving at the first empty interval saves more than overlap gains.
+        for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
+            R qx, qy, mx, my;
+            view.get(j_pos, qx, qy, mx, my);
             qx = qx - zz * mx;
             qy = qy - zz * my;
+            const R a = dx * mx + dy * my;
+            const R b = (qx - px) * mx + (qy - py) * my;
+            if (R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS)) {
+                if (b > R(0)) return false;
+                continue;
+            }
+            const R t = div_rn<R>(b, a);
+            if (a > R(0)) {
+                if (t > t_left) t_left = t;
+            } else {
+                if (t < t_right) t_right = t;
+            }
+            if (t_left > t_right) return false;
         }
-        const R a = dx * mx + dy * my;
-        const R b = (qx - px) * mx + (qy - py) * my;
-        if (R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS)) {
-            if (b > R(0)) return false;
-            continue;
-        }
-        const R t = div_rn<R>(b, a);
-        if (a > R(0)) {
-            if (t > t_left) t_left = t;
-        } else {
-            if (t < t_right) t_right = t;
-        }
-        if (t_left > t_right) return false;
     }
     R t = (tx - px) * dx + (ty - py) * dy;
     if (t < t_left) t = t_left;
@@ -266,6 +295,22 @@ __device__ __forceinline__ bool lp1_dir(const P &proj, int upto, R cap, R ox, R 
     const R sq = sqrt_rn<R>(disc);
     R t_left = -pd - sq;
     R t_right = -pd + sq;
+#if ORCA_LP1DIR_NOEXIT
+    bool bad = false;
+#pragma unroll 4
+    for (int j = 0; j < upto; ++j) {
+        R qx, qy, mx, my;
+        proj.get(j, qx, qy, mx, my);
+        const R a = dx * mx + dy * my;
+        const R b = (qx - px) * mx + (qy - py) * my;
+        const bool par = R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS);
+        bad = bad || (par && b > R(0));
+        const R t = div_rn<R>(b, a); // unused when par
+        if (!par && a > R(0) && t > t_left) t_left = t;
+        if (!par && !(a > R(0)) && t < t_right) t_right = t;
+    }
+    if (bad || t_left > t_right) return false;
+#else
     for (int j = 0; j < upto; ++j) {
         R qx, qy, mx, my;
         proj.get(j, qx, qy, mx, my);
@@ -283,6 +328,7 @@ __device__ __forceinline__ bool lp1_dir(const P &proj, int upto, R cap, R ox, R 
         }
         if (t_left > t_right) return false;
     }
+#endif
     const R t = (dx * ox + dy * oy) > R(0) ? t_right : t_left;
     rx = px + t * dx;
     ry = py + t * dy;
@@ -326,19 +372,38 @@ __device__ __forceinline__ void lp3_minmax(const V &view, P &proj, int k, int be
         const R viol = (cpx - vx) * cnx + (cpy - vy) * cny;
         if (viol > dist) {
             int m = 0;
+#if ORCA_PAIRS_UNROLLED
+#pragma unroll 2
             for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
                 R jpx, jpy, jnx, jny;
                 view.get(j_pos, jpx, jpy, jnx, jny);
                 const R mx = jnx - cnx;
                 const R my = jny - cny;
                 const R ml2 = mx * mx + my * my;
-                if (ml2 < R(1e-24)) continue;
+                const R rhs = jpx * jnx + jpy * jny - cpx * cnx - cpy * cny;
+                const R ml = sqrt_rn<R>(ml2);
+                const R ppx = div_rn<R>(mx * rhs, ml2), ppy = div_rn<R>(my * rhs, ml2);
+                const R pnx = div_rn<R>(mx, ml), pny = div_rn<R>(my, ml);
+                if (!(ml2 < R(1e-24))) { // same normal: no half-plane induced (K:231-235)
+                    proj.set(m, ppx, ppy, pnx, pny);
+                    ++m;
+                }
+            }
+#else
+            for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
+                R jpx, jpy, jnx, jny;
+                view.get(j_pos, jpx, jpy, jnx, jny);
+                const R mx = jnx - cnx;
+                const R my = jny - cny;
+                const R ml2 = mx * mx + my * my;
+                if (ml2 < R(1e-24)) continue; // same normal: no half-plane induced (K:231-235)
                 const R rhs = jpx * jnx + jpy * jny - cpx * cnx - cpy * cny;
                 const R ml = sqrt_rn<R>(ml2);
                 proj.set(m, div_rn<R>(mx * rhs, ml2), div_rn<R>(my * rhs, ml2), div_rn<R>(mx, ml),
                          div_rn<R>(my, ml));
                 ++m;
             }
+#endif
             R nvx, nvy;
             if (lp2_dir<R, P>(proj, m, cap, cnx, cny, nvx, nvy)) {
                 vx = nvx;
@@ -372,6 +437,265 @@ __device__ __forceinline__ void least_penetration(const VS &shuf, const VI &iden
         int fail;
         R qx, qy;
         if (lp2_target<R, true, VI>(ident, k, zz, cap, wx, wy, fail, qx, qy)) {
+            rx = qx;
+            ry = qy;
+            return;
+        }
+        slack = slack * R(1e3) + R(1e-12) * (R(1) + z);
+    }
+    rx = vx;
+    ry = vy;
+}
+
+} // namespace orca
+
+// ---------------------------------------------------------------------------
+// Group-cooperative variants of the fallback stage: GL (= 8) adjacent lanes work on
+// ONE agent. The outer loops (constraint insertion order) stay sequential and are
+// executed redundantly by every lane of the group; the inner loops over earlier
+// constraints are split across the lanes and combined with shuffles. Nothing changes
+// numerically: each (i, j) term is evaluated by exactly the same operations, and the
+// combinations are max / min / any, which are exact and order-independent -- so the
+// FP64 build stays bit-identical to K:153-283.
+// ---------------------------------------------------------------------------
+
+namespace orca {
+
+#define ORCA_GL 8 // lanes per agent
+
+template <typename R> __device__ __forceinline__ R group_max(R v, unsigned gmask)
+{
+#pragma unroll
+    for (int o = ORCA_GL / 2; o > 0; o >>= 1) {
+        const R u = __shfl_xor_sync(gmask, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+
+template <typename R> __device__ __forceinline__ R group_min(R v, unsigned gmask)
+{
+#pragma unroll
+    for (int o = ORCA_GL / 2; o > 0; o >>= 1) {
+        const R u = __shfl_xor_sync(gmask, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+// K:74-119 with the j loop split over the group
+template <typename R, bool SHIFT, typename V>
+__device__ __forceinline__ bool g_lp1_target(const V &view, int i_pos, R zz, R cap, R tx, R ty, R &ox,
+                                             R &oy, int gl, unsigned gmask)
+{
+    R px, py, nx, ny;
+    view.get(i_pos, px, py, nx, ny);
+    if (SHIFT) {
+        px = px - zz * nx;
+        py = py - zz * ny;
+    }
+    const R dx = -ny, dy = nx;
+    const R pd = px * dx + py * dy;
+    const R disc = pd * pd + cap * cap - (px * px + py * py);
+    if (disc < R(0)) return false; // uniform over the group
+    const R sq = sqrt_rn<R>(disc);
+    R t_left = -pd - sq;
+    R t_right = -pd + sq;
+    bool bad = false;
+    for (int j_pos = gl; j_pos < i_pos; j_pos += ORCA_GL) {
+        R qx, qy, mx, my;
+        view.get(j_pos, qx, qy, mx, my);
+        if (SHIFT) {
+            qx = qx - zz * mx;
+            qy = qy - zz * my;
+        }
+        const R a = dx * mx + dy * my;
+        const R b = (qx - px) * mx + (qy - py) * my;
+        const bool par = R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS);
+        bad = bad || (par && b > R(0));
+        const R t = div_rn<R>(b, a); // unused when par
+        if (!par && a > R(0) && t > t_left) t_left = t;
+        if (!par && !(a > R(0)) && t < t_right) t_right = t;
+    }
+    bad = (__ballot_sync(gmask, bad) & gmask) != 0u;
+    t_left = group_max<R>(t_left, gmask);
+    t_right = group_min<R>(t_right, gmask);
+    if (bad || t_left > t_right) return false;
+    R t = (tx - px) * dx + (ty - py) * dy;
+    if (t < t_left) t = t_left;
+    else if (t > t_right) t = t_right;
+    ox = px + t * dx;
+    oy = py + t * dy;
+    return true;
+}
+
+// K:122-146
+template <typename R, bool SHIFT, typename V>
+__device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, R tx, R ty, int &fail_pos,
+                                             R &vx, R &vy, int gl, unsigned gmask)
+{
+    const R t2 = tx * tx + ty * ty;
+    if (t2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(t2));
+        vx = tx * s;
+        vy = ty * s;
+    } else {
+        vx = tx;
+        vy = ty;
+    }
+    for (int i_pos = 0; i_pos < k; ++i_pos) {
+        R px, py, nx, ny;
+        view.get(i_pos, px, py, nx, ny);
+        if (SHIFT) {
+            px = px - zz * nx;
+            py = py - zz * ny;
+        }
+        if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+            R nvx, nvy;
+            if (!g_lp1_target<R, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy, gl, gmask)) {
+                fail_pos = i_pos;
+                return false;
+            }
+            vx = nvx;
+            vy = nvy;
+        }
+    }
+    fail_pos = -1;
+    return true;
+}
+
+// K:153-190
+template <typename R, typename P>
+__device__ __forceinline__ bool g_lp1_dir(const P &proj, int upto, R cap, R ox, R oy, R &rx, R &ry, int gl,
+                                          unsigned gmask)
+{
+    R px, py, nx, ny;
+    proj.get(upto, px, py, nx, ny);
+    const R dx = -ny, dy = nx;
+    const R pd = px * dx + py * dy;
+    const R disc = pd * pd + cap * cap - (px * px + py * py);
+    if (disc < R(0)) return false;
+    const R sq = sqrt_rn<R>(disc);
+    R t_left = -pd - sq;
+    R t_right = -pd + sq;
+    bool bad = false;
+    for (int j = gl; j < upto; j += ORCA_GL) {
+        R qx, qy, mx, my;
+        proj.get(j, qx, qy, mx, my);
+        const R a = dx * mx + dy * my;
+        const R b = (qx - px) * mx + (qy - py) * my;
+        const bool par = R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS);
+        bad = bad || (par && b > R(0));
+        const R t = div_rn<R>(b, a);
+        if (!par && a > R(0) && t > t_left) t_left = t;
+        if (!par && !(a > R(0)) && t < t_right) t_right = t;
+    }
+    bad = (__ballot_sync(gmask, bad) & gmask) != 0u;
+    t_left = group_max<R>(t_left, gmask);
+    t_right = group_min<R>(t_right, gmask);
+    if (bad || t_left > t_right) return false;
+    const R t = (dx * ox + dy * oy) > R(0) ? t_right : t_left;
+    rx = px + t * dx;
+    ry = py + t * dy;
+    return true;
+}
+
+// K:193-205
+template <typename R, typename P>
+__device__ __forceinline__ bool g_lp2_dir(const P &proj, int m, R cap, R ox, R oy, R &rx, R &ry, int gl,
+                                          unsigned gmask)
+{
+    R vx = cap * ox, vy = cap * oy;
+    for (int i = 0; i < m; ++i) {
+        R px, py, nx, ny;
+        proj.get(i, px, py, nx, ny);
+        if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+            R nvx, nvy;
+            if (!g_lp1_dir<R, P>(proj, i, cap, ox, oy, nvx, nvy, gl, gmask)) {
+                rx = vx;
+                ry = vy;
+                return false;
+            }
+            vx = nvx;
+            vy = nvy;
+        }
+    }
+    rx = vx;
+    ry = vy;
+    return true;
+}
+
+// K:212-251. The projected constraints of one (c, j<i_pos) sweep are built GL at a time
+// and compacted in ascending j (ballot rank), which is the order K:226-243 appends them.
+template <typename R, typename V, typename P>
+__device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int begin, R cap, R &vx, R &vy,
+                                             R &z, int gl, unsigned gmask, int gshift)
+{
+    R dist = R(0);
+    for (int i_pos = begin; i_pos < k; ++i_pos) {
+        R cpx, cpy, cnx, cny;
+        view.get(i_pos, cpx, cpy, cnx, cny);
+        const R viol = (cpx - vx) * cnx + (cpy - vy) * cny;
+        if (viol > dist) {
+            int m = 0;
+            for (int j0 = 0; j0 < i_pos; j0 += ORCA_GL) {
+                const int j_pos = j0 + gl;
+                bool valid = false;
+                R ppx = R(0), ppy = R(0), pnx = R(0), pny = R(0);
+                if (j_pos < i_pos) {
+                    R jpx, jpy, jnx, jny;
+                    view.get(j_pos, jpx, jpy, jnx, jny);
+                    const R mx = jnx - cnx;
+                    const R my = jny - cny;
+                    const R ml2 = mx * mx + my * my;
+                    if (!(ml2 < R(1e-24))) {
+                        const R rhs = jpx * jnx + jpy * jny - cpx * cnx - cpy * cny;
+                        const R ml = sqrt_rn<R>(ml2);
+                        ppx = div_rn<R>(mx * rhs, ml2);
+                        ppy = div_rn<R>(my * rhs, ml2);
+                        pnx = div_rn<R>(mx, ml);
+                        pny = div_rn<R>(my, ml);
+                        valid = true;
+                    }
+                }
+                const unsigned bits = (__ballot_sync(gmask, valid) & gmask) >> gshift; // GL bits
+                if (valid) proj.set(m + __popc(bits & ((1u << gl) - 1u)), ppx, ppy, pnx, pny);
+                m += __popc(bits);
+            }
+            __syncwarp(gmask); // projected constraints visible to the whole group
+            R nvx, nvy;
+            if (g_lp2_dir<R, P>(proj, m, cap, cnx, cny, nvx, nvy, gl, gmask)) {
+                vx = nvx;
+                vy = nvy;
+            }
+            dist = (cpx - vx) * cnx + (cpy - vy) * cny;
+            if (dist < R(0)) dist = R(0);
+            __syncwarp(gmask); // everyone is done reading before the next sweep overwrites
+        }
+    }
+    z = dist;
+}
+
+// K:254-283
+template <typename R, typename VS, typename VI, typename P>
+__device__ __forceinline__ void g_least_penetration(const VS &shuf, const VI &ident, P &proj, int k, int begin,
+                                                    R cap, R wx, R wy, R &rx, R &ry, int gl, unsigned gmask,
+                                                    int gshift)
+{
+    const R w2 = wx * wx + wy * wy;
+    if (w2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(w2));
+        wx = wx * s;
+        wy = wy * s;
+    }
+    R vx = wx, vy = wy, z;
+    g_lp3_minmax<R, VS, P>(shuf, proj, k, begin, cap, vx, vy, z, gl, gmask, gshift);
+    R slack = R(0);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const R zz = z + slack;
+        int fail;
+        R qx, qy;
+        if (g_lp2_target<R, true, VI>(ident, k, zz, cap, wx, wy, fail, qx, qy, gl, gmask)) {
             rx = qx;
             ry = qy;
             return;
