@@ -196,10 +196,17 @@ def run_ours(args):
     if not torch.cuda.is_available():
         raise RuntimeError("bench.py needs a CUDA device; there is no CPU fallback")
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or os.environ.get("ORCA_BENCH_FORCE_STRIPS"):
+        # the strip-decomposed path; ORCA_BENCH_FORCE_STRIPS=1 runs it with a single rank
+        # (no neighbours) to smoke-test the NCCL plumbing on a one-GPU box
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2008_11578_b200.parallel import strips
-        return strips.run_bench(args, rank, world, local)
+        try:
+            return strips.run_bench(args, rank, world, local)
+        finally:
+            dist.destroy_process_group()
 
     state, cfg, wl = build_workload(args.workload)
     n = state.active_count

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "orca_common.cuh"
+#include "orca_sortnet.inc"
 
 namespace orca {
 
@@ -347,6 +348,34 @@ template <int MAXN> struct TopK {
         return true;
     }
 
+    // compare-exchange of slots a < b under the (d2, id) order; sentinels (idx < 0) never tie-break
+    __device__ __forceinline__ void cex(int a, int b, const int *__restrict__ s_row, const i64 *__restrict__ ids)
+    {
+        bool sw = key[b] < key[a];
+        if (key[b] == key[a] && idx[a] >= 0 && idx[b] >= 0) sw = ids[s_row[idx[b]]] < ids[s_row[idx[a]]];
+        const double ka = key[a], kb = key[b];
+        const int ia = idx[a], ib = idx[b];
+        key[a] = sw ? kb : ka;
+        key[b] = sw ? ka : kb;
+        idx[a] = sw ? ib : ia;
+        idx[b] = sw ? ia : ib;
+    }
+
+    // Batcher's merge-exchange network over all MAXN slots (63 compare-exchanges for 16,
+    // 191 for 32; written out by scripts/gen_sortnet.py so every slot stays a register).
+    // Used by the fast pass to order its first max_n candidates at once instead of max_n
+    // shifting insertions.
+    __device__ __forceinline__ void sort_all(const int *__restrict__ s_row, const i64 *__restrict__ ids)
+    {
+#define CEX(a, b) cex(a, b, s_row, ids);
+        if constexpr (MAXN == 16) {
+            ORCA_SORTNET_16
+        } else {
+            ORCA_SORTNET_32
+        }
+#undef CEX
+    }
+
     // slot-major neighbour table + count + next step's radius hint
     __device__ __forceinline__ void store(int s, int row, int max_n, int stride, int *__restrict__ nb,
                                           u8 *__restrict__ nb_cnt, float *__restrict__ hint) const
@@ -433,7 +462,27 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
     TopK<MAXN> top;
     top.init(max_n);
     if (ok) {
-        for (int e = 0; e < nbuf; ++e) {
+        // the first max_n buffered candidates: exact keys straight into the slots, one
+        // sorting network; self and out-of-range candidates become +inf / -1 entries
+        const int off = MAXN - max_n;
+#pragma unroll
+        for (int t = 0; t < MAXN; ++t) {
+            const int e = t - off;
+            if (e >= 0 && e < nbuf) {
+                const int s2 = my_buf[e * 128];
+                const typename Vec<R>::T2 q = s_xy[s2];
+                const double dx = (double)q.x - mx, dy = (double)q.y - my;
+                const double d2 = dx * dx + dy * dy;
+                if (s2 != s && !(d2 > rad2)) {
+                    top.key[t] = d2;
+                    top.idx[t] = s2;
+                    ++top.cnt;
+                }
+            }
+        }
+        top.sort_all(s_row, ids);
+        // the rest (a handful: the threshold is tight) by shifting insertion
+        for (int e = max_n; e < nbuf; ++e) {
             const int s2 = my_buf[e * 128];
             const typename Vec<R>::T2 q = s_xy[s2];
             const double dx = (double)q.x - mx, dy = (double)q.y - my;
@@ -599,7 +648,9 @@ __device__ __forceinline__ void shuffle_smem(u8 *perm, int stride, int k, u64 se
 }
 
 // Build the ORCA half-planes of agent s into `cons` in SHUFFLED order
-// (_kernels.py:525-541). Returns false on exactly coincident centres.
+// (_kernels.py:525-541). Returns false on exactly coincident centres. (Walking the
+// neighbour ranks and scattering to the inverse permutation instead was measured 6 %
+// slower, profiles/r01_notes.md.)
 template <typename S, typename R>
 __device__ __forceinline__ bool build_constraints(
     int s, int cnt, const StepParams &P, const typename Vec<S>::T4 *__restrict__ s_pv,
@@ -678,7 +729,6 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
 
     shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
-
     int bad_j = -1;
     if (!build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, THREADS, cons, bad_j)) {
         // _kernels.py:542-547 + engine.py:239-245

@@ -461,7 +461,9 @@ __device__ __forceinline__ void least_penetration(const VS &shuf, const VI &iden
 
 namespace orca {
 
-#define ORCA_GL 8 // lanes per agent
+#ifndef ORCA_GL
+#define ORCA_GL 4 // lanes per agent (4 measured best for dense crowds, 8 for sparse)
+#endif
 
 template <typename R> __device__ __forceinline__ R group_max(R v, unsigned gmask)
 {
