@@ -75,6 +75,24 @@ struct orca_sim {
     int fb_lanes = 8;          // ORCA_FB_LANES: lanes per warp that take a fallback agent
     bool gather_fast = true;   // ORCA_GATHER_FAST=0: exact ring search for every agent
     bool fb_coop = true;       // ORCA_FB_COOP=0: thread-per-agent least-penetration stage
+    bool use_graph = true;     // ORCA_GRAPH=0: launch the step's kernels one by one
+
+    // CUDA graphs of one whole step, keyed by everything the launch sequence depends on
+    struct StepGraph {
+        int cur, acur;             // key: buffer rotation state before the step
+        int64_t n_bound;           // key: launch grid sizes
+        bool had_bins;             // key: sorted arrays already valid (metrics mode)
+        cudaGraphExec_t exec;
+        int new_cur, new_acur, new_pre; // host state after the step
+        bool leaves_bins;
+        int64_t launches;
+    };
+    std::vector<StepGraph> graphs;
+    void drop_graphs()
+    {
+        for (auto &g : graphs) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+    }
 
     // optional per-stage timing (orca_profile_stages)
     bool profiling = false;
@@ -198,6 +216,7 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->plan);
     cudaFree(sim->stg);
     cudaFree(sim->dbg);
+    sim->drop_graphs();
     for (cudaEvent_t e : sim->ev_pool) cudaEventDestroy(e);
     if (sim->h_plan) cudaFreeHost(sim->h_plan);
     if (sim->own_stream) cudaStreamDestroy(sim->own_stream);
@@ -230,6 +249,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     if (const char *r0 = getenv("ORCA_R0")) sim->r0_override = atoi(r0);
     if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
     if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
+    if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
     if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
@@ -301,6 +321,7 @@ extern "C" int orca_set_stream(orca_sim *sim, void *cuda_stream)
     CK(sim, cudaSetDevice(sim->device));
     CK(sim, cudaStreamSynchronize(sim->stream));
     sim->stream = cuda_stream ? reinterpret_cast<cudaStream_t>(cuda_stream) : sim->own_stream;
+    sim->drop_graphs();
     return ORCA_OK;
 }
 
@@ -318,6 +339,7 @@ extern "C" int orca_set_params(orca_sim *sim, const orca_params *p)
     if (p->max_neighbors > ORCA_MAX_NEIGHBORS)
         return fail(sim, ORCA_EUNSUPPORTED, "max_neighbors %d exceeds ORCA_MAX_NEIGHBORS (%d)",
                     p->max_neighbors, ORCA_MAX_NEIGHBORS);
+    if (!sim->have_params || memcmp(&sim->params, p, sizeof(orca_params)) != 0) sim->drop_graphs();
     sim->params = *p;
     sim->have_params = true;
     sim->binned_frame = -1;
@@ -437,6 +459,8 @@ extern "C" int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const dou
     CK(sim, cudaSetDevice(sim->device));
     sim->frame = frame;
     sim->binned_frame = -1;
+    k_set_frame<<<1, 1, 0, sim->stream>>>(sim->plan, frame);
+    CKL(sim);
     if (n == 0) return ORCA_OK;
     return sim->precision != ORCA_F64 ? upload_pv_impl<float>(sim, n, positions, velocities)
                                       : upload_pv_impl<double>(sim, n, positions, velocities);
@@ -567,7 +591,6 @@ static StepParams make_params(const orca_sim *sim)
     for (int i = 0; i < 4; ++i) P.fmat[i] = p.fmat[i];
     P.max_n = p.max_neighbors;
     P.stride = (int)(sim->capacity > 0 ? sim->capacity : 1);
-    P.frame = sim->frame;
     P.max_cells = (int)std::min<int64_t>(sim->max_cells, 2 * sim->n_bound + 1024);
     P.occ_target = sim->occ_target;
     P.r0_override = sim->r0_override;
@@ -658,10 +681,10 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     return ORCA_OK;
 }
 
-__global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids, i64 frame_new)
+__global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids)
 {
     if (plan->err_pair != ORCA_NO_ERR && plan->err_frame < 0) {
-        plan->err_frame = frame_new;
+        plan->err_frame = plan->frame + 1; // the reference names the frame being computed
         plan->err_id_i = ids[(unsigned)(plan->err_pair >> 32)];
         plan->err_id_j = ids[(unsigned)(plan->err_pair & 0xFFFFFFFFu)];
     }
@@ -721,7 +744,7 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     k_begin_step<<<1, 1, 0, sim->stream>>>(sim->plan);
     sim->launches += 1;
     if (n == 0) { // engine.py:202-209
-        k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->frame + 1, sim->params.remove_arrivals);
+        k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals);
         CKL(sim);
         sim->launches += 1;
         for (int i = 0; i < ORCA_N_STAGES; ++i) sim->mark();
@@ -736,8 +759,8 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     const int out_idx = (sim->cur + 1) % 3;
     rc = P.max_n <= 16 ? solve_stage<S, R, 16>(sim, P, out_idx) : solve_stage<S, R, 32>(sim, P, out_idx);
     if (rc) return rc;
-    k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur], sim->frame + 1);
-    k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->frame + 1, sim->params.remove_arrivals);
+    k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur]);
+    k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals);
     CKL(sim);
     sim->launches += 2;
     sim->pre = sim->cur;
@@ -767,17 +790,79 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     return ORCA_OK;
 }
 
+static int step_plain(orca_sim *sim)
+{
+    switch (sim->precision) {
+    case ORCA_F32: return step_impl<float, float>(sim);
+    case ORCA_MIXED: return step_impl<float, double>(sim);
+    default: return step_impl<double, double>(sim);
+    }
+}
+
+// Replay (or capture on first use) the CUDA graph of one step. The launch sequence of a
+// step depends only on the buffer rotation state, the launch bound n_bound and whether
+// the bins are already valid; everything else the kernels need (n, frame, grid plan,
+// queues) lives in device memory.
+static int step_graphed(orca_sim *sim)
+{
+    const bool had_bins = sim->binned_frame == sim->frame;
+    for (auto &g : sim->graphs) {
+        if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins) {
+            CK(sim, cudaGraphLaunch(g.exec, sim->stream));
+            sim->n_pre = sim->n_bound;
+            sim->pre = g.new_pre;
+            sim->cur = g.new_cur;
+            sim->acur = g.new_acur;
+            sim->frame += 1;
+            sim->binned_frame = g.leaves_bins ? sim->frame : -1;
+            sim->launches += g.launches;
+            return ORCA_OK;
+        }
+    }
+    if (sim->graphs.size() >= 16) sim->drop_graphs(); // n_bound kept shrinking: start over
+    orca_sim::StepGraph g{};
+    g.cur = sim->cur;
+    g.acur = sim->acur;
+    g.n_bound = sim->n_bound;
+    g.had_bins = had_bins;
+    const int64_t l0 = sim->launches;
+    if (cudaStreamBeginCapture(sim->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+        cudaGetLastError();
+        return step_plain(sim);
+    }
+    const int rc = step_plain(sim); // records the launches, advances the host-side state
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(sim->stream, &graph);
+    if (rc != ORCA_OK || e != cudaSuccess || !graph) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        sim->use_graph = false; // fall back to plain launches for good
+        return rc != ORCA_OK ? rc : fail(sim, ORCA_ECUDA, "CUDA graph capture failed: %s", cudaGetErrorString(e));
+    }
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        sim->use_graph = false;
+        return fail(sim, ORCA_ECUDA, "cudaGraphInstantiate failed: %s", cudaGetErrorString(e));
+    }
+    g.new_cur = sim->cur;
+    g.new_acur = sim->acur;
+    g.new_pre = sim->pre;
+    g.leaves_bins = sim->binned_frame == sim->frame;
+    g.launches = sim->launches - l0;
+    sim->graphs.push_back(g);
+    CK(sim, cudaGraphLaunch(g.exec, sim->stream)); // the capture itself executed nothing
+    return ORCA_OK;
+}
+
 extern "C" int orca_step(orca_sim *sim)
 {
     if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_step: sim is NULL");
     if (!sim->loaded) return fail(sim, ORCA_EINVAL, "orca_step: no state uploaded");
     if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_step: orca_set_params was not called");
     CK(sim, cudaSetDevice(sim->device));
-    switch (sim->precision) {
-    case ORCA_F32: return step_impl<float, float>(sim);
-    case ORCA_MIXED: return step_impl<float, double>(sim);
-    default: return step_impl<double, double>(sim);
-    }
+    if (sim->use_graph && !sim->profiling && sim->ghost_bound == 0 && sim->n_bound > 0) return step_graphed(sim);
+    return step_plain(sim);
 }
 
 extern "C" int orca_profile_stages(orca_sim *sim, int enable)

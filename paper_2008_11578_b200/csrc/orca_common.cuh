@@ -55,7 +55,6 @@ struct StepParams {
     double fmat[4];
     int max_n;
     int stride;  // leading dimension of the slot-major neighbour table
-    i64 frame;   // pre-step frame index (seed input, engine.py:233)
     int max_cells;
     int r0_override; // > 0: force the first ring radius (experiments)
     double occ_target;

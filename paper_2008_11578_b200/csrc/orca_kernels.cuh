@@ -728,7 +728,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     u8 *perm = sm_perm + threadIdx.x;
     SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
 
-    shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(P.frame, ids[row]));
+    shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(plan->frame, ids[row]));
     int bad_j = -1;
     if (!build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, THREADS, cons, bad_j)) {
         // _kernels.py:542-547 + engine.py:239-245
@@ -796,7 +796,7 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
         SmemCons<R> cons{sm_cons + at, AT};
         SmemCons<R> proj{sm_proj + at, AT};
 
-        shuffle_smem<MAXN>(perm, AT, cnt, problem_seed(P.frame, ids[row]));
+        shuffle_smem<MAXN>(perm, AT, cnt, problem_seed(plan->frame, ids[row]));
         for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * AT] * AT] = (u8)pos;
         int bad_j;
         build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, AT, cons, bad_j);
@@ -850,7 +850,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         SmemCons<R> proj{sm_proj + g, NG};
 
         if (gl == 0) {
-            shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(P.frame, ids[row]));
+            shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
             for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * NG] * NG] = (u8)pos;
         }
         __syncwarp(gmask);
@@ -887,9 +887,11 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
 // K4: finish, arrival removal
 // ---------------------------------------------------------------------------
 
-__global__ void k_finish(GridPlan *plan, i64 frame_new, int remove_arrivals)
+// frames completed += 1 (the frame index lives on the device so that a captured CUDA
+// graph of the step can be replayed without patching kernel arguments)
+__global__ void k_finish(GridPlan *plan, int remove_arrivals)
 {
-    plan->frame = frame_new;
+    plan->frame = plan->frame + 1;
     if (!remove_arrivals) {
         plan->removed = 0;
         plan->n_after = plan->n_owned;
@@ -1035,6 +1037,8 @@ __global__ void k_after_append(GridPlan *plan, int count, int ghost)
 }
 
 __global__ void k_drop_ghosts(GridPlan *plan) { plan->n = plan->n_owned; }
+
+__global__ void k_set_frame(GridPlan *plan, i64 frame) { plan->frame = frame; }
 
 // ---------------------------------------------------------------------------
 // metrics: min separation / collision count (_kernels.py:559-589) on the
