@@ -1121,6 +1121,8 @@ struct orca_lp_batch {
     int *perm = nullptr;
     double *out_v = nullptr;
     i64 *out_status = nullptr, *out_failed = nullptr;
+    int *fq = nullptr, *fq_count = nullptr; // problems queued for the least-penetration stage
+    void *fq_state = nullptr;
 };
 
 extern "C" void orca_lp_batch_destroy(orca_lp_batch *b)
@@ -1137,6 +1139,9 @@ extern "C" void orca_lp_batch_destroy(orca_lp_batch *b)
     cudaFree(b->out_v);
     cudaFree(b->out_status);
     cudaFree(b->out_failed);
+    cudaFree(b->fq);
+    cudaFree(b->fq_count);
+    cudaFree(b->fq_state);
     if (b->own_stream) cudaStreamDestroy(b->own_stream);
     delete b;
 }
@@ -1220,6 +1225,9 @@ extern "C" int orca_lp_batch_create(orca_lp_batch **out, int device, int precisi
     CKB(dalloc(&b->out_v, 2 * nn));
     CKB(dalloc(&b->out_status, nn));
     CKB(dalloc(&b->out_failed, nn));
+    CKB(dalloc(&b->fq, nn));
+    CKB(dalloc(&b->fq_count, 1));
+    CKB(cudaMalloc(&b->fq_state, nn * 4 * rs));
     CKB(cudaMemcpyAsync(b->coff, coff, sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, b->stream));
     if (n) CKB(cudaMemcpyAsync(b->seeds, seeds, sizeof(u64) * n, cudaMemcpyHostToDevice, b->stream));
     CKB(precision == ORCA_F32 ? lp_pack<float>(b, cpts, cnrm, tgt, caps) : lp_pack<double>(b, cpts, cnrm, tgt, caps));
@@ -1242,14 +1250,28 @@ extern "C" int orca_lp_batch_solve(orca_lp_batch *b)
     if (!b) return fail(nullptr, ORCA_EINVAL, "orca_lp_batch_solve: NULL batch");
     CK(nullptr, cudaSetDevice(b->device));
     if (b->n == 0) return ORCA_OK;
+    if (b->n > 0x7FFFFFFF) return fail(nullptr, ORCA_EUNSUPPORTED, "orca_lp_batch_solve: more than 2^31-1 problems");
+    CK(nullptr, cudaMemsetAsync(b->fq_count, 0, sizeof(int), b->stream));
+    const int fb_ng = 128 / ORCA_LP_GL; // problems per block and pass
+    const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (b->n + fb_ng - 1) / fb_ng));
     if (b->precision == ORCA_F32) {
         k_lp_batch<float><<<grid_for(b->n, 128), 128, 0, b->stream>>>(
             b->n, b->coff, reinterpret_cast<const float4 *>(b->cons), reinterpret_cast<const float4 *>(b->prob),
-            b->seeds, b->perm, reinterpret_cast<float4 *>(b->proj), b->out_v, b->out_status, b->out_failed);
+            b->seeds, b->perm, b->out_v, b->out_status, b->out_failed, b->fq_count, b->fq,
+            reinterpret_cast<float4 *>(b->fq_state));
+        k_lp_batch_fallback<float><<<fb_blocks, 128, 0, b->stream>>>(
+            b->fq_count, b->fq, reinterpret_cast<const float4 *>(b->fq_state), b->coff,
+            reinterpret_cast<const float4 *>(b->cons), reinterpret_cast<const float4 *>(b->prob), b->perm,
+            reinterpret_cast<float4 *>(b->proj), b->out_v);
     } else {
         k_lp_batch<double><<<grid_for(b->n, 128), 128, 0, b->stream>>>(
             b->n, b->coff, reinterpret_cast<const double4 *>(b->cons), reinterpret_cast<const double4 *>(b->prob),
-            b->seeds, b->perm, reinterpret_cast<double4 *>(b->proj), b->out_v, b->out_status, b->out_failed);
+            b->seeds, b->perm, b->out_v, b->out_status, b->out_failed, b->fq_count, b->fq,
+            reinterpret_cast<double4 *>(b->fq_state));
+        k_lp_batch_fallback<double><<<fb_blocks, 128, 0, b->stream>>>(
+            b->fq_count, b->fq, reinterpret_cast<const double4 *>(b->fq_state), b->coff,
+            reinterpret_cast<const double4 *>(b->cons), reinterpret_cast<const double4 *>(b->prob), b->perm,
+            reinterpret_cast<double4 *>(b->proj), b->out_v);
     }
     CKL(nullptr);
     return ORCA_OK;

@@ -876,7 +876,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
 
         SmemConsIdent<R> ident{sm_cons + g, inv, NG};
         R rx, ry;
-        g_least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+        g_least_penetration<R, ORCA_GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift);
         if (gl == 0) integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
         __syncwarp(gmask); // the group's shared memory is reused by the next queue entry

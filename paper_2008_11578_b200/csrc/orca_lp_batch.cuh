@@ -67,14 +67,17 @@ k_lp_pack_problems(i64 n, const double *__restrict__ tgt, const double *__restri
     prob[i] = mk4((R)tgt[2 * i], (R)tgt[2 * i + 1], (R)caps[i], R(0));
 }
 
-// One thread per problem; per-problem scratch (order, projected constraints)
-// lives in global memory at the problem's own CSR offsets, so any k works.
+// Main pass: one thread per problem, shuffled incremental LP (K:290-299). Per-problem
+// scratch (order, projected constraints) lives in global memory at the problem's own
+// CSR offsets, so any k works. Infeasible problems are queued with the state the
+// least-penetration stage starts from.
 template <typename R>
 __global__ void __launch_bounds__(128)
 k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__restrict__ cons,
            const typename Vec<R>::T4 *__restrict__ prob, const u64 *__restrict__ seeds,
-           int *__restrict__ perm_scratch, typename Vec<R>::T4 *__restrict__ proj_scratch,
-           double *__restrict__ out_v, i64 *__restrict__ out_status, i64 *__restrict__ out_failed)
+           int *__restrict__ perm_scratch, double *__restrict__ out_v, i64 *__restrict__ out_status,
+           i64 *__restrict__ out_failed, int *__restrict__ fq_count, int *__restrict__ fq,
+           typename Vec<R>::T4 *__restrict__ fq_state)
 {
     const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -105,15 +108,51 @@ k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__res
         out_failed[i] = -1;
         return;
     }
-    GlobalIdent<R> ident{cons + lo};
-    GlobalProj<R> proj{proj_scratch + lo};
-    R rx, ry;
-    least_penetration<R, GlobalShuf<R>, GlobalIdent<R>, GlobalProj<R>>(shuf, ident, proj, k, fail_pos,
-                                                                     pr.z, vx, vy, rx, ry);
-    out_v[2 * i] = (double)rx;
-    out_v[2 * i + 1] = (double)ry;
     out_status[i] = 1;
     out_failed[i] = perm[fail_pos];
+    const int q = atomicAdd(fq_count, 1);
+    fq[q] = (int)i;
+    fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
+}
+
+// Least-penetration stage of the queued problems, ORCA_GL lanes per problem (see
+// k_fallback_coop): the lanes split the loops over earlier constraints and combine with
+// exact max / min / any shuffles, so the FP64 build stays bit-identical to K:254-283.
+#ifndef ORCA_LP_GL
+#define ORCA_LP_GL 16 // lanes per queued problem: k reaches 64 here, against 16 in the step
+#endif
+
+template <typename R>
+__global__ void __launch_bounds__(128)
+k_lp_batch_fallback(const int *__restrict__ fq_count, const int *__restrict__ fq,
+                    const typename Vec<R>::T4 *__restrict__ fq_state, const i64 *__restrict__ coff,
+                    const typename Vec<R>::T4 *__restrict__ cons, const typename Vec<R>::T4 *__restrict__ prob,
+                    const int *__restrict__ perm_scratch, typename Vec<R>::T4 *__restrict__ proj_scratch,
+                    double *__restrict__ out_v)
+{
+    constexpr int GL = ORCA_LP_GL;
+    constexpr int NG = 128 / GL;
+    const int g = threadIdx.x / GL, gl = threadIdx.x % GL;
+    const int gshift = (threadIdx.x & 31) - gl;
+    const unsigned gmask = (GL == 32 ? 0xFFFFFFFFu : ((1u << GL) - 1u)) << gshift;
+    const int nq = *fq_count;
+    for (int q = blockIdx.x * NG + g; q < nq; q += gridDim.x * NG) {
+        const int i = fq[q];
+        const typename Vec<R>::T4 st = fq_state[q];
+        const i64 lo = coff[i];
+        const int k = (int)(coff[i + 1] - lo);
+        const typename Vec<R>::T4 pr = prob[i];
+        GlobalShuf<R> shuf{cons + lo, perm_scratch + lo};
+        GlobalIdent<R> ident{cons + lo};
+        GlobalProj<R> proj{proj_scratch + lo};
+        R rx, ry;
+        g_least_penetration<R, GL, GlobalShuf<R>, GlobalIdent<R>, GlobalProj<R>>(
+            shuf, ident, proj, k, (int)st.z, pr.z, st.x, st.y, rx, ry, gl, gmask, gshift);
+        if (gl == 0) {
+            out_v[2 * (i64)i] = (double)rx;
+            out_v[2 * (i64)i + 1] = (double)ry;
+        }
+    }
 }
 
 // ---- taps -------------------------------------------------------------------

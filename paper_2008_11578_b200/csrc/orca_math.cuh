@@ -462,23 +462,23 @@ __device__ __forceinline__ void least_penetration(const VS &shuf, const VI &iden
 namespace orca {
 
 #ifndef ORCA_GL
-#define ORCA_GL 4 // lanes per agent (4 measured best for dense crowds, 8 for sparse)
+#define ORCA_GL 4 // lanes per agent in the step (4 measured best for dense crowds, 8 for sparse)
 #endif
 
-template <typename R> __device__ __forceinline__ R group_max(R v, unsigned gmask)
+template <typename R, int GL> __device__ __forceinline__ R group_max(R v, unsigned gmask)
 {
 #pragma unroll
-    for (int o = ORCA_GL / 2; o > 0; o >>= 1) {
+    for (int o = GL / 2; o > 0; o >>= 1) {
         const R u = __shfl_xor_sync(gmask, v, o);
         v = u > v ? u : v;
     }
     return v;
 }
 
-template <typename R> __device__ __forceinline__ R group_min(R v, unsigned gmask)
+template <typename R, int GL> __device__ __forceinline__ R group_min(R v, unsigned gmask)
 {
 #pragma unroll
-    for (int o = ORCA_GL / 2; o > 0; o >>= 1) {
+    for (int o = GL / 2; o > 0; o >>= 1) {
         const R u = __shfl_xor_sync(gmask, v, o);
         v = u < v ? u : v;
     }
@@ -486,7 +486,7 @@ template <typename R> __device__ __forceinline__ R group_min(R v, unsigned gmask
 }
 
 // K:74-119 with the j loop split over the group
-template <typename R, bool SHIFT, typename V>
+template <typename R, int GL, bool SHIFT, typename V>
 __device__ __forceinline__ bool g_lp1_target(const V &view, int i_pos, R zz, R cap, R tx, R ty, R &ox,
                                              R &oy, int gl, unsigned gmask)
 {
@@ -504,7 +504,7 @@ __device__ __forceinline__ bool g_lp1_target(const V &view, int i_pos, R zz, R c
     R t_left = -pd - sq;
     R t_right = -pd + sq;
     bool bad = false;
-    for (int j_pos = gl; j_pos < i_pos; j_pos += ORCA_GL) {
+    for (int j_pos = gl; j_pos < i_pos; j_pos += GL) {
         R qx, qy, mx, my;
         view.get(j_pos, qx, qy, mx, my);
         if (SHIFT) {
@@ -520,8 +520,8 @@ __device__ __forceinline__ bool g_lp1_target(const V &view, int i_pos, R zz, R c
         if (!par && !(a > R(0)) && t < t_right) t_right = t;
     }
     bad = (__ballot_sync(gmask, bad) & gmask) != 0u;
-    t_left = group_max<R>(t_left, gmask);
-    t_right = group_min<R>(t_right, gmask);
+    t_left = group_max<R, GL>(t_left, gmask);
+    t_right = group_min<R, GL>(t_right, gmask);
     if (bad || t_left > t_right) return false;
     R t = (tx - px) * dx + (ty - py) * dy;
     if (t < t_left) t = t_left;
@@ -532,7 +532,7 @@ __device__ __forceinline__ bool g_lp1_target(const V &view, int i_pos, R zz, R c
 }
 
 // K:122-146
-template <typename R, bool SHIFT, typename V>
+template <typename R, int GL, bool SHIFT, typename V>
 __device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, R tx, R ty, int &fail_pos,
                                              R &vx, R &vy, int gl, unsigned gmask)
 {
@@ -554,7 +554,7 @@ __device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, 
         }
         if ((vx - px) * nx + (vy - py) * ny < R(0)) {
             R nvx, nvy;
-            if (!g_lp1_target<R, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy, gl, gmask)) {
+            if (!g_lp1_target<R, GL, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy, gl, gmask)) {
                 fail_pos = i_pos;
                 return false;
             }
@@ -567,7 +567,7 @@ __device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, 
 }
 
 // K:153-190
-template <typename R, typename P>
+template <typename R, int GL, typename P>
 __device__ __forceinline__ bool g_lp1_dir(const P &proj, int upto, R cap, R ox, R oy, R &rx, R &ry, int gl,
                                           unsigned gmask)
 {
@@ -581,7 +581,7 @@ __device__ __forceinline__ bool g_lp1_dir(const P &proj, int upto, R cap, R ox, 
     R t_left = -pd - sq;
     R t_right = -pd + sq;
     bool bad = false;
-    for (int j = gl; j < upto; j += ORCA_GL) {
+    for (int j = gl; j < upto; j += GL) {
         R qx, qy, mx, my;
         proj.get(j, qx, qy, mx, my);
         const R a = dx * mx + dy * my;
@@ -593,8 +593,8 @@ __device__ __forceinline__ bool g_lp1_dir(const P &proj, int upto, R cap, R ox, 
         if (!par && !(a > R(0)) && t < t_right) t_right = t;
     }
     bad = (__ballot_sync(gmask, bad) & gmask) != 0u;
-    t_left = group_max<R>(t_left, gmask);
-    t_right = group_min<R>(t_right, gmask);
+    t_left = group_max<R, GL>(t_left, gmask);
+    t_right = group_min<R, GL>(t_right, gmask);
     if (bad || t_left > t_right) return false;
     const R t = (dx * ox + dy * oy) > R(0) ? t_right : t_left;
     rx = px + t * dx;
@@ -603,7 +603,7 @@ __device__ __forceinline__ bool g_lp1_dir(const P &proj, int upto, R cap, R ox, 
 }
 
 // K:193-205
-template <typename R, typename P>
+template <typename R, int GL, typename P>
 __device__ __forceinline__ bool g_lp2_dir(const P &proj, int m, R cap, R ox, R oy, R &rx, R &ry, int gl,
                                           unsigned gmask)
 {
@@ -613,7 +613,7 @@ __device__ __forceinline__ bool g_lp2_dir(const P &proj, int m, R cap, R ox, R o
         proj.get(i, px, py, nx, ny);
         if ((vx - px) * nx + (vy - py) * ny < R(0)) {
             R nvx, nvy;
-            if (!g_lp1_dir<R, P>(proj, i, cap, ox, oy, nvx, nvy, gl, gmask)) {
+            if (!g_lp1_dir<R, GL, P>(proj, i, cap, ox, oy, nvx, nvy, gl, gmask)) {
                 rx = vx;
                 ry = vy;
                 return false;
@@ -629,7 +629,7 @@ __device__ __forceinline__ bool g_lp2_dir(const P &proj, int m, R cap, R ox, R o
 
 // K:212-251. The projected constraints of one (c, j<i_pos) sweep are built GL at a time
 // and compacted in ascending j (ballot rank), which is the order K:226-243 appends them.
-template <typename R, typename V, typename P>
+template <typename R, int GL, typename V, typename P>
 __device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int begin, R cap, R &vx, R &vy,
                                              R &z, int gl, unsigned gmask, int gshift)
 {
@@ -640,7 +640,7 @@ __device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int 
         const R viol = (cpx - vx) * cnx + (cpy - vy) * cny;
         if (viol > dist) {
             int m = 0;
-            for (int j0 = 0; j0 < i_pos; j0 += ORCA_GL) {
+            for (int j0 = 0; j0 < i_pos; j0 += GL) {
                 const int j_pos = j0 + gl;
                 bool valid = false;
                 R ppx = R(0), ppy = R(0), pnx = R(0), pny = R(0);
@@ -661,12 +661,12 @@ __device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int 
                     }
                 }
                 const unsigned bits = (__ballot_sync(gmask, valid) & gmask) >> gshift; // GL bits
-                if (valid) proj.set(m + __popc(bits & ((1u << gl) - 1u)), ppx, ppy, pnx, pny);
+                if (valid) proj.set(m + __popc(bits & ((1u << gl) - 1u)), ppx, ppy, pnx, pny); // gl < 32
                 m += __popc(bits);
             }
             __syncwarp(gmask); // projected constraints visible to the whole group
             R nvx, nvy;
-            if (g_lp2_dir<R, P>(proj, m, cap, cnx, cny, nvx, nvy, gl, gmask)) {
+            if (g_lp2_dir<R, GL, P>(proj, m, cap, cnx, cny, nvx, nvy, gl, gmask)) {
                 vx = nvx;
                 vy = nvy;
             }
@@ -679,7 +679,7 @@ __device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int 
 }
 
 // K:254-283
-template <typename R, typename VS, typename VI, typename P>
+template <typename R, int GL, typename VS, typename VI, typename P>
 __device__ __forceinline__ void g_least_penetration(const VS &shuf, const VI &ident, P &proj, int k, int begin,
                                                     R cap, R wx, R wy, R &rx, R &ry, int gl, unsigned gmask,
                                                     int gshift)
@@ -691,13 +691,13 @@ __device__ __forceinline__ void g_least_penetration(const VS &shuf, const VI &id
         wy = wy * s;
     }
     R vx = wx, vy = wy, z;
-    g_lp3_minmax<R, VS, P>(shuf, proj, k, begin, cap, vx, vy, z, gl, gmask, gshift);
+    g_lp3_minmax<R, GL, VS, P>(shuf, proj, k, begin, cap, vx, vy, z, gl, gmask, gshift);
     R slack = R(0);
     for (int attempt = 0; attempt < 3; ++attempt) {
         const R zz = z + slack;
         int fail;
         R qx, qy;
-        if (g_lp2_target<R, true, VI>(ident, k, zz, cap, wx, wy, fail, qx, qy, gl, gmask)) {
+        if (g_lp2_target<R, GL, true, VI>(ident, k, zz, cap, wx, wy, fail, qx, qy, gl, gmask)) {
             rx = qx;
             ry = qy;
             return;

@@ -129,6 +129,10 @@ class StripDriver:
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+            if self.device.type == "cuda":
+                # the append kernels run on the handle's stream, the NCCL copies on torch's:
+                # make the received records globally visible before anyone reads them
+                torch.cuda.current_stream(self.device).synchronize()
         return got
 
     # -- protocol phases (split so a test can drive two ranks in one process) ------
@@ -194,7 +198,8 @@ def run_bench(args, rank: int, world: int, local: int):
     state.goals[:, 0] = rng.uniform(0.0, world * side, size=n_local).astype(np.float32)
     bounds = [side * r for r in range(1, world)]
     device = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)       # NCCL ops order themselves against the current stream
     capacity = int(n_local * 1.15) + 65536
     sim = Simulation(cfg, capacity=capacity, precision=args.precision, device=local,
                      remove_arrivals=False, stream=stream)
