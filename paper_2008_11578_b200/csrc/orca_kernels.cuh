@@ -24,6 +24,10 @@
 #include "orca_common.cuh"
 #include "orca_sortnet.inc"
 
+#ifndef ORCA_SCAN_UNROLL
+#define ORCA_SCAN_UNROLL 4
+#endif
+
 namespace orca {
 
 // ---------------------------------------------------------------------------
@@ -348,11 +352,10 @@ template <int MAXN> struct TopK {
         return true;
     }
 
-    // compare-exchange of slots a < b under the (d2, id) order; sentinels (idx < 0) never tie-break
-    __device__ __forceinline__ void cex(int a, int b, const int *__restrict__ s_row, const i64 *__restrict__ ids)
+    // compare-exchange of slots a < b by key only (ties are detected afterwards)
+    __device__ __forceinline__ void cex(int a, int b)
     {
-        bool sw = key[b] < key[a];
-        if (key[b] == key[a] && idx[a] >= 0 && idx[b] >= 0) sw = ids[s_row[idx[b]]] < ids[s_row[idx[a]]];
+        const bool sw = key[b] < key[a];
         const double ka = key[a], kb = key[b];
         const int ia = idx[a], ib = idx[b];
         key[a] = sw ? kb : ka;
@@ -365,15 +368,23 @@ template <int MAXN> struct TopK {
     // 191 for 32; written out by scripts/gen_sortnet.py so every slot stays a register).
     // Used by the fast pass to order its first max_n candidates at once instead of max_n
     // shifting insertions.
-    __device__ __forceinline__ void sort_all(const int *__restrict__ s_row, const i64 *__restrict__ ids)
+    // Returns false if two kept candidates have exactly equal keys: their order is decided
+    // by id (K:473-476), which the network does not look at -- the caller then hands the
+    // agent to the exact ring search. Exact ties do not occur between generic float
+    // positions; they do on lattices.
+    __device__ __forceinline__ bool sort_all()
     {
-#define CEX(a, b) cex(a, b, s_row, ids);
+#define CEX(a, b) cex(a, b);
         if constexpr (MAXN == 16) {
             ORCA_SORTNET_16
         } else {
             ORCA_SORTNET_32
         }
 #undef CEX
+        bool tie = false;
+#pragma unroll
+        for (int t = 0; t + 1 < MAXN; ++t) tie = tie || (key[t] == key[t + 1] && idx[t] >= 0 && idx[t + 1] >= 0);
+        return !tie;
     }
 
     // slot-major neighbour table + count + next step's radius hint
@@ -442,6 +453,8 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
     for (int gx = gx_lo; gx <= gx_hi; ++gx) {
         const int *cs = cell_start + gx * ny;
         const int e = cs[y_hi + 1];
+        constexpr int kScanUnroll = ORCA_SCAN_UNROLL;
+#pragma unroll kScanUnroll
         for (int s2 = cs[y_lo]; s2 < e; ++s2) {
             const typename Vec<R>::T2 q = s_xy[s2];
             bool pass;
@@ -480,7 +493,7 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
                 }
             }
         }
-        top.sort_all(s_row, ids);
+        ok = top.sort_all();
         // the rest (a handful: the threshold is tight) by shifting insertion
         for (int e = max_n; e < nbuf; ++e) {
             const int s2 = my_buf[e * 128];
@@ -491,7 +504,7 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
             top.insert(d2, s2, max_n, s_row, ids);
         }
         // exact iff nothing outside the buffer can precede the last kept entry
-        ok = T >= rad2 || (top.cnt == max_n && top.key[MAXN - 1] <= T);
+        ok = ok && (T >= rad2 || (top.cnt == max_n && top.key[MAXN - 1] <= T));
     }
     if (ok) {
         top.store(s, row, max_n, P.stride, nb, nb_cnt, hint);
