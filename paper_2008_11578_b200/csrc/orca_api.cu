@@ -402,6 +402,8 @@ static int reset_plan(orca_sim *sim, int64_t n, int64_t frame)
     h.frame = frame;
     h.min_sep_enc = enc_double(INFINITY);
     h.vmax_enc = enc_double(0.0);
+    h.rmax_enc = enc_double(0.0);
+    h.sep_ub_enc = enc_double(INFINITY);
     *sim->h_plan = h;
     CK(sim, cudaMemcpyAsync(sim->plan, sim->h_plan, sizeof(GridPlan), cudaMemcpyHostToDevice, sim->stream));
     // the pinned mirror is reused by later reads; make sure this copy has left it
@@ -726,11 +728,14 @@ template <typename R> static int metrics_stage(orca_sim *sim, const StepParams &
 {
     typedef typename Vec<R>::T2 R2;
     const int64_t n = sim->n_bound;
+    k_min_sep_bound<R><<<grid_for(n, 128), 128, 0, sim->stream>>>(
+        sim->plan, P, reinterpret_cast<const R2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+        reinterpret_cast<const R2 *>(sim->radmax[sim->acur]));
     k_min_sep<R><<<grid_for(n, 128), 128, 0, sim->stream>>>(
         sim->plan, P, reinterpret_cast<const R2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
         sim->ids[sim->acur], reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), 1e-6 /* engine.py:36 */);
     CKL(sim);
-    sim->launches += 1;
+    sim->launches += 2;
     return ORCA_OK;
 }
 

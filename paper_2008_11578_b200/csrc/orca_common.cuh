@@ -45,6 +45,8 @@ struct GridPlan {
     int n_after;   // rows after arrival removal
     // metrics
     u64 min_sep_enc; // order-preserving encoding of the running minimum
+    u64 sep_ub_enc;  // upper bound on it from each agent's closest candidate (k_min_sep_bound)
+    u64 rmax_enc;    // largest agent radius ever uploaded
     u64 collisions;
     // frames completed
     i64 frame;

@@ -41,6 +41,7 @@ __global__ void k_begin_step(GridPlan *plan)
     plan->gq_count = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
+    plan->sep_ub_enc = plan->min_sep_enc;
     plan->collisions = 0;
 }
 
@@ -1040,6 +1041,7 @@ k_strip_append(GridPlan *__restrict__ plan, const orca_agent_record *__restrict_
     failed[row] = -1;
     hint[row] = __int_as_float(0x7F800000);
     atomicMax(&plan->vmax_enc, enc_double(r.max_speed));
+    atomicMax(&plan->rmax_enc, enc_double(r.radius));
 }
 
 __global__ void k_after_append(GridPlan *plan, int count, int ghost)
@@ -1058,6 +1060,48 @@ __global__ void k_set_frame(GridPlan *plan, i64 frame) { plan->frame = frame; }
 // post-step positions, using the grid of the NEXT bin build (same positions).
 // ---------------------------------------------------------------------------
 
+// Pass 1: an upper bound on the minimum separation -- the separation of each agent's
+// closest candidate in the 3x3 block of search cells (one square root per agent).
+template <typename R>
+__global__ void __launch_bounds__(128)
+k_min_sep_bound(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *__restrict__ s_xy,
+                const int *__restrict__ cell_start, const int *__restrict__ s_cell,
+                const int *__restrict__ s_row, const typename Vec<R>::T2 *__restrict__ radmax)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    double ub = ORCA_INF;
+    if (s < plan->n) {
+        const int nx = plan->nx, ny = plan->ny, r = min(1, plan->rmax);
+        const typename Vec<R>::T2 me = s_xy[s];
+        const int c0 = s_cell[s];
+        const int cx = c0 / ny, cy = c0 - cx * ny;
+        const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
+        double best_d2 = ORCA_INF;
+        int best_s = -1;
+        for (int gx = max(cx - r, 0); gx <= min(cx + r, nx - 1); ++gx) {
+            const int *cs = cell_start + gx * ny;
+            for (int s2 = cs[y_lo]; s2 < cs[y_hi + 1]; ++s2) {
+                const typename Vec<R>::T2 q = s_xy[s2];
+                const double dx = (double)q.x - (double)me.x, dy = (double)q.y - (double)me.y;
+                const double d2 = dx * dx + dy * dy;
+                if (s2 != s && d2 < best_d2) {
+                    best_d2 = d2;
+                    best_s = s2;
+                }
+            }
+        }
+        if (best_s >= 0 && best_d2 <= P.rad2)
+            ub = __dsqrt_rn(best_d2) - ((double)radmax[s_row[s]].x + (double)radmax[s_row[best_s]].x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ub = fmin(ub, __shfl_xor_sync(0xFFFFFFFFu, ub, o));
+    if ((threadIdx.x & 31) == 0 && ub < ORCA_INF) atomicMin(&plan->sep_ub_enc, enc_double(ub));
+}
+
+// Pass 2: exact minimum separation and collision count (K:559-589), each pair counted
+// from its lower-id side. Only pairs closer than  max(bound, 0) + 2 * (largest radius)
+// can attain the minimum or collide, so the scan covers that distance instead of the
+// whole neighbor_radius (about 50x fewer candidates in a typical crowd).
 template <typename R>
 __global__ void __launch_bounds__(128)
 k_min_sep(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *__restrict__ s_xy,
@@ -1066,10 +1110,15 @@ k_min_sep(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *
           const typename Vec<R>::T2 *__restrict__ radmax, double coll_tol)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    double best = __longlong_as_double(0x7FF0000000000000LL);
+    double best = ORCA_INF;
     unsigned cnt = 0;
     if (s < plan->n) {
-        const int nx = plan->nx, ny = plan->ny, r = plan->rmax;
+        const double ub = dec_double(plan->sep_ub_enc);
+        const double rr = fmax(dec_double(plan->rmax_enc), 0.0);
+        double reach = ub < ORCA_INF ? (fmax(ub, 0.0) + 2.0 * rr) * (1.0 + 1e-9) + 1e-9 : P.nr;
+        const double T2 = fmin(reach * reach, P.rad2);
+        const int nx = plan->nx, ny = plan->ny;
+        const int r = min(plan->rmax, (int)(sqrt(T2) * plan->inv_cell * (1.0 + 1e-9)) + 1);
         const typename Vec<R>::T2 me = s_xy[s];
         const int row = s_row[s];
         const i64 my_id = ids[row];
@@ -1083,7 +1132,7 @@ k_min_sep(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *
                 const typename Vec<R>::T2 q = s_xy[s2];
                 const double dx = (double)q.x - (double)me.x, dy = (double)q.y - (double)me.y;
                 const double d2 = dx * dx + dy * dy;
-                if (d2 > P.rad2) continue;
+                if (d2 > T2) continue;
                 const int row2 = s_row[s2];
                 if (ids[row2] <= my_id) continue;
                 const double sep = __dsqrt_rn(d2) - (my_r + (double)radmax[row2].x);
@@ -1130,6 +1179,7 @@ k_import_attrs(int n, const double *__restrict__ radii, const double *__restrict
     if (i >= n) return;
     hint[i] = __int_as_float(0x7F800000); // no neighbour list yet
     atomicMax(&plan->vmax_enc, enc_double(maxs[i]));
+    atomicMax(&plan->rmax_enc, enc_double(radii[i]));
     goalpref[i] = mk4((R)goals[2 * i], (R)goals[2 * i + 1], (R)pref[i], (R)gtol[i]);
     radmax[i] = mk2((R)radii[i], (R)maxs[i]);
     cls[i] = (u8)cls_in[i];

@@ -75,6 +75,31 @@ def desired_velocity(agent, dt: float) -> np.ndarray:
     return np.array([dx * scale, dy * scale])
 
 
+_torch = None
+
+
+def _host_empty(shape, dtype=np.float64):
+    """Readback buffers. With PyTorch available they come from its caching pinned-memory
+    allocator (cheap after the first call), so device->host copies run at PCIe speed;
+    the numpy array keeps its tensor alive. ORCA_B200_PINNED=0 forces plain numpy."""
+    global _torch
+    if _torch is None:
+        _torch = False
+        if os.environ.get("ORCA_B200_PINNED", "1") != "0":
+            try:
+                import torch
+                _torch = torch
+            except Exception:       # torch is optional plumbing here
+                _torch = False
+    if _torch:
+        try:
+            tdt = {np.dtype(np.float64): _torch.float64, np.dtype(np.int64): _torch.int64}[np.dtype(dtype)]
+            return _torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+        except Exception:
+            pass
+    return np.empty(shape, dtype=dtype)
+
+
 def _f64(a, shape=None):
     a = np.ascontiguousarray(a, dtype=np.float64)
     return a if shape is None else a.reshape(shape)
@@ -210,10 +235,10 @@ class Simulation:
     def state(self, state_type=None) -> SimState:
         info = self.info()
         n = int(info.active_agents)
-        ids = np.empty(n, dtype=np.int64)
-        pos, vel, goals = np.empty((n, 2)), np.empty((n, 2)), np.empty((n, 2))
-        radii, pref, maxs, gtol = np.empty(n), np.empty(n), np.empty(n), np.empty(n)
-        cls = np.empty(n, dtype=np.int64)
+        ids = _host_empty(n, np.int64)
+        pos, vel, goals = _host_empty((n, 2)), _host_empty((n, 2)), _host_empty((n, 2))
+        radii, pref, maxs, gtol = _host_empty(n), _host_empty(n), _host_empty(n), _host_empty(n)
+        cls = _host_empty(n, np.int64)
         self._raise_like_reference(self._L.orca_download(
             self._h, ptr(ids), ptr(pos), ptr(vel), ptr(radii), ptr(pref), ptr(maxs), ptr(goals),
             ptr(gtol), ptr(cls)))
@@ -225,7 +250,7 @@ class Simulation:
 
     def positions_velocities(self):
         n = int(self._L_active())
-        pos, vel = np.empty((n, 2)), np.empty((n, 2))
+        pos, vel = _host_empty((n, 2)), _host_empty((n, 2))
         self._raise_like_reference(self._L.orca_download_pv(self._h, ptr(pos), ptr(vel)))
         return pos, vel
 
@@ -335,7 +360,7 @@ def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
     static = tuple(getattr(state, f) for f in _STATIC)
     res = getattr(sim, "_resident", None)
     if (reuse_resident and res is not None and len(res) == len(static)
-            and all(a is b for a, b in zip(res, static))):
+            and all(a is b for a, b in zip(res, static)) and sim._L_active() == n):
         sim.load_pv(state.positions, state.velocities, state.frame)
         sim._rng_state = getattr(state, "rng_state", None)
         sim._state_type = type(state)
