@@ -76,6 +76,9 @@ struct orca_sim {
     bool gather_fast = true;   // ORCA_GATHER_FAST=0: exact ring search for every agent
     bool fb_coop = true;       // ORCA_FB_COOP=0: thread-per-agent least-penetration stage
     bool use_graph = true;     // ORCA_GRAPH=0: launch the step's kernels one by one
+    int chunks = 1;            // ORCA_CHUNKS: gather+solve ranges issued on two streams
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     // CUDA graphs of one whole step, keyed by everything the launch sequence depends on
     struct StepGraph {
@@ -220,6 +223,9 @@ extern "C" void orca_destroy(orca_sim *sim)
     for (cudaEvent_t e : sim->ev_pool) cudaEventDestroy(e);
     if (sim->h_plan) cudaFreeHost(sim->h_plan);
     if (sim->own_stream) cudaStreamDestroy(sim->own_stream);
+    if (sim->aux_stream) cudaStreamDestroy(sim->aux_stream);
+    if (sim->ev_fork) cudaEventDestroy(sim->ev_fork);
+    if (sim->ev_join) cudaEventDestroy(sim->ev_join);
     delete sim;
 }
 
@@ -250,6 +256,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
     if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
     if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
+    if (const char *ch = getenv("ORCA_CHUNKS")) sim->chunks = std::min(ORCA_MAX_CHUNKS, std::max(1, atoi(ch)));
     if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
@@ -268,6 +275,9 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
 
     CKC(cudaStreamCreateWithFlags(&sim->own_stream, cudaStreamNonBlocking));
     sim->stream = sim->own_stream;
+    CKC(cudaStreamCreateWithFlags(&sim->aux_stream, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&sim->ev_fork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&sim->ev_join, cudaEventDisableTiming));
     for (int i = 0; i < 3; ++i) CKC(cudaMalloc(&sim->pv[i], cap * 4 * rs));
     for (int i = 0; i < 2; ++i) {
         CKC(cudaMalloc(&sim->goalpref[i], cap * 4 * rs));
@@ -639,24 +649,46 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
-    if (sim->gather_fast)
-        k_gather_fast<S, MAXN, 48><<<grid_for(n, 128), 128, 0, st>>>(
+    // Gather + solve over `chunks` ranges of sorted slots, alternating between the handle's
+    // stream and an auxiliary one: the neighbour search (ALU/issue bound) of one range
+    // overlaps the LP (FP64/latency bound) of another. chunks == 1 is the plain sequence.
+    const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(sim->chunks, (n + 4095) / 4096));
+    const int64_t per = ((n + chunks - 1) / chunks + 127) / 128 * 128;
+    if (chunks > 1) {
+        CK(sim, cudaEventRecord(sim->ev_fork, st));
+        CK(sim, cudaStreamWaitEvent(sim->aux_stream, sim->ev_fork, 0));
+    }
+    for (int c = 0; c < chunks; ++c) {
+        cudaStream_t cs = (c & 1) ? sim->aux_stream : st;
+        const int s0 = (int)std::min<int64_t>(n, c * per), s1 = (int)std::min<int64_t>(n, (c + 1) * per);
+        const int64_t m = s1 - s0;
+        if (m <= 0) continue;
+        if (sim->gather_fast)
+            k_gather_fast<S, MAXN, 48><<<grid_for(m, 128), 128, 0, cs>>>(
+                sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+                sim->ids[a], reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt,
+                sim->gq, s0, s1, c);
+        else
+            k_enqueue_all<<<grid_for(m, 256), 256, 0, cs>>>(sim->plan, P.max_n, sim->s_row, sim->nb_cnt, sim->gq,
+                                                             s0, s1, c);
+        const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (m + 127) / 128));
+        k_gather<S, MAXN><<<gq_blocks, 128, 0, cs>>>(
             sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-            sim->ids[a], reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt,
-            sim->gq);
-    else
-        k_enqueue_all<<<grid_for(n, 256), 256, 0, st>>>(sim->plan, P.max_n, sim->s_row, sim->nb_cnt, sim->gq);
-    const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 127) / 128));
-    k_gather<S, MAXN><<<gq_blocks, 128, 0, st>>>(
-        sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-        sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq);
-    sim->mark();
-    k_solve<S, R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
-                                            C::solve_bpt * C::solve_threads, st>>>(
-        sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
-        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
-        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
-        sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state));
+            sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, s0, c);
+        if (chunks == 1) sim->mark();
+        k_solve<S, R, MAXN, C::solve_threads><<<grid_for(m, C::solve_threads), C::solve_threads,
+                                                C::solve_bpt * C::solve_threads, cs>>>(
+            sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
+            reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
+            reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
+            sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1);
+        sim->launches += 3;
+    }
+    if (chunks > 1) {
+        CK(sim, cudaEventRecord(sim->ev_join, sim->aux_stream));
+        CK(sim, cudaStreamWaitEvent(st, sim->ev_join, 0));
+        sim->mark(); // with overlap the gather / solve split is not observable: all of it
+    }                //  is booked under "gather" and "solve" reads 0
     sim->mark();
     if (sim->fb_coop) {
         const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
@@ -679,7 +711,7 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     }
     sim->mark();
     CKL(sim);
-    sim->launches += 4;
+    sim->launches += 1;
     return ORCA_OK;
 }
 

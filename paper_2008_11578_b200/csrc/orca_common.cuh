@@ -19,6 +19,9 @@ typedef signed char i8;
 
 #define ORCA_NO_ERR 0xFFFFFFFFFFFFFFFFULL
 
+// gather+solve can be issued as up to this many agent ranges on two streams (orca_api.cu)
+#define ORCA_MAX_CHUNKS 8
+
 // Device-resident per-step plan and counters. Written by k_plan / k_finish and
 // read by every kernel of the step, so a step needs no host round trip.
 struct GridPlan {
@@ -37,7 +40,7 @@ struct GridPlan {
     int err_range;  // a position left the reference's indexable grid range
     // per-step counters
     int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
-    int gq_count;  // agents queued for the exact ring search (k_gather)
+    int gq_count[ORCA_MAX_CHUNKS]; // agents queued for the exact ring search (k_gather), per chunk
     int pack_count; // rows selected by the last orca_strip_pack
     u64 vmax_enc;  // order-preserving encoding of the largest max_speed ever uploaded
     double vmax;

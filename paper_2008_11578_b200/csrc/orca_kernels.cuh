@@ -38,7 +38,7 @@ namespace orca {
 __global__ void k_begin_step(GridPlan *plan)
 {
     plan->fq_count = 0;
-    plan->gq_count = 0;
+    for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) plan->gq_count[c] = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
     plan->sep_ub_enc = plan->min_sep_enc;
@@ -423,11 +423,11 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
               const int *__restrict__ cell_start, const int *__restrict__ s_cell,
               const int *__restrict__ s_row, const i64 *__restrict__ ids,
               const typename Vec<R>::T2 *__restrict__ radmax, float *__restrict__ hint,
-              int *__restrict__ nb, u8 *__restrict__ nb_cnt, int *__restrict__ gq)
+              int *__restrict__ nb, u8 *__restrict__ nb_cnt, int *__restrict__ gq, int s0, int s1, int chunk)
 {
     __shared__ int buf[CAP * 128];
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= plan->n) return;
+    const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x; // this launch covers sorted slots [s0, s1)
+    if (s >= min(s1, plan->n)) return;
     const int row = s_row[s];
     if (row >= plan->n_owned || P.max_n == 0) {
         nb_cnt[s] = 0;
@@ -510,22 +510,22 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
     if (ok) {
         top.store(s, row, max_n, P.stride, nb, nb_cnt, hint);
     } else {
-        gq[atomicAdd(&plan->gq_count, 1)] = s;
+        gq[s0 + atomicAdd(&plan->gq_count[chunk], 1)] = s;
     }
 }
 
 // every owned agent goes to the exact ring search (fast pass disabled)
 __global__ void __launch_bounds__(256)
 k_enqueue_all(GridPlan *__restrict__ plan, int max_n, const int *__restrict__ s_row,
-              u8 *__restrict__ nb_cnt, int *__restrict__ gq)
+              u8 *__restrict__ nb_cnt, int *__restrict__ gq, int s0, int s1, int chunk)
 {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= plan->n) return;
+    const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= min(s1, plan->n)) return;
     if (s_row[s] >= plan->n_owned || max_n == 0) {
         nb_cnt[s] = 0;
         return;
     }
-    gq[atomicAdd(&plan->gq_count, 1)] = s;
+    gq[s0 + atomicAdd(&plan->gq_count[chunk], 1)] = s;
 }
 
 // Exact ring search for the agents the fast pass queued (all of them on the first step
@@ -539,9 +539,10 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
          const typename Vec<R>::T2 *__restrict__ s_xy, const int *__restrict__ cell_start,
          const int *__restrict__ s_cell, const int *__restrict__ s_row,
          const i64 *__restrict__ ids, float *__restrict__ hint, int *__restrict__ nb,
-         u8 *__restrict__ nb_cnt, const int *__restrict__ gq)
+         u8 *__restrict__ nb_cnt, const int *__restrict__ gq, int s0, int chunk)
 {
-    const int nq = plan->gq_count;
+    const int nq = plan->gq_count[chunk];
+    gq += s0; // this chunk's segment of the queue
     const int nx = plan->nx, ny = plan->ny, rmax = plan->rmax;
     const double cell = plan->cell;
     const double rad2 = P.rad2;
@@ -725,14 +726,14 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
         const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
         typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
         i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
-        typename Vec<R>::T4 *__restrict__ fq_state)
+        typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typename Vec<R>::T4 *sm_cons = reinterpret_cast<typename Vec<R>::T4 *>(smem_raw);
     u8 *sm_perm = smem_raw + sizeof(typename Vec<R>::T4) * MAXN * THREADS;
 
-    const int s = blockIdx.x * THREADS + threadIdx.x;
-    if (s >= plan->n) return;
+    const int s = s0 + blockIdx.x * THREADS + threadIdx.x; // sorted slots [s0, s1)
+    if (s >= min(s1, plan->n)) return;
     const int row = s_row[s];
     if (row >= plan->n_owned) return; // halo ghost: searched, never solved
 
