@@ -143,6 +143,12 @@ ORCA_API int orca_download(orca_sim *sim, int64_t *ids, double *positions, doubl
 /* Only positions and velocities (the arrays a step changes). */
 ORCA_API int orca_download_pv(orca_sim *sim, double *positions, double *velocities);
 
+/* The un-compacted result of the LAST step: new positions and velocities of every row
+ * that was active during that frame, arrivals included, in pre-step row order (what
+ * engine._advance records in its FrameLog, engine.py:257-263). n must be the agent count
+ * before that step. Synchronises. */
+ORCA_API int orca_download_last_step_pv(orca_sim *sim, int64_t n, double *positions, double *velocities);
+
 /* Host -> device refresh of positions and velocities only (same n, same rows). */
 ORCA_API int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
                    const double *velocities);

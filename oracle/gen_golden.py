@@ -22,6 +22,9 @@ Fixtures (all small, compressed):
   frame_*.npz        engine._advance on seeded plaza crowds incl. per-agent
                      cell (ix,iy), ordered neighbour rows, constraints, out_v,
                      status, failed_at, new state, metrics.
+  run_*.npz          whole engine.run() of the built-in 2-way / 4-way crossings: the crowd
+                     the reference spawned, its guard, summary, per-frame metrics,
+                     arrival times and sampled trajectories.
   chain_1k.npz       config 1: 100 consecutive reference steps of 1,024
                      pedestrians (each input = previous output rounded to
                      float32 so an FP32 device state sees identical inputs);
@@ -315,9 +318,71 @@ def gen_chain():
     print("chain_1k.npz active", active[[0, -1]], "fallbacks/step", fallbacks.mean())
 
 
-if __name__ == "__main__":
+def main():
     os.makedirs(OUT, exist_ok=True)
+    if os.environ.get("GEN_ONLY_RUN"):
+        return gen_run()
     gen_kat()
     gen_lp_batches()
     gen_frames()
     gen_chain()
+    gen_run()
+
+
+def gen_run():
+    """Whole reference runs (engine.run) of the built-in crossing scenarios: the spawned
+    crowd (the reference's own seeded sampling), the guard, and everything run() reports."""
+    from orcasim.crossings import crossing_config
+    for name, kind, per_arm, vf, seed in (("two_way_80", "two_way", 40, 0.1, 3),
+                                          ("four_way_96", "four_way", 24, 0.25, 5)):
+        cfg = crossing_config(kind, per_arm, vf, seed)
+        st = E.init_state(cfg)
+        res = E.run(cfg, worker_count=2, record_trajectories=True)
+        s = res.summary
+        nf = len(res.frame_metrics)
+        n0 = st.active_count
+        # trajectories: positions of every 10th frame (padded with NaN for removed agents)
+        sample = list(range(0, nf, 10)) + [nf - 1]
+        traj = np.full((len(sample), n0, 4), np.nan)
+        row_of = {int(a): i for i, a in enumerate(st.ids)}
+        for k, f in enumerate(sample):
+            log = res.frame_logs[f]
+            rows = [row_of[int(a)] for a in log.ids]
+            traj[k, rows, :2] = log.positions
+            traj[k, rows, 2:] = log.velocities
+        arr_ids = np.array(sorted(row_of), dtype=np.int64)
+        # arrival time per agent id, NaN if it never arrived
+        arrival = np.full(n0, np.nan)
+        last_seen = {}
+        for log in res.frame_logs:
+            for a in log.ids:
+                last_seen[int(a)] = log.time
+        if s.terminated or s.arrived:
+            final_ids = set(int(a) for a in res.final_state.ids)
+            for a, t in last_seen.items():
+                if a not in final_ids:
+                    arrival[row_of[a]] = t
+        np.savez_compressed(
+            os.path.join(OUT, f"run_{name}.npz"),
+            ids=st.ids, positions=st.positions, velocities=st.velocities, radii=st.radii,
+            pref_speeds=st.pref_speeds, max_speeds=st.max_speeds, goals=st.goals,
+            goal_tols=st.goal_tols, class_codes=st.class_codes.astype(np.int8),
+            dt=cfg.dt, tau=cfg.tau, neighbor_radius=cfg.neighbor_radius,
+            max_neighbors=np.int64(cfg.max_neighbors), avoidance_margin=cfg.avoidance_margin,
+            fmat=cfg.responsibility.as_array(), guard=np.int64(cfg.frame_guard()), seed=np.int64(cfg.seed),
+            frames=np.int64(s.frames), terminated=np.bool_(s.terminated), arrived=np.int64(s.arrived),
+            total_collisions=np.int64(s.total_collisions), min_separation=np.float64(s.min_separation),
+            total_fallbacks=np.int64(s.total_fallbacks),
+            travel_ped=np.float64(s.mean_travel_time.get(E.AgentClass.PEDESTRIAN, np.nan)),
+            travel_veh=np.float64(s.mean_travel_time.get(E.AgentClass.VEHICLE, np.nan)),
+            m_min_sep=np.array([m.min_separation for m in res.frame_metrics]),
+            m_coll=np.array([m.collision_count for m in res.frame_metrics], dtype=np.int64),
+            m_active=np.array([m.active_agents for m in res.frame_metrics], dtype=np.int64),
+            arrival=arrival, sample_frames=np.array(sample, dtype=np.int64), traj=traj,
+            final_ids=res.final_state.ids)
+        print(f"run_{name}.npz agents={n0} frames={s.frames} terminated={s.terminated} "
+              f"arrived={s.arrived} collisions={s.total_collisions} fallbacks={s.total_fallbacks}")
+
+
+if __name__ == "__main__":
+    main()

@@ -6,13 +6,13 @@ Importing the package does not touch the GPU; the first call into
 is missing -- there is no CPU fallback.
 """
 
-from .types import (AgentClass, ClassParams, FrameMetrics, ResponsibilityMatrix,
-                    ScenarioConfig, SimState)
-from .engine import Simulation, desired_velocity, init_state, problem_seed, step
+from .types import (AgentClass, ClassParams, FrameLog, FrameMetrics, ResponsibilityMatrix,
+                    RunResult, RunSummary, ScenarioConfig, SimState)
+from .engine import Simulation, desired_velocity, init_state, problem_seed, run, step
 from .lp import (HalfPlaneConstraint, LpBatch, LpProblem, LpResult, LpStatus, shuffle_order,
                  solve_batch, solve_closest_point, solve_range)
 
 __all__ = ["AgentClass", "ClassParams", "FrameMetrics", "ResponsibilityMatrix",
            "ScenarioConfig", "SimState", "Simulation", "desired_velocity", "init_state",
-           "problem_seed", "step", "HalfPlaneConstraint", "LpBatch", "LpProblem", "LpResult",
+           "problem_seed", "run", "step", "FrameLog", "RunResult", "RunSummary", "HalfPlaneConstraint", "LpBatch", "LpProblem", "LpResult",
            "LpStatus", "shuffle_order", "solve_batch", "solve_closest_point", "solve_range"]

@@ -27,6 +27,7 @@ ORCA_ECOINCIDENT, ORCA_ERANGE = -3, -4
 SYMBOLS = [
     "orca_abi_version", "orca_create", "orca_destroy", "orca_set_stream", "orca_set_params",
     "orca_last_error", "orca_upload", "orca_download", "orca_download_pv", "orca_upload_pv",
+    "orca_download_last_step_pv",
     "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host",
     "orca_profile_stages", "orca_get_stage_ms",
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
@@ -91,6 +92,7 @@ def load():
     L.orca_upload.argtypes = [vp, i64, i64] + [vp] * 9
     L.orca_download.argtypes = [vp] + [vp] * 9
     L.orca_download_pv.argtypes = [vp, vp, vp]
+    L.orca_download_last_step_pv.argtypes = [vp, i64, vp, vp]
     L.orca_upload_pv.argtypes = [vp, i64, i64, vp, vp]
     L.orca_step.argtypes = [vp]
     L.orca_run.argtypes = [vp, i64]

@@ -581,6 +581,26 @@ extern "C" int orca_download(orca_sim *sim, int64_t *ids, double *positions, dou
     return ORCA_OK;
 }
 
+extern "C" int orca_download_last_step_pv(orca_sim *sim, int64_t n, double *positions, double *velocities)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_download_last_step_pv: no resident state");
+    if (n != sim->n_pre)
+        return fail(sim, ORCA_EINVAL, "orca_download_last_step_pv: n = %lld, last step had %lld rows",
+                    (long long)n, (long long)sim->n_pre);
+    int rc = fetch_plan(sim);
+    if (rc) return rc;
+    if (n == 0) return ORCA_OK;
+    // the step wrote pv[(pre+1)%3]; arrival removal compacts into a third buffer and leaves it intact
+    const int keep_cur = sim->cur;
+    sim->cur = (sim->pre + 1) % 3;
+    rc = sim->precision != ORCA_F64 ? download_pv_impl<float>(sim, n, positions, velocities)
+                                    : download_pv_impl<double>(sim, n, positions, velocities);
+    sim->cur = keep_cur;
+    if (rc) return rc;
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    return ORCA_OK;
+}
+
 extern "C" int orca_download_pv(orca_sim *sim, double *positions, double *velocities)
 {
     return orca_download(sim, nullptr, positions, velocities, nullptr, nullptr, nullptr, nullptr, nullptr,

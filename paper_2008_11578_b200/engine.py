@@ -32,9 +32,10 @@ import numpy as np
 
 from . import _lib
 from ._lib import OrcaError, OrcaInfo, OrcaParams, check, load, precision_code, ptr
-from .types import AgentClass, FrameMetrics, ScenarioConfig, SimState
+from .types import (AgentClass, FrameLog, FrameMetrics, RunResult, RunSummary, ScenarioConfig,
+                    SimState)
 
-__all__ = ["Simulation", "init_state", "step", "problem_seed", "desired_velocity",
+__all__ = ["Simulation", "init_state", "step", "run", "problem_seed", "desired_velocity",
            "DEFAULT_PRECISION", "COLLISION_TOLERANCE", "DEFAULT_WORK_UNIT_STEPS"]
 
 COLLISION_TOLERANCE = 1e-6          # engine.py:36 (applied inside k_min_sep)
@@ -254,6 +255,19 @@ class Simulation:
         self._raise_like_reference(self._L.orca_download_pv(self._h, ptr(pos), ptr(vel)))
         return pos, vel
 
+    def last_step_positions_velocities(self, n_pre: int):
+        """Un-compacted result of the last step for every row active during that frame,
+        arrivals included (what the reference logs per frame, engine.py:257-263)."""
+        pos, vel = _host_empty((n_pre, 2)), _host_empty((n_pre, 2))
+        self._raise_like_reference(self._L.orca_download_last_step_pv(self._h, int(n_pre), ptr(pos), ptr(vel)))
+        return pos, vel
+
+    def ids(self):
+        n = self._L_active()
+        ids = np.empty(n, dtype=np.int64)
+        self._raise_like_reference(self._L.orca_download(self._h, ptr(ids), *([None] * 8)))
+        return ids
+
     def step_host(self, positions, velocities, frame: int, out_pos=None, out_vel=None,
                   out_status=None):
         """One frame through host buffers (orca_step_host): H2D of positions and
@@ -390,3 +404,72 @@ def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
                            collision_count=int(info.collision_count) if n2 >= 2 else 0,
                            active_agents=int(n2))
     return new_state, metrics
+
+
+def run(config: ScenarioConfig, worker_count: int = 1, record_trajectories: bool = True,
+        work_unit_steps: int = DEFAULT_WORK_UNIT_STEPS, *, agents=None, state: SimState | None = None,
+        precision=None, device: int = 0) -> RunResult:
+    """Step until every agent reaches its goal or the frame guard trips (engine.py:311-370).
+    The crowd stays on the device for the whole run; per frame the host reads back the
+    counters (frame metrics, fallbacks, arrivals) and, when record_trajectories is set, the
+    frame's positions and velocities. `agents` / `state` supply the spawned crowd (the
+    reference samples it from config.regions, which is outside this package's scope).
+    summary.terminated is False when the guard stopped the run."""
+    del worker_count, work_unit_steps
+    if state is None:
+        state = init_state(config, agents)
+    n0 = state.active_count
+    agent_records = [{"id": int(state.ids[i]), "agent_class": AgentClass(int(state.class_codes[i])),
+                      "spawn": state.positions[i].copy(), "goal": state.goals[i].copy(),
+                      "radius": float(state.radii[i])} for i in range(n0)]
+    guard = config.frame_guard()
+    logs, metrics, arrival, fallbacks = [], [], {}, 0
+    ids = np.ascontiguousarray(state.ids, dtype=np.int64)
+    classes = np.asarray(state.class_codes).astype(np.int8)
+    radii = np.ascontiguousarray(state.radii, dtype=np.float64)
+    frame, dt = int(state.frame), float(config.dt)
+    sim = Simulation(config, capacity=max(n0, 1), precision=precision, device=device,
+                     remove_arrivals=True, compute_metrics=True)
+    try:
+        sim.load(state)
+        while ids.shape[0] > 0 and frame < guard:
+            t0 = _time.perf_counter()
+            n_pre = ids.shape[0]
+            sim.step()
+            info = sim.info()                       # synchronises; raises the reference's errors
+            wall_ms = (_time.perf_counter() - t0) * 1e3
+            frame = int(info.frame)
+            if record_trajectories:
+                pos, vel = sim.last_step_positions_velocities(n_pre)
+                logs.append(FrameLog(frame=frame, time=frame * dt, ids=ids.copy(), classes=classes.copy(),
+                                     positions=pos, velocities=vel, radii=radii.copy()))
+            if int(info.removed_agents):
+                kept = sim.ids()
+                gone = ~np.isin(ids, kept, assume_unique=True)
+                for agent_id in ids[gone]:
+                    arrival[int(agent_id)] = frame * dt
+                ids, classes, radii = ids[~gone], classes[~gone], radii[~gone]
+            n2 = ids.shape[0]
+            metrics.append(FrameMetrics(
+                frame=frame, wall_ms=wall_ms,
+                min_separation=float(info.min_separation) if n2 >= 2 else float("inf"),
+                collision_count=int(info.collision_count) if n2 >= 2 else 0, active_agents=int(n2)))
+            fallbacks += int(info.lp_fallbacks)
+        final_state = sim.state(type(state))
+    finally:
+        sim.close()
+    wall = np.array([m.wall_ms for m in metrics]) if metrics else np.zeros(1)
+    class_of = {rec["id"]: rec["agent_class"] for rec in agent_records}
+    travel = {}
+    for cls in AgentClass:
+        times = [t for agent_id, t in arrival.items() if class_of[agent_id] == cls]
+        if times:
+            travel[cls] = float(np.mean(times))
+    summary = RunSummary(
+        total_collisions=int(sum(m.collision_count for m in metrics)),
+        min_separation=float(min((m.min_separation for m in metrics), default=np.inf)),
+        mean_frame_ms=float(wall.mean()), p95_frame_ms=float(np.percentile(wall, 95)), agents=n0,
+        seed=config.seed, frames=frame, terminated=ids.shape[0] == 0, arrived=len(arrival),
+        total_fallbacks=fallbacks, mean_travel_time=travel)
+    return RunResult(frame_logs=logs, frame_metrics=metrics, summary=summary,
+                     agent_records=agent_records, final_state=final_state)

@@ -20,10 +20,13 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from enum import IntEnum
 
+import math
+
 import numpy as np
 
 __all__ = ["AgentClass", "ResponsibilityMatrix", "ClassParams", "ScenarioConfig",
-           "SimState", "FrameMetrics", "DEFAULTS", "DEFAULT_CLASS_PARAMS"]
+           "SimState", "FrameMetrics", "FrameLog", "RunSummary", "RunResult", "DEFAULTS",
+           "DEFAULT_CLASS_PARAMS"]
 
 
 class AgentClass(IntEnum):
@@ -133,6 +136,22 @@ class ScenarioConfig:
             return self.goal_tolerance
         return self.class_params[AgentClass(agent_class)].radius
 
+    def frame_guard(self) -> int:
+        """max_frames, defaulting to a generous multiple of the straight-line crossing
+        time over the scenario extent (scenario.py:101-114). Regions are objects with
+        .spawn / .goal rectangles (x0, y0, x1, y1) and .agent_class."""
+        if self.max_frames is not None:
+            return self.max_frames
+        rects = [r.spawn for r in self.regions] + [r.goal for r in self.regions]
+        if not rects:
+            return 1
+        xs = [r[0] for r in rects] + [r[2] for r in rects]
+        ys = [r[1] for r in rects] + [r[3] for r in rects]
+        diag = math.hypot(max(xs) - min(xs), max(ys) - min(ys))
+        used = {AgentClass(r.agent_class) for r in self.regions}
+        min_pref = min(self.class_params[c].pref_speed for c in used)
+        return max(1, int(100.0 * (diag / min_pref) / self.dt))
+
 
 @dataclass
 class FrameMetrics:
@@ -165,3 +184,45 @@ class SimState:
     @property
     def active_count(self) -> int:
         return int(self.ids.shape[0])
+
+
+@dataclass
+class FrameLog:
+    """Positions and velocities of every agent active during one frame
+    (scenario.py:117-140): post-step values, arrivals of that frame included."""
+
+    frame: int
+    time: float
+    ids: np.ndarray
+    classes: np.ndarray
+    positions: np.ndarray
+    velocities: np.ndarray
+    radii: np.ndarray
+
+
+@dataclass
+class RunSummary:
+    """engine.py:90-102"""
+
+    total_collisions: int
+    min_separation: float
+    mean_frame_ms: float
+    p95_frame_ms: float
+    agents: int
+    seed: int
+    frames: int
+    terminated: bool
+    arrived: int
+    total_fallbacks: int
+    mean_travel_time: dict
+
+
+@dataclass
+class RunResult:
+    """engine.py:105-111"""
+
+    frame_logs: list
+    frame_metrics: list
+    summary: RunSummary
+    agent_records: list = field(default_factory=list)
+    final_state: SimState | None = None
