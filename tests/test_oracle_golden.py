@@ -147,3 +147,32 @@ def test_coincident_centres_error_text():
 def test_grid_range_error():
     with pytest.raises(ValueError, match="out of indexable grid range"):
         O.grid_arrays(np.array([[1e12, 0.0]]), 1.0)
+
+
+@pytest.mark.parametrize("name", ["run_two_way_80.npz", "run_four_way_96.npz"])
+def test_whole_run_bitwise(name):
+    """The oracle stepped in a loop reproduces the reference's engine.run of the built-in
+    crossing scenarios (spawned crowd taken from the fixture): frames, arrivals, metrics."""
+    from paper_2008_11578_b200.types import (AgentClass, ResponsibilityMatrix, ScenarioConfig,
+                                             SimState)
+    g = load_golden(name)
+    fm = g["fmat"]
+    P, V = AgentClass.PEDESTRIAN, AgentClass.VEHICLE
+    cfg = ScenarioConfig(responsibility=ResponsibilityMatrix({(P, P): fm[0, 0], (P, V): fm[0, 1],
+                                                              (V, P): fm[1, 0], (V, V): fm[1, 1]}),
+                         dt=float(g["dt"]), tau=float(g["tau"]), neighbor_radius=float(g["neighbor_radius"]),
+                         max_neighbors=int(g["max_neighbors"]), avoidance_margin=float(g["avoidance_margin"]))
+    st = SimState(frame=0, time=0.0, ids=g["ids"].astype(np.int64), positions=g["positions"],
+                  velocities=g["velocities"], radii=g["radii"], pref_speeds=g["pref_speeds"],
+                  max_speeds=g["max_speeds"], goals=g["goals"], goal_tols=g["goal_tols"],
+                  class_codes=g["class_codes"].astype(np.int64))
+    f = 0
+    fallbacks = collisions = 0
+    while st.ids.shape[0] > 0 and st.frame < int(g["guard"]):
+        st, sep, coll, fb, _removed = O.advance(st, cfg)
+        assert sep == g["m_min_sep"][f] and coll == g["m_coll"][f] and st.ids.shape[0] == g["m_active"][f]
+        fallbacks += fb
+        collisions += coll
+        f += 1
+    assert f == int(g["frames"]) and fallbacks == int(g["total_fallbacks"])
+    assert collisions == int(g["total_collisions"])
