@@ -27,6 +27,9 @@
 #ifndef ORCA_SCAN_UNROLL
 #define ORCA_SCAN_UNROLL 4
 #endif
+#ifndef ORCA_LP_RUNAHEAD
+#define ORCA_LP_RUNAHEAD 1 // k_solve: per-lane run-ahead LP (orca_math.cuh, lp2_target_runahead)
+#endif
 
 namespace orca {
 
@@ -733,9 +736,11 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     u8 *sm_perm = smem_raw + sizeof(typename Vec<R>::T4) * MAXN * THREADS;
 
     const int s = s0 + blockIdx.x * THREADS + threadIdx.x; // sorted slots [s0, s1)
-    if (s >= min(s1, plan->n)) return;
-    const int row = s_row[s];
-    if (row >= plan->n_owned) return; // halo ghost: searched, never solved
+    const bool in_range = s < min(s1, plan->n);
+    const int row = in_range ? s_row[s] : 0;
+    const bool active = in_range && row < plan->n_owned; // halo ghosts are searched, never solved
+    const unsigned live = __ballot_sync(0xFFFFFFFFu, active);
+    if (!active) return;
 
     const int cnt = nb_cnt[s];
     const typename Vec<S>::T4 me = s_pv[s];
@@ -745,7 +750,16 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
 
     shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(plan->frame, ids[row]));
     int bad_j = -1;
-    if (!build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, THREADS, cons, bad_j)) {
+    const bool built = build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, THREADS, cons, bad_j);
+#if !ORCA_LP_RUNAHEAD
+    if (!built) {
+#else
+    int fail_pos;
+    R vx, vy;
+    const bool feasible =
+        lp2_target_runahead<R, SmemCons<R>>(cons, cnt, dm.z, dm.x, dm.y, fail_pos, vx, vy, live, built);
+    if (!built) {
+#endif
         // _kernels.py:542-547 + engine.py:239-245
         if (plan->err_frame < 0) // sticky: only the first failing frame is reported
             atomicMin(&plan->err_pair, ((u64)(unsigned)row << 32) | (u64)(unsigned)s_row[bad_j]);
@@ -754,10 +768,12 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
         integrate_row<S, R>(row, me, (R)me.z, (R)me.w, P, goalpref, pv_out, arrived);
         return;
     }
-
+#if !ORCA_LP_RUNAHEAD
     int fail_pos;
     R vx, vy;
-    if (lp2_target<R, false, SmemCons<R>>(cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy)) {
+    const bool feasible = lp2_target<R, false, SmemCons<R>>(cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy);
+#endif
+    if (feasible) {
         status[row] = 0;
         failed_at[row] = -1;
         integrate_row<S, R>(row, me, vx, vy, P, goalpref, pv_out, arrived);

@@ -72,9 +72,81 @@ __device__ __forceinline__ uint32_t mod_small(u64 x, uint32_t m)
 // Returns false only for exactly coincident centres. (ux,uy) is the shortest
 // displacement of the relative velocity to the VO boundary, (nx,ny) the outward
 // unit normal there.
+#ifndef ORCA_VO_BRANCHY
+#define ORCA_VO_BRANCHY 0 // 1: the reference's control flow (A/B switch)
+#endif
+template <typename R>
+__device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
+                                                R &ux, R &uy, R &nx, R &ny);
+//
+// Two implementations with identical results (every value that reaches an output is
+// produced by the same operations on the same operands):
+//   vo_exit_branchy  the reference's control flow, one branch per case;
+//   vo_exit          the overlap / cut-off-arc / tangent-leg cases merged into ONE
+//                    straight-line sequence (one square root, two divisions, selects),
+//                    because in a warp of 32 agent-neighbour pairs ~28 lanes take the arc
+//                    and ~3 a leg, and the branchy form runs both paths back to back
+//                    (profiles/r01_notes.md). Only the two measure-zero cases (coincident
+//                    centres, |w|^2 < 1e-24) still branch.
 template <typename R>
 __device__ __forceinline__ bool vo_exit(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
                                         R &ux, R &uy, R &nx, R &ny)
+{
+#if ORCA_VO_BRANCHY
+    return vo_exit_branchy<R>(rpx, rpy, rvx, rvy, comb_r, tau, dt, ux, uy, nx, ny);
+#endif
+    const R d2 = rpx * rpx + rpy * rpy;
+    const R r2 = comb_r * comb_r;
+    const bool overlap = d2 < r2;                                   // K:357
+    const R inv_dt = div_rn<R>(R(1), dt), inv_tau = div_rn<R>(R(1), tau); // loop-invariant for callers
+    const R inv = overlap ? inv_dt : inv_tau;                       // K:358 / K:378
+    const R cx = rpx * inv, cy = rpy * inv;
+    const R rr = comb_r * inv;
+    const R wx = rvx - cx, wy = rvy - cy;
+    const R wl2 = wx * wx + wy * wy;
+    const R dot_wp = wx * rpx + wy * rpy;
+    if ((rpx == R(0) && rpy == R(0)) || wl2 < R(1e-24)) {           // measure-zero cases
+        if (rpx == R(0) && rpy == R(0)) {
+            ux = uy = nx = ny = R(0);
+            return false;
+        }
+        // relative velocity at the centre of the (dt or tau) disc, K:364-368 / K:387-393
+        const R d = sqrt_rn<R>(d2);
+        const R hx = div_rn<R>(-rpx, d), hy = div_rn<R>(-rpy, d);
+        ux = rr * hx; // overlap: (rr - 0) * h == rr * h exactly
+        uy = rr * hy;
+        nx = hx;
+        ny = hy;
+        return true;
+    }
+    const bool arc = overlap || (dot_wp < R(0) && dot_wp * dot_wp > r2 * wl2); // K:395
+    const R sq = sqrt_rn<R>(arc ? wl2 : d2 - r2);                   // |w|  or  leg
+    const bool side = rpx * wy - rpy * wx > R(0);                   // K:404
+    const R a1 = rpx * sq, a2 = rpy * comb_r, b1 = rpx * comb_r, b2 = rpy * sq;
+    const R lx = side ? a1 - a2 : -(a1 + a2);                       // K:405-410 numerators
+    const R ly = side ? b1 + b2 : b1 - b2;
+    const R den = arc ? sq : d2;
+    const R qx = div_rn<R>(arc ? wx : lx, den);                     // w/|w|  or  leg direction
+    const R qy = div_rn<R>(arc ? wy : ly, den);
+    // arc: K:397-401
+    const R s = rr - sq;
+    // leg: K:411-419
+    const R t = rvx * qx + rvy * qy;
+    R mx = -qy, my = qx;
+    if (mx * rpx + my * rpy > R(0)) {
+        mx = -mx;
+        my = -my;
+    }
+    ux = arc ? s * qx : t * qx - rvx;
+    uy = arc ? s * qy : t * qy - rvy;
+    nx = arc ? qx : mx;
+    ny = arc ? qy : my;
+    return true;
+}
+
+template <typename R>
+__device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
+                                                R &ux, R &uy, R &nx, R &ny)
 {
     if (rpx == R(0) && rpy == R(0)) {
         ux = uy = nx = ny = R(0);
@@ -280,6 +352,63 @@ __device__ __forceinline__ bool lp2_target(const V &view, int k, R zz, R cap, R 
     }
     fail_pos = -1;
     return true;
+}
+
+// K:122-146 again, same arithmetic, different loop nest for a warp of 32 independent LPs.
+// lp2_target walks the positions in lock step: at every position the ~2 lanes whose
+// constraint is violated run lp1_target while 30 wait (measured: 55 % of k_solve's warp
+// instructions at 2 of 32 lanes, profiles/r02_notes.md). Here every lane first runs ahead
+// to ITS next violated position (a cheap scan), then all lanes that found one solve their
+// 1-D problems together: the warp pays max-over-lanes(#violations) rounds (~4) instead of
+// k (16). The vote between the two phases is what keeps them apart -- without it the
+// control-flow graph is the lock-step one and the compiler emits the same code.
+// `live` = the lanes of this warp that call the function (all of them must);
+// `enabled` = false lets a lane ride along without a problem of its own.
+template <typename R, typename V>
+__device__ __forceinline__ bool lp2_target_runahead(const V &view, int k, R cap, R tx, R ty,
+                                                    int &fail_pos, R &vx, R &vy, unsigned live,
+                                                    bool enabled)
+{
+    const R t2 = tx * tx + ty * ty;
+    if (t2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(t2));
+        vx = tx * s;
+        vy = ty * s;
+    } else {
+        vx = tx;
+        vy = ty;
+    }
+    int i_pos = 0;
+    bool done = !enabled, ok = true;
+    fail_pos = -1;
+    while (true) {
+        bool found = false;
+        if (!done) {
+            for (; i_pos < k; ++i_pos) {
+                R px, py, nx, ny;
+                view.get(i_pos, px, py, nx, ny);
+                if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+                    found = true;
+                    break;
+                }
+            }
+            done = !found;
+        }
+        if (!__any_sync(live, found)) break;
+        if (found) {
+            R nvx, nvy;
+            if (lp1_target<R, false, V>(view, i_pos, R(0), cap, tx, ty, nvx, nvy)) {
+                vx = nvx;
+                vy = nvy;
+                ++i_pos;
+            } else {
+                fail_pos = i_pos;
+                ok = false;
+                done = true;
+            }
+        }
+    }
+    return ok;
 }
 
 // K:153-190, identity order over the projected constraints
