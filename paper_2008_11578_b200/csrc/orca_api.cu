@@ -74,7 +74,10 @@ struct orca_sim {
     int r0_override = 0;       // ORCA_R0: force the first ring radius (experiments)
     int fb_lanes = 8;          // ORCA_FB_LANES: lanes per warp that take a fallback agent
     bool gather_fast = true;   // ORCA_GATHER_FAST=0: exact ring search for every agent
+    bool gather_keys32 = true; // ORCA_GATHER_KEYS32=0: FP64-keyed fast pass (k_gather_fast)
     bool fb_coop = true;       // ORCA_FB_COOP=0: thread-per-agent least-penetration stage
+    int solve_gl = 2;          // ORCA_SOLVE_GL: lanes per agent in the LP kernel (1, 2 or 4);
+                               //  default 2 with FP64 arithmetic, 1 with FP32 (measured)
     bool use_graph = true;     // ORCA_GRAPH=0: launch the step's kernels one by one
     int chunks = 1;            // ORCA_CHUNKS: gather+solve ranges issued on two streams
     cudaStream_t aux_stream = nullptr;
@@ -171,6 +174,12 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::solve_bpt * C::solve_threads);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::solve_bpt * 64);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::solve_bpt * 32);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::fb_bpt * (C::fb_threads / 32) * 16);
@@ -254,7 +263,10 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     }
     if (const char *r0 = getenv("ORCA_R0")) sim->r0_override = atoi(r0);
     if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
+    if (const char *gk = getenv("ORCA_GATHER_KEYS32")) sim->gather_keys32 = atoi(gk) != 0;
     if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
+    sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
+    if (const char *sg = getenv("ORCA_SOLVE_GL")) sim->solve_gl = atoi(sg) >= 4 ? 4 : (atoi(sg) >= 2 ? 2 : 1);
     if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
     if (const char *ch = getenv("ORCA_CHUNKS")) sim->chunks = std::min(ORCA_MAX_CHUNKS, std::max(1, atoi(ch)));
     if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
@@ -683,7 +695,12 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         const int s0 = (int)std::min<int64_t>(n, c * per), s1 = (int)std::min<int64_t>(n, (c + 1) * per);
         const int64_t m = s1 - s0;
         if (m <= 0) continue;
-        if (sim->gather_fast)
+        if (sim->gather_fast && sim->gather_keys32)
+            k_gather_fast32<S, MAXN, 48><<<grid_for(m, 128), 128, 0, cs>>>(
+                sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+                reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, s0, s1,
+                c);
+        else if (sim->gather_fast)
             k_gather_fast<S, MAXN, 48><<<grid_for(m, 128), 128, 0, cs>>>(
                 sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
                 sim->ids[a], reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt,
@@ -696,12 +713,19 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
             sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
             sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, s0, c);
         if (chunks == 1) sim->mark();
-        k_solve<S, R, MAXN, C::solve_threads><<<grid_for(m, C::solve_threads), C::solve_threads,
-                                                C::solve_bpt * C::solve_threads, cs>>>(
-            sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
-            reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
-            reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
-            sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1);
+#define ORCA_SOLVE_ARGS                                                                                    \
+    sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),        \
+        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
+        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
+        sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1
+        if (sim->solve_gl == 2)
+            k_solve_group<S, R, MAXN, 128, 2><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(ORCA_SOLVE_ARGS);
+        else if (sim->solve_gl == 4)
+            k_solve_group<S, R, MAXN, 128, 4><<<grid_for(m, 32), 128, C::solve_bpt * 32, cs>>>(ORCA_SOLVE_ARGS);
+        else
+            k_solve<S, R, MAXN, C::solve_threads><<<grid_for(m, C::solve_threads), C::solve_threads,
+                                                    C::solve_bpt * C::solve_threads, cs>>>(ORCA_SOLVE_ARGS);
+#undef ORCA_SOLVE_ARGS
         sim->launches += 3;
     }
     if (chunks > 1) {

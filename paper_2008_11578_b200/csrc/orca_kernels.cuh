@@ -517,6 +517,160 @@ k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::
     }
 }
 
+// Fast pass, 32-bit keys. Same contract as k_gather_fast (provably exact list, or the
+// agent goes to the exact ring search), different selection arithmetic: the candidates
+// that pass the FP32 distance test are ranked by ONE 32-bit integer each,
+//     key = (bits of the FP32 squared distance with the low 6 mantissa bits cleared) | slot
+// where slot < 64 is the candidate's position in the shared-memory buffer. Positive
+// floats order like their bit patterns, so the sorting network and the insertion of the
+// candidates beyond max_n are plain integer min / max pairs (2 instructions per
+// compare-exchange, 16 registers for the list, against an FP64 compare + 6 selects and 48
+// registers). The order is the exact (d2, id) order whenever neighbouring keys differ by
+// at least 2 units of the kept 17 mantissa bits (2^-17 relative; FP32 evaluation error is
+// below 2^-21), which is checked on the final list and against the closest rejected
+// candidate; otherwise -- about 0.4 % of agents, and every exact tie -- the agent is
+// queued for k_gather. Nothing here decides a result that FP64 would decide differently.
+template <typename R, int MAXN, int CAP>
+__global__ void __launch_bounds__(128)
+k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *__restrict__ s_xy,
+                const int *__restrict__ cell_start, const int *__restrict__ s_cell,
+                const int *__restrict__ s_row, const typename Vec<R>::T2 *__restrict__ radmax,
+                float *__restrict__ hint, int *__restrict__ nb, u8 *__restrict__ nb_cnt,
+                int *__restrict__ gq, int s0, int s1, int chunk)
+{
+    static_assert(CAP <= 64, "slot must fit the 6 cleared mantissa bits");
+    __shared__ int buf[CAP * 128];
+    const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= min(s1, plan->n)) return;
+    const int row = s_row[s];
+    if (row >= plan->n_owned || P.max_n == 0) {
+        nb_cnt[s] = 0;
+        return;
+    }
+    const float h = hint[row];
+    const double rad2 = P.rad2;
+    const int max_n = P.max_n;
+    const typename Vec<R>::T2 me = s_xy[s];
+    const double mx = (double)me.x, my = (double)me.y;
+    double b = (double)h + ((double)radmax[row].y + plan->vmax) * P.dt * (1.0 + 1e-6) + 1e-3;
+    const double T = fmin(b * b, rad2);
+    const float T_f = __double2float_ru(T * (1.0 + 1e-6));
+    // scanning (nearly) the whole radius: the d2 <= rad2 cut itself must be exact (K:470)
+    const bool full = T * (1.0 + 1e-5) >= rad2;
+
+    const int nx = plan->nx, ny = plan->ny;
+    const int c0 = s_cell[s];
+    const int cx = c0 / ny, cy = c0 - cx * ny;
+    const int r = min(plan->rmax, (int)(sqrt(T) * plan->inv_cell * (1.0 + 1e-9)) + 1);
+    const int gx_lo = max(cx - r, 0), gx_hi = min(cx + r, nx - 1);
+    const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
+    int *my_buf = buf + threadIdx.x;
+
+    auto d2_f32 = [&](const typename Vec<R>::T2 &q) -> float {
+        float dxf, dyf;
+        if (Fmt<R>::is_f32) {
+            dxf = (float)q.x - (float)me.x;
+            dyf = (float)q.y - (float)me.y;
+        } else {
+            dxf = (float)((double)q.x - mx);
+            dyf = (float)((double)q.y - my);
+        }
+        return dxf * dxf + dyf * dyf;
+    };
+
+    int nbuf = 0;
+    for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+        const int *cs = cell_start + gx * ny;
+        const int e = cs[y_hi + 1];
+        constexpr int kScanUnroll = ORCA_SCAN_UNROLL;
+#pragma unroll kScanUnroll
+        for (int s2 = cs[y_lo]; s2 < e; ++s2) {
+            if (d2_f32(s_xy[s2]) <= T_f && s2 != s) {
+                if (nbuf < CAP) my_buf[nbuf * 128] = s2;
+                ++nbuf;
+            }
+        }
+    }
+    bool ok = nbuf <= CAP;
+    if (ok) {
+        auto make_key = [&](int e) -> unsigned {
+            const typename Vec<R>::T2 q = s_xy[my_buf[e * 128]];
+            unsigned k = (__float_as_uint(d2_f32(q)) & ~63u) | (unsigned)e;
+            if (full) {
+                const double dx = (double)q.x - mx, dy = (double)q.y - my;
+                if (dx * dx + dy * dy > rad2) k = 0xFFFFFFFFu;
+            }
+            return k;
+        };
+        // sentinels 0 in front so the list proper is the last max_n registers
+        const int off = MAXN - max_n;
+        unsigned key[MAXN];
+#pragma unroll
+        for (int t = 0; t < MAXN; ++t) {
+            const int e = t - off;
+            key[t] = e < 0 ? 0u : 0xFFFFFFFFu;
+            if (e >= 0 && e < nbuf) key[t] = make_key(e);
+        }
+#define CEX(a, b)                                                                                  \
+    {                                                                                              \
+        const unsigned lo_ = min(key[a], key[b]), hi_ = max(key[a], key[b]);                       \
+        key[a] = lo_;                                                                              \
+        key[b] = hi_;                                                                              \
+    }
+        if constexpr (MAXN == 16) {
+            ORCA_SORTNET_16
+        } else {
+            ORCA_SORTNET_32
+        }
+#undef CEX
+        // the candidates beyond max_n: min/max chain through the sorted list; what falls
+        // off the end is rejected, and the closest rejected key is remembered
+        unsigned rej = 0xFFFFFFFFu;
+        for (int e = max_n; e < nbuf; ++e) {
+            unsigned x = make_key(e);
+#pragma unroll
+            for (int t = 0; t < MAXN; ++t) {
+                const unsigned lo_ = min(key[t], x);
+                x = max(key[t], x);
+                key[t] = lo_;
+            }
+            rej = min(rej, x);
+        }
+        // separated by >= 2 units of the kept mantissa bits => same order as exact (d2, id)
+        int cnt = 0;
+        unsigned prev = 0u; // sentinel / nothing
+#pragma unroll
+        for (int t = 0; t < MAXN; ++t) {
+            const bool real = t >= off && key[t] != 0xFFFFFFFFu;
+            if (real) {
+                ok = ok && ((key[t] >> 6) >= (prev >> 6) + 2u);
+                prev = key[t];
+                ++cnt;
+            }
+        }
+        if (rej != 0xFFFFFFFFu) ok = ok && ((rej >> 6) >= (prev >> 6) + 2u);
+        // exact squared distance of the last kept entry: the acceptance test and the hint
+        double d2_last = 0.0;
+        if (cnt > 0) {
+            const typename Vec<R>::T2 q = s_xy[my_buf[(int)(prev & 63u) * 128]]; // prev = last real key
+            const double dx = (double)q.x - mx, dy = (double)q.y - my;
+            d2_last = dx * dx + dy * dy;
+        }
+        ok = ok && (T >= rad2 || (cnt == max_n && d2_last <= T));
+        if (ok) {
+            nb_cnt[s] = (u8)cnt;
+#pragma unroll
+            for (int t = 0; t < MAXN; ++t) {
+                const int slot = t - off;
+                if (slot >= 0 && slot < cnt) nb[(size_t)slot * P.stride + s] = my_buf[(int)(key[t] & 63u) * 128];
+            }
+            hint[row] = cnt == max_n ? __double2float_ru(__dsqrt_ru(d2_last)) : __int_as_float(0x7F800000);
+            return;
+        }
+    }
+    gq[s0 + atomicAdd(&plan->gq_count[chunk], 1)] = s;
+}
+
 // every owned agent goes to the exact ring search (fast pass disabled)
 __global__ void __launch_bounds__(256)
 k_enqueue_all(GridPlan *__restrict__ plan, int max_n, const int *__restrict__ s_row,
@@ -782,6 +936,95 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     // queue for the least-penetration stage (warp-aggregated by the compiler)
     status[row] = 1;
     failed_at[row] = (i8)perm[fail_pos * THREADS];
+    const int q = atomicAdd(&plan->fq_count, 1);
+    fq[q] = s;
+    fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
+}
+
+// k_solve with GL (2 or 4) adjacent lanes per agent. k_solve is bound by the latency of
+// dependent FP64 chains at the 12 warps/SM its shared memory allows (512 B of constraints
+// per thread). A group shares ONE agent's constraints, so the same shared memory holds GL
+// times more threads, each with a 1/GL share of the serial work: lane gl builds the
+// half-planes at positions gl, gl+GL, ..., the run-ahead scan is executed redundantly and
+// the j loops of the 1-D solves are split over the group (max / min / any combinations:
+// exact and order-independent, so results are unchanged).
+template <typename S, typename R, int MAXN, int THREADS, int GL>
+__global__ void __launch_bounds__(THREADS, (GL == 2 ? 6 : 8))
+k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__restrict__ s_pv,
+              const typename Vec<R>::T4 *__restrict__ s_dm, const typename Vec<S>::T2 *__restrict__ s_rc,
+              const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
+              const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
+              typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
+              i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
+              typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int NG = THREADS / GL; // agents per block
+    typename Vec<R>::T4 *sm_cons = reinterpret_cast<typename Vec<R>::T4 *>(smem_raw);
+    u8 *sm_perm = smem_raw + sizeof(typename Vec<R>::T4) * MAXN * NG;
+
+    const int g = threadIdx.x / GL, gl = threadIdx.x % GL;
+    const int gshift = (threadIdx.x & 31) - gl;
+    const unsigned gmask = ((1u << GL) - 1u) << gshift;
+    const int s = s0 + blockIdx.x * NG + g;
+    const bool in_range = s < min(s1, plan->n);
+    const int row = in_range ? s_row[s] : 0;
+    const bool active = in_range && row < plan->n_owned;
+    const unsigned live = __ballot_sync(0xFFFFFFFFu, active);
+    if (!active) return; // uniform over the group
+
+    const int cnt = nb_cnt[s];
+    const typename Vec<S>::T4 me = s_pv[s];
+    const typename Vec<R>::T4 dm = s_dm[s];
+    u8 *perm = sm_perm + g;
+    SmemCons<R> cons{sm_cons + g, NG};
+
+    if (gl == 0) shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
+    __syncwarp(gmask);
+    bool ok_mine = true;
+    {   // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
+        const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
+        const typename Vec<S>::T2 rc_i = s_rc[s];
+        const R ri = (R)((double)rc_i.x + P.half_margin);
+        const int ci = (int)rc_i.y;
+        const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
+        const R tau = (R)P.tau, dt = (R)P.dt;
+#pragma unroll 2
+        for (int pos = gl; pos < cnt; pos += GL) {
+            const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
+            const typename Vec<S>::T4 qv = s_pv[j];
+            const typename Vec<S>::T2 rc_j = s_rc[j];
+            const R rj = (R)((double)rc_j.x + P.half_margin);
+            R ux, uy, nx, ny;
+            ok_mine &= vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, tau,
+                                  dt, ux, uy, nx, ny);
+            const R f = rc_j.y != S(0) ? f1 : f0;
+            cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
+        }
+    }
+    const bool built = (__ballot_sync(gmask, !ok_mine) & gmask) == 0u; // also orders the stores
+    int fail_pos;
+    R vx, vy;
+    const bool feasible = g_lp2_target_runahead<R, GL, SmemCons<R>>(cons, cnt, dm.z, dm.x, dm.y, fail_pos, vx,
+                                                                     vy, live, built, gl, gmask);
+    if (gl != 0) return;
+    if (!built) {
+        // _kernels.py:542-547 + engine.py:239-245; coincident neighbours lead the list
+        if (plan->err_frame < 0)
+            atomicMin(&plan->err_pair, ((u64)(unsigned)row << 32) | (u64)(unsigned)s_row[nb[s]]);
+        status[row] = 0;
+        failed_at[row] = -1;
+        integrate_row<S, R>(row, me, (R)me.z, (R)me.w, P, goalpref, pv_out, arrived);
+        return;
+    }
+    if (feasible) {
+        status[row] = 0;
+        failed_at[row] = -1;
+        integrate_row<S, R>(row, me, vx, vy, P, goalpref, pv_out, arrived);
+        return;
+    }
+    status[row] = 1;
+    failed_at[row] = (i8)perm[fail_pos * NG];
     const int q = atomicAdd(&plan->fq_count, 1);
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));

@@ -695,6 +695,56 @@ __device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, 
     return true;
 }
 
+// lp2_target_runahead for a group of GL lanes per problem: the scan is executed
+// redundantly by the group's lanes (same data, same result), the 1-D solves split their
+// j loops over the group.
+template <typename R, int GL, typename V>
+__device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R cap, R tx, R ty,
+                                                      int &fail_pos, R &vx, R &vy, unsigned live,
+                                                      bool enabled, int gl, unsigned gmask)
+{
+    const R t2 = tx * tx + ty * ty;
+    if (t2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(t2));
+        vx = tx * s;
+        vy = ty * s;
+    } else {
+        vx = tx;
+        vy = ty;
+    }
+    int i_pos = 0;
+    bool done = !enabled, ok = true;
+    fail_pos = -1;
+    while (true) {
+        bool found = false;
+        if (!done) {
+            for (; i_pos < k; ++i_pos) {
+                R px, py, nx, ny;
+                view.get(i_pos, px, py, nx, ny);
+                if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+                    found = true;
+                    break;
+                }
+            }
+            done = !found;
+        }
+        if (!__any_sync(live, found)) break;
+        if (found) {
+            R nvx, nvy;
+            if (g_lp1_target<R, GL, false, V>(view, i_pos, R(0), cap, tx, ty, nvx, nvy, gl, gmask)) {
+                vx = nvx;
+                vy = nvy;
+                ++i_pos;
+            } else {
+                fail_pos = i_pos;
+                ok = false;
+                done = true;
+            }
+        }
+    }
+    return ok;
+}
+
 // K:153-190
 template <typename R, int GL, typename P>
 __device__ __forceinline__ bool g_lp1_dir(const P &proj, int upto, R cap, R ox, R oy, R &rx, R &ry, int gl,
