@@ -704,7 +704,17 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
     const double cell = plan->cell;
     const double rad2 = P.rad2;
     const int max_n = P.max_n;
-    for (int qi = blockIdx.x * blockDim.x + threadIdx.x; qi < nq; qi += gridDim.x * blockDim.x) {
+    // A short queue (the steady state: the few agents the fast pass could not certify) is
+    // spread over the warps of the grid, L entries per warp: with 32 unrelated searches in
+    // one warp every insertion of any lane stalls the other 31, and the kernel's time is the
+    // latency of its slowest warp. L reaches 32 (the plain thread-per-agent mapping, which
+    // keeps neighbouring agents in neighbouring lanes) when everyone is queued.
+    const int total_warps = gridDim.x * (blockDim.x >> 5);
+    const int L = min(32, max(1, (nq + total_warps - 1) / total_warps));
+    const int lane = threadIdx.x & 31;
+    if (lane >= L) return;
+    const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int qi = warp * L + lane; qi < nq; qi += total_warps * L) {
         const int s = gq[qi];
         const int row = s_row[s];
         const typename Vec<R>::T2 me = s_xy[s];
