@@ -51,6 +51,16 @@ SOLVE_BYTES_PER_AGENT = 16 + 32 + 1 + 4 * 16 + 1 + 16 + 16 + 2 + 1  # sorted sna
 BINS_BYTES_PER_AGENT = 16 + 4 + 4 + (16 + 16 + 8 + 1 + 8) + (8 + 16 + 32 + 4 + 4 + 1)  # bbox+count pass, scatter reads, scatter writes
 
 
+def load_traffic(workload, precision, kernel):
+    """ncu-measured DRAM bytes per launch of `kernel` (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(f"{workload}/{precision}", {})
+        return t.get(kernel), t.get("source")
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -263,13 +273,16 @@ def run_ours(args):
     host_state = type(state)(frame=0, time=0.0, rng_state=None, lp_fallbacks=0, **pinned)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
     cur = host_state
-    for _ in range(5):      # warm-up: pinned-buffer pool, first full upload, graph capture
+    for _ in range(5):      # warm-up: first full upload, graph capture (the pinned pool is pre-warmed)
         cur, _m = E.step(cur, cfg, precision=args.precision, device=local)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h2d = d2h = 0
+    per_call = []
     for _ in range(e2e_steps):
+        tc = time.perf_counter()
         cur, metrics = E.step(cur, cfg, precision=args.precision, device=local)
+        per_call.append((time.perf_counter() - tc) * 1e3)
         # bytes actually copied: positions + velocities always; the 7 attribute arrays
         # (72 B/agent) only when not already resident / re-read after arrivals
         h2d += E.step.last_traffic[0]
@@ -277,6 +290,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     e2e_value = n / e2e_ms * 1e3
+    print("e2e per-call ms:", " ".join(f"{t:.2f}" for t in per_call), file=sys.stderr)
 
     # ---- e2e through the C ABI with pinned buffers (positions/velocities only) ---
     sim = Simulation(cfg, capacity=n, precision=args.precision, device=local, remove_arrivals=False,
@@ -304,6 +318,10 @@ def run_ours(args):
     cpu_value, _ = cpu_port_rate(state, cfg, rows, threads, repeats=2)
     cpu1_value, _ = cpu_port_rate(state, cfg, max(1024, rows // 32), 1)
 
+    dom_kernel = {"bins": "k_scatter", "gather": "k_gather_fast32",
+                  "solve": "k_solve" if args.precision == "f32" else "k_solve_group",
+                  "fallback": "k_fallback_coop"}[dom]
+    traffic, traffic_src = load_traffic(args.workload, args.precision, dom_kernel)
     dtype = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision]
     wl.update(precision=args.precision,
               cache="state advances every step; per-step working set ~%.0f MB > 126 MB L2, no flush"
@@ -322,10 +340,9 @@ def run_ours(args):
                                     "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 40 * n}},
         "gpu_launches": launches,
         "stages_ms": stage_ms,
-        "roofline": {"bound": "hbm", "kernel": {"bins": "k_count+k_scan+k_scatter", "gather": "k_gather",
-                                                "solve": "k_solve", "fallback": "k_fallback"}[dom],
+        "roofline": {"bound": "hbm", "kernel": dom_kernel,
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "step_frac": STEP_BYTES_PER_AGENT * n / (ms_step * 1e-3) / 1e9 / hbm_peak,
                      "note": "the step is issue/latency bound, not HBM bound (DESIGN.md s5); "

@@ -80,6 +80,7 @@ k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__res
            typename Vec<R>::T4 *__restrict__ fq_state)
 {
     const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned live = __ballot_sync(0xFFFFFFFFu, i < n);
     if (i >= n) return;
     const i64 lo = coff[i];
     const int k = (int)(coff[i + 1] - lo);
@@ -101,7 +102,9 @@ k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__res
     GlobalShuf<R> shuf{cons + lo, perm};
     int fail_pos;
     R vx, vy;
-    if (lp2_target<R, false, GlobalShuf<R>>(shuf, k, R(0), pr.z, pr.x, pr.y, fail_pos, vx, vy)) {
+    // per-lane run-ahead (orca_math.cuh): the problems of a warp differ in k and in where
+    // their constraints are violated
+    if (lp2_target_runahead<R, GlobalShuf<R>>(shuf, k, pr.z, pr.x, pr.y, fail_pos, vx, vy, live, true)) {
         out_v[2 * i] = (double)vx;
         out_v[2 * i + 1] = (double)vy;
         out_status[i] = 0;

@@ -348,7 +348,22 @@ def _handle_for(config, n: int, precision, device: int) -> Simulation:
                          remove_arrivals=True, compute_metrics=True)
         sim._resident = None
         _handles[key] = sim
+        _prewarm_host_buffers(n)       # the allocator pools by rounded size: warm the size in use
     return sim
+
+
+def _prewarm_host_buffers(n: int):
+    """Page-locking host memory costs ~0.3 ms per MB the first time. A step() loop needs,
+    live at once, the returned state and the previous one: 2 x (pos, vel) always and, on
+    a frame that removes arrived agents, 2 x the seven attribute arrays as well. Allocate
+    and release them once so the caching pinned allocator serves every later call,
+    including the first frame with arrivals, from its pool."""
+    bufs = []
+    for _ in range(2):
+        bufs += [_host_empty((n, 2)) for _ in range(3)]                 # positions, velocities, goals
+        bufs += [_host_empty(n) for _ in range(4)]                      # radii, pref, max, tolerances
+        bufs += [_host_empty(n, np.int64) for _ in range(2)]            # ids, classes
+    del bufs
 
 
 def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
