@@ -195,6 +195,21 @@ ORCA_API int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const doubl
                    const double *velocities, double *new_positions, double *new_velocities,
                    int64_t *out_status);
 
+/* engine._advance through host buffers (engine.py:194-295; what engine.step,
+ * engine.py:298-308, does per call once the static agent attributes are
+ * resident from orca_upload): host positions/velocities [n,2] in, the new state's
+ * positions/velocities out, arrival removal and frame metrics per orca_params,
+ * counters in *info (orca_get_info). The copies overlap the step: the bin build
+ * and neighbour gather run on the positions while the velocities are still being
+ * copied in, and the result is copied out while the metrics are computed.
+ * new_positions/new_velocities must hold n rows; rows [0, info->active_agents)
+ * are the new state, in storage order (engine.py:288-294). When agents were
+ * removed (info->removed_agents > 0) fetch the compacted attributes with
+ * orca_download. Pinned host memory makes the copies asynchronous. */
+ORCA_API int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
+                      const double *velocities, double *new_positions, double *new_velocities,
+                      orca_info *info);
+
 /* ---- parity taps (pre-step snapshot of the LAST step; storage-row order) --- */
 
 /* cell_ix/cell_iy: floor(pos / neighbor_radius) as int64 (engine.py:150-151).

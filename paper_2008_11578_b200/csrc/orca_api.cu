@@ -82,6 +82,10 @@ struct orca_sim {
     int chunks = 1;            // ORCA_CHUNKS: gather+solve ranges issued on two streams
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // orca_advance_host: copies overlapped with the step (see there)
+    cudaEvent_t ev_vel = nullptr, ev_state = nullptr, ev_dl = nullptr;
+    bool split_vel = false;             // velocities arrive on aux_stream; patched in before k_solve
+    double *early_pos = nullptr, *early_vel = nullptr; // host targets of the early download
 
     // CUDA graphs of one whole step, keyed by everything the launch sequence depends on
     struct StepGraph {
@@ -235,6 +239,9 @@ extern "C" void orca_destroy(orca_sim *sim)
     if (sim->aux_stream) cudaStreamDestroy(sim->aux_stream);
     if (sim->ev_fork) cudaEventDestroy(sim->ev_fork);
     if (sim->ev_join) cudaEventDestroy(sim->ev_join);
+    if (sim->ev_vel) cudaEventDestroy(sim->ev_vel);
+    if (sim->ev_state) cudaEventDestroy(sim->ev_state);
+    if (sim->ev_dl) cudaEventDestroy(sim->ev_dl);
     delete sim;
 }
 
@@ -290,6 +297,9 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(cudaStreamCreateWithFlags(&sim->aux_stream, cudaStreamNonBlocking));
     CKC(cudaEventCreateWithFlags(&sim->ev_fork, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&sim->ev_join, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&sim->ev_vel, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&sim->ev_state, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&sim->ev_dl, cudaEventDisableTiming));
     for (int i = 0; i < 3; ++i) CKC(cudaMalloc(&sim->pv[i], cap * 4 * rs));
     for (int i = 0; i < 2; ++i) {
         CKC(cudaMalloc(&sim->goalpref[i], cap * 4 * rs));
@@ -713,6 +723,15 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
             sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
             sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, s0, c);
         if (chunks == 1) sim->mark();
+        if (sim->split_vel) {
+            // the velocities were still in flight while the bins and the neighbour lists
+            // were built from the positions; they are needed from here on
+            CK(sim, cudaStreamWaitEvent(cs, sim->ev_vel, 0));
+            k_patch_vel<S><<<grid_for(n, 256), 256, 0, cs>>>(
+                sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
+                reinterpret_cast<S4 *>(sim->s_pv), sim->cell_of, sim->rank_of, sim->cell_start);
+            sim->launches += 1;
+        }
 #define ORCA_SOLVE_ARGS                                                                                    \
     sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),        \
         reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
@@ -858,6 +877,25 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     sim->mark();
     sim->frame += 1;
     sim->binned_frame = -1;
+    if (sim->early_pos || sim->early_vel) {
+        // the step's result is final here: ship it to the host on the copy stream while
+        // this stream goes on with the metrics
+        typedef typename Vec<S>::T4 S4;
+        const int64_t m = sim->n_pre; // rows beyond the kept ones are don't-care
+        CK(sim, cudaEventRecord(sim->ev_state, sim->stream));
+        CK(sim, cudaStreamWaitEvent(sim->aux_stream, sim->ev_state, 0));
+        k_export_pv<S><<<grid_for(m, 256), 256, 0, sim->aux_stream>>>(
+            (int)m, reinterpret_cast<const S4 *>(sim->pv[sim->cur]), sim->stg, sim->stg + 2 * m);
+        CKL(sim);
+        if (sim->early_pos)
+            CK(sim, cudaMemcpyAsync(sim->early_pos, sim->stg, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost,
+                                    sim->aux_stream));
+        if (sim->early_vel)
+            CK(sim, cudaMemcpyAsync(sim->early_vel, sim->stg + 2 * m, sizeof(double) * 2 * m,
+                                    cudaMemcpyDeviceToHost, sim->aux_stream));
+        CK(sim, cudaEventRecord(sim->ev_dl, sim->aux_stream));
+        sim->launches += 1;
+    }
     if (sim->params.compute_metrics) {
         // engine.py:270-286: metrics of the post-step, post-removal positions. The bin
         // build it needs is the one the next step would do anyway, so it is kept.
@@ -1007,6 +1045,70 @@ extern "C" int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const dou
         }
     }
     return fetch_plan(sim);
+}
+
+// engine._advance through host buffers with the copies overlapped (engine.py:194-295 with
+// the static attributes resident): positions go up first and the bin build + neighbour
+// gather start on them while the velocities are still on the wire; the new positions and
+// velocities go down on the copy stream while the metrics of the new state are computed.
+// Rows [0, info->active_agents) of new_positions / new_velocities are the new state (the
+// buffers must hold n rows). Same results as orca_upload_pv + orca_step + orca_download_pv.
+extern "C" int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
+                                 const double *velocities, double *new_positions, double *new_velocities,
+                                 orca_info *info)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_advance_host: no resident state");
+    if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_advance_host: orca_set_params was not called");
+    if (n != sim->n_bound || sim->ghost_bound != 0)
+        return fail(sim, ORCA_EINVAL, "orca_advance_host: n = %lld but %lld rows are resident", (long long)n,
+                    (long long)sim->n_bound);
+    if (!info || (n > 0 && (!positions || !velocities || !new_positions || !new_velocities)))
+        return fail(sim, ORCA_EINVAL, "orca_advance_host: NULL argument");
+    CK(sim, cudaSetDevice(sim->device));
+    sim->frame = frame;
+    sim->binned_frame = -1;
+    k_set_frame<<<1, 1, 0, sim->stream>>>(sim->plan, frame);
+    CKL(sim);
+    int rc = ORCA_OK;
+    if (n > 0) {
+        cudaStream_t st = sim->stream, cp = sim->aux_stream;
+        double *d_pos = sim->stg, *d_vel = sim->stg + 2 * n;
+        // earlier work on the main stream (a previous download) may still read the staging area
+        CK(sim, cudaEventRecord(sim->ev_fork, st));
+        CK(sim, cudaStreamWaitEvent(cp, sim->ev_fork, 0));
+        CK(sim, cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
+        CK(sim, cudaMemcpyAsync(d_vel, velocities, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, cp));
+        CK(sim, cudaEventRecord(sim->ev_vel, cp));
+        if (sim->precision != ORCA_F64)
+            k_import_pos<float><<<grid_for(n, 256), 256, 0, st>>>((int)n, d_pos,
+                                                                  reinterpret_cast<float4 *>(sim->pv[sim->cur]));
+        else
+            k_import_pos<double><<<grid_for(n, 256), 256, 0, st>>>((int)n, d_pos,
+                                                                   reinterpret_cast<double4 *>(sim->pv[sim->cur]));
+        CKL(sim);
+        sim->split_vel = sim->chunks <= 1;
+        if (!sim->split_vel) { // chunked gather/solve: no overlap, patch right away
+            CK(sim, cudaStreamWaitEvent(st, sim->ev_vel, 0));
+            if (sim->precision != ORCA_F64)
+                k_import_pv<float><<<grid_for(n, 256), 256, 0, st>>>((int)n, d_pos, d_vel,
+                                                                     reinterpret_cast<float4 *>(sim->pv[sim->cur]));
+            else
+                k_import_pv<double><<<grid_for(n, 256), 256, 0, st>>>(
+                    (int)n, d_pos, d_vel, reinterpret_cast<double4 *>(sim->pv[sim->cur]));
+            CKL(sim);
+        }
+        sim->early_pos = new_positions;
+        sim->early_vel = new_velocities;
+        rc = step_plain(sim);
+        sim->split_vel = false;
+        sim->early_pos = sim->early_vel = nullptr;
+        if (rc) return rc;
+        CK(sim, cudaStreamWaitEvent(st, sim->ev_dl, 0)); // fetch_plan's sync then covers the copies
+    } else {
+        rc = step_plain(sim);
+        if (rc) return rc;
+    }
+    return orca_get_info(sim, info);
 }
 
 // ---------------------------------------------------------------------------

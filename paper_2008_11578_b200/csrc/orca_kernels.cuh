@@ -1437,6 +1437,38 @@ k_import_pv(int n, const double *__restrict__ pos, const double *__restrict__ ve
     pv[i] = mk4((R)pos[2 * i], (R)pos[2 * i + 1], (R)vel[2 * i], (R)vel[2 * i + 1]);
 }
 
+// positions only (orca_advance_host): the velocity half of pv keeps its old content until
+// k_patch_vel replaces it
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_import_pos(int n, const double *__restrict__ pos, typename Vec<R>::T4 *__restrict__ pv)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    typename Vec<R>::T4 a = pv[i];
+    a.x = (R)pos[2 * i];
+    a.y = (R)pos[2 * i + 1];
+    pv[i] = a;
+}
+
+// velocities that arrived after the bin build: into the row-ordered state and into the
+// cell-sorted snapshot k_scatter already wrote (slot = cell_start[cell] + rank)
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_patch_vel(const GridPlan *__restrict__ plan, const double *__restrict__ vel,
+            typename Vec<R>::T4 *__restrict__ pv, typename Vec<R>::T4 *__restrict__ s_pv,
+            const int *__restrict__ cell_of, const int *__restrict__ rank_of,
+            const int *__restrict__ cell_start)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= plan->n) return;
+    typename Vec<R>::T4 a = pv[i];
+    a.z = (R)vel[2 * i];
+    a.w = (R)vel[2 * i + 1];
+    pv[i] = a;
+    s_pv[cell_start[cell_of[i]] + rank_of[i]] = a;
+}
+
 template <typename R>
 __global__ void __launch_bounds__(256)
 k_import_attrs(int n, const double *__restrict__ radii, const double *__restrict__ pref,

@@ -280,6 +280,31 @@ class Simulation:
             self._h, n, int(frame), ptr(pos), ptr(vel), ptr(out_pos), ptr(out_vel), ptr(out_status)))
         return out_pos, out_vel
 
+    def advance_host(self, positions, velocities, frame: int):
+        """One frame of engine._advance through host buffers with overlapped copies
+        (orca_advance_host): -> (new_positions, new_velocities, info). The returned arrays
+        are the first info.active_agents rows of pinned buffers sized for the input."""
+        pos, vel = _f64(positions), _f64(velocities)
+        n = pos.shape[0] if pos.ndim == 2 else pos.size // 2
+        self._keep_pv = (pos, vel)
+        out_pos, out_vel = _host_empty((n, 2)), _host_empty((n, 2))
+        info = OrcaInfo()
+        self._raise_like_reference(self._L.orca_advance_host(
+            self._h, n, int(frame), ptr(pos), ptr(vel), ptr(out_pos), ptr(out_vel), C.byref(info)))
+        m = int(info.active_agents)
+        return out_pos[:m], out_vel[:m], info
+
+    def attributes(self):
+        """The seven per-agent arrays a step never changes, as resident now (after a frame
+        that removed agents: the compacted ones), in _STATIC order."""
+        n = self._L_active()
+        ids, cls = _host_empty(n, np.int64), _host_empty(n, np.int64)
+        goals = _host_empty((n, 2))
+        radii, pref, maxs, gtol = _host_empty(n), _host_empty(n), _host_empty(n), _host_empty(n)
+        self._raise_like_reference(self._L.orca_download(
+            self._h, ptr(ids), None, None, ptr(radii), ptr(pref), ptr(maxs), ptr(goals), ptr(gtol), ptr(cls)))
+        return ids, radii, pref, maxs, goals, gtol, cls
+
     def debug_last_step(self, n: int, max_neighbors: int):
         """Parity taps of the last step (orca_debug_last_step), storage-row order."""
         k = max(int(max_neighbors), 1)
@@ -388,28 +413,29 @@ def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
     sim.set_config(config, remove_arrivals=True, compute_metrics=True)
     static = tuple(getattr(state, f) for f in _STATIC)
     res = getattr(sim, "_resident", None)
-    if (reuse_resident and res is not None and len(res) == len(static)
+    if not (reuse_resident and res is not None and len(res) == len(static)
             and all(a is b for a, b in zip(res, static)) and sim._L_active() == n):
-        sim.load_pv(state.positions, state.velocities, state.frame)
-        sim._rng_state = getattr(state, "rng_state", None)
-        sim._state_type = type(state)
-        h2d = 32 * n
+        sim.load(state)                     # everything goes up (104 B/agent), then pos/vel again below
+        h2d = 136 * n
     else:
-        sim.load(state)
-        h2d = 104 * n
+        h2d = 32 * n                        # positions + velocities only
+    sim._rng_state = getattr(state, "rng_state", None)
+    sim._state_type = type(state)
     sim._resident = None
-    sim.step()
-    info = sim.info()                       # raises the reference's ValueError on device errors
+    # positions/velocities in, step, positions/velocities out, copies overlapped with the
+    # bin build / the metrics (orca_advance_host); raises the reference's ValueError on
+    # device-side errors
+    pos, vel, info = sim.advance_host(state.positions, state.velocities, state.frame)
+    frame = int(info.frame)
+    d2h = 32 * n
     if int(info.removed_agents) == 0 and reuse_resident:
-        pos, vel = sim.positions_velocities()
-        frame = int(info.frame)
-        new_state = type(state)(frame=frame, time=frame * float(config.dt), positions=pos,
-                                velocities=vel, rng_state=getattr(state, "rng_state", None),
-                                lp_fallbacks=int(info.lp_fallbacks), **dict(zip(_STATIC, static)))
-        d2h = 32 * n
+        new_static = static
     else:
-        new_state = sim.state(type(state))
-        d2h = 104 * int(new_state.ids.shape[0])
+        new_static = sim.attributes()       # compacted (or not to be shared with the input)
+        d2h += 72 * int(info.active_agents)
+    new_state = type(state)(frame=frame, time=frame * float(config.dt), positions=pos, velocities=vel,
+                            rng_state=getattr(state, "rng_state", None),
+                            lp_fallbacks=int(info.lp_fallbacks), **dict(zip(_STATIC, new_static)))
     step.last_traffic = (h2d, d2h)          # bytes copied host->device, device->host by this call
     sim._resident = tuple(getattr(new_state, f) for f in _STATIC)
     wall_ms = (_time.perf_counter() - t0) * 1e3
