@@ -25,6 +25,9 @@ Fixtures (all small, compressed):
   run_*.npz          whole engine.run() of the built-in 2-way / 4-way crossings: the crowd
                      the reference spawned, its guard, summary, per-frame metrics,
                      arrival times and sampled trajectories.
+  scenario_cases.json, traj_two_way_12.csv, agents_two_way_12.csv
+                     crossing documents, spawned crowds, validation messages and CSV
+                     bytes of the reference's scenario / crossings / cli modules.
   chain_1k.npz       config 1: 100 consecutive reference steps of 1,024
                      pedestrians (each input = previous output rounded to
                      float32 so an FP32 device state sees identical inputs);
@@ -318,15 +321,150 @@ def gen_chain():
     print("chain_1k.npz active", active[[0, -1]], "fallbacks/step", fallbacks.mean())
 
 
+def gen_scenarios():
+    """The callers either side of the step, from the reference:
+    crossing scenario documents, the crowds its seeded sampler spawns from them, frame
+    guards, validation messages for broken documents, and the bytes of its CSV writers."""
+    import hashlib
+    import json
+    import tempfile
+
+    import orcasim.scenario as S
+    from orcasim.cli import _write_agents_csv
+    from orcasim.crossings import arm_size, four_way_dict, two_way_dict
+
+    cases = []
+    for kind, per_arm, vf, seed, kw in (
+            ("two_way", 40, 0.1, 3, {}), ("four_way", 24, 0.25, 5, {}), ("four_way", 625, 0.0, 0, {}),
+            ("two_way", 300, 0.5, 11, {}), ("four_way", 60, 0.3, 2, {"size_for_worst_class": True}),
+            ("two_way", 25, 1.0, 7, {"arm_width": 30.0, "arm_depth": 50.0, "clearance_time": 0.8}),
+            ("four_way", 10, 0.5, 1, {"dt": 0.05, "tau": 3.0, "max_frames": 77, "goal_tolerance": 0.4}),
+            ("two_way", 0, 0.0, 0, {})):
+        maker = two_way_dict if kind == "two_way" else four_way_dict
+        doc = maker(per_arm, vf, seed, **kw)
+        cfg = S.scenario_from_dict(doc, source=f"<{kind} crossing>")
+        st = E.init_state(cfg)
+        cases.append(dict(kind=kind, per_arm=per_arm, vehicle_fraction=vf, seed=seed, kwargs=kw, doc=doc,
+                          guard=cfg.frame_guard(), warnings=cfg.warnings,
+                          arm_size=list(arm_size(per_arm, vf, kw.get("clearance_time", 0.5),
+                                                 kw.get("size_for_worst_class", False))),
+                          ids=st.ids.tolist(), positions=st.positions.tolist(), goals=st.goals.tolist(),
+                          velocities=st.velocities.tolist(), radii=st.radii.tolist(),
+                          pref_speeds=st.pref_speeds.tolist(), max_speeds=st.max_speeds.tolist(),
+                          goal_tols=st.goal_tols.tolist(), class_codes=st.class_codes.tolist()))
+        print(f"scenario {kind} per_arm={per_arm} vf={vf} seed={seed}: {st.active_count} agents, guard {cfg.frame_guard()}")
+
+    # validation: broken documents and the reference's message for each
+    good = two_way_dict(4, 0.5, 1)
+    broken = []
+
+    def bad(label, mutate):
+        doc = json.loads(json.dumps(good))
+        doc = mutate(doc) or doc
+        try:
+            S.scenario_from_dict(doc, source="<t>")
+            msg = None
+        except S.ScenarioError as exc:
+            msg = str(exc)
+        broken.append(dict(label=label, doc=doc, message=msg))
+
+    bad("not a mapping", lambda d: [1, 2])
+    bad("version", lambda d: d.update(format_version=2))
+    bad("unknown top-level", lambda d: d.update(speed=3))
+    bad("dt string", lambda d: d.update(dt="fast"))
+    bad("dt zero", lambda d: d.update(dt=0))
+    bad("dt inf", lambda d: d.update(dt=float("inf")))
+    bad("tau bool", lambda d: d.update(tau=True))
+    bad("clearance negative", lambda d: d.update(clearance_time=-1))
+    bad("margin negative", lambda d: d.update(avoidance_margin=-0.5))
+    bad("max_neighbors float", lambda d: d.update(max_neighbors=3.5))
+    bad("seed float", lambda d: d.update(seed=1.5))
+    bad("max_frames zero", lambda d: d.update(max_frames=0))
+    bad("goal_tolerance negative", lambda d: d.update(goal_tolerance=-1.0))
+    bad("classes unknown", lambda d: d.update(classes={"bicycle": {"radius": 1}}))
+    bad("classes not mapping", lambda d: d.update(classes={"vehicle": 3}))
+    bad("class unknown field", lambda d: d.update(classes={"vehicle": {"mass": 3}}))
+    bad("pref above max", lambda d: d.update(classes={"pedestrian": {"pref_speed": 9.0}}))
+    bad("regions missing", lambda d: d.pop("regions") and None)
+    bad("region not mapping", lambda d: d["regions"].__setitem__(0, 5))
+    bad("region unknown field", lambda d: d["regions"][0].update(colour="red"))
+    bad("rect short", lambda d: d["regions"][0].update(spawn=[0, 1, 2]))
+    bad("rect degenerate", lambda d: d["regions"][0].update(goal=[5, 0, 1, 3]))
+    bad("rect nan", lambda d: d["regions"][0].update(goal=[0, 0, float("nan"), 3]))
+    bad("region class", lambda d: d["regions"][0].update(agent_class="tram"))
+    bad("region class type", lambda d: d["regions"][0].update(agent_class=7))
+    bad("count negative", lambda d: d["regions"][0].update(count=-2))
+    bad("responsibility list", lambda d: d.update(responsibility=[1]))
+    bad("responsibility key", lambda d: d.update(responsibility={"pedestrian": 1.0}))
+    bad("responsibility value", lambda d: d["responsibility"].update({"pedestrian|vehicle": "all"}))
+    bad("responsibility range", lambda d: d["responsibility"].update({"pedestrian|vehicle": 1.5}))
+    bad("responsibility missing", lambda d: d["responsibility"].pop("vehicle|pedestrian") and None)
+    bad("unguaranteed pair (warning only)", lambda d: d["responsibility"].update({"pedestrian|vehicle": 0.3}))
+    bad("too dense", lambda d: d["regions"][0].update(count=100000))
+    warn_cfg = S.scenario_from_dict({**json.loads(json.dumps(good)),
+                                     "responsibility": {**good["responsibility"], "pedestrian|vehicle": 0.3,
+                                                        "vehicle|vehicle": 0.2}}, source="<w>")
+    # spawn failures surface at build time
+    dense = json.loads(json.dumps(good))
+    dense["regions"][0]["count"] = 100000
+    try:
+        S.build_agents(S.scenario_from_dict(dense, source="<t>"))
+        dense_msg = None
+    except S.ScenarioError as exc:
+        dense_msg = str(exc)
+
+    # CSV bytes of the reference's writers on a short reference run
+    from orcasim.crossings import crossing_config
+    cfg = crossing_config("two_way", 6, 0.34, seed=9)
+    cfg.max_frames = 12
+    res = E.run(cfg, worker_count=1, record_trajectories=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        S.write_trajectories(res.frame_logs, os.path.join(tmp, "t.csv"))
+        S.write_metrics_summary(res.summary, os.path.join(tmp, "m.csv"))
+        _write_agents_csv(res, os.path.join(tmp, "a.csv"))
+        traj_csv = open(os.path.join(tmp, "t.csv"), "rb").read()
+        metrics_csv = open(os.path.join(tmp, "m.csv"), "rb").read()
+        agents_csv = open(os.path.join(tmp, "a.csv"), "rb").read()
+    with open(os.path.join(OUT, "traj_two_way_12.csv"), "wb") as f:
+        f.write(traj_csv)
+    with open(os.path.join(OUT, "agents_two_way_12.csv"), "wb") as f:
+        f.write(agents_csv)
+
+    # sha256 of the full trajectory files of the two whole-run fixtures (run_*.npz)
+    run_sha = {}
+    for name, kind, per_arm, vf, seed in (("two_way_80", "two_way", 40, 0.1, 3),
+                                          ("four_way_96", "four_way", 24, 0.25, 5)):
+        r = E.run(crossing_config(kind, per_arm, vf, seed), worker_count=2, record_trajectories=True)
+        with tempfile.TemporaryDirectory() as tmp:
+            S.write_trajectories(r.frame_logs, os.path.join(tmp, "t.csv"))
+            _write_agents_csv(r, os.path.join(tmp, "a.csv"))
+            run_sha[name] = dict(trajectories=hashlib.sha256(open(os.path.join(tmp, "t.csv"), "rb").read()).hexdigest(),
+                                 agents=hashlib.sha256(open(os.path.join(tmp, "a.csv"), "rb").read()).hexdigest(),
+                                 kind=kind, per_arm=per_arm, vehicle_fraction=vf, seed=seed,
+                                 frames=r.summary.frames)
+    with open(os.path.join(OUT, "scenario_cases.json"), "w") as f:
+        json.dump(dict(cases=cases, broken=broken, warnings_two_pairs=warn_cfg.warnings,
+                       dense_build_message=dense_msg,
+                       short_run=dict(kind="two_way", per_arm=6, vehicle_fraction=0.34, seed=9, max_frames=12,
+                                      metrics_csv_head=metrics_csv.decode().splitlines()[0],
+                                      total_collisions=res.summary.total_collisions,
+                                      min_separation=res.summary.min_separation, frames=res.summary.frames),
+                       run_sha=run_sha), f)
+    print("scenario_cases.json:", len(cases), "cases,", len(broken), "broken documents")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if os.environ.get("GEN_ONLY_RUN"):
         return gen_run()
+    if os.environ.get("GEN_ONLY_SCENARIO"):
+        return gen_scenarios()
     gen_kat()
     gen_lp_batches()
     gen_frames()
     gen_chain()
     gen_run()
+    gen_scenarios()
 
 
 def gen_run():

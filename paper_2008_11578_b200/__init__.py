@@ -9,10 +9,16 @@ is missing -- there is no CPU fallback.
 from .types import (AgentClass, ClassParams, FrameLog, FrameMetrics, ResponsibilityMatrix,
                     RunResult, RunSummary, ScenarioConfig, SimState)
 from .engine import Simulation, desired_velocity, init_state, problem_seed, run, step
+from .scenario import (Region, ScenarioError, build_agents, load_scenario, read_trajectories,
+                       scenario_from_dict, write_metrics_summary, write_trajectories)
+from .crossings import crossing_config, four_way_dict, two_way_dict
 from .lp import (HalfPlaneConstraint, LpBatch, LpProblem, LpResult, LpStatus, shuffle_order,
                  solve_batch, solve_closest_point, solve_range)
 
 __all__ = ["AgentClass", "ClassParams", "FrameMetrics", "ResponsibilityMatrix",
            "ScenarioConfig", "SimState", "Simulation", "desired_velocity", "init_state",
            "problem_seed", "run", "step", "FrameLog", "RunResult", "RunSummary", "HalfPlaneConstraint", "LpBatch", "LpProblem", "LpResult",
-           "LpStatus", "shuffle_order", "solve_batch", "solve_closest_point", "solve_range"]
+           "LpStatus", "shuffle_order", "solve_batch", "solve_closest_point", "solve_range",
+           "Region", "ScenarioError", "build_agents", "load_scenario", "read_trajectories",
+           "scenario_from_dict", "write_metrics_summary", "write_trajectories", "crossing_config",
+           "four_way_dict", "two_way_dict"]

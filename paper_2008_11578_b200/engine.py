@@ -328,23 +328,29 @@ class Simulation:
 def init_state(config: ScenarioConfig, agents=None) -> SimState:
     """Start agents at their desired velocities (engine.py:173-191).
 
-    The reference samples spawn positions from config.regions
-    (scenario.build_agents, out of this package's scope); here the caller hands
-    over the spawned agents as `agents` (objects with id, position, radius,
-    pref_speed, max_speed, goal, agent_class -- e.g. orcasim.AgentState) or as
-    `config.agents`. With neither, the crowd is empty."""
+    Without `agents` the crowd is spawned from config.regions with the reference's seeded
+    sampling (scenario.spawn_arrays: same seed, same crowd, bit for bit). `agents` may
+    instead be a list of already spawned agents (objects with id, position, radius,
+    pref_speed, max_speed, goal, agent_class -- e.g. orcasim.AgentState)."""
     if agents is None:
-        agents = getattr(config, "agents", None) or []
-    n = len(agents)
-    ids = np.array([a.id for a in agents], dtype=np.int64)
-    positions = np.array([a.position for a in agents], dtype=np.float64).reshape(n, 2)
-    radii = np.array([a.radius for a in agents], dtype=np.float64)
-    pref = np.array([a.pref_speed for a in agents], dtype=np.float64)
-    maxs = np.array([a.max_speed for a in agents], dtype=np.float64)
-    goals = np.array([a.goal for a in agents], dtype=np.float64).reshape(n, 2)
-    codes = np.array([int(a.agent_class) for a in agents], dtype=np.int64)
-    gtols = np.array([config.goal_tolerance_for(AgentClass(int(a.agent_class))) for a in agents],
-                     dtype=np.float64)
+        agents = getattr(config, "agents", None)
+    if agents is None:
+        from .scenario import spawn_arrays
+        a = spawn_arrays(config)
+        ids, positions, goals, codes = a["ids"], a["positions"], a["goals"], a["class_codes"]
+        radii, pref, maxs = a["radii"], a["pref_speeds"], a["max_speeds"]
+        n = ids.shape[0]
+    else:
+        n = len(agents)
+        ids = np.array([a.id for a in agents], dtype=np.int64)
+        positions = np.array([a.position for a in agents], dtype=np.float64).reshape(n, 2)
+        radii = np.array([a.radius for a in agents], dtype=np.float64)
+        pref = np.array([a.pref_speed for a in agents], dtype=np.float64)
+        maxs = np.array([a.max_speed for a in agents], dtype=np.float64)
+        goals = np.array([a.goal for a in agents], dtype=np.float64).reshape(n, 2)
+        codes = np.array([int(a.agent_class) for a in agents], dtype=np.int64)
+    tol_of = {int(c): config.goal_tolerance_for(AgentClass(int(c))) for c in np.unique(codes)}
+    gtols = np.array([tol_of[int(c)] for c in codes], dtype=np.float64)
     # engine.py:133-139 (host-side setup, once per run)
     d = goals - positions
     dist = np.sqrt(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1])

@@ -92,6 +92,19 @@ class ResponsibilityMatrix:
     def guarantee_holds(self, a, b) -> bool:
         return self.get(a, b) + self.get(b, a) >= 1.0
 
+    def unguaranteed_pairs(self) -> list:
+        """Unordered class pairs (low, high) whose two fractions sum below 1, in the order
+        the matrix first lists them (orca.py:110-121). Pairs with one direction missing
+        are not reported."""
+        visited, below = set(), []
+        for a, b in self.f:
+            pair = (min(a, b), max(a, b))
+            if (b, a) in self.f and pair not in visited:
+                visited.add(pair)
+                if not self.guarantee_holds(a, b):
+                    below.append(pair)
+        return below
+
     def as_array(self) -> np.ndarray:
         n = max(int(c) for c in AgentClass) + 1
         arr = np.zeros((n, n), dtype=np.float64)
@@ -186,7 +199,7 @@ class SimState:
         return int(self.ids.shape[0])
 
 
-@dataclass
+@dataclass(eq=False)
 class FrameLog:
     """Positions and velocities of every agent active during one frame
     (scenario.py:117-140): post-step values, arrivals of that frame included."""
@@ -198,6 +211,13 @@ class FrameLog:
     positions: np.ndarray
     velocities: np.ndarray
     radii: np.ndarray
+
+    def __eq__(self, other):
+        if not isinstance(other, FrameLog):
+            return NotImplemented
+        return (self.frame == other.frame and self.time == other.time
+                and all(np.array_equal(getattr(self, k), getattr(other, k))
+                        for k in ("ids", "classes", "positions", "velocities", "radii")))
 
 
 @dataclass
