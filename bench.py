@@ -126,6 +126,14 @@ class ClockSampler:
 def build_workload(name: str, rank: int = 0, world: int = 1):
     n_ped, n_veh, density = CONFIGS[name]
     state, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100 + rank)
+    if os.environ.get("ORCA_BENCH_SORTED"):
+        # experiment: storage rows in spatial (column-major cell) order instead of random order
+        c = float(os.environ["ORCA_BENCH_SORTED"])
+        key = np.floor(state.positions[:, 0] / c) * 1e6 + np.floor(state.positions[:, 1] / c)
+        o = np.argsort(key, kind="stable")
+        for f in ("ids", "positions", "velocities", "radii", "pref_speeds", "max_speeds", "goals", "goal_tols",
+                  "class_codes"):
+            setattr(state, f, np.ascontiguousarray(getattr(state, f)[o]))
     return state, cfg, dict(workload=name, pedestrians=n_ped, vehicles=n_veh, density_per_m2=density,
                             neighbor_radius=cfg.neighbor_radius, max_neighbors=cfg.max_neighbors,
                             dt=cfg.dt, tau=cfg.tau)

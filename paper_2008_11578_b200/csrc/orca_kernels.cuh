@@ -27,6 +27,9 @@
 #ifndef ORCA_SCAN_UNROLL
 #define ORCA_SCAN_UNROLL 4
 #endif
+#ifndef ORCA_FB_RUNAHEAD
+#define ORCA_FB_RUNAHEAD 1 // k_fallback_coop: warp-voted run-ahead stage (orca_math.cuh, g_*_ra)
+#endif
 #ifndef ORCA_LP_RUNAHEAD
 #define ORCA_LP_RUNAHEAD 1 // k_solve: per-lane run-ahead LP (orca_math.cuh, lp2_target_runahead)
 #endif
@@ -555,8 +558,9 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
     double b = (double)h + ((double)radmax[row].y + plan->vmax) * P.dt * (1.0 + 1e-6) + 1e-3;
     const double T = fmin(b * b, rad2);
     const float T_f = __double2float_ru(T * (1.0 + 1e-6));
-    // scanning (nearly) the whole radius: the d2 <= rad2 cut itself must be exact (K:470)
-    const bool full = T * (1.0 + 1e-5) >= rad2;
+    // FP32 band around rad2 that the FP32 squared distance cannot resolve (its error is
+    // below 2^-22 relative; the band is 1e-6 on either side)
+    const float cut_lo = __double2float_rd(rad2 * (1.0 - 1e-6)), cut_hi = __double2float_ru(rad2 * (1.0 + 1e-6));
 
     const int nx = plan->nx, ny = plan->ny;
     const int c0 = s_cell[s];
@@ -593,14 +597,14 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
     }
     bool ok = nbuf <= CAP;
     if (ok) {
+        // The d2 <= rad2 cut (K:470) in FP32: candidates clearly outside are dropped, a
+        // candidate within the rounding band around rad2 sends the agent to the exact
+        // search. Both tests are vacuous unless the scan reaches the whole radius.
+        bool near_cut = false;
         auto make_key = [&](int e) -> unsigned {
-            const typename Vec<R>::T2 q = s_xy[my_buf[e * 128]];
-            unsigned k = (__float_as_uint(d2_f32(q)) & ~63u) | (unsigned)e;
-            if (full) {
-                const double dx = (double)q.x - mx, dy = (double)q.y - my;
-                if (dx * dx + dy * dy > rad2) k = 0xFFFFFFFFu;
-            }
-            return k;
+            const float d2f = d2_f32(s_xy[my_buf[e * 128]]);
+            near_cut = near_cut || (d2f >= cut_lo && d2f <= cut_hi);
+            return d2f > cut_hi ? 0xFFFFFFFFu : ((__float_as_uint(d2f) & ~63u) | (unsigned)e);
         };
         // sentinels 0 in front so the list proper is the last max_n registers
         const int off = MAXN - max_n;
@@ -649,6 +653,7 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
             }
         }
         if (rej != 0xFFFFFFFFu) ok = ok && ((rej >> 6) >= (prev >> 6) + 2u);
+        ok = ok && !near_cut;
         // exact squared distance of the last kept entry: the acceptance test and the hint
         double d2_last = 0.0;
         if (cnt > 0) {
@@ -1015,8 +1020,8 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
     const bool built = (__ballot_sync(gmask, !ok_mine) & gmask) == 0u; // also orders the stores
     int fail_pos;
     R vx, vy;
-    const bool feasible = g_lp2_target_runahead<R, GL, SmemCons<R>>(cons, cnt, dm.z, dm.x, dm.y, fail_pos, vx,
-                                                                     vy, live, built, gl, gmask);
+    const bool feasible = g_lp2_target_runahead<R, GL, false, SmemCons<R>>(
+        cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy, live, built, gl, gmask);
     if (gl != 0) return;
     if (!built) {
         // _kernels.py:542-547 + engine.py:239-245; coincident neighbours lead the list
@@ -1121,24 +1126,43 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
     u8 *sm_inv = sm_perm + MAXN * NG;
 
     const int nq = plan->fq_count;
+#if ORCA_FB_RUNAHEAD
+    // every lane makes the same number of passes (a group without an agent rides along
+    // disabled), so the run-ahead stage can vote over the whole warp
+    for (int base = blockIdx.x * NG; base < nq; base += gridDim.x * NG) {
+        const int q = base + g;
+        const bool enabled = q < nq;
+        const int s = enabled ? fq[q] : 0;
+        const R4 st = enabled ? fq_state[q] : mk4(R(0), R(0), R(0), R(0));
+        const int row = enabled ? s_row[s] : 0;
+        const int cnt = enabled ? (int)nb_cnt[s] : 0;
+        typename Vec<S>::T4 me = mk4(S(0), S(0), S(0), S(0));
+        R4 dm = mk4(R(0), R(0), R(0), R(0));
+        if (enabled) {
+            me = s_pv[s];
+            dm = s_dm[s];
+        }
+#else
     for (int q = blockIdx.x * NG + g; q < nq; q += gridDim.x * NG) {
+        const bool enabled = true;
         const int s = fq[q];
         const R4 st = fq_state[q];
         const int row = s_row[s];
         const int cnt = nb_cnt[s];
         const typename Vec<S>::T4 me = s_pv[s];
         const R4 dm = s_dm[s];
+#endif
         u8 *perm = sm_perm + g;
         u8 *inv = sm_inv + g;
         SmemCons<R> cons{sm_cons + g, NG};
         SmemCons<R> proj{sm_proj + g, NG};
 
-        if (gl == 0) {
+        if (gl == 0 && enabled) {
             shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
             for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * NG] * NG] = (u8)pos;
         }
         __syncwarp(gmask);
-        {   // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
+        if (enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
             const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
             const typename Vec<S>::T2 rc_i = s_rc[s];
             const R ri = (R)((double)rc_i.x + P.half_margin);
@@ -1160,9 +1184,14 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
 
         SmemConsIdent<R> ident{sm_cons + g, inv, NG};
         R rx, ry;
+#if ORCA_FB_RUNAHEAD
+        g_least_penetration_ra<R, ORCA_GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+            cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift, 0xFFFFFFFFu, enabled);
+#else
         g_least_penetration<R, ORCA_GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift);
-        if (gl == 0) integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
+#endif
+        if (gl == 0 && enabled) integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
         __syncwarp(gmask); // the group's shared memory is reused by the next queue entry
     }
 }

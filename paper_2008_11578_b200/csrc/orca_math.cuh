@@ -697,9 +697,9 @@ __device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, 
 
 // lp2_target_runahead for a group of GL lanes per problem: the scan is executed
 // redundantly by the group's lanes (same data, same result), the 1-D solves split their
-// j loops over the group.
-template <typename R, int GL, typename V>
-__device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R cap, R tx, R ty,
+// j loops over the group. SHIFT / zz as in lp1_target (the z-relaxed set of K:276-278).
+template <typename R, int GL, bool SHIFT, typename V>
+__device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R zz, R cap, R tx, R ty,
                                                       int &fail_pos, R &vx, R &vy, unsigned live,
                                                       bool enabled, int gl, unsigned gmask)
 {
@@ -721,6 +721,10 @@ __device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R ca
             for (; i_pos < k; ++i_pos) {
                 R px, py, nx, ny;
                 view.get(i_pos, px, py, nx, ny);
+                if (SHIFT) {
+                    px = px - zz * nx;
+                    py = py - zz * ny;
+                }
                 if ((vx - px) * nx + (vy - py) * ny < R(0)) {
                     found = true;
                     break;
@@ -731,7 +735,7 @@ __device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R ca
         if (!__any_sync(live, found)) break;
         if (found) {
             R nvx, nvy;
-            if (g_lp1_target<R, GL, false, V>(view, i_pos, R(0), cap, tx, ty, nvx, nvy, gl, gmask)) {
+            if (g_lp1_target<R, GL, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy, gl, gmask)) {
                 vx = nvx;
                 vy = nvy;
                 ++i_pos;
@@ -885,6 +889,155 @@ __device__ __forceinline__ void g_least_penetration(const VS &shuf, const VI &id
     }
     rx = vx;
     ry = vy;
+}
+
+// ---------------------------------------------------------------------------
+// Run-ahead versions of the group-cooperative fallback stage. In k_fallback_coop a warp
+// holds 32/GL agents whose control flow differs (which constraint raises the maximum
+// violation, which projected constraint is violated, which attempt succeeds): executed
+// as written above, a warp runs the union of its groups' paths one after the other
+// (measured: 8.5 of 32 lanes active). Here every data-dependent "find the next index
+// that needs work" scan is followed by a warp vote, so that the expensive bodies -- the
+// projected-constraint sweep, g_lp1_dir, g_lp1_target -- are entered by all groups that
+// need them at the same time. Same operations per agent, same results.
+// `live`: lanes that execute the call (all must); `enabled`: this group has an agent.
+// ---------------------------------------------------------------------------
+
+template <typename R, int GL, typename P>
+__device__ __forceinline__ bool g_lp2_dir_ra(const P &proj, int m, R cap, R ox, R oy, R &rx, R &ry, int gl,
+                                             unsigned gmask, unsigned live, bool enabled)
+{
+    R vx = cap * ox, vy = cap * oy;
+    int i = 0;
+    bool done = !enabled, ok = true;
+    while (true) {
+        bool found = false;
+        if (!done) {
+            for (; i < m; ++i) {
+                R px, py, nx, ny;
+                proj.get(i, px, py, nx, ny);
+                if ((vx - px) * nx + (vy - py) * ny < R(0)) {
+                    found = true;
+                    break;
+                }
+            }
+            done = !found;
+        }
+        if (!__any_sync(live, found)) break;
+        if (found) {
+            R nvx, nvy;
+            if (g_lp1_dir<R, GL, P>(proj, i, cap, ox, oy, nvx, nvy, gl, gmask)) {
+                vx = nvx;
+                vy = nvy;
+                ++i;
+            } else { // K:199-202: keep the last point, report failure
+                ok = false;
+                done = true;
+            }
+        }
+    }
+    rx = vx;
+    ry = vy;
+    return ok;
+}
+
+template <typename R, int GL, typename V, typename P>
+__device__ __forceinline__ void g_lp3_minmax_ra(const V &view, P &proj, int k, int begin, R cap, R &vx, R &vy,
+                                                R &z, int gl, unsigned gmask, int gshift, unsigned live,
+                                                bool enabled)
+{
+    R dist = R(0);
+    int i_pos = begin;
+    bool done = !enabled;
+    while (true) {
+        bool found = false;
+        R cpx = R(0), cpy = R(0), cnx = R(0), cny = R(0);
+        if (!done) {
+            for (; i_pos < k; ++i_pos) {
+                view.get(i_pos, cpx, cpy, cnx, cny);
+                if ((cpx - vx) * cnx + (cpy - vy) * cny > dist) {
+                    found = true;
+                    break;
+                }
+            }
+            done = !found;
+        }
+        if (!__any_sync(live, found)) break;
+        int m = 0;
+        if (found) { // projected constraints of (c, j < i_pos), K:226-243, GL at a time
+            for (int j0 = 0; j0 < i_pos; j0 += GL) {
+                const int j_pos = j0 + gl;
+                bool valid = false;
+                R ppx = R(0), ppy = R(0), pnx = R(0), pny = R(0);
+                if (j_pos < i_pos) {
+                    R jpx, jpy, jnx, jny;
+                    view.get(j_pos, jpx, jpy, jnx, jny);
+                    const R mx = jnx - cnx;
+                    const R my = jny - cny;
+                    const R ml2 = mx * mx + my * my;
+                    if (!(ml2 < R(1e-24))) {
+                        const R rhs = jpx * jnx + jpy * jny - cpx * cnx - cpy * cny;
+                        const R ml = sqrt_rn<R>(ml2);
+                        ppx = div_rn<R>(mx * rhs, ml2);
+                        ppy = div_rn<R>(my * rhs, ml2);
+                        pnx = div_rn<R>(mx, ml);
+                        pny = div_rn<R>(my, ml);
+                        valid = true;
+                    }
+                }
+                const unsigned bits = (__ballot_sync(gmask, valid) & gmask) >> gshift;
+                if (valid) proj.set(m + __popc(bits & ((1u << gl) - 1u)), ppx, ppy, pnx, pny);
+                m += __popc(bits);
+            }
+            __syncwarp(gmask); // projected constraints visible to the whole group
+        }
+        R nvx, nvy;
+        const bool ok = g_lp2_dir_ra<R, GL, P>(proj, m, cap, cnx, cny, nvx, nvy, gl, gmask, live, found);
+        if (found) {
+            if (ok) {
+                vx = nvx;
+                vy = nvy;
+            }
+            dist = (cpx - vx) * cnx + (cpy - vy) * cny;
+            if (dist < R(0)) dist = R(0);
+            ++i_pos;
+            __syncwarp(gmask); // everyone is done reading before the next sweep overwrites
+        }
+    }
+    z = dist;
+}
+
+template <typename R, int GL, typename VS, typename VI, typename P>
+__device__ __forceinline__ void g_least_penetration_ra(const VS &shuf, const VI &ident, P &proj, int k,
+                                                       int begin, R cap, R wx, R wy, R &rx, R &ry, int gl,
+                                                       unsigned gmask, int gshift, unsigned live, bool enabled)
+{
+    const R w2 = wx * wx + wy * wy;
+    if (w2 > cap * cap) {
+        const R s = div_rn<R>(cap, sqrt_rn<R>(w2));
+        wx = wx * s;
+        wy = wy * s;
+    }
+    R vx = wx, vy = wy, z = R(0);
+    g_lp3_minmax_ra<R, GL, VS, P>(shuf, proj, k, begin, cap, vx, vy, z, gl, gmask, gshift, live, enabled);
+    rx = vx; // K:283: the min-max point unless a re-solve succeeds
+    ry = vy;
+    R slack = R(0);
+    bool open = enabled; // still looking for a feasible re-solve
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const R zz = z + slack;
+        int fail;
+        R qx, qy;
+        const bool ok = g_lp2_target_runahead<R, GL, true, VI>(ident, k, zz, cap, wx, wy, fail, qx, qy, live,
+                                                               open, gl, gmask);
+        if (open && ok) {
+            rx = qx;
+            ry = qy;
+            open = false;
+        }
+        slack = slack * R(1e3) + R(1e-12) * (R(1) + z);
+        if (!__any_sync(live, open)) break;
+    }
 }
 
 } // namespace orca
