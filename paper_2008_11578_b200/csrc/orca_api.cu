@@ -41,6 +41,16 @@ struct orca_sim {
     i8 *status[2] = {nullptr, nullptr};
     i8 *failed[2] = {nullptr, nullptr};
     float *hint[2] = {nullptr, nullptr};       // radius that held last step's neighbour list
+    // Physical rows may be stored in a different order than the reference's (logical) rows:
+    // lrow[.][p] is the logical row of physical row p (identity until the first reordering).
+    // Every host-facing copy goes through it; the kernels of the step never need it.
+    int *lrow[2] = {nullptr, nullptr};
+    int *lkeep = nullptr, *lscan = nullptr;    // compaction: keep flags / new rows in logical order
+    bool rows_permuted = false;
+    bool reorder_due = false;                  // lay the rows out in cell order at the next step
+    int reorder_every = 128;                   // ORCA_REORDER_EVERY: frames between reorderings (0: never)
+    int64_t since_reorder = 0;
+    int apre = 0;                              // attribute buffer index before the last step's compaction
     int acur = 0;
     u8 *arrived = nullptr;
     int *keep = nullptr, *dst_idx = nullptr;
@@ -213,6 +223,10 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->dst_idx);
     cudaFree(sim->sel);
     cudaFree(sim->sel_idx);
+    cudaFree(sim->lrow[0]);
+    cudaFree(sim->lrow[1]);
+    cudaFree(sim->lkeep);
+    cudaFree(sim->lscan);
     cudaFree(sim->cell_of);
     cudaFree(sim->rank_of);
     cudaFree(sim->cell_count);
@@ -274,6 +288,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
     sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
     if (const char *sg = getenv("ORCA_SOLVE_GL")) sim->solve_gl = atoi(sg) >= 4 ? 4 : (atoi(sg) >= 2 ? 2 : 1);
+    if (const char *re = getenv("ORCA_REORDER_EVERY")) sim->reorder_every = std::max(0, atoi(re));
     if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
     if (const char *ch = getenv("ORCA_CHUNKS")) sim->chunks = std::min(ORCA_MAX_CHUNKS, std::max(1, atoi(ch)));
     if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
@@ -315,6 +330,10 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->dst_idx, cap + 1));
     CKC(dalloc(&sim->sel, cap + 1));
     CKC(dalloc(&sim->sel_idx, cap + 1));
+    CKC(dalloc(&sim->lrow[0], cap));
+    CKC(dalloc(&sim->lrow[1], cap));
+    CKC(dalloc(&sim->lkeep, cap + 1));
+    CKC(dalloc(&sim->lscan, cap + 1));
     CKC(dalloc(&sim->cell_of, cap));
     CKC(dalloc(&sim->rank_of, cap));
     CKC(dalloc(&sim->cell_count, (size_t)sim->max_cells + 1));
@@ -391,8 +410,8 @@ static int upload_pv_impl(orca_sim *sim, int64_t n, const double *positions, con
     double *d_pos = sim->stg, *d_vel = sim->stg + 2 * n;
     CK(sim, cudaMemcpyAsync(d_pos, positions, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, sim->stream));
     CK(sim, cudaMemcpyAsync(d_vel, velocities, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, sim->stream));
-    k_import_pv<R><<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, d_pos, d_vel,
-                                                              reinterpret_cast<R4 *>(sim->pv[sim->cur]));
+    k_import_pv<R><<<grid_for(n, 256), 256, 0, sim->stream>>>(
+        (int)n, d_pos, d_vel, reinterpret_cast<R4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
     CKL(sim);
     return ORCA_OK;
 }
@@ -462,7 +481,12 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->acur = 0;
     int rc = reset_plan(sim, n, frame);
     if (rc) return rc;
+    sim->rows_permuted = false;
+    sim->reorder_due = sim->reorder_every > 0;
+    sim->since_reorder = 0;
+    sim->apre = 0;
     if (n > 0) {
+        k_iota<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->lrow[0]);
         CK(sim, cudaMemcpyAsync(sim->ids[0], ids, sizeof(i64) * n, cudaMemcpyHostToDevice, sim->stream));
         CK(sim, cudaMemsetAsync(sim->status[0], 0, n, sim->stream));
         CK(sim, cudaMemsetAsync(sim->failed[0], 0xFF, n, sim->stream));
@@ -541,12 +565,14 @@ extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
     return rc;
 }
 
-template <typename R> static int download_pv_impl(orca_sim *sim, int64_t n, double *positions, double *velocities)
+template <typename R>
+static int download_pv_impl(orca_sim *sim, int64_t n, double *positions, double *velocities, int lidx = -1)
 {
     typedef typename Vec<R>::T4 R4;
     double *d_pos = sim->stg, *d_vel = sim->stg + 2 * n;
     k_export_pv<R><<<grid_for(n, 256), 256, 0, sim->stream>>>(
-        (int)n, reinterpret_cast<const R4 *>(sim->pv[sim->cur]), d_pos, d_vel);
+        (int)n, reinterpret_cast<const R4 *>(sim->pv[sim->cur]), d_pos, d_vel,
+        sim->lrow[lidx < 0 ? sim->acur : lidx]);
     CKL(sim);
     if (positions)
         CK(sim, cudaMemcpyAsync(positions, d_pos, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, sim->stream));
@@ -568,7 +594,7 @@ static int download_attrs_impl(orca_sim *sim, int64_t n, double *radii, double *
     k_export_attrs<R><<<grid_for(n, 256), 256, 0, st>>>(
         (int)n, reinterpret_cast<const R4 *>(sim->goalpref[sim->acur]),
         reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], d_rad, d_pref, d_max,
-        d_goal, d_gtol, d_cls);
+        d_goal, d_gtol, d_cls, sim->lrow[sim->acur]);
     CKL(sim);
     if (radii) CK(sim, cudaMemcpyAsync(radii, d_rad, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     if (pref) CK(sim, cudaMemcpyAsync(pref, d_pref, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -588,7 +614,13 @@ extern "C" int orca_download(orca_sim *sim, int64_t *ids, double *positions, dou
     if (rc) return rc;
     const int64_t n = sim->h_plan->n_owned;
     if (n == 0) return ORCA_OK;
-    if (ids) CK(sim, cudaMemcpyAsync(ids, sim->ids[sim->acur], sizeof(i64) * n, cudaMemcpyDeviceToHost, sim->stream));
+    if (ids) {
+        i64 *d_ids = reinterpret_cast<i64 *>(sim->stg + 11 * n);
+        k_export_i64<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->ids[sim->acur], d_ids,
+                                                                sim->lrow[sim->acur]);
+        CKL(sim);
+        CK(sim, cudaMemcpyAsync(ids, d_ids, sizeof(i64) * n, cudaMemcpyDeviceToHost, sim->stream));
+    }
     if (positions || velocities) {
         rc = sim->precision != ORCA_F64 ? download_pv_impl<float>(sim, n, positions, velocities)
                                         : download_pv_impl<double>(sim, n, positions, velocities);
@@ -615,8 +647,8 @@ extern "C" int orca_download_last_step_pv(orca_sim *sim, int64_t n, double *posi
     // the step wrote pv[(pre+1)%3]; arrival removal compacts into a third buffer and leaves it intact
     const int keep_cur = sim->cur;
     sim->cur = (sim->pre + 1) % 3;
-    rc = sim->precision != ORCA_F64 ? download_pv_impl<float>(sim, n, positions, velocities)
-                                    : download_pv_impl<double>(sim, n, positions, velocities);
+    rc = sim->precision != ORCA_F64 ? download_pv_impl<float>(sim, n, positions, velocities, sim->apre)
+                                    : download_pv_impl<double>(sim, n, positions, velocities, sim->apre);
     sim->cur = keep_cur;
     if (rc) return rc;
     CK(sim, cudaStreamSynchronize(sim->stream));
@@ -729,14 +761,15 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
             CK(sim, cudaStreamWaitEvent(cs, sim->ev_vel, 0));
             k_patch_vel<S><<<grid_for(n, 256), 256, 0, cs>>>(
                 sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
-                reinterpret_cast<S4 *>(sim->s_pv), sim->cell_of, sim->rank_of, sim->cell_start);
+                reinterpret_cast<S4 *>(sim->s_pv), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
             sim->launches += 1;
         }
 #define ORCA_SOLVE_ARGS                                                                                    \
     sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),        \
         reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
-        sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1
+        sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1,  \
+        sim->lrow[a]
         if (sim->solve_gl == 2)
             k_solve_group<S, R, MAXN, 128, 2><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(ORCA_SOLVE_ARGS);
         else if (sim->solve_gl == 4)
@@ -778,12 +811,17 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     return ORCA_OK;
 }
 
-__global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids)
+// err_pair holds LOGICAL rows (the reference reports the first bad row in its storage
+// order); the ids are looked up by a linear search -- this runs once, on the way to an error.
+__global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids, const int *__restrict__ lrow)
 {
     if (plan->err_pair != ORCA_NO_ERR && plan->err_frame < 0) {
         plan->err_frame = plan->frame + 1; // the reference names the frame being computed
-        plan->err_id_i = ids[(unsigned)(plan->err_pair >> 32)];
-        plan->err_id_j = ids[(unsigned)(plan->err_pair & 0xFFFFFFFFu)];
+        const int li = (int)(unsigned)(plan->err_pair >> 32), lj = (int)(unsigned)(plan->err_pair & 0xFFFFFFFFu);
+        for (int p = 0; p < plan->n; ++p) {
+            if (lrow[p] == li) plan->err_id_i = ids[p];
+            if (lrow[p] == lj) plan->err_id_j = ids[p];
+        }
     }
 }
 
@@ -806,12 +844,25 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
     k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
     k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums,
                                                        sim->dst_idx);
+    const int *lscan = nullptr;
+    if (sim->rows_permuted) {
+        // survivors keep the reference's relative order: new logical row = rank among the
+        // surviving logical rows
+        k_keep_by_logical<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->keep, sim->lrow[a], sim->lkeep);
+        k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->lkeep, sim->block_sums);
+        k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
+        k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->lkeep, sim->block_sums,
+                                                           sim->lscan);
+        sim->launches += 4;
+        lscan = sim->lscan;
+    }
     k_compact<R><<<grid_for(n, 256), 256, 0, st>>>(
         sim->plan, sim->keep, sim->dst_idx, reinterpret_cast<const R4 *>(sim->pv[src_idx]),
         reinterpret_cast<R4 *>(sim->pv[dst_pv_idx]), reinterpret_cast<const R4 *>(sim->goalpref[a]),
         reinterpret_cast<R4 *>(sim->goalpref[b]), reinterpret_cast<const R2 *>(sim->radmax[a]),
         reinterpret_cast<R2 *>(sim->radmax[b]), sim->ids[a], sim->ids[b], sim->cls[a], sim->cls[b],
-        sim->status[a], sim->status[b], sim->failed[a], sim->failed[b], sim->hint[a], sim->hint[b]);
+        sim->status[a], sim->status[b], sim->failed[a], sim->failed[b], sim->hint[a], sim->hint[b],
+        sim->lrow[a], sim->lrow[b], lscan);
     k_after_compact<<<1, 1, 0, st>>>(sim->plan, sim->dst_idx);
     CKL(sim);
     sim->launches += 6;
@@ -834,12 +885,42 @@ template <typename R> static int metrics_stage(orca_sim *sim, const StepParams &
     return ORCA_OK;
 }
 
+// Lay the rows out in the cell-sorted order of a fresh bin build (k_permute_rows).
+template <typename S, typename R> static int reorder_rows(orca_sim *sim, const StepParams &P)
+{
+    typedef typename Vec<S>::T4 S4;
+    typedef typename Vec<S>::T2 S2;
+    const int64_t n = sim->n_bound;
+    int rc = bin_build<S, R>(sim, P);
+    if (rc) return rc;
+    const int a = sim->acur, b = 1 - a, dst = (sim->cur + 1) % 3;
+    k_permute_rows<S><<<grid_for(n, 256), 256, 0, sim->stream>>>(
+        sim->plan, sim->s_row, reinterpret_cast<const S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->pv[dst]),
+        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->goalpref[b]),
+        reinterpret_cast<const S2 *>(sim->radmax[a]), reinterpret_cast<S2 *>(sim->radmax[b]), sim->ids[a],
+        sim->ids[b], sim->cls[a], sim->cls[b], sim->status[a], sim->status[b], sim->failed[a], sim->failed[b],
+        sim->hint[a], sim->hint[b], sim->lrow[a], sim->lrow[b]);
+    CKL(sim);
+    sim->launches += 1;
+    sim->cur = dst;
+    sim->acur = b;
+    sim->rows_permuted = true;
+    sim->binned_frame = -1; // the sorted arrays refer to the old rows
+    return ORCA_OK;
+}
+
 template <typename S, typename R> static int step_impl(orca_sim *sim)
 {
     StepParams P = make_params(sim);
     int rc;
     const int64_t n = sim->n_bound;
     sim->n_pre = n;
+    if (sim->reorder_due && sim->ghost_bound == 0 && n > 1) {
+        rc = reorder_rows<S, R>(sim, P);
+        if (rc) return rc;
+        sim->reorder_due = false;
+        sim->since_reorder = 0;
+    }
     sim->mark(); // stage boundaries: bins | gather | solve | fallback | finish+compact | metrics
     k_begin_step<<<1, 1, 0, sim->stream>>>(sim->plan);
     sim->launches += 1;
@@ -859,11 +940,13 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     const int out_idx = (sim->cur + 1) % 3;
     rc = P.max_n <= 16 ? solve_stage<S, R, 16>(sim, P, out_idx) : solve_stage<S, R, 32>(sim, P, out_idx);
     if (rc) return rc;
-    k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur]);
+    k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur], sim->lrow[sim->acur]);
     k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals);
     CKL(sim);
     sim->launches += 2;
     sim->pre = sim->cur;
+    sim->apre = sim->acur;
+    if (sim->reorder_every > 0 && ++sim->since_reorder >= sim->reorder_every) sim->reorder_due = true;
     if (sim->params.remove_arrivals || sim->ghost_bound > 0) {
         const int dst = (sim->cur + 2) % 3;
         rc = compact_stage<S>(sim, out_idx, dst);
@@ -884,8 +967,11 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
         const int64_t m = sim->n_pre; // rows beyond the kept ones are don't-care
         CK(sim, cudaEventRecord(sim->ev_state, sim->stream));
         CK(sim, cudaStreamWaitEvent(sim->aux_stream, sim->ev_state, 0));
+        // (only the surviving rows: the export scatters by logical row, and rows beyond them
+        //  hold stale mappings)
         k_export_pv<S><<<grid_for(m, 256), 256, 0, sim->aux_stream>>>(
-            (int)m, reinterpret_cast<const S4 *>(sim->pv[sim->cur]), sim->stg, sim->stg + 2 * m);
+            (int)m, reinterpret_cast<const S4 *>(sim->pv[sim->cur]), sim->stg, sim->stg + 2 * m,
+            sim->lrow[sim->acur], &sim->plan->n_owned);
         CKL(sim);
         if (sim->early_pos)
             CK(sim, cudaMemcpyAsync(sim->early_pos, sim->stg, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost,
@@ -929,6 +1015,8 @@ static int step_graphed(orca_sim *sim)
         if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins) {
             CK(sim, cudaGraphLaunch(g.exec, sim->stream));
             sim->n_pre = sim->n_bound;
+            sim->apre = g.acur;
+            if (sim->reorder_every > 0 && ++sim->since_reorder >= sim->reorder_every) sim->reorder_due = true;
             sim->pre = g.new_pre;
             sim->cur = g.new_cur;
             sim->acur = g.new_acur;
@@ -980,7 +1068,8 @@ extern "C" int orca_step(orca_sim *sim)
     if (!sim->loaded) return fail(sim, ORCA_EINVAL, "orca_step: no state uploaded");
     if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_step: orca_set_params was not called");
     CK(sim, cudaSetDevice(sim->device));
-    if (sim->use_graph && !sim->profiling && sim->ghost_bound == 0 && sim->n_bound > 0) return step_graphed(sim);
+    if (sim->use_graph && !sim->profiling && sim->ghost_bound == 0 && sim->n_bound > 0 && !sim->reorder_due)
+        return step_graphed(sim);
     return step_plain(sim);
 }
 
@@ -1039,7 +1128,8 @@ extern "C" int orca_step_host(orca_sim *sim, int64_t n, int64_t frame, const dou
         if (rc) return rc;
         if (out_status) {
             i64 *d = reinterpret_cast<i64 *>(sim->stg + 4 * n);
-            k_export_i8<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->status[sim->acur], d);
+            k_export_i8<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->status[sim->acur], d,
+                                                                   sim->lrow[sim->acur]);
             CKL(sim);
             CK(sim, cudaMemcpyAsync(out_status, d, sizeof(i64) * n, cudaMemcpyDeviceToHost, sim->stream));
         }
@@ -1080,21 +1170,21 @@ extern "C" int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const 
         CK(sim, cudaMemcpyAsync(d_vel, velocities, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, cp));
         CK(sim, cudaEventRecord(sim->ev_vel, cp));
         if (sim->precision != ORCA_F64)
-            k_import_pos<float><<<grid_for(n, 256), 256, 0, st>>>((int)n, d_pos,
-                                                                  reinterpret_cast<float4 *>(sim->pv[sim->cur]));
+            k_import_pos<float><<<grid_for(n, 256), 256, 0, st>>>(
+                (int)n, d_pos, reinterpret_cast<float4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
         else
-            k_import_pos<double><<<grid_for(n, 256), 256, 0, st>>>((int)n, d_pos,
-                                                                   reinterpret_cast<double4 *>(sim->pv[sim->cur]));
+            k_import_pos<double><<<grid_for(n, 256), 256, 0, st>>>(
+                (int)n, d_pos, reinterpret_cast<double4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
         CKL(sim);
         sim->split_vel = sim->chunks <= 1;
         if (!sim->split_vel) { // chunked gather/solve: no overlap, patch right away
             CK(sim, cudaStreamWaitEvent(st, sim->ev_vel, 0));
             if (sim->precision != ORCA_F64)
-                k_import_pv<float><<<grid_for(n, 256), 256, 0, st>>>((int)n, d_pos, d_vel,
-                                                                     reinterpret_cast<float4 *>(sim->pv[sim->cur]));
+                k_import_pv<float><<<grid_for(n, 256), 256, 0, st>>>(
+                    (int)n, d_pos, d_vel, reinterpret_cast<float4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
             else
                 k_import_pv<double><<<grid_for(n, 256), 256, 0, st>>>(
-                    (int)n, d_pos, d_vel, reinterpret_cast<double4 *>(sim->pv[sim->cur]));
+                    (int)n, d_pos, d_vel, reinterpret_cast<double4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
             CKL(sim);
         }
         sim->early_pos = new_positions;
@@ -1174,7 +1264,7 @@ template <typename S> static int strip_append_impl(orca_sim *sim, const orca_age
     k_strip_append<S><<<grid_for(count, 256), 256, 0, sim->stream>>>(
         sim->plan, records, (int)count, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
         reinterpret_cast<S4 *>(sim->goalpref[a]), reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a],
-        sim->cls[a], sim->status[a], sim->failed[a], sim->hint[a]);
+        sim->cls[a], sim->status[a], sim->failed[a], sim->hint[a], sim->lrow[a]);
     k_after_append<<<1, 1, 0, sim->stream>>>(sim->plan, (int)count, ghost);
     CKL(sim);
     sim->launches += 2;
@@ -1247,12 +1337,12 @@ static int debug_impl(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_
     i64 *d_fa = d_st + n;
     k_debug_rows<S, R><<<grid_for(n, 256), 256, 0, st>>>(
         (int)n, P, reinterpret_cast<const S4 *>(sim->pv[sim->pre]), sim->s_row, sim->nb, sim->nb_cnt,
-        reinterpret_cast<const R4 *>(sim->s_dm), d_ix, d_iy, d_rows, d_cnt, d_des);
+        reinterpret_cast<const R4 *>(sim->s_dm), d_ix, d_iy, d_rows, d_cnt, d_des, sim->lrow[sim->acur]);
     // the un-compacted post-step buffer is pv[(pre+1)%3]
     k_export_pv<S><<<grid_for(n, 256), 256, 0, st>>>(
-        (int)n, reinterpret_cast<const S4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel);
-    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->status[sim->acur], d_st);
-    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->failed[sim->acur], d_fa);
+        (int)n, reinterpret_cast<const S4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel, sim->lrow[sim->acur]);
+    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->status[sim->acur], d_st, sim->lrow[sim->acur]);
+    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->failed[sim->acur], d_fa, sim->lrow[sim->acur]);
     CKL(sim);
     if (cell_ix) CK(sim, cudaMemcpyAsync(cell_ix, d_ix, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
     if (cell_iy) CK(sim, cudaMemcpyAsync(cell_iy, d_iy, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
