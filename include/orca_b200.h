@@ -210,6 +210,14 @@ ORCA_API int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const do
                       const double *velocities, double *new_positions, double *new_velocities,
                       orca_info *info);
 
+/* Lay the resident rows out in the cell-sorted order of a fresh bin build (an internal
+ * layout change for memory coherence; no reference counterpart -- the reference keeps
+ * numpy arrays in spawn order, engine.py:179-186). orca_step does this by itself after an
+ * upload and periodically; callers that keep ghost rows resident at every step
+ * (parallel/strips.py) call it between migration and the next halo exchange. Every array
+ * the host reads or writes stays in the reference's storage order. */
+ORCA_API int orca_reorder_rows(orca_sim *sim);
+
 /* ---- parity taps (pre-step snapshot of the LAST step; storage-row order) --- */
 
 /* cell_ix/cell_iy: floor(pos / neighbor_radius) as int64 (engine.py:150-151).

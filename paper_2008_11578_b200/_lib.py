@@ -28,7 +28,7 @@ SYMBOLS = [
     "orca_abi_version", "orca_create", "orca_destroy", "orca_set_stream", "orca_set_params",
     "orca_last_error", "orca_upload", "orca_download", "orca_download_pv", "orca_upload_pv",
     "orca_download_last_step_pv",
-    "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host", "orca_advance_host",
+    "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host", "orca_advance_host", "orca_reorder_rows",
     "orca_profile_stages", "orca_get_stage_ms",
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
@@ -100,6 +100,7 @@ def load():
     L.orca_get_info.argtypes = [vp, P(OrcaInfo)]
     L.orca_step_host.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp]
     L.orca_advance_host.argtypes = [vp, i64, i64, vp, vp, vp, vp, C.POINTER(OrcaInfo)]
+    L.orca_reorder_rows.argtypes = [vp]
     L.orca_profile_stages.argtypes = [vp, ci]
     L.orca_get_stage_ms.argtypes = [vp, P(C.c_double), P(i64)]
     L.orca_debug_last_step.argtypes = [vp, i64] + [vp] * 8

@@ -1073,6 +1073,30 @@ extern "C" int orca_step(orca_sim *sim)
     return step_plain(sim);
 }
 
+// Lay the resident rows out in cell-sorted order now. orca_step does this by
+// itself after an upload and every ORCA_REORDER_EVERY frames when no ghost rows are resident;
+// the strip-decomposed driver, which always steps with ghosts appended, calls it explicitly
+// between migration and the next halo exchange. Nothing the host can observe changes.
+extern "C" int orca_reorder_rows(orca_sim *sim)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_reorder_rows: no resident state");
+    if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_reorder_rows: orca_set_params was not called");
+    if (sim->ghost_bound > 0)
+        return fail(sim, ORCA_EINVAL, "orca_reorder_rows: ghost rows are resident (drop them first)");
+    CK(sim, cudaSetDevice(sim->device));
+    if (sim->n_bound < 2) return ORCA_OK;
+    const StepParams P = make_params(sim);
+    int rc;
+    switch (sim->precision) {
+    case ORCA_F32: rc = reorder_rows<float, float>(sim, P); break;
+    case ORCA_MIXED: rc = reorder_rows<float, double>(sim, P); break;
+    default: rc = reorder_rows<double, double>(sim, P); break;
+    }
+    sim->reorder_due = false;
+    sim->since_reorder = 0;
+    return rc;
+}
+
 extern "C" int orca_profile_stages(orca_sim *sim, int enable)
 {
     if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_profile_stages: sim is NULL");

@@ -208,6 +208,11 @@ class Simulation:
     def sync(self):
         self._raise_like_reference(self._L.orca_sync(self._h))
 
+    def reorder_rows(self):
+        """Lay the resident rows out in cell-sorted order now (orca_reorder_rows); invisible
+        to every host-facing array."""
+        check(self._L.orca_reorder_rows(self._h), self._h)
+
     def info(self) -> OrcaInfo:
         info = OrcaInfo()
         self._raise_like_reference(self._L.orca_get_info(self._h, C.byref(info)))

@@ -73,6 +73,9 @@ class DeviceStripOps:
     def step(self):
         self.sim.step()
 
+    def reorder(self):
+        self.sim.reorder_rows()
+
 
 class StripDriver:
     """One rank's side of the strip protocol."""
@@ -95,6 +98,8 @@ class StripDriver:
         self.recv = {"left": mk(), "right": mk()}
         self.capacity = int(halo_capacity)
         self.stats = {"halo_sent": 0, "halo_recv": 0, "migr_sent": 0, "migr_recv": 0}
+        self.frames = 0
+        self.reorder_every = 64      # frames between row reorderings (no ghosts resident then)
 
     # -- one exchange with both neighbours --------------------------------------
     def _swap(self, counts: dict) -> dict:
@@ -172,6 +177,9 @@ class StripDriver:
 
     def step(self):
         """One frame of the whole strip-decomposed crowd, as seen by this rank."""
+        if self.reorder_every and self.frames % self.reorder_every == 0 and hasattr(self.ops, "reorder"):
+            self.ops.reorder()       # rows in cell order: memory coherence only, results unchanged
+        self.frames += 1
         self.exchange_halo()
         self.ops.step()
         self.migrate()
