@@ -221,6 +221,7 @@ def run_ours(args):
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2008_11578_b200.parallel import strips
+        args.make_sampler = lambda: ClockSampler(local)
         try:
             return strips.run_bench(args, rank, world, local)
         finally:

@@ -222,6 +222,9 @@ def run_bench(args, rank: int, world: int, local: int):
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = args.make_sampler() if hasattr(args, "make_sampler") else None
+    if sampler is not None:
+        sampler.__enter__()
     e0.record(stream)
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -230,6 +233,8 @@ def run_bench(args, rank: int, world: int, local: int):
     sim.sync()
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - t0) * 1e3
+    if sampler is not None:
+        sampler.__exit__(None, None, None)
     ms = torch.tensor([max(e0.elapsed_time(e1), 0.0), wall_ms], device=device, dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     info = sim.info()
@@ -238,7 +243,47 @@ def run_bench(args, rank: int, world: int, local: int):
                        device=device, dtype=torch.float64)
     dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     dist.barrier()
+
+    # ---- e2e: the same step with this rank's positions / velocities going up from pinned host
+    # memory and coming back every frame (what a host-side caller of a strip-decomposed crowd pays)
+    e2e_steps = max(3, min(args.steps, getattr(args, "e2e_steps", 20)))
+    pos, vel = sim.positions_velocities()
+    h2d = d2h = 0
+    for k in range(2 + e2e_steps):
+        if k == 2:
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h2d = d2h = 0
+        sim.load_pv(pos, vel, int(sim.info().frame))
+        h2d += pos.nbytes + vel.nbytes
+        drv.step()
+        pos, vel = sim.positions_velocities()
+        d2h += pos.nbytes + vel.nbytes
+    torch.cuda.synchronize()
+    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device=device, dtype=torch.float64)
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    io = torch.tensor([float(h2d), float(d2h), float(sim.info().active_agents)], device=device, dtype=torch.float64)
+    dist.all_reduce(io, op=dist.ReduceOp.SUM)
+
+    # ---- roofline of the dominant kernel on rank 0 (same definition as the N=1 line)
+    sim.profile_stages(True)
+    for _ in range(5):
+        drv.step()
+    stage_ms, covered = sim.stage_ms()
+    sim.profile_stages(False)
+    stage_ms = {k: v / max(covered, 1) for k, v in stage_ms.items()}
+    dist.barrier()
     if rank == 0:
+        import os
+        hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+        pk = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
+                          "MEASURED_PEAKS.json")
+        if os.path.exists(pk):
+            with open(pk) as f:
+                hbm_peak, peak_src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        solve_bytes = (16 + 32 + 1 + 4 * 16 + 1 + 16 + 16 + 2 + 1) * n_local     # bench.py SOLVE_BYTES_PER_AGENT
+        achieved = solve_bytes / (max(stage_ms["solve"], 1e-9) * 1e-3) / 1e9
         ms_step = float(ms[0]) / args.steps
         n_total = int(tot[0])
         line = {"metric": "agent_steps_per_s", "value": n_total / ms_step * 1e3, "unit": "agent-steps/s",
@@ -253,8 +298,19 @@ def run_bench(args, rank: int, world: int, local: int):
                            "migrants_per_step": float(tot[3]) / args.steps,
                            "cache": "state advances every step; working set > L2"},
                 "gpu_launches": int(tot[1]), "host_wall_ms_per_step": float(ms[1]) / args.steps,
-                "e2e": None, "roofline": None, "cpu_baseline": None,
-                "note": "multi-GPU line: device-timed max over ranks; e2e/roofline/cpu_baseline are "
-                        "reported by the N=1 run"}
+                "stages_ms": stage_ms,
+                "clocks": sampler.summary() if sampler is not None else None,
+                "e2e": {"value": float(io[2]) / float(e2e[0]) * 1e3, "unit": "agent-steps/s",
+                        "ms_per_step": float(e2e[0]), "h2d_bytes_per_step": int(float(io[0]) / e2e_steps),
+                        "d2h_bytes_per_step": int(float(io[1]) / e2e_steps),
+                        "call": "per rank and frame: Simulation.load_pv(host pos, vel) -> StripDriver.step() "
+                                "(halo exchange, orca_step, migration) -> Simulation.positions_velocities()"},
+                "roofline": {"bound": "hbm", "kernel": "k_solve" if args.precision == "f32" else "k_solve_group",
+                             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                             "traffic": None, "peak_source": peak_src,
+                             "algorithmic_bytes_per_launch": solve_bytes,
+                             "note": "rank 0's dominant kernel; the step is issue/latency bound (DESIGN.md s5)"},
+                "cpu_baseline": None,
+                "note": "multi-GPU line: device-timed max over ranks; cpu_baseline is reported by the N=1 run"}
         print(json.dumps(line), flush=True)
     sim.close()
