@@ -27,6 +27,16 @@
 #ifndef ORCA_SCAN_UNROLL
 #define ORCA_SCAN_UNROLL 4
 #endif
+#ifndef ORCA_BUILD_UNROLL
+#define ORCA_BUILD_UNROLL 1 // vo_exit chains interleaved per lane in k_solve_group's constraint build
+                            // (measured at 1 M agents: 1 -> 0.498 ms, 2 -> 0.511, 4 -> 0.537: registers, not ILP)
+#endif
+#ifndef ORCA_SG_BLOCKS
+#define ORCA_SG_BLOCKS 6    // resident blocks per SM k_solve_group is compiled for (register cap)
+#endif
+#ifndef ORCA_FB_BLOCKS
+#define ORCA_FB_BLOCKS 1    // resident blocks per SM k_fallback_coop is compiled for (1: no register cap)
+#endif
 #ifndef ORCA_FB_RUNAHEAD
 #define ORCA_FB_RUNAHEAD 1 // k_fallback_coop: warp-voted run-ahead stage (orca_math.cuh, g_*_ra)
 #endif
@@ -850,7 +860,7 @@ __device__ __forceinline__ bool build_constraints(
     const R ri = (R)((double)rc_i.x + P.half_margin); // engine.py:227, as in k_scatter
     const int ci = (int)rc_i.y;
     const R tau = (R)P.tau, dt = (R)P.dt;
-    const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
+    const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
     bool ok_all = true;
 #pragma unroll 2
     for (int pos = 0; pos < cnt; ++pos) {
@@ -964,7 +974,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
 // the j loops of the 1-D solves are split over the group (max / min / any combinations:
 // exact and order-independent, so results are unchanged).
 template <typename S, typename R, int MAXN, int THREADS, int GL>
-__global__ void __launch_bounds__(THREADS, (GL == 2 ? 6 : 8))
+__global__ void __launch_bounds__(THREADS, (GL == 2 ? ORCA_SG_BLOCKS : 8))
 k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__restrict__ s_pv,
               const typename Vec<R>::T4 *__restrict__ s_dm, const typename Vec<S>::T2 *__restrict__ s_rc,
               const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
@@ -1002,9 +1012,10 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
         const typename Vec<S>::T2 rc_i = s_rc[s];
         const R ri = (R)((double)rc_i.x + P.half_margin);
         const int ci = (int)rc_i.y;
-        const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
+        const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
         const R tau = (R)P.tau, dt = (R)P.dt;
-#pragma unroll 2
+        constexpr int kBuildUnroll = ORCA_BUILD_UNROLL;
+#pragma unroll kBuildUnroll
         for (int pos = gl; pos < cnt; pos += GL) {
             const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
             const typename Vec<S>::T4 qv = s_pv[j];
@@ -1104,7 +1115,7 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
 // the stage (orca_math.cuh, g_* functions). Against k_fallback this cuts the warp
 // instructions per agent ~3x in dense crowds, where the stage dominates the step.
 template <typename S, typename R, int MAXN, int THREADS>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, ORCA_FB_BLOCKS)
 k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
                 const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ s_row,
@@ -1167,7 +1178,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
             const typename Vec<S>::T2 rc_i = s_rc[s];
             const R ri = (R)((double)rc_i.x + P.half_margin);
             const int ci = (int)rc_i.y;
-            const R f0 = (R)P.fmat[ci * 2 + 0], f1 = (R)P.fmat[ci * 2 + 1];
+            const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
             for (int pos = gl; pos < cnt; pos += ORCA_GL) {
                 const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
                 const typename Vec<S>::T4 qv = s_pv[j];
