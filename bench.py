@@ -170,7 +170,7 @@ def run_reference(args):
     state, cfg, wl = build_workload(args.workload)
     threads = os.cpu_count() or 1
     n = state.active_count
-    rows = min(n, args.cpu_rows)
+    rows = min(n, args.cpu_rows if args.cpu_rows > 0 else 262144)
     for _ in range(max(args.warmup, 1)):
         cpu_port_rate(state, cfg, min(rows, 8192), threads)
     rates = []
@@ -322,15 +322,42 @@ def run_ours(args):
 
     # ---- CPU baseline: the oracle port on a bounded sample ------------------------
     threads = os.cpu_count() or 1
-    rows = min(n, args.cpu_rows)
+    rows = n if args.cpu_rows <= 0 else min(n, args.cpu_rows)   # default: the whole crowd, no extrapolation
     cpu_port_rate(state, cfg, min(rows, 8192), threads)          # warm the page cache / threads
-    cpu_value, _ = cpu_port_rate(state, cfg, rows, threads, repeats=2)
-    cpu1_value, _ = cpu_port_rate(state, cfg, max(1024, rows // 32), 1)
+    cpu_value, _ = cpu_port_rate(state, cfg, rows, threads, repeats=3)
+    cpu1_value, _ = cpu_port_rate(state, cfg, max(1024, min(rows, 65536)), 1)
 
     dom_kernel = {"bins": "k_scatter", "gather": "k_gather_fast32",
                   "solve": "k_solve" if args.precision == "f32" else "k_solve_group",
                   "fallback": "k_fallback_coop"}[dom]
     traffic, traffic_src = load_traffic(args.workload, args.precision, dom_kernel)
+    # ---- context lines: the other precision modes on this workload, and BASELINE config 5
+    # (8.5 M agents) resident on this one GPU
+    extras = {}
+    if not args.no_extras:
+        def resident_ms(st, cf, precision, steps):
+            with Simulation(cf, capacity=st.active_count, precision=precision, device=local,
+                            remove_arrivals=False, compute_metrics=False, stream=stream) as sm:
+                sm.load(st)
+                sm.run(5)
+                sm.sync()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                sm.run(steps)
+                b.record(stream)
+                sm.sync()
+                torch.cuda.synchronize()
+                return a.elapsed_time(b) / steps
+        extras["precision_modes_ms_per_step"] = {
+            p: resident_ms(state, cfg, p, 50) for p in ("mixed", "f32", "f64") if p != args.precision}
+        if args.workload == "plaza_1m":
+            big, bcfg, _ = build_workload("config5_8m")
+            ms8 = resident_ms(big, bcfg, args.precision, 20)
+            extras["config5_8m_single_gpu"] = {"agents": big.active_count, "ms_per_step": ms8,
+                                               "agent_steps_per_s": big.active_count / ms8 * 1e3,
+                                               "precision": args.precision}
+            del big
+
     dtype = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision]
     wl.update(precision=args.precision,
               cache="state advances every step; per-step working set ~%.0f MB > 126 MB L2, no flush"
@@ -349,6 +376,7 @@ def run_ours(args):
                                     "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 40 * n}},
         "gpu_launches": launches,
         "stages_ms": stage_ms,
+        "extras": extras,
         "roofline": {"bound": "hbm", "kernel": dom_kernel,
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
@@ -374,7 +402,11 @@ def main():
     ap.add_argument("--workload", default="plaza_1m", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="mixed", choices=["mixed", "f32", "f64"])
     ap.add_argument("--e2e-steps", type=int, default=30)
-    ap.add_argument("--cpu-rows", type=int, default=131072)
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="agents the CPU port solves per step (0: the whole crowd for cpu_baseline, "
+                         "262144 per step for --impl reference)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the context measurements (other precision modes, 8.5 M agents on one GPU)")
     ap.add_argument("--resident-only", action="store_true",
                     help="only the HBM-resident timing (for runs under ncu)")
     args = ap.parse_args()
