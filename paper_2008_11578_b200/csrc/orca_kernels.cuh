@@ -31,11 +31,14 @@
 #define ORCA_BUILD_UNROLL 1 // vo_exit chains interleaved per lane in k_solve_group's constraint build
                             // (measured at 1 M agents: 1 -> 0.498 ms, 2 -> 0.511, 4 -> 0.537: registers, not ILP)
 #endif
+#ifndef ORCA_BUILD_PREFETCH
+#define ORCA_BUILD_PREFETCH 1 // k_solve_group: request the next neighbour's record one iteration ahead
+#endif
 #ifndef ORCA_SG_BLOCKS
 #define ORCA_SG_BLOCKS 6    // resident blocks per SM k_solve_group is compiled for (register cap)
 #endif
 #ifndef ORCA_FB_BLOCKS
-#define ORCA_FB_BLOCKS 1    // resident blocks per SM k_fallback_coop is compiled for (1: no register cap)
+#define ORCA_FB_BLOCKS 0    // > 0: compile k_fallback_coop for this many resident blocks per SM (6, 8 measured: worse)
 #endif
 #ifndef ORCA_FB_RUNAHEAD
 #define ORCA_FB_RUNAHEAD 1 // k_fallback_coop: warp-voted run-ahead stage (orca_math.cuh, g_*_ra)
@@ -862,12 +865,22 @@ __device__ __forceinline__ bool build_constraints(
     const R tau = (R)P.tau, dt = (R)P.dt;
     const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
     bool ok_all = true;
-#pragma unroll 2
+    // software pipeline, as in k_solve_group: next neighbour's record requested one iteration ahead
+    typename Vec<S>::T4 q_next = me_s;
+    typename Vec<S>::T2 rc_next = rc_i;
+    if (cnt > 0) {
+        const int jn = nb[(size_t)perm[0] * P.stride + s];
+        q_next = s_pv[jn];
+        rc_next = s_rc[jn];
+    }
     for (int pos = 0; pos < cnt; ++pos) {
-        const int t = perm[pos * stride];
-        const int j = nb[(size_t)t * P.stride + s];
-        const typename Vec<S>::T4 q = s_pv[j];
-        const typename Vec<S>::T2 rc_j = s_rc[j];
+        const typename Vec<S>::T4 q = q_next;
+        const typename Vec<S>::T2 rc_j = rc_next;
+        if (pos + 1 < cnt) {
+            const int jn = nb[(size_t)perm[(pos + 1) * stride] * P.stride + s];
+            q_next = s_pv[jn];
+            rc_next = s_rc[jn];
+        }
         const R rj = (R)((double)rc_j.x + P.half_margin);
         R ux, uy, nx, ny;
         ok_all &= vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, tau, dt,
@@ -1015,11 +1028,32 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
         const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
         const R tau = (R)P.tau, dt = (R)P.dt;
         constexpr int kBuildUnroll = ORCA_BUILD_UNROLL;
+#if ORCA_BUILD_PREFETCH
+        // software pipeline: the next neighbour's index and record are requested before this
+        // neighbour's ~130-instruction FP64 chain starts, so their (L2) latency hides behind it
+        typename Vec<S>::T4 q_next = me;
+        typename Vec<S>::T2 rc_next = rc_i;
+        if (gl < cnt) {
+            const int jn = nb[(size_t)perm[gl * NG] * P.stride + s];
+            q_next = s_pv[jn];
+            rc_next = s_rc[jn];
+        }
+#endif
 #pragma unroll kBuildUnroll
         for (int pos = gl; pos < cnt; pos += GL) {
+#if ORCA_BUILD_PREFETCH
+            const typename Vec<S>::T4 qv = q_next;
+            const typename Vec<S>::T2 rc_j = rc_next;
+            if (pos + GL < cnt) {
+                const int jn = nb[(size_t)perm[(pos + GL) * NG] * P.stride + s];
+                q_next = s_pv[jn];
+                rc_next = s_rc[jn];
+            }
+#else
             const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
             const typename Vec<S>::T4 qv = s_pv[j];
             const typename Vec<S>::T2 rc_j = s_rc[j];
+#endif
             const R rj = (R)((double)rc_j.x + P.half_margin);
             R ux, uy, nx, ny;
             ok_mine &= vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, tau,
@@ -1115,7 +1149,11 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
 // the stage (orca_math.cuh, g_* functions). Against k_fallback this cuts the warp
 // instructions per agent ~3x in dense crowds, where the stage dominates the step.
 template <typename S, typename R, int MAXN, int THREADS>
+#if ORCA_FB_BLOCKS > 0
 __global__ void __launch_bounds__(THREADS, ORCA_FB_BLOCKS)
+#else
+__global__ void __launch_bounds__(THREADS)
+#endif
 k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
                 const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ s_row,
