@@ -31,6 +31,9 @@
 #define ORCA_BUILD_UNROLL 1 // vo_exit chains interleaved per lane in k_solve_group's constraint build
                             // (measured at 1 M agents: 1 -> 0.498 ms, 2 -> 0.511, 4 -> 0.537: registers, not ILP)
 #endif
+#ifndef ORCA_GATHER_WARP
+#define ORCA_GATHER_WARP 1 // k_gather: a short queue is searched one entry per WARP (cooperatively)
+#endif
 #ifndef ORCA_BUILD_PREFETCH
 #define ORCA_BUILD_PREFETCH 1 // k_solve_group: request the next neighbour's record one iteration ahead
 #endif
@@ -592,16 +595,30 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
             dxf = (float)((double)q.x - mx);
             dyf = (float)((double)q.y - my);
         }
-        return dxf * dxf + dyf * dyf;
+        return __fmaf_rn(dxf, dxf, dyf * dyf); // one rounding fewer than mul+add: inside the same error bound
     };
 
     int nbuf = 0;
-    for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+    const float cell_f = (float)plan->cell * (1.0f - 1e-6f), inv_cell_f = (float)plan->inv_cell * (1.0f + 1e-6f);
+    // Clip each column's rows to the circle: everything in column gx is at least
+    // (|gx - cx| - 1) cells away in x (cell indices are monotone in x), so only rows within
+    // sqrt(T - that^2) of mine, rounded up by a cell, can hold a candidate. The candidate
+    // range of the NEXT column is requested while this column is scanned.
+    auto column_range = [&](int gx, int &first, int &end) {
+        const float dxc = (float)max(abs(gx - cx) - 1, 0) * cell_f;
+        const int ry = (int)(sqrtf(fmaxf(T_f - dxc * dxc, 0.0f)) * inv_cell_f) + 1;
         const int *cs = cell_start + gx * ny;
-        const int e = cs[y_hi + 1];
+        first = cs[max(cy - ry, y_lo)];
+        end = cs[min(cy + ry, y_hi) + 1];
+    };
+    int a_next, e_next;
+    column_range(gx_lo, a_next, e_next);
+    for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+        const int a0 = a_next, e = e_next;
+        if (gx < gx_hi) column_range(gx + 1, a_next, e_next);
         constexpr int kScanUnroll = ORCA_SCAN_UNROLL;
 #pragma unroll kScanUnroll
-        for (int s2 = cs[y_lo]; s2 < e; ++s2) {
+        for (int s2 = a0; s2 < e; ++s2) {
             if (d2_f32(s_xy[s2]) <= T_f && s2 != s) {
                 if (nbuf < CAP) my_buf[nbuf * 128] = s2;
                 ++nbuf;
@@ -730,8 +747,148 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
     const int total_warps = gridDim.x * (blockDim.x >> 5);
     const int L = min(32, max(1, (nq + total_warps - 1) / total_warps));
     const int lane = threadIdx.x & 31;
-    if (lane >= L) return;
     const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+#if ORCA_GATHER_WARP
+    // One entry per warp at most: the whole warp searches for it. The lanes stride over the
+    // candidate ranges (coalesced), the in-range candidates are compacted into shared memory
+    // with their exact FP64 keys, and max_n + 1 rounds of a warp-wide arg-min pick the list in
+    // order. A single thread needs ~40 us for this (~90 candidates, ~50 register insertions of
+    // 115 instructions, every load exposed); the warp ~6. Exactly equal keys -- the order is
+    // then decided by id (K:473-476) -- or more than WCAP candidates send the entry to the
+    // single-lane search below, which handles everything.
+    constexpr int WCAP = 256;
+    __shared__ double w_key[4][WCAP];
+    __shared__ int w_idx[4][WCAP];
+    bool warp_done = false;
+    if (L == 1 && warp < nq && max_n <= 31) { // (uniform per warp; grid >= nq warps when L == 1)
+        double *wk = w_key[threadIdx.x >> 5];
+        int *wi = w_idx[threadIdx.x >> 5];
+        const int s = gq[warp];
+        const typename Vec<R>::T2 me = s_xy[s];
+        const double mx = (double)me.x, my = (double)me.y;
+        const int c0 = s_cell[s];
+        const int cx = c0 / ny, cy = c0 - cx * ny;
+        const unsigned lt = (1u << lane) - 1u;
+        // start at the ring that held last step's list, when there was one (an entry of a
+        // short queue normally has a finite hint: the fast pass only failed to certify it)
+        int r = plan->r0;
+        const float h = hint[s_row[s]];
+        if (h < 1e30f) r = max(r, min(rmax, (int)((double)h * plan->inv_cell) + 1));
+        bool bail = false;
+        while (true) {
+            const int gx_lo = max(cx - r, 0), gx_hi = min(cx + r, nx - 1);
+            const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
+            if (gx_hi - gx_lo >= 32) { // (never with rmax <= 15; keeps the lane-per-column load valid)
+                bail = true;
+                break;
+            }
+            // lane c fetches the candidate range of column gx_lo + c: all columns at once
+            int col_a = 0, col_e = 0;
+            if (gx_lo + lane <= gx_hi) {
+                const int *cs = cell_start + (gx_lo + lane) * ny;
+                col_a = cs[y_lo];
+                col_e = cs[y_hi + 1];
+            }
+            int count = 0;
+            for (int gx = gx_lo; gx <= gx_hi; ++gx) {
+                const int a = __shfl_sync(0xFFFFFFFFu, col_a, gx - gx_lo);
+                const int e = __shfl_sync(0xFFFFFFFFu, col_e, gx - gx_lo);
+                for (int base = a; base < e; base += 32) {
+                    const int s2 = base + lane;
+                    bool pass = false;
+                    double d2 = 0.0;
+                    if (s2 < e && s2 != s) {
+                        const typename Vec<R>::T2 q = s_xy[s2];
+                        const double dx = (double)q.x - mx, dy = (double)q.y - my;
+                        d2 = dx * dx + dy * dy;
+                        pass = !(d2 > rad2);
+                    }
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+                    const int at = count + __popc(m & lt);
+                    if (pass && at < WCAP) {
+                        wk[at] = d2;
+                        wi[at] = s2;
+                    }
+                    count += __popc(m);
+                }
+            }
+            if (count > WCAP) {
+                bail = true;
+                break;
+            }
+            __syncwarp();
+            // max_n + 1 smallest keys in ascending order; lane t keeps the t-th
+            double my_key = ORCA_INF, prev = -1.0;
+            int my_s2 = -1, found = 0;
+            bool tie = false;
+            for (int t = 0; t <= max_n && t < count; ++t) {
+                double best = ORCA_INF;
+                int best_at = -1;
+                for (int e = lane; e < count; e += 32) {
+                    const double k = wk[e];
+                    if (k < best) {
+                        best = k;
+                        best_at = e;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ok_ = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+                    const int oa = __shfl_xor_sync(0xFFFFFFFFu, best_at, o);
+                    if (ok_ < best || (ok_ == best && oa >= 0 && (best_at < 0 || oa < best_at))) {
+                        best = ok_;
+                        best_at = oa;
+                    }
+                }
+                // (all lanes agree on best / best_at now)
+                tie = tie || best == prev;
+                prev = best;
+                if (t < max_n) {
+                    if (lane == t) {
+                        my_key = best;
+                        my_s2 = wi[best_at];
+                    }
+                    found = t + 1;
+                }
+                if (lane == 0) wk[best_at] = ORCA_INF; // taken
+                __syncwarp();
+            }
+            if (tie) {
+                bail = true;
+                break;
+            }
+            // ring termination, as in the single-lane search
+            if (r >= rmax) {
+                bail = false;
+            } else if (found == max_n) {
+                const double d_last = __shfl_sync(0xFFFFFFFFu, my_key, max_n - 1);
+                const double reach = (double)r * cell;
+                if (!(d_last < reach * reach * (1.0 - 1e-9))) {
+                    const int need = (int)(sqrt(d_last) / cell * (1.0 + 1e-9)) + 1;
+                    r = min(rmax, max(r + 1, need));
+                    __syncwarp();
+                    continue;
+                }
+            } else {
+                r = min(rmax, r + 1);
+                __syncwarp();
+                continue;
+            }
+            // store: slot-major table, count, next step's radius hint
+            const int row = s_row[s];
+            if (lane < found) nb[(size_t)lane * P.stride + s] = my_s2;
+            const double d_last = __shfl_sync(0xFFFFFFFFu, my_key, max(found - 1, 0));
+            if (lane == 0) {
+                nb_cnt[s] = (u8)found;
+                hint[row] = found == max_n ? __double2float_ru(__dsqrt_ru(d_last)) : __int_as_float(0x7F800000);
+            }
+            break;
+        }
+        warp_done = !bail;
+    }
+    if (L == 1 && warp_done) return;
+#endif
+    if (lane >= L) return;
     for (int qi = warp * L + lane; qi < nq; qi += total_warps * L) {
         const int s = gq[qi];
         const int row = s_row[s];
