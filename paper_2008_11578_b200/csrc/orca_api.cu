@@ -79,6 +79,9 @@ struct orca_sim {
     size_t dbg_bytes = 0;
 
     int64_t binned_frame = -1; // the sorted arrays describe the state after this many frames
+    int64_t bbox_frame = -1;   // frame whose positions k_count's per-block boxes describe (-1: none)
+    double4 *box_part = nullptr; // one bounding box per k_count block of the last bin build
+    int box_parts = 0;
     int64_t launches = 0;      // kernels launched by this handle since creation
     double occ_target = 4.0;   // mean agents per search cell the plan aims for (ORCA_OCC_TARGET)
     int r0_override = 0;       // ORCA_R0: force the first ring radius (experiments)
@@ -102,6 +105,8 @@ struct orca_sim {
         int cur, acur;             // key: buffer rotation state before the step
         int64_t n_bound;           // key: launch grid sizes
         bool had_bins;             // key: sorted arrays already valid (metrics mode)
+        int bbox_gap;              // key: which bounding-box path the bin build takes (-1: k_bbox)
+        int bbox_rel;              // bbox_frame - frame after the step
         cudaGraphExec_t exec;
         int new_cur, new_acur, new_pre; // host state after the step
         bool leaves_bins;
@@ -223,6 +228,7 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->dst_idx);
     cudaFree(sim->sel);
     cudaFree(sim->sel_idx);
+    cudaFree(sim->box_part);
     cudaFree(sim->lrow[0]);
     cudaFree(sim->lrow[1]);
     cudaFree(sim->lkeep);
@@ -330,6 +336,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->dst_idx, cap + 1));
     CKC(dalloc(&sim->sel, cap + 1));
     CKC(dalloc(&sim->sel_idx, cap + 1));
+    CKC(dalloc(&sim->box_part, (size_t)((std::max<int64_t>(cap, 1) + 255) / 256)));
     CKC(dalloc(&sim->lrow[0], cap));
     CKC(dalloc(&sim->lrow[1], cap));
     CKC(dalloc(&sim->lkeep, cap + 1));
@@ -503,6 +510,7 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->ghost_bound = 0;
     sim->loaded = true;
     sim->binned_frame = -1;
+    sim->bbox_frame = -1;
     return ORCA_OK;
 }
 
@@ -517,6 +525,7 @@ extern "C" int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const dou
     CK(sim, cudaSetDevice(sim->device));
     sim->frame = frame;
     sim->binned_frame = -1;
+    sim->bbox_frame = -1; // positions replaced from outside
     k_set_frame<<<1, 1, 0, sim->stream>>>(sim->plan, frame);
     CKL(sim);
     if (n == 0) return ORCA_OK;
@@ -692,12 +701,23 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const S4 *pv = reinterpret_cast<const S4 *>(sim->pv[sim->cur]);
-    k_begin_bins<<<1, 1, 0, st>>>(sim->plan);
     CK(sim, cudaMemsetAsync(sim->cell_count, 0, sizeof(int) * ((size_t)P.max_cells + 1), st));
-    const int bbox_blocks = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (n + 255) / 256));
-    k_bbox<S><<<bbox_blocks, 256, 0, st>>>(sim->plan, pv);
-    k_plan<<<1, 1, 0, st>>>(sim->plan, P);
-    k_count<S><<<grid_for(n, 256), 256, 0, st>>>(sim->plan, pv, sim->cell_of, sim->rank_of, sim->cell_count, P.nr);
+    // the box of the previous build (k_count accumulated it), grown by the frames since, or a
+    // fresh reduction over the positions when they were replaced from outside
+    const int64_t gap = sim->bbox_frame < 0 ? -1 : sim->frame - sim->bbox_frame;
+    if (gap < 0 || gap > 1) {
+        const int bbox_blocks = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (n + 255) / 256));
+        k_begin_bins<<<1, 1, 0, st>>>(sim->plan);
+        k_bbox<S><<<bbox_blocks, 256, 0, st>>>(sim->plan, pv);
+        k_plan<<<1, 256, 0, st>>>(sim->plan, P, -1.0, sim->box_part, 0);
+        sim->launches += 2;
+    } else {
+        k_plan<<<1, 256, 0, st>>>(sim->plan, P, (double)gap, sim->box_part, sim->box_parts);
+    }
+    sim->bbox_frame = sim->frame;
+    sim->box_parts = (int)std::max<int64_t>(1, (n + 255) / 256);
+    k_count<S><<<grid_for(n, 256), 256, 0, st>>>(sim->plan, pv, sim->cell_of, sim->rank_of, sim->cell_count, P.nr,
+                                                sim->box_part);
     const int scan_blocks = (P.max_cells + 1 + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count, sim->block_sums);
     k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->block_sums);
@@ -709,7 +729,7 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
         sim->cell_start, reinterpret_cast<S2 *>(sim->s_xy), reinterpret_cast<S4 *>(sim->s_pv),
         reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell, reinterpret_cast<S2 *>(sim->s_rc));
     CKL(sim);
-    sim->launches += 8;
+    sim->launches += 6;
     sim->binned_frame = sim->frame;
     return ORCA_OK;
 }
@@ -1011,8 +1031,11 @@ static int step_plain(orca_sim *sim)
 static int step_graphed(orca_sim *sim)
 {
     const bool had_bins = sim->binned_frame == sim->frame;
+    const int64_t gap64 = sim->bbox_frame < 0 ? -1 : sim->frame - sim->bbox_frame;
+    const int bbox_gap = gap64 < 0 || gap64 > 1 ? -1 : (int)gap64;
     for (auto &g : sim->graphs) {
-        if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins) {
+        if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins &&
+            g.bbox_gap == bbox_gap) {
             CK(sim, cudaGraphLaunch(g.exec, sim->stream));
             sim->n_pre = sim->n_bound;
             sim->apre = g.acur;
@@ -1021,6 +1044,7 @@ static int step_graphed(orca_sim *sim)
             sim->cur = g.new_cur;
             sim->acur = g.new_acur;
             sim->frame += 1;
+            sim->bbox_frame = sim->frame + g.bbox_rel;
             sim->binned_frame = g.leaves_bins ? sim->frame : -1;
             sim->launches += g.launches;
             return ORCA_OK;
@@ -1032,6 +1056,7 @@ static int step_graphed(orca_sim *sim)
     g.acur = sim->acur;
     g.n_bound = sim->n_bound;
     g.had_bins = had_bins;
+    g.bbox_gap = bbox_gap;
     const int64_t l0 = sim->launches;
     if (cudaStreamBeginCapture(sim->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
         cudaGetLastError();
@@ -1056,6 +1081,7 @@ static int step_graphed(orca_sim *sim)
     g.new_acur = sim->acur;
     g.new_pre = sim->pre;
     g.leaves_bins = sim->binned_frame == sim->frame;
+    g.bbox_rel = (int)(sim->bbox_frame - sim->frame);
     g.launches = sim->launches - l0;
     sim->graphs.push_back(g);
     CK(sim, cudaGraphLaunch(g.exec, sim->stream)); // the capture itself executed nothing
@@ -1181,6 +1207,7 @@ extern "C" int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const 
     CK(sim, cudaSetDevice(sim->device));
     sim->frame = frame;
     sim->binned_frame = -1;
+    sim->bbox_frame = -1; // positions replaced from outside
     k_set_frame<<<1, 1, 0, sim->stream>>>(sim->plan, frame);
     CKL(sim);
     int rc = ORCA_OK;
@@ -1312,6 +1339,7 @@ extern "C" int orca_strip_append(orca_sim *sim, const orca_agent_record *records
     sim->n_bound += count;
     if (ghost) sim->ghost_bound += count;
     sim->binned_frame = -1;
+    sim->bbox_frame = -1; // rows appended from outside
     return ORCA_OK;
 }
 

@@ -104,16 +104,57 @@ __global__ void __launch_bounds__(256) k_bbox(GridPlan *plan, const typename Vec
 
 // One thread: choose the search-cell edge from the mean density, snap it so an
 // integer number of rings covers neighbor_radius, and make the dense grid fit.
-__global__ void k_plan(GridPlan *plan, StepParams P)
+// grow >= 0: no k_bbox ran; take the box k_count accumulated at the previous build, grown by
+// `grow` frames of the largest possible displacement (|v| <= max_speed after every LP, K:127-135).
+// A position that still ends up outside is clamped into an edge cell by search_cell, which
+// only makes it look closer to the grid than it is -- the ring-search bound stays valid.
+__global__ void __launch_bounds__(256)
+k_plan(GridPlan *plan, StepParams P, double grow, const double4 *__restrict__ box_part, int nparts)
 {
+    __shared__ double4 sm_box[8];
+    if (grow >= 0.0) { // reduce the per-block boxes of the previous build's k_count
+        double4 b = make_double4(1e300, 1e300, -1e300, -1e300);
+        for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+            const double4 p = box_part[i];
+            b.x = fmin(b.x, p.x);
+            b.y = fmin(b.y, p.y);
+            b.z = fmax(b.z, p.z);
+            b.w = fmax(b.w, p.w);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            b.x = fmin(b.x, __shfl_xor_sync(0xFFFFFFFFu, b.x, o));
+            b.y = fmin(b.y, __shfl_xor_sync(0xFFFFFFFFu, b.y, o));
+            b.z = fmax(b.z, __shfl_xor_sync(0xFFFFFFFFu, b.z, o));
+            b.w = fmax(b.w, __shfl_xor_sync(0xFFFFFFFFu, b.w, o));
+        }
+        if ((threadIdx.x & 31) == 0) sm_box[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     const int n = plan->n;
     plan->vmax = fmax(dec_double(plan->vmax_enc), 0.0);
     double x0 = 0.0, y0 = 0.0, w = 0.0, h = 0.0;
     if (n > 0) {
-        x0 = dec_double(plan->minx);
-        y0 = dec_double(plan->miny);
-        w = dec_double(plan->maxx) - x0;
-        h = dec_double(plan->maxy) - y0;
+        if (grow >= 0.0) {
+            double4 b = sm_box[0];
+            for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+                b.x = fmin(b.x, sm_box[k].x);
+                b.y = fmin(b.y, sm_box[k].y);
+                b.z = fmax(b.z, sm_box[k].z);
+                b.w = fmax(b.w, sm_box[k].w);
+            }
+            const double m = grow * plan->vmax * P.dt * (1.0 + 1e-6) + 1e-9;
+            x0 = b.x - m;
+            y0 = b.y - m;
+            w = b.z + m - x0;
+            h = b.w + m - y0;
+        } else {
+            x0 = dec_double(plan->minx);
+            y0 = dec_double(plan->miny);
+            w = dec_double(plan->maxx) - x0;
+            h = dec_double(plan->maxy) - y0;
+        }
     }
     const double nr = P.nr;
     const double area = fmax(w, 1e-3 * nr) * fmax(h, 1e-3 * nr);
@@ -122,7 +163,19 @@ __global__ void k_plan(GridPlan *plan, StepParams P)
     // snap: rings * c covers nr with a 1e-6 relative margin, so rmax == rings
     const double rings = ceil(nr / c);
     c = nr / rings * (1.0 + 1e-6);
-    while ((floor(w / c) + 1.0) * (floor(h / c) + 1.0) > (double)P.max_cells) c *= 1.25;
+    while ((floor(w / c) + 2.0) * (floor(h / c) + 2.0) > (double)P.max_cells) c *= 1.25;
+    // Anchor the grid to multiples of the cell edge: the cells then stay where they are from
+    // step to step (c only takes the values nr / rings), so the cell-sorted order -- and with
+    // it the row order chosen at the last reordering -- stays coherent while the box breathes.
+    {
+        const double ax = floor(x0 / c) * c, ay = floor(y0 / c) * c;
+        if (isfinite(ax) && isfinite(ay) && x0 - ax <= c && y0 - ay <= c) {
+            w += x0 - ax;
+            h += y0 - ay;
+            x0 = ax;
+            y0 = ay;
+        }
+    }
     const int nx = (int)floor(w / c) + 1, ny = (int)floor(h / c) + 1;
     plan->x0 = x0;
     plan->y0 = y0;
@@ -156,12 +209,39 @@ __device__ __forceinline__ void search_cell(const GridPlan *plan, double x, doub
 template <typename R>
 __global__ void __launch_bounds__(256)
 k_count(GridPlan *plan, const typename Vec<R>::T4 *__restrict__ pv, int *__restrict__ cell_of,
-        int *__restrict__ rank_of, int *__restrict__ cell_count, double nr)
+        int *__restrict__ rank_of, int *__restrict__ cell_count, double nr, double4 *__restrict__ box_part)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= plan->n) return;
-    const typename Vec<R>::T4 a = pv[i];
+    const bool live = i < plan->n;
+    const typename Vec<R>::T4 a = pv[live ? i : 0];
     const double x = (double)a.x, y = (double)a.y;
+    {   // bounding box of what is binned now, for the next build's plan (see k_plan)
+        double lox = live ? x : 1e300, hix = live ? x : -1e300, loy = live ? y : 1e300, hiy = live ? y : -1e300;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lox = fmin(lox, __shfl_xor_sync(0xFFFFFFFFu, lox, o));
+            loy = fmin(loy, __shfl_xor_sync(0xFFFFFFFFu, loy, o));
+            hix = fmax(hix, __shfl_xor_sync(0xFFFFFFFFu, hix, o));
+            hiy = fmax(hiy, __shfl_xor_sync(0xFFFFFFFFu, hiy, o));
+        }
+        // one partial box per block, reduced by the next k_plan: same-address atomics (or even
+        // same-address loads) from every warp of the grid serialise in one L2 slice and cost
+        // more than the k_bbox pass this replaces
+        __shared__ double4 sm_box[8];
+        if ((threadIdx.x & 31) == 0) sm_box[threadIdx.x >> 5] = make_double4(lox, loy, hix, hiy);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double4 b = sm_box[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                b.x = fmin(b.x, sm_box[w].x);
+                b.y = fmin(b.y, sm_box[w].y);
+                b.z = fmax(b.z, sm_box[w].z);
+                b.w = fmax(b.w, sm_box[w].w);
+            }
+            box_part[blockIdx.x] = b;
+        }
+    }
+    if (!live) return;
     // engine.py:150-153: the reference's own bin index must stay indexable
     const double rix = floor(__ddiv_rn(x, nr)), riy = floor(__ddiv_rn(y, nr));
     if (!(fabs(rix) <= ORCA_CELL_LIMIT) || !(fabs(riy) <= ORCA_CELL_LIMIT)) plan->err_range = 1;
