@@ -203,7 +203,11 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::fb_bpt * (C::fb_threads / 32) * 16);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads>,
+    e = cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL_SHORT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::fb_bpt * (C::fb_threads / ORCA_GL_SHORT));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 C::fb_bpt * (C::fb_threads / ORCA_GL));
 }
@@ -807,13 +811,25 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     }                //  is booked under "gather" and "solve" reads 0
     sim->mark();
     if (sim->fb_coop) {
+#define ORCA_FB_ARGS                                                                                       \
+    sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),        \
+        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
+        reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
+        sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state)
+        // long-queue and short-queue instance; the device-side queue length decides which one works
         const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
         const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + ng - 1) / ng));
-        k_fallback_coop<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
-            sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),
-            reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,
-            reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),
-            sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state));
+        k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
+            ORCA_FB_ARGS);
+        if (ORCA_GL_SHORT != ORCA_GL) {
+            const int ngs = C::fb_threads / ORCA_GL_SHORT;
+            const int64_t qmax = std::min<int64_t>(n, ORCA_FB_SHORT_QUEUE);
+            const int sb = (int)std::max<int64_t>(1, (qmax + ngs - 1) / ngs);
+            k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL_SHORT><<<sb, C::fb_threads, C::fb_bpt * ngs, st>>>(
+                ORCA_FB_ARGS);
+            sim->launches += 1;
+        }
+#undef ORCA_FB_ARGS
     } else {
         const int lanes = sim->fb_lanes;                          // active lanes per warp (<= 16)
         const int fb_at = (C::fb_threads / 32) * lanes;           // agents per block per pass
@@ -829,20 +845,6 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     CKL(sim);
     sim->launches += 1;
     return ORCA_OK;
-}
-
-// err_pair holds LOGICAL rows (the reference reports the first bad row in its storage
-// order); the ids are looked up by a linear search -- this runs once, on the way to an error.
-__global__ void k_resolve_error(GridPlan *plan, const i64 *__restrict__ ids, const int *__restrict__ lrow)
-{
-    if (plan->err_pair != ORCA_NO_ERR && plan->err_frame < 0) {
-        plan->err_frame = plan->frame + 1; // the reference names the frame being computed
-        const int li = (int)(unsigned)(plan->err_pair >> 32), lj = (int)(unsigned)(plan->err_pair & 0xFFFFFFFFu);
-        for (int p = 0; p < plan->n; ++p) {
-            if (lrow[p] == li) plan->err_id_i = ids[p];
-            if (lrow[p] == lj) plan->err_id_j = ids[p];
-        }
-    }
 }
 
 // Order-preserving removal of rows: arrivals and ghosts after a step (from_sel == false)
@@ -945,7 +947,7 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     k_begin_step<<<1, 1, 0, sim->stream>>>(sim->plan);
     sim->launches += 1;
     if (n == 0) { // engine.py:202-209
-        k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals);
+        k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals, nullptr, nullptr);
         CKL(sim);
         sim->launches += 1;
         for (int i = 0; i < ORCA_N_STAGES; ++i) sim->mark();
@@ -960,10 +962,10 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     const int out_idx = (sim->cur + 1) % 3;
     rc = P.max_n <= 16 ? solve_stage<S, R, 16>(sim, P, out_idx) : solve_stage<S, R, 32>(sim, P, out_idx);
     if (rc) return rc;
-    k_resolve_error<<<1, 1, 0, sim->stream>>>(sim->plan, sim->ids[sim->acur], sim->lrow[sim->acur]);
-    k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals);
+    k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals, sim->ids[sim->acur],
+                                       sim->lrow[sim->acur]);
     CKL(sim);
-    sim->launches += 2;
+    sim->launches += 1;
     sim->pre = sim->cur;
     sim->apre = sim->acur;
     if (sim->reorder_every > 0 && ++sim->since_reorder >= sim->reorder_every) sim->reorder_due = true;

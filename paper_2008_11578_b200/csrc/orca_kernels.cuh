@@ -31,6 +31,12 @@
 #define ORCA_BUILD_UNROLL 1 // vo_exit chains interleaved per lane in k_solve_group's constraint build
                             // (measured at 1 M agents: 1 -> 0.498 ms, 2 -> 0.511, 4 -> 0.537: registers, not ILP)
 #endif
+#ifndef ORCA_GL_SHORT
+#define ORCA_GL_SHORT 16         // lanes per agent in k_fallback_coop when the queue is short
+#endif
+#ifndef ORCA_FB_SHORT_QUEUE
+#define ORCA_FB_SHORT_QUEUE 4096 // "short": every queued agent gets half a warp in one wave
+#endif
 #ifndef ORCA_GATHER_WARP
 #define ORCA_GATHER_WARP 1 // k_gather: a short queue is searched one entry per WARP (cooperatively)
 #endif
@@ -1380,12 +1386,16 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
     }
 }
 
-// Group-cooperative least-penetration stage: ORCA_GL (8) adjacent lanes per queued agent,
-// four agents per warp. The lanes share the agent's constraints through shared memory,
-// build them in parallel (one vo_exit per lane and round), and split every inner loop of
-// the stage (orca_math.cuh, g_* functions). Against k_fallback this cuts the warp
-// instructions per agent ~3x in dense crowds, where the stage dominates the step.
-template <typename S, typename R, int MAXN, int THREADS>
+// Group-cooperative least-penetration stage: GL adjacent lanes per queued agent. The lanes
+// share the agent's constraints through shared memory, build them in parallel (one vo_exit
+// per lane and round), and split every inner loop of the stage (orca_math.cuh, g_*
+// functions). Against k_fallback this cuts the warp instructions per agent ~3x in dense
+// crowds, where the stage dominates the step.
+// Two instances are launched back to back and the queue length picks the one that works:
+// GL = ORCA_GL (4) when the queue is long (throughput: 8 agents per warp), GL = ORCA_GL_SHORT
+// (16) when every queued agent can have half a warp to itself (a short queue's time is the
+// latency of one agent's dependent chain: 54 -> 31 us at 1,024 agents, 64 -> 38 us at 16,640).
+template <typename S, typename R, int MAXN, int THREADS, int GL>
 #if ORCA_FB_BLOCKS > 0
 __global__ void __launch_bounds__(THREADS, ORCA_FB_BLOCKS)
 #else
@@ -1401,11 +1411,15 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef typename Vec<R>::T4 R4;
-    constexpr int NG = THREADS / ORCA_GL;             // agents (groups) per block and pass
-    const int g = threadIdx.x / ORCA_GL;              // group within the block
-    const int gl = threadIdx.x % ORCA_GL;             // lane within the group
+    {   // which instance serves this queue length (both see the same count, exactly one runs)
+        const bool is_short = plan->fq_count <= ORCA_FB_SHORT_QUEUE;
+        if (ORCA_GL_SHORT != ORCA_GL && is_short != (GL == ORCA_GL_SHORT)) return;
+    }
+    constexpr int NG = THREADS / GL;                  // agents (groups) per block and pass
+    const int g = threadIdx.x / GL;                   // group within the block
+    const int gl = threadIdx.x % GL;                  // lane within the group
     const int gshift = (threadIdx.x & 31) - gl;       // first lane of the group within its warp
-    const unsigned gmask = ((1u << ORCA_GL) - 1u) << gshift;
+    const unsigned gmask = ((1u << GL) - 1u) << gshift;
     R4 *sm_cons = reinterpret_cast<R4 *>(smem_raw);
     R4 *sm_proj = sm_cons + MAXN * NG;
     u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * NG);
@@ -1454,7 +1468,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
             const R ri = (R)((double)rc_i.x + P.half_margin);
             const int ci = (int)rc_i.y;
             const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
-            for (int pos = gl; pos < cnt; pos += ORCA_GL) {
+            for (int pos = gl; pos < cnt; pos += GL) {
                 const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
                 const typename Vec<S>::T4 qv = s_pv[j];
                 const typename Vec<S>::T2 rc_j = s_rc[j];
@@ -1471,10 +1485,10 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         SmemConsIdent<R> ident{sm_cons + g, inv, NG};
         R rx, ry;
 #if ORCA_FB_RUNAHEAD
-        g_least_penetration_ra<R, ORCA_GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+        g_least_penetration_ra<R, GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift, 0xFFFFFFFFu, enabled);
 #else
-        g_least_penetration<R, ORCA_GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+        g_least_penetration<R, GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift);
 #endif
         if (gl == 0 && enabled) integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
@@ -1488,8 +1502,20 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
 
 // frames completed += 1 (the frame index lives on the device so that a captured CUDA
 // graph of the step can be replayed without patching kernel arguments)
-__global__ void k_finish(GridPlan *plan, int remove_arrivals)
+// ids != nullptr: also resolve a pending coincident-centre error. err_pair holds LOGICAL rows
+// (the reference reports the first bad row in its storage order); the ids are looked up by a
+// linear search -- this runs once, on the way to an error.
+__global__ void k_finish(GridPlan *plan, int remove_arrivals, const i64 *__restrict__ ids,
+                         const int *__restrict__ lrow)
 {
+    if (ids && plan->err_pair != ORCA_NO_ERR && plan->err_frame < 0) {
+        plan->err_frame = plan->frame + 1; // the reference names the frame being computed
+        const int li = (int)(unsigned)(plan->err_pair >> 32), lj = (int)(unsigned)(plan->err_pair & 0xFFFFFFFFu);
+        for (int p = 0; p < plan->n; ++p) {
+            if (lrow[p] == li) plan->err_id_i = ids[p];
+            if (lrow[p] == lj) plan->err_id_j = ids[p];
+        }
+    }
     plan->frame = plan->frame + 1;
     if (!remove_arrivals) {
         plan->removed = 0;
