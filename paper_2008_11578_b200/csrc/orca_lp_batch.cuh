@@ -8,12 +8,15 @@
 
 namespace orca {
 
+#define LP_SMEM_K 64 // problems up to this many constraints keep their insertion order in shared memory
+
 template <typename R> struct GlobalShuf {
     const typename Vec<R>::T4 *cons; // this problem's rows
     const int *perm;
+    const u8 *sperm; // shared-memory copy of the order, [position * 128] (k_lp_batch), or nullptr
     __device__ __forceinline__ void get(int pos, R &px, R &py, R &nx, R &ny) const
     {
-        const typename Vec<R>::T4 c = cons[perm[pos]];
+        const typename Vec<R>::T4 c = cons[sperm ? (int)sperm[pos * 128] : perm[pos]];
         px = c.x;
         py = c.y;
         nx = c.z;
@@ -86,20 +89,38 @@ k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__res
     const int k = (int)(coff[i + 1] - lo);
     const typename Vec<R>::T4 pr = prob[i];
     int *perm = perm_scratch + lo;
+    // The insertion order lives in shared memory (one byte per position, [position][thread])
+    // when k <= LP_SMEM_K: the Fisher-Yates swaps and the order look-ups of the LP then stay
+    // on chip instead of being uncoalesced 4-byte global accesses. Larger problems use the
+    // global scratch; the least-penetration stage always reads the global copy, written below
+    // for the problems that need it.
+    __shared__ u8 sm_perm[LP_SMEM_K * 128];
+    u8 *sperm = k <= LP_SMEM_K ? sm_perm + threadIdx.x : nullptr;
 
     // _kernels.py:43-54
-    for (int t = 0; t < k; ++t) perm[t] = t;
     u64 state = seeds[i];
-    for (int t = k - 1; t > 0; --t) {
-        state += ORCA_GOLDEN;
-        const u64 r = mix64(state);
-        const int j = (t + 1) <= 0xFFFF ? (int)mod_small(r, (uint32_t)(t + 1)) : (int)(r % (u64)(t + 1));
-        const int tmp = perm[t];
-        perm[t] = perm[j];
-        perm[j] = tmp;
+    if (sperm) {
+        for (int t = 0; t < k; ++t) sperm[t * 128] = (u8)t;
+        for (int t = k - 1; t > 0; --t) {
+            state += ORCA_GOLDEN;
+            const int j = (int)mod_small(mix64(state), (uint32_t)(t + 1));
+            const u8 tmp = sperm[t * 128];
+            sperm[t * 128] = sperm[j * 128];
+            sperm[j * 128] = tmp;
+        }
+    } else {
+        for (int t = 0; t < k; ++t) perm[t] = t;
+        for (int t = k - 1; t > 0; --t) {
+            state += ORCA_GOLDEN;
+            const u64 r = mix64(state);
+            const int j = (t + 1) <= 0xFFFF ? (int)mod_small(r, (uint32_t)(t + 1)) : (int)(r % (u64)(t + 1));
+            const int tmp = perm[t];
+            perm[t] = perm[j];
+            perm[j] = tmp;
+        }
     }
 
-    GlobalShuf<R> shuf{cons + lo, perm};
+    GlobalShuf<R> shuf{cons + lo, perm, sperm};
     int fail_pos;
     R vx, vy;
     // per-lane run-ahead (orca_math.cuh): the problems of a warp differ in k and in where
@@ -112,6 +133,8 @@ k_lp_batch(i64 n, const i64 *__restrict__ coff, const typename Vec<R>::T4 *__res
         return;
     }
     out_status[i] = 1;
+    if (sperm)
+        for (int t = 0; t < k; ++t) perm[t] = (int)sperm[t * 128];
     out_failed[i] = perm[fail_pos];
     const int q = atomicAdd(fq_count, 1);
     fq[q] = (int)i;
@@ -138,6 +161,9 @@ k_lp_batch_fallback(const int *__restrict__ fq_count, const int *__restrict__ fq
     const int g = threadIdx.x / GL, gl = threadIdx.x % GL;
     const int gshift = (threadIdx.x & 31) - gl;
     const unsigned gmask = (GL == 32 ? 0xFFFFFFFFu : ((1u << GL) - 1u)) << gshift;
+    __shared__ typename Vec<R>::T4 sm_cons[LP_SMEM_K * NG];
+    __shared__ typename Vec<R>::T4 sm_proj[LP_SMEM_K * NG];
+    __shared__ u8 sm_inv[LP_SMEM_K * NG];
     const int nq = *fq_count;
     for (int q = blockIdx.x * NG + g; q < nq; q += gridDim.x * NG) {
         const int i = fq[q];
@@ -145,12 +171,32 @@ k_lp_batch_fallback(const int *__restrict__ fq_count, const int *__restrict__ fq
         const i64 lo = coff[i];
         const int k = (int)(coff[i + 1] - lo);
         const typename Vec<R>::T4 pr = prob[i];
-        GlobalShuf<R> shuf{cons + lo, perm_scratch + lo};
-        GlobalIdent<R> ident{cons + lo};
-        GlobalProj<R> proj{proj_scratch + lo};
         R rx, ry;
-        g_least_penetration<R, GL, GlobalShuf<R>, GlobalIdent<R>, GlobalProj<R>>(
-            shuf, ident, proj, k, (int)st.z, pr.z, st.x, st.y, rx, ry, gl, gmask, gshift);
+        if (k <= LP_SMEM_K) {
+            // the group stages its problem in shared memory -- constraints in shuffled order,
+            // the inverse order for the identity-order re-solve, room for the projected
+            // constraints -- so the stage's many passes over them stay on chip
+            SmemCons<R> sc{sm_cons + g, NG};
+            SmemCons<R> sp{sm_proj + g, NG};
+            const int *perm = perm_scratch + lo;
+            for (int pos = gl; pos < k; pos += GL) {
+                const int t = perm[pos];
+                const typename Vec<R>::T4 c = cons[lo + t];
+                sc.set(pos, c.x, c.y, c.z, c.w);
+                sm_inv[t * NG + g] = (u8)pos;
+            }
+            __syncwarp(gmask);
+            SmemConsIdent<R> si{sm_cons + g, sm_inv + g, NG};
+            g_least_penetration<R, GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
+                sc, si, sp, k, (int)st.z, pr.z, st.x, st.y, rx, ry, gl, gmask, gshift);
+            __syncwarp(gmask); // the group's shared memory is reused by its next queue entry
+        } else {
+            GlobalShuf<R> shuf{cons + lo, perm_scratch + lo, nullptr};
+            GlobalIdent<R> ident{cons + lo};
+            GlobalProj<R> proj{proj_scratch + lo};
+            g_least_penetration<R, GL, GlobalShuf<R>, GlobalIdent<R>, GlobalProj<R>>(
+                shuf, ident, proj, k, (int)st.z, pr.z, st.x, st.y, rx, ry, gl, gmask, gshift);
+        }
         if (gl == 0) {
             out_v[2 * (i64)i] = (double)rx;
             out_v[2 * (i64)i + 1] = (double)ry;
