@@ -1105,7 +1105,7 @@ __device__ __forceinline__ bool build_constraints(
     const typename Vec<S>::T2 rc_i = s_rc[s];
     const R ri = (R)((double)rc_i.x + P.half_margin); // engine.py:227, as in k_scatter
     const int ci = (int)rc_i.y;
-    const R tau = (R)P.tau, dt = (R)P.dt;
+    const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt); // K:358 / K:378, once
     const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
     bool ok_all = true;
     // software pipeline, as in k_solve_group: next neighbour's record requested one iteration ahead
@@ -1126,8 +1126,13 @@ __device__ __forceinline__ bool build_constraints(
         }
         const R rj = (R)((double)rc_j.x + P.half_margin);
         R ux, uy, nx, ny;
-        ok_all &= vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, tau, dt,
-                             ux, uy, nx, ny);
+#if ORCA_VO_BRANCHY
+        ok_all &= vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, (R)P.tau,
+                             (R)P.dt, ux, uy, nx, ny);
+#else
+        ok_all &= vo_exit_inv<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, inv_tau,
+                                 inv_dt, ux, uy, nx, ny);
+#endif
         const R f = rc_j.y != S(0) ? f1 : f0; // fmat[cls_i, cls_j], _kernels.py:537
         cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
     }
@@ -1269,7 +1274,7 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
         const R ri = (R)((double)rc_i.x + P.half_margin);
         const int ci = (int)rc_i.y;
         const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
-        const R tau = (R)P.tau, dt = (R)P.dt;
+        const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt); // K:358 / K:378, once
         constexpr int kBuildUnroll = ORCA_BUILD_UNROLL;
 #if ORCA_BUILD_PREFETCH
         // software pipeline: the next neighbour's index and record are requested before this
@@ -1299,8 +1304,13 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
 #endif
             const R rj = (R)((double)rc_j.x + P.half_margin);
             R ux, uy, nx, ny;
-            ok_mine &= vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, tau,
-                                  dt, ux, uy, nx, ny);
+#if ORCA_VO_BRANCHY
+            ok_mine &= vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj,
+                                  (R)P.tau, (R)P.dt, ux, uy, nx, ny);
+#else
+            ok_mine &= vo_exit_inv<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj,
+                                      inv_tau, inv_dt, ux, uy, nx, ny);
+#endif
             const R f = rc_j.y != S(0) ? f1 : f0;
             cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
         }
@@ -1468,14 +1478,15 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
             const R ri = (R)((double)rc_i.x + P.half_margin);
             const int ci = (int)rc_i.y;
             const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
+            const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt);
             for (int pos = gl; pos < cnt; pos += GL) {
                 const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
                 const typename Vec<S>::T4 qv = s_pv[j];
                 const typename Vec<S>::T2 rc_j = s_rc[j];
                 const R rj = (R)((double)rc_j.x + P.half_margin);
                 R ux, uy, nx, ny;
-                vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, (R)P.tau,
-                           (R)P.dt, ux, uy, nx, ny);
+                vo_exit_inv<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, inv_tau,
+                               inv_dt, ux, uy, nx, ny);
                 const R f = rc_j.y != S(0) ? f1 : f0;
                 cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
             }

@@ -88,6 +88,12 @@ __device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R co
 //                    and ~3 a leg, and the branchy form runs both paths back to back
 //                    (profiles/r01_notes.md). Only the two measure-zero cases (coincident
 //                    centres, |w|^2 < 1e-24) still branch.
+// vo_exit_inv takes 1/tau and 1/dt (K:358, K:378: `inv = 1.0 / tau`) so that callers with a
+// loop over neighbours divide once per kernel, not per neighbour; vo_exit computes them.
+template <typename R>
+__device__ __forceinline__ bool vo_exit_inv(R rpx, R rpy, R rvx, R rvy, R comb_r, R inv_tau, R inv_dt,
+                                            R &ux, R &uy, R &nx, R &ny);
+
 template <typename R>
 __device__ __forceinline__ bool vo_exit(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
                                         R &ux, R &uy, R &nx, R &ny)
@@ -95,10 +101,16 @@ __device__ __forceinline__ bool vo_exit(R rpx, R rpy, R rvx, R rvy, R comb_r, R 
 #if ORCA_VO_BRANCHY
     return vo_exit_branchy<R>(rpx, rpy, rvx, rvy, comb_r, tau, dt, ux, uy, nx, ny);
 #endif
+    return vo_exit_inv<R>(rpx, rpy, rvx, rvy, comb_r, div_rn<R>(R(1), tau), div_rn<R>(R(1), dt), ux, uy, nx, ny);
+}
+
+template <typename R>
+__device__ __forceinline__ bool vo_exit_inv(R rpx, R rpy, R rvx, R rvy, R comb_r, R inv_tau, R inv_dt,
+                                            R &ux, R &uy, R &nx, R &ny)
+{
     const R d2 = rpx * rpx + rpy * rpy;
     const R r2 = comb_r * comb_r;
     const bool overlap = d2 < r2;                                   // K:357
-    const R inv_dt = div_rn<R>(R(1), dt), inv_tau = div_rn<R>(R(1), tau); // loop-invariant for callers
     const R inv = overlap ? inv_dt : inv_tau;                       // K:358 / K:378
     const R cx = rpx * inv, cy = rpy * inv;
     const R rr = comb_r * inv;
