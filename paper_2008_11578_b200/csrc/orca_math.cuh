@@ -253,6 +253,9 @@ __device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R co
 #define ORCA_PARALLEL_EPS 1e-12
 
 // experiment switches (see profiles/): defaults are the measured-best variants
+#ifndef ORCA_RA_SCAN_UNROLL
+#define ORCA_RA_SCAN_UNROLL 1 // positions per iteration of the run-ahead scan loops (1, 2, 4 measured: no difference)
+#endif
 #ifndef ORCA_LP1DIR_NOEXIT
 #define ORCA_LP1DIR_NOEXIT 0
 #endif
@@ -396,6 +399,8 @@ __device__ __forceinline__ bool lp2_target_runahead(const V &view, int k, R cap,
     while (true) {
         bool found = false;
         if (!done) {
+            constexpr int kRaScanUnroll = ORCA_RA_SCAN_UNROLL;
+#pragma unroll kRaScanUnroll
             for (; i_pos < k; ++i_pos) {
                 R px, py, nx, ny;
                 view.get(i_pos, px, py, nx, ny);
@@ -730,6 +735,8 @@ __device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R zz
     while (true) {
         bool found = false;
         if (!done) {
+            constexpr int kRaScanUnroll = ORCA_RA_SCAN_UNROLL;
+#pragma unroll kRaScanUnroll
             for (; i_pos < k; ++i_pos) {
                 R px, py, nx, ny;
                 view.get(i_pos, px, py, nx, ny);
