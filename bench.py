@@ -23,6 +23,9 @@ synthetic crowd. Prints ONE JSON line on rank 0.
   --impl reference   times that CPU port as the reference arm (the Python+numba
                reference itself cannot travel to the GPU box)
 
+--workload lp_1m_feasible | lp_1m_half | lp_1m_infeasible: the batched-LP microbench of
+BASELINE config 4 (metric LP/s), same JSON contract.
+
 Multi-GPU (torchrun, one rank per GPU): the plaza is cut into x-strips, one per
 rank, with per-step halo exchange and migration over NCCL (parallel/strips.py);
 weak scaling: every rank owns `workload` agents.
@@ -393,13 +396,102 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+LP_WORKLOADS = {"lp_1m_feasible": 0.0, "lp_1m_half": 0.5, "lp_1m_infeasible": 1.0}
+
+
+def run_lp(args):
+    """BASELINE config 4: 1,048,576 independent 2-D LPs with 8..64 half-plane constraints each
+    (the CSR layout of _kernels.solve_range), all feasible / half / (almost) all infeasible.
+    One step = one solve of the whole batch. value: batch resident on the device; e2e: the
+    reference-shaped call lp.solve_range(host arrays) -> host arrays."""
+    import torch
+
+    from paper_2008_11578_b200 import LpBatch, solve_range
+    from paper_2008_11578_b200.synth import lp_batch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("bench.py needs a CUDA device; there is no CPU fallback")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    n = 1 << 20
+    frac = LP_WORKLOADS[args.workload]
+    coff, cpts, cnrm, tgt, caps, seeds = lp_batch(n, 8, 64, frac, seed=5)
+    m = int(coff[-1])
+    prec = "f32" if args.precision == "f32" else "f64"
+    hbm_peak, peak_src = load_peaks()
+    stream = torch.cuda.Stream()
+    b = LpBatch(coff, cpts, cnrm, tgt, caps, seeds, precision=prec, device=local, stream=stream)
+    for _ in range(max(args.warmup, 3)):
+        b.solve()
+    b.results()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            b.solve()
+        e1.record(stream)
+        _v, status, _f = b.results()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    b.close()
+    e2e_steps = max(3, min(args.steps, 5))
+    keep = []
+    def pin(a):      # the contract's e2e copies its inputs from pinned host memory
+        a = np.ascontiguousarray(a)
+        t = torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).pin_memory()
+        keep.append(t)
+        return t.numpy().view(a.dtype)
+    coff, cpts, cnrm, tgt, caps, seeds = (pin(a) for a in (coff, cpts, cnrm, tgt, caps, seeds))
+    solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision=prec, device=local)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision=prec, device=local)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    h2d = coff.nbytes + cpts.nbytes + cnrm.nbytes + tgt.nbytes + caps.nbytes + seeds.nbytes
+    d2h = n * (16 + 8 + 8)
+    # CPU port of solve_range on a bounded sample of the same batch
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    cn = min(n, 1 << 17)
+    sub = (coff[:cn + 1], cpts[:coff[cn]], cnrm[:coff[cn]], tgt[:cn], caps[:cn], seeds[:cn])
+    O.solve_range(*sub, worker_count=threads)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        O.solve_range(*sub, worker_count=threads)
+    cpu_rate = 3 * cn / (time.perf_counter() - t0)
+    rs = 4 if prec == "f32" else 8
+    alg_bytes = (4 * rs) * m + (3 * rs + 8 + 8 + 16 + 16) * n      # SURVEY s8(d): constraints + per-LP in/out
+    achieved = alg_bytes / (ms * 1e-3) / 1e9
+    line = {"metric": "lp_per_s", "value": n / ms * 1e3, "unit": "LP/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": {"workload": args.workload, "lps": n, "constraints": m, "k": "U{8..64}",
+                       "infeasible_fraction_requested": frac, "fallback_fraction": float((status != 0).mean()),
+                       "constraints_per_s": m / ms * 1e3,
+                       "cache": f"batch of {alg_bytes / 1e6:.0f} MB > 126 MB L2, no flush"},
+            "clocks": clocks.summary(),
+            "e2e": {"value": n / e2e_ms * 1e3, "unit": "LP/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "call": "paper_2008_11578_b200.lp.solve_range(host CSR arrays) -> host arrays"},
+            "gpu_launches": 2 * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "k_lp_batch" + ("+k_lp_batch_fallback" if frac > 0 else ""),
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": None, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                         "note": "thread-per-problem incremental LP: issue/latency bound, not HBM bound"},
+            "cpu_baseline": {"value": cpu_rate, "unit": "LP/s", "cores": threads, "kind": "port",
+                             "sample": f"oracle/orca_oracle.c solve_range on the first {cn} problems of the batch, "
+                                       f"{threads} pthreads, 3 repeats"}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="plaza_1m", choices=sorted(CONFIGS))
+    ap.add_argument("--workload", default="plaza_1m", choices=sorted(CONFIGS) + sorted(LP_WORKLOADS))
     ap.add_argument("--precision", default="mixed", choices=["mixed", "f32", "f64"])
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-rows", type=int, default=0,
@@ -410,7 +502,13 @@ def main():
     ap.add_argument("--resident-only", action="store_true",
                     help="only the HBM-resident timing (for runs under ncu)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.workload in LP_WORKLOADS:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the steering step; "
+                              "the LP microbench line carries its CPU port rate as cpu_baseline"}))
+        else:
+            run_lp(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
