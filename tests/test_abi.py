@@ -65,3 +65,12 @@ def test_product_never_imports_the_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", text, flags=re.M), f
                 assert "liborca_oracle" not in text and "orca_oracle" not in text, f
+    # outside the package only tests/, bench.py (CPU legs) and __graft_entry__.py (smoke, build)
+    # may touch oracle/
+    for dirpath, dirs, files in os.walk(ROOT):
+        dirs[:] = [d for d in dirs if d not in (".git", "tests", "oracle", "gpurun_out", "__pycache__",
+                                               "paper_2008_11578_b200", "variants", ".pytest_cache")]
+        for f in files:
+            if f.endswith(".py") and not (dirpath == ROOT and f in ("bench.py", "__graft_entry__.py")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", text, flags=re.M), os.path.join(dirpath, f)
