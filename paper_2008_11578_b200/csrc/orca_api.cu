@@ -48,7 +48,8 @@ struct orca_sim {
     int *lkeep = nullptr, *lscan = nullptr;    // compaction: keep flags / new rows in logical order
     bool rows_permuted = false;
     bool reorder_due = false;                  // lay the rows out in cell order at the next step
-    int reorder_every = 128;                   // ORCA_REORDER_EVERY: frames between reorderings (0: never)
+    int reorder_every = 32;                    // ORCA_REORDER_EVERY: frames between reorderings (0: never);
+                                               // 1500-step run at 1 M agents: 32 -> 0.954 ms, 128 -> 0.963, 512 -> 0.986, once -> 1.006
     int64_t since_reorder = 0;
     int apre = 0;                              // attribute buffer index before the last step's compaction
     int acur = 0;
