@@ -176,7 +176,10 @@ template <typename R, int MAXN> struct KCfg {
     static constexpr int solve_bpt = (int)sizeof(R4) * MAXN + MAXN;
     static constexpr int solve_threads = pick_threads(solve_bpt);
     static constexpr int fb_bpt = 2 * (int)sizeof(R4) * MAXN + 2 * MAXN; // per ACTIVE thread
-    static constexpr int fb_threads = 128;
+#ifndef ORCA_FB_THREADS
+#define ORCA_FB_THREADS 128
+#endif
+    static constexpr int fb_threads = ORCA_FB_THREADS;
 };
 
 extern "C" int orca_abi_version(void) { return ORCA_ABI_VERSION; }
