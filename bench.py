@@ -59,9 +59,9 @@ def load_traffic(workload, precision, kernel):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f).get(f"{workload}/{precision}", {})
-        return t.get(kernel), t.get("source")
+        return t.get(kernel), t.get("source"), t.get("ncu", {}).get(kernel)
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def load_peaks():
@@ -333,7 +333,7 @@ def run_ours(args):
     dom_kernel = {"bins": "k_scatter", "gather": "k_gather_fast32",
                   "solve": "k_solve" if args.precision == "f32" else "k_solve_group",
                   "fallback": "k_fallback_coop"}[dom]
-    traffic, traffic_src = load_traffic(args.workload, args.precision, dom_kernel)
+    traffic, traffic_src, ncu_util = load_traffic(args.workload, args.precision, dom_kernel)
     # ---- context lines: the other precision modes on this workload, and BASELINE config 5
     # (8.5 M agents) resident on this one GPU
     extras = {}
@@ -383,6 +383,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": dom_kernel,
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                     "ncu": ncu_util,   # what actually bounds it: issue slots (ipc of 4), FP64 pipe, lanes, warps
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "step_frac": STEP_BYTES_PER_AGENT * n / (ms_step * 1e-3) / 1e9 / hbm_peak,
                      "note": "the step is issue/latency bound, not HBM bound (DESIGN.md s5); "
