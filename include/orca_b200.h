@@ -29,6 +29,10 @@
  *   - orca_step / orca_run are asynchronous with respect to the host; errors
  *     raised by device code (coincident centres, grid range) are sticky and
  *     surface at the next orca_sync / orca_download / orca_get_info.
+ *   - Every array that crosses this boundary is in the reference's storage-row
+ *     order (engine.py:56-74; compaction keeps the survivors' order,
+ *     engine.py:288-294). The handle keeps its rows in cell-sorted order
+ *     internally and maps them back (orca_reorder_rows).
  *   - precision (cell indices and neighbour-ordering keys are FP64 in every
  *     mode, so bins and neighbour lists are bit-exact whenever the inputs are
  *     representable in the storage type):
