@@ -717,10 +717,10 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
         const int bbox_blocks = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (n + 255) / 256));
         k_begin_bins<<<1, 1, 0, st>>>(sim->plan);
         k_bbox<S><<<bbox_blocks, 256, 0, st>>>(sim->plan, pv);
-        k_plan<<<1, 256, 0, st>>>(sim->plan, P, -1.0, sim->box_part, 0);
+        k_plan<<<1, 1, 0, st>>>(sim->plan, P, -1.0);
         sim->launches += 2;
     } else {
-        k_plan<<<1, 256, 0, st>>>(sim->plan, P, (double)gap, sim->box_part, sim->box_parts);
+        k_plan<<<1, 1, 0, st>>>(sim->plan, P, (double)gap);
     }
     sim->bbox_frame = sim->frame;
     sim->box_parts = (int)std::max<int64_t>(1, (n + 255) / 256);

@@ -33,6 +33,10 @@ struct GridPlan {
     double x0, y0, cell, inv_cell;
     // bounding-box accumulators, order-preserving u64 encodings of doubles
     u64 minx, miny, maxx, maxy;
+    // bounding box of the positions the LAST bin build binned (k_count's last block folds the
+    // per-block boxes into it); the next build grows it by one frame's largest displacement
+    double nbox[4];
+    unsigned box_done; // blocks of the running k_count that have published their box
     // sticky errors
     u64 err_pair;   // (row_i << 32 | row_j) of the first coincident pair in row order
     i64 err_frame;  // frame_new of that step

@@ -114,47 +114,18 @@ __global__ void __launch_bounds__(256) k_bbox(GridPlan *plan, const typename Vec
 // `grow` frames of the largest possible displacement (|v| <= max_speed after every LP, K:127-135).
 // A position that still ends up outside is clamped into an edge cell by search_cell, which
 // only makes it look closer to the grid than it is -- the ring-search bound stays valid.
-__global__ void __launch_bounds__(256)
-k_plan(GridPlan *plan, StepParams P, double grow, const double4 *__restrict__ box_part, int nparts)
+__global__ void k_plan(GridPlan *plan, StepParams P, double grow)
 {
-    __shared__ double4 sm_box[8];
-    if (grow >= 0.0) { // reduce the per-block boxes of the previous build's k_count
-        double4 b = make_double4(1e300, 1e300, -1e300, -1e300);
-        for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-            const double4 p = box_part[i];
-            b.x = fmin(b.x, p.x);
-            b.y = fmin(b.y, p.y);
-            b.z = fmax(b.z, p.z);
-            b.w = fmax(b.w, p.w);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            b.x = fmin(b.x, __shfl_xor_sync(0xFFFFFFFFu, b.x, o));
-            b.y = fmin(b.y, __shfl_xor_sync(0xFFFFFFFFu, b.y, o));
-            b.z = fmax(b.z, __shfl_xor_sync(0xFFFFFFFFu, b.z, o));
-            b.w = fmax(b.w, __shfl_xor_sync(0xFFFFFFFFu, b.w, o));
-        }
-        if ((threadIdx.x & 31) == 0) sm_box[threadIdx.x >> 5] = b;
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
     const int n = plan->n;
     plan->vmax = fmax(dec_double(plan->vmax_enc), 0.0);
     double x0 = 0.0, y0 = 0.0, w = 0.0, h = 0.0;
     if (n > 0) {
         if (grow >= 0.0) {
-            double4 b = sm_box[0];
-            for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
-                b.x = fmin(b.x, sm_box[k].x);
-                b.y = fmin(b.y, sm_box[k].y);
-                b.z = fmax(b.z, sm_box[k].z);
-                b.w = fmax(b.w, sm_box[k].w);
-            }
             const double m = grow * plan->vmax * P.dt * (1.0 + 1e-6) + 1e-9;
-            x0 = b.x - m;
-            y0 = b.y - m;
-            w = b.z + m - x0;
-            h = b.w + m - y0;
+            x0 = plan->nbox[0] - m;
+            y0 = plan->nbox[1] - m;
+            w = plan->nbox[2] + m - x0;
+            h = plan->nbox[3] + m - y0;
         } else {
             x0 = dec_double(plan->minx);
             y0 = dec_double(plan->miny);
@@ -215,7 +186,7 @@ __device__ __forceinline__ void search_cell(const GridPlan *plan, double x, doub
 template <typename R>
 __global__ void __launch_bounds__(256)
 k_count(GridPlan *plan, const typename Vec<R>::T4 *__restrict__ pv, int *__restrict__ cell_of,
-        int *__restrict__ rank_of, int *__restrict__ cell_count, double nr, double4 *__restrict__ box_part)
+        int *__restrict__ rank_of, int *__restrict__ cell_count, double nr, double4 *box_part)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = i < plan->n;
@@ -230,12 +201,13 @@ k_count(GridPlan *plan, const typename Vec<R>::T4 *__restrict__ pv, int *__restr
             hix = fmax(hix, __shfl_xor_sync(0xFFFFFFFFu, hix, o));
             hiy = fmax(hiy, __shfl_xor_sync(0xFFFFFFFFu, hiy, o));
         }
-        // one partial box per block, reduced by the next k_plan: same-address atomics (or even
-        // same-address loads) from every warp of the grid serialise in one L2 slice and cost
-        // more than the k_bbox pass this replaces
+        // one partial box per block, folded by the block that finishes last: same-address atomics
+        // (or even same-address loads) from every warp of the grid serialise in one L2 slice and
+        // cost more than the k_bbox pass this replaces
         __shared__ double4 sm_box[8];
         if ((threadIdx.x & 31) == 0) sm_box[threadIdx.x >> 5] = make_double4(lox, loy, hix, hiy);
         __syncthreads();
+        __shared__ bool sm_last;
         if (threadIdx.x == 0) {
             double4 b = sm_box[0];
             for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
@@ -245,6 +217,45 @@ k_count(GridPlan *plan, const typename Vec<R>::T4 *__restrict__ pv, int *__restr
                 b.w = fmax(b.w, sm_box[w].w);
             }
             box_part[blockIdx.x] = b;
+            __threadfence();
+            sm_last = atomicAdd(&plan->box_done, 1u) == gridDim.x - 1u;
+        }
+        __syncthreads();
+        if (sm_last) { // the block that finishes last folds the partial boxes into the plan
+            double4 b = make_double4(1e300, 1e300, -1e300, -1e300);
+            for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+                // (written by other blocks of this launch: read through L2, not the L1 of this SM)
+                const double2 lo2 = __ldcg(reinterpret_cast<const double2 *>(&box_part[i]));
+                const double2 hi2 = __ldcg(reinterpret_cast<const double2 *>(&box_part[i]) + 1);
+                const double4 p = make_double4(lo2.x, lo2.y, hi2.x, hi2.y);
+                b.x = fmin(b.x, p.x);
+                b.y = fmin(b.y, p.y);
+                b.z = fmax(b.z, p.z);
+                b.w = fmax(b.w, p.w);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                b.x = fmin(b.x, __shfl_xor_sync(0xFFFFFFFFu, b.x, o));
+                b.y = fmin(b.y, __shfl_xor_sync(0xFFFFFFFFu, b.y, o));
+                b.z = fmax(b.z, __shfl_xor_sync(0xFFFFFFFFu, b.z, o));
+                b.w = fmax(b.w, __shfl_xor_sync(0xFFFFFFFFu, b.w, o));
+            }
+            __syncthreads(); // sm_box is reused
+            if ((threadIdx.x & 31) == 0) sm_box[threadIdx.x >> 5] = b;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+                    b.x = fmin(b.x, sm_box[w].x);
+                    b.y = fmin(b.y, sm_box[w].y);
+                    b.z = fmax(b.z, sm_box[w].z);
+                    b.w = fmax(b.w, sm_box[w].w);
+                }
+                plan->nbox[0] = b.x;
+                plan->nbox[1] = b.y;
+                plan->nbox[2] = b.z;
+                plan->nbox[3] = b.w;
+                plan->box_done = 0u;
+            }
         }
     }
     if (!live) return;
