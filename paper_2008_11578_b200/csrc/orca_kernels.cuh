@@ -947,6 +947,7 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
                     }
                     found = t + 1;
                 }
+                __syncwarp(); // every lane has read the keys of this round
                 if (lane == 0) wk[best_at] = ORCA_INF; // taken
                 __syncwarp();
             }
