@@ -24,6 +24,12 @@ for prec in ("mixed", "f32", "f64"):
             sim.step()
             sim.sync()
         print(prec, dens, "ok", s2.active_count, int(info.active_agents))
+# a queue long enough for the 4-lanes-per-agent fallback instance and the lane-per-entry exact search
+st, cfg = plaza_crowd(40000, 800, density=1.5, seed=6)
+with Simulation(cfg, capacity=st.active_count, precision="mixed", remove_arrivals=False) as sim:
+    sim.load(st)
+    sim.run(3)
+    print("dense 40k ok, fallbacks", int(sim.info().lp_fallbacks))
 cur, cfg = plaza_crowd(2000, 50, density=0.5, seed=4)
 for _ in range(3):
     cur, m = step(cur, cfg)
