@@ -17,9 +17,13 @@ synthetic crowd. Prints ONE JSON line on rank 0.
   roofline     the dominant kernel of the step, timed live with CUDA events on
                the launching stream (orca_profile_stages), against the measured
                HBM peak of MEASURED_PEAKS.json
+  roofline.traffic / roofline.ncu   DRAM bytes per launch and issue / pipe utilisation of
+               that kernel from the committed ncu capture (profiles/traffic.json)
   cpu_baseline oracle/orca_oracle.c (a C port of the reference's step, pinned
-               bit-exactly to the reference) on this box's host cores, on a
-               bounded sample of the same workload
+               bit-exactly to the reference) on this box's host cores: one whole
+               step of the same crowd, all host threads
+  extras       context: the other precision modes on this workload and BASELINE
+               config 5 (8.5 M agents) resident on this one GPU (--no-extras skips)
   --impl reference   times that CPU port as the reference arm (the Python+numba
                reference itself cannot travel to the GPU box)
 
