@@ -1,6 +1,6 @@
 """Soak of the randomised parity tests over many more seeds than the test-suite runs
 (development tooling; imports the tests, which use the oracle):
-    python scripts/soak_fuzz.py [first_seed] [count]
+    python tests/soak/soak_fuzz.py [first_seed] [count]
 Per seed: tests/test_gpu_fuzz.py::test_random_step_matches_oracle, then five resident frames
 (radius-hint fast pass, exact-search queue, row reordering every 2 frames) of the same random
 crowd in f64 and mixed, every frame against the oracle fed the device's own state."""
@@ -8,7 +8,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("ORCA_REORDER_EVERY", "2")

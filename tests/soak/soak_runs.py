@@ -2,12 +2,12 @@
 oracle): random crowd size 5k-60k, density 0.05-3 /m2, vehicle share, goals close enough that agents
 keep arriving; 6 resident frames in f64 must equal oracle.advance bit for bit (state, metrics,
 fallback counts), the same frames through orca_advance_host as well, mixed within 1e-6 m/s of it
-frame by frame.   python scripts/soak_runs.py [first_seed] [count]"""
+frame by frame.   python tests/soak/soak_runs.py [first_seed] [count]"""
 import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("ORCA_REORDER_EVERY", "3")
 

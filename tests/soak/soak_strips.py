@@ -2,12 +2,12 @@
 adjacent strips with device-to-device buffer swaps in place of NCCL (tests/test_gpu_strips.py),
 random crowds / densities / strip counts, 12 frames with a row reordering every third frame; the
 decomposed crowd must equal the single-handle run bit for bit, keyed by id.
-    python scripts/soak_strips.py [first_seed] [count]"""
+    python tests/soak/soak_strips.py [first_seed] [count]"""
 import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, ROOT)
 
