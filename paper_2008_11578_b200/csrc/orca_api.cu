@@ -62,9 +62,8 @@ struct orca_sim {
     int max_cells = 0;
     int *cell_of = nullptr, *rank_of = nullptr, *cell_count = nullptr, *cell_start = nullptr,
         *block_sums = nullptr;
-    void *s_xy = nullptr, *s_pv = nullptr, *s_dm = nullptr;
+    void *s_xy = nullptr, *s_nr = nullptr, *s_dm = nullptr; // s_nr: NbRec<S>, 8 storage words per slot
     int *s_row = nullptr, *s_cell = nullptr;
-    void *s_rc = nullptr; // (radius, class) in the storage type
     int *nb = nullptr;
     u8 *nb_cnt = nullptr;
     int *fq = nullptr;
@@ -247,11 +246,10 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->cell_start);
     cudaFree(sim->block_sums);
     cudaFree(sim->s_xy);
-    cudaFree(sim->s_pv);
+    cudaFree(sim->s_nr);
     cudaFree(sim->s_dm);
     cudaFree(sim->s_row);
     cudaFree(sim->s_cell);
-    cudaFree(sim->s_rc);
     cudaFree(sim->nb);
     cudaFree(sim->nb_cnt);
     cudaFree(sim->fq);
@@ -355,11 +353,10 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->cell_start, (size_t)sim->max_cells + 1));
     CKC(dalloc(&sim->block_sums, (size_t)sim->max_cells / SCAN_TILE + 2));
     CKC(cudaMalloc(&sim->s_xy, cap * 2 * rs));
-    CKC(cudaMalloc(&sim->s_pv, cap * 4 * rs));
+    CKC(cudaMalloc(&sim->s_nr, cap * 8 * rs));
     CKC(cudaMalloc(&sim->s_dm, cap * 4 * as));
     CKC(dalloc(&sim->s_row, cap));
     CKC(dalloc(&sim->s_cell, cap));
-    CKC(cudaMalloc(&sim->s_rc, cap * 2 * rs));
     CKC(dalloc(&sim->nb, cap * ORCA_MAX_NEIGHBORS));
     CKC(dalloc(&sim->nb_cnt, cap));
     CKC(dalloc(&sim->fq, cap));
@@ -734,8 +731,8 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
     k_scatter<S, R><<<grid_for(n, 256), 256, 0, st>>>(
         sim->plan, P, pv, reinterpret_cast<const S4 *>(sim->goalpref[sim->acur]),
         reinterpret_cast<const S2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], sim->cell_of, sim->rank_of,
-        sim->cell_start, reinterpret_cast<S2 *>(sim->s_xy), reinterpret_cast<S4 *>(sim->s_pv),
-        reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell, reinterpret_cast<S2 *>(sim->s_rc));
+        sim->cell_start, reinterpret_cast<S2 *>(sim->s_xy), reinterpret_cast<NbRec<S> *>(sim->s_nr),
+        reinterpret_cast<R4 *>(sim->s_dm), sim->s_row, sim->s_cell);
     CKL(sim);
     sim->launches += 6;
     sim->binned_frame = sim->frame;
@@ -789,12 +786,12 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
             CK(sim, cudaStreamWaitEvent(cs, sim->ev_vel, 0));
             k_patch_vel<S><<<grid_for(n, 256), 256, 0, cs>>>(
                 sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
-                reinterpret_cast<S4 *>(sim->s_pv), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
+                reinterpret_cast<NbRec<S> *>(sim->s_nr), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
             sim->launches += 1;
         }
 #define ORCA_SOLVE_ARGS                                                                                    \
-    sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),        \
-        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
+    sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
+        sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1,  \
         sim->lrow[a]
@@ -816,8 +813,8 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     sim->mark();
     if (sim->fb_coop) {
 #define ORCA_FB_ARGS                                                                                       \
-    sim->plan, P, reinterpret_cast<const S4 *>(sim->s_pv), reinterpret_cast<const R4 *>(sim->s_dm),        \
-        reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
+    sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
+        sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
         sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state)
         // long-queue and short-queue instance; the device-side queue length decides which one works
@@ -839,8 +836,8 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         const int fb_at = (C::fb_threads / 32) * lanes;           // agents per block per pass
         const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + fb_at - 1) / fb_at));
         k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * fb_at, st>>>(
-            sim->plan, P, lanes, reinterpret_cast<const S4 *>(sim->s_pv),
-            reinterpret_cast<const R4 *>(sim->s_dm), reinterpret_cast<const S2 *>(sim->s_rc), sim->s_row,
+            sim->plan, P, lanes, reinterpret_cast<const NbRec<S> *>(sim->s_nr),
+            reinterpret_cast<const R4 *>(sim->s_dm), sim->s_row,
             sim->ids[a], sim->nb, sim->nb_cnt, reinterpret_cast<const S4 *>(sim->goalpref[a]),
             reinterpret_cast<S4 *>(sim->pv[out_idx]), sim->arrived, sim->fq,
             reinterpret_cast<const R4 *>(sim->fq_state));

@@ -366,9 +366,9 @@ k_scan_apply(const int *__restrict__ len_ptr, int len_extra, const int *__restri
 
 // Scatter into cell-sorted order. Writes, per sorted slot s:
 //   s_xy  (x, y)                         candidate stream of the neighbour search
-//   s_pv  (x, y, vx, vy)                 pre-step snapshot
+//   s_nr  (x, y, vx, vy | radius, class code | pad)   pre-step snapshot, one 32 B record (NbRec):
+//                                                      what neighbours read of an agent
 //   s_dm  (des_vx, des_vy, max_speed, avoid_radius)   own LP inputs, arithmetic type
-//   s_rc  (radius, class code)                         what neighbours read of an agent
 //   s_row storage row, s_cell search cell
 template <typename S, typename R>
 __global__ void __launch_bounds__(256)
@@ -377,8 +377,8 @@ k_scatter(const GridPlan *__restrict__ plan, StepParams P,
           const typename Vec<S>::T2 *__restrict__ radmax, const u8 *__restrict__ cls,
           const int *__restrict__ cell_of, const int *__restrict__ rank_of,
           const int *__restrict__ cell_start, typename Vec<S>::T2 *__restrict__ s_xy,
-          typename Vec<S>::T4 *__restrict__ s_pv, typename Vec<R>::T4 *__restrict__ s_dm,
-          int *__restrict__ s_row, int *__restrict__ s_cell, typename Vec<S>::T2 *__restrict__ s_rc)
+          NbRec<S> *__restrict__ s_nr, typename Vec<R>::T4 *__restrict__ s_dm,
+          int *__restrict__ s_row, int *__restrict__ s_cell)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= plan->n) return;
@@ -396,11 +396,14 @@ k_scatter(const GridPlan *__restrict__ plan, StepParams P,
     // engine.py:227 (evaluated in FP64, then rounded to R)
     const R avoid = (R)((double)rm.x + P.half_margin);
     s_xy[s] = mk2(a.x, a.y);
-    s_pv[s] = a;
+    NbRec<S> rec;
+    rec.pv = a;
+    rec.rc = mk2(rm.x, (S)cls[i]); // radius and class: what a neighbour needs besides pv
+    rec.pad = mk2(S(0), S(0));
+    s_nr[s] = rec;
     s_dm[s] = mk4(dx * scale, dy * scale, (R)rm.y, avoid);
     s_row[s] = i;
     s_cell[s] = c;
-    s_rc[s] = mk2(rm.x, (S)cls[i]); // what a neighbour needs besides s_pv: radius and class
 }
 
 // ---------------------------------------------------------------------------
@@ -1108,13 +1111,13 @@ __device__ __forceinline__ void shuffle_smem(u8 *perm, int stride, int k, u64 se
 // slower, profiles/r01_notes.md.)
 template <typename S, typename R>
 __device__ __forceinline__ bool build_constraints(
-    int s, int cnt, const StepParams &P, const typename Vec<S>::T4 *__restrict__ s_pv,
-    const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ nb, const u8 *perm,
+    int s, int cnt, const StepParams &P, const NbRec<S> *__restrict__ s_nr,
+    const int *__restrict__ nb, const u8 *perm,
     int stride, SmemCons<R> &cons, int &bad_j)
 {
-    const typename Vec<S>::T4 me_s = s_pv[s];
+    const typename Vec<S>::T4 me_s = s_nr[s].pv;
     const R mex = (R)me_s.x, mey = (R)me_s.y, mevx = (R)me_s.z, mevy = (R)me_s.w;
-    const typename Vec<S>::T2 rc_i = s_rc[s];
+    const typename Vec<S>::T2 rc_i = s_nr[s].rc;
     const R ri = (R)((double)rc_i.x + P.half_margin); // engine.py:227, as in k_scatter
     const int ci = (int)rc_i.y;
     const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt); // K:358 / K:378, once
@@ -1125,16 +1128,18 @@ __device__ __forceinline__ bool build_constraints(
     typename Vec<S>::T2 rc_next = rc_i;
     if (cnt > 0) {
         const int jn = nb[(size_t)perm[0] * P.stride + s];
-        q_next = s_pv[jn];
-        rc_next = s_rc[jn];
+        const NbRec<S> rn = s_nr[jn];
+        q_next = rn.pv;
+        rc_next = rn.rc;
     }
     for (int pos = 0; pos < cnt; ++pos) {
         const typename Vec<S>::T4 q = q_next;
         const typename Vec<S>::T2 rc_j = rc_next;
         if (pos + 1 < cnt) {
             const int jn = nb[(size_t)perm[(pos + 1) * stride] * P.stride + s];
-            q_next = s_pv[jn];
-            rc_next = s_rc[jn];
+            const NbRec<S> rn = s_nr[jn];
+            q_next = rn.pv;
+            rc_next = rn.rc;
         }
         const R rj = (R)((double)rc_j.x + P.half_margin);
         R ux, uy, nx, ny;
@@ -1175,8 +1180,8 @@ __device__ __forceinline__ void integrate_row(int row, const typename Vec<S>::T4
 
 template <typename S, typename R, int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
-k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__restrict__ s_pv,
-        const typename Vec<R>::T4 *__restrict__ s_dm, const typename Vec<S>::T2 *__restrict__ s_rc,
+k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
+        const typename Vec<R>::T4 *__restrict__ s_dm,
         const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
         const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
         typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
@@ -1195,14 +1200,14 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
     if (!active) return;
 
     const int cnt = nb_cnt[s];
-    const typename Vec<S>::T4 me = s_pv[s];
+    const typename Vec<S>::T4 me = s_nr[s].pv;
     const typename Vec<R>::T4 dm = s_dm[s];
     u8 *perm = sm_perm + threadIdx.x;
     SmemCons<R> cons{sm_cons + threadIdx.x, THREADS};
 
     shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(plan->frame, ids[row]));
     int bad_j = -1;
-    const bool built = build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, THREADS, cons, bad_j);
+    const bool built = build_constraints<S, R>(s, cnt, P, s_nr, nb, perm, THREADS, cons, bad_j);
 #if !ORCA_LP_RUNAHEAD
     if (!built) {
 #else
@@ -1248,8 +1253,8 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__
 // exact and order-independent, so results are unchanged).
 template <typename S, typename R, int MAXN, int THREADS, int GL>
 __global__ void __launch_bounds__(THREADS, (GL == 2 ? ORCA_SG_BLOCKS : 8))
-k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::T4 *__restrict__ s_pv,
-              const typename Vec<R>::T4 *__restrict__ s_dm, const typename Vec<S>::T2 *__restrict__ s_rc,
+k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
+              const typename Vec<R>::T4 *__restrict__ s_dm,
               const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
               const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
               typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
@@ -1272,7 +1277,7 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
     if (!active) return; // uniform over the group
 
     const int cnt = nb_cnt[s];
-    const typename Vec<S>::T4 me = s_pv[s];
+    const typename Vec<S>::T4 me = s_nr[s].pv;
     const typename Vec<R>::T4 dm = s_dm[s];
     u8 *perm = sm_perm + g;
     SmemCons<R> cons{sm_cons + g, NG};
@@ -1282,7 +1287,7 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
     bool ok_mine = true;
     {   // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
         const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
-        const typename Vec<S>::T2 rc_i = s_rc[s];
+        const typename Vec<S>::T2 rc_i = s_nr[s].rc;
         const R ri = (R)((double)rc_i.x + P.half_margin);
         const int ci = (int)rc_i.y;
         const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
@@ -1295,8 +1300,9 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
         typename Vec<S>::T2 rc_next = rc_i;
         if (gl < cnt) {
             const int jn = nb[(size_t)perm[gl * NG] * P.stride + s];
-            q_next = s_pv[jn];
-            rc_next = s_rc[jn];
+            const NbRec<S> rn = s_nr[jn];
+            q_next = rn.pv;
+            rc_next = rn.rc;
         }
 #endif
 #pragma unroll kBuildUnroll
@@ -1306,13 +1312,15 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
             const typename Vec<S>::T2 rc_j = rc_next;
             if (pos + GL < cnt) {
                 const int jn = nb[(size_t)perm[(pos + GL) * NG] * P.stride + s];
-                q_next = s_pv[jn];
-                rc_next = s_rc[jn];
+                const NbRec<S> rn = s_nr[jn];
+                q_next = rn.pv;
+                rc_next = rn.rc;
             }
 #else
             const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
-            const typename Vec<S>::T4 qv = s_pv[j];
-            const typename Vec<S>::T2 rc_j = s_rc[j];
+            const NbRec<S> rj_rec = s_nr[j];
+            const typename Vec<S>::T4 qv = rj_rec.pv;
+            const typename Vec<S>::T2 rc_j = rj_rec.rc;
 #endif
             const R rj = (R)((double)rc_j.x + P.half_margin);
             R ux, uy, nx, ny;
@@ -1364,8 +1372,8 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const typename Vec<S>::
 template <typename S, typename R, int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
-           const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
-           const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ s_row,
+           const NbRec<S> *__restrict__ s_nr, const typename Vec<R>::T4 *__restrict__ s_dm,
+        const int *__restrict__ s_row,
            const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
            const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
            u8 *__restrict__ arrived, const int *__restrict__ fq,
@@ -1388,7 +1396,7 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
         const R4 st = fq_state[q];
         const int row = s_row[s];
         const int cnt = nb_cnt[s];
-        const typename Vec<S>::T4 me = s_pv[s];
+        const typename Vec<S>::T4 me = s_nr[s].pv;
         const R4 dm = s_dm[s];
         u8 *perm = sm_perm + at;
         u8 *inv = sm_inv + at;
@@ -1398,7 +1406,7 @@ k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
         shuffle_smem<MAXN>(perm, AT, cnt, problem_seed(plan->frame, ids[row]));
         for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * AT] * AT] = (u8)pos;
         int bad_j;
-        build_constraints<S, R>(s, cnt, P, s_pv, s_rc, nb, perm, AT, cons, bad_j);
+        build_constraints<S, R>(s, cnt, P, s_nr, nb, perm, AT, cons, bad_j);
 
         SmemConsIdent<R> ident{sm_cons + at, inv, AT};
         R rx, ry;
@@ -1424,8 +1432,8 @@ __global__ void __launch_bounds__(THREADS, ORCA_FB_BLOCKS)
 __global__ void __launch_bounds__(THREADS)
 #endif
 k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
-                const typename Vec<S>::T4 *__restrict__ s_pv, const typename Vec<R>::T4 *__restrict__ s_dm,
-                const typename Vec<S>::T2 *__restrict__ s_rc, const int *__restrict__ s_row,
+                const NbRec<S> *__restrict__ s_nr, const typename Vec<R>::T4 *__restrict__ s_dm,
+        const int *__restrict__ s_row,
                 const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
                 const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
                 u8 *__restrict__ arrived, const int *__restrict__ fq,
@@ -1461,7 +1469,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         typename Vec<S>::T4 me = mk4(S(0), S(0), S(0), S(0));
         R4 dm = mk4(R(0), R(0), R(0), R(0));
         if (enabled) {
-            me = s_pv[s];
+            me = s_nr[s].pv;
             dm = s_dm[s];
         }
 #else
@@ -1471,7 +1479,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         const R4 st = fq_state[q];
         const int row = s_row[s];
         const int cnt = nb_cnt[s];
-        const typename Vec<S>::T4 me = s_pv[s];
+        const typename Vec<S>::T4 me = s_nr[s].pv;
         const R4 dm = s_dm[s];
 #endif
         u8 *perm = sm_perm + g;
@@ -1486,15 +1494,16 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         __syncwarp(gmask);
         if (enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
             const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
-            const typename Vec<S>::T2 rc_i = s_rc[s];
+            const typename Vec<S>::T2 rc_i = s_nr[s].rc;
             const R ri = (R)((double)rc_i.x + P.half_margin);
             const int ci = (int)rc_i.y;
             const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
             const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt);
             for (int pos = gl; pos < cnt; pos += GL) {
                 const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
-                const typename Vec<S>::T4 qv = s_pv[j];
-                const typename Vec<S>::T2 rc_j = s_rc[j];
+                const NbRec<S> rj_rec = s_nr[j];
+                const typename Vec<S>::T4 qv = rj_rec.pv;
+                const typename Vec<S>::T2 rc_j = rj_rec.rc;
                 const R rj = (R)((double)rc_j.x + P.half_margin);
                 R ux, uy, nx, ny;
                 vo_exit_inv<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, inv_tau,
@@ -1874,7 +1883,7 @@ k_import_pos(int n, const double *__restrict__ pos, typename Vec<R>::T4 *__restr
 template <typename R>
 __global__ void __launch_bounds__(256)
 k_patch_vel(const GridPlan *__restrict__ plan, const double *__restrict__ vel,
-            typename Vec<R>::T4 *__restrict__ pv, typename Vec<R>::T4 *__restrict__ s_pv,
+            typename Vec<R>::T4 *__restrict__ pv, NbRec<R> *__restrict__ s_nr,
             const int *__restrict__ cell_of, const int *__restrict__ rank_of,
             const int *__restrict__ cell_start, const int *__restrict__ lrow)
 {
@@ -1885,7 +1894,7 @@ k_patch_vel(const GridPlan *__restrict__ plan, const double *__restrict__ vel,
     a.z = (R)vel[2 * l];
     a.w = (R)vel[2 * l + 1];
     pv[i] = a;
-    s_pv[cell_start[cell_of[i]] + rank_of[i]] = a;
+    s_nr[cell_start[cell_of[i]] + rank_of[i]].pv = a;
 }
 
 template <typename R>

@@ -26,6 +26,15 @@ template <typename R> struct Vec;
 template <> struct Vec<float> { typedef float2 T2; typedef float4 T4; };
 template <> struct Vec<double> { typedef double2 T2; typedef double4 T4; };
 
+// What a neighbour reads of an agent, in ONE aligned record of the cell-sorted snapshot:
+// (x, y, vx, vy) and (radius, class code). FP32 state: 32 B = one DRAM/L2 sector, fetched by a
+// single 256-bit load (LDG.E.ENL2.256); as two arrays (16 B + 8 B) every neighbour cost two sectors.
+template <typename S> struct __align__(8 * sizeof(S)) NbRec {
+    typename Vec<S>::T4 pv;
+    typename Vec<S>::T2 rc;
+    typename Vec<S>::T2 pad;
+};
+
 template <typename R> __device__ __forceinline__ R rsqrt_exact(R x);
 template <> __device__ __forceinline__ float rsqrt_exact<float>(float x) { return __fsqrt_rn(x); }
 template <> __device__ __forceinline__ double rsqrt_exact<double>(double x) { return __dsqrt_rn(x); }
