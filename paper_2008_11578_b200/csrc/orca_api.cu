@@ -68,6 +68,12 @@ struct orca_sim {
     u8 *nb_cnt = nullptr;
     int *fq = nullptr;
     void *fq_state = nullptr;
+    // half-planes (R4 x MAXN) and insertion order (u8 x MAXN) of the queued agents, written by the
+    // solve kernels, read by k_fallback_coop; sized by orca_set_params for the max_neighbors in use
+    void *fq_cons = nullptr;
+    u8 *fq_perm = nullptr;
+    int spill_maxn = 0;
+    bool fb_spill = true;
     int *gq = nullptr; // agents queued for the exact ring search
     GridPlan *plan = nullptr;
     GridPlan *h_plan = nullptr; // pinned mirror
@@ -254,6 +260,8 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->nb_cnt);
     cudaFree(sim->fq);
     cudaFree(sim->fq_state);
+    cudaFree(sim->fq_cons);
+    cudaFree(sim->fq_perm);
     cudaFree(sim->gq);
     cudaFree(sim->plan);
     cudaFree(sim->stg);
@@ -298,6 +306,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
     if (const char *gk = getenv("ORCA_GATHER_KEYS32")) sim->gather_keys32 = atoi(gk) != 0;
     if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
+    if (const char *fs = getenv("ORCA_FB_SPILL")) sim->fb_spill = atoi(fs) != 0;
     sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
     if (const char *sg = getenv("ORCA_SOLVE_GL")) sim->solve_gl = atoi(sg) >= 4 ? 4 : (atoi(sg) >= 2 ? 2 : 1);
     if (const char *re = getenv("ORCA_REORDER_EVERY")) sim->reorder_every = std::max(0, atoi(re));
@@ -403,6 +412,22 @@ extern "C" int orca_set_params(orca_sim *sim, const orca_params *p)
         return fail(sim, ORCA_EUNSUPPORTED, "max_neighbors %d exceeds ORCA_MAX_NEIGHBORS (%d)",
                     p->max_neighbors, ORCA_MAX_NEIGHBORS);
     if (!sim->have_params || memcmp(&sim->params, p, sizeof(orca_params)) != 0) sim->drop_graphs();
+    const int maxn = p->max_neighbors <= 16 ? 16 : 32; // the MAXN the step's kernels are instantiated for
+    if (sim->fb_spill && sim->fb_coop && maxn > sim->spill_maxn) {
+        CK(sim, cudaSetDevice(sim->device));
+        CK(sim, cudaStreamSynchronize(sim->stream));
+        sim->drop_graphs(); // captured launches hold the old pointers
+        cudaFree(sim->fq_cons);
+        cudaFree(sim->fq_perm);
+        sim->fq_cons = nullptr;
+        sim->fq_perm = nullptr;
+        sim->spill_maxn = 0;
+        const size_t cap = (size_t)(sim->capacity > 0 ? sim->capacity : 1);
+        const size_t as = sim->precision == ORCA_F32 ? sizeof(float) : sizeof(double);
+        CK(sim, cudaMalloc(&sim->fq_cons, cap * maxn * 4 * as));
+        CK(sim, dalloc(&sim->fq_perm, cap * maxn));
+        sim->spill_maxn = maxn;
+    }
     sim->params = *p;
     sim->have_params = true;
     sim->binned_frame = -1;
@@ -748,6 +773,7 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
+    const bool spill = sim->fb_spill && sim->fb_coop && sim->spill_maxn >= MAXN && sim->fq_cons && sim->fq_perm;
     // Gather + solve over `chunks` ranges of sorted slots, alternating between the handle's
     // stream and an auxiliary one: the neighbour search (ALU/issue bound) of one range
     // overlaps the LP (FP64/latency bound) of another. chunks == 1 is the plain sequence.
@@ -794,7 +820,7 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1,  \
-        sim->lrow[a]
+        sim->lrow[a], spill ? reinterpret_cast<R4 *>(sim->fq_cons) : nullptr, spill ? sim->fq_perm : nullptr
         if (sim->solve_gl == 2)
             k_solve_group<S, R, MAXN, 128, 2><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(ORCA_SOLVE_ARGS);
         else if (sim->solve_gl == 4)
@@ -816,7 +842,8 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
         sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
-        sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state)
+        sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state),                               \
+        spill ? reinterpret_cast<const R4 *>(sim->fq_cons) : nullptr, spill ? sim->fq_perm : nullptr
         // long-queue and short-queue instance; the device-side queue length decides which one works
         const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
         const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + ng - 1) / ng));

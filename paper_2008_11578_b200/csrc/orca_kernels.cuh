@@ -43,6 +43,9 @@
 #ifndef ORCA_BUILD_PREFETCH
 #define ORCA_BUILD_PREFETCH 1 // k_solve_group: request the next neighbour's record one iteration ahead
 #endif
+#ifndef ORCA_FB_SPILL
+#define ORCA_FB_SPILL 1     // solve kernels hand the queued agents' constraints to k_fallback_coop through HBM
+#endif
 #ifndef ORCA_SG_BLOCKS
 #define ORCA_SG_BLOCKS 6    // resident blocks per SM k_solve_group is compiled for (register cap)
 #endif
@@ -1105,6 +1108,25 @@ __device__ __forceinline__ void shuffle_smem(u8 *perm, int stride, int k, u64 se
     }
 }
 
+// An agent queued for the least-penetration stage takes its half-planes (in shuffled order,
+// as they sit in shared memory) and its insertion order along: k_fallback_coop used to redo
+// the Fisher-Yates shuffle (one lane, ~630 instructions) and the whole constraint build
+// (16 vo_exit chains + 16 neighbour gathers) for every queued agent -- a quarter of its
+// instructions. MAXN * (sizeof(R4) + 1) bytes per queued agent go through L2/HBM instead.
+template <typename R, int MAXN>
+__device__ __forceinline__ void spill_constraints(typename Vec<R>::T4 *__restrict__ fq_cons,
+                                                  u8 *__restrict__ fq_perm, int q, int cnt,
+                                                  const typename Vec<R>::T4 *cons_base, const u8 *perm,
+                                                  int stride, int first, int step)
+{
+    typename Vec<R>::T4 *dst = fq_cons + (size_t)q * MAXN;
+    u8 *dp = fq_perm + (size_t)q * MAXN;
+    for (int pos = first; pos < cnt; pos += step) {
+        dst[pos] = cons_base[pos * stride];
+        dp[pos] = perm[pos * stride];
+    }
+}
+
 // Build the ORCA half-planes of agent s into `cons` in SHUFFLED order
 // (_kernels.py:525-541). Returns false on exactly coincident centres. (Walking the
 // neighbour ranks and scattering to the inverse permutation instead was measured 6 %
@@ -1186,7 +1208,8 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
         const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
         typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
         i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
-        typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow)
+        typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
+        typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typename Vec<R>::T4 *sm_cons = reinterpret_cast<typename Vec<R>::T4 *>(smem_raw);
@@ -1242,6 +1265,9 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
     const int q = atomicAdd(&plan->fq_count, 1);
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
+#if ORCA_FB_SPILL
+    if (fq_cons) spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + threadIdx.x, perm, THREADS, 0, 1);
+#endif
 }
 
 // k_solve with GL (2 or 4) adjacent lanes per agent. k_solve is bound by the latency of
@@ -1259,7 +1285,8 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
               const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
               typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
               i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
-              typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow)
+              typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
+              typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int NG = THREADS / GL; // agents per block
@@ -1340,6 +1367,14 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     R vx, vy;
     const bool feasible = g_lp2_target_runahead<R, GL, false, SmemCons<R>>(
         cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy, live, built, gl, gmask);
+    int q = 0;
+    if (built && !feasible) { // uniform over the group: queue for the least-penetration stage
+        if (gl == 0) q = atomicAdd(&plan->fq_count, 1);
+        q = __shfl_sync(gmask, q, gshift);
+#if ORCA_FB_SPILL
+        if (fq_cons) spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + g, perm, NG, gl, GL);
+#endif
+    }
     if (gl != 0) return;
     if (!built) {
         // _kernels.py:542-547 + engine.py:239-245; coincident neighbours lead the list
@@ -1358,7 +1393,6 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     }
     status[row] = 1;
     failed_at[row] = (i8)perm[fail_pos * NG];
-    const int q = atomicAdd(&plan->fq_count, 1);
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
 }
@@ -1437,7 +1471,8 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
                 const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
                 u8 *__restrict__ arrived, const int *__restrict__ fq,
-                const typename Vec<R>::T4 *__restrict__ fq_state)
+                const typename Vec<R>::T4 *__restrict__ fq_state,
+                const typename Vec<R>::T4 *__restrict__ fq_cons, const u8 *__restrict__ fq_perm)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef typename Vec<R>::T4 R4;
@@ -1487,12 +1522,27 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         SmemCons<R> cons{sm_cons + g, NG};
         SmemCons<R> proj{sm_proj + g, NG};
 
-        if (gl == 0 && enabled) {
+#if ORCA_FB_SPILL
+        const bool spilled = fq_cons != nullptr;
+        if (spilled && enabled) { // the half-planes and their order as the solve kernel left them
+            const R4 *src = fq_cons + (size_t)q * MAXN;
+            const u8 *sp = fq_perm + (size_t)q * MAXN;
+            for (int pos = gl; pos < cnt; pos += GL) {
+                sm_cons[g + pos * NG] = src[pos];
+                const int t = (int)sp[pos];
+                perm[pos * NG] = (u8)t;
+                inv[t * NG] = (u8)pos;
+            }
+        }
+#else
+        const bool spilled = false;
+#endif
+        if (!spilled && gl == 0 && enabled) {
             shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
             for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * NG] * NG] = (u8)pos;
         }
         __syncwarp(gmask);
-        if (enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
+        if (!spilled && enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
             const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
             const typename Vec<S>::T2 rc_i = s_nr[s].rc;
             const R ri = (R)((double)rc_i.x + P.half_margin);
