@@ -73,7 +73,6 @@ struct orca_sim {
     void *fq_cons = nullptr;
     u8 *fq_perm = nullptr;
     int spill_maxn = 0;
-    bool fb_spill = true;
     int *gq = nullptr; // agents queued for the exact ring search
     GridPlan *plan = nullptr;
     GridPlan *h_plan = nullptr; // pinned mirror
@@ -306,7 +305,6 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
     if (const char *gk = getenv("ORCA_GATHER_KEYS32")) sim->gather_keys32 = atoi(gk) != 0;
     if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
-    if (const char *fs = getenv("ORCA_FB_SPILL")) sim->fb_spill = atoi(fs) != 0;
     sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
     if (const char *sg = getenv("ORCA_SOLVE_GL")) sim->solve_gl = atoi(sg) >= 4 ? 4 : (atoi(sg) >= 2 ? 2 : 1);
     if (const char *re = getenv("ORCA_REORDER_EVERY")) sim->reorder_every = std::max(0, atoi(re));
@@ -413,7 +411,7 @@ extern "C" int orca_set_params(orca_sim *sim, const orca_params *p)
                     p->max_neighbors, ORCA_MAX_NEIGHBORS);
     if (!sim->have_params || memcmp(&sim->params, p, sizeof(orca_params)) != 0) sim->drop_graphs();
     const int maxn = p->max_neighbors <= 16 ? 16 : 32; // the MAXN the step's kernels are instantiated for
-    if (sim->fb_spill && sim->fb_coop && maxn > sim->spill_maxn) {
+    if (ORCA_FB_SPILL && maxn > sim->spill_maxn) {
         CK(sim, cudaSetDevice(sim->device));
         CK(sim, cudaStreamSynchronize(sim->stream));
         sim->drop_graphs(); // captured launches hold the old pointers
@@ -773,7 +771,9 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
-    const bool spill = sim->fb_spill && sim->fb_coop && sim->spill_maxn >= MAXN && sim->fq_cons && sim->fq_perm;
+    const bool spill = ORCA_FB_SPILL != 0;
+    if (spill && (sim->spill_maxn < MAXN || !sim->fq_cons || !sim->fq_perm))
+        return fail(sim, ORCA_EINVAL, "solve_stage: no spill buffers for max_neighbors %d", P.max_n);
     // Gather + solve over `chunks` ranges of sorted slots, alternating between the handle's
     // stream and an auxiliary one: the neighbour search (ALU/issue bound) of one range
     // overlaps the LP (FP64/latency bound) of another. chunks == 1 is the plain sequence.

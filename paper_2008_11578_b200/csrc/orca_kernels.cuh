@@ -1266,7 +1266,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
 #if ORCA_FB_SPILL
-    if (fq_cons) spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + threadIdx.x, perm, THREADS, 0, 1);
+    spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + threadIdx.x, perm, THREADS, 0, 1);
 #endif
 }
 
@@ -1372,7 +1372,7 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
         if (gl == 0) q = atomicAdd(&plan->fq_count, 1);
         q = __shfl_sync(gmask, q, gshift);
 #if ORCA_FB_SPILL
-        if (fq_cons) spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + g, perm, NG, gl, GL);
+        spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + g, perm, NG, gl, GL);
 #endif
     }
     if (gl != 0) return;
@@ -1521,28 +1521,24 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
         u8 *inv = sm_inv + g;
         SmemCons<R> cons{sm_cons + g, NG};
         SmemCons<R> proj{sm_proj + g, NG};
+        (void)perm;
 
 #if ORCA_FB_SPILL
-        const bool spilled = fq_cons != nullptr;
-        if (spilled && enabled) { // the half-planes and their order as the solve kernel left them
+        if (enabled) { // the half-planes and their order as the solve kernel left them
             const R4 *src = fq_cons + (size_t)q * MAXN;
             const u8 *sp = fq_perm + (size_t)q * MAXN;
             for (int pos = gl; pos < cnt; pos += GL) {
                 sm_cons[g + pos * NG] = src[pos];
-                const int t = (int)sp[pos];
-                perm[pos * NG] = (u8)t;
-                inv[t * NG] = (u8)pos;
+                inv[(int)sp[pos] * NG] = (u8)pos;
             }
         }
 #else
-        const bool spilled = false;
-#endif
-        if (!spilled && gl == 0 && enabled) {
+        if (gl == 0 && enabled) {
             shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
             for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * NG] * NG] = (u8)pos;
         }
         __syncwarp(gmask);
-        if (!spilled && enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
+        if (enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
             const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
             const typename Vec<S>::T2 rc_i = s_nr[s].rc;
             const R ri = (R)((double)rc_i.x + P.half_margin);
@@ -1562,6 +1558,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
             }
         }
+#endif
         __syncwarp(gmask);
 
         SmemConsIdent<R> ident{sm_cons + g, inv, NG};
