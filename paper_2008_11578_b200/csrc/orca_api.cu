@@ -72,6 +72,7 @@ struct orca_sim {
     // solve kernels, read by k_fallback_coop; sized by orca_set_params for the max_neighbors in use
     void *fq_cons = nullptr;
     u8 *fq_perm = nullptr;
+    u8 *s_perm = nullptr; // insertion order per sorted slot (k_shuffle -> k_solve_group), spill_maxn bytes each
     int spill_maxn = 0;
     int *gq = nullptr; // agents queued for the exact ring search
     GridPlan *plan = nullptr;
@@ -201,10 +202,16 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::solve_bpt * C::solve_threads);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::solve_bpt * 64);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::solve_bpt * 64);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::solve_bpt * 32);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::solve_bpt * 32);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
@@ -261,6 +268,7 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->fq_state);
     cudaFree(sim->fq_cons);
     cudaFree(sim->fq_perm);
+    cudaFree(sim->s_perm);
     cudaFree(sim->gq);
     cudaFree(sim->plan);
     cudaFree(sim->stg);
@@ -417,13 +425,16 @@ extern "C" int orca_set_params(orca_sim *sim, const orca_params *p)
         sim->drop_graphs(); // captured launches hold the old pointers
         cudaFree(sim->fq_cons);
         cudaFree(sim->fq_perm);
+        cudaFree(sim->s_perm);
         sim->fq_cons = nullptr;
         sim->fq_perm = nullptr;
+        sim->s_perm = nullptr;
         sim->spill_maxn = 0;
         const size_t cap = (size_t)(sim->capacity > 0 ? sim->capacity : 1);
         const size_t as = sim->precision == ORCA_F32 ? sizeof(float) : sizeof(double);
         CK(sim, cudaMalloc(&sim->fq_cons, cap * maxn * 4 * as));
         CK(sim, dalloc(&sim->fq_perm, cap * maxn));
+        CK(sim, dalloc(&sim->s_perm, cap * maxn));
         sim->spill_maxn = maxn;
     }
     sim->params = *p;
@@ -821,10 +832,27 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1,  \
         sim->lrow[a], spill ? reinterpret_cast<R4 *>(sim->fq_cons) : nullptr, spill ? sim->fq_perm : nullptr
-        if (sim->solve_gl == 2)
-            k_solve_group<S, R, MAXN, 128, 2><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(ORCA_SOLVE_ARGS);
+        // below ~64 k agents the step is launch-latency bound and the extra launch costs more than the
+        // idle lanes of the in-kernel shuffle (16,640 agents: +1.8 us)
+        const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && n >= ORCA_PRESHUFFLE_MIN_AGENTS;
+        const uint32_t *s_perm = preshuffle ? reinterpret_cast<const uint32_t *>(sim->s_perm) : nullptr;
+        if (preshuffle) {
+            k_shuffle<MAXN><<<grid_for(m, 128), 128, 0, cs>>>(sim->plan, sim->s_row, sim->ids[a], sim->nb_cnt,
+                                                             reinterpret_cast<uint4 *>(sim->s_perm), s0, s1);
+            sim->launches += 1;
+        }
+        if (sim->solve_gl == 2 && preshuffle)
+            k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(
+                ORCA_SOLVE_ARGS, s_perm);
+        else if (sim->solve_gl == 2)
+            k_solve_group<S, R, MAXN, 128, 2, false><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(
+                ORCA_SOLVE_ARGS, s_perm);
+        else if (sim->solve_gl == 4 && preshuffle)
+            k_solve_group<S, R, MAXN, 128, 4, true><<<grid_for(m, 32), 128, C::solve_bpt * 32, cs>>>(
+                ORCA_SOLVE_ARGS, s_perm);
         else if (sim->solve_gl == 4)
-            k_solve_group<S, R, MAXN, 128, 4><<<grid_for(m, 32), 128, C::solve_bpt * 32, cs>>>(ORCA_SOLVE_ARGS);
+            k_solve_group<S, R, MAXN, 128, 4, false><<<grid_for(m, 32), 128, C::solve_bpt * 32, cs>>>(
+                ORCA_SOLVE_ARGS, s_perm);
         else
             k_solve<S, R, MAXN, C::solve_threads><<<grid_for(m, C::solve_threads), C::solve_threads,
                                                     C::solve_bpt * C::solve_threads, cs>>>(ORCA_SOLVE_ARGS);

@@ -43,6 +43,12 @@
 #ifndef ORCA_BUILD_PREFETCH
 #define ORCA_BUILD_PREFETCH 1 // k_solve_group: request the next neighbour's record one iteration ahead
 #endif
+#ifndef ORCA_PRESHUFFLE
+#define ORCA_PRESHUFFLE 1   // k_solve_group reads the insertion order k_shuffle computed, one thread per agent
+#endif
+#ifndef ORCA_PRESHUFFLE_MIN_AGENTS
+#define ORCA_PRESHUFFLE_MIN_AGENTS 65536
+#endif
 #ifndef ORCA_FB_SPILL
 #define ORCA_FB_SPILL 1     // solve kernels hand the queued agents' constraints to k_fallback_coop through HBM
 #endif
@@ -1270,6 +1276,33 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
 #endif
 }
 
+// The seeded Fisher-Yates order of every agent (K:43-61), one THREAD per agent. Inside
+// k_solve_group one lane of each pair drew it while its partner idled (12 % of that kernel's
+// warp instructions at half the lanes); here all 32 lanes of a warp draw. MAXN bytes per agent
+// go through L2 to the solve kernel.
+template <int MAXN>
+__global__ void __launch_bounds__(128)
+k_shuffle(const GridPlan *__restrict__ plan, const int *__restrict__ s_row, const i64 *__restrict__ ids,
+          const u8 *__restrict__ nb_cnt, uint4 *__restrict__ s_perm, int s0, int s1)
+{
+    __shared__ __align__(16) u8 sm[MAXN * 128];
+    const int s = s0 + blockIdx.x * 128 + threadIdx.x;
+    if (s >= min(s1, plan->n)) return;
+    const int row = s_row[s];
+    if (row >= plan->n_owned) return;
+    u8 *perm = sm + threadIdx.x;
+    const int cnt = nb_cnt[s];
+    shuffle_smem<MAXN>(perm, 128, cnt, problem_seed(plan->frame, ids[row]));
+    uint32_t w[MAXN / 4];
+#pragma unroll
+    for (int t = 0; t < MAXN / 4; ++t)
+        w[t] = (uint32_t)perm[(4 * t) * 128] | ((uint32_t)perm[(4 * t + 1) * 128] << 8) |
+               ((uint32_t)perm[(4 * t + 2) * 128] << 16) | ((uint32_t)perm[(4 * t + 3) * 128] << 24);
+#pragma unroll
+    for (int t = 0; t < MAXN / 16; ++t)
+        s_perm[(size_t)s * (MAXN / 16) + t] = make_uint4(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3]);
+}
+
 // k_solve with GL (2 or 4) adjacent lanes per agent. k_solve is bound by the latency of
 // dependent FP64 chains at the 12 warps/SM its shared memory allows (512 B of constraints
 // per thread). A group shares ONE agent's constraints, so the same shared memory holds GL
@@ -1277,7 +1310,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
 // half-planes at positions gl, gl+GL, ..., the run-ahead scan is executed redundantly and
 // the j loops of the 1-D solves are split over the group (max / min / any combinations:
 // exact and order-independent, so results are unchanged).
-template <typename S, typename R, int MAXN, int THREADS, int GL>
+template <typename S, typename R, int MAXN, int THREADS, int GL, bool PRESH>
 __global__ void __launch_bounds__(THREADS, (GL == 2 ? ORCA_SG_BLOCKS : 8))
 k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
               const typename Vec<R>::T4 *__restrict__ s_dm,
@@ -1286,7 +1319,8 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
               typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
               i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
               typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
-              typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm)
+              typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm,
+              const uint32_t *__restrict__ s_perm)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int NG = THREADS / GL; // agents per block
@@ -1309,7 +1343,19 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     u8 *perm = sm_perm + g;
     SmemCons<R> cons{sm_cons + g, NG};
 
-    if (gl == 0) shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
+    if constexpr (PRESH) { // the order k_shuffle drew: lane gl copies words gl, gl + GL, ... (4 positions each)
+        const uint32_t *src = s_perm + (size_t)s * (MAXN / 4);
+        for (int t = gl; 4 * t < cnt; t += GL) {
+            const uint32_t w = src[t];
+            perm[(4 * t) * NG] = (u8)(w & 0xFFu);
+            perm[(4 * t + 1) * NG] = (u8)((w >> 8) & 0xFFu);
+            perm[(4 * t + 2) * NG] = (u8)((w >> 16) & 0xFFu);
+            perm[(4 * t + 3) * NG] = (u8)(w >> 24);
+        }
+    } else { // small crowds: one launch fewer beats the idle lanes (separate instance: with both
+             // paths in one kernel the register cap spills and the gain is gone)
+        if (gl == 0) shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
+    }
     __syncwarp(gmask);
     bool ok_mine = true;
     {   // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
