@@ -1,0 +1,95 @@
+#!/usr/bin/env python
+"""Turn one scripts/final_evidence.sh run (gpurun_out/g_*) into the tracked files under profiles/
+(development tooling):   python scripts/refresh_profiles.py <tag>      e.g. tag = g"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = os.path.join(ROOT, "gpurun_out")
+P = os.path.join(ROOT, "profiles")
+tag = sys.argv[1] if len(sys.argv) > 1 else "g"
+
+
+def summary(kind, src):
+    return subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), kind, src],
+                          capture_output=True, text=True, check=True).stdout
+
+
+def last_json_line(path):
+    with open(path) as f:
+        lines = [l for l in f.read().splitlines() if l.startswith("{")]
+    return lines[-1]
+
+
+# bench lines
+for name in ("mixed", "f32", "f64", "ref"):
+    with open(os.path.join(P, f"bench_r01_{name}.json"), "w") as f:
+        f.write(last_json_line(os.path.join(G, f"g_{name}.json")) + "\n")
+shutil.copy(os.path.join(G, "g_configs.jsonl"), os.path.join(P, "bench_r01_configs.jsonl"))
+
+# ncu launch list and full captures
+head_l = (f"# Round 1 ({tag}) — ncu launch list, 1,048,576 agents, mixed precision, final state of the round\n\n"
+          "Command: `ORCA_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python "
+          "bench.py --steps 3 --warmup 3 --resident-only` (per-launch times are cold-cache and serialised: compare "
+          "shares; `k_import_*`, `k_iota`, `k_bbox`, `k_begin_bins`, `k_permute_rows` run once after the upload; the "
+          "first `k_gather` launch searches for every agent, ~0.9 ms, the others ~25 us).\n\n")
+with open(os.path.join(P, f"r01_{tag}_launches_mixed_1m.md"), "w") as f:
+    f.write(head_l + summary("launches", os.path.join(G, "g_launches.csv")))
+head_f = (f"# Round 1 ({tag}) — ncu --set full, kernels of the step, 1,048,576 agents, mixed precision, final state "
+          "of the round\n\nCommand: `ORCA_GRAPH=0 ncu --set full --clock-control none --import-source on -k "
+          "regex:\"k_solve_group|k_gather_fast32|k_scatter|k_fallback_coop|k_count|k_gather\" -s 40 -c 7 python "
+          "bench.py --steps 3 --warmup 4 --resident-only`\n\n")
+with open(os.path.join(P, f"r01_{tag}_full_mixed_1m.md"), "w") as f:
+    f.write(head_f + summary("full", os.path.join(G, "g_full.ncu-rep")))
+head_d = (f"# Round 1 ({tag}) — ncu --set full, solve and fallback kernels, 266,240 agents at 2.0 /m2 (79 % of the "
+          "agents in the least-penetration stage), mixed precision\n\nCommand: `ORCA_GRAPH=0 ncu --set full "
+          "--clock-control none -k regex:\"k_solve_group|k_fallback_coop\" -s 12 -c 3 python bench.py --steps 3 "
+          "--warmup 4 --resident-only --workload config3_262k_d2`\n\n")
+with open(os.path.join(P, f"r01_{tag}_full_mixed_dense2.md"), "w") as f:
+    f.write(head_d + summary("full", os.path.join(G, "g_full_d2.ncu-rep")))
+
+
+# traffic.json: DRAM bytes per launch and issue / pipe utilisation of the 1 M mixed capture
+def raw_rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return rows[0], rows[1], rows[2:]
+
+
+hdr, units, rows = raw_rows(os.path.join(G, "g_full.ncu-rep"))
+col = {k: i for i, k in enumerate(hdr)}
+
+
+def val(r, key):
+    v = float(r[col[key]].replace(",", ""))
+    u = units[col[key]]
+    return v * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}.get(u, 1.0)
+
+
+entry = {"source": f"profiles/r01_{tag}_full_mixed_1m.md", "ncu": {}}
+for r in rows:
+    name = r[col["Kernel Name"]]
+    short = name.split("<")[0].split()[-1].split("::")[-1]
+    if short in entry and short != "k_fallback_coop":
+        continue
+    if short == "k_fallback_coop" and ", 16>" in name.split("(")[0]:
+        continue          # the short-queue instance exits at once on this workload
+    entry[short] = int(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum"))
+    entry["ncu"][short] = {
+        "ipc": round(val(r, "sm__inst_executed.avg.per_cycle_elapsed"), 3),
+        "fp64_pipe_pct": round(val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"), 1),
+        "lanes": round(val(r, "smsp__thread_inst_executed_per_inst_executed.ratio"), 2),
+        "warps_pct": round(val(r, "sm__warps_active.avg.pct_of_peak_sustained_active"), 1)}
+tj = os.path.join(P, "traffic.json")
+with open(tj) as f:
+    t = json.load(f)
+t["plaza_1m/mixed"] = entry
+with open(tj, "w") as f:
+    json.dump(t, f, indent=1)
+    f.write("\n")
+print(json.dumps(entry, indent=1))
