@@ -758,10 +758,15 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
     k_count<S><<<grid_for(n, 256), 256, 0, st>>>(sim->plan, pv, sim->cell_of, sim->rank_of, sim->cell_count, P.nr,
                                                 sim->box_part);
     const int scan_blocks = (P.max_cells + 1 + SCAN_TILE - 1) / SCAN_TILE;
-    k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count, sim->block_sums);
-    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->block_sums);
-    k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count,
-                                                       sim->block_sums, sim->cell_start);
+    if (P.max_cells <= ORCA_SCAN_SMALL_CELLS) { // ncells <= max_cells: at most 33 tiles, typically a few
+        k_scan_small<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count, sim->cell_start);
+        sim->launches -= 2;
+    } else {
+        k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count, sim->block_sums);
+        k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->block_sums);
+        k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->ncells, 1, sim->cell_count,
+                                                           sim->block_sums, sim->cell_start);
+    }
     k_scatter<S, R><<<grid_for(n, 256), 256, 0, st>>>(
         sim->plan, P, pv, reinterpret_cast<const S4 *>(sim->goalpref[sim->acur]),
         reinterpret_cast<const S2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], sim->cell_of, sim->rank_of,

@@ -46,6 +46,9 @@
 #ifndef ORCA_PRESHUFFLE
 #define ORCA_PRESHUFFLE 1   // k_solve_group reads the insertion order k_shuffle computed, one thread per agent
 #endif
+#ifndef ORCA_SCAN_SMALL_CELLS
+#define ORCA_SCAN_SMALL_CELLS 65536 // search grids up to this many cells are scanned by one block (k_scan_small)
+#endif
 #ifndef ORCA_PRESHUFFLE_MIN_AGENTS
 #define ORCA_PRESHUFFLE_MIN_AGENTS 65536
 #endif
@@ -370,6 +373,35 @@ k_scan_apply(const int *__restrict__ len_ptr, int len_extra, const int *__restri
     for (int k = 0; k < SCAN_ITEMS; ++k) {
         if ((first + k) < len) out[first + k] = run;
         run += v[k];
+    }
+}
+
+// The same exclusive scan by ONE block, tile after tile with a running carry: for the search
+// grids of small crowds (a few tiles) one launch instead of three -- those steps are bound by
+// launch latency, not by work (1,024 agents: 13 dependent kernels in ~0.09 ms).
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_small(const int *__restrict__ len_ptr, int len_extra, const int *__restrict__ in, int *__restrict__ out)
+{
+    const int len = *len_ptr + len_extra;
+    __shared__ int sm[64];
+    int carry = 0;
+    for (int base = 0; base < len; base += SCAN_TILE) {
+        const int first = base + threadIdx.x * SCAN_ITEMS;
+        int v[SCAN_ITEMS];
+        int s = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) {
+            v[k] = (first + k) < len ? in[first + k] : 0;
+            s += v[k];
+        }
+        int total;
+        int run = carry + block_exclusive_scan(s, sm, total);
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) {
+            if ((first + k) < len) out[first + k] = run;
+            run += v[k];
+        }
+        carry += total;
     }
 }
 
