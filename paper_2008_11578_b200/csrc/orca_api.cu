@@ -880,8 +880,11 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         // long-queue and short-queue instance; the device-side queue length decides which one works
         const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
         const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + ng - 1) / ng));
-        k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
-            ORCA_FB_ARGS);
+        if (ORCA_GL_SHORT == ORCA_GL || n > ORCA_FB_SHORT_QUEUE) // a queue of <= n entries is never "long"
+            k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
+                ORCA_FB_ARGS);
+        else
+            sim->launches -= 1;
         if (ORCA_GL_SHORT != ORCA_GL) {
             const int ngs = C::fb_threads / ORCA_GL_SHORT;
             const int64_t qmax = std::min<int64_t>(n, ORCA_FB_SHORT_QUEUE);
