@@ -122,6 +122,11 @@ ORCA_API void orca_destroy(orca_sim *sim);
  * handle's own stream). Lets the caller order the step against its own work. */
 ORCA_API int orca_set_stream(orca_sim *sim, void *cuda_stream);
 
+/* Step parameters (ScenarioConfig fields consumed by engine._advance, scenario.py:80-99).
+ * The first call, and a later call that raises max_neighbors from <= 16 to > 16, also allocates
+ * the device scratch whose size depends on it (capacity * MAXN * 34 bytes with FP64 arithmetic,
+ * 18 with FP32, MAXN = 16 or 32: insertion orders, and the half-planes handed to the least-penetration stage);
+ * ORCA_ECUDA if that allocation fails. */
 ORCA_API int orca_set_params(orca_sim *sim, const orca_params *params);
 
 ORCA_API const char *orca_last_error(const orca_sim *sim);
