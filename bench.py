@@ -220,19 +220,29 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise RuntimeError("bench.py needs a CUDA device; there is no CPU fallback")
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
     if world > 1 or os.environ.get("ORCA_BENCH_FORCE_STRIPS"):
         # the strip-decomposed path; ORCA_BENCH_FORCE_STRIPS=1 runs it with a single rank
-        # (no neighbours) to smoke-test the NCCL plumbing on a one-GPU box
+        # (no neighbours) to smoke-test the NCCL plumbing on a one-GPU box.
+        # One rank per GPU over NCCL. With fewer GPUs than ranks (a functional run of the
+        # multi-process protocol on a smaller box) the ranks share devices, which NCCL refuses:
+        # the slabs are then staged through the host and travel over gloo -- labelled in the line.
         if "MASTER_ADDR" not in os.environ:
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("ORCA_STRIPS_BACKEND") or ("nccl" if ndev >= world else "gloo")
+        local = local % ndev
+        torch.cuda.set_device(local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         from paper_2008_11578_b200.parallel import strips
         args.make_sampler = lambda: ClockSampler(local)
         try:
             return strips.run_bench(args, rank, world, local)
         finally:
             dist.destroy_process_group()
+    torch.cuda.set_device(local)
 
     state, cfg, wl = build_workload(args.workload)
     n = state.active_count
@@ -366,15 +376,14 @@ def run_ours(args):
             del big
 
     dtype = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision]
-    wl.update(precision=args.precision,
-              cache="state advances every step; per-step working set ~%.0f MB > 126 MB L2, no flush"
-                    % (n * 260 / 1e6),
-              lp_fallbacks_last_step=fallbacks)
     line = {
         "metric": "agent_steps_per_s", "value": value, "unit": "agent-steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
-        "data": "synthetic", "config": wl, "clocks": clocks.summary(),
+        "data": "synthetic", "config": wl, "precision": args.precision,
+        "cache": "state advances every step; per-step working set ~%.0f MB > 126 MB L2, no flush"
+                 % (n * 260 / 1e6),
+        "lp_fallbacks_last_step": fallbacks, "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "agent-steps/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                 "call": "paper_2008_11578_b200.engine.step(state, config) -- full drop-in incl. "
@@ -490,6 +499,19 @@ def run_lp(args):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """python bench.py --gpus N (N > 1) outside torchrun: start N ranks of this script, one per
+    GPU, the way the driver's own multi-GPU launch does, and pass their exit code on."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -506,7 +528,15 @@ def main():
                     help="skip the context measurements (other precision modes, 8.5 M agents on one GPU)")
     ap.add_argument("--resident-only", action="store_true",
                     help="only the HBM-resident timing (for runs under ncu)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="--gpus N > 1: weak = one `workload` plaza per GPU (default), strong = ONE "
+                         "`workload` crowd cut into N strips (BASELINE config 5: --workload config5_8m)")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="--gpus N > 1: skip the bit-equality check against the same crowd on one GPU")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.workload not in LP_WORKLOADS:
+        if args.impl != "reference":   # (the CPU arm is one process whatever N is)
+            sys.exit(self_launch(args))
     if args.workload in LP_WORKLOADS:
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the steering step; "

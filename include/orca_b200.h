@@ -317,6 +317,75 @@ ORCA_API int orca_strip_append(orca_sim *sim, const orca_agent_record *records, 
 /* Forget the ghost rows without stepping. */
 ORCA_API int orca_strip_drop_ghosts(orca_sim *sim);
 
+/* ---- the same protocol without the host in the loop ----------------------------
+ *
+ * orca_strip_pack reports its count to the host, so every exchange costs host
+ * synchronisations. The calls below keep the counts on the device: a SLAB is a
+ * fixed-capacity DEVICE buffer of  sizeof(orca_slab_header) + cap * record_bytes  bytes;
+ * the packing kernels count into the header, the whole slab travels (its size is
+ * known to both ranks without asking), and the appending kernels read the count
+ * from the header. All five calls are asynchronous; the host keeps only upper
+ * bounds on the row count, refreshed whenever it does synchronise (orca_sync /
+ * orca_get_info, e.g. every 16 frames). A slab, or the handle, that turns out too
+ * small raises a sticky device-side flag reported by the next orca_sync as
+ * ORCA_ECAPACITY; nothing is lost silently.
+ *
+ * Per frame and rank (parallel/strips.py):
+ *   orca_strip_pack_halo(left slab, right slab)   -> exchange ->  orca_strip_append_slab(ghost = 1) x2
+ *   orca_strip_step(left slab, right slab)        -> exchange ->  orca_strip_append_slab(ghost = 0) x2
+ * Halo slabs carry orca_halo_record_f32 (32 B; FP32 state: ORCA_MIXED, ORCA_F32) or
+ * orca_halo_record_f64 (64 B; ORCA_F64): what a neighbour reads of an agent
+ * (_kernels.py:525-541: position, velocity, radius, class) plus the id that orders
+ * equal distances (_kernels.py:473-476). Migrant slabs carry full orca_agent_record. */
+
+typedef struct orca_slab_header {
+    int32_t count;    /* records the sender produced (may exceed the capacity: then `overflow`) */
+    int32_t overflow; /* the sender could not fit a record */
+    int64_t reserved[3];
+} orca_slab_header; /* 32 bytes */
+
+typedef struct orca_halo_record_f32 {
+    float x, y, vx, vy;
+    float radius;
+    uint32_t class_code;
+    int64_t id;
+} orca_halo_record_f32; /* 32 bytes */
+
+typedef struct orca_halo_record_f64 {
+    double x, y, vx, vy;
+    double radius;
+    int64_t id;
+    int64_t class_code;
+    int64_t pad;
+} orca_halo_record_f64; /* 64 bytes */
+
+/* sizeof the halo record this handle's precision uses (32 or 64). */
+ORCA_API int64_t orca_strip_halo_record_bytes(const orca_sim *sim);
+
+/* This handle owns x in [x_lo, x_hi) (+-inf at the ends of the domain). vmax_floor:
+ * the largest max_speed of the WHOLE crowd (ghosts travel without theirs; the
+ * neighbour search's displacement bound needs it). */
+ORCA_API int orca_strip_configure(orca_sim *sim, double x_lo, double x_hi, double vmax_floor);
+
+/* Owned rows with x < x_lo + reach -> left slab, x >= x_hi - reach -> right slab
+ * (either may be NULL: no neighbour on that side). cap = records per slab. */
+ORCA_API int orca_strip_pack_halo(orca_sim *sim, double reach, void *slab_left, void *slab_right,
+                                  int64_t cap);
+
+/* Append the records of a received slab: ghost != 0 -> halo records as ghost rows,
+ * ghost == 0 -> orca_agent_record as owned rows (not while ghosts are resident). */
+ORCA_API int orca_strip_append_slab(orca_sim *sim, const void *slab, int64_t cap, int ghost);
+
+/* orca_step for a strip: the step, then ONE compaction that drops the ghosts, the
+ * arrivals (if remove_arrivals) and the owned rows whose new x left [x_lo, x_hi) --
+ * those are written to the migrant slabs (NULL = no neighbour on that side) as
+ * orca_agent_record. */
+ORCA_API int orca_strip_step(orca_sim *sim, void *migrants_left, void *migrants_right, int64_t cap);
+
+/* Rows appended from slabs since the last orca_upload: ghosts, migrants (for
+ * benchmarks). Synchronises. */
+ORCA_API int orca_strip_stats(orca_sim *sim, int64_t *ghost_rows, int64_t *migrant_rows);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,12 +34,23 @@ SYMBOLS = [
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
     "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
     "orca_strip_pack", "orca_strip_append", "orca_strip_drop_ghosts",
+    "orca_strip_halo_record_bytes", "orca_strip_configure", "orca_strip_pack_halo",
+    "orca_strip_append_slab", "orca_strip_step", "orca_strip_stats",
 ]
 
 RECORD_BYTES = 96   # sizeof(orca_agent_record)
 RECORD_DTYPE = np.dtype([("x", "f8"), ("y", "f8"), ("vx", "f8"), ("vy", "f8"), ("radius", "f8"),
                          ("pref_speed", "f8"), ("max_speed", "f8"), ("goal_tol", "f8"),
                          ("goal_x", "f8"), ("goal_y", "f8"), ("id", "i8"), ("class_code", "i8")])
+
+
+# slabs of the device-side exchange protocol (orca_slab_header + records)
+SLAB_HEADER_BYTES = 32
+SLAB_HEADER_DTYPE = np.dtype([("count", "i4"), ("overflow", "i4"), ("reserved", "i8", (3,))])
+HALO_DTYPE_F32 = np.dtype([("x", "f4"), ("y", "f4"), ("vx", "f4"), ("vy", "f4"), ("radius", "f4"),
+                           ("class_code", "u4"), ("id", "i8")])                      # 32 bytes
+HALO_DTYPE_F64 = np.dtype([("x", "f8"), ("y", "f8"), ("vx", "f8"), ("vy", "f8"), ("radius", "f8"),
+                           ("id", "i8"), ("class_code", "i8"), ("pad", "i8")])       # 64 bytes
 
 
 class OrcaError(RuntimeError):
@@ -117,9 +128,17 @@ def load():
     L.orca_strip_pack.argtypes = [vp, f64, f64, ci, vp, i64, P(i64)]
     L.orca_strip_append.argtypes = [vp, vp, i64, ci]
     L.orca_strip_drop_ghosts.argtypes = [vp]
+    L.orca_strip_halo_record_bytes.argtypes = [vp]
+    L.orca_strip_configure.argtypes = [vp, f64, f64, f64]
+    L.orca_strip_pack_halo.argtypes = [vp, f64, vp, vp, i64]
+    L.orca_strip_append_slab.argtypes = [vp, vp, i64, ci]
+    L.orca_strip_step.argtypes = [vp, vp, vp, i64]
+    L.orca_strip_stats.argtypes = [vp, P(i64), P(i64)]
     for name in SYMBOLS:
         fn = getattr(L, name)
-        if name not in ("orca_destroy", "orca_last_error", "orca_lp_batch_destroy"):
+        if name == "orca_strip_halo_record_bytes":
+            fn.restype = i64
+        elif name not in ("orca_destroy", "orca_last_error", "orca_lp_batch_destroy"):
             fn.restype = ci
     _lib = L
     return L

@@ -56,7 +56,12 @@ struct orca_sim {
     u8 *arrived = nullptr;
     int *keep = nullptr, *dst_idx = nullptr;
     int *sel = nullptr, *sel_idx = nullptr; // strip selection flags and their scan
-    int64_t ghost_bound = 0;                // ghost rows currently appended
+    int64_t ghost_bound = 0;                // ghost rows currently appended (upper bound)
+    // strip decomposition without host round trips (orca_strip_configure / _step)
+    bool strip_on = false;
+    double strip_lo = -INFINITY, strip_hi = INFINITY;
+    void *mig_slab[2] = {nullptr, nullptr}; // migrant slabs of the running orca_strip_step
+    int64_t mig_cap = 0;
 
     // per-step scratch
     int max_cells = 0;
@@ -494,6 +499,7 @@ static int reset_plan(orca_sim *sim, int64_t n, int64_t frame)
     h.n = (int)n;
     h.n_owned = (int)n;
     h.n_after = (int)n;
+    h.n_pre = (int)n;
     h.err_pair = ORCA_NO_ERR;
     h.err_frame = -1;
     h.frame = frame;
@@ -531,6 +537,7 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->reorder_due = sim->reorder_every > 0;
     sim->since_reorder = 0;
     sim->apre = 0;
+    sim->drop_graphs(); // captured compactions assume the row-order state they were recorded in
     if (n > 0) {
         k_iota<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->lrow[0]);
         CK(sim, cudaMemcpyAsync(sim->ids[0], ids, sizeof(i64) * n, cudaMemcpyHostToDevice, sim->stream));
@@ -581,6 +588,9 @@ static int fetch_plan(orca_sim *sim)
     const GridPlan &h = *sim->h_plan;
     sim->n_bound = h.n;
     if (h.err_range) return fail(sim, ORCA_ERANGE, "agent position out of indexable grid range");
+    if (h.err_capacity)
+        return fail(sim, ORCA_ECAPACITY, "strip exchange: a slab or the handle capacity (%lld rows) overflowed",
+                    (long long)sim->capacity);
     if (h.err_pair != ORCA_NO_ERR)
         return fail(sim, ORCA_ECOINCIDENT,
                     "frame %lld: agents %lld and %lld have exactly coincident centers; "
@@ -686,11 +696,13 @@ extern "C" int orca_download(orca_sim *sim, int64_t *ids, double *positions, dou
 extern "C" int orca_download_last_step_pv(orca_sim *sim, int64_t n, double *positions, double *velocities)
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_download_last_step_pv: no resident state");
+    int rc = fetch_plan(sim);
+    if (rc) return rc;
+    // (the device knows how many rows the last step had even after graph replays with removal)
+    if (sim->frame > 0 || sim->h_plan->n_pre > 0) sim->n_pre = sim->h_plan->n_pre;
     if (n != sim->n_pre)
         return fail(sim, ORCA_EINVAL, "orca_download_last_step_pv: n = %lld, last step had %lld rows",
                     (long long)n, (long long)sim->n_pre);
-    int rc = fetch_plan(sim);
-    if (rc) return rc;
     if (n == 0) return ORCA_OK;
     // the step wrote pv[(pre+1)%3]; arrival removal compacts into a third buffer and leaves it intact
     const int keep_cur = sim->cur;
@@ -922,7 +934,17 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
     const int a = sim->acur, b = 1 - a;
     if (from_sel)
         k_keep_unselected<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->sel, sim->keep);
-    else
+    else if (sim->mig_cap > 0) {
+        // strip step: rows whose new x left the strip go to the migrant slabs and are dropped
+        orca_slab_header *hl = reinterpret_cast<orca_slab_header *>(sim->mig_slab[0]);
+        orca_slab_header *hr = reinterpret_cast<orca_slab_header *>(sim->mig_slab[1]);
+        k_strip_keep_flags<R><<<grid_for(n + 1, 256), 256, 0, st>>>(
+            sim->plan, sim->arrived, sim->keep, sim->params.remove_arrivals,
+            reinterpret_cast<const R4 *>(sim->pv[src_idx]), reinterpret_cast<const R4 *>(sim->goalpref[a]),
+            reinterpret_cast<const R2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->strip_lo, sim->strip_hi,
+            hl, hl ? reinterpret_cast<orca_agent_record *>(hl + 1) : nullptr, hr,
+            hr ? reinterpret_cast<orca_agent_record *>(hr + 1) : nullptr, (int)sim->mig_cap);
+    } else
         k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
                                                            sim->params.remove_arrivals);
     const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
@@ -1033,7 +1055,7 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     sim->pre = sim->cur;
     sim->apre = sim->acur;
     if (sim->reorder_every > 0 && ++sim->since_reorder >= sim->reorder_every) sim->reorder_due = true;
-    if (sim->params.remove_arrivals || sim->ghost_bound > 0) {
+    if (sim->params.remove_arrivals || sim->ghost_bound > 0 || sim->mig_cap > 0) {
         const int dst = (sim->cur + 2) % 3;
         rc = compact_stage<S>(sim, out_idx, dst);
         if (rc) return rc;
@@ -1179,6 +1201,7 @@ extern "C" int orca_reorder_rows(orca_sim *sim)
     if (sim->n_bound < 2) return ORCA_OK;
     const StepParams P = make_params(sim);
     int rc;
+    if (!sim->rows_permuted) sim->drop_graphs(); // graphs captured with identity row order are stale now
     switch (sim->precision) {
     case ORCA_F32: rc = reorder_rows<float, float>(sim, P); break;
     case ORCA_MIXED: rc = reorder_rows<float, double>(sim, P); break;
@@ -1420,6 +1443,139 @@ extern "C" int orca_strip_drop_ghosts(orca_sim *sim)
     sim->ghost_bound = 0;
     sim->binned_frame = -1;
     return ORCA_OK;
+}
+
+// ---- the protocol with the counts kept on the device (see include/orca_b200.h) ----------
+
+extern "C" int64_t orca_strip_halo_record_bytes(const orca_sim *sim)
+{
+    return sim && sim->precision == ORCA_F64 ? (int64_t)sizeof(orca_halo_record_f64)
+                                             : (int64_t)sizeof(orca_halo_record_f32);
+}
+
+extern "C" int orca_strip_configure(orca_sim *sim, double x_lo, double x_hi, double vmax_floor)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_strip_configure: sim is NULL");
+    if (!(x_lo < x_hi)) return fail(sim, ORCA_EINVAL, "orca_strip_configure: empty strip [%g, %g)", x_lo, x_hi);
+    if (!(vmax_floor >= 0.0) || !std::isfinite(vmax_floor))
+        return fail(sim, ORCA_EINVAL, "orca_strip_configure: vmax_floor = %g", vmax_floor);
+    CK(sim, cudaSetDevice(sim->device));
+    sim->strip_on = true;
+    sim->strip_lo = x_lo;
+    sim->strip_hi = x_hi;
+    k_strip_configure<<<1, 1, 0, sim->stream>>>(sim->plan, vmax_floor);
+    CKL(sim);
+    sim->launches += 1;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_pack_halo(orca_sim *sim, double reach, void *slab_left, void *slab_right, int64_t cap)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: no resident state");
+    if (!sim->strip_on) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: orca_strip_configure was not called");
+    if (cap < 0 || cap > 0x7FFFFFFF || !(reach >= 0.0)) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: bad arguments");
+    if (sim->ghost_bound > 0) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: ghost rows are resident");
+    CK(sim, cudaSetDevice(sim->device));
+    cudaStream_t st = sim->stream;
+    orca_slab_header *hl = reinterpret_cast<orca_slab_header *>(slab_left);
+    orca_slab_header *hr = reinterpret_cast<orca_slab_header *>(slab_right);
+    if (hl) CK(sim, cudaMemsetAsync(hl, 0, sizeof(orca_slab_header), st));
+    if (hr) CK(sim, cudaMemsetAsync(hr, 0, sizeof(orca_slab_header), st));
+    if (!hl && !hr) return ORCA_OK;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur;
+    const double le = sim->strip_lo + reach, re = sim->strip_hi - reach;
+    if (sim->precision == ORCA_F64)
+        k_strip_pack_halo<double><<<grid_for(n, 256), 256, 0, st>>>(
+            sim->plan, reinterpret_cast<const double4 *>(sim->pv[sim->cur]),
+            reinterpret_cast<const double2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], le, re, hl,
+            hl ? reinterpret_cast<HaloRec<double> *>(hl + 1) : nullptr, hr,
+            hr ? reinterpret_cast<HaloRec<double> *>(hr + 1) : nullptr, (int)cap);
+    else
+        k_strip_pack_halo<float><<<grid_for(n, 256), 256, 0, st>>>(
+            sim->plan, reinterpret_cast<const float4 *>(sim->pv[sim->cur]),
+            reinterpret_cast<const float2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], le, re, hl,
+            hl ? reinterpret_cast<HaloRec<float> *>(hl + 1) : nullptr, hr,
+            hr ? reinterpret_cast<HaloRec<float> *>(hr + 1) : nullptr, (int)cap);
+    CKL(sim);
+    sim->launches += 1;
+    return ORCA_OK;
+}
+
+template <typename S> static int strip_append_slab_impl(orca_sim *sim, const void *slab, int64_t cap, int ghost)
+{
+    typedef typename Vec<S>::T4 S4;
+    typedef typename Vec<S>::T2 S2;
+    const int a = sim->acur;
+    const orca_slab_header *hdr = reinterpret_cast<const orca_slab_header *>(slab);
+    cudaStream_t st = sim->stream;
+    if (ghost)
+        k_strip_append_halo<S><<<grid_for(cap, 256), 256, 0, st>>>(
+            sim->plan, hdr, reinterpret_cast<const HaloRec<S> *>(hdr + 1), (int)cap, (int)sim->capacity,
+            reinterpret_cast<S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->goalpref[a]),
+            reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->status[a], sim->failed[a],
+            sim->hint[a], sim->lrow[a]);
+    else
+        k_strip_append_slab<S><<<grid_for(cap, 256), 256, 0, st>>>(
+            sim->plan, hdr, reinterpret_cast<const orca_agent_record *>(hdr + 1), (int)cap, (int)sim->capacity,
+            reinterpret_cast<S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->goalpref[a]),
+            reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->status[a], sim->failed[a],
+            sim->hint[a], sim->lrow[a]);
+    k_after_append_slab<<<1, 1, 0, st>>>(sim->plan, hdr, (int)cap, (int)sim->capacity, ghost);
+    CKL(sim);
+    sim->launches += 2;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_append_slab(orca_sim *sim, const void *slab, int64_t cap, int ghost)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: no resident state");
+    if (!slab || cap < 0 || cap > 0x7FFFFFFF) return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: bad arguments");
+    if (!ghost && sim->ghost_bound > 0)
+        return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: owned rows cannot follow ghost rows");
+    if (cap == 0) return ORCA_OK;
+    CK(sim, cudaSetDevice(sim->device));
+    int rc = sim->precision == ORCA_F64 ? strip_append_slab_impl<double>(sim, slab, cap, ghost)
+                                        : strip_append_slab_impl<float>(sim, slab, cap, ghost);
+    if (rc) return rc;
+    // the host does not know the count: its row bound grows by the slab capacity (the device
+    // clamps at the handle capacity and raises the sticky overflow flag beyond it)
+    const int64_t grown = std::min<int64_t>(sim->capacity, sim->n_bound + cap);
+    if (ghost) sim->ghost_bound += grown - sim->n_bound;
+    sim->n_bound = grown;
+    sim->binned_frame = -1;
+    sim->bbox_frame = -1; // rows appended from outside
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_step(orca_sim *sim, void *migrants_left, void *migrants_right, int64_t cap)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_step: no resident state");
+    if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_strip_step: orca_set_params was not called");
+    if (!sim->strip_on) return fail(sim, ORCA_EINVAL, "orca_strip_step: orca_strip_configure was not called");
+    if (cap < 1 || cap > 0x7FFFFFFF) return fail(sim, ORCA_EINVAL, "orca_strip_step: slab capacity %lld", (long long)cap);
+    if (sim->params.compute_metrics)
+        return fail(sim, ORCA_EUNSUPPORTED, "orca_strip_step: frame metrics are per handle and would miss the "
+                                            "pairs that straddle strips; set compute_metrics = 0");
+    CK(sim, cudaSetDevice(sim->device));
+    if (migrants_left) CK(sim, cudaMemsetAsync(migrants_left, 0, sizeof(orca_slab_header), sim->stream));
+    if (migrants_right) CK(sim, cudaMemsetAsync(migrants_right, 0, sizeof(orca_slab_header), sim->stream));
+    sim->mig_slab[0] = migrants_left;
+    sim->mig_slab[1] = migrants_right;
+    sim->mig_cap = cap;
+    const int rc = step_plain(sim);
+    sim->mig_slab[0] = sim->mig_slab[1] = nullptr;
+    sim->mig_cap = 0;
+    return rc;
+}
+
+extern "C" int orca_strip_stats(orca_sim *sim, int64_t *ghost_rows, int64_t *migrant_rows)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_strip_stats: sim is NULL");
+    const int rc = fetch_plan(sim);
+    if (ghost_rows) *ghost_rows = (int64_t)sim->h_plan->strip_recv[0];
+    if (migrant_rows) *migrant_rows = (int64_t)sim->h_plan->strip_recv[1];
+    return rc;
 }
 
 // ---------------------------------------------------------------------------

@@ -28,6 +28,7 @@ struct GridPlan {
     // population
     int n;       // rows in the state arrays (owned + ghost)
     int n_owned; // rows [0, n_owned) are solved and integrated; the rest are halo ghosts
+    int n_pre;   // n_owned at the start of the last step (rows of the un-compacted result)
     // search grid (rebuilt every step from the bounding box)
     int nx, ny, ncells, rmax, r0;
     double x0, y0, cell, inv_cell;
@@ -42,6 +43,8 @@ struct GridPlan {
     i64 err_frame;  // frame_new of that step
     i64 err_id_i, err_id_j;
     int err_range;  // a position left the reference's indexable grid range
+    int err_capacity; // a strip-exchange slab (or the handle) overflowed: rows were dropped or kept back
+    unsigned long long strip_recv[2]; // ghost rows / migrant rows appended from slabs since the upload
     // per-step counters
     int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
     int gq_count[ORCA_MAX_CHUNKS]; // agents queued for the exact ring search (k_gather), per chunk

@@ -78,6 +78,7 @@ namespace orca {
 __global__ void k_begin_step(GridPlan *plan)
 {
     plan->fq_count = 0;
+    plan->n_pre = plan->n_owned;
     for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) plan->gq_count[c] = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
@@ -1871,6 +1872,192 @@ __global__ void k_after_append(GridPlan *plan, int count, int ghost)
 }
 
 __global__ void k_drop_ghosts(GridPlan *plan) { plan->n = plan->n_owned; }
+
+// ---- device-side exchange protocol (no host round trip per frame) -------------------
+//
+// A slab is a fixed-capacity device buffer: an orca_slab_header (32 B) followed by `cap`
+// records. The sender's kernels count into the header with atomics, the whole slab travels
+// (NCCL send/recv of a size both sides know without asking), and the receiver's append
+// kernel reads the count from the header. The host only keeps upper bounds (orca_api.cu).
+
+// What a ghost needs: the pre-step snapshot a neighbour reads (NbRec) plus the id that
+// breaks distance ties (K:473-476). 32 B with FP32 state, 64 B with FP64 state.
+template <typename S> struct HaloRec;
+template <> struct __align__(16) HaloRec<float> {
+    float x, y, vx, vy;
+    float radius;
+    unsigned cls;
+    i64 id;
+};
+template <> struct __align__(16) HaloRec<double> {
+    double x, y, vx, vy;
+    double radius;
+    i64 id;
+    i64 cls;
+    i64 pad;
+};
+static_assert(sizeof(HaloRec<float>) == 32 && sizeof(HaloRec<double>) == 64, "halo record layout");
+
+__global__ void k_strip_configure(GridPlan *plan, double vmax_floor)
+{
+    // ghosts travel without their max_speed: the fast gather's displacement bound
+    // (hint + (own + fastest max_speed) * dt) must cover the fastest agent of ANY strip
+    atomicMax(&plan->vmax_enc, enc_double(vmax_floor));
+}
+
+// Owned agents within `reach` of a strip edge -> that side's halo slab (either may be null).
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_pack_halo(const GridPlan *__restrict__ plan, const typename Vec<S>::T4 *__restrict__ pv,
+                  const typename Vec<S>::T2 *__restrict__ radmax, const i64 *__restrict__ ids,
+                  const u8 *__restrict__ cls, double left_edge, double right_edge,
+                  orca_slab_header *hdr_l, HaloRec<S> *__restrict__ rec_l, orca_slab_header *hdr_r,
+                  HaloRec<S> *__restrict__ rec_r, int cap)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= plan->n_owned) return;
+    const typename Vec<S>::T4 a = pv[i];
+    const double x = (double)a.x;
+    const bool to_l = hdr_l && x < left_edge, to_r = hdr_r && x >= right_edge;
+    if (!to_l && !to_r) return;
+    HaloRec<S> r;
+    r.x = a.x;
+    r.y = a.y;
+    r.vx = a.z;
+    r.vy = a.w;
+    r.radius = radmax[i].x;
+    r.cls = cls[i];
+    r.id = ids[i];
+    if (to_l) {
+        const int slot = atomicAdd(&hdr_l->count, 1);
+        if (slot < cap) rec_l[slot] = r;
+    }
+    if (to_r) {
+        const int slot = atomicAdd(&hdr_r->count, 1);
+        if (slot < cap) rec_r[slot] = r;
+    }
+}
+
+// Ghost rows from a halo slab, appended after the resident rows. cap_rows = handle capacity.
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_append_halo(GridPlan *__restrict__ plan, const orca_slab_header *__restrict__ hdr,
+                    const HaloRec<S> *__restrict__ rec, int cap, int cap_rows,
+                    typename Vec<S>::T4 *__restrict__ pv, typename Vec<S>::T4 *__restrict__ goalpref,
+                    typename Vec<S>::T2 *__restrict__ radmax, i64 *__restrict__ ids, u8 *__restrict__ cls,
+                    i8 *__restrict__ status, i8 *__restrict__ failed, float *__restrict__ hint,
+                    int *__restrict__ lrow)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int count = min(min(hdr->count, cap), cap_rows - plan->n);
+    if (i >= count) return;
+    const int row = plan->n + i;
+    const HaloRec<S> r = rec[i];
+    lrow[row] = row;
+    pv[row] = mk4(r.x, r.y, r.vx, r.vy);
+    goalpref[row] = mk4(r.x, r.y, S(0), S(0)); // a ghost is never steered: goal = where it stands
+    radmax[row] = mk2(r.radius, S(0));         // (its max_speed is covered by the strip-wide vmax floor)
+    ids[row] = r.id;
+    cls[row] = (u8)r.cls;
+    status[row] = 0;
+    failed[row] = -1;
+    hint[row] = __int_as_float(0x7F800000);
+    atomicMax(&plan->rmax_enc, enc_double((double)r.radius));
+}
+
+// Owned rows from a migrant slab (orca_agent_record), count taken from the slab header.
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_append_slab(GridPlan *__restrict__ plan, const orca_slab_header *__restrict__ hdr,
+                    const orca_agent_record *__restrict__ rec, int cap, int cap_rows,
+                    typename Vec<S>::T4 *__restrict__ pv, typename Vec<S>::T4 *__restrict__ goalpref,
+                    typename Vec<S>::T2 *__restrict__ radmax, i64 *__restrict__ ids, u8 *__restrict__ cls,
+                    i8 *__restrict__ status, i8 *__restrict__ failed, float *__restrict__ hint,
+                    int *__restrict__ lrow)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int count = min(min(hdr->count, cap), cap_rows - plan->n);
+    if (i >= count) return;
+    const int row = plan->n + i;
+    lrow[row] = row;
+    const orca_agent_record r = rec[i];
+    pv[row] = mk4((S)r.x, (S)r.y, (S)r.vx, (S)r.vy);
+    goalpref[row] = mk4((S)r.goal_x, (S)r.goal_y, (S)r.pref_speed, (S)r.goal_tol);
+    radmax[row] = mk2((S)r.radius, (S)r.max_speed);
+    ids[row] = r.id;
+    cls[row] = (u8)r.class_code;
+    status[row] = 0;
+    failed[row] = -1;
+    hint[row] = __int_as_float(0x7F800000);
+    atomicMax(&plan->vmax_enc, enc_double(r.max_speed));
+    atomicMax(&plan->rmax_enc, enc_double(r.radius));
+}
+
+// after either append: the row counts, and the sticky overflow flag when the sender produced
+// more records than the slab (or this handle) holds
+__global__ void k_after_append_slab(GridPlan *plan, const orca_slab_header *__restrict__ hdr, int cap,
+                                    int cap_rows, int ghost)
+{
+    const int want = hdr->count;
+    const int count = min(min(want, cap), cap_rows - plan->n);
+    if (count < want || hdr->overflow) plan->err_capacity = 1;
+    plan->n += count;
+    if (!ghost) plan->n_owned += count;
+    plan->n_after = plan->n_owned;
+    plan->strip_recv[ghost ? 0 : 1] += (unsigned long long)count;
+}
+
+// keep flags of the strip step: owned rows that have not arrived AND whose new x is still
+// inside [lo, hi); the ones that left go into the migrant slab of that side as full records
+// and are removed by the compaction that follows (ghosts are always dropped). A row that does
+// not fit its slab stays (and raises the sticky overflow flag on both sides of the exchange).
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_strip_keep_flags(GridPlan *__restrict__ plan, const u8 *__restrict__ arrived, int *__restrict__ keep,
+                   int remove_arrivals, const typename Vec<S>::T4 *__restrict__ pv_new,
+                   const typename Vec<S>::T4 *__restrict__ goalpref,
+                   const typename Vec<S>::T2 *__restrict__ radmax, const i64 *__restrict__ ids,
+                   const u8 *__restrict__ cls, double lo, double hi, orca_slab_header *hdr_l,
+                   orca_agent_record *__restrict__ rec_l, orca_slab_header *hdr_r,
+                   orca_agent_record *__restrict__ rec_r, int cap)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = plan->n;
+    if (i > n) return;
+    int k = 0;
+    if (i < plan->n_owned && !(remove_arrivals && arrived[i])) {
+        const typename Vec<S>::T4 a = pv_new[i];
+        const double x = (double)a.x;
+        orca_slab_header *hdr = x < lo ? hdr_l : (x >= hi ? hdr_r : nullptr);
+        k = 1;
+        if (hdr) {
+            const int slot = atomicAdd(&hdr->count, 1);
+            if (slot < cap) {
+                const typename Vec<S>::T4 g = goalpref[i];
+                const typename Vec<S>::T2 rm = radmax[i];
+                orca_agent_record r;
+                r.x = (double)a.x;
+                r.y = (double)a.y;
+                r.vx = (double)a.z;
+                r.vy = (double)a.w;
+                r.radius = (double)rm.x;
+                r.pref_speed = (double)g.z;
+                r.max_speed = (double)rm.y;
+                r.goal_tol = (double)g.w;
+                r.goal_x = (double)g.x;
+                r.goal_y = (double)g.y;
+                r.id = ids[i];
+                r.class_code = (i64)cls[i];
+                (x < lo ? rec_l : rec_r)[slot] = r;
+                k = 0;
+            } else {
+                hdr->overflow = 1;
+                plan->err_capacity = 1;
+            }
+        }
+    }
+    keep[i] = k;
+}
 
 __global__ void k_set_frame(GridPlan *plan, i64 frame) { plan->frame = frame; }
 

@@ -8,21 +8,34 @@ only on the pre-step snapshot of the agents within neighbor_radius, so a rank th
 sees its owned agents plus every foreign agent within neighbor_radius of its strip
 computes exactly what a single device would. Per step and per rank:
 
-  1. halo     pack owned agents with x in [lo, lo+nr] / [hi-nr, hi)   (C ABI:
-              orca_strip_pack) and send them left / right; append what arrives
-              as ghosts (orca_strip_append, ghost=1)
-  2. step     orca_step solves owned agents only and drops the ghosts
-  3. migrate  pack-and-remove owned agents whose new x left [lo, hi), send,
-              append arrivals as owned rows
+  1. halo     owned agents within neighbor_radius of a strip edge are packed
+              into that side's HALO SLAB (orca_strip_pack_halo: 32-byte records --
+              position, velocity, radius, class, id); the slabs are swapped with
+              the two adjacent strips; what arrives is appended as ghost rows
+              (orca_strip_append_slab, ghost=1)
+  2. step     orca_strip_step solves the owned agents, then ONE compaction drops
+              the ghosts, the arrivals and the owned agents whose new x left the
+              strip -- those go into the MIGRANT SLABS as full 96-byte records
+  3. migrate  the migrant slabs are swapped and appended as owned rows
 
-The exchange is point-to-point with the two adjacent strips only (counts first,
-then the 96-byte records as raw bytes); there is no collective on the data path.
+The host is not in this loop. A slab is a fixed-capacity device buffer whose
+32-byte header carries the record count; the packing kernels count with atomics,
+the whole slab travels (a size both ranks know without asking), the appending
+kernels read the count from the header. Each exchange is one grouped NCCL
+send/recv with the two adjacent strips (no collective on the data path) ordered
+against the handle's stream on the device. The host only keeps an upper bound on
+its row count and re-synchronises every `resync_every` frames (default 16), which
+is also when a slab overflow -- a sticky device-side flag -- surfaces as an error.
+
 `StripDriver` holds this protocol and is written against a small ops interface so
 the same code runs on NCCL with the CUDA handle (DeviceStripOps) and, in the CPU
 tests, on gloo with a host-side stand-in (tests/strip_ops_cpu.py).
 
-Constraint: a strip must be wider than neighbor_radius + max_speed*dt (an agent
-may cross at most one boundary per step, and a halo reaches one strip deep).
+Constraint, checked at construction: every interior strip must be at least
+neighbor_radius + max_speed*dt wide (a halo reaches one strip deep, and an agent
+may cross at most one boundary per step). Frame metrics (min separation,
+collisions) are per handle and would miss pairs that straddle strips:
+compute_metrics is not supported under strips (orca_strip_step refuses it).
 """
 
 from __future__ import annotations
@@ -30,48 +43,111 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
+import os
 import time
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
-from .._lib import RECORD_BYTES, check, load
+from .._lib import RECORD_BYTES, SLAB_HEADER_BYTES, check, load
 
-__all__ = ["DeviceStripOps", "StripDriver", "strip_bounds", "run_bench"]
+__all__ = ["DeviceStripOps", "StripDriver", "strip_bounds", "check_strip_widths", "state_hash",
+           "run_bench"]
 
 
-def strip_bounds(x: np.ndarray, world: int) -> np.ndarray:
+def strip_bounds(x: np.ndarray, world: int, min_width: float = 0.0) -> np.ndarray:
     """Interior strip boundaries (world-1 values) that split the agents evenly:
     quantiles of the x coordinates. Strip r owns x in [b[r-1], b[r]) with
-    b[-1] = -inf and b[world-1] = +inf."""
+    b[-1] = -inf and b[world-1] = +inf. With min_width > 0 the boundaries are
+    validated (see check_strip_widths)."""
     if world <= 1:
         return np.zeros(0)
     qs = np.arange(1, world) / world
-    return np.quantile(np.asarray(x, dtype=np.float64), qs)
+    b = np.quantile(np.asarray(x, dtype=np.float64), qs)
+    if min_width > 0.0:
+        check_strip_widths(b, min_width)
+    return b
+
+
+def check_strip_widths(bounds, min_width: float):
+    """Raise ValueError if an interior strip is narrower than min_width
+    (= neighbor_radius + max_speed*dt): its halo would have to reach two strips
+    deep and an agent could cross two boundaries in one step -- the results would
+    silently differ from a single device."""
+    b = np.asarray(bounds, dtype=np.float64)
+    if b.size and np.any(np.diff(b) < 0):
+        raise ValueError(f"strip boundaries must be non-decreasing, got {b.tolist()}")
+    w = np.diff(b)
+    if w.size and float(w.min()) < min_width:
+        k = int(np.argmin(w))
+        raise ValueError(f"strip {k + 1} is {float(w[k]):.6g} m wide; strips must be at least "
+                         f"neighbor_radius + max_speed*dt = {min_width:.6g} m wide "
+                         "(use fewer strips for a crowd this clustered)")
+
+
+_MIX = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _mix64(z: np.ndarray) -> np.ndarray:
+    z = z.astype(np.uint64, copy=True)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def state_hash(ids, positions, velocities) -> int:
+    """Order-independent 64-bit digest of {id: (position bits, velocity bits)}: the sum
+    (mod 2^64) of a per-agent mix. Equal for a strip-decomposed crowd and the single-device
+    run exactly when every agent's position and velocity agree bit for bit, whatever the
+    row order and whichever rank holds the agent (per-rank digests add up)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64).view(np.uint64)
+    p = np.ascontiguousarray(positions, dtype=np.float64).view(np.uint64).reshape(-1, 2)
+    v = np.ascontiguousarray(velocities, dtype=np.float64).view(np.uint64).reshape(-1, 2)
+    with np.errstate(over="ignore"):
+        h = _mix64(ids * _MIX + np.uint64(1))
+        for col in (p[:, 0], p[:, 1], v[:, 0], v[:, 1]):
+            h = _mix64(h ^ (col + _MIX))
+        return int(h.sum(dtype=np.uint64))
 
 
 class DeviceStripOps:
-    """pack / append on a Simulation's resident state through the C ABI."""
+    """The slab protocol on a Simulation's resident state through the C ABI."""
 
     def __init__(self, sim):
         self.sim = sim
         self._L = load()
+        self.halo_record_bytes = int(self._L.orca_strip_halo_record_bytes(sim._h))
 
-    def pack(self, x_lo: float, x_hi: float, remove: bool, buf: torch.Tensor) -> int:
-        count = C.c_int64()
-        cap = buf.numel() // RECORD_BYTES
-        check(self._L.orca_strip_pack(self.sim._h, float(x_lo), float(x_hi), 1 if remove else 0,
-                                      C.c_void_p(buf.data_ptr()), cap, C.byref(count)), self.sim._h)
-        return int(count.value)
+    def configure(self, x_lo: float, x_hi: float, vmax_floor: float):
+        check(self._L.orca_strip_configure(self.sim._h, float(x_lo), float(x_hi), float(vmax_floor)),
+              self.sim._h)
 
-    def append(self, buf: torch.Tensor, count: int, ghost: bool):
-        if count:
-            check(self._L.orca_strip_append(self.sim._h, C.c_void_p(buf.data_ptr()), int(count),
-                                            1 if ghost else 0), self.sim._h)
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr()) if t is not None else None
 
-    def step(self):
-        self.sim.step()
+    def pack_halo(self, reach: float, slab_left, slab_right, cap: int):
+        check(self._L.orca_strip_pack_halo(self.sim._h, float(reach), self._p(slab_left),
+                                           self._p(slab_right), int(cap)), self.sim._h)
+
+    def append_slab(self, slab, cap: int, ghost: bool):
+        check(self._L.orca_strip_append_slab(self.sim._h, self._p(slab), int(cap), 1 if ghost else 0),
+              self.sim._h)
+
+    def step(self, mig_left, mig_right, cap: int):
+        check(self._L.orca_strip_step(self.sim._h, self._p(mig_left), self._p(mig_right), int(cap)),
+              self.sim._h)
+
+    def resync(self):
+        """The one host synchronisation: tightens the host's row bound and raises if a
+        slab or the handle overflowed (or on the reference's own errors)."""
+        self.sim.sync()
+
+    def stats(self):
+        g, m = C.c_int64(), C.c_int64()
+        check(self._L.orca_strip_stats(self.sim._h, C.byref(g), C.byref(m)), self.sim._h)
+        return int(g.value), int(m.value)
 
     def reorder(self):
         self.sim.reorder_rows()
@@ -80,173 +156,301 @@ class DeviceStripOps:
 class StripDriver:
     """One rank's side of the strip protocol."""
 
+    SIDES = ("left", "right")
+
     def __init__(self, ops, rank: int, world: int, bounds, neighbor_radius: float, device,
-                 halo_capacity: int, group=None):
+                 halo_capacity: int, migrant_capacity: int | None = None, group=None,
+                 vmax: float = 0.0, dt: float = 0.0, resync_every: int = 16):
         self.ops, self.rank, self.world, self.group = ops, rank, world, group
         b = [-math.inf] + [float(v) for v in bounds] + [math.inf]
-        assert len(b) == world + 1 and all(b[i] <= b[i + 1] for i in range(world))
-        self.lo, self.hi = b[rank], b[rank + 1]
-        self.left = rank - 1 if rank > 0 else None
-        self.right = rank + 1 if rank < world - 1 else None
+        if len(b) != world + 1:
+            raise ValueError(f"{world} strips need {world - 1} interior boundaries, got {len(b) - 2}")
         # halo reach with a relative margin: including a few extra agents is harmless,
         # missing one that sits exactly at distance neighbor_radius is not
         self.reach = float(neighbor_radius) * (1.0 + 1e-9) + 1e-9
-        self.device = device
-        nbytes = int(halo_capacity) * RECORD_BYTES
-        mk = lambda: torch.empty(nbytes, dtype=torch.uint8, device=device)  # noqa: E731
-        self.send = {"left": mk(), "right": mk()}
-        self.recv = {"left": mk(), "right": mk()}
-        self.capacity = int(halo_capacity)
-        self.stats = {"halo_sent": 0, "halo_recv": 0, "migr_sent": 0, "migr_recv": 0}
-        self.frames = 0
-        self.reorder_every = 64      # frames between row reorderings (no ghosts resident then)
+        check_strip_widths(b[1:-1], self.reach + float(vmax) * float(dt))
+        self.lo, self.hi = b[rank], b[rank + 1]
+        self.peer = {"left": rank - 1 if rank > 0 else None,
+                     "right": rank + 1 if rank < world - 1 else None}
+        self.device = torch.device(device)
+        self.halo_cap = int(halo_capacity)
+        self.mig_cap = int(migrant_capacity if migrant_capacity is not None else halo_capacity)
+        hb = SLAB_HEADER_BYTES + self.halo_cap * int(ops.halo_record_bytes)
+        mb = SLAB_HEADER_BYTES + self.mig_cap * RECORD_BYTES
 
-    # -- one exchange with both neighbours --------------------------------------
-    def _swap(self, counts: dict) -> dict:
-        """Send self.send[side][:counts[side]] to that side, receive into self.recv.
-        Returns the received counts. Counts travel first, then the payloads."""
-        peers = {"left": self.left, "right": self.right}
-        cnt_out = {s: torch.tensor([counts.get(s, 0)], dtype=torch.int64, device=self.device)
-                   for s in peers}
-        cnt_in = {s: torch.zeros(1, dtype=torch.int64, device=self.device) for s in peers}
-        ops = []
-        for s, p in peers.items():
-            if p is not None:
-                ops.append(dist.P2POp(dist.isend, cnt_out[s], p, group=self.group))
-                ops.append(dist.P2POp(dist.irecv, cnt_in[s], p, group=self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        got = {s: int(cnt_in[s].item()) if peers[s] is not None else 0 for s in peers}
-        ops = []
-        for s, p in peers.items():
+        def slabs(nbytes):
+            return {s: (torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+                        if self.peer[s] is not None else None) for s in self.SIDES}
+        self.send_halo, self.recv_halo = slabs(hb), slabs(hb)
+        self.send_mig, self.recv_mig = slabs(mb), slabs(mb)
+        self.frames = 0
+        self.reorder_every = 64          # frames between row reorderings (no ghosts resident then)
+        self.resync_every = int(resync_every)
+        self.host_syncs = 0
+        # gloo moves host memory only: device slabs are staged through the host (the 2-process
+        # test on one GPU); NCCL sends them as they are
+        self._stage = (self.device.type == "cuda" and dist.is_available() and dist.is_initialized()
+                       and dist.get_backend(group) == "gloo")
+        ops.configure(self.lo, self.hi, float(vmax))
+
+    # -- one exchange with both neighbours: fixed-size slabs, one grouped call ----
+    def _swap(self, send: dict, recv: dict):
+        p2p, staged = [], []
+        for s in self.SIDES:
+            p = self.peer[s]
             if p is None:
                 continue
-            if got[s] > self.capacity:
-                raise RuntimeError(f"rank {self.rank}: {got[s]} records from the {s} exceed the "
-                                   f"exchange capacity {self.capacity}")
-            if counts.get(s, 0):
-                ops.append(dist.P2POp(dist.isend, self.send[s][:counts[s] * RECORD_BYTES], p,
-                                      group=self.group))
-            if got[s]:
-                ops.append(dist.P2POp(dist.irecv, self.recv[s][:got[s] * RECORD_BYTES], p,
-                                      group=self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-            if self.device.type == "cuda":
-                # the append kernels run on the handle's stream, the NCCL copies on torch's:
-                # make the received records globally visible before anyone reads them
-                torch.cuda.current_stream(self.device).synchronize()
-        return got
+            if self._stage:
+                out = send[s].cpu()                      # (synchronises: test transport only)
+                inn = torch.empty_like(out)
+                staged.append((recv[s], inn))
+                p2p += [dist.P2POp(dist.isend, out, p, group=self.group),
+                        dist.P2POp(dist.irecv, inn, p, group=self.group)]
+            else:
+                p2p += [dist.P2POp(dist.isend, send[s], p, group=self.group),
+                        dist.P2POp(dist.irecv, recv[s], p, group=self.group)]
+        if not p2p:
+            return
+        # NCCL: the grouped send/recv is ordered after the packing kernels through the current
+        # stream, and wait() makes the current stream (= the handle's) wait for it -- the host
+        # does not block. gloo (CPU tests): wait() blocks until the bytes are there.
+        for w in dist.batch_isend_irecv(p2p):
+            w.wait()
+        for dst, src in staged:
+            dst.copy_(src)
 
-    # -- protocol phases (split so a test can drive two ranks in one process) ------
-    def pack_halo(self) -> dict:
-        counts = {}
-        if self.left is not None:
-            counts["left"] = self.ops.pack(self.lo, self.lo + self.reach, False, self.send["left"])
-        if self.right is not None:
-            counts["right"] = self.ops.pack(self.hi - self.reach, self.hi, False, self.send["right"])
-        self.stats["halo_sent"] += sum(counts.values())
-        return counts
+    # -- protocol phases (split so a test can drive several ranks in one process) ------
+    def pack_halo(self):
+        self.ops.pack_halo(self.reach, self.send_halo["left"], self.send_halo["right"], self.halo_cap)
 
-    def unpack_halo(self, got: dict):
-        for s in ("left", "right"):
-            self.ops.append(self.recv[s], got.get(s, 0), True)
-        self.stats["halo_recv"] += sum(got.values())
+    def unpack_halo(self):
+        for s in self.SIDES:
+            if self.peer[s] is not None:
+                self.ops.append_slab(self.recv_halo[s], self.halo_cap, True)
 
-    def pack_migrants(self) -> dict:
-        counts = {}
-        if self.left is not None:
-            counts["left"] = self.ops.pack(-math.inf, self.lo, True, self.send["left"])
-        if self.right is not None:
-            counts["right"] = self.ops.pack(self.hi, math.inf, True, self.send["right"])
-        self.stats["migr_sent"] += sum(counts.values())
-        return counts
+    def step_and_pack_migrants(self):
+        self.ops.step(self.send_mig["left"], self.send_mig["right"], self.mig_cap)
 
-    def unpack_migrants(self, got: dict):
-        for s in ("left", "right"):
-            self.ops.append(self.recv[s], got.get(s, 0), False)
-        self.stats["migr_recv"] += sum(got.values())
+    def unpack_migrants(self):
+        for s in self.SIDES:
+            if self.peer[s] is not None:
+                self.ops.append_slab(self.recv_mig[s], self.mig_cap, False)
 
-    def exchange_halo(self):
-        self.unpack_halo(self._swap(self.pack_halo()))
-
-    def migrate(self):
-        self.unpack_migrants(self._swap(self.pack_migrants()))
-
-    def step(self):
-        """One frame of the whole strip-decomposed crowd, as seen by this rank."""
+    def begin_frame(self):
         if self.reorder_every and self.frames % self.reorder_every == 0 and hasattr(self.ops, "reorder"):
             self.ops.reorder()       # rows in cell order: memory coherence only, results unchanged
         self.frames += 1
-        self.exchange_halo()
-        self.ops.step()
-        self.migrate()
+
+    def end_frame(self):
+        if self.resync_every and self.frames % self.resync_every == 0:
+            self.resync()
+
+    def resync(self):
+        self.host_syncs += 1
+        self.ops.resync()
+
+    def step(self):
+        """One frame of the whole strip-decomposed crowd, as seen by this rank."""
+        self.begin_frame()
+        self.pack_halo()
+        self._swap(self.send_halo, self.recv_halo)
+        self.unpack_halo()
+        self.step_and_pack_migrants()
+        self._swap(self.send_mig, self.recv_mig)
+        self.unpack_migrants()
+        self.end_frame()
 
 
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun, one rank per GPU)
+# bench.py --gpus N (one rank per GPU)
 # ---------------------------------------------------------------------------
 
-def run_bench(args, rank: int, world: int, local: int):
-    """Weak scaling: every rank owns one `workload` plaza; the plazas sit side by
-    side along x and form one crowd of world * n agents with halo exchange and
-    migration every step. Prints the JSON line on rank 0."""
+def _select(state, mask):
+    fields = ("ids", "positions", "velocities", "radii", "pref_speeds", "max_speeds", "goals",
+              "goal_tols", "class_codes")
+    return type(state)(frame=state.frame, time=state.time, rng_state=None, lp_fallbacks=0,
+                       **{f: np.ascontiguousarray(getattr(state, f)[mask]) for f in fields})
+
+
+def _slab_capacities(cfg, n_local: int, height: float, density: float, vmax: float):
+    """Records per slab: 2x the expected halo population of one edge (edge length x reach x
+    density) and 16x the expected per-frame migrants, with floors."""
+    halo = int(2.0 * cfg.neighbor_radius * height * density) + 8192
+    mig = int(16.0 * vmax * cfg.dt * height * density) + 4096
+    return min(halo, n_local + 8192), min(mig, n_local + 4096)
+
+
+def _strip_sim(cfg, state, args, local, stream, halo_cap, mig_cap, resync_every):
     from .. import Simulation
-    from ..synth import CONFIGS, plaza_crowd
-
-    n_ped, n_veh, density = CONFIGS[args.workload]
-    n_local = n_ped + n_veh
-    side = math.sqrt(n_local / density)
-    state, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100 + rank, origin=(rank * side, 0.0))
-    state.ids = state.ids + rank * n_local
-    # goals anywhere in the whole crowd's plaza, so agents do cross strip boundaries
-    rng = np.random.default_rng(1000 + rank)
-    state.goals[:, 0] = rng.uniform(0.0, world * side, size=n_local).astype(np.float32)
-    bounds = [side * r for r in range(1, world)]
-    device = torch.device("cuda", local)
-    stream = torch.cuda.Stream(device)
-    torch.cuda.set_stream(stream)       # NCCL ops order themselves against the current stream
-    capacity = int(n_local * 1.15) + 65536
+    n_local = state.active_count
+    capacity = n_local + 2 * halo_cap + 2 * mig_cap * (resync_every + 1) + max(65536, n_local // 8)
     sim = Simulation(cfg, capacity=capacity, precision=args.precision, device=local,
-                     remove_arrivals=False, stream=stream)
+                     remove_arrivals=False, compute_metrics=False, stream=stream)
     sim.load(state)
-    halo_cap = int(4 * cfg.neighbor_radius * side * density) + 65536
-    drv = StripDriver(DeviceStripOps(sim), rank, world, bounds, cfg.neighbor_radius, device, halo_cap)
+    return sim
 
-    for _ in range(max(args.warmup, 3)):
-        drv.step()
-    sim.sync()
-    l0 = sim.info().kernel_launches
+
+def _timed(drv, sim, stream, steps, device, sampler=None):
+    """K frames between a barrier + synchronize on both sides; (device ms, host wall ms),
+    each the max over ranks."""
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = args.make_sampler() if hasattr(args, "make_sampler") else None
     if sampler is not None:
         sampler.__enter__()
+    syncs0 = drv.host_syncs
     e0.record(stream)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(steps):
         drv.step()
     e1.record(stream)
+    t_enq = (time.perf_counter() - t0) * 1e3
     sim.sync()
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - t0) * 1e3
     if sampler is not None:
         sampler.__exit__(None, None, None)
-    ms = torch.tensor([max(e0.elapsed_time(e1), 0.0), wall_ms], device=device, dtype=torch.float64)
+    ms = torch.tensor([max(e0.elapsed_time(e1), 0.0), wall_ms, t_enq, float(drv.host_syncs - syncs0)],
+                      device=_rdev(device), dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    return [float(v) for v in ms]
+
+
+def _rdev(device):
+    """Where the (set-up / reporting) reductions live: on the GPU with NCCL, on the host with gloo."""
+    return device if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
+def _gather_hash(sim, device):
+    """Sum over ranks of the per-rank state_hash (mod 2^64) and the total agent count."""
+    st = sim.state()
+    h = state_hash(st.ids, st.positions, st.velocities)
+    t = torch.tensor([h - (1 << 64) if h >= (1 << 63) else h, st.ids.shape[0]], dtype=torch.int64,
+                     device=_rdev(device))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)          # int64 addition wraps: mod 2^64
+    return int(t[0].item()) & ((1 << 64) - 1), int(t[1].item())
+
+
+def run_bench(args, rank: int, world: int, local: int):
+    """bench.py --gpus N. Two modes (--scaling):
+
+    weak    every rank owns one `workload` plaza; the plazas sit side by side along x and
+            form ONE crowd of world * n agents with halo exchange and migration every step.
+    strong  ONE `workload` crowd (BASELINE config 5: config5_8m) cut into `world` strips at
+            the quantiles of x.
+
+    Either way the line carries `bit_equal_vs_1gpu`: after the timed frames the id-keyed digest
+    of (position, velocity) over all ranks is compared with the digest of the same crowd stepped
+    the same number of frames on ONE device by rank 0 (SURVEY.md s8(e) correctness gate; the
+    multi-rank analogue of pkg/tests/test_engine.py:197). Skipped (null) when the whole crowd
+    does not fit rank 0's GPU next to its strip, or with --no-verify. Prints the JSON line on
+    rank 0."""
+    from .. import Simulation
+    from ..synth import CONFIGS, plaza_crowd
+
+    n_ped, n_veh, density = CONFIGS[args.workload]
+    n_cfg = n_ped + n_veh
+    strong = getattr(args, "scaling", "weak") == "strong"
+    side = math.sqrt(n_cfg / density)
+    device = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)       # NCCL ops order themselves against the current stream
+    if strong:
+        whole, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100)
+        vmax = float(whole.max_speeds.max())
+        bounds = strip_bounds(whole.positions[:, 0], world)
+        b = [-math.inf] + [float(v) for v in bounds] + [math.inf]
+        x = whole.positions[:, 0]
+        state = _select(whole, (x >= b[rank]) & (x < b[rank + 1]))
+        if rank != 0 or getattr(args, "no_verify", False):
+            whole = None
+    else:
+        state, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100 + rank, origin=(rank * side, 0.0))
+        state.ids = state.ids + rank * n_cfg
+        # goals anywhere in the whole crowd's plaza, so agents do cross strip boundaries
+        rng = np.random.default_rng(1000 + rank)
+        state.goals[:, 0] = rng.uniform(0.0, world * side, size=n_cfg).astype(np.float32)
+        bounds = [side * r for r in range(1, world)]
+        vmax = float(state.max_speeds.max())
+        whole = None
+    n_local = state.active_count
+    rdev = _rdev(device)
+    vm = torch.tensor([vmax], dtype=torch.float64, device=rdev)
+    dist.all_reduce(vm, op=dist.ReduceOp.MAX)      # set-up only; nothing collective per frame
+    vmax = float(vm.item())
+    resync_every = 16
+    halo_cap, mig_cap = _slab_capacities(cfg, n_local, side, density, vmax)
+    sim = _strip_sim(cfg, state, args, local, stream, halo_cap, mig_cap, resync_every)
+    drv = StripDriver(DeviceStripOps(sim), rank, world, bounds, cfg.neighbor_radius, device, halo_cap,
+                      mig_cap, vmax=vmax, dt=cfg.dt, resync_every=resync_every)
+
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
+        drv.step()
+    drv.resync()
+    l0 = sim.info().kernel_launches
+    g0, m0 = drv.ops.stats()
+    sampler = args.make_sampler() if hasattr(args, "make_sampler") else None
+    dev_ms, wall_ms, enq_ms, syncs = _timed(drv, sim, stream, args.steps, device, sampler)
     info = sim.info()
-    tot = torch.tensor([float(info.active_agents), float(info.kernel_launches - l0),
-                        float(drv.stats["halo_sent"]), float(drv.stats["migr_sent"])],
-                       device=device, dtype=torch.float64)
+    g1, m1 = drv.ops.stats()
+    tot = torch.tensor([float(info.active_agents), float(info.kernel_launches - l0), float(g1 - g0),
+                        float(m1 - m0)], device=rdev, dtype=torch.float64)
     dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    frames_done = warm + args.steps
+
+    # ---- correctness gate: id-keyed digest over all ranks vs the same crowd on ONE device ----
+    verify = None
+    if not getattr(args, "no_verify", False):
+        got_hash, got_n = _gather_hash(sim, device)
+        want = torch.zeros(2, dtype=torch.int64, device=rdev)
+        if rank == 0:
+            if strong:
+                ref_state = whole
+            else:
+                # the weak-scaling crowd is the concatenation of every rank's plaza (same seeds)
+                parts = []
+                for r in range(world):
+                    st_r, _ = plaza_crowd(n_ped, n_veh, density=density, seed=100 + r, origin=(r * side, 0.0))
+                    st_r.ids = st_r.ids + r * n_cfg
+                    st_r.goals[:, 0] = np.random.default_rng(1000 + r).uniform(
+                        0.0, world * side, size=n_cfg).astype(np.float32)
+                    parts.append(st_r)
+                ref_state = parts[0]
+                if world > 1:
+                    for f in ("ids", "positions", "velocities", "radii", "pref_speeds", "max_speeds", "goals",
+                              "goal_tols", "class_codes"):
+                        setattr(ref_state, f, np.concatenate([getattr(p, f) for p in parts]))
+            n_ref = ref_state.active_count
+            free_b, _total = torch.cuda.mem_get_info(device)
+            if n_ref * 1200 < free_b:                  # ~0.8 KB/agent resident + staging
+                with Simulation(cfg, capacity=n_ref, precision=args.precision, device=local,
+                                remove_arrivals=False, compute_metrics=False, stream=stream) as ref:
+                    ref.load(ref_state)
+                    ref.run(frames_done)
+                    rs = ref.state()
+                h = state_hash(rs.ids, rs.positions, rs.velocities)
+                want[0] = h - (1 << 64) if h >= (1 << 63) else h
+                want[1] = rs.ids.shape[0]
+            else:
+                want[1] = -1
+            del ref_state
+        dist.broadcast(want, src=0)
+        if int(want[1].item()) >= 0:
+            want_hash = int(want[0].item()) & ((1 << 64) - 1)
+            verify = {"bit_equal_vs_1gpu": bool(got_hash == want_hash and got_n == int(want[1].item())),
+                      "frames": frames_done, "agents": got_n,
+                      "digest": f"{got_hash:016x}", "digest_1gpu": f"{want_hash:016x}"}
+        else:
+            verify = {"bit_equal_vs_1gpu": None, "note": "the whole crowd does not fit rank 0's GPU"}
+    whole = None
     dist.barrier()
 
     # ---- e2e: the same step with this rank's positions / velocities going up from pinned host
     # memory and coming back every frame (what a host-side caller of a strip-decomposed crowd pays)
     e2e_steps = max(3, min(args.steps, getattr(args, "e2e_steps", 20)))
+    drv.resync()
     pos, vel = sim.positions_velocities()
     h2d = d2h = 0
     for k in range(2 + e2e_steps):
@@ -258,12 +462,13 @@ def run_bench(args, rank: int, world: int, local: int):
         sim.load_pv(pos, vel, int(sim.info().frame))
         h2d += pos.nbytes + vel.nbytes
         drv.step()
+        drv.resync()
         pos, vel = sim.positions_velocities()
         d2h += pos.nbytes + vel.nbytes
     torch.cuda.synchronize()
-    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device=device, dtype=torch.float64)
+    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / e2e_steps], device=rdev, dtype=torch.float64)
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
-    io = torch.tensor([float(h2d), float(d2h), float(sim.info().active_agents)], device=device, dtype=torch.float64)
+    io = torch.tensor([float(h2d), float(d2h), float(sim.info().active_agents)], device=rdev, dtype=torch.float64)
     dist.all_reduce(io, op=dist.ReduceOp.SUM)
 
     # ---- roofline of the dominant kernel on rank 0 (same definition as the N=1 line)
@@ -275,7 +480,6 @@ def run_bench(args, rank: int, world: int, local: int):
     stage_ms = {k: v / max(covered, 1) for k, v in stage_ms.items()}
     dist.barrier()
     if rank == 0:
-        import os
         hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         pk = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
                           "MEASURED_PEAKS.json")
@@ -284,27 +488,40 @@ def run_bench(args, rank: int, world: int, local: int):
                 hbm_peak, peak_src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
         solve_bytes = (16 + 32 + 1 + 4 * 16 + 1 + 16 + 16 + 2 + 1) * n_local     # bench.py SOLVE_BYTES_PER_AGENT
         achieved = solve_bytes / (max(stage_ms["solve"], 1e-9) * 1e-3) / 1e9
-        ms_step = float(ms[0]) / args.steps
+        ms_step = dev_ms / args.steps
         n_total = int(tot[0])
         line = {"metric": "agent_steps_per_s", "value": n_total / ms_step * 1e3, "unit": "agent-steps/s",
-                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-                "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "n_gpus": world, "steps": args.steps, "warmup": warm,
+                "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+                "vs_baseline": None,
                 "dtype": {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision],
                 "data": "synthetic",
-                "config": {"workload": args.workload, "agents_per_gpu": n_local, "agents_total": n_total,
-                           "parallelism": f"x-strips={world}, halo+migration over NCCL send/recv",
-                           "precision": args.precision, "density_per_m2": density,
-                           "halo_records_per_step": float(tot[2]) / args.steps,
-                           "migrants_per_step": float(tot[3]) / args.steps,
-                           "cache": "state advances every step; working set > L2"},
-                "gpu_launches": int(tot[1]), "host_wall_ms_per_step": float(ms[1]) / args.steps,
+                "config": {"workload": args.workload, "pedestrians": n_ped, "vehicles": n_veh,
+                           "density_per_m2": density, "neighbor_radius": cfg.neighbor_radius,
+                           "max_neighbors": cfg.max_neighbors, "dt": cfg.dt, "tau": cfg.tau},
+                "parallelism": {"layout": f"x-strips={world}", "agents_rank0": n_local, "agents_total": n_total,
+                                "exchange": "fixed-capacity slabs, device-side counts, grouped send/recv "
+                                            "with the adjacent strips; no collective per frame",
+                                "backend": dist.get_backend() + (" (slabs staged through the host: several "
+                                                                 "ranks share a GPU)" if drv._stage else ""),
+                                "halo_record_bytes": drv.ops.halo_record_bytes, "migrant_record_bytes": RECORD_BYTES,
+                                "halo_slab_records": halo_cap, "migrant_slab_records": mig_cap,
+                                "halo_records_per_step": float(tot[2]) / args.steps,
+                                "migrants_per_step": float(tot[3]) / args.steps,
+                                "host_syncs_per_step": syncs / args.steps,
+                                "host_wall_ms_per_step": wall_ms / args.steps,
+                                "host_enqueue_ms_per_step": enq_ms / args.steps},
+                "precision": args.precision,
+                "cache": "state advances every step; working set > L2, no flush",
+                "verify": verify,
+                "gpu_launches": int(tot[1]), "host_wall_ms_per_step": wall_ms / args.steps,
                 "stages_ms": stage_ms,
                 "clocks": sampler.summary() if sampler is not None else None,
                 "e2e": {"value": float(io[2]) / float(e2e[0]) * 1e3, "unit": "agent-steps/s",
                         "ms_per_step": float(e2e[0]), "h2d_bytes_per_step": int(float(io[0]) / e2e_steps),
                         "d2h_bytes_per_step": int(float(io[1]) / e2e_steps),
                         "call": "per rank and frame: Simulation.load_pv(host pos, vel) -> StripDriver.step() "
-                                "(halo exchange, orca_step, migration) -> Simulation.positions_velocities()"},
+                                "(halo exchange, orca_strip_step, migration) -> Simulation.positions_velocities()"},
                 "roofline": {"bound": "hbm", "kernel": "k_solve" if args.precision == "f32" else "k_solve_group",
                              "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                              "traffic": None, "peak_source": peak_src,

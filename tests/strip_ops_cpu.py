@@ -1,10 +1,11 @@
 """Host-side stand-in for the CUDA handle in the strip protocol tests (TEST
 INFRASTRUCTURE: the product binds StripDriver to the C ABI via DeviceStripOps).
 
-OracleStripOps keeps one rank's agent table in numpy, packs / appends the same
-96-byte records as orca_strip_pack / orca_strip_append, and steps with the CPU
-oracle exactly the way the device does: owned + ghost agents are searched, only
-owned agents are solved and integrated, ghosts are dropped after the step.
+OracleStripOps keeps one rank's agent table in numpy, fills / reads the same slabs
+as orca_strip_pack_halo / orca_strip_step / orca_strip_append_slab, and steps with the
+CPU oracle exactly the way the device does: owned + ghost agents are searched, only
+owned agents are solved and integrated, ghosts are dropped after the step, agents whose
+new x left the strip go to the migrant slabs.
 """
 
 import os
@@ -17,7 +18,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
-from paper_2008_11578_b200._lib import RECORD_BYTES, RECORD_DTYPE  # noqa: E402
+from paper_2008_11578_b200._lib import (HALO_DTYPE_F64, RECORD_BYTES, RECORD_DTYPE,  # noqa: E402
+                                        SLAB_HEADER_BYTES, SLAB_HEADER_DTYPE)
 from paper_2008_11578_b200.types import SimState  # noqa: E402
 
 FIELDS = ("ids", "positions", "velocities", "radii", "pref_speeds", "max_speeds", "goals",
@@ -54,37 +56,68 @@ def append_records(state, r):
     state.class_codes = cat([state.class_codes, r["class_code"]])
 
 
+def _header(slab):
+    return slab.numpy()[:SLAB_HEADER_BYTES].view(SLAB_HEADER_DTYPE)
+
+
+def _records(slab, dtype, cap):
+    return slab.numpy()[SLAB_HEADER_BYTES:SLAB_HEADER_BYTES + cap * dtype.itemsize].view(dtype)
+
+
 class OracleStripOps:
+    """The ops interface of StripDriver (DeviceStripOps) on host memory: the same slabs
+    (32-byte header with the count + records), halo records in the FP64 layout."""
+
+    halo_record_bytes = HALO_DTYPE_F64.itemsize
+
     def __init__(self, state, cfg):
         self.state, self.cfg = state, cfg
         self.n_owned = state.ids.shape[0]
+        self.ghosts = self.migrants = 0
+        self.overflow = False
 
-    def pack(self, x_lo, x_hi, remove, buf):
+    def configure(self, x_lo, x_hi, vmax_floor):
+        self.lo, self.hi = x_lo, x_hi
+
+    def pack_halo(self, reach, slab_left, slab_right, cap):
         st = self.state
-        n = st.ids.shape[0]
-        mask = np.zeros(n, dtype=bool)
-        x = st.positions[: self.n_owned, 0]
-        mask[: self.n_owned] = (x >= x_lo) & (x < x_hi)
-        rec = to_records(st, mask)
-        assert rec.nbytes <= buf.numel()
-        buf.numpy()[: rec.nbytes] = rec.view(np.uint8)
-        if remove and rec.shape[0]:
-            assert n == self.n_owned, "cannot remove rows while ghosts are resident"
-            self.state = take(st, ~mask)
-            self.n_owned = self.state.ids.shape[0]
-        return rec.shape[0]
+        assert st.ids.shape[0] == self.n_owned, "ghost rows are resident"
+        x = st.positions[:, 0]
+        for slab, mask in ((slab_left, x < self.lo + reach), (slab_right, x >= self.hi - reach)):
+            if slab is None:
+                continue
+            n = int(mask.sum())
+            h = _header(slab)
+            h["count"], h["overflow"] = n, 0
+            rec = _records(slab, HALO_DTYPE_F64, cap)
+            m = min(n, cap)
+            rec["x"][:m], rec["y"][:m] = st.positions[mask, 0][:m], st.positions[mask, 1][:m]
+            rec["vx"][:m], rec["vy"][:m] = st.velocities[mask, 0][:m], st.velocities[mask, 1][:m]
+            rec["radius"][:m], rec["id"][:m] = st.radii[mask][:m], st.ids[mask][:m]
+            rec["class_code"][:m] = st.class_codes[mask][:m]
 
-    def append(self, buf, count, ghost):
-        if not count:
-            return
-        rec = buf.numpy()[: count * RECORD_BYTES].view(RECORD_DTYPE).copy()
-        if not ghost:
+    def append_slab(self, slab, cap, ghost):
+        h = _header(slab)
+        count = int(h["count"][0])
+        if count > cap or int(h["overflow"][0]):
+            self.overflow = True
+        count = min(count, cap)
+        if ghost:
+            g = _records(slab, HALO_DTYPE_F64, cap)[:count]
+            rec = np.zeros(count, dtype=RECORD_DTYPE)
+            for f in ("x", "y", "vx", "vy", "radius", "id", "class_code"):
+                rec[f] = g[f]
+            rec["goal_x"], rec["goal_y"] = g["x"], g["y"]
+            self.ghosts += count
+        else:
             assert self.state.ids.shape[0] == self.n_owned
+            rec = _records(slab, RECORD_DTYPE, cap)[:count].copy()
+            self.migrants += count
         append_records(self.state, rec)
         if not ghost:
             self.n_owned += count
 
-    def step(self):
+    def step(self, mig_left, mig_right, cap):
         st, cfg = self.state, self.cfg
         m = self.n_owned
         fs = O.frame_solve(st, cfg, rows=m)
@@ -96,8 +129,29 @@ class OracleStripOps:
         new.velocities = fs.out_v[:m].copy()
         new.frame = st.frame + 1
         new.time = new.frame * cfg.dt
-        self.state = new
-        self.n_owned = m
+        x = new.positions[:, 0]
+        keep = np.ones(m, dtype=bool)
+        for slab, mask in ((mig_left, x < self.lo), (mig_right, x >= self.hi)):
+            if slab is None:
+                assert not mask.any()
+                continue
+            rec = to_records(new, mask)
+            h = _header(slab)
+            h["count"], h["overflow"] = rec.shape[0], int(rec.shape[0] > cap)
+            if rec.shape[0] > cap:
+                self.overflow = True
+            k = min(rec.shape[0], cap)
+            _records(slab, RECORD_DTYPE, cap)[:k] = rec[:k]
+            keep &= ~mask
+        self.state = take(new, keep)
+        self.n_owned = self.state.ids.shape[0]
+
+    def resync(self):
+        if self.overflow:
+            raise RuntimeError("strip exchange: a slab overflowed")
+
+    def stats(self):
+        return self.ghosts, self.migrants
 
 
 def reference_run(state, cfg, steps):
@@ -127,6 +181,11 @@ def make_crowd(seed=0, n_ped=700, n_veh=60, density=0.35):
     return st, cfg
 
 
+def crowd_for(world):
+    """Strips must be at least neighbor_radius + max_speed*dt wide: a wider plaza for 3 strips."""
+    return make_crowd() if world <= 2 else make_crowd(n_ped=1150, n_veh=80)
+
+
 def gloo_worker(rank, world, port, steps, out_dir):
     """Entry point of one spawned rank (torch.multiprocessing.spawn)."""
     import torch
@@ -138,19 +197,57 @@ def gloo_worker(rank, world, port, steps, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        st, cfg = make_crowd()
+        st, cfg = crowd_for(world)
         bounds = strip_bounds(st.positions[:, 0], world)
         b = [-np.inf] + list(bounds) + [np.inf]
         mine = (st.positions[:, 0] >= b[rank]) & (st.positions[:, 0] < b[rank + 1])
         ops = OracleStripOps(take(st, mine), cfg)
         drv = StripDriver(ops, rank, world, bounds, cfg.neighbor_radius, torch.device("cpu"),
-                          halo_capacity=st.ids.shape[0])
+                          halo_capacity=st.ids.shape[0], vmax=float(st.max_speeds.max()), dt=cfg.dt,
+                          resync_every=4)
         for _ in range(steps):
             drv.step()
+        drv.resync()
         out = ops.state
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=out.ids, positions=out.positions,
                  velocities=out.velocities, frame=out.frame, lo=drv.lo, hi=drv.hi,
-                 **{k: v for k, v in drv.stats.items()})
+                 halo_recv=ops.stats()[0], migr_recv=ops.stats()[1], host_syncs=drv.host_syncs)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def gpu_gloo_worker(rank, world, port, steps, out_dir, precision):
+    """One of several ranks sharing cuda:0: the CUDA handle behind DeviceStripOps, slabs staged
+    through the host and sent over gloo (tests/test_gpu_strips.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_11578_b200 import Simulation
+    from paper_2008_11578_b200.parallel.strips import DeviceStripOps, StripDriver, strip_bounds
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        st, cfg = make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
+        n = st.ids.shape[0]
+        bounds = strip_bounds(st.positions[:, 0], world)
+        b = [-np.inf] + list(bounds) + [np.inf]
+        mine = (st.positions[:, 0] >= b[rank]) & (st.positions[:, 0] < b[rank + 1])
+        with Simulation(cfg, capacity=2 * n, precision=precision, remove_arrivals=False) as sim:
+            sim.load(take(st, mine))
+            drv = StripDriver(DeviceStripOps(sim), rank, world, bounds, cfg.neighbor_radius,
+                              torch.device("cuda", 0), halo_capacity=n, migrant_capacity=n // 4,
+                              vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=4)
+            assert drv._stage
+            for _ in range(steps):
+                drv.step()
+            drv.resync()
+            out = sim.state()
+            g, m = drv.ops.stats()
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=out.ids, positions=out.positions,
+                 velocities=out.velocities, halo_recv=g, migr_recv=m)
         dist.barrier()
     finally:
         dist.destroy_process_group()

@@ -9,42 +9,65 @@ import torch
 
 import strip_ops_cpu as S
 from paper_2008_11578_b200 import Simulation
+import ctypes as C
+
+from paper_2008_11578_b200 import _lib
 from paper_2008_11578_b200._lib import RECORD_BYTES, RECORD_DTYPE, OrcaError
-from paper_2008_11578_b200.parallel.strips import DeviceStripOps, StripDriver, strip_bounds
+from paper_2008_11578_b200.parallel.strips import DeviceStripOps, StripDriver, state_hash, strip_bounds
 
 pytestmark = pytest.mark.gpu
 
 SIDE = {"left": "right", "right": "left"}
 
 
-def lockstep(drivers, steps):
-    """Drive all ranks phase by phase; rank r's `right` buffer goes to rank r+1's `left`."""
-    def swap(counts):
-        got = [dict() for _ in drivers]
-        for r, d in enumerate(drivers):
-            for side, c in counts[r].items():
-                peer = r - 1 if side == "left" else r + 1
-                dst = drivers[peer].recv[SIDE[side]]
-                dst[: c * RECORD_BYTES].copy_(d.send[side][: c * RECORD_BYTES])
-                got[peer][SIDE[side]] = c
+def lockstep(drivers, steps, reorder_every=3):
+    """Drive all ranks phase by phase; rank r's `right` slab goes to rank r+1's `left`
+    (a device-to-device copy on the legacy stream in place of the NCCL send/recv)."""
+    def swap(which):
         torch.cuda.synchronize()
-        return got
+        for r, d in enumerate(drivers):
+            for side in ("left", "right"):
+                if d.peer[side] is not None:
+                    getattr(drivers[d.peer[side]], "recv_" + which)[SIDE[side]].copy_(
+                        getattr(d, "send_" + which)[side])
+        torch.cuda.synchronize()
 
-    for k in range(steps):
-        if k % 3 == 0:                     # what StripDriver.step does every reorder_every frames
-            for d in drivers:
-                d.ops.reorder()
-        got = swap([d.pack_halo() for d in drivers])
-        for d, g in zip(drivers, got):
-            d.unpack_halo(g)
+    for d in drivers:
+        d.reorder_every = reorder_every
+    for _ in range(steps):
         for d in drivers:
-            d.ops.step()
-        got = swap([d.pack_migrants() for d in drivers])
-        for d, g in zip(drivers, got):
-            d.unpack_migrants(g)
+            d.begin_frame()
+        for d in drivers:
+            d.pack_halo()
+        swap("halo")
+        for d in drivers:
+            d.unpack_halo()
+        for d in drivers:
+            d.step_and_pack_migrants()
+        swap("mig")
+        for d in drivers:
+            d.unpack_migrants()
+        for d in drivers:
+            d.end_frame()
 
 
-@pytest.mark.parametrize("precision,world", [("f64", 2), ("mixed", 3)])
+def build_strips(st, cfg, precision, world, halo_cap, mig_cap, resync_every=4, capacity=None):
+    n = st.ids.shape[0]
+    bounds = strip_bounds(st.positions[:, 0], world)
+    b = [-np.inf] + list(bounds) + [np.inf]
+    sims, drivers = [], []
+    for r in range(world):
+        mine = (st.positions[:, 0] >= b[r]) & (st.positions[:, 0] < b[r + 1])
+        sim = Simulation(cfg, capacity=capacity or 2 * n, precision=precision, remove_arrivals=False)
+        sim.load(S.take(st, mine))
+        sims.append(sim)
+        drivers.append(StripDriver(DeviceStripOps(sim), r, world, bounds, cfg.neighbor_radius,
+                                   torch.device("cuda", 0), halo_cap, mig_cap,
+                                   vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=resync_every))
+    return sims, drivers, b
+
+
+@pytest.mark.parametrize("precision,world", [("f64", 2), ("mixed", 3), ("f32", 2)])
 def test_strips_on_device_equal_single_handle(precision, world):
     st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
     n = st.ids.shape[0]
@@ -53,17 +76,11 @@ def test_strips_on_device_equal_single_handle(precision, world):
         ref.load(st)
         ref.run(steps)
         want = ref.state()
-    bounds = strip_bounds(st.positions[:, 0], world)
-    b = [-np.inf] + list(bounds) + [np.inf]
-    sims, drivers = [], []
-    for r in range(world):
-        mine = (st.positions[:, 0] >= b[r]) & (st.positions[:, 0] < b[r + 1])
-        sim = Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False)
-        sim.load(S.take(st, mine))
-        sims.append(sim)
-        drivers.append(StripDriver(DeviceStripOps(sim), r, world, bounds, cfg.neighbor_radius,
-                                   torch.device("cuda", 0), halo_capacity=n))
+    sims, drivers, b = build_strips(st, cfg, precision, world, halo_cap=n, mig_cap=n // 4)
+    assert drivers[0].ops.halo_record_bytes == (64 if precision == "f64" else 32)
     lockstep(drivers, steps)
+    for d in drivers:
+        d.resync()
     parts = [s.state() for s in sims]
     for r, p in enumerate(parts):
         assert p.frame == steps
@@ -74,11 +91,157 @@ def test_strips_on_device_equal_single_handle(precision, world):
     for f in ("positions", "velocities", "goals", "radii", "max_speeds", "class_codes"):
         got = np.concatenate([getattr(p, f) for p in parts])[order]
         assert np.array_equal(got, getattr(want, f)[ref_order]), f
-    assert sum(d.stats["migr_sent"] for d in drivers) > 0
-    assert sum(d.stats["halo_sent"] for d in drivers) > 0
+    stats = [d.ops.stats() for d in drivers]
+    assert sum(g for g, _m in stats) > 0 and sum(m for _g, m in stats) > 0     # both paths exercised
     assert sum(int(s.info().lp_fallbacks) for s in sims) == want.lp_fallbacks
+    assert all(d.host_syncs <= steps // 4 + 1 for d in drivers)                # the host is not in the frame loop
+    # the digest bench.py compares across ranks
+    assert sum(state_hash(p.ids, p.positions, p.velocities) for p in parts) % (1 << 64) == \
+        state_hash(want.ids, want.positions, want.velocities)
     for s in sims:
         s.close()
+
+
+def test_strips_with_arrival_removal_equal_single_handle():
+    """Arrivals are removed by the strip that owns the agent, in the same compaction that drops
+    ghosts and migrants; who is left, and where, equals the single-handle run."""
+    st, cfg = S.make_crowd(seed=9, n_ped=3000, n_veh=100, density=0.5)
+    rng = np.random.default_rng(2)
+    near = rng.random(st.ids.shape[0]) < 0.4  # 40 % of the agents: a goal 5.5 .. 7.5 m ahead, tolerance 6 m,
+    ang = rng.uniform(0, 2 * np.pi, near.sum())  # so they arrive one after the other during the run
+    dist = rng.uniform(5.5, 7.5, near.sum())
+    st.goals[near] = (st.positions[near] + np.column_stack([np.cos(ang), np.sin(ang)]) * dist[:, None]
+                      ).astype(np.float32)
+    st.goal_tols[near] = 6.0
+    n = st.ids.shape[0]
+    steps = 12
+    with Simulation(cfg, capacity=n, precision="f64", remove_arrivals=True) as ref:
+        ref.load(st)
+        ref.run(steps)
+        want = ref.state()
+    assert 0 < want.ids.shape[0] < n
+    sims, drivers, _b = build_strips(st, cfg, "f64", 2, halo_cap=n, mig_cap=n // 4)
+    for s in sims:
+        s.set_config(cfg, remove_arrivals=True, compute_metrics=False)
+    lockstep(drivers, steps)
+    parts = [s.state() for s in sims]
+    ids = np.concatenate([p.ids for p in parts])
+    order, ref_order = np.argsort(ids), np.argsort(want.ids)
+    assert np.array_equal(ids[order], want.ids[ref_order])
+    assert np.array_equal(np.concatenate([p.positions for p in parts])[order], want.positions[ref_order])
+    assert np.array_equal(np.concatenate([p.velocities for p in parts])[order], want.velocities[ref_order])
+    for s in sims:
+        s.close()
+
+
+def test_slab_overflow_is_reported_not_silent():
+    st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
+    # halo slabs far too small for the ~1,000 agents within neighbor_radius of the edge
+    sims, drivers, _b = build_strips(st, cfg, "mixed", 2, halo_cap=16, mig_cap=4096, resync_every=0)
+    lockstep(drivers, 1)
+    with pytest.raises(OrcaError) as ei:
+        drivers[0].resync()
+    assert ei.value.code == -5 and "overflow" in str(ei.value)
+    for s in sims:
+        s.close()
+    # migrant slabs too small: the rows that do not fit stay put and the flag is raised
+    sims, drivers, _b = build_strips(st, cfg, "mixed", 2, halo_cap=8192, mig_cap=1, resync_every=0)
+    lockstep(drivers, 6)
+    with pytest.raises(OrcaError) as ei:
+        for d in drivers:
+            d.resync()
+    assert ei.value.code == -5
+    for s in sims:
+        s.close()
+
+
+def test_halo_slab_layout_and_refusals():
+    st, cfg = S.make_crowd(seed=5, n_ped=600, n_veh=40)
+    n = st.ids.shape[0]
+    mid = float(np.median(st.positions[:, 0]))
+    for precision, dtype in (("mixed", _lib.HALO_DTYPE_F32), ("f64", _lib.HALO_DTYPE_F64)):
+        with Simulation(cfg, capacity=2 * n, precision=precision, remove_arrivals=False) as sim:
+            sim.load(st)
+            ops = DeviceStripOps(sim)
+            assert ops.halo_record_bytes == dtype.itemsize
+            with pytest.raises(OrcaError):
+                ops.pack_halo(3.0, None, None, n)                     # not configured yet
+            ops.configure(-np.inf, mid, 2.0)
+            slab = torch.zeros(_lib.SLAB_HEADER_BYTES + n * dtype.itemsize, dtype=torch.uint8, device="cuda")
+            ops.pack_halo(cfg.neighbor_radius, None, slab, n)
+            raw = slab.cpu().numpy()
+            hdr = raw[:32].view(_lib.SLAB_HEADER_DTYPE)
+            mask = st.positions[:, 0] >= mid - cfg.neighbor_radius    # owned or not: the handle holds all rows
+            assert int(hdr["count"][0]) == int(mask.sum()) and int(hdr["overflow"][0]) == 0
+            rec = raw[32:32 + int(hdr["count"][0]) * dtype.itemsize].view(dtype)
+            o, ro = np.argsort(rec["id"]), np.argsort(st.ids[mask])
+            assert np.array_equal(rec["id"][o], st.ids[mask][ro])
+            for f, src in (("x", st.positions[mask, 0]), ("vy", st.velocities[mask, 1]), ("radius", st.radii[mask]),
+                           ("class_code", st.class_codes[mask])):
+                assert np.array_equal(rec[f][o].astype(np.float64), src[ro].astype(np.float64)), f
+            # ghosts from a slab: invisible to readback, dropped by the strip step
+            ops.append_slab(slab, n, True)
+            assert int(sim.info().active_agents) == n
+            with pytest.raises(OrcaError):
+                ops.append_slab(slab, n, False)                       # owned rows cannot follow ghosts
+            sim.set_config(cfg, remove_arrivals=False, compute_metrics=True)
+            mig = torch.zeros(_lib.SLAB_HEADER_BYTES + n * RECORD_BYTES, dtype=torch.uint8, device="cuda")
+            with pytest.raises(OrcaError) as ei:
+                ops.step(None, mig, n)                                # metrics would miss cross-strip pairs
+            assert ei.value.code == -6
+            sim.set_config(cfg, remove_arrivals=False, compute_metrics=False)
+            ops.step(None, mig, n)
+            left = sim.state()
+            moved = mig.cpu().numpy()
+            cnt = int(moved[:32].view(_lib.SLAB_HEADER_DTYPE)["count"][0])
+            out = moved[32:32 + cnt * RECORD_BYTES].view(RECORD_DTYPE)
+            assert left.ids.shape[0] + cnt == n                       # every agent is in exactly one place
+            assert np.all(left.positions[:, 0] < mid) and np.all(out["x"] >= mid)
+            assert np.array_equal(np.sort(np.concatenate([left.ids, out["id"]])), np.sort(st.ids))
+
+
+def test_two_processes_one_gpu_over_gloo(tmp_path):
+    """The real device ops under the real multi-process protocol: two ranks share cuda:0, the
+    slabs are staged through host memory and travel over gloo (NCCL refuses two ranks on one
+    device). Equal to the single-handle run, keyed by id."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    world, steps = 2, 6
+    mp.spawn(S.gpu_gloo_worker, args=(world, port, steps, str(tmp_path), "mixed"), nprocs=world, join=True)
+    st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
+    with Simulation(cfg, capacity=st.ids.shape[0], precision="mixed", remove_arrivals=False) as ref:
+        ref.load(st)
+        ref.run(steps)
+        want = ref.state()
+    import os
+    parts = [np.load(os.path.join(tmp_path, f"rank{r}.npz")) for r in range(world)]
+    ids = np.concatenate([p["ids"] for p in parts])
+    order, ref_order = np.argsort(ids), np.argsort(want.ids)
+    assert np.array_equal(ids[order], want.ids[ref_order])
+    assert np.array_equal(np.concatenate([p["positions"] for p in parts])[order], want.positions[ref_order])
+    assert np.array_equal(np.concatenate([p["velocities"] for p in parts])[order], want.velocities[ref_order])
+    assert sum(int(p["migr_recv"]) for p in parts) > 0 and sum(int(p["halo_recv"]) for p in parts) > 0
+
+
+class HostCountOps:
+    """orca_strip_pack / orca_strip_append: the variant that reports its count to the host."""
+
+    def __init__(self, sim):
+        self.sim, self._L = sim, _lib.load()
+
+    def pack(self, x_lo, x_hi, remove, buf):
+        count = C.c_int64()
+        _lib.check(self._L.orca_strip_pack(self.sim._h, float(x_lo), float(x_hi), 1 if remove else 0,
+                                           C.c_void_p(buf.data_ptr()), buf.numel() // RECORD_BYTES,
+                                           C.byref(count)), self.sim._h)
+        return int(count.value)
+
+    def append(self, buf, count, ghost):
+        _lib.check(self._L.orca_strip_append(self.sim._h, C.c_void_p(buf.data_ptr()), int(count),
+                                             1 if ghost else 0), self.sim._h)
 
 
 def test_pack_record_layout_and_errors():
@@ -86,7 +249,7 @@ def test_pack_record_layout_and_errors():
     n = st.ids.shape[0]
     with Simulation(cfg, capacity=n + 64, precision="f64", remove_arrivals=False) as sim:
         sim.load(st)
-        ops = DeviceStripOps(sim)
+        ops = HostCountOps(sim)
         buf = torch.empty(n * RECORD_BYTES, dtype=torch.uint8, device="cuda")
         mid = float(np.median(st.positions[:, 0]))
         c = ops.pack(-np.inf, mid, False, buf)
