@@ -49,7 +49,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2008_11578_b200.synth import CONFIGS, plaza_crowd  # noqa: E402
+from paper_2008_11578_b200.synth import CONFIGS, make_workload  # noqa: E402
 
 # algorithmic bytes
 STEP_BYTES_PER_AGENT = 64          # read 44 + write 20, FP32 state
@@ -132,7 +132,7 @@ class ClockSampler:
 
 def build_workload(name: str, rank: int = 0, world: int = 1):
     n_ped, n_veh, density = CONFIGS[name]
-    state, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100 + rank)
+    state, cfg = make_workload(name, seed=100 + rank)
     if os.environ.get("ORCA_BENCH_SORTED"):
         # experiment: storage rows in spatial (column-major cell) order instead of random order
         c = float(os.environ["ORCA_BENCH_SORTED"])

@@ -264,7 +264,8 @@ def frame_solve(state, config, worker_count: int = 1,
     if debug:
         out.nb_rows = np.empty((n_solved, max(max_n, 1)), dtype=np.int64)
         out.nb_count = np.empty(n_solved, dtype=np.int64)
-        out.constraints = np.empty((n_solved, max(max_n, 1), 4))
+        # debug="lists": neighbour lists only (the constraint dump is 512 B/agent)
+        out.constraints = None if debug == "lists" else np.empty((n_solved, max(max_n, 1), 4))
     if n == 0:
         return out
     rc = lib().oracle_frame_solve(

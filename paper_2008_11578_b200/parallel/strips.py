@@ -114,10 +114,18 @@ def state_hash(ids, positions, velocities) -> int:
 class DeviceStripOps:
     """The slab protocol on a Simulation's resident state through the C ABI."""
 
-    def __init__(self, sim):
+    def __init__(self, sim, stream=None):
+        """`stream`: the torch.cuda.Stream the exchange is ordered on (default: the current
+        one). The handle is moved onto it: the packing / appending kernels and the send/recv
+        of the slabs must follow each other on ONE stream, since nothing else orders them."""
         self.sim = sim
         self._L = load()
         self.halo_record_bytes = int(self._L.orca_strip_halo_record_bytes(sim._h))
+        dev = torch.device("cuda", sim.device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        if not self.stream.cuda_stream:      # the legacy default stream: orca_set_stream reads 0 as
+            self.stream = torch.cuda.Stream(dev)   # "the handle's own stream" -- take a real one
+        sim.set_stream(self.stream)
 
     def configure(self, x_lo: float, x_hi: float, vmax_floor: float):
         check(self._L.orca_strip_configure(self.sim._h, float(x_lo), float(x_hi), float(vmax_floor)),
@@ -219,6 +227,13 @@ class StripDriver:
         for dst, src in staged:
             dst.copy_(src)
 
+    def _exchange(self, send: dict, recv: dict):
+        stream = getattr(self.ops, "stream", None)
+        if stream is None:
+            return self._swap(send, recv)
+        with torch.cuda.stream(stream):      # the handle's stream is the current one for the transport
+            return self._swap(send, recv)
+
     # -- protocol phases (split so a test can drive several ranks in one process) ------
     def pack_halo(self):
         self.ops.pack_halo(self.reach, self.send_halo["left"], self.send_halo["right"], self.halo_cap)
@@ -253,10 +268,10 @@ class StripDriver:
         """One frame of the whole strip-decomposed crowd, as seen by this rank."""
         self.begin_frame()
         self.pack_halo()
-        self._swap(self.send_halo, self.recv_halo)
+        self._exchange(self.send_halo, self.recv_halo)
         self.unpack_halo()
         self.step_and_pack_migrants()
-        self._swap(self.send_mig, self.recv_mig)
+        self._exchange(self.send_mig, self.recv_mig)
         self.unpack_migrants()
         self.end_frame()
 
@@ -347,7 +362,7 @@ def run_bench(args, rank: int, world: int, local: int):
     does not fit rank 0's GPU next to its strip, or with --no-verify. Prints the JSON line on
     rank 0."""
     from .. import Simulation
-    from ..synth import CONFIGS, plaza_crowd
+    from ..synth import CONFIGS, make_workload
 
     n_ped, n_veh, density = CONFIGS[args.workload]
     n_cfg = n_ped + n_veh
@@ -357,7 +372,7 @@ def run_bench(args, rank: int, world: int, local: int):
     stream = torch.cuda.Stream(device)
     torch.cuda.set_stream(stream)       # NCCL ops order themselves against the current stream
     if strong:
-        whole, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100)
+        whole, cfg = make_workload(args.workload, seed=100)
         vmax = float(whole.max_speeds.max())
         bounds = strip_bounds(whole.positions[:, 0], world)
         b = [-math.inf] + [float(v) for v in bounds] + [math.inf]
@@ -366,7 +381,7 @@ def run_bench(args, rank: int, world: int, local: int):
         if rank != 0 or getattr(args, "no_verify", False):
             whole = None
     else:
-        state, cfg = plaza_crowd(n_ped, n_veh, density=density, seed=100 + rank, origin=(rank * side, 0.0))
+        state, cfg = make_workload(args.workload, seed=100 + rank, origin=(rank * side, 0.0))
         state.ids = state.ids + rank * n_cfg
         # goals anywhere in the whole crowd's plaza, so agents do cross strip boundaries
         rng = np.random.default_rng(1000 + rank)
@@ -382,7 +397,7 @@ def run_bench(args, rank: int, world: int, local: int):
     resync_every = 16
     halo_cap, mig_cap = _slab_capacities(cfg, n_local, side, density, vmax)
     sim = _strip_sim(cfg, state, args, local, stream, halo_cap, mig_cap, resync_every)
-    drv = StripDriver(DeviceStripOps(sim), rank, world, bounds, cfg.neighbor_radius, device, halo_cap,
+    drv = StripDriver(DeviceStripOps(sim, stream), rank, world, bounds, cfg.neighbor_radius, device, halo_cap,
                       mig_cap, vmax=vmax, dt=cfg.dt, resync_every=resync_every)
 
     warm = max(args.warmup, 3)
@@ -412,7 +427,7 @@ def run_bench(args, rank: int, world: int, local: int):
                 # the weak-scaling crowd is the concatenation of every rank's plaza (same seeds)
                 parts = []
                 for r in range(world):
-                    st_r, _ = plaza_crowd(n_ped, n_veh, density=density, seed=100 + r, origin=(r * side, 0.0))
+                    st_r, _ = make_workload(args.workload, seed=100 + r, origin=(r * side, 0.0))
                     st_r.ids = st_r.ids + r * n_cfg
                     st_r.goals[:, 0] = np.random.default_rng(1000 + r).uniform(
                         0.0, world * side, size=n_cfg).astype(np.float32)

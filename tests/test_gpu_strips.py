@@ -180,6 +180,10 @@ def test_halo_slab_layout_and_refusals():
                            ("class_code", st.class_codes[mask])):
                 assert np.array_equal(rec[f][o].astype(np.float64), src[ro].astype(np.float64)), f
             # ghosts from a slab: invisible to readback, dropped by the strip step
+            # (the same agents, nudged aside and renamed so that no two centres coincide)
+            rec["x"] += 0.37
+            rec["id"] += 10**6
+            slab.copy_(torch.from_numpy(raw))
             ops.append_slab(slab, n, True)
             assert int(sim.info().active_agents) == n
             with pytest.raises(OrcaError):
