@@ -169,6 +169,77 @@ def cpu_port_rate(state, cfg, rows: int, threads: int, repeats: int = 1):
     return n / best_full, spent
 
 
+def numba_reference(state, cfg, budget_s: float = 40.0):
+    """The UNMODIFIED reference (Python + numba, installed into baseline/_ref by
+    __graft_entry__.build(); git-ignored, travels with the snapshot) through ITS OWN public
+    engine.step (pkg/src/orcasim/engine.py:298; arrival removal and frame metrics included, as
+    in this repository's e2e), after its own JIT warm-up (pkg/src/orcasim/bench.py:55-58), at
+    worker_count = all host cores and 1, on the crowd the GPU arm was timed on. The state and
+    config objects of this package mirror the reference's field for field, so they are passed
+    as they are. Returns a dict for cpu_baseline["reference_numba"]."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "orcasim")):
+        return {"unavailable": "baseline/_ref/orcasim is not installed (run __graft_entry__.build() "
+                               "where /root/reference exists)"}
+    try:
+        import tempfile
+        os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
+        if ref_dir not in sys.path:
+            sys.path.insert(0, ref_dir)
+        from orcasim import bench as rbench
+        from orcasim import engine as rengine
+        t0 = time.perf_counter()
+        rbench.warmup()
+        warm_s = time.perf_counter() - t0
+        n = state.active_count
+        threads = os.cpu_count() or 1
+        out = {"kind": "reference", "impl": "orcasim 0.1.0 (numba %s), engine.step" % __import__("numba").__version__,
+               "agents": n, "jit_warmup_s": round(warm_s, 2), "unit": "agent-steps/s"}
+        spent = 0.0
+        for w in (threads, 1):
+            times = []
+            while len(times) < 3 and spent < budget_s * (0.6 if w == threads else 1.0):
+                t0 = time.perf_counter()
+                rengine.step(state, cfg, worker_count=w)
+                times.append(time.perf_counter() - t0)
+                spent += times[-1]
+                if len(times) == 1 and times[0] * 2 > budget_s * 0.5:
+                    break
+            if times:
+                out[f"workers_{w}"] = {"value": n / min(times), "s_per_step": min(times), "steps_timed": len(times)}
+        return out
+    except Exception as e:      # the reference arm must never take the GPU line down
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
+def parity_census(state, cfg, precisions, device):
+    """One frame of the benchmarked crowd from its initial state in each precision mode against
+    the CPU oracle on EVERY agent (run after the timed region; the oracle is the checker only):
+    status flips, agents beyond the 1e-4 m/s gate, worst |dv|, and whether bins and ordered
+    neighbour lists are bit-identical (north_star: "LP tie/degenerate cases counted and reported")."""
+    from oracle import oracle as O
+    from paper_2008_11578_b200 import Simulation
+    n = state.active_count
+    fs = O.frame_solve(state, cfg, worker_count=os.cpu_count() or 1, debug="lists")
+    out = {"agents": n, "oracle": "oracle/orca_oracle.c, one frame from the initial state, every agent",
+           "fallbacks_oracle": int((fs.status != 0).sum())}
+    for prec in precisions:
+        with Simulation(cfg, capacity=n, precision=prec, device=device, remove_arrivals=False) as sim:
+            sim.load(state)
+            sim.step()
+            sim.sync()
+            d = sim.debug_last_step(n, cfg.max_neighbors)
+        dv = np.abs(d["out_v"] - fs.out_v).max(axis=1)
+        out[prec] = {"status_flips": int((d["status"] != fs.status).sum()),
+                     "failed_at_diffs": int((d["failed_at"] != fs.failed_at).sum()),
+                     "over_1e-4": int((dv > 1e-4).sum()), "max_dv": float(dv.max()),
+                     "bit_exact_velocities": bool(np.array_equal(d["out_v"], fs.out_v)),
+                     "bins_and_neighbour_lists_bit_exact": bool(
+                         np.array_equal(d["cell_ix"], fs.cell_ix) and np.array_equal(d["cell_iy"], fs.cell_iy)
+                         and np.array_equal(d["nb_rows"], fs.nb_rows))}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU port of the reference step on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -348,15 +419,16 @@ def run_ours(args):
                   "solve": "k_solve" if args.precision == "f32" else "k_solve_group",
                   "fallback": "k_fallback_coop"}[dom]
     traffic, traffic_src, ncu_util = load_traffic(args.workload, args.precision, dom_kernel)
-    # ---- context lines: the other precision modes on this workload, and BASELINE config 5
-    # (8.5 M agents) resident on this one GPU
+    # ---- context lines the driver sees too: the other precision modes on this workload, every
+    # other BASELINE config resident on this one GPU, a NON-uniform crowd, the LP microbench
     extras = {}
+    census = None
     if not args.no_extras:
-        def resident_ms(st, cf, precision, steps):
+        def resident(st, cf, precision, steps, warm=5):
             with Simulation(cf, capacity=st.active_count, precision=precision, device=local,
                             remove_arrivals=False, compute_metrics=False, stream=stream) as sm:
                 sm.load(st)
-                sm.run(5)
+                sm.run(warm)
                 sm.sync()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -364,16 +436,31 @@ def run_ours(args):
                 b.record(stream)
                 sm.sync()
                 torch.cuda.synchronize()
-                return a.elapsed_time(b) / steps
+                inf = sm.info()
+                ms = a.elapsed_time(b) / steps
+                return {"agents": st.active_count, "ms_per_step": ms,
+                        "agent_steps_per_s": st.active_count / ms * 1e3,
+                        "fallback_fraction": float(inf.lp_fallbacks) / max(st.active_count, 1),
+                        "fast_gather_reject_fraction": float(inf.gather_queue) / max(st.active_count, 1)}
         extras["precision_modes_ms_per_step"] = {
-            p: resident_ms(state, cfg, p, 50) for p in ("mixed", "f32", "f64") if p != args.precision}
+            p: resident(state, cfg, p, 50)["ms_per_step"] for p in PRECISIONS if p != args.precision}
         if args.workload == "plaza_1m":
-            big, bcfg, _ = build_workload("config5_8m")
-            ms8 = resident_ms(big, bcfg, args.precision, 20)
-            extras["config5_8m_single_gpu"] = {"agents": big.active_count, "ms_per_step": ms8,
-                                               "agent_steps_per_s": big.active_count / ms8 * 1e3,
-                                               "precision": args.precision}
-            del big
+            other = {}
+            for name, steps in (("config1_1k", 200), ("config2_16k", 200), ("config3_262k_d1", 50),
+                                ("config3_262k_d2", 50), ("config3_262k_d1_nr3", 50), ("config3_262k_d2_nr3", 50),
+                                ("blobs_1m", 50), ("config5_8m", 20)):
+                st2, cf2, _ = build_workload(name)
+                other[name] = resident(st2, cf2, args.precision, steps)
+                other[name]["precision"] = args.precision
+                del st2
+            extras["other_configs_resident"] = other
+            extras["config5_8m_single_gpu"] = other["config5_8m"]
+            extras["lp_1m_resident_ms"] = {k: lp_resident(k, "f64", local, stream, 10)
+                                           for k in sorted(LP_WORKLOADS)}
+        census = parity_census(state, cfg, [args.precision] + [p for p in ("f32",) if p != args.precision], local)
+        ref_numba = numba_reference(state, cfg)
+    else:
+        ref_numba = {"skipped": "--no-extras"}
 
     dtype = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision]
     line = {
@@ -383,7 +470,7 @@ def run_ours(args):
         "data": "synthetic", "config": wl, "precision": args.precision,
         "cache": "state advances every step; per-step working set ~%.0f MB > 126 MB L2, no flush"
                  % (n * 260 / 1e6),
-        "lp_fallbacks_last_step": fallbacks, "clocks": clocks.summary(),
+        "lp_fallbacks_last_step": fallbacks, "parity": census, "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "agent-steps/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                 "call": "paper_2008_11578_b200.engine.step(state, config) -- full drop-in incl. "
@@ -405,12 +492,39 @@ def run_ours(args):
                          "sample": f"one step: grid build + desired velocities over all {n} agents, "
                                    f"per-agent solve on rows [0,{rows}) scaled by n/rows; "
                                    f"oracle/orca_oracle.c ({threads} pthreads); "
-                                   f"1 thread: {cpu1_value:.3e} agent-steps/s"},
+                                   f"1 thread: {cpu1_value:.3e} agent-steps/s",
+                         "reference_numba": ref_numba},
     }
     print(json.dumps(line), flush=True)
 
 
+PRECISIONS = ("mixed", "f32", "f64")
+
 LP_WORKLOADS = {"lp_1m_feasible": 0.0, "lp_1m_half": 0.5, "lp_1m_infeasible": 1.0}
+
+
+def lp_resident(workload, prec, local, stream, steps):
+    """ms per solve of the resident 1,048,576-LP batch of BASELINE config 4 (for `extras`)."""
+    import torch
+
+    from paper_2008_11578_b200 import LpBatch
+    from paper_2008_11578_b200.synth import lp_batch
+    coff, cpts, cnrm, tgt, caps, seeds = lp_batch(1 << 20, 8, 64, LP_WORKLOADS[workload], seed=5)
+    b = LpBatch(coff, cpts, cnrm, tgt, caps, seeds, precision=prec, device=local, stream=stream)
+    del cpts, cnrm
+    for _ in range(3):
+        b.solve()
+    b.results()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        b.solve()
+    e1.record(stream)
+    _v, status, _f = b.results()
+    torch.cuda.synchronize()
+    b.close()
+    return {"ms_per_solve": e0.elapsed_time(e1) / steps, "precision": prec,
+            "fallback_fraction": float((status != 0).mean())}
 
 
 def run_lp(args):
@@ -519,7 +633,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="plaza_1m", choices=sorted(CONFIGS) + sorted(LP_WORKLOADS))
-    ap.add_argument("--precision", default="mixed", choices=["mixed", "f32", "f64"])
+    ap.add_argument("--precision", default="mixed", choices=list(PRECISIONS))
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="agents the CPU port solves per step (0: the whole crowd for cpu_baseline, "

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define ORCA_ABI_VERSION 1
+#define ORCA_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ORCA_API __attribute__((visibility("default")))
@@ -108,6 +108,10 @@ typedef struct orca_info {
     int32_t grid_nx, grid_ny; /* search-grid dimensions used by the last step */
     double grid_cell;         /* search-grid cell edge (m) */
     int64_t kernel_launches;  /* kernels this handle has launched since orca_create */
+    int64_t gather_queue;     /* last step: agents whose neighbour list the certified fast pass could
+                                 not prove exact and handed to the exact ring search */
+    int64_t solve_queue;      /* last step, ORCA_CERT32 only: agents whose FP32 solve could not be
+                                 certified and was redone in FP64 */
 } orca_info;
 
 /* ---- lifetime ----------------------------------------------------------- */

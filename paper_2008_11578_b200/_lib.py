@@ -73,7 +73,8 @@ class OrcaInfo(C.Structure):
     _fields_ = [("frame", C.c_int64), ("active_agents", C.c_int64), ("lp_fallbacks", C.c_int64),
                 ("removed_agents", C.c_int64), ("collision_count", C.c_int64),
                 ("min_separation", C.c_double), ("grid_nx", C.c_int32), ("grid_ny", C.c_int32),
-                ("grid_cell", C.c_double), ("kernel_launches", C.c_int64)]
+                ("grid_cell", C.c_double), ("kernel_launches", C.c_int64),
+                ("gather_queue", C.c_int64), ("solve_queue", C.c_int64)]
 
 
 _lib = None

@@ -620,6 +620,9 @@ extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
     info->grid_ny = h.ny;
     info->grid_cell = h.cell;
     info->kernel_launches = sim->launches;
+    info->gather_queue = 0;
+    for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) info->gather_queue += h.gq_count[c];
+    info->solve_queue = h.cq_count;
     return rc;
 }
 

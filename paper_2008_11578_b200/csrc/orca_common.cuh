@@ -48,6 +48,7 @@ struct GridPlan {
     // per-step counters
     int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
     int gq_count[ORCA_MAX_CHUNKS]; // agents queued for the exact ring search (k_gather), per chunk
+    int cq_count;   // ORCA_CERT32: agents whose FP32 solve was not certified (redone in FP64)
     int pack_count; // rows selected by the last orca_strip_pack
     u64 vmax_enc;  // order-preserving encoding of the largest max_speed ever uploaded
     double vmax;

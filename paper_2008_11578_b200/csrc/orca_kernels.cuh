@@ -78,6 +78,7 @@ namespace orca {
 __global__ void k_begin_step(GridPlan *plan)
 {
     plan->fq_count = 0;
+    plan->cq_count = 0;
     plan->n_pre = plan->n_owned;
     for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) plan->gq_count[c] = 0;
     plan->removed = 0;

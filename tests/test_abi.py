@@ -30,13 +30,13 @@ def test_library_exports_every_declared_symbol():
     lib = C.CDLL(_lib.LIB_PATH)      # loading must not need a GPU
     for name in header_symbols():
         assert hasattr(lib, name), name
-    assert lib.orca_abi_version() == 1
+    assert lib.orca_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
-    # orca_params: 8 doubles + 4 int32; orca_info: 5 int64 + double + 2 int32 + double + int64
+    # orca_params: 8 doubles + 4 int32; orca_info: 5 int64 + double + 2 int32 + double + 3 int64
     assert C.sizeof(_lib.OrcaParams) == 8 * 8 + 4 * 4
-    assert C.sizeof(_lib.OrcaInfo) == 5 * 8 + 8 + 2 * 4 + 8 + 8
+    assert C.sizeof(_lib.OrcaInfo) == 5 * 8 + 8 + 2 * 4 + 8 + 3 * 8
     src = open(HEADER).read()
     assert "#define ORCA_N_STAGES 6" in src and _lib.ORCA_N_STAGES == 6
     assert "ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2" in src
