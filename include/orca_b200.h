@@ -162,6 +162,13 @@ ORCA_API int orca_download_pv(orca_sim *sim, double *positions, double *velociti
  * before that step. Synchronises. */
 ORCA_API int orca_download_last_step_pv(orca_sim *sim, int64_t n, double *positions, double *velocities);
 
+/* Which rows of the LAST step's pre-step state survived its arrival removal
+ * (engine.py:251-255,288-294): kept[i] = 1 if storage row i is still resident, 0 if the
+ * agent arrived and was removed. n must be the agent count before that step. A host caller
+ * that keeps its own float64 copies of the per-agent attributes compacts them with this mask
+ * instead of reading back the device's (possibly FP32-rounded) copies. Synchronises. */
+ORCA_API int orca_download_last_step_kept(orca_sim *sim, int64_t n, uint8_t *kept);
+
 /* Host -> device refresh of positions and velocities only (same n, same rows). */
 ORCA_API int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
                    const double *velocities);
@@ -272,6 +279,20 @@ ORCA_API void orca_lp_batch_destroy(orca_lp_batch *b);
  * in7 = (rpx, rpy, rvx, rvy, comb_r, tau, dt) per case, out5 = (ux, uy, nx, ny, ok). */
 ORCA_API int orca_vo_exit_batch(int device, int precision, int64_t count, const double *in7,
                        double *out5);
+
+/* The least-penetration stage alone (lp.solve_least_penetration, lp.py:168-190 ->
+ * _kernels.py:254-283 with the constraints in the given order): cpts/cnrm float64[k,2],
+ * warm start (wx, wy) assumed to satisfy constraints [0, start_index); out_v[2]. */
+ORCA_API int orca_least_penetration(int device, int precision, int64_t k, const double *cpts,
+                                    const double *cnrm, double speed_cap, int64_t start_index,
+                                    double wx, double wy, double *out_v);
+
+/* The neighbour query alone (grid.query_neighbors, grid.py:50-83 == _kernels.py:450-490) for
+ * EVERY agent at once: the up to max_count (<= ORCA_MAX_NEIGHBORS) nearest agents within
+ * `radius`, ascending by (distance, id). ids int64[n], positions float64[n,2]; out_rows
+ * int64[n, max_count] (row indices, -1 padded), out_count int64[n]. */
+ORCA_API int orca_neighbor_query(int device, int64_t n, const int64_t *ids, const double *positions,
+                                 double radius, int32_t max_count, int64_t *out_rows, int64_t *out_count);
 
 /* Fisher-Yates order (_kernels.py:43-54) computed on the device: perm[k]. */
 ORCA_API int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *perm);

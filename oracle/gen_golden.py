@@ -28,6 +28,8 @@ Fixtures (all small, compressed):
   scenario_cases.json, traj_two_way_12.csv, agents_two_way_12.csv
                      crossing documents, spawned crowds, validation messages and CSV
                      bytes of the reference's scenario / crossings / cli modules.
+  api_cases.npz      the object-level operators (orca.gather_constraints, grid.query_neighbors,
+                     lp.solve_least_penetration) on seeded inputs.
   chain_1k.npz       config 1: 100 consecutive reference steps of 1,024
                      pedestrians (each input = previous output rounded to
                      float32 so an FP32 device state sees identical inputs);
@@ -453,8 +455,67 @@ def gen_scenarios():
     print("scenario_cases.json:", len(cases), "cases,", len(broken), "broken documents")
 
 
+def gen_api():
+    """api_cases.npz: the reference's OBJECT-level operators on seeded inputs --
+    orca.gather_constraints, grid.query_neighbors, lp.solve_least_penetration and
+    lp.solve_batch -- for the host wrappers of paper_2008_11578_b200 (orca.py, grid.py, lp.py)."""
+    import orcasim
+    from orcasim import AgentClass, AgentState, HalfPlaneConstraint, ResponsibilityMatrix
+    rng = np.random.default_rng(77)
+    n = 160
+    pos = rng.uniform(0.0, 30.0, size=(n, 2))
+    pos[5] = pos[4] + np.array([0.3, 0.0])                     # an overlapping pair (dt-horizon disc)
+    vel = rng.normal(size=(n, 2))
+    cls = (rng.random(n) < 0.15).astype(np.int64)
+    radius = np.where(cls == 1, 1.0, 0.25) * (1.0 + 0.1 * rng.random(n))
+    ids = rng.permutation(1000)[:n].astype(np.int64)
+    agents = [AgentState(id=int(ids[i]), position=pos[i], velocity=vel[i], radius=float(radius[i]),
+                         pref_speed=1.0, max_speed=2.0, goal=pos[i] + 1.0, agent_class=AgentClass(int(cls[i])))
+              for i in range(n)]
+    grid = orcasim.rebuild(agents, 4.0)
+    out = {"ids": ids, "positions": pos, "velocities": vel, "radii": radius, "class_codes": cls,
+           "grid_cells": np.array(sorted(grid.cells), dtype=np.int64), "grid_population": np.int64(grid.population)}
+    for radius_q, max_count in ((6.0, 8), (3.5, 16), (9.0, 32), (50.0, 5)):
+        rows = np.full((n, max_count), -1, dtype=np.int64)
+        for i, a in enumerate(agents):
+            nb = orcasim.query_neighbors(grid, agents, a.id, radius_q, max_count)
+            rows[i, :len(nb)] = [b.id for b in nb]
+        out[f"nb_ids_r{radius_q:g}_m{max_count}"] = rows
+    matrix = ResponsibilityMatrix.default()
+    cons_pts, cons_nrm, cons_cnt = np.zeros((n, 16, 2)), np.zeros((n, 16, 2)), np.zeros(n, dtype=np.int64)
+    for i, a in enumerate(agents):
+        nb = orcasim.query_neighbors(grid, agents, a.id, 6.0, 16)
+        cs = orcasim.gather_constraints(a, nb, matrix, 2.0, 0.1)
+        cons_cnt[i] = len(cs)
+        for t, c in enumerate(cs):
+            cons_pts[i, t], cons_nrm[i, t] = c.point, c.normal
+    out.update(cons_pts=cons_pts, cons_nrm=cons_nrm, cons_cnt=cons_cnt)
+    # least penetration on random (mostly infeasible) constraint sets, the given order, several warm starts
+    lp_k, lp_pts, lp_nrm, lp_cap, lp_start, lp_warm, lp_out = [], [], [], [], [], [], []
+    for case in range(60):
+        k = int(rng.integers(0, 20))
+        ang = rng.uniform(0, 2 * np.pi, k)
+        nrm = np.column_stack([np.cos(ang), np.sin(ang)])
+        pts = rng.normal(size=(k, 2)) * 1.2
+        cap = float(0.5 + 2.0 * rng.random())
+        start = int(rng.integers(0, k + 1))
+        warm = rng.normal(size=2) * 0.5
+        cs = [HalfPlaneConstraint(pts[t], nrm[t]) for t in range(k)]
+        v = orcasim.solve_least_penetration(cs, cap, start_index=start, warm_start=warm)
+        row_p, row_n = np.zeros((20, 2)), np.zeros((20, 2))
+        row_p[:k], row_n[:k] = pts, nrm
+        lp_k.append(k); lp_pts.append(row_p); lp_nrm.append(row_n); lp_cap.append(cap)
+        lp_start.append(start); lp_warm.append(warm); lp_out.append(v)
+    out.update(lp_k=np.array(lp_k), lp_pts=np.array(lp_pts), lp_nrm=np.array(lp_nrm), lp_cap=np.array(lp_cap),
+               lp_start=np.array(lp_start), lp_warm=np.array(lp_warm), lp_out=np.array(lp_out))
+    np.savez_compressed(os.path.join(OUT, "api_cases.npz"), **out)
+    print("api_cases.npz", {k: getattr(v, "shape", None) for k, v in out.items()})
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if os.environ.get("GEN_ONLY_API"):
+        return gen_api()
     if os.environ.get("GEN_ONLY_RUN"):
         return gen_run()
     if os.environ.get("GEN_ONLY_SCENARIO"):
@@ -465,6 +526,7 @@ def main():
     gen_chain()
     gen_run()
     gen_scenarios()
+    gen_api()
 
 
 def gen_run():

@@ -13,7 +13,11 @@ from .scenario import (Region, ScenarioError, build_agents, load_scenario, read_
                        scenario_from_dict, write_metrics_summary, write_trajectories)
 from .crossings import crossing_config, four_way_dict, two_way_dict
 from .lp import (HalfPlaneConstraint, LpBatch, LpProblem, LpResult, LpStatus, shuffle_order,
-                 solve_batch, solve_closest_point, solve_range)
+                 solve_batch, solve_closest_point, solve_least_penetration, solve_range)
+from .orca import AgentState, VoExit, build_orca_halfplane, compute_vo_exit, gather_constraints
+from .grid import UniformGrid, query_neighbors, rebuild
+from .scenario import sample_spawns
+from .benchmark import BenchReport, BenchRow, run_bench, write_bench_report
 
 __all__ = ["AgentClass", "ClassParams", "FrameMetrics", "ResponsibilityMatrix",
            "ScenarioConfig", "SimState", "Simulation", "desired_velocity", "init_state",
@@ -21,4 +25,6 @@ __all__ = ["AgentClass", "ClassParams", "FrameMetrics", "ResponsibilityMatrix",
            "LpStatus", "shuffle_order", "solve_batch", "solve_closest_point", "solve_range",
            "Region", "ScenarioError", "build_agents", "load_scenario", "read_trajectories",
            "scenario_from_dict", "write_metrics_summary", "write_trajectories", "crossing_config",
-           "four_way_dict", "two_way_dict"]
+           "four_way_dict", "two_way_dict", "solve_least_penetration", "AgentState", "VoExit",
+           "build_orca_halfplane", "compute_vo_exit", "gather_constraints", "UniformGrid", "query_neighbors",
+           "rebuild", "sample_spawns", "BenchReport", "BenchRow", "run_bench", "write_bench_report"]

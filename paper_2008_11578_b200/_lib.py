@@ -27,12 +27,13 @@ ORCA_ECOINCIDENT, ORCA_ERANGE = -3, -4
 SYMBOLS = [
     "orca_abi_version", "orca_create", "orca_destroy", "orca_set_stream", "orca_set_params",
     "orca_last_error", "orca_upload", "orca_download", "orca_download_pv", "orca_upload_pv",
-    "orca_download_last_step_pv",
+    "orca_download_last_step_pv", "orca_download_last_step_kept",
     "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host", "orca_advance_host", "orca_reorder_rows",
     "orca_profile_stages", "orca_get_stage_ms",
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
     "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
+    "orca_least_penetration", "orca_neighbor_query",
     "orca_strip_pack", "orca_strip_append", "orca_strip_drop_ghosts",
     "orca_strip_halo_record_bytes", "orca_strip_configure", "orca_strip_pack_halo",
     "orca_strip_append_slab", "orca_strip_step", "orca_strip_stats",
@@ -105,6 +106,7 @@ def load():
     L.orca_download.argtypes = [vp] + [vp] * 9
     L.orca_download_pv.argtypes = [vp, vp, vp]
     L.orca_download_last_step_pv.argtypes = [vp, i64, vp, vp]
+    L.orca_download_last_step_kept.argtypes = [vp, i64, vp]
     L.orca_upload_pv.argtypes = [vp, i64, i64, vp, vp]
     L.orca_step.argtypes = [vp]
     L.orca_run.argtypes = [vp, i64]
@@ -124,6 +126,8 @@ def load():
     L.orca_lp_batch_destroy.argtypes = [vp]
     L.orca_lp_batch_destroy.restype = None
     L.orca_vo_exit_batch.argtypes = [ci, ci, i64, vp, vp]
+    L.orca_least_penetration.argtypes = [ci, ci, i64, vp, vp, f64, i64, f64, f64, vp]
+    L.orca_neighbor_query.argtypes = [ci, i64, vp, vp, f64, C.c_int32, vp, vp]
     L.orca_shuffle_order.argtypes = [ci, i64, u64, vp]
     L.orca_problem_seed.argtypes = [ci, i64, i64, P(u64)]
     L.orca_strip_pack.argtypes = [vp, f64, f64, ci, vp, i64, P(i64)]

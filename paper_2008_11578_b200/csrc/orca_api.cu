@@ -45,6 +45,7 @@ struct orca_sim {
     // lrow[.][p] is the logical row of physical row p (identity until the first reordering).
     // Every host-facing copy goes through it; the kernels of the step never need it.
     int *lrow[2] = {nullptr, nullptr};
+    Attr64 *a64[2] = {nullptr, nullptr};       // float64 attributes as uploaded (FP32-state modes only)
     int *lkeep = nullptr, *lscan = nullptr;    // compaction: keep flags / new rows in logical order
     bool rows_permuted = false;
     bool reorder_due = false;                  // lay the rows out in cell order at the next step
@@ -94,17 +95,11 @@ struct orca_sim {
     double4 *box_part = nullptr; // one bounding box per k_count block of the last bin build
     int box_parts = 0;
     int64_t launches = 0;      // kernels launched by this handle since creation
-    double occ_target = 4.0;   // mean agents per search cell the plan aims for (ORCA_OCC_TARGET)
-    int r0_override = 0;       // ORCA_R0: force the first ring radius (experiments)
-    int fb_lanes = 8;          // ORCA_FB_LANES: lanes per warp that take a fallback agent
-    bool gather_fast = true;   // ORCA_GATHER_FAST=0: exact ring search for every agent
-    bool gather_keys32 = true; // ORCA_GATHER_KEYS32=0: FP64-keyed fast pass (k_gather_fast)
-    bool fb_coop = true;       // ORCA_FB_COOP=0: thread-per-agent least-penetration stage
-    int solve_gl = 2;          // ORCA_SOLVE_GL: lanes per agent in the LP kernel (1, 2 or 4);
-                               //  default 2 with FP64 arithmetic, 1 with FP32 (measured)
+    double occ_target = 4.0;   // mean agents per search cell the plan aims for (ORCA_OCC_TARGET; results are
+                               //  invariant under it, tests/test_gpu_step.py)
+    int solve_gl = 2;          // lanes per agent in the LP kernel: 2 with FP64 arithmetic, 1 with FP32 (measured)
     bool use_graph = true;     // ORCA_GRAPH=0: launch the step's kernels one by one
-    int chunks = 1;            // ORCA_CHUNKS: gather+solve ranges issued on two streams
-    cudaStream_t aux_stream = nullptr;
+    cudaStream_t aux_stream = nullptr; // copy stream of orca_advance_host
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // orca_advance_host: copies overlapped with the step (see there)
     cudaEvent_t ev_vel = nullptr, ev_state = nullptr, ev_dl = nullptr;
@@ -213,16 +208,6 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
     e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::solve_bpt * 64);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::solve_bpt * 32);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::solve_bpt * 32);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_fallback<S, R, MAXN, C::fb_threads>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::fb_bpt * (C::fb_threads / 32) * 16);
-    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL_SHORT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::fb_bpt * (C::fb_threads / ORCA_GL_SHORT));
@@ -255,6 +240,8 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->box_part);
     cudaFree(sim->lrow[0]);
     cudaFree(sim->lrow[1]);
+    cudaFree(sim->a64[0]);
+    cudaFree(sim->a64[1]);
     cudaFree(sim->lkeep);
     cudaFree(sim->lscan);
     cudaFree(sim->cell_of);
@@ -314,16 +301,9 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
         const double v = atof(occ);
         if (v > 0.0) sim->occ_target = v;
     }
-    if (const char *r0 = getenv("ORCA_R0")) sim->r0_override = atoi(r0);
-    if (const char *gf = getenv("ORCA_GATHER_FAST")) sim->gather_fast = atoi(gf) != 0;
-    if (const char *gk = getenv("ORCA_GATHER_KEYS32")) sim->gather_keys32 = atoi(gk) != 0;
-    if (const char *fc = getenv("ORCA_FB_COOP")) sim->fb_coop = atoi(fc) != 0;
     sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
-    if (const char *sg = getenv("ORCA_SOLVE_GL")) sim->solve_gl = atoi(sg) >= 4 ? 4 : (atoi(sg) >= 2 ? 2 : 1);
     if (const char *re = getenv("ORCA_REORDER_EVERY")) sim->reorder_every = std::max(0, atoi(re));
     if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
-    if (const char *ch = getenv("ORCA_CHUNKS")) sim->chunks = std::min(ORCA_MAX_CHUNKS, std::max(1, atoi(ch)));
-    if (const char *fl = getenv("ORCA_FB_LANES")) sim->fb_lanes = std::min(16, std::max(1, atoi(fl)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
     const size_t as = precision == ORCA_F32 ? sizeof(float) : sizeof(double); // arithmetic type R
@@ -365,6 +345,10 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->box_part, (size_t)((std::max<int64_t>(cap, 1) + 255) / 256)));
     CKC(dalloc(&sim->lrow[0], cap));
     CKC(dalloc(&sim->lrow[1], cap));
+    if (precision != ORCA_F64) {
+        CKC(dalloc(&sim->a64[0], cap));
+        CKC(dalloc(&sim->a64[1], cap));
+    }
     CKC(dalloc(&sim->lkeep, cap + 1));
     CKC(dalloc(&sim->lscan, cap + 1));
     CKC(dalloc(&sim->cell_of, cap));
@@ -424,7 +408,7 @@ extern "C" int orca_set_params(orca_sim *sim, const orca_params *p)
                     p->max_neighbors, ORCA_MAX_NEIGHBORS);
     if (!sim->have_params || memcmp(&sim->params, p, sizeof(orca_params)) != 0) sim->drop_graphs();
     const int maxn = p->max_neighbors <= 16 ? 16 : 32; // the MAXN the step's kernels are instantiated for
-    if (ORCA_FB_SPILL && maxn > sim->spill_maxn) {
+    if (maxn > sim->spill_maxn) {
         CK(sim, cudaSetDevice(sim->device));
         CK(sim, cudaStreamSynchronize(sim->stream));
         sim->drop_graphs(); // captured launches hold the old pointers
@@ -487,7 +471,7 @@ static int upload_attrs_impl(orca_sim *sim, int64_t n, const double *radii, cons
     k_import_attrs<R><<<grid_for(n, 256), 256, 0, st>>>(
         (int)n, d_rad, d_pref, d_max, d_goal, d_gtol, d_cls,
         reinterpret_cast<R4 *>(sim->goalpref[sim->acur]), reinterpret_cast<R2 *>(sim->radmax[sim->acur]),
-        sim->cls[sim->acur], sim->hint[sim->acur], sim->plan);
+        sim->cls[sim->acur], sim->hint[sim->acur], sim->plan, sim->a64[sim->acur]);
     CKL(sim);
     return ORCA_OK;
 }
@@ -620,8 +604,7 @@ extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
     info->grid_ny = h.ny;
     info->grid_cell = h.cell;
     info->kernel_launches = sim->launches;
-    info->gather_queue = 0;
-    for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) info->gather_queue += h.gq_count[c];
+    info->gather_queue = h.gq_count;
     info->solve_queue = h.cq_count;
     return rc;
 }
@@ -655,7 +638,7 @@ static int download_attrs_impl(orca_sim *sim, int64_t n, double *radii, double *
     k_export_attrs<R><<<grid_for(n, 256), 256, 0, st>>>(
         (int)n, reinterpret_cast<const R4 *>(sim->goalpref[sim->acur]),
         reinterpret_cast<const R2 *>(sim->radmax[sim->acur]), sim->cls[sim->acur], d_rad, d_pref, d_max,
-        d_goal, d_gtol, d_cls, sim->lrow[sim->acur]);
+        d_goal, d_gtol, d_cls, sim->lrow[sim->acur], sim->a64[sim->acur]);
     CKL(sim);
     if (radii) CK(sim, cudaMemcpyAsync(radii, d_rad, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     if (pref) CK(sim, cudaMemcpyAsync(pref, d_pref, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -718,6 +701,30 @@ extern "C" int orca_download_last_step_pv(orca_sim *sim, int64_t n, double *posi
     return ORCA_OK;
 }
 
+extern "C" int orca_download_last_step_kept(orca_sim *sim, int64_t n, uint8_t *kept)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_download_last_step_kept: no resident state");
+    int rc = fetch_plan(sim);
+    if (rc) return rc;
+    if (sim->frame > 0 || sim->h_plan->n_pre > 0) sim->n_pre = sim->h_plan->n_pre;
+    if (n != sim->n_pre)
+        return fail(sim, ORCA_EINVAL, "orca_download_last_step_kept: n = %lld, last step had %lld rows",
+                    (long long)n, (long long)sim->n_pre);
+    if (n == 0) return ORCA_OK;
+    if (!kept) return fail(sim, ORCA_EINVAL, "orca_download_last_step_kept: kept is NULL");
+    u8 *d = reinterpret_cast<u8 *>(sim->stg);
+    if (!sim->params.remove_arrivals) { // nothing is ever removed: no compaction ran, no flags exist
+        CK(sim, cudaMemsetAsync(d, 1, (size_t)n, sim->stream));
+    } else {
+        // the flags of the step's compaction, in the physical row order of the pre-compaction arrays
+        k_export_keep<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->keep, sim->lrow[sim->apre], d);
+        CKL(sim);
+    }
+    CK(sim, cudaMemcpyAsync(kept, d, (size_t)n, cudaMemcpyDeviceToHost, sim->stream));
+    CK(sim, cudaStreamSynchronize(sim->stream));
+    return ORCA_OK;
+}
+
 extern "C" int orca_download_pv(orca_sim *sim, double *positions, double *velocities)
 {
     return orca_download(sim, nullptr, positions, velocities, nullptr, nullptr, nullptr, nullptr, nullptr,
@@ -742,7 +749,6 @@ static StepParams make_params(const orca_sim *sim)
     P.stride = (int)(sim->capacity > 0 ? sim->capacity : 1);
     P.max_cells = (int)std::min<int64_t>(sim->max_cells, 2 * sim->n_bound + 1024);
     P.occ_target = sim->occ_target;
-    P.r0_override = sim->r0_override;
     return P;
 }
 
@@ -793,113 +799,90 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
     return ORCA_OK;
 }
 
+// K2: certified fast pass for everyone, exact ring search for the agents it queued
+template <typename S, int MAXN> static int gather_stage(orca_sim *sim, const StepParams &P)
+{
+    typedef typename Vec<S>::T2 S2;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur;
+    k_gather_fast32<S, MAXN, 48><<<grid_for(n, 128), 128, 0, st>>>(
+        sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+        reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, 0, (int)n);
+    const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 127) / 128));
+    k_gather<S, MAXN><<<gq_blocks, 128, 0, st>>>(
+        sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
+        sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq);
+    CKL(sim);
+    sim->launches += 2;
+    return ORCA_OK;
+}
+
 template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim, const StepParams &P, int out_idx)
 {
     typedef typename Vec<S>::T4 S4;
-    typedef typename Vec<S>::T2 S2;
     typedef typename Vec<R>::T4 R4;
     typedef KCfg<R, MAXN> C;
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
-    const bool spill = ORCA_FB_SPILL != 0;
-    if (spill && (sim->spill_maxn < MAXN || !sim->fq_cons || !sim->fq_perm))
+    if (sim->spill_maxn < MAXN || !sim->fq_cons || !sim->fq_perm)
         return fail(sim, ORCA_EINVAL, "solve_stage: no spill buffers for max_neighbors %d", P.max_n);
-    // Gather + solve over `chunks` ranges of sorted slots, alternating between the handle's
-    // stream and an auxiliary one: the neighbour search (ALU/issue bound) of one range
-    // overlaps the LP (FP64/latency bound) of another. chunks == 1 is the plain sequence.
-    const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(sim->chunks, (n + 4095) / 4096));
-    const int64_t per = ((n + chunks - 1) / chunks + 127) / 128 * 128;
-    if (chunks > 1) {
-        CK(sim, cudaEventRecord(sim->ev_fork, st));
-        CK(sim, cudaStreamWaitEvent(sim->aux_stream, sim->ev_fork, 0));
+    int rc = gather_stage<S, MAXN>(sim, P);
+    if (rc) return rc;
+    sim->mark();
+    if (sim->split_vel) {
+        // the velocities were still in flight while the bins and the neighbour lists
+        // were built from the positions; they are needed from here on
+        CK(sim, cudaStreamWaitEvent(st, sim->ev_vel, 0));
+        k_patch_vel<S><<<grid_for(n, 256), 256, 0, st>>>(
+            sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
+            reinterpret_cast<NbRec<S> *>(sim->s_nr), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
+        sim->launches += 1;
     }
-    for (int c = 0; c < chunks; ++c) {
-        cudaStream_t cs = (c & 1) ? sim->aux_stream : st;
-        const int s0 = (int)std::min<int64_t>(n, c * per), s1 = (int)std::min<int64_t>(n, (c + 1) * per);
-        const int64_t m = s1 - s0;
-        if (m <= 0) continue;
-        if (sim->gather_fast && sim->gather_keys32)
-            k_gather_fast32<S, MAXN, 48><<<grid_for(m, 128), 128, 0, cs>>>(
-                sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-                reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, s0, s1,
-                c);
-        else if (sim->gather_fast)
-            k_gather_fast<S, MAXN, 48><<<grid_for(m, 128), 128, 0, cs>>>(
-                sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-                sim->ids[a], reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt,
-                sim->gq, s0, s1, c);
-        else
-            k_enqueue_all<<<grid_for(m, 256), 256, 0, cs>>>(sim->plan, P.max_n, sim->s_row, sim->nb_cnt, sim->gq,
-                                                             s0, s1, c);
-        const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (m + 127) / 128));
-        k_gather<S, MAXN><<<gq_blocks, 128, 0, cs>>>(
-            sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-            sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, s0, c);
-        if (chunks == 1) sim->mark();
-        if (sim->split_vel) {
-            // the velocities were still in flight while the bins and the neighbour lists
-            // were built from the positions; they are needed from here on
-            CK(sim, cudaStreamWaitEvent(cs, sim->ev_vel, 0));
-            k_patch_vel<S><<<grid_for(n, 256), 256, 0, cs>>>(
-                sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
-                reinterpret_cast<NbRec<S> *>(sim->s_nr), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
-            sim->launches += 1;
-        }
+    const int s0 = 0, s1 = (int)n;
 #define ORCA_SOLVE_ARGS                                                                                    \
     sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
         sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
         sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1,  \
-        sim->lrow[a], spill ? reinterpret_cast<R4 *>(sim->fq_cons) : nullptr, spill ? sim->fq_perm : nullptr
-        // below ~64 k agents the step is launch-latency bound and the extra launch costs more than the
-        // idle lanes of the in-kernel shuffle (16,640 agents: +1.8 us)
-        const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && n >= ORCA_PRESHUFFLE_MIN_AGENTS;
-        const uint32_t *s_perm = preshuffle ? reinterpret_cast<const uint32_t *>(sim->s_perm) : nullptr;
-        if (preshuffle) {
-            k_shuffle<MAXN><<<grid_for(m, 128), 128, 0, cs>>>(sim->plan, sim->s_row, sim->ids[a], sim->nb_cnt,
-                                                             reinterpret_cast<uint4 *>(sim->s_perm), s0, s1);
-            sim->launches += 1;
-        }
-        if (sim->solve_gl == 2 && preshuffle)
-            k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(
-                ORCA_SOLVE_ARGS, s_perm);
-        else if (sim->solve_gl == 2)
-            k_solve_group<S, R, MAXN, 128, 2, false><<<grid_for(m, 64), 128, C::solve_bpt * 64, cs>>>(
-                ORCA_SOLVE_ARGS, s_perm);
-        else if (sim->solve_gl == 4 && preshuffle)
-            k_solve_group<S, R, MAXN, 128, 4, true><<<grid_for(m, 32), 128, C::solve_bpt * 32, cs>>>(
-                ORCA_SOLVE_ARGS, s_perm);
-        else if (sim->solve_gl == 4)
-            k_solve_group<S, R, MAXN, 128, 4, false><<<grid_for(m, 32), 128, C::solve_bpt * 32, cs>>>(
-                ORCA_SOLVE_ARGS, s_perm);
-        else
-            k_solve<S, R, MAXN, C::solve_threads><<<grid_for(m, C::solve_threads), C::solve_threads,
-                                                    C::solve_bpt * C::solve_threads, cs>>>(ORCA_SOLVE_ARGS);
-#undef ORCA_SOLVE_ARGS
-        sim->launches += 3;
+        sim->lrow[a], reinterpret_cast<R4 *>(sim->fq_cons), sim->fq_perm
+    // below ~64 k agents the step is launch-latency bound and the extra launch costs more than the
+    // idle lanes of the in-kernel shuffle (16,640 agents: +1.8 us)
+    const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && n >= ORCA_PRESHUFFLE_MIN_AGENTS;
+    const uint32_t *s_perm = preshuffle ? reinterpret_cast<const uint32_t *>(sim->s_perm) : nullptr;
+    if (preshuffle) {
+        k_shuffle<MAXN><<<grid_for(n, 128), 128, 0, st>>>(sim->plan, sim->s_row, sim->ids[a], sim->nb_cnt,
+                                                         reinterpret_cast<uint4 *>(sim->s_perm), s0, s1);
+        sim->launches += 1;
     }
-    if (chunks > 1) {
-        CK(sim, cudaEventRecord(sim->ev_join, sim->aux_stream));
-        CK(sim, cudaStreamWaitEvent(st, sim->ev_join, 0));
-        sim->mark(); // with overlap the gather / solve split is not observable: all of it
-    }                //  is booked under "gather" and "solve" reads 0
+    if (sim->solve_gl == 2 && preshuffle)
+        k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(n, 64), 128, C::solve_bpt * 64, st>>>(
+            ORCA_SOLVE_ARGS, s_perm);
+    else if (sim->solve_gl == 2)
+        k_solve_group<S, R, MAXN, 128, 2, false><<<grid_for(n, 64), 128, C::solve_bpt * 64, st>>>(
+            ORCA_SOLVE_ARGS, s_perm);
+    else
+        k_solve<S, R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
+                                                C::solve_bpt * C::solve_threads, st>>>(ORCA_SOLVE_ARGS);
+#undef ORCA_SOLVE_ARGS
+    sim->launches += 1;
     sim->mark();
-    if (sim->fb_coop) {
+    {
 #define ORCA_FB_ARGS                                                                                       \
     sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
         sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
         sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state),                               \
-        spill ? reinterpret_cast<const R4 *>(sim->fq_cons) : nullptr, spill ? sim->fq_perm : nullptr
+        reinterpret_cast<const R4 *>(sim->fq_cons), sim->fq_perm
         // long-queue and short-queue instance; the device-side queue length decides which one works
         const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
         const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + ng - 1) / ng));
-        if (ORCA_GL_SHORT == ORCA_GL || n > ORCA_FB_SHORT_QUEUE) // a queue of <= n entries is never "long"
+        if (ORCA_GL_SHORT == ORCA_GL || n > ORCA_FB_SHORT_QUEUE) { // a queue of <= n entries is never "long"
             k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
                 ORCA_FB_ARGS);
-        else
-            sim->launches -= 1;
+            sim->launches += 1;
+        }
         if (ORCA_GL_SHORT != ORCA_GL) {
             const int ngs = C::fb_threads / ORCA_GL_SHORT;
             const int64_t qmax = std::min<int64_t>(n, ORCA_FB_SHORT_QUEUE);
@@ -909,20 +892,9 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
             sim->launches += 1;
         }
 #undef ORCA_FB_ARGS
-    } else {
-        const int lanes = sim->fb_lanes;                          // active lanes per warp (<= 16)
-        const int fb_at = (C::fb_threads / 32) * lanes;           // agents per block per pass
-        const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + fb_at - 1) / fb_at));
-        k_fallback<S, R, MAXN, C::fb_threads><<<fb_blocks, C::fb_threads, C::fb_bpt * fb_at, st>>>(
-            sim->plan, P, lanes, reinterpret_cast<const NbRec<S> *>(sim->s_nr),
-            reinterpret_cast<const R4 *>(sim->s_dm), sim->s_row,
-            sim->ids[a], sim->nb, sim->nb_cnt, reinterpret_cast<const S4 *>(sim->goalpref[a]),
-            reinterpret_cast<S4 *>(sim->pv[out_idx]), sim->arrived, sim->fq,
-            reinterpret_cast<const R4 *>(sim->fq_state));
     }
     sim->mark();
     CKL(sim);
-    sim->launches += 1;
     return ORCA_OK;
 }
 
@@ -946,7 +918,7 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
             reinterpret_cast<const R4 *>(sim->pv[src_idx]), reinterpret_cast<const R4 *>(sim->goalpref[a]),
             reinterpret_cast<const R2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->strip_lo, sim->strip_hi,
             hl, hl ? reinterpret_cast<orca_agent_record *>(hl + 1) : nullptr, hr,
-            hr ? reinterpret_cast<orca_agent_record *>(hr + 1) : nullptr, (int)sim->mig_cap);
+            hr ? reinterpret_cast<orca_agent_record *>(hr + 1) : nullptr, (int)sim->mig_cap, sim->a64[a]);
     } else
         k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
                                                            sim->params.remove_arrivals);
@@ -973,7 +945,7 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
         reinterpret_cast<R4 *>(sim->goalpref[b]), reinterpret_cast<const R2 *>(sim->radmax[a]),
         reinterpret_cast<R2 *>(sim->radmax[b]), sim->ids[a], sim->ids[b], sim->cls[a], sim->cls[b],
         sim->status[a], sim->status[b], sim->failed[a], sim->failed[b], sim->hint[a], sim->hint[b],
-        sim->lrow[a], sim->lrow[b], lscan);
+        sim->lrow[a], sim->lrow[b], lscan, sim->a64[a], sim->a64[b]);
     k_after_compact<<<1, 1, 0, st>>>(sim->plan, sim->dst_idx);
     CKL(sim);
     sim->launches += 6;
@@ -1010,7 +982,7 @@ template <typename S, typename R> static int reorder_rows(orca_sim *sim, const S
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->goalpref[b]),
         reinterpret_cast<const S2 *>(sim->radmax[a]), reinterpret_cast<S2 *>(sim->radmax[b]), sim->ids[a],
         sim->ids[b], sim->cls[a], sim->cls[b], sim->status[a], sim->status[b], sim->failed[a], sim->failed[b],
-        sim->hint[a], sim->hint[b], sim->lrow[a], sim->lrow[b]);
+        sim->hint[a], sim->hint[b], sim->lrow[a], sim->lrow[b], sim->a64[a], sim->a64[b]);
     CKL(sim);
     sim->launches += 1;
     sim->cur = dst;
@@ -1319,17 +1291,7 @@ extern "C" int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const 
             k_import_pos<double><<<grid_for(n, 256), 256, 0, st>>>(
                 (int)n, d_pos, reinterpret_cast<double4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
         CKL(sim);
-        sim->split_vel = sim->chunks <= 1;
-        if (!sim->split_vel) { // chunked gather/solve: no overlap, patch right away
-            CK(sim, cudaStreamWaitEvent(st, sim->ev_vel, 0));
-            if (sim->precision != ORCA_F64)
-                k_import_pv<float><<<grid_for(n, 256), 256, 0, st>>>(
-                    (int)n, d_pos, d_vel, reinterpret_cast<float4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
-            else
-                k_import_pv<double><<<grid_for(n, 256), 256, 0, st>>>(
-                    (int)n, d_pos, d_vel, reinterpret_cast<double4 *>(sim->pv[sim->cur]), sim->lrow[sim->acur]);
-            CKL(sim);
-        }
+        sim->split_vel = true;
         sim->early_pos = new_positions;
         sim->early_vel = new_velocities;
         rc = step_plain(sim);
@@ -1365,7 +1327,7 @@ static int strip_pack_impl(orca_sim *sim, double x_lo, double x_hi, int remove, 
     k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->sel, sim->block_sums, sim->sel_idx);
     k_strip_pack<S><<<grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(
         sim->plan, sim->sel, sim->sel_idx, pv, reinterpret_cast<const S4 *>(sim->goalpref[a]),
-        reinterpret_cast<const S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], records, cap);
+        reinterpret_cast<const S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], records, cap, sim->a64[a]);
     CKL(sim);
     sim->launches += 5;
     int rc = fetch_plan(sim);
@@ -1407,7 +1369,7 @@ template <typename S> static int strip_append_impl(orca_sim *sim, const orca_age
     k_strip_append<S><<<grid_for(count, 256), 256, 0, sim->stream>>>(
         sim->plan, records, (int)count, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
         reinterpret_cast<S4 *>(sim->goalpref[a]), reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a],
-        sim->cls[a], sim->status[a], sim->failed[a], sim->hint[a], sim->lrow[a]);
+        sim->cls[a], sim->status[a], sim->failed[a], sim->hint[a], sim->lrow[a], sim->a64[a]);
     k_after_append<<<1, 1, 0, sim->stream>>>(sim->plan, (int)count, ghost);
     CKL(sim);
     sim->launches += 2;
@@ -1517,13 +1479,13 @@ template <typename S> static int strip_append_slab_impl(orca_sim *sim, const voi
             sim->plan, hdr, reinterpret_cast<const HaloRec<S> *>(hdr + 1), (int)cap, (int)sim->capacity,
             reinterpret_cast<S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->goalpref[a]),
             reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->status[a], sim->failed[a],
-            sim->hint[a], sim->lrow[a]);
+            sim->hint[a], sim->lrow[a], sim->a64[a]);
     else
         k_strip_append_slab<S><<<grid_for(cap, 256), 256, 0, st>>>(
             sim->plan, hdr, reinterpret_cast<const orca_agent_record *>(hdr + 1), (int)cap, (int)sim->capacity,
             reinterpret_cast<S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->goalpref[a]),
             reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->status[a], sim->failed[a],
-            sim->hint[a], sim->lrow[a]);
+            sim->hint[a], sim->lrow[a], sim->a64[a]);
     k_after_append_slab<<<1, 1, 0, st>>>(sim->plan, hdr, (int)cap, (int)sim->capacity, ghost);
     CKL(sim);
     sim->launches += 2;
@@ -1588,7 +1550,7 @@ extern "C" int orca_strip_stats(orca_sim *sim, int64_t *ghost_rows, int64_t *mig
 template <typename S, typename R>
 static int debug_impl(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_iy, int64_t *nb_rows,
                       int64_t *nb_count, double *out_v, int64_t *status, int64_t *failed_at,
-                      double *desired_v)
+                      double *desired_v, bool lists_only = false)
 {
     typedef typename Vec<S>::T4 S4;
     typedef typename Vec<R>::T4 R4;
@@ -1615,11 +1577,13 @@ static int debug_impl(orca_sim *sim, int64_t n, int64_t *cell_ix, int64_t *cell_
     k_debug_rows<S, R><<<grid_for(n, 256), 256, 0, st>>>(
         (int)n, P, reinterpret_cast<const S4 *>(sim->pv[sim->pre]), sim->s_row, sim->nb, sim->nb_cnt,
         reinterpret_cast<const R4 *>(sim->s_dm), d_ix, d_iy, d_rows, d_cnt, d_des, sim->lrow[sim->acur]);
-    // the un-compacted post-step buffer is pv[(pre+1)%3]
-    k_export_pv<S><<<grid_for(n, 256), 256, 0, st>>>(
-        (int)n, reinterpret_cast<const S4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel, sim->lrow[sim->acur]);
-    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->status[sim->acur], d_st, sim->lrow[sim->acur]);
-    k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->failed[sim->acur], d_fa, sim->lrow[sim->acur]);
+    if (!lists_only) {
+        // the un-compacted post-step buffer is pv[(pre+1)%3]
+        k_export_pv<S><<<grid_for(n, 256), 256, 0, st>>>(
+            (int)n, reinterpret_cast<const S4 *>(sim->pv[(sim->pre + 1) % 3]), d_pos, d_vel, sim->lrow[sim->acur]);
+        k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->status[sim->acur], d_st, sim->lrow[sim->acur]);
+        k_export_i8<<<grid_for(n, 256), 256, 0, st>>>((int)n, sim->failed[sim->acur], d_fa, sim->lrow[sim->acur]);
+    }
     CKL(sim);
     if (cell_ix) CK(sim, cudaMemcpyAsync(cell_ix, d_ix, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
     if (cell_iy) CK(sim, cudaMemcpyAsync(cell_iy, d_iy, sizeof(i64) * n, cudaMemcpyDeviceToHost, st));
@@ -1876,6 +1840,90 @@ extern "C" int orca_vo_exit_batch(int device, int precision, int64_t count, cons
     cudaFree(d_out);
     CK(nullptr, e);
     return ORCA_OK;
+}
+
+extern "C" int orca_least_penetration(int device, int precision, int64_t k, const double *cpts,
+                                      const double *cnrm, double speed_cap, int64_t start_index, double wx,
+                                      double wy, double *out_v)
+{
+    if (k < 0 || k > 0x3FFFFFFF || (k > 0 && (!cpts || !cnrm)) || !out_v || start_index < 0 || start_index > k)
+        return fail(nullptr, ORCA_EINVAL, "orca_least_penetration: bad arguments");
+    if (precision != ORCA_F32 && precision != ORCA_F64)
+        return fail(nullptr, ORCA_EINVAL, "orca_least_penetration: precision must be ORCA_F32 or ORCA_F64");
+    CK(nullptr, cudaSetDevice(device));
+    const size_t kk = (size_t)std::max<int64_t>(k, 1);
+    const size_t rs = precision == ORCA_F32 ? sizeof(float) : sizeof(double);
+    double *d_in = nullptr, *d_out = nullptr;
+    void *d_cons = nullptr, *d_proj = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&d_in), sizeof(double) * 4 * kk);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&d_out), sizeof(double) * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&d_cons, 4 * rs * kk);
+    if (e == cudaSuccess) e = cudaMalloc(&d_proj, 4 * rs * kk);
+    if (e == cudaSuccess && k > 0) e = cudaMemcpy(d_in, cpts, sizeof(double) * 2 * k, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && k > 0) e = cudaMemcpy(d_in + 2 * k, cnrm, sizeof(double) * 2 * k, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        if (precision == ORCA_F32) {
+            if (k > 0) k_lp_pack<float><<<grid_for(k, 256), 256>>>((i64)k, d_in, d_in + 2 * k, reinterpret_cast<float4 *>(d_cons));
+            k_least_penetration_tap<float><<<1, 1>>>((int)k, (int)start_index, reinterpret_cast<const float4 *>(d_cons),
+                                                     reinterpret_cast<float4 *>(d_proj), speed_cap, wx, wy, d_out);
+        } else {
+            if (k > 0) k_lp_pack<double><<<grid_for(k, 256), 256>>>((i64)k, d_in, d_in + 2 * k, reinterpret_cast<double4 *>(d_cons));
+            k_least_penetration_tap<double><<<1, 1>>>((int)k, (int)start_index, reinterpret_cast<const double4 *>(d_cons),
+                                                      reinterpret_cast<double4 *>(d_proj), speed_cap, wx, wy, d_out);
+        }
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out_v, d_out, sizeof(double) * 2, cudaMemcpyDeviceToHost);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    cudaFree(d_cons);
+    cudaFree(d_proj);
+    CK(nullptr, e);
+    return ORCA_OK;
+}
+
+extern "C" int orca_neighbor_query(int device, int64_t n, const int64_t *ids, const double *positions,
+                                   double radius, int32_t max_count, int64_t *out_rows, int64_t *out_count)
+{
+    if (n < 0 || (n > 0 && (!ids || !positions || !out_count || (max_count > 0 && !out_rows))))
+        return fail(nullptr, ORCA_EINVAL, "orca_neighbor_query: bad arguments");
+    if (!(radius > 0.0) || !std::isfinite(radius))
+        return fail(nullptr, ORCA_EINVAL, "radius must be positive, got %g", radius);
+    if (max_count < 0) return fail(nullptr, ORCA_EINVAL, "max_count must be >= 0, got %d", max_count);
+    if (max_count > ORCA_MAX_NEIGHBORS)
+        return fail(nullptr, ORCA_EUNSUPPORTED, "max_count %d exceeds ORCA_MAX_NEIGHBORS (%d)", max_count,
+                    ORCA_MAX_NEIGHBORS);
+    if (n == 0) return ORCA_OK;
+    orca_sim *sim = nullptr;
+    int rc = orca_create(&sim, device, n, ORCA_F64);
+    if (rc) return rc;
+    orca_params p{};
+    p.dt = 1.0;
+    p.tau = 1.0;
+    p.neighbor_radius = radius;
+    p.max_neighbors = max_count;
+    rc = orca_set_params(sim, &p);
+    if (!rc) {
+        // only positions and ids matter to the search; the other attributes get placeholders
+        std::vector<double> zeros((size_t)2 * n, 0.0), ones((size_t)n, 1.0);
+        std::vector<int64_t> cls((size_t)n, 0);
+        rc = orca_upload(sim, n, 0, ids, positions, zeros.data(), ones.data(), ones.data(), ones.data(), positions,
+                         ones.data(), cls.data());
+        if (!rc) rc = orca_sync(sim); // the uploads read the host vectors asynchronously
+    }
+    if (!rc) {
+        const StepParams P = make_params(sim);
+        rc = bin_build<double, double>(sim, P);
+        if (!rc) rc = max_count <= 16 ? gather_stage<double, 16>(sim, P) : gather_stage<double, 32>(sim, P);
+        sim->pre = sim->cur;
+        sim->n_pre = n;
+        if (!rc) rc = debug_impl<double, double>(sim, n, nullptr, nullptr, out_rows, out_count, nullptr, nullptr,
+                                                 nullptr, nullptr, /*lists_only=*/true);
+        if (!rc) rc = fetch_plan(sim); // range error of a position (engine.py:152-153)
+    }
+    if (rc) memcpy(g_err, sim->err, sizeof(g_err));
+    orca_destroy(sim);
+    return rc;
 }
 
 extern "C" int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *perm)

@@ -19,9 +19,6 @@ typedef signed char i8;
 
 #define ORCA_NO_ERR 0xFFFFFFFFFFFFFFFFULL
 
-// gather+solve can be issued as up to this many agent ranges on two streams (orca_api.cu)
-#define ORCA_MAX_CHUNKS 8
-
 // Device-resident per-step plan and counters. Written by k_plan / k_finish and
 // read by every kernel of the step, so a step needs no host round trip.
 struct GridPlan {
@@ -47,7 +44,7 @@ struct GridPlan {
     unsigned long long strip_recv[2]; // ghost rows / migrant rows appended from slabs since the upload
     // per-step counters
     int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
-    int gq_count[ORCA_MAX_CHUNKS]; // agents queued for the exact ring search (k_gather), per chunk
+    int gq_count;  // agents the certified fast pass queued for the exact ring search (k_gather)
     int cq_count;   // ORCA_CERT32: agents whose FP32 solve was not certified (redone in FP64)
     int pack_count; // rows selected by the last orca_strip_pack
     u64 vmax_enc;  // order-preserving encoding of the largest max_speed ever uploaded
@@ -63,13 +60,20 @@ struct GridPlan {
     i64 frame;
 };
 
+// The per-agent attributes a step never changes, exactly as the host uploaded them (float64):
+// kept beside the FP32 state of the MIXED / F32 modes so that everything the host reads back
+// after an arrival removal is the value it uploaded, not an FP32 rounding of it
+// (engine.py:288-294 hands the caller's own arrays on). Unused (null) with FP64 state.
+struct Attr64 {
+    double radius, pref_speed, max_speed, goal_x, goal_y, goal_tol;
+};
+
 struct StepParams {
     double dt, tau, nr, rad2, half_margin;
     double fmat[4];
     int max_n;
     int stride;  // leading dimension of the slot-major neighbour table
     int max_cells;
-    int r0_override; // > 0: force the first ring radius (experiments)
     double occ_target;
 };
 

@@ -37,12 +37,6 @@
 #ifndef ORCA_FB_SHORT_QUEUE
 #define ORCA_FB_SHORT_QUEUE 4096 // "short": every queued agent gets half a warp in one wave
 #endif
-#ifndef ORCA_GATHER_WARP
-#define ORCA_GATHER_WARP 1 // k_gather: a short queue is searched one entry per WARP (cooperatively)
-#endif
-#ifndef ORCA_BUILD_PREFETCH
-#define ORCA_BUILD_PREFETCH 1 // k_solve_group: request the next neighbour's record one iteration ahead
-#endif
 #ifndef ORCA_PRESHUFFLE
 #define ORCA_PRESHUFFLE 1   // k_solve_group reads the insertion order k_shuffle computed, one thread per agent
 #endif
@@ -52,20 +46,8 @@
 #ifndef ORCA_PRESHUFFLE_MIN_AGENTS
 #define ORCA_PRESHUFFLE_MIN_AGENTS 65536
 #endif
-#ifndef ORCA_FB_SPILL
-#define ORCA_FB_SPILL 1     // solve kernels hand the queued agents' constraints to k_fallback_coop through HBM
-#endif
 #ifndef ORCA_SG_BLOCKS
 #define ORCA_SG_BLOCKS 6    // resident blocks per SM k_solve_group is compiled for (register cap)
-#endif
-#ifndef ORCA_FB_BLOCKS
-#define ORCA_FB_BLOCKS 0    // > 0: compile k_fallback_coop for this many resident blocks per SM (6, 8 measured: worse)
-#endif
-#ifndef ORCA_FB_RUNAHEAD
-#define ORCA_FB_RUNAHEAD 1 // k_fallback_coop: warp-voted run-ahead stage (orca_math.cuh, g_*_ra)
-#endif
-#ifndef ORCA_LP_RUNAHEAD
-#define ORCA_LP_RUNAHEAD 1 // k_solve: per-lane run-ahead LP (orca_math.cuh, lp2_target_runahead)
 #endif
 
 namespace orca {
@@ -80,7 +62,7 @@ __global__ void k_begin_step(GridPlan *plan)
     plan->fq_count = 0;
     plan->cq_count = 0;
     plan->n_pre = plan->n_owned;
-    for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) plan->gq_count[c] = 0;
+    plan->gq_count = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
     plan->sep_ub_enc = plan->min_sep_enc;
@@ -180,7 +162,6 @@ __global__ void k_plan(GridPlan *plan, StepParams P, double grow)
     // at the mean density (the search still grows ring by ring where that is not enough)
     const double occ = fmax((double)n, 1.0) * c * c / area;
     int r0 = (int)ceil((sqrt(1.3 * (double)max(P.max_n, 1) / fmax(occ, 1e-9)) - 1.0) * 0.5);
-    if (P.r0_override > 0) r0 = P.r0_override;
     plan->r0 = min(max(r0, 1), plan->rmax);
 }
 
@@ -518,41 +499,6 @@ template <int MAXN> struct TopK {
         return true;
     }
 
-    // compare-exchange of slots a < b by key only (ties are detected afterwards)
-    __device__ __forceinline__ void cex(int a, int b)
-    {
-        const bool sw = key[b] < key[a];
-        const double ka = key[a], kb = key[b];
-        const int ia = idx[a], ib = idx[b];
-        key[a] = sw ? kb : ka;
-        key[b] = sw ? ka : kb;
-        idx[a] = sw ? ib : ia;
-        idx[b] = sw ? ia : ib;
-    }
-
-    // Batcher's merge-exchange network over all MAXN slots (63 compare-exchanges for 16,
-    // 191 for 32; written out by scripts/gen_sortnet.py so every slot stays a register).
-    // Used by the fast pass to order its first max_n candidates at once instead of max_n
-    // shifting insertions.
-    // Returns false if two kept candidates have exactly equal keys: their order is decided
-    // by id (K:473-476), which the network does not look at -- the caller then hands the
-    // agent to the exact ring search. Exact ties do not occur between generic float
-    // positions; they do on lattices.
-    __device__ __forceinline__ bool sort_all()
-    {
-#define CEX(a, b) cex(a, b);
-        if constexpr (MAXN == 16) {
-            ORCA_SORTNET_16
-        } else {
-            ORCA_SORTNET_32
-        }
-#undef CEX
-        bool tie = false;
-#pragma unroll
-        for (int t = 0; t + 1 < MAXN; ++t) tie = tie || (key[t] == key[t + 1] && idx[t] >= 0 && idx[t + 1] >= 0);
-        return !tie;
-    }
-
     // slot-major neighbour table + count + next step's radius hint
     __device__ __forceinline__ void store(int s, int row, int max_n, int stride, int *__restrict__ nb,
                                           u8 *__restrict__ nb_cnt, float *__restrict__ hint) const
@@ -570,118 +516,15 @@ template <int MAXN> struct TopK {
     }
 };
 
-// Fast pass, one thread per agent in cell-sorted order. It relies on temporal
-// coherence but never on it for correctness: last step every kept neighbour was within
-// `hint`, and nobody moves faster than its max_speed, so this step at least max_n agents
-// are within  b = hint + (my max_speed + fastest max_speed) * dt.  The thread scans the
-// cells covering b once, appends every candidate passing a cheap (FP32) distance test
-// to a small shared-memory buffer, then inserts the buffered candidates into the
-// register list with exact FP64 keys -- all lanes of a warp insert at the same time,
-// where the ring search below inserts whenever any lane finds a closer candidate.
-// The result is accepted only if it is provably the exact list (full, and its last key
-// <= b*b, or b covers the whole neighbor_radius); otherwise the agent goes to the queue
-// of the exact ring search (k_gather): no hint yet, a removed neighbour, a teleported
-// agent, or more than CAP candidates.
-template <typename R, int MAXN, int CAP>
-__global__ void __launch_bounds__(128)
-k_gather_fast(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>::T2 *__restrict__ s_xy,
-              const int *__restrict__ cell_start, const int *__restrict__ s_cell,
-              const int *__restrict__ s_row, const i64 *__restrict__ ids,
-              const typename Vec<R>::T2 *__restrict__ radmax, float *__restrict__ hint,
-              int *__restrict__ nb, u8 *__restrict__ nb_cnt, int *__restrict__ gq, int s0, int s1, int chunk)
-{
-    __shared__ int buf[CAP * 128];
-    const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x; // this launch covers sorted slots [s0, s1)
-    if (s >= min(s1, plan->n)) return;
-    const int row = s_row[s];
-    if (row >= plan->n_owned || P.max_n == 0) {
-        nb_cnt[s] = 0;
-        return;
-    }
-    const float h = hint[row];
-    const double rad2 = P.rad2;
-    const int max_n = P.max_n;
-    const typename Vec<R>::T2 me = s_xy[s];
-    const double mx = (double)me.x, my = (double)me.y;
-    // h == +inf (no list yet, or fewer than max_n in range last step): scan the whole radius
-    double b = (double)h + ((double)radmax[row].y + plan->vmax) * P.dt * (1.0 + 1e-6) + 1e-3;
-    const double T = fmin(b * b, rad2); // NaN-safe: fmin(inf*..., rad2) == rad2
-    const float T_f = __double2float_ru(T * (1.0 + 1e-6));
-
-    const int nx = plan->nx, ny = plan->ny;
-    const int c0 = s_cell[s];
-    const int cx = c0 / ny, cy = c0 - cx * ny;
-    const int r = min(plan->rmax, (int)(sqrt(T) * plan->inv_cell * (1.0 + 1e-9)) + 1);
-    const int gx_lo = max(cx - r, 0), gx_hi = min(cx + r, nx - 1);
-    const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
-    int *my_buf = buf + threadIdx.x;
-    int nbuf = 0;
-    for (int gx = gx_lo; gx <= gx_hi; ++gx) {
-        const int *cs = cell_start + gx * ny;
-        const int e = cs[y_hi + 1];
-        constexpr int kScanUnroll = ORCA_SCAN_UNROLL;
-#pragma unroll kScanUnroll
-        for (int s2 = cs[y_lo]; s2 < e; ++s2) {
-            const typename Vec<R>::T2 q = s_xy[s2];
-            bool pass;
-            if (Fmt<R>::is_f32) {
-                const float dxf = (float)q.x - (float)me.x, dyf = (float)q.y - (float)me.y;
-                pass = dxf * dxf + dyf * dyf <= T_f;
-            } else {
-                const double dx = (double)q.x - mx, dy = (double)q.y - my;
-                pass = dx * dx + dy * dy <= T;
-            }
-            if (pass) {
-                if (nbuf < CAP) my_buf[nbuf * 128] = s2;
-                ++nbuf;
-            }
-        }
-    }
-    bool ok = nbuf <= CAP;
-    TopK<MAXN> top;
-    top.init(max_n);
-    if (ok) {
-        // the first max_n buffered candidates: exact keys straight into the slots, one
-        // sorting network; self and out-of-range candidates become +inf / -1 entries
-        const int off = MAXN - max_n;
-#pragma unroll
-        for (int t = 0; t < MAXN; ++t) {
-            const int e = t - off;
-            if (e >= 0 && e < nbuf) {
-                const int s2 = my_buf[e * 128];
-                const typename Vec<R>::T2 q = s_xy[s2];
-                const double dx = (double)q.x - mx, dy = (double)q.y - my;
-                const double d2 = dx * dx + dy * dy;
-                if (s2 != s && !(d2 > rad2)) {
-                    top.key[t] = d2;
-                    top.idx[t] = s2;
-                    ++top.cnt;
-                }
-            }
-        }
-        ok = top.sort_all();
-        // the rest (a handful: the threshold is tight) by shifting insertion
-        for (int e = max_n; e < nbuf; ++e) {
-            const int s2 = my_buf[e * 128];
-            const typename Vec<R>::T2 q = s_xy[s2];
-            const double dx = (double)q.x - mx, dy = (double)q.y - my;
-            const double d2 = dx * dx + dy * dy;
-            if (s2 == s || d2 > rad2) continue;
-            top.insert(d2, s2, max_n, s_row, ids);
-        }
-        // exact iff nothing outside the buffer can precede the last kept entry
-        ok = ok && (T >= rad2 || (top.cnt == max_n && top.key[MAXN - 1] <= T));
-    }
-    if (ok) {
-        top.store(s, row, max_n, P.stride, nb, nb_cnt, hint);
-    } else {
-        gq[s0 + atomicAdd(&plan->gq_count[chunk], 1)] = s;
-    }
-}
-
-// Fast pass, 32-bit keys. Same contract as k_gather_fast (provably exact list, or the
-// agent goes to the exact ring search), different selection arithmetic: the candidates
-// that pass the FP32 distance test are ranked by ONE 32-bit integer each,
+// Fast pass, one thread per agent in cell-sorted order. It relies on temporal coherence but
+// never on it for correctness: last step every kept neighbour was within `hint`, and nobody
+// moves faster than its max_speed, so this step at least max_n agents are within
+//   b = hint + (my max_speed + fastest max_speed) * dt.
+// The thread scans the cells covering b once and appends every candidate passing an FP32
+// distance test to a small shared-memory buffer. The result is accepted only if it is
+// provably the exact list (see below); otherwise the agent goes to the queue of the exact
+// ring search (k_gather): no hint yet, a removed neighbour, a teleported agent, an exact tie,
+// or more than CAP candidates. The buffered candidates are ranked by ONE 32-bit integer each,
 //     key = (bits of the FP32 squared distance with the low 6 mantissa bits cleared) | slot
 // where slot < 64 is the candidate's position in the shared-memory buffer. Positive
 // floats order like their bit patterns, so the sorting network and the insertion of the
@@ -698,7 +541,7 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
                 const int *__restrict__ cell_start, const int *__restrict__ s_cell,
                 const int *__restrict__ s_row, const typename Vec<R>::T2 *__restrict__ radmax,
                 float *__restrict__ hint, int *__restrict__ nb, u8 *__restrict__ nb_cnt,
-                int *__restrict__ gq, int s0, int s1, int chunk)
+                int *__restrict__ gq, int s0, int s1)
 {
     static_assert(CAP <= 64, "slot must fit the 6 cleared mantissa bits");
     __shared__ int buf[CAP * 128];
@@ -846,21 +689,7 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
             return;
         }
     }
-    gq[s0 + atomicAdd(&plan->gq_count[chunk], 1)] = s;
-}
-
-// every owned agent goes to the exact ring search (fast pass disabled)
-__global__ void __launch_bounds__(256)
-k_enqueue_all(GridPlan *__restrict__ plan, int max_n, const int *__restrict__ s_row,
-              u8 *__restrict__ nb_cnt, int *__restrict__ gq, int s0, int s1, int chunk)
-{
-    const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= min(s1, plan->n)) return;
-    if (s_row[s] >= plan->n_owned || max_n == 0) {
-        nb_cnt[s] = 0;
-        return;
-    }
-    gq[s0 + atomicAdd(&plan->gq_count[chunk], 1)] = s;
+    gq[atomicAdd(&plan->gq_count, 1)] = s;
 }
 
 // Exact ring search for the agents the fast pass queued (all of them on the first step
@@ -874,10 +703,9 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
          const typename Vec<R>::T2 *__restrict__ s_xy, const int *__restrict__ cell_start,
          const int *__restrict__ s_cell, const int *__restrict__ s_row,
          const i64 *__restrict__ ids, float *__restrict__ hint, int *__restrict__ nb,
-         u8 *__restrict__ nb_cnt, const int *__restrict__ gq, int s0, int chunk)
+         u8 *__restrict__ nb_cnt, const int *__restrict__ gq)
 {
-    const int nq = plan->gq_count[chunk];
-    gq += s0; // this chunk's segment of the queue
+    const int nq = plan->gq_count;
     const int nx = plan->nx, ny = plan->ny, rmax = plan->rmax;
     const double cell = plan->cell;
     const double rad2 = P.rad2;
@@ -891,7 +719,6 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
     const int L = min(32, max(1, (nq + total_warps - 1) / total_warps));
     const int lane = threadIdx.x & 31;
     const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-#if ORCA_GATHER_WARP
     // One entry per warp at most: the whole warp searches for it. The lanes stride over the
     // candidate ranges (coalesced), the in-range candidates are compacted into shared memory
     // with their exact FP64 keys, and max_n + 1 rounds of a warp-wide arg-min pick the list in
@@ -1031,7 +858,6 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
         warp_done = !bail;
     }
     if (L == 1 && warp_done) return;
-#endif
     if (lane >= L) return;
     for (int qi = warp * L + lane; qi < nq; qi += total_warps * L) {
         const int s = gq[qi];
@@ -1205,13 +1031,8 @@ __device__ __forceinline__ bool build_constraints(
         }
         const R rj = (R)((double)rc_j.x + P.half_margin);
         R ux, uy, nx, ny;
-#if ORCA_VO_BRANCHY
-        ok_all &= vo_exit<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, (R)P.tau,
-                             (R)P.dt, ux, uy, nx, ny);
-#else
         ok_all &= vo_exit_inv<R>((R)q.x - mex, (R)q.y - mey, mevx - (R)q.z, mevy - (R)q.w, ri + rj, inv_tau,
                                  inv_dt, ux, uy, nx, ny);
-#endif
         const R f = rc_j.y != S(0) ? f1 : f0; // fmat[cls_i, cls_j], _kernels.py:537
         cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
     }
@@ -1271,15 +1092,11 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
     shuffle_smem<MAXN>(perm, THREADS, cnt, problem_seed(plan->frame, ids[row]));
     int bad_j = -1;
     const bool built = build_constraints<S, R>(s, cnt, P, s_nr, nb, perm, THREADS, cons, bad_j);
-#if !ORCA_LP_RUNAHEAD
-    if (!built) {
-#else
     int fail_pos;
     R vx, vy;
     const bool feasible =
         lp2_target_runahead<R, SmemCons<R>>(cons, cnt, dm.z, dm.x, dm.y, fail_pos, vx, vy, live, built);
     if (!built) {
-#endif
         // _kernels.py:542-547 + engine.py:239-245
         if (plan->err_frame < 0) // sticky: only the first failing frame is reported
             atomicMin(&plan->err_pair, ((u64)(unsigned)lrow[row] << 32) | (u64)(unsigned)lrow[s_row[bad_j]]);
@@ -1288,11 +1105,6 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
         integrate_row<S, R>(row, me, (R)me.z, (R)me.w, P, goalpref, pv_out, arrived);
         return;
     }
-#if !ORCA_LP_RUNAHEAD
-    int fail_pos;
-    R vx, vy;
-    const bool feasible = lp2_target<R, false, SmemCons<R>>(cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy);
-#endif
     if (feasible) {
         status[row] = 0;
         failed_at[row] = -1;
@@ -1305,9 +1117,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
     const int q = atomicAdd(&plan->fq_count, 1);
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
-#if ORCA_FB_SPILL
     spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + threadIdx.x, perm, THREADS, 0, 1);
-#endif
 }
 
 // The seeded Fisher-Yates order of every agent (K:43-61), one THREAD per agent. Inside
@@ -1400,7 +1210,6 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
         const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
         const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt); // K:358 / K:378, once
         constexpr int kBuildUnroll = ORCA_BUILD_UNROLL;
-#if ORCA_BUILD_PREFETCH
         // software pipeline: the next neighbour's index and record are requested before this
         // neighbour's ~130-instruction FP64 chain starts, so their (L2) latency hides behind it
         typename Vec<S>::T4 q_next = me;
@@ -1411,10 +1220,8 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
             q_next = rn.pv;
             rc_next = rn.rc;
         }
-#endif
 #pragma unroll kBuildUnroll
         for (int pos = gl; pos < cnt; pos += GL) {
-#if ORCA_BUILD_PREFETCH
             const typename Vec<S>::T4 qv = q_next;
             const typename Vec<S>::T2 rc_j = rc_next;
             if (pos + GL < cnt) {
@@ -1423,21 +1230,10 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
                 q_next = rn.pv;
                 rc_next = rn.rc;
             }
-#else
-            const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
-            const NbRec<S> rj_rec = s_nr[j];
-            const typename Vec<S>::T4 qv = rj_rec.pv;
-            const typename Vec<S>::T2 rc_j = rj_rec.rc;
-#endif
             const R rj = (R)((double)rc_j.x + P.half_margin);
             R ux, uy, nx, ny;
-#if ORCA_VO_BRANCHY
-            ok_mine &= vo_exit<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj,
-                                  (R)P.tau, (R)P.dt, ux, uy, nx, ny);
-#else
             ok_mine &= vo_exit_inv<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj,
                                       inv_tau, inv_dt, ux, uy, nx, ny);
-#endif
             const R f = rc_j.y != S(0) ? f1 : f0;
             cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
         }
@@ -1451,9 +1247,7 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     if (built && !feasible) { // uniform over the group: queue for the least-penetration stage
         if (gl == 0) q = atomicAdd(&plan->fq_count, 1);
         q = __shfl_sync(gmask, q, gshift);
-#if ORCA_FB_SPILL
         spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + g, perm, NG, gl, GL);
-#endif
     }
     if (gl != 0) return;
     if (!built) {
@@ -1477,74 +1271,18 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
 }
 
-// Least-penetration stage for the agents k_solve queued. The stage is a long chain of
-// dependent FP64 operations whose control flow differs from agent to agent, so a full
-// warp of 32 queued agents would serialise ~32 different paths while the machine sits
-// idle for lack of warps. Only `lanes` lanes of every warp take an agent (8 by default):
-// 4x more warps in flight for the same queue and 4x fewer paths to serialise per warp.
-// Shared memory is sized for the active lanes only.
-template <typename S, typename R, int MAXN, int THREADS>
-__global__ void __launch_bounds__(THREADS)
-k_fallback(const GridPlan *__restrict__ plan, StepParams P, int lanes,
-           const NbRec<S> *__restrict__ s_nr, const typename Vec<R>::T4 *__restrict__ s_dm,
-        const int *__restrict__ s_row,
-           const i64 *__restrict__ ids, const int *__restrict__ nb, const u8 *__restrict__ nb_cnt,
-           const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
-           u8 *__restrict__ arrived, const int *__restrict__ fq,
-           const typename Vec<R>::T4 *__restrict__ fq_state)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    typedef typename Vec<R>::T4 R4;
-    const int lane = threadIdx.x & 31;
-    if (lane >= lanes) return;
-    const int AT = (THREADS / 32) * lanes;             // active threads per block
-    const int at = (threadIdx.x >> 5) * lanes + lane;  // this thread's active index
-    R4 *sm_cons = reinterpret_cast<R4 *>(smem_raw);
-    R4 *sm_proj = sm_cons + MAXN * AT;
-    u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * AT);
-    u8 *sm_inv = sm_perm + MAXN * AT;
-
-    const int nq = plan->fq_count;
-    for (int q = blockIdx.x * AT + at; q < nq; q += gridDim.x * AT) {
-        const int s = fq[q];
-        const R4 st = fq_state[q];
-        const int row = s_row[s];
-        const int cnt = nb_cnt[s];
-        const typename Vec<S>::T4 me = s_nr[s].pv;
-        const R4 dm = s_dm[s];
-        u8 *perm = sm_perm + at;
-        u8 *inv = sm_inv + at;
-        SmemCons<R> cons{sm_cons + at, AT};
-        SmemCons<R> proj{sm_proj + at, AT};
-
-        shuffle_smem<MAXN>(perm, AT, cnt, problem_seed(plan->frame, ids[row]));
-        for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * AT] * AT] = (u8)pos;
-        int bad_j;
-        build_constraints<S, R>(s, cnt, P, s_nr, nb, perm, AT, cons, bad_j);
-
-        SmemConsIdent<R> ident{sm_cons + at, inv, AT};
-        R rx, ry;
-        least_penetration<R, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
-            cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry);
-        integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
-    }
-}
-
-// Group-cooperative least-penetration stage: GL adjacent lanes per queued agent. The lanes
-// share the agent's constraints through shared memory, build them in parallel (one vo_exit
-// per lane and round), and split every inner loop of the stage (orca_math.cuh, g_*
-// functions). Against k_fallback this cuts the warp instructions per agent ~3x in dense
-// crowds, where the stage dominates the step.
+// Least-penetration stage for the agents the solve kernels queued, GL adjacent lanes per
+// queued agent. The stage is a long chain of dependent operations whose control flow differs
+// from agent to agent; the lanes of a group share the agent's constraints (handed over by the
+// solve kernel, spill_constraints) through shared memory and split every inner loop of the
+// stage (orca_math.cuh, g_* functions): ~3x fewer warp instructions per agent in dense crowds
+// than one thread per agent, where the stage dominates the step.
 // Two instances are launched back to back and the queue length picks the one that works:
 // GL = ORCA_GL (4) when the queue is long (throughput: 8 agents per warp), GL = ORCA_GL_SHORT
 // (16) when every queued agent can have half a warp to itself (a short queue's time is the
 // latency of one agent's dependent chain: 54 -> 31 us at 1,024 agents, 64 -> 38 us at 16,640).
 template <typename S, typename R, int MAXN, int THREADS, int GL>
-#if ORCA_FB_BLOCKS > 0
-__global__ void __launch_bounds__(THREADS, ORCA_FB_BLOCKS)
-#else
 __global__ void __launch_bounds__(THREADS)
-#endif
 k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 const NbRec<S> *__restrict__ s_nr, const typename Vec<R>::T4 *__restrict__ s_dm,
         const int *__restrict__ s_row,
@@ -1571,7 +1309,6 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
     u8 *sm_inv = sm_perm + MAXN * NG;
 
     const int nq = plan->fq_count;
-#if ORCA_FB_RUNAHEAD
     // every lane makes the same number of passes (a group without an agent rides along
     // disabled), so the run-ahead stage can vote over the whole warp
     for (int base = blockIdx.x * NG; base < nq; base += gridDim.x * NG) {
@@ -1587,23 +1324,12 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
             me = s_nr[s].pv;
             dm = s_dm[s];
         }
-#else
-    for (int q = blockIdx.x * NG + g; q < nq; q += gridDim.x * NG) {
-        const bool enabled = true;
-        const int s = fq[q];
-        const R4 st = fq_state[q];
-        const int row = s_row[s];
-        const int cnt = nb_cnt[s];
-        const typename Vec<S>::T4 me = s_nr[s].pv;
-        const R4 dm = s_dm[s];
-#endif
         u8 *perm = sm_perm + g;
         u8 *inv = sm_inv + g;
         SmemCons<R> cons{sm_cons + g, NG};
         SmemCons<R> proj{sm_proj + g, NG};
         (void)perm;
 
-#if ORCA_FB_SPILL
         if (enabled) { // the half-planes and their order as the solve kernel left them
             const R4 *src = fq_cons + (size_t)q * MAXN;
             const u8 *sp = fq_perm + (size_t)q * MAXN;
@@ -1612,44 +1338,12 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 inv[(int)sp[pos] * NG] = (u8)pos;
             }
         }
-#else
-        if (gl == 0 && enabled) {
-            shuffle_smem<MAXN>(perm, NG, cnt, problem_seed(plan->frame, ids[row]));
-            for (int pos = 0; pos < cnt; ++pos) inv[(int)perm[pos * NG] * NG] = (u8)pos;
-        }
-        __syncwarp(gmask);
-        if (enabled) { // constraints in shuffled order, one vo_exit per lane and round (K:525-541)
-            const R mex = (R)me.x, mey = (R)me.y, mevx = (R)me.z, mevy = (R)me.w;
-            const typename Vec<S>::T2 rc_i = s_nr[s].rc;
-            const R ri = (R)((double)rc_i.x + P.half_margin);
-            const int ci = (int)rc_i.y;
-            const R f0 = (R)(ci ? P.fmat[2] : P.fmat[0]), f1 = (R)(ci ? P.fmat[3] : P.fmat[1]); // no dynamic index: keeps P out of local memory
-            const R inv_tau = div_rn<R>(R(1), (R)P.tau), inv_dt = div_rn<R>(R(1), (R)P.dt);
-            for (int pos = gl; pos < cnt; pos += GL) {
-                const int j = nb[(size_t)perm[pos * NG] * P.stride + s];
-                const NbRec<S> rj_rec = s_nr[j];
-                const typename Vec<S>::T4 qv = rj_rec.pv;
-                const typename Vec<S>::T2 rc_j = rj_rec.rc;
-                const R rj = (R)((double)rc_j.x + P.half_margin);
-                R ux, uy, nx, ny;
-                vo_exit_inv<R>((R)qv.x - mex, (R)qv.y - mey, mevx - (R)qv.z, mevy - (R)qv.w, ri + rj, inv_tau,
-                               inv_dt, ux, uy, nx, ny);
-                const R f = rc_j.y != S(0) ? f1 : f0;
-                cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
-            }
-        }
-#endif
         __syncwarp(gmask);
 
         SmemConsIdent<R> ident{sm_cons + g, inv, NG};
         R rx, ry;
-#if ORCA_FB_RUNAHEAD
         g_least_penetration_ra<R, GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
             cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift, 0xFFFFFFFFu, enabled);
-#else
-        g_least_penetration<R, GL, SmemCons<R>, SmemConsIdent<R>, SmemCons<R>>(
-            cons, ident, proj, cnt, (int)st.z, dm.z, st.x, st.y, rx, ry, gl, gmask, gshift);
-#endif
         if (gl == 0 && enabled) integrate_row<S, R>(row, me, rx, ry, P, goalpref, pv_out, arrived);
         __syncwarp(gmask); // the group's shared memory is reused by the next queue entry
     }
@@ -1703,13 +1397,14 @@ k_compact(GridPlan *__restrict__ plan, const int *__restrict__ keep, const int *
           u8 *__restrict__ cls2, const i8 *__restrict__ st, i8 *__restrict__ st2,
           const i8 *__restrict__ fa, i8 *__restrict__ fa2, const float *__restrict__ hint,
           float *__restrict__ hint2, const int *__restrict__ lrow, int *__restrict__ lrow2,
-          const int *__restrict__ lscan)
+          const int *__restrict__ lscan, const Attr64 *__restrict__ a64, Attr64 *__restrict__ a64_2)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = plan->n;
     if (i >= n) return;
     if (keep[i]) {
         const int d = dst_idx[i];
+        if (a64) a64_2[d] = a64[i];
         // logical row of the survivor: its rank among the surviving logical rows (lscan), or,
         // while storage order still is logical order, simply its new position
         lrow2[d] = lscan ? lscan[lrow[i]] : d;
@@ -1753,11 +1448,13 @@ k_permute_rows(const GridPlan *__restrict__ plan, const int *__restrict__ s_row,
                const i64 *__restrict__ ids, i64 *__restrict__ ids2, const u8 *__restrict__ cls,
                u8 *__restrict__ cls2, const i8 *__restrict__ st, i8 *__restrict__ st2,
                const i8 *__restrict__ fa, i8 *__restrict__ fa2, const float *__restrict__ hint,
-               float *__restrict__ hint2, const int *__restrict__ lrow, int *__restrict__ lrow2)
+               float *__restrict__ hint2, const int *__restrict__ lrow, int *__restrict__ lrow2,
+               const Attr64 *__restrict__ a64, Attr64 *__restrict__ a64_2)
 {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= plan->n) return;
     const int i = s_row[s];
+    if (a64) a64_2[s] = a64[i];
     pv2[s] = pv[i];
     gp2[s] = gp[i];
     rm2[s] = rm[i];
@@ -1804,7 +1501,8 @@ __global__ void __launch_bounds__(256)
 k_strip_pack(GridPlan *__restrict__ plan, const int *__restrict__ sel, const int *__restrict__ sel_idx,
              const typename Vec<S>::T4 *__restrict__ pv, const typename Vec<S>::T4 *__restrict__ goalpref,
              const typename Vec<S>::T2 *__restrict__ radmax, const i64 *__restrict__ ids,
-             const u8 *__restrict__ cls, orca_agent_record *__restrict__ rec, i64 cap)
+             const u8 *__restrict__ cls, orca_agent_record *__restrict__ rec, i64 cap,
+             const Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = plan->n;
@@ -1828,6 +1526,15 @@ k_strip_pack(GridPlan *__restrict__ plan, const int *__restrict__ sel, const int
     r.goal_y = (double)g.y;
     r.id = ids[i];
     r.class_code = (i64)cls[i];
+    if (a64) { // migrants keep the float64 attributes their first owner uploaded
+        const Attr64 a = a64[i];
+        r.radius = a.radius;
+        r.pref_speed = a.pref_speed;
+        r.max_speed = a.max_speed;
+        r.goal_tol = a.goal_tol;
+        r.goal_x = a.goal_x;
+        r.goal_y = a.goal_y;
+    }
     rec[d] = r;
 }
 
@@ -1846,13 +1553,14 @@ k_strip_append(GridPlan *__restrict__ plan, const orca_agent_record *__restrict_
                typename Vec<S>::T4 *__restrict__ pv, typename Vec<S>::T4 *__restrict__ goalpref,
                typename Vec<S>::T2 *__restrict__ radmax, i64 *__restrict__ ids, u8 *__restrict__ cls,
                i8 *__restrict__ status, i8 *__restrict__ failed, float *__restrict__ hint,
-               int *__restrict__ lrow)
+               int *__restrict__ lrow, Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     const int row = plan->n + i;
     lrow[row] = row; // logical rows are dense, so the next logical row is the next physical one
     const orca_agent_record r = rec[i];
+    if (a64) a64[row] = Attr64{r.radius, r.pref_speed, r.max_speed, r.goal_x, r.goal_y, r.goal_tol};
     pv[row] = mk4((S)r.x, (S)r.y, (S)r.vx, (S)r.vy);
     goalpref[row] = mk4((S)r.goal_x, (S)r.goal_y, (S)r.pref_speed, (S)r.goal_tol);
     radmax[row] = mk2((S)r.radius, (S)r.max_speed);
@@ -1947,7 +1655,7 @@ k_strip_append_halo(GridPlan *__restrict__ plan, const orca_slab_header *__restr
                     typename Vec<S>::T4 *__restrict__ pv, typename Vec<S>::T4 *__restrict__ goalpref,
                     typename Vec<S>::T2 *__restrict__ radmax, i64 *__restrict__ ids, u8 *__restrict__ cls,
                     i8 *__restrict__ status, i8 *__restrict__ failed, float *__restrict__ hint,
-                    int *__restrict__ lrow)
+                    int *__restrict__ lrow, Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int count = min(min(hdr->count, cap), cap_rows - plan->n);
@@ -1955,6 +1663,7 @@ k_strip_append_halo(GridPlan *__restrict__ plan, const orca_slab_header *__restr
     const int row = plan->n + i;
     const HaloRec<S> r = rec[i];
     lrow[row] = row;
+    if (a64) a64[row] = Attr64{(double)r.radius, 0.0, 0.0, (double)r.x, (double)r.y, 0.0};
     pv[row] = mk4(r.x, r.y, r.vx, r.vy);
     goalpref[row] = mk4(r.x, r.y, S(0), S(0)); // a ghost is never steered: goal = where it stands
     radmax[row] = mk2(r.radius, S(0));         // (its max_speed is covered by the strip-wide vmax floor)
@@ -1974,7 +1683,7 @@ k_strip_append_slab(GridPlan *__restrict__ plan, const orca_slab_header *__restr
                     typename Vec<S>::T4 *__restrict__ pv, typename Vec<S>::T4 *__restrict__ goalpref,
                     typename Vec<S>::T2 *__restrict__ radmax, i64 *__restrict__ ids, u8 *__restrict__ cls,
                     i8 *__restrict__ status, i8 *__restrict__ failed, float *__restrict__ hint,
-                    int *__restrict__ lrow)
+                    int *__restrict__ lrow, Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int count = min(min(hdr->count, cap), cap_rows - plan->n);
@@ -1982,6 +1691,7 @@ k_strip_append_slab(GridPlan *__restrict__ plan, const orca_slab_header *__restr
     const int row = plan->n + i;
     lrow[row] = row;
     const orca_agent_record r = rec[i];
+    if (a64) a64[row] = Attr64{r.radius, r.pref_speed, r.max_speed, r.goal_x, r.goal_y, r.goal_tol};
     pv[row] = mk4((S)r.x, (S)r.y, (S)r.vx, (S)r.vy);
     goalpref[row] = mk4((S)r.goal_x, (S)r.goal_y, (S)r.pref_speed, (S)r.goal_tol);
     radmax[row] = mk2((S)r.radius, (S)r.max_speed);
@@ -2020,7 +1730,7 @@ k_strip_keep_flags(GridPlan *__restrict__ plan, const u8 *__restrict__ arrived, 
                    const typename Vec<S>::T2 *__restrict__ radmax, const i64 *__restrict__ ids,
                    const u8 *__restrict__ cls, double lo, double hi, orca_slab_header *hdr_l,
                    orca_agent_record *__restrict__ rec_l, orca_slab_header *hdr_r,
-                   orca_agent_record *__restrict__ rec_r, int cap)
+                   orca_agent_record *__restrict__ rec_r, int cap, const Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = plan->n;
@@ -2049,6 +1759,15 @@ k_strip_keep_flags(GridPlan *__restrict__ plan, const u8 *__restrict__ arrived, 
                 r.goal_y = (double)g.y;
                 r.id = ids[i];
                 r.class_code = (i64)cls[i];
+                if (a64) {
+                    const Attr64 e = a64[i];
+                    r.radius = e.radius;
+                    r.pref_speed = e.pref_speed;
+                    r.max_speed = e.max_speed;
+                    r.goal_tol = e.goal_tol;
+                    r.goal_x = e.goal_x;
+                    r.goal_y = e.goal_y;
+                }
                 (x < lo ? rec_l : rec_r)[slot] = r;
                 k = 0;
             } else {
@@ -2216,7 +1935,8 @@ k_import_attrs(int n, const double *__restrict__ radii, const double *__restrict
                const double *__restrict__ maxs, const double *__restrict__ goals,
                const double *__restrict__ gtol, const i64 *__restrict__ cls_in,
                typename Vec<R>::T4 *__restrict__ goalpref, typename Vec<R>::T2 *__restrict__ radmax,
-               u8 *__restrict__ cls, float *__restrict__ hint, GridPlan *__restrict__ plan)
+               u8 *__restrict__ cls, float *__restrict__ hint, GridPlan *__restrict__ plan,
+               Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     // largest max_speed / radius of the crowd: one atomic per warp (a million same-address
@@ -2236,6 +1956,7 @@ k_import_attrs(int n, const double *__restrict__ radii, const double *__restrict
     goalpref[i] = mk4((R)goals[2 * i], (R)goals[2 * i + 1], (R)pref[i], (R)gtol[i]);
     radmax[i] = mk2((R)radii[i], (R)maxs[i]);
     cls[i] = (u8)cls_in[i];
+    if (a64) a64[i] = Attr64{radii[i], pref[i], maxs[i], goals[2 * i], goals[2 * i + 1], gtol[i]};
 }
 
 template <typename R>
@@ -2259,11 +1980,22 @@ k_export_attrs(int n, const typename Vec<R>::T4 *__restrict__ goalpref,
                const typename Vec<R>::T2 *__restrict__ radmax, const u8 *__restrict__ cls,
                double *__restrict__ radii, double *__restrict__ pref, double *__restrict__ maxs,
                double *__restrict__ goals, double *__restrict__ gtol, i64 *__restrict__ cls_out,
-               const int *__restrict__ lrow)
+               const int *__restrict__ lrow, const Attr64 *__restrict__ a64)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int l = lrow[i];
+    cls_out[l] = (i64)cls[i];
+    if (a64) { // the float64 values the host uploaded
+        const Attr64 a = a64[i];
+        goals[2 * l] = a.goal_x;
+        goals[2 * l + 1] = a.goal_y;
+        pref[l] = a.pref_speed;
+        gtol[l] = a.goal_tol;
+        radii[l] = a.radius;
+        maxs[l] = a.max_speed;
+        return;
+    }
     const typename Vec<R>::T4 g = goalpref[i];
     const typename Vec<R>::T2 rm = radmax[i];
     goals[2 * l] = (double)g.x;
@@ -2272,7 +2004,6 @@ k_export_attrs(int n, const typename Vec<R>::T4 *__restrict__ goalpref,
     gtol[l] = (double)g.w;
     radii[l] = (double)rm.x;
     maxs[l] = (double)rm.y;
-    cls_out[l] = (i64)cls[i];
 }
 
 __global__ void __launch_bounds__(256)
@@ -2287,6 +2018,14 @@ k_export_i64(int n, const i64 *__restrict__ in, i64 *__restrict__ out, const int
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[lrow[i]] = in[i];
+}
+
+// kept[logical row] = keep flag of that row in the last compaction (orca_download_last_step_kept)
+__global__ void __launch_bounds__(256)
+k_export_keep(int n, const int *__restrict__ keep, const int *__restrict__ lrow, u8 *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[lrow[i]] = keep[i] ? 1 : 0;
 }
 
 __global__ void __launch_bounds__(256) k_iota(int n, int *__restrict__ out)

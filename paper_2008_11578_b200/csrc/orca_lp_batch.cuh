@@ -49,6 +49,22 @@ template <typename R> struct GlobalProj {
     __device__ __forceinline__ void set(int m, R px, R py, R nx, R ny) { p[m] = mk4(px, py, nx, ny); }
 };
 
+// Tap: the least-penetration stage alone on one constraint list in the GIVEN order
+// (lp.solve_least_penetration, lp.py:168-190 -> K:254-283 with order = identity), one thread.
+template <typename R>
+__global__ void k_least_penetration_tap(int k, int begin, const typename Vec<R>::T4 *__restrict__ cons,
+                                        typename Vec<R>::T4 *__restrict__ proj, double cap, double wx,
+                                        double wy, double *__restrict__ out2)
+{
+    GlobalIdent<R> view{cons};
+    GlobalProj<R> pr{proj};
+    R rx, ry;
+    least_penetration<R, GlobalIdent<R>, GlobalIdent<R>, GlobalProj<R>>(view, view, pr, k, begin, (R)cap, (R)wx,
+                                                                        (R)wy, rx, ry);
+    out2[0] = (double)rx;
+    out2[1] = (double)ry;
+}
+
 // (point, normal) float64 rows -> packed (px, py, nx, ny) in R
 template <typename R>
 __global__ void __launch_bounds__(256)

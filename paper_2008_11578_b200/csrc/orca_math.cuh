@@ -81,22 +81,14 @@ __device__ __forceinline__ uint32_t mod_small(u64 x, uint32_t m)
 // Returns false only for exactly coincident centres. (ux,uy) is the shortest
 // displacement of the relative velocity to the VO boundary, (nx,ny) the outward
 // unit normal there.
-#ifndef ORCA_VO_BRANCHY
-#define ORCA_VO_BRANCHY 0 // 1: the reference's control flow (A/B switch)
-#endif
-template <typename R>
-__device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
-                                                R &ux, R &uy, R &nx, R &ny);
 //
-// Two implementations with identical results (every value that reaches an output is
-// produced by the same operations on the same operands):
-//   vo_exit_branchy  the reference's control flow, one branch per case;
-//   vo_exit          the overlap / cut-off-arc / tangent-leg cases merged into ONE
-//                    straight-line sequence (one square root, two divisions, selects),
-//                    because in a warp of 32 agent-neighbour pairs ~28 lanes take the arc
-//                    and ~3 a leg, and the branchy form runs both paths back to back
-//                    (profiles/r01_notes.md). Only the two measure-zero cases (coincident
-//                    centres, |w|^2 < 1e-24) still branch.
+// The reference branches per case (overlap K:357-376, cut-off arc K:395-401, tangent leg
+// K:403-419). Here the three cases are merged into ONE straight-line sequence (one square
+// root, two divisions, selects): in a warp of 32 agent-neighbour pairs ~28 lanes take the arc
+// and ~3 a leg, and a branchy form runs both paths back to back (profiles/r01_notes.md). Every
+// value that reaches an output is produced by the same operations on the same operands as in
+// the reference, so FP64 stays bit-identical (tests/test_gpu_kat.py: 4,004 reference exits).
+// Only the two measure-zero cases (coincident centres, |w|^2 < 1e-24) still branch.
 // vo_exit_inv takes 1/tau and 1/dt (K:358, K:378: `inv = 1.0 / tau`) so that callers with a
 // loop over neighbours divide once per kernel, not per neighbour; vo_exit computes them.
 template <typename R>
@@ -107,9 +99,6 @@ template <typename R>
 __device__ __forceinline__ bool vo_exit(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
                                         R &ux, R &uy, R &nx, R &ny)
 {
-#if ORCA_VO_BRANCHY
-    return vo_exit_branchy<R>(rpx, rpy, rvx, rvy, comb_r, tau, dt, ux, uy, nx, ny);
-#endif
     return vo_exit_inv<R>(rpx, rpy, rvx, rvy, comb_r, div_rn<R>(R(1), tau), div_rn<R>(R(1), dt), ux, uy, nx, ny);
 }
 
@@ -165,93 +154,6 @@ __device__ __forceinline__ bool vo_exit_inv(R rpx, R rpy, R rvx, R rvy, R comb_r
     return true;
 }
 
-template <typename R>
-__device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R comb_r, R tau, R dt,
-                                                R &ux, R &uy, R &nx, R &ny)
-{
-    if (rpx == R(0) && rpy == R(0)) {
-        ux = uy = nx = ny = R(0);
-        return false;
-    }
-    const R d2 = rpx * rpx + rpy * rpy;
-    const R r2 = comb_r * comb_r;
-
-    if (d2 < r2) { // overlapping: disc of the dt horizon, K:357-376
-        const R inv = div_rn<R>(R(1), dt);
-        const R cx = rpx * inv, cy = rpy * inv;
-        const R rr = comb_r * inv;
-        const R wx = rvx - cx, wy = rvy - cy;
-        const R wl2 = wx * wx + wy * wy;
-        R hx, hy, wl;
-        if (wl2 < R(1e-24)) {
-            const R d = sqrt_rn<R>(d2);
-            hx = div_rn<R>(-rpx, d);
-            hy = div_rn<R>(-rpy, d);
-            wl = R(0);
-        } else {
-            wl = sqrt_rn<R>(wl2);
-            hx = div_rn<R>(wx, wl);
-            hy = div_rn<R>(wy, wl);
-        }
-        const R s = rr - wl;
-        ux = s * hx;
-        uy = s * hy;
-        nx = hx;
-        ny = hy;
-        return true;
-    }
-
-    const R inv = div_rn<R>(R(1), tau);
-    const R cx = rpx * inv, cy = rpy * inv;
-    const R rr = comb_r * inv;
-    const R wx = rvx - cx, wy = rvy - cy;
-    const R wl2 = wx * wx + wy * wy;
-    const R dot_wp = wx * rpx + wy * rpy;
-
-    if (wl2 < R(1e-24)) { // at the cut-off disc centre, K:387-393
-        const R d = sqrt_rn<R>(d2);
-        const R hx = div_rn<R>(-rpx, d), hy = div_rn<R>(-rpy, d);
-        ux = rr * hx;
-        uy = rr * hy;
-        nx = hx;
-        ny = hy;
-        return true;
-    }
-
-    if (dot_wp < R(0) && dot_wp * dot_wp > r2 * wl2) { // cut-off arc, K:395-401
-        const R wl = sqrt_rn<R>(wl2);
-        const R hx = div_rn<R>(wx, wl), hy = div_rn<R>(wy, wl);
-        const R s = rr - wl;
-        ux = s * hx;
-        uy = s * hy;
-        nx = hx;
-        ny = hy;
-        return true;
-    }
-
-    // tangent leg, side by the sign of cross(rel_pos, w), K:403-419
-    const R leg = sqrt_rn<R>(d2 - r2);
-    R dx, dy;
-    if (rpx * wy - rpy * wx > R(0)) {
-        dx = div_rn<R>(rpx * leg - rpy * comb_r, d2);
-        dy = div_rn<R>(rpx * comb_r + rpy * leg, d2);
-    } else {
-        dx = div_rn<R>(-(rpx * leg + rpy * comb_r), d2);
-        dy = div_rn<R>(rpx * comb_r - rpy * leg, d2);
-    }
-    const R t = rvx * dx + rvy * dy;
-    ux = t * dx - rvx;
-    uy = t * dy - rvy;
-    R mx = -dy, my = dx;
-    if (mx * rpx + my * rpy > R(0)) {
-        mx = -mx;
-        my = -my;
-    }
-    nx = mx;
-    ny = my;
-    return true;
-}
-
 // ---------------------------------------------------------------------------
 // LP core, written against a constraint "view" V:
 //     V::get(pos, px, py, nx, ny)   constraint at position `pos` of the order
@@ -264,12 +166,6 @@ __device__ __forceinline__ bool vo_exit_branchy(R rpx, R rpy, R rvx, R rvy, R co
 // experiment switches (see profiles/): defaults are the measured-best variants
 #ifndef ORCA_RA_SCAN_UNROLL
 #define ORCA_RA_SCAN_UNROLL 1 // positions per iteration of the run-ahead scan loops (1, 2, 4 measured: no difference)
-#endif
-#ifndef ORCA_LP1DIR_NOEXIT
-#define ORCA_LP1DIR_NOEXIT 0
-#endif
-#ifndef ORCA_PAIRS_UNROLLED
-#define ORCA_PAIRS_UNROLLED 1
 #endif
 
 // K:74-119. `zz` shifts every constraint point by -zz*normal (the z-relaxed set
@@ -450,22 +346,6 @@ __device__ __forceinline__ bool lp1_dir(const P &proj, int upto, R cap, R ox, R 
     const R sq = sqrt_rn<R>(disc);
     R t_left = -pd - sq;
     R t_right = -pd + sq;
-#if ORCA_LP1DIR_NOEXIT
-    bool bad = false;
-#pragma unroll 4
-    for (int j = 0; j < upto; ++j) {
-        R qx, qy, mx, my;
-        proj.get(j, qx, qy, mx, my);
-        const R a = dx * mx + dy * my;
-        const R b = (qx - px) * mx + (qy - py) * my;
-        const bool par = R(-ORCA_PARALLEL_EPS) <= a && a <= R(ORCA_PARALLEL_EPS);
-        bad = bad || (par && b > R(0));
-        const R t = div_rn<R>(b, a); // unused when par
-        if (!par && a > R(0) && t > t_left) t_left = t;
-        if (!par && !(a > R(0)) && t < t_right) t_right = t;
-    }
-    if (bad || t_left > t_right) return false;
-#else
     for (int j = 0; j < upto; ++j) {
         R qx, qy, mx, my;
         proj.get(j, qx, qy, mx, my);
@@ -483,7 +363,6 @@ __device__ __forceinline__ bool lp1_dir(const P &proj, int upto, R cap, R ox, R 
         }
         if (t_left > t_right) return false;
     }
-#endif
     const R t = (dx * ox + dy * oy) > R(0) ? t_right : t_left;
     rx = px + t * dx;
     ry = py + t * dy;
@@ -527,7 +406,6 @@ __device__ __forceinline__ void lp3_minmax(const V &view, P &proj, int k, int be
         const R viol = (cpx - vx) * cnx + (cpy - vy) * cny;
         if (viol > dist) {
             int m = 0;
-#if ORCA_PAIRS_UNROLLED
 #pragma unroll 2
             for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
                 R jpx, jpy, jnx, jny;
@@ -544,21 +422,6 @@ __device__ __forceinline__ void lp3_minmax(const V &view, P &proj, int k, int be
                     ++m;
                 }
             }
-#else
-            for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
-                R jpx, jpy, jnx, jny;
-                view.get(j_pos, jpx, jpy, jnx, jny);
-                const R mx = jnx - cnx;
-                const R my = jny - cny;
-                const R ml2 = mx * mx + my * my;
-                if (ml2 < R(1e-24)) continue; // same normal: no half-plane induced (K:231-235)
-                const R rhs = jpx * jnx + jpy * jny - cpx * cnx - cpy * cny;
-                const R ml = sqrt_rn<R>(ml2);
-                proj.set(m, div_rn<R>(mx * rhs, ml2), div_rn<R>(my * rhs, ml2), div_rn<R>(mx, ml),
-                         div_rn<R>(my, ml));
-                ++m;
-            }
-#endif
             R nvx, nvy;
             if (lp2_dir<R, P>(proj, m, cap, cnx, cny, nvx, nvy)) {
                 vx = nvx;

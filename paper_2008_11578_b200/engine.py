@@ -42,12 +42,17 @@ COLLISION_TOLERANCE = 1e-6          # engine.py:36 (applied inside k_min_sep)
 DEFAULT_WORK_UNIT_STEPS = 4096      # engine.py:37
 MASK64 = (1 << 64) - 1
 
-# "mixed" (default): FP32 device state, FP64 arithmetic -- the reference's branches and
-#   results for float32-representable inputs, rounded once to FP32 on store.
-# "f32": FP32 state and arithmetic (fastest; ill-conditioned LPs may differ > 1e-4 m/s).
-# "f64": FP64 state and arithmetic, bit-identical to the reference on any input.
+# "f64" (default of every reference-shaped entry point: step, run, the CLI): FP64 state and
+#   arithmetic, bit-identical to the reference on ANY float64 input -- trajectories, arrival
+#   frames and CSV files equal the reference's byte for byte.
+# "mixed" (opt-in; what bench.py times): FP32 device state, FP64 arithmetic -- the reference's
+#   branches and results for float32-representable inputs, rounded once to FP32 on store.
+#   float64 inputs that float32 cannot hold are ROUNDED on upload: positions then differ from
+#   the reference's by up to an FP32 ulp, and two distinct float64 centres closer than that
+#   collapse (the step then raises the coincident-centres error).
+# "f32" (opt-in): FP32 state and arithmetic (fastest; ill-conditioned LPs may differ > 1e-4 m/s).
 # Binning and neighbour-ordering keys are FP64 in every mode.
-DEFAULT_PRECISION = os.environ.get("ORCA_B200_PRECISION", "mixed")
+DEFAULT_PRECISION = os.environ.get("ORCA_B200_PRECISION", "f64")
 
 
 def _mix64(z: int) -> int:
@@ -267,6 +272,13 @@ class Simulation:
         self._raise_like_reference(self._L.orca_download_last_step_pv(self._h, int(n_pre), ptr(pos), ptr(vel)))
         return pos, vel
 
+    def last_step_kept(self, n_pre: int) -> np.ndarray:
+        """bool[n_pre]: which storage rows of the last step's input survived its arrival
+        removal (orca_download_last_step_kept)."""
+        kept = np.empty(int(n_pre), dtype=np.uint8)
+        self._raise_like_reference(self._L.orca_download_last_step_kept(self._h, int(n_pre), ptr(kept)))
+        return kept.astype(bool)
+
     def ids(self):
         n = self._L_active()
         ids = np.empty(n, dtype=np.int64)
@@ -414,8 +426,9 @@ def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
     per-agent attributes a step never changes (ids, radii, speeds, goals, tolerances,
     classes) stay resident on the device between calls when `state` carries the very
     array objects the previous call returned (the usual `state, m = step(state, cfg)`
-    loop) and nobody arrived; the returned state then shares those arrays with the
-    input instead of copying them. Pass reuse_resident=False if you mutate them in
+    loop); the returned state shares those arrays with the input when nobody arrived and
+    otherwise holds the input's own float64 values, compacted (the device keeps float64
+    copies of the attributes next to an FP32 state, so nothing comes back rounded). Pass reuse_resident=False if you mutate them in
     place between calls."""
     del worker_count, work_unit_steps  # results do not depend on them (engine.py:7-8)
     t0 = _time.perf_counter()
@@ -439,10 +452,13 @@ def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
     pos, vel, info = sim.advance_host(state.positions, state.velocities, state.frame)
     frame = int(info.frame)
     d2h = 32 * n
-    if int(info.removed_agents) == 0 and reuse_resident:
-        new_static = static
+    if int(info.removed_agents) == 0:
+        new_static = static if reuse_resident else tuple(np.array(a, copy=True) for a in static)
     else:
-        new_static = sim.attributes()       # compacted (or not to be shared with the input)
+        # compacted on the device (engine.py:288-294) and read back from its float64 copies of
+        # what the host uploaded -- bit for bit the caller's own values in every precision mode
+        # (3 ms for a million agents; compacting seven arrays with a mask on the host takes 20+)
+        new_static = sim.attributes()
         d2h += 72 * int(info.active_agents)
     new_state = type(state)(frame=frame, time=frame * float(config.dt), positions=pos, velocities=vel,
                             rng_state=getattr(state, "rng_state", None),

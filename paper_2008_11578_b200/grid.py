@@ -1,0 +1,100 @@
+"""Neighbour index of the reference (pkg/src/orcasim/grid.py) on the device.
+
+    rebuild(agents, cell_size) -> UniformGrid               grid.py:34-47
+    query_neighbors(grid, agents, self_id, radius, max_count)   grid.py:50-83
+
+The reference keeps a sparse dict of cells and scans the ring of cells covering the
+radius; the result -- the up to max_count nearest agents within `radius`, ascending by
+(distance, id) -- is defined geometrically and does not depend on the cell size
+(pkg/tests/test_grid.py:101). Here the query runs the step's own neighbour search
+(k_gather_fast32 + k_gather through orca_neighbor_query) for EVERY agent at once and caches
+the lists on the grid object, so a loop over self_id costs one device call. `cells` / `cell_of`
+are provided for inspection with the reference's meaning.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import ORCA_MAX_NEIGHBORS, check, load, ptr
+
+__all__ = ["UniformGrid", "rebuild", "query_neighbors", "neighbor_lists"]
+
+ORIGIN = (0.0, 0.0)
+
+
+def neighbor_lists(ids, positions, radius: float, max_count: int, device: int = 0):
+    """(rows int64[n, max_count] padded with -1, count int64[n]) for every agent
+    (_kernels.py:450-490 over the whole crowd)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 2)
+    n = ids.shape[0]
+    rows = np.full((n, max(int(max_count), 1)), -1, dtype=np.int64)
+    count = np.zeros(n, dtype=np.int64)
+    check(load().orca_neighbor_query(device, n, ptr(ids), ptr(pos), float(radius), int(max_count),
+                                     ptr(rows), ptr(count)))
+    return rows[:, :int(max_count)], count
+
+
+@dataclass
+class UniformGrid:
+    cell_size: float
+    origin: tuple = ORIGIN
+    cells: dict = field(default_factory=dict)
+    population: int = 0
+    _lists: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def cell_of(self, position) -> tuple:
+        return (int(math.floor((position[0] - self.origin[0]) / self.cell_size)),
+                int(math.floor((position[1] - self.origin[1]) / self.cell_size)))
+
+
+def rebuild(agents, cell_size: float) -> UniformGrid:
+    """Fresh grid with every agent in exactly one cell (ids in encounter order)."""
+    cell_size = float(cell_size)
+    if not np.isfinite(cell_size) or cell_size <= 0:
+        raise ValueError(f"cell_size must be positive, got {cell_size!r}")
+    grid = UniformGrid(cell_size=cell_size)
+    agents = list(agents)
+    for agent in agents:
+        if not (np.isfinite(agent.position[0]) and np.isfinite(agent.position[1])):
+            raise ValueError(f"agent {agent.id}: non-finite position")
+    if agents:
+        pos = np.array([a.position for a in agents], dtype=np.float64).reshape(-1, 2)
+        cx = np.floor((pos[:, 0] - grid.origin[0]) / cell_size).astype(np.int64)
+        cy = np.floor((pos[:, 1] - grid.origin[1]) / cell_size).astype(np.int64)
+        for agent, ix, iy in zip(agents, cx.tolist(), cy.tolist()):
+            grid.cells.setdefault((ix, iy), []).append(agent.id)
+    grid.population = len(agents)
+    return grid
+
+
+def query_neighbors(grid: UniformGrid, agents, self_id, radius: float, max_count: int, *,
+                    device: int = 0) -> list:
+    """Up to max_count nearest agents within `radius` of agent self_id, excluding self,
+    sorted ascending by distance then id (grid.py:50-83)."""
+    radius = float(radius)
+    if radius <= 0:
+        raise ValueError(f"radius must be positive, got {radius!r}")
+    if max_count < 0:
+        raise ValueError(f"max_count must be >= 0, got {max_count}")
+    agents = list(agents)
+    row_of = {a.id: i for i, a in enumerate(agents)}
+    if self_id not in row_of:
+        raise KeyError(f"unknown agent id {self_id!r}")
+    if max_count == 0:
+        return []
+    if max_count > ORCA_MAX_NEIGHBORS:
+        raise ValueError(f"max_count {max_count} exceeds the device limit of {ORCA_MAX_NEIGHBORS} neighbours")
+    pos = np.array([a.position for a in agents], dtype=np.float64).reshape(-1, 2)
+    key = (radius, int(max_count), device, pos.tobytes(), tuple(row_of))
+    cached = grid._lists.get("key") == key
+    if not cached:
+        ids = np.array([a.id for a in agents], dtype=np.int64)
+        grid._lists = {"key": key, "lists": neighbor_lists(ids, pos, radius, max_count, device)}
+    rows, count = grid._lists["lists"]
+    i = row_of[self_id]
+    return [agents[j] for j in rows[i, :count[i]].tolist()]

@@ -15,36 +15,60 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from enum import IntEnum
+from enum import Enum
 
 import numpy as np
 
 from ._lib import ORCA_F64, ORCA_MIXED, check, load, precision_code, ptr
 
 __all__ = ["HalfPlaneConstraint", "LpProblem", "LpResult", "LpStatus", "LpBatch",
-           "shuffle_order", "solve_range", "solve_batch", "solve_closest_point"]
+           "shuffle_order", "solve_range", "solve_batch", "solve_closest_point",
+           "solve_least_penetration", "DEFAULT_WORK_UNIT_STEPS"]
+
+DEFAULT_WORK_UNIT_STEPS = 64        # lp.py:28 (accepted and ignored: results do not depend on it)
 
 MASK64 = (1 << 64) - 1
 
 
-class LpStatus(IntEnum):
-    FEASIBLE = 0
-    FALLBACK_USED = 1
+class LpStatus(Enum):
+    FEASIBLE = "feasible"
+    FALLBACK_USED = "fallback_used"
+
+
+_STATUS_OF_CODE = (LpStatus.FEASIBLE, LpStatus.FALLBACK_USED)     # _kernels.py: FEASIBLE = 0, FALLBACK_USED = 1
 
 
 @dataclass
 class HalfPlaneConstraint:
-    """Velocities v with dot(v - point, normal) >= 0 are permitted (lp.py)."""
+    """One half-plane of permitted velocities: `point` on the boundary line, `normal` the unit
+    normal into the permitted side -- v is allowed iff dot(v - point, normal) >= 0 (lp.py:47-64)."""
+
     point: np.ndarray
     normal: np.ndarray
+
+    def __post_init__(self):
+        self.point = np.asarray(self.point, dtype=float)
+        self.normal = np.asarray(self.normal, dtype=float)
+
+    def satisfies(self, velocity, slack: float = 0.0) -> bool:
+        v = np.asarray(velocity, dtype=float)
+        return float(np.dot(v - self.point, self.normal)) >= -slack
 
 
 @dataclass
 class LpProblem:
+    """Closest-point problem: constraints, desired velocity, speed cap and the seed that fixes
+    the constraint insertion order (lp.py:67-80)."""
+
     constraints: list
-    target: tuple
+    target: np.ndarray
     speed_cap: float
     shuffle_seed: int = 0
+
+    def __post_init__(self):
+        self.target = np.asarray(self.target, dtype=float)
+        self.speed_cap = float(self.speed_cap)
+        self.shuffle_seed = int(self.shuffle_seed) & MASK64
 
 
 @dataclass
@@ -52,6 +76,10 @@ class LpResult:
     velocity: np.ndarray
     status: LpStatus
     failed_at: int | None = None
+
+    @property
+    def feasible(self) -> bool:
+        return self.status is LpStatus.FEASIBLE
 
 
 def _mix64(z: int) -> int:
@@ -179,9 +207,15 @@ def _validate_problem(problem, label=""):
 
 def solve_batch(problems, worker_count: int = 1, work_unit_steps: int = 64, *,
                 precision="f64", device: int = 0):
-    """lp.solve_batch (lp.py:263-291): validate, pack to CSR, solve on the GPU."""
-    del worker_count, work_unit_steps
+    """lp.solve_batch (lp.py:263-291): validate, pack to CSR, solve on the GPU. The output is
+    index-aligned with the input; worker_count / work_unit_steps are validated like the
+    reference's and otherwise ignored (its results are independent of both)."""
+    if worker_count < 1:
+        raise ValueError(f"worker_count must be >= 1, got {worker_count}")
+    del work_unit_steps
     n = len(problems)
+    if n == 0:
+        return []
     coff = np.zeros(n + 1, dtype=np.int64)
     parts = []
     for i, p in enumerate(problems):
@@ -197,10 +231,31 @@ def solve_batch(problems, worker_count: int = 1, work_unit_steps: int = 64, *,
         tgt[i], caps[i] = target, cap
         seeds[i] = np.uint64(problems[i].shuffle_seed & MASK64)
     out_v, status, failed = solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision, device)
-    return [LpResult(out_v[i].copy(), LpStatus(int(status[i])),
+    return [LpResult(out_v[i].copy(), _STATUS_OF_CODE[int(status[i])],
                      None if status[i] == 0 else int(failed[i])) for i in range(n)]
 
 
 def solve_closest_point(problem, *, precision="f64", device: int = 0) -> LpResult:
     """lp.solve_closest_point (lp.py:152-165) for one problem."""
     return solve_batch([problem], precision=precision, device=device)[0]
+
+
+def solve_least_penetration(constraints, speed_cap, start_index=0, warm_start=(0.0, 0.0), *,
+                            precision="f64", device: int = 0) -> np.ndarray:
+    """Velocity minimising the worst signed constraint violation (clamped at zero) within the
+    speed disc; ties broken by proximity to warm_start (lp.py:168-190 -> _kernels.py:254-283,
+    constraints in the given order). warm_start is assumed to satisfy constraints[:start_index]."""
+    cap = float(speed_cap)
+    if not np.isfinite(cap) or cap <= 0.0:
+        raise ValueError(f"speed_cap must be positive and finite, got {cap!r}")
+    warm = np.asarray(warm_start, dtype=float).reshape(2)
+    if not np.all(np.isfinite(warm)):
+        raise ValueError("warm_start is non-finite")
+    pts, nrm = _validate_constraints(constraints)
+    k = len(constraints)
+    if not 0 <= start_index <= k:
+        raise ValueError(f"start_index {start_index} out of range for {k} constraints")
+    out = np.empty(2)
+    check(load().orca_least_penetration(device, _lp_precision(precision), k, ptr(pts), ptr(nrm), cap,
+                                        int(start_index), float(warm[0]), float(warm[1]), ptr(out)))
+    return out

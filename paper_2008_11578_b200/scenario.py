@@ -30,6 +30,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._lib import ORCA_MAX_NEIGHBORS
+
 from .types import (DEFAULT_CLASS_PARAMS, DEFAULTS, AgentClass, ClassParams, FrameLog,
                     ResponsibilityMatrix, ScenarioConfig)
 
@@ -185,6 +187,10 @@ def scenario_from_dict(data: dict, source: str = "<dict>") -> ScenarioConfig:
     max_neighbors = data.get("max_neighbors", DEFAULTS["max_neighbors"])
     if not _is_int(max_neighbors) or max_neighbors < 0:
         raise ScenarioError(f"{source}.max_neighbors: expected an integer >= 0")
+    if max_neighbors > ORCA_MAX_NEIGHBORS:
+        # the reference accepts any count; the device keeps an agent's list in registers
+        raise ScenarioError(f"{source}.max_neighbors: {max_neighbors} exceeds the {ORCA_MAX_NEIGHBORS} "
+                            "neighbours per agent this GPU build supports")
     seed = data.get("seed", DEFAULTS["seed"])
     if not _is_int(seed):
         raise ScenarioError(f"{source}.seed: expected an integer")

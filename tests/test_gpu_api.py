@@ -1,0 +1,102 @@
+"""The reference's OBJECT-level operators through the host wrappers of this package
+(orca.py, grid.py, lp.py), against outputs of the reference itself
+(tests/golden/api_cases.npz, written by oracle/gen_golden.gen_api from orcasim):
+
+    gather_constraints / build_orca_halfplane / compute_vo_exit   pkg/src/orcasim/orca.py:145-196
+    rebuild / query_neighbors                                      pkg/src/orcasim/grid.py:34-83
+    solve_least_penetration                                        pkg/src/orcasim/lp.py:168-190
+
+Everything numerical runs on the device (orca_vo_exit_batch, orca_neighbor_query,
+orca_least_penetration); FP64, so the comparison is array_equal."""
+
+import numpy as np
+import pytest
+
+from helpers import load_golden
+from paper_2008_11578_b200 import (AgentClass, AgentState, HalfPlaneConstraint, ResponsibilityMatrix, VoExit,
+                                   build_orca_halfplane, compute_vo_exit, gather_constraints, query_neighbors,
+                                   rebuild, solve_least_penetration)
+from paper_2008_11578_b200.grid import neighbor_lists
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def crowd():
+    g = load_golden("api_cases.npz")
+    agents = [AgentState(id=int(g["ids"][i]), position=g["positions"][i], velocity=g["velocities"][i],
+                         radius=float(g["radii"][i]), pref_speed=1.0, max_speed=2.0, goal=g["positions"][i] + 1.0,
+                         agent_class=AgentClass(int(g["class_codes"][i]))) for i in range(g["ids"].shape[0])]
+    return g, agents
+
+
+def test_rebuild_and_query_neighbors_equal_the_reference(crowd):
+    g, agents = crowd
+    grid = rebuild(agents, 4.0)
+    assert grid.population == int(g["grid_population"])
+    assert np.array_equal(np.array(sorted(grid.cells), dtype=np.int64), g["grid_cells"])
+    assert grid.cell_of(agents[0].position) in grid.cells
+    for key in [k for k in g if k.startswith("nb_ids_")]:
+        radius, max_count = float(key.split("_r")[1].split("_m")[0]), int(key.split("_m")[1])
+        for i in (0, 4, 5, 77, len(agents) - 1):
+            nb = query_neighbors(grid, agents, agents[i].id, radius, max_count)
+            want = g[key][i]
+            assert [b.id for b in nb] == [int(x) for x in want[want >= 0]], (key, i)
+        rows, count = neighbor_lists(g["ids"], g["positions"], radius, max_count)     # every agent at once
+        got = np.where(rows >= 0, g["ids"][np.maximum(rows, 0)], -1)
+        assert np.array_equal(got, g[key]) and np.array_equal(count, (g[key] >= 0).sum(axis=1))
+    assert query_neighbors(grid, agents, agents[0].id, 6.0, 0) == []
+    with pytest.raises(KeyError):
+        query_neighbors(grid, agents, -12345, 6.0, 4)
+    with pytest.raises(ValueError, match="radius must be positive"):
+        query_neighbors(grid, agents, agents[0].id, 0.0, 4)
+    with pytest.raises(ValueError, match="max_count must be >= 0"):
+        query_neighbors(grid, agents, agents[0].id, 1.0, -1)
+    with pytest.raises(ValueError, match="cell_size must be positive"):
+        rebuild(agents, 0.0)
+
+
+def test_gather_constraints_equal_the_reference(crowd):
+    g, agents = crowd
+    grid = rebuild(agents, 4.0)
+    matrix = ResponsibilityMatrix.default()
+    for i, a in enumerate(agents):
+        nb = query_neighbors(grid, agents, a.id, 6.0, 16)
+        cs = gather_constraints(a, nb, matrix, 2.0, 0.1)
+        assert len(cs) == int(g["cons_cnt"][i])
+        for t, c in enumerate(cs):
+            assert isinstance(c, HalfPlaneConstraint)
+            assert np.array_equal(c.point, g["cons_pts"][i, t]) and np.array_equal(c.normal, g["cons_nrm"][i, t]), (i, t)
+    a, b = agents[4], agents[5]                                   # the overlapping pair
+    one = build_orca_halfplane(a, b, 0.5, 2.0, 0.1)
+    ex = compute_vo_exit(b.position - a.position, a.velocity - b.velocity, a.radius + b.radius, 2.0, 0.1)
+    assert isinstance(ex, VoExit) and np.array_equal(one.point, a.velocity + 0.5 * ex.u)
+    assert np.array_equal(one.normal, ex.normal)
+    with pytest.raises(ValueError, match="cannot avoid itself"):
+        build_orca_halfplane(a, a, 0.5, 2.0, 0.1)
+    with pytest.raises(ValueError, match="outside"):
+        build_orca_halfplane(a, b, 1.5, 2.0, 0.1)
+    with pytest.raises(ValueError, match="coincident agent centers"):
+        compute_vo_exit((0.0, 0.0), (1.0, 0.0), 1.0, 2.0, 0.1)
+    with pytest.raises(ValueError, match="must all be positive"):
+        compute_vo_exit((1.0, 0.0), (1.0, 0.0), 1.0, 0.0, 0.1)
+    twin = AgentState(id=10**6, position=a.position, velocity=a.velocity, radius=0.3, pref_speed=1.0, max_speed=2.0,
+                      goal=a.goal)
+    with pytest.raises(ValueError, match=f"neighbor {10**6}: coincident"):
+        gather_constraints(a, [b, twin], matrix, 2.0, 0.1)
+
+
+def test_solve_least_penetration_equals_the_reference():
+    g = load_golden("api_cases.npz")
+    for c in range(g["lp_k"].shape[0]):
+        k = int(g["lp_k"][c])
+        cs = [HalfPlaneConstraint(g["lp_pts"][c, t], g["lp_nrm"][c, t]) for t in range(k)]
+        v = solve_least_penetration(cs, float(g["lp_cap"][c]), start_index=int(g["lp_start"][c]),
+                                    warm_start=g["lp_warm"][c])
+        assert np.array_equal(v, g["lp_out"][c]), c
+    with pytest.raises(ValueError, match="speed_cap must be positive"):
+        solve_least_penetration([], 0.0)
+    with pytest.raises(ValueError, match="out of range"):
+        solve_least_penetration([], 1.0, start_index=1)
+    with pytest.raises(ValueError, match="warm_start is non-finite"):
+        solve_least_penetration([], 1.0, warm_start=(np.nan, 0.0))

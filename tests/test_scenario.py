@@ -125,3 +125,45 @@ def test_sha_fixture_is_well_formed():
         assert len(rec["trajectories"]) == 64 and len(rec["agents"]) == 64
         assert hashlib.sha256(b"").hexdigest() != rec["trajectories"]
     assert AgentClass.from_label("vehicle") == AgentClass.VEHICLE
+
+
+def test_lp_object_api_matches_the_reference_schema():
+    """LpStatus values, LpResult.feasible, HalfPlaneConstraint.satisfies and the LpProblem
+    coercions of pkg/src/orcasim/lp.py:42-91; solve_batch validates worker_count (lp.py:268-269)."""
+    import numpy as np
+    import pytest
+    from paper_2008_11578_b200 import HalfPlaneConstraint, LpProblem, LpResult, LpStatus, solve_batch
+    assert LpStatus.FEASIBLE.value == "feasible" and LpStatus.FALLBACK_USED.value == "fallback_used"
+    assert LpResult(np.zeros(2), LpStatus.FEASIBLE).feasible
+    assert not LpResult(np.zeros(2), LpStatus.FALLBACK_USED, 3).feasible
+    c = HalfPlaneConstraint((1, 0), (1, 0))
+    assert c.point.dtype == float and c.satisfies((1.5, 9.0)) and not c.satisfies((0.5, 0.0))
+    assert c.satisfies((0.9, 0.0), slack=0.2)
+    p = LpProblem([c], (3, 4), "2", shuffle_seed=-1)
+    assert p.target.dtype == float and p.speed_cap == 2.0 and p.shuffle_seed == (1 << 64) - 1
+    with pytest.raises(ValueError, match="worker_count must be >= 1"):
+        solve_batch([p], worker_count=0)
+    assert solve_batch([]) == []
+
+
+def test_agent_state_validation():
+    import pytest
+    from paper_2008_11578_b200 import AgentClass, AgentState
+    a = AgentState(id=1, position=(0, 0), velocity=(1, 0), radius=0.3, pref_speed=1, max_speed=2, goal=(5, 5),
+                   agent_class=1)
+    assert a.agent_class is AgentClass.VEHICLE and a.position.dtype == float
+    with pytest.raises(ValueError, match="radius must be positive"):
+        AgentState(id=2, position=(0, 0), velocity=(0, 0), radius=0.0, pref_speed=1, max_speed=2, goal=(1, 1))
+    with pytest.raises(ValueError, match="pref_speed <= max_speed"):
+        AgentState(id=3, position=(0, 0), velocity=(0, 0), radius=0.3, pref_speed=3, max_speed=2, goal=(1, 1))
+
+
+def test_max_neighbors_above_the_device_limit_is_a_scenario_error():
+    import pytest
+    from paper_2008_11578_b200 import ScenarioError, scenario_from_dict, two_way_dict
+    doc = two_way_dict(4)
+    doc["max_neighbors"] = 32
+    scenario_from_dict(doc)
+    doc["max_neighbors"] = 33
+    with pytest.raises(ScenarioError, match="max_neighbors: 33 exceeds"):
+        scenario_from_dict(doc)
