@@ -181,6 +181,35 @@ ORCA_API int orca_step(orca_sim *sim);
 /* `steps` consecutive frames without host round trips. */
 ORCA_API int orca_run(orca_sim *sim, int64_t steps);
 
+/* What engine.run reads after every frame (engine.py:333-346: FrameMetrics, the fallback count,
+ * who arrived), recorded on the device so that a run needs no host round trip per frame. */
+typedef struct orca_frame_record {
+    int64_t frame;           /* frames completed after this step */
+    int64_t active_agents;   /* rows alive after arrival removal */
+    int64_t rows_before;     /* rows active during the frame (length of its trajectory block) */
+    int64_t lp_fallbacks;
+    int64_t removed_agents;
+    int64_t collision_count; /* 0 unless compute_metrics */
+    double min_separation;   /* +inf unless compute_metrics */
+} orca_frame_record; /* 56 bytes */
+
+/* Up to `steps` frames with NO host synchronisation in between, then one readback:
+ *   records[0 .. *n_records)   one orca_frame_record per frame actually stepped. A frame
+ *                              that would start with no agents left is not stepped (the
+ *                              reference's loop ends there, engine.py:333), so
+ *                              *n_records < steps means the crowd has fully arrived.
+ *   traj (may be NULL)         float64 [rows, 4] = (x, y, vx, vy): for each frame in turn the
+ *                              un-compacted result of every row active during that frame, in
+ *                              storage-row order (what engine._advance logs, engine.py:257-263);
+ *                              frame f's block has records[f].rows_before rows. traj_cap_rows
+ *                              bounds it (steps * current agent count always suffices).
+ *   arr_ids / arr_frames       the agents removed during these frames and the frame count at
+ *                              which each arrived (any order); arr_cap bounds them.
+ * Requires a loaded state and orca_set_params. Synchronises once, at the end. */
+ORCA_API int orca_run_logged(orca_sim *sim, int64_t steps, orca_frame_record *records, int64_t *n_records,
+                             double *traj, int64_t traj_cap_rows, int64_t *traj_rows, int64_t *arr_ids,
+                             int64_t *arr_frames, int64_t arr_cap, int64_t *n_arrivals);
+
 /* Wait for all queued work and report sticky device errors:
  * ORCA_ECOINCIDENT with the reference's message
  *   "frame F: agents A and B have exactly coincident centers; avoidance direction is undefined"

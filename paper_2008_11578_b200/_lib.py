@@ -28,7 +28,7 @@ SYMBOLS = [
     "orca_abi_version", "orca_create", "orca_destroy", "orca_set_stream", "orca_set_params",
     "orca_last_error", "orca_upload", "orca_download", "orca_download_pv", "orca_upload_pv",
     "orca_download_last_step_pv", "orca_download_last_step_kept",
-    "orca_step", "orca_run", "orca_sync", "orca_get_info", "orca_step_host", "orca_advance_host", "orca_reorder_rows",
+    "orca_step", "orca_run", "orca_run_logged", "orca_sync", "orca_get_info", "orca_step_host", "orca_advance_host", "orca_reorder_rows",
     "orca_profile_stages", "orca_get_stage_ms",
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
@@ -44,6 +44,11 @@ RECORD_DTYPE = np.dtype([("x", "f8"), ("y", "f8"), ("vx", "f8"), ("vy", "f8"), (
                          ("pref_speed", "f8"), ("max_speed", "f8"), ("goal_tol", "f8"),
                          ("goal_x", "f8"), ("goal_y", "f8"), ("id", "i8"), ("class_code", "i8")])
 
+
+# orca_frame_record (orca_run_logged)
+FRAME_RECORD_DTYPE = np.dtype([("frame", "i8"), ("active_agents", "i8"), ("rows_before", "i8"),
+                               ("lp_fallbacks", "i8"), ("removed_agents", "i8"), ("collision_count", "i8"),
+                               ("min_separation", "f8")])
 
 # slabs of the device-side exchange protocol (orca_slab_header + records)
 SLAB_HEADER_BYTES = 32
@@ -110,6 +115,7 @@ def load():
     L.orca_upload_pv.argtypes = [vp, i64, i64, vp, vp]
     L.orca_step.argtypes = [vp]
     L.orca_run.argtypes = [vp, i64]
+    L.orca_run_logged.argtypes = [vp, i64, vp, P(i64), vp, i64, P(i64), vp, vp, i64, P(i64)]
     L.orca_sync.argtypes = [vp]
     L.orca_get_info.argtypes = [vp, P(OrcaInfo)]
     L.orca_step_host.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp]

@@ -58,6 +58,14 @@ struct orca_sim {
     int *keep = nullptr, *dst_idx = nullptr;
     int *sel = nullptr, *sel_idx = nullptr; // strip selection flags and their scan
     int64_t ghost_bound = 0;                // ghost rows currently appended (upper bound)
+    // device-side frame log (orca_run_logged)
+    int log_mode = 0;                       // 0 off, 1 records, 2 records + trajectories
+    orca_frame_record *log_rec = nullptr;
+    int log_cap = 0;
+    double4 *log_traj = nullptr;
+    int64_t log_traj_cap = 0;
+    i64 *arr_ids = nullptr, *arr_frames = nullptr; // arrivals since the upload (capacity rows)
+    int64_t arr_read = 0;                          // ... of which the host has fetched this many
     // strip decomposition without host round trips (orca_strip_configure / _step)
     bool strip_on = false;
     double strip_lo = -INFINITY, strip_hi = INFINITY;
@@ -112,6 +120,7 @@ struct orca_sim {
         int64_t n_bound;           // key: launch grid sizes
         bool had_bins;             // key: sorted arrays already valid (metrics mode)
         int bbox_gap;              // key: which bounding-box path the bin build takes (-1: k_bbox)
+        int log_mode;              // key: the frame-log kernels are part of the sequence
         int bbox_rel;              // bbox_frame - frame after the step
         cudaGraphExec_t exec;
         int new_cur, new_acur, new_pre; // host state after the step
@@ -242,6 +251,10 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->lrow[1]);
     cudaFree(sim->a64[0]);
     cudaFree(sim->a64[1]);
+    cudaFree(sim->log_rec);
+    cudaFree(sim->log_traj);
+    cudaFree(sim->arr_ids);
+    cudaFree(sim->arr_frames);
     cudaFree(sim->lkeep);
     cudaFree(sim->lscan);
     cudaFree(sim->cell_of);
@@ -522,6 +535,7 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->since_reorder = 0;
     sim->apre = 0;
     sim->drop_graphs(); // captured compactions assume the row-order state they were recorded in
+    sim->arr_read = 0;
     if (n > 0) {
         k_iota<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->lrow[0]);
         CK(sim, cudaMemcpyAsync(sim->ids[0], ids, sizeof(i64) * n, cudaMemcpyHostToDevice, sim->stream));
@@ -945,7 +959,8 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
         reinterpret_cast<R4 *>(sim->goalpref[b]), reinterpret_cast<const R2 *>(sim->radmax[a]),
         reinterpret_cast<R2 *>(sim->radmax[b]), sim->ids[a], sim->ids[b], sim->cls[a], sim->cls[b],
         sim->status[a], sim->status[b], sim->failed[a], sim->failed[b], sim->hint[a], sim->hint[b],
-        sim->lrow[a], sim->lrow[b], lscan, sim->a64[a], sim->a64[b]);
+        sim->lrow[a], sim->lrow[b], lscan, sim->a64[a], sim->a64[b],
+        sim->log_mode && !from_sel ? sim->arr_ids : nullptr, sim->arr_frames, (int)sim->capacity);
     k_after_compact<<<1, 1, 0, st>>>(sim->plan, sim->dst_idx);
     CKL(sim);
     sim->launches += 6;
@@ -1009,8 +1024,10 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     sim->launches += 1;
     if (n == 0) { // engine.py:202-209
         k_finish<<<1, 1, 0, sim->stream>>>(sim->plan, sim->params.remove_arrivals, nullptr, nullptr);
+        if (sim->log_mode)
+            k_log_frame<<<1, 1, 0, sim->stream>>>(sim->plan, sim->log_rec, sim->log_cap, sim->log_mode == 2);
         CKL(sim);
-        sim->launches += 1;
+        sim->launches += 1 + (sim->log_mode ? 1 : 0);
         for (int i = 0; i < ORCA_N_STAGES; ++i) sim->mark();
         sim->frame += 1;
         return ORCA_OK;
@@ -1074,6 +1091,18 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
         rc = metrics_stage<S>(sim, P2);
         if (rc) return rc;
     }
+    if (sim->log_mode) {
+        if (sim->log_mode == 2) {
+            typedef typename Vec<S>::T4 S4;
+            k_log_traj<S><<<grid_for(n, 256), 256, 0, sim->stream>>>(
+                sim->plan, reinterpret_cast<const S4 *>(sim->pv[out_idx]), sim->lrow[sim->apre], sim->log_traj,
+                (i64)sim->log_traj_cap);
+            sim->launches += 1;
+        }
+        k_log_frame<<<1, 1, 0, sim->stream>>>(sim->plan, sim->log_rec, sim->log_cap, sim->log_mode == 2);
+        CKL(sim);
+        sim->launches += 1;
+    }
     sim->mark();
     return ORCA_OK;
 }
@@ -1098,7 +1127,7 @@ static int step_graphed(orca_sim *sim)
     const int bbox_gap = gap64 < 0 || gap64 > 1 ? -1 : (int)gap64;
     for (auto &g : sim->graphs) {
         if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins &&
-            g.bbox_gap == bbox_gap) {
+            g.bbox_gap == bbox_gap && g.log_mode == sim->log_mode) {
             CK(sim, cudaGraphLaunch(g.exec, sim->stream));
             sim->n_pre = sim->n_bound;
             sim->apre = g.acur;
@@ -1120,6 +1149,7 @@ static int step_graphed(orca_sim *sim)
     g.n_bound = sim->n_bound;
     g.had_bins = had_bins;
     g.bbox_gap = bbox_gap;
+    g.log_mode = sim->log_mode;
     const int64_t l0 = sim->launches;
     if (cudaStreamBeginCapture(sim->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
         cudaGetLastError();
@@ -1222,6 +1252,94 @@ extern "C" int orca_run(orca_sim *sim, int64_t steps)
         int rc = orca_step(sim);
         if (rc) return rc;
     }
+    return ORCA_OK;
+}
+
+extern "C" int orca_run_logged(orca_sim *sim, int64_t steps, orca_frame_record *records, int64_t *n_records,
+                               double *traj, int64_t traj_cap_rows, int64_t *traj_rows, int64_t *arr_ids,
+                               int64_t *arr_frames, int64_t arr_cap, int64_t *n_arrivals)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_run_logged: no resident state");
+    if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_run_logged: orca_set_params was not called");
+    if (steps < 0 || steps > 0x3FFFFFFF || (steps > 0 && !records) || !n_records ||
+        (traj && (traj_cap_rows < 0 || !traj_rows)) || arr_cap < 0 || (arr_cap > 0 && (!arr_ids || !arr_frames)) ||
+        !n_arrivals)
+        return fail(sim, ORCA_EINVAL, "orca_run_logged: bad arguments");
+    if (sim->ghost_bound > 0) return fail(sim, ORCA_EINVAL, "orca_run_logged: ghost rows are resident");
+    CK(sim, cudaSetDevice(sim->device));
+    *n_records = 0;
+    *n_arrivals = 0;
+    if (traj_rows) *traj_rows = 0;
+    if (steps == 0) return ORCA_OK;
+    // device-side log buffers (grown on demand; a new buffer invalidates captured launches)
+    if (sim->log_cap < steps) {
+        CK(sim, cudaStreamSynchronize(sim->stream));
+        sim->drop_graphs();
+        cudaFree(sim->log_rec);
+        sim->log_rec = nullptr;
+        sim->log_cap = 0;
+        CK(sim, dalloc(&sim->log_rec, (size_t)steps));
+        sim->log_cap = (int)steps;
+    }
+    if (traj && sim->log_traj_cap < traj_cap_rows) {
+        CK(sim, cudaStreamSynchronize(sim->stream));
+        sim->drop_graphs();
+        cudaFree(sim->log_traj);
+        sim->log_traj = nullptr;
+        sim->log_traj_cap = 0;
+        CK(sim, dalloc(&sim->log_traj, (size_t)std::max<int64_t>(traj_cap_rows, 1)));
+        sim->log_traj_cap = traj_cap_rows;
+    }
+    if (!sim->arr_ids) {
+        const size_t cap = (size_t)std::max<int64_t>(sim->capacity, 1);
+        CK(sim, dalloc(&sim->arr_ids, cap));
+        CK(sim, dalloc(&sim->arr_frames, cap));
+    }
+    k_log_reset<<<1, 1, 0, sim->stream>>>(sim->plan, 1);
+    CKL(sim);
+    sim->launches += 1;
+    sim->log_mode = traj ? 2 : 1;
+    int rc = ORCA_OK;
+    for (int64_t i = 0; i < steps && rc == ORCA_OK; ++i) rc = orca_step(sim);
+    sim->log_mode = 0;
+    // ONE synchronisation: the plan (counters, sticky errors), then the logs it describes
+    const int rc_plan = fetch_plan(sim);
+    const GridPlan h = *sim->h_plan;
+    k_log_reset<<<1, 1, 0, sim->stream>>>(sim->plan, 0);
+    sim->launches += 1;
+    if (rc) return rc;
+    if (rc_plan) return rc_plan;
+    // idle steps (nobody left) did not advance the device's frame counter: follow it
+    sim->frame = h.frame;
+    sim->bbox_frame = -1;
+    sim->binned_frame = -1;
+    const int64_t nrec = std::min<int64_t>(h.log_count, steps);
+    if (nrec > 0)
+        CK(sim, cudaMemcpyAsync(records, sim->log_rec, sizeof(orca_frame_record) * nrec, cudaMemcpyDeviceToHost,
+                                sim->stream));
+    *n_records = nrec;
+    if (traj) {
+        if (h.traj_rows > traj_cap_rows)
+            return fail(sim, ORCA_ECAPACITY, "orca_run_logged: %lld trajectory rows, buffer holds %lld",
+                        (long long)h.traj_rows, (long long)traj_cap_rows);
+        if (h.traj_rows > 0)
+            CK(sim, cudaMemcpyAsync(traj, sim->log_traj, sizeof(double4) * h.traj_rows, cudaMemcpyDeviceToHost,
+                                    sim->stream));
+        *traj_rows = h.traj_rows;
+    }
+    const int64_t fresh = (int64_t)h.arr_count - sim->arr_read;
+    if (fresh > arr_cap)
+        return fail(sim, ORCA_ECAPACITY, "orca_run_logged: %lld arrivals, buffers hold %lld", (long long)fresh,
+                    (long long)arr_cap);
+    if (fresh > 0) {
+        CK(sim, cudaMemcpyAsync(arr_ids, sim->arr_ids + sim->arr_read, sizeof(i64) * fresh, cudaMemcpyDeviceToHost,
+                                sim->stream));
+        CK(sim, cudaMemcpyAsync(arr_frames, sim->arr_frames + sim->arr_read, sizeof(i64) * fresh,
+                                cudaMemcpyDeviceToHost, sim->stream));
+    }
+    *n_arrivals = fresh;
+    sim->arr_read = h.arr_count;
+    CK(sim, cudaStreamSynchronize(sim->stream));
     return ORCA_OK;
 }
 

@@ -58,6 +58,12 @@ struct GridPlan {
     u64 collisions;
     // frames completed
     i64 frame;
+    // orca_run_logged: per-frame records / trajectories / arrivals kept on the device
+    int halt_when_empty; // a frame that starts with no agents left is not a frame (engine.py:333)
+    int idle;            // ... and this step is such a non-frame
+    int log_count;       // frame records written since the chunk began
+    i64 traj_rows;       // trajectory rows written since the chunk began
+    int arr_count;       // arrivals logged since the upload
 };
 
 // The per-agent attributes a step never changes, exactly as the host uploaded them (float64):

@@ -62,6 +62,7 @@ __global__ void k_begin_step(GridPlan *plan)
     plan->fq_count = 0;
     plan->cq_count = 0;
     plan->n_pre = plan->n_owned;
+    plan->idle = plan->halt_when_empty && plan->n_owned == 0;
     plan->gq_count = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
@@ -1369,7 +1370,7 @@ __global__ void k_finish(GridPlan *plan, int remove_arrivals, const i64 *__restr
             if (lrow[p] == lj) plan->err_id_j = ids[p];
         }
     }
-    plan->frame = plan->frame + 1;
+    if (!plan->idle) plan->frame = plan->frame + 1;
     if (!remove_arrivals) {
         plan->removed = 0;
         plan->n_after = plan->n_owned;
@@ -1397,11 +1398,21 @@ k_compact(GridPlan *__restrict__ plan, const int *__restrict__ keep, const int *
           u8 *__restrict__ cls2, const i8 *__restrict__ st, i8 *__restrict__ st2,
           const i8 *__restrict__ fa, i8 *__restrict__ fa2, const float *__restrict__ hint,
           float *__restrict__ hint2, const int *__restrict__ lrow, int *__restrict__ lrow2,
-          const int *__restrict__ lscan, const Attr64 *__restrict__ a64, Attr64 *__restrict__ a64_2)
+          const int *__restrict__ lscan, const Attr64 *__restrict__ a64, Attr64 *__restrict__ a64_2,
+          i64 *__restrict__ arr_ids, i64 *__restrict__ arr_frames, int arr_cap)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = plan->n;
     if (i >= n) return;
+    if (arr_ids && !keep[i] && i < plan->n_owned) {
+        // an owned row that is dropped arrived in the frame just completed (engine.py:251-255):
+        // who and when, for the run loop's travel times (orca_run_logged)
+        const int slot = atomicAdd(&plan->arr_count, 1);
+        if (slot < arr_cap) {
+            arr_ids[slot] = ids[i];
+            arr_frames[slot] = plan->frame;
+        }
+    }
     if (keep[i]) {
         const int d = dst_idx[i];
         if (a64) a64_2[d] = a64[i];
@@ -1581,6 +1592,49 @@ __global__ void k_after_append(GridPlan *plan, int count, int ghost)
 }
 
 __global__ void k_drop_ghosts(GridPlan *plan) { plan->n = plan->n_owned; }
+
+// ---- device-side frame log (orca_run_logged): what engine.run reads per frame, kept in HBM ----
+
+__global__ void k_log_reset(GridPlan *plan, int halt_when_empty)
+{
+    plan->halt_when_empty = halt_when_empty;
+    plan->log_count = 0;
+    plan->traj_rows = 0;
+}
+
+// the frame's un-compacted result (every row active during the frame, arrivals included,
+// engine.py:257-263) appended to the trajectory buffer in storage-row order
+template <typename S>
+__global__ void __launch_bounds__(256)
+k_log_traj(const GridPlan *__restrict__ plan, const typename Vec<S>::T4 *__restrict__ pv_out,
+           const int *__restrict__ lrow, double4 *__restrict__ traj, i64 cap_rows)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (plan->idle || i >= plan->n_pre) return;
+    const i64 dst = plan->traj_rows + lrow[i];
+    if (dst >= cap_rows) return;
+    const typename Vec<S>::T4 a = pv_out[i];
+    traj[dst] = make_double4((double)a.x, (double)a.y, (double)a.z, (double)a.w);
+}
+
+// one record per frame (engine.FrameMetrics + SimState.lp_fallbacks, engine.py:46-52,247,270-286)
+__global__ void k_log_frame(GridPlan *plan, orca_frame_record *__restrict__ rec, int cap, int with_traj)
+{
+    if (plan->idle) return;
+    if (plan->log_count < cap) {
+        orca_frame_record r;
+        r.frame = plan->frame;
+        r.active_agents = plan->n_owned;
+        r.rows_before = plan->n_pre;
+        r.lp_fallbacks = plan->fq_count;
+        r.removed_agents = plan->removed;
+        r.collision_count = (i64)plan->collisions;
+        r.min_separation = dec_double(plan->min_sep_enc);
+        rec[plan->log_count] = r;
+    }
+    plan->log_count += 1;
+    if (with_traj) plan->traj_rows += plan->n_pre;
+}
 
 // ---- device-side exchange protocol (no host round trip per frame) -------------------
 //

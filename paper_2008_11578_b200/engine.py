@@ -210,6 +210,27 @@ class Simulation:
     def run(self, steps: int):
         check(self._L.orca_run(self._h, int(steps)), self._h)
 
+    def run_logged(self, steps: int, n_bound: int, with_trajectories: bool = False):
+        """Up to `steps` frames with NO host synchronisation in between (orca_run_logged), then
+        one readback of what engine.run needs per frame. `n_bound`: an upper bound on the rows
+        active during these frames (the current agent count). Returns
+          records  structured array (_lib.FRAME_RECORD_DTYPE), one row per frame actually
+                   stepped -- fewer than `steps` when the crowd fully arrived,
+          traj     float64 [rows, 4] (x, y, vx, vy), the frames' un-compacted results back to
+                   back (records["rows_before"] rows each), or None,
+          arrivals (ids int64[m], frames int64[m]) of the agents removed during these frames."""
+        steps, n_bound = int(steps), max(int(n_bound), 1)
+        rec = np.empty(max(steps, 1), dtype=_lib.FRAME_RECORD_DTYPE)
+        traj = _host_empty((steps * n_bound, 4)) if with_trajectories else None
+        arr_ids, arr_frames = np.empty(n_bound, dtype=np.int64), np.empty(n_bound, dtype=np.int64)
+        n_rec, n_traj, n_arr = C.c_int64(), C.c_int64(), C.c_int64()
+        self._raise_like_reference(self._L.orca_run_logged(
+            self._h, steps, ptr(rec), C.byref(n_rec), ptr(traj), steps * n_bound if with_trajectories else 0,
+            C.byref(n_traj), ptr(arr_ids), ptr(arr_frames), n_bound, C.byref(n_arr)))
+        m = int(n_arr.value)
+        return (rec[:int(n_rec.value)], traj[:int(n_traj.value)] if with_trajectories else None,
+                (arr_ids[:m], arr_frames[:m]))
+
     def sync(self):
         self._raise_like_reference(self._L.orca_sync(self._h))
 
@@ -474,15 +495,23 @@ def step(state: SimState, config: ScenarioConfig, worker_count: int = 1,
     return new_state, metrics
 
 
+RUN_CHUNK_FRAMES = 64                 # frames between host synchronisations in run()
+RUN_CHUNK_TRAJ_BYTES = 256 << 20      # ... fewer when trajectories of a large crowd are recorded
+
+
 def run(config: ScenarioConfig, worker_count: int = 1, record_trajectories: bool = True,
         work_unit_steps: int = DEFAULT_WORK_UNIT_STEPS, *, agents=None, state: SimState | None = None,
         precision=None, device: int = 0) -> RunResult:
     """Step until every agent reaches its goal or the frame guard trips (engine.py:311-370).
-    The crowd stays on the device for the whole run; per frame the host reads back the
-    counters (frame metrics, fallbacks, arrivals) and, when record_trajectories is set, the
-    frame's positions and velocities. `agents` / `state` supply the spawned crowd (the
-    reference samples it from config.regions, which is outside this package's scope).
-    summary.terminated is False when the guard stopped the run."""
+    The crowd stays on the device for the whole run and the HOST IS NOT IN THE FRAME LOOP: frames
+    are issued in chunks of up to RUN_CHUNK_FRAMES (orca_run_logged); the per-frame metrics, the
+    fallback counts, who arrived when and -- when record_trajectories is set -- every frame's
+    positions and velocities accumulate in device buffers and are read back once per chunk (one
+    synchronisation per chunk; `run.last_host_syncs` counts them). A frame that would start with no
+    agents left is never stepped, exactly like the reference's loop. FrameMetrics.wall_ms is the
+    chunk's wall time divided by its frames (a per-frame wall time needs a per-frame sync).
+    `agents` / `state` supply an already spawned crowd; otherwise it is sampled from config.regions
+    with the reference's seeded sampler. summary.terminated is False when the guard stopped the run."""
     del worker_count, work_unit_steps
     if state is None:
         state = init_state(config, agents)
@@ -498,31 +527,41 @@ def run(config: ScenarioConfig, worker_count: int = 1, record_trajectories: bool
     frame, dt = int(state.frame), float(config.dt)
     sim = Simulation(config, capacity=max(n0, 1), precision=precision, device=device,
                      remove_arrivals=True, compute_metrics=True)
+    run.last_host_syncs = 0
     try:
         sim.load(state)
         while ids.shape[0] > 0 and frame < guard:
-            t0 = _time.perf_counter()
-            n_pre = ids.shape[0]
-            sim.step()
-            info = sim.info()                       # synchronises; raises the reference's errors
-            wall_ms = (_time.perf_counter() - t0) * 1e3
-            frame = int(info.frame)
+            chunk = min(RUN_CHUNK_FRAMES, guard - frame)
             if record_trajectories:
-                pos, vel = sim.last_step_positions_velocities(n_pre)
-                logs.append(FrameLog(frame=frame, time=frame * dt, ids=ids.copy(), classes=classes.copy(),
-                                     positions=pos, velocities=vel, radii=radii.copy()))
-            if int(info.removed_agents):
-                kept = sim.ids()
-                gone = ~np.isin(ids, kept, assume_unique=True)
-                for agent_id in ids[gone]:
-                    arrival[int(agent_id)] = frame * dt
-                ids, classes, radii = ids[~gone], classes[~gone], radii[~gone]
-            n2 = ids.shape[0]
-            metrics.append(FrameMetrics(
-                frame=frame, wall_ms=wall_ms,
-                min_separation=float(info.min_separation) if n2 >= 2 else float("inf"),
-                collision_count=int(info.collision_count) if n2 >= 2 else 0, active_agents=int(n2)))
-            fallbacks += int(info.lp_fallbacks)
+                chunk = max(1, min(chunk, RUN_CHUNK_TRAJ_BYTES // (32 * ids.shape[0])))
+            t0 = _time.perf_counter()
+            recs, traj, (arr_ids, arr_frames) = sim.run_logged(chunk, ids.shape[0], record_trajectories)
+            run.last_host_syncs += 1
+            wall_ms = (_time.perf_counter() - t0) * 1e3 / max(len(recs), 1)
+            row0 = 0
+            for r in recs:
+                frame = int(r["frame"])
+                n_pre = int(r["rows_before"])
+                if record_trajectories:
+                    block = traj[row0:row0 + n_pre]
+                    row0 += n_pre
+                    logs.append(FrameLog(frame=frame, time=frame * dt, ids=ids.copy(), classes=classes.copy(),
+                                         positions=np.ascontiguousarray(block[:, 0:2]),
+                                         velocities=np.ascontiguousarray(block[:, 2:4]), radii=radii.copy()))
+                if int(r["removed_agents"]):
+                    gone_ids = arr_ids[arr_frames == frame]
+                    for agent_id in gone_ids:
+                        arrival[int(agent_id)] = frame * dt
+                    keep = ~np.isin(ids, gone_ids, assume_unique=True)
+                    ids, classes, radii = ids[keep], classes[keep], radii[keep]
+                n2 = int(r["active_agents"])
+                metrics.append(FrameMetrics(
+                    frame=frame, wall_ms=wall_ms,
+                    min_separation=float(r["min_separation"]) if n2 >= 2 else float("inf"),
+                    collision_count=int(r["collision_count"]) if n2 >= 2 else 0, active_agents=n2))
+                fallbacks += int(r["lp_fallbacks"])
+            if len(recs) < chunk:          # the device stopped stepping: nobody is left
+                break
         final_state = sim.state(type(state))
     finally:
         sim.close()
