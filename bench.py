@@ -462,7 +462,7 @@ def run_ours(args):
     else:
         ref_numba = {"skipped": "--no-extras"}
 
-    dtype = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision]
+    dtype = DTYPES[args.precision]
     line = {
         "metric": "agent_steps_per_s", "value": value, "unit": "agent-steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
@@ -498,7 +498,9 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
-PRECISIONS = ("mixed", "f32", "f64")
+PRECISIONS = ("mixed", "cert32", "f32", "f64")
+DTYPES = {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64",
+          "cert32": "f32 state / f32 arithmetic with an f64-evaluated, certified result (f64 otherwise)"}
 
 LP_WORKLOADS = {"lp_1m_feasible": 0.0, "lp_1m_half": 0.5, "lp_1m_infeasible": 1.0}
 

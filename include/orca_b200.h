@@ -47,6 +47,12 @@
  *                   than 1e-4 m/s -- counted and reported by the parity tests.
  *       ORCA_F64    FP64 state and arithmetic: bit-identical to the reference on
  *                   any float64 input.
+ *       ORCA_CERT32 the results of ORCA_MIXED, faster: the half-planes and the LP run in
+ *                   FP32 only to find which (at most two) half-planes decide the result;
+ *                   the result itself is evaluated in FP64 on those, and accepted only
+ *                   with a certificate (feasibility and optimality margins above the FP32
+ *                   error bounds, csrc/orca_cert.cuh). Everything else -- infeasible LPs,
+ *                   thin margins -- goes through the FP64 kernels of ORCA_MIXED.
  */
 #ifndef ORCA_B200_H
 #define ORCA_B200_H
@@ -75,7 +81,7 @@ enum {
     ORCA_EUNSUPPORTED = -6 /* e.g. max_neighbors above ORCA_MAX_NEIGHBORS */
 };
 
-enum { ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2 };
+enum { ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2, ORCA_CERT32 = 3 };
 
 #define ORCA_MAX_NEIGHBORS 32
 

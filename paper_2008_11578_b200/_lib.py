@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # ORCA_B200_LIB: load another build of the same ABI (kernel experiments)
 LIB_PATH = os.environ.get("ORCA_B200_LIB") or os.path.join(_HERE, "liborca_b200.so")
 
-ORCA_F32, ORCA_F64, ORCA_MIXED = 0, 1, 2
+ORCA_F32, ORCA_F64, ORCA_MIXED, ORCA_CERT32 = 0, 1, 2, 3
 ORCA_MAX_NEIGHBORS = 32
 ORCA_N_STAGES = 6
 STAGE_NAMES = ["bins", "gather", "solve", "fallback", "finish", "metrics"]
@@ -171,7 +171,8 @@ def ptr(a):
 
 
 _PRECISIONS = {"f32": ORCA_F32, "float32": ORCA_F32, "f64": ORCA_F64, "float64": ORCA_F64,
-               "mixed": ORCA_MIXED, ORCA_F32: ORCA_F32, ORCA_F64: ORCA_F64, ORCA_MIXED: ORCA_MIXED}
+               "mixed": ORCA_MIXED, "cert32": ORCA_CERT32, ORCA_F32: ORCA_F32, ORCA_F64: ORCA_F64,
+               ORCA_MIXED: ORCA_MIXED, ORCA_CERT32: ORCA_CERT32}
 
 
 def precision_code(precision) -> int:
@@ -179,8 +180,8 @@ def precision_code(precision) -> int:
     try:
         return _PRECISIONS[precision]
     except (KeyError, TypeError):
-        raise ValueError(f"unknown precision {precision!r} (use 'mixed', 'f32' or 'f64')") from None
+        raise ValueError(f"unknown precision {precision!r} (use 'f64', 'mixed', 'cert32' or 'f32')") from None
 
 
 def precision_name(code: int) -> str:
-    return {ORCA_F32: "f32", ORCA_F64: "f64", ORCA_MIXED: "mixed"}[code]
+    return {ORCA_F32: "f32", ORCA_F64: "f64", ORCA_MIXED: "mixed", ORCA_CERT32: "cert32"}[code]

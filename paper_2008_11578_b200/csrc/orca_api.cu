@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "orca_kernels.cuh"
+#include "orca_cert.cuh"
 #include "orca_lp_batch.cuh"
 
 using namespace orca;
@@ -88,6 +89,7 @@ struct orca_sim {
     u8 *fq_perm = nullptr;
     u8 *s_perm = nullptr; // insertion order per sorted slot (k_shuffle -> k_solve_group), spill_maxn bytes each
     int spill_maxn = 0;
+    int *cq = nullptr; // ORCA_CERT32: agents whose FP32 solve was not certified (solved in FP64)
     int *gq = nullptr; // agents queued for the exact ring search
     GridPlan *plan = nullptr;
     GridPlan *h_plan = nullptr; // pinned mirror
@@ -217,6 +219,9 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
     e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::solve_bpt * 64);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_solve_group_queue<S, R, MAXN, 128, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::solve_bpt * 64);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL_SHORT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::fb_bpt * (C::fb_threads / ORCA_GL_SHORT));
@@ -275,6 +280,7 @@ extern "C" void orca_destroy(orca_sim *sim)
     cudaFree(sim->fq_perm);
     cudaFree(sim->s_perm);
     cudaFree(sim->gq);
+    cudaFree(sim->cq);
     cudaFree(sim->plan);
     cudaFree(sim->stg);
     cudaFree(sim->dbg);
@@ -297,7 +303,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     *out = nullptr;
     if (capacity < 0 || capacity > 0x3FFFFFFF)
         return fail(nullptr, ORCA_EINVAL, "orca_create: capacity %lld out of range", (long long)capacity);
-    if (precision != ORCA_F32 && precision != ORCA_F64 && precision != ORCA_MIXED)
+    if (precision != ORCA_F32 && precision != ORCA_F64 && precision != ORCA_MIXED && precision != ORCA_CERT32)
         return fail(nullptr, ORCA_EINVAL, "orca_create: unknown precision %d", precision);
     int ndev = 0;
     CK(nullptr, cudaGetDeviceCount(&ndev));
@@ -379,6 +385,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(dalloc(&sim->fq, cap));
     CKC(cudaMalloc(&sim->fq_state, cap * 4 * as));
     CKC(dalloc(&sim->gq, cap));
+    if (precision == ORCA_CERT32) CKC(dalloc(&sim->cq, cap));
     CKC(dalloc(&sim->plan, 1));
     CKC(cudaMallocHost(reinterpret_cast<void **>(&sim->h_plan), sizeof(GridPlan)));
     sim->stg_bytes = cap * 12 * sizeof(double);
@@ -390,6 +397,8 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC((set_smem_attrs<float, double, 32>()));
     CKC((set_smem_attrs<double, double, 16>()));
     CKC((set_smem_attrs<double, double, 32>()));
+    CKC(cudaFuncSetAttribute(k_solve_cert<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 16 * 128));
+    CKC(cudaFuncSetAttribute(k_solve_cert<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 128));
 #undef CKC
     *out = sim;
     return ORCA_OK;
@@ -863,14 +872,30 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         sim->lrow[a], reinterpret_cast<R4 *>(sim->fq_cons), sim->fq_perm
     // below ~64 k agents the step is launch-latency bound and the extra launch costs more than the
     // idle lanes of the in-kernel shuffle (16,640 agents: +1.8 us)
-    const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && n >= ORCA_PRESHUFFLE_MIN_AGENTS;
+    const bool cert = sim->precision == ORCA_CERT32;
+    const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && (cert || n >= ORCA_PRESHUFFLE_MIN_AGENTS);
     const uint32_t *s_perm = preshuffle ? reinterpret_cast<const uint32_t *>(sim->s_perm) : nullptr;
     if (preshuffle) {
         k_shuffle<MAXN><<<grid_for(n, 128), 128, 0, st>>>(sim->plan, sim->s_row, sim->ids[a], sim->nb_cnt,
                                                          reinterpret_cast<uint4 *>(sim->s_perm), s0, s1);
         sim->launches += 1;
     }
-    if (sim->solve_gl == 2 && preshuffle)
+    if (cert) {
+        // FP32 solve with a certificate for everyone, the FP64 kernel for the agents it queued
+        if constexpr (Fmt<S>::is_f32 && !Fmt<R>::is_f32) {
+            k_solve_cert<MAXN, 128><<<grid_for(n, 128), 128, 21 * MAXN * 128, st>>>(
+                sim->plan, P, reinterpret_cast<const NbRec<float> *>(sim->s_nr),
+                reinterpret_cast<const double4 *>(sim->s_dm), sim->s_row, sim->nb, sim->nb_cnt,
+                reinterpret_cast<const float4 *>(sim->goalpref[a]), reinterpret_cast<float4 *>(sim->pv[out_idx]),
+                sim->status[a], sim->failed[a], sim->arrived, sim->cq, s_perm);
+            // (4x the resident blocks: a typical queue -- the ~6 % of a sparse crowd -- is ONE chunk per
+            //  block, spread over every SM at once; blocks beyond the queue exit at their first test)
+            const int qblocks = (int)std::min<int64_t>(148 * ORCA_SG_BLOCKS * 4, std::max<int64_t>(1, (n + 63) / 64));
+            k_solve_group_queue<S, R, MAXN, 128, 2, true><<<qblocks, 128, C::solve_bpt * 64, st>>>(
+                ORCA_SOLVE_ARGS, s_perm, sim->cq);
+            sim->launches += 1;
+        }
+    } else if (sim->solve_gl == 2 && preshuffle)
         k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(n, 64), 128, C::solve_bpt * 64, st>>>(
             ORCA_SOLVE_ARGS, s_perm);
     else if (sim->solve_gl == 2)
@@ -1111,7 +1136,8 @@ static int step_plain(orca_sim *sim)
 {
     switch (sim->precision) {
     case ORCA_F32: return step_impl<float, float>(sim);
-    case ORCA_MIXED: return step_impl<float, double>(sim);
+    case ORCA_MIXED:
+    case ORCA_CERT32: return step_impl<float, double>(sim);
     default: return step_impl<double, double>(sim);
     }
 }
@@ -1209,7 +1235,8 @@ extern "C" int orca_reorder_rows(orca_sim *sim)
     if (!sim->rows_permuted) sim->drop_graphs(); // graphs captured with identity row order are stale now
     switch (sim->precision) {
     case ORCA_F32: rc = reorder_rows<float, float>(sim, P); break;
-    case ORCA_MIXED: rc = reorder_rows<float, double>(sim, P); break;
+    case ORCA_MIXED:
+    case ORCA_CERT32: rc = reorder_rows<float, double>(sim, P); break;
     default: rc = reorder_rows<double, double>(sim, P); break;
     }
     sim->reorder_due = false;
@@ -1733,6 +1760,7 @@ extern "C" int orca_debug_last_step(orca_sim *sim, int64_t n, int64_t *cell_ix, 
     case ORCA_F32:
         return debug_impl<float, float>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
     case ORCA_MIXED:
+    case ORCA_CERT32:
         return debug_impl<float, double>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);
     default:
         return debug_impl<double, double>(sim, n, cell_ix, cell_iy, nb_rows, nb_count, out_v, status, failed_at, desired_v);

@@ -1,0 +1,395 @@
+// orca_cert.cuh -- ORCA_CERT32: the solve stage in FP32 with a certificate, FP64 only where
+// the result is decided.
+//
+// What bounds the FP64 solve kernel (k_solve_group, profiles/) is sixteen ~130-instruction FP64
+// vo_exit chains per agent plus the FP64 incremental LP -- yet the RESULT of a feasible LP
+// depends on at most two of the sixteen half-planes: the optimum is the preferred velocity
+// itself, its projection onto one constraint line, or the intersection of two lines
+// (_kernels.py:74-146). k_solve_cert therefore
+//
+//   1. builds all half-planes and runs the shuffled incremental LP in FP32 (the arithmetic of
+//      k_solve<float>), remembering which constraints ended up ACTIVE: the line L of the last
+//      1-D solve and the earlier constraint B that bound it (or none);
+//   2. re-evaluates in FP64 exactly what the reference evaluates on that active set -- the
+//      half-planes of L and B (vo_exit<double>, same operations, K:343-419) and the closing
+//      formula of _lp1_target (K:98-119) -- which costs 0-2 FP64 vo_exit chains instead of 16;
+//   3. CERTIFIES that candidate, independently of the path the FP32 LP took: it must satisfy
+//      every other half-plane with a margin above that half-plane's FP32 error bound, lie
+//      strictly inside the speed disc, and satisfy the optimality (KKT) sign conditions of its
+//      active set with margins. A feasible point with a valid KKT certificate IS the optimum of
+//      this strictly convex problem, the optimum is unique, the margins make the active set
+//      non-degenerate, and with a non-degenerate active set the reference's last 1-D solve is
+//      on the later-inserted active constraint bounded by the earlier one -- i.e. the value
+//      computed in step 2, bit for bit. (The FP32 run only GUESSES the active set; nothing it
+//      decides is trusted.)
+//
+// An agent that is not certified -- infeasible LP (the least-penetration stage needs FP64
+// half-planes anyway), an active speed disc, near-parallel active lines, a margin too small, an
+// FP32 half-plane whose branch decisions (overlap K:357, leg side K:404) sit within rounding of
+// flipping -- is queued (plan->cq_count / cq) and solved by the FP64 kernels exactly as in
+// ORCA_MIXED. Results are therefore those of ORCA_MIXED: identical status / failed_at, FP64
+// velocities rounded once to the FP32 state (tests/test_gpu_step.py: every agent of every
+// BASELINE crowd against the oracle).
+#pragma once
+
+#include "orca_kernels.cuh"
+
+namespace orca {
+
+#define CERT_EPS 1.1920929e-07f // 2^-23
+#define CERT_INF 1e30f
+#ifndef CERT_SAFETY
+#define CERT_SAFETY 8.0f        // multiplies every first-order error estimate below
+#endif
+#define CERT_CROSS_MIN 0.02f    // |n_L x n_B| below this: the vertex is ill-conditioned, leave it to FP64
+
+// vo_exit<float> (orca_math.cuh) plus a first-order bound on how far the FP32 half-plane can be
+// from the FP64 one: err_n on the unit normal (radians), err_u on the exit vector. CERT_INF when
+// a DIScontinuous branch decision could flip under rounding (the arc / leg choice is continuous:
+// both formulas meet at the tangent points, so it needs no guard).
+__device__ __forceinline__ bool vo_exit_cond(float rpx, float rpy, float rvx, float rvy, float comb_r,
+                                             float inv_tau, float inv_dt, float &ux, float &uy, float &nx,
+                                             float &ny, float &err_u, float &err_n)
+{
+    // (explicit fused multiply-adds and approximate reciprocals: this translation unit is compiled
+    //  with -fmad=false for the bit-exact FP64 paths, but the FP32 pass is only a guess with an
+    //  error bound a few times wider than any of these shortcuts)
+    const float d2 = __fmaf_rn(rpx, rpx, rpy * rpy);
+    const float r2 = comb_r * comb_r;
+    const bool overlap = d2 < r2; // K:357
+    const float inv = overlap ? inv_dt : inv_tau;
+    const float cx = rpx * inv, cy = rpy * inv;
+    const float rr = comb_r * inv;
+    const float wx = rvx - cx, wy = rvy - cy;
+    const float wl2 = __fmaf_rn(wx, wx, wy * wy);
+    const float dot_wp = __fmaf_rn(wx, rpx, wy * rpy);
+    const bool arc = overlap || (dot_wp < 0.0f && dot_wp * dot_wp > r2 * wl2); // K:395
+    const float arg = arc ? wl2 : d2 - r2;
+    const float rsq = rsqrtf(arg);          // 1 / |w|  or  1 / leg
+    const float sq = arg * rsq;
+    const float crs = __fmaf_rn(rpx, wy, -(rpy * wx));
+    const bool side = crs > 0.0f; // K:404
+    const float a1 = rpx * sq, a2 = rpy * comb_r, b1 = rpx * comb_r, b2 = rpy * sq;
+    const float lx = side ? a1 - a2 : -(a1 + a2);
+    const float ly = side ? b1 + b2 : b1 - b2;
+    const float rd2 = __fdividef(1.0f, d2);
+    const float iden = arc ? rsq : rd2;
+    const float qx = (arc ? wx : lx) * iden;
+    const float qy = (arc ? wy : ly) * iden;
+    const float s = rr - sq;
+    const float t = __fmaf_rn(rvx, qx, rvy * qy);
+    float mx = -qy, my = qx;
+    if (__fmaf_rn(mx, rpx, my * rpy) > 0.0f) {
+        mx = -mx;
+        my = -my;
+    }
+    ux = arc ? s * qx : __fmaf_rn(t, qx, -rvx);
+    uy = arc ? s * qy : __fmaf_rn(t, qy, -rvy);
+    nx = arc ? qx : mx;
+    ny = arc ? qy : my;
+    // --- conditioning (first order; CERT_SAFETY covers the approximations above) ---
+    const float sw = fabsf(rvx) + fabsf(rvy) + fabsf(cx) + fabsf(cy); // scale of the operands of w
+    const float srv = fabsf(rvx) + fabsf(rvy);
+    // arc: q = w / |w|, u = (rr - |w|) q.   leg = sqrt(d2 - r2): cancellation when the discs almost touch,
+    // kappa = (d2 + r2) / (d2 - r2) = (d2 + r2) * rsq^2, and the direction error is kappa * leg / |rp|
+    const float en_arc = 4.0f * CERT_EPS * (sw * rsq + 1.0f);
+    const float eu_arc = 4.0f * CERT_EPS * (sw + fabsf(rr)) + fabsf(s) * en_arc;
+    const float en_leg = 2.0f * CERT_EPS * ((d2 + r2) * rsq * rsqrtf(d2) + 3.0f);
+    const float eu_leg = srv * (2.0f * en_leg + 4.0f * CERT_EPS);
+    const float en = arc ? en_arc : en_leg, eu = arc ? eu_arc : eu_leg;
+    bool sure = fabsf(d2 - r2) > 64.0f * CERT_EPS * (d2 + r2);                        // overlap decision
+    sure = sure && wl2 > 1e-9f * (sw * sw) && wl2 > 1e-20f;                            // |w|^2 < 1e-24 branch, q = w/|w|
+    sure = sure && (overlap || fabsf(crs) > 64.0f * CERT_EPS * (fabsf(rpx * wy) + fabsf(rpy * wx))); // leg side
+    sure = sure && d2 > 0.0f;
+    err_n = sure ? CERT_SAFETY * en : CERT_INF;
+    err_u = sure ? CERT_SAFETY * eu : CERT_INF;
+    return d2 > 0.0f;
+}
+
+// _lp1_target (K:74-119) in FP32 that also reports WHICH bound closed the interval:
+// kind 0 = the projection of the target itself, 1 / 2 = an earlier constraint (position j_sel)
+// from the left / right, 3 / 4 = the speed disc.
+template <typename V>
+__device__ __forceinline__ bool lp1_target_act(const V &view, int i_pos, float cap, float tx, float ty,
+                                               float &ox, float &oy, int &kind, int &j_sel)
+{
+    float px, py, nx, ny;
+    view.get(i_pos, px, py, nx, ny);
+    const float dx = -ny, dy = nx;
+    const float pd = __fmaf_rn(px, dx, py * dy);
+    const float disc = __fmaf_rn(pd, pd, cap * cap) - __fmaf_rn(px, px, py * py);
+    if (disc < 0.0f) return false;
+    const float sq = disc * rsqrtf(fmaxf(disc, 1e-30f));
+    float t_left = -pd - sq, t_right = -pd + sq;
+    int jl = -1, jr = -1;
+    bool bad = false;
+#pragma unroll 4
+    for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
+        float qx, qy, mx, my;
+        view.get(j_pos, qx, qy, mx, my);
+        const float a = __fmaf_rn(dx, mx, dy * my);
+        const float b = __fmaf_rn(qx - px, mx, (qy - py) * my);
+        const bool par = fabsf(a) <= 1e-6f;
+        bad = bad || (par && b > 0.0f);
+        const float t = __fdividef(b, a);
+        if (!par && a > 0.0f && t > t_left) {
+            t_left = t;
+            jl = j_pos;
+        }
+        if (!par && !(a > 0.0f) && t < t_right) {
+            t_right = t;
+            jr = j_pos;
+        }
+    }
+    if (bad || t_left > t_right) return false;
+    float t = __fmaf_rn(tx - px, dx, (ty - py) * dy);
+    kind = 0;
+    j_sel = -1;
+    if (t < t_left) {
+        t = t_left;
+        kind = jl >= 0 ? 1 : 3;
+        j_sel = jl;
+    } else if (t > t_right) {
+        t = t_right;
+        kind = jr >= 0 ? 2 : 4;
+        j_sel = jr;
+    }
+    ox = __fmaf_rn(t, dx, px);
+    oy = __fmaf_rn(t, dy, py);
+    return true;
+}
+
+// lp2_target_runahead (orca_math.cuh) in FP32, reporting the active set of the LAST 1-D solve
+// (c_last = -1: the clamped target violated nothing).
+template <typename V>
+__device__ __forceinline__ bool lp2_target_runahead_act(const V &view, int k, float cap, float tx, float ty,
+                                                        float &vx, float &vy, int &c_last, int &kind,
+                                                        int &j_sel, unsigned live, bool enabled)
+{
+    const float t2 = __fmaf_rn(tx, tx, ty * ty);
+    if (t2 > cap * cap) {
+        const float s = cap * rsqrtf(t2);
+        vx = tx * s;
+        vy = ty * s;
+    } else {
+        vx = tx;
+        vy = ty;
+    }
+    int i_pos = 0;
+    bool done = !enabled, ok = true;
+    c_last = -1;
+    kind = 0;
+    j_sel = -1;
+    while (true) {
+        bool found = false;
+        if (!done) {
+            for (; i_pos < k; ++i_pos) {
+                float px, py, nx, ny;
+                view.get(i_pos, px, py, nx, ny);
+                if (__fmaf_rn(vx - px, nx, (vy - py) * ny) < 0.0f) {
+                    found = true;
+                    break;
+                }
+            }
+            done = !found;
+        }
+        if (!__any_sync(live, found)) break;
+        if (found) {
+            float nvx, nvy;
+            int kd, js;
+            if (lp1_target_act<V>(view, i_pos, cap, tx, ty, nvx, nvy, kd, js)) {
+                vx = nvx;
+                vy = nvy;
+                c_last = i_pos;
+                kind = kd;
+                j_sel = js;
+                ++i_pos;
+            } else {
+                ok = false;
+                done = true;
+            }
+        }
+    }
+    return ok;
+}
+
+// One half-plane of agent s in FP64, exactly as k_solve_group<float, double> builds it
+// (K:525-541): the neighbour at shuffled position `pos`.
+__device__ __forceinline__ bool halfplane64(int s, int pos, const StepParams &P, const NbRec<float> *__restrict__ s_nr,
+                                            const int *__restrict__ nb, const u8 *perm, int pstride,
+                                            double inv_tau, double inv_dt, double &px, double &py, double &nx,
+                                            double &ny)
+{
+    const NbRec<float> me = s_nr[s];
+    const int j = nb[(size_t)perm[pos * pstride] * P.stride + s];
+    const NbRec<float> o = s_nr[j];
+    const double ri = (double)me.rc.x + P.half_margin, rj = (double)o.rc.x + P.half_margin;
+    const int ci = (int)me.rc.y;
+    const double f0 = ci ? P.fmat[2] : P.fmat[0], f1 = ci ? P.fmat[3] : P.fmat[1];
+    const double mevx = (double)me.pv.z, mevy = (double)me.pv.w;
+    double ux, uy;
+    const bool ok = vo_exit_inv<double>((double)o.pv.x - (double)me.pv.x, (double)o.pv.y - (double)me.pv.y,
+                                        mevx - (double)o.pv.z, mevy - (double)o.pv.w, ri + rj, inv_tau, inv_dt, ux,
+                                        uy, nx, ny);
+    const double f = o.rc.y != 0.0f ? f1 : f0;
+    px = mevx + f * ux;
+    py = mevy + f * uy;
+    return ok;
+}
+
+// The solve stage of ORCA_CERT32 (see the header of this file). One thread per agent, FP32
+// half-planes + their error bounds in shared memory ([position][thread]); the insertion
+// order comes from k_shuffle. Certified agents are finished here (status 0, FP64 velocity,
+// integration); the others are appended to cq for k_solve_group<float, double>.
+template <int MAXN, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__restrict__ s_nr,
+             const double4 *__restrict__ s_dm, const int *__restrict__ s_row, const int *__restrict__ nb,
+             const u8 *__restrict__ nb_cnt, const float4 *__restrict__ goalpref, float4 *__restrict__ pv_out,
+             i8 *__restrict__ status, i8 *__restrict__ failed_at, u8 *__restrict__ arrived,
+             int *__restrict__ cq, const uint32_t *__restrict__ s_perm)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4 *sm_cons = reinterpret_cast<float4 *>(smem_raw);
+    float *sm_err = reinterpret_cast<float *>(sm_cons + MAXN * THREADS);
+    u8 *sm_perm = reinterpret_cast<u8 *>(sm_err + MAXN * THREADS);
+
+    const int s = blockIdx.x * THREADS + threadIdx.x;
+    const bool in_range = s < plan->n;
+    const int row = in_range ? s_row[s] : 0;
+    const bool active = in_range && row < plan->n_owned;
+    const unsigned live = __ballot_sync(0xFFFFFFFFu, active);
+    if (!active) return;
+
+    const int cnt = nb_cnt[s];
+    const NbRec<float> me_rec = s_nr[s];
+    const float4 me = me_rec.pv;
+    const double4 dm = s_dm[s]; // desired velocity (FP64, k_scatter), max_speed, avoid radius
+    u8 *perm = sm_perm + threadIdx.x;
+    float *cerr = sm_err + threadIdx.x;
+    SmemCons<float> cons{sm_cons + threadIdx.x, THREADS};
+    {
+        const uint32_t *src = s_perm + (size_t)s * (MAXN / 4);
+        for (int t = 0; 4 * t < cnt; ++t) {
+            const uint32_t w = src[t];
+            perm[(4 * t) * THREADS] = (u8)(w & 0xFFu);
+            perm[(4 * t + 1) * THREADS] = (u8)((w >> 8) & 0xFFu);
+            perm[(4 * t + 2) * THREADS] = (u8)((w >> 16) & 0xFFu);
+            perm[(4 * t + 3) * THREADS] = (u8)(w >> 24);
+        }
+    }
+    const float cap = (float)dm.z;
+    bool built = true;
+    {   // FP32 half-planes in shuffled order, each with its error bound against |v| <= cap
+        const float ri = (float)((double)me_rec.rc.x + P.half_margin);
+        const int ci = (int)me_rec.rc.y;
+        const float f0 = (float)(ci ? P.fmat[2] : P.fmat[0]), f1 = (float)(ci ? P.fmat[3] : P.fmat[1]);
+        const float inv_tau = __fdividef(1.0f, (float)P.tau), inv_dt = __fdividef(1.0f, (float)P.dt);
+        float4 q_next = me;
+        float2 rc_next = me_rec.rc;
+        if (cnt > 0) {
+            const NbRec<float> rn = s_nr[nb[(size_t)perm[0] * P.stride + s]];
+            q_next = rn.pv;
+            rc_next = rn.rc;
+        }
+        for (int pos = 0; pos < cnt; ++pos) {
+            const float4 q = q_next;
+            const float2 rc_j = rc_next;
+            if (pos + 1 < cnt) {
+                const NbRec<float> rn = s_nr[nb[(size_t)perm[(pos + 1) * THREADS] * P.stride + s]];
+                q_next = rn.pv;
+                rc_next = rn.rc;
+            }
+            const float rj = (float)((double)rc_j.x + P.half_margin);
+            float ux, uy, nx, ny, eu, en;
+            built &= vo_exit_cond(q.x - me.x, q.y - me.y, me.z - q.z, me.w - q.w, ri + rj, inv_tau, inv_dt, ux, uy,
+                                  nx, ny, eu, en);
+            const float f = rc_j.y != 0.0f ? f1 : f0;
+            const float px = __fmaf_rn(f, ux, me.z), py = __fmaf_rn(f, uy, me.w);
+            cons.set(pos, px, py, nx, ny);
+            // |(v - p).n evaluated in FP32 - the same in exact arithmetic on the FP64 half-plane|, any |v| <= cap
+            const float reach = cap + fabsf(px) + fabsf(py);
+            cerr[pos * THREADS] = f * eu + en * reach + CERT_SAFETY * 4.0f * CERT_EPS * (reach + fabsf(me.z) + fabsf(me.w));
+        }
+    }
+    float vxf, vyf;
+    int c_last, kind, j_sel;
+    const bool feasible = lp2_target_runahead_act<SmemCons<float>>(cons, cnt, cap, (float)dm.x, (float)dm.y, vxf, vyf,
+                                                                  c_last, kind, j_sel, live, built);
+    bool certified = built && feasible && kind <= 2;
+    double vx = 0.0, vy = 0.0;
+    if (certified) {
+        const double tx = dm.x, ty = dm.y, capd = dm.z;
+        if (c_last < 0) { // K:129-136
+            const double t2 = tx * tx + ty * ty;
+            if (t2 > capd * capd) {
+                const double sc = __ddiv_rn(capd, __dsqrt_rn(t2));
+                vx = tx * sc;
+                vy = ty * sc;
+            } else {
+                vx = tx;
+                vy = ty;
+            }
+        } else { // the closing formula of _lp1_target on line L = c_last, bound B = j_sel (K:98-119)
+            const double inv_tau = __ddiv_rn(1.0, P.tau), inv_dt = __ddiv_rn(1.0, P.dt);
+            double px, py, nx, ny;
+            halfplane64(s, c_last, P, s_nr, nb, perm, THREADS, inv_tau, inv_dt, px, py, nx, ny);
+            const double dx = -ny, dy = nx;
+            double t;
+            if (kind == 0) {
+                t = (tx - px) * dx + (ty - py) * dy;
+            } else {
+                double qx, qy, mx, my;
+                halfplane64(s, j_sel, P, s_nr, nb, perm, THREADS, inv_tau, inv_dt, qx, qy, mx, my);
+                const double a = dx * mx + dy * my;
+                const double b = (qx - px) * mx + (qy - py) * my;
+                t = __ddiv_rn(b, a);
+            }
+            vx = px + t * dx;
+            vy = py + t * dy;
+        }
+        // ---- the certificate, at the FP64 candidate ----
+        const float cvx = (float)vx, cvy = (float)vy;
+        const float txf = (float)tx, tyf = (float)ty;
+        // strictly inside the speed disc (an active disc is left to FP64); the unclamped start needs none
+        if (c_last >= 0) certified = cvx * cvx + cvy * cvy < cap * cap * (1.0f - 1e-4f);
+        float e_act = 0.0f;
+        for (int pos = 0; pos < cnt; ++pos) { // every inactive half-plane holds with a margin above its error
+            float px, py, nx, ny;
+            cons.get(pos, px, py, nx, ny);
+            const float e = cerr[pos * THREADS];
+            const bool act = pos == c_last || (kind != 0 && pos == j_sel);
+            const float slack = __fmaf_rn(cvx - px, nx, (cvy - py) * ny);
+            if (act) e_act += e;
+            certified = certified && (act ? e < 1.0f : slack > e);
+        }
+        if (certified && c_last >= 0) { // optimality: target - v = alpha n_L + beta n_B with alpha, beta < 0
+            float lx, ly, lnx, lny;
+            cons.get(c_last, lx, ly, lnx, lny);
+            const float gx = txf - cvx, gy = tyf - cvy;
+            const float gl = fabsf(gx) + fabsf(gy);
+            if (kind == 0) { // the target violates L: its projection is the optimum
+                const float viol = (txf - lx) * lnx + (tyf - ly) * lny;
+                certified = viol < -(e_act + CERT_SAFETY * 8.0f * CERT_EPS * (gl + 1.0f));
+            } else {
+                float bx, by, bnx, bny;
+                cons.get(j_sel, bx, by, bnx, bny);
+                const float D = lnx * bny - lny * bnx;
+                const float alpha = __fdiv_rn(gx * bny - gy * bnx, D);
+                const float beta = __fdiv_rn(lnx * gy - lny * gx, D);
+                const float m = __fdiv_rn((e_act + CERT_SAFETY * 8.0f * CERT_EPS) * (gl + fabsf(alpha) + fabsf(beta) + 1.0f),
+                                          fabsf(D));
+                certified = fabsf(D) > CERT_CROSS_MIN && alpha < -m && beta < -m;
+            }
+        }
+    }
+    if (!certified) {
+        cq[atomicAdd(&plan->cq_count, 1)] = s;
+        return;
+    }
+    status[row] = 0;
+    failed_at[row] = -1;
+    integrate_row<float, double>(row, me, vx, vy, P, goalpref, pv_out, arrived);
+}
+
+} // namespace orca

@@ -1156,8 +1156,9 @@ k_shuffle(const GridPlan *__restrict__ plan, const int *__restrict__ s_row, cons
 // the j loops of the 1-D solves are split over the group (max / min / any combinations:
 // exact and order-independent, so results are unchanged).
 template <typename S, typename R, int MAXN, int THREADS, int GL, bool PRESH>
-__global__ void __launch_bounds__(THREADS, (GL == 2 ? ORCA_SG_BLOCKS : 8))
-k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
+__device__ __forceinline__ void
+solve_group_body(int idx, bool in_range, int s,
+              GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
               const typename Vec<R>::T4 *__restrict__ s_dm,
               const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
               const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
@@ -1175,8 +1176,9 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     const int g = threadIdx.x / GL, gl = threadIdx.x % GL;
     const int gshift = (threadIdx.x & 31) - gl;
     const unsigned gmask = ((1u << GL) - 1u) << gshift;
-    const int s = s0 + blockIdx.x * NG + g;
-    const bool in_range = s < min(s1, plan->n);
+    (void)idx;
+    (void)s0;
+    (void)s1;
     const int row = in_range ? s_row[s] : 0;
     const bool active = in_range && row < plan->n_owned;
     const unsigned live = __ballot_sync(0xFFFFFFFFu, active);
@@ -1270,6 +1272,51 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
     failed_at[row] = (i8)perm[fail_pos * NG];
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
+}
+
+template <typename S, typename R, int MAXN, int THREADS, int GL, bool PRESH>
+__global__ void __launch_bounds__(THREADS, (GL == 2 ? ORCA_SG_BLOCKS : 8))
+k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
+              const typename Vec<R>::T4 *__restrict__ s_dm,
+              const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
+              const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
+              typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
+              i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
+              typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
+              typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm,
+              const uint32_t *__restrict__ s_perm)
+{
+    const int idx = s0 + blockIdx.x * (THREADS / GL) + threadIdx.x / GL;
+    solve_group_body<S, R, MAXN, THREADS, GL, PRESH>(idx, idx < min(s1, plan->n), idx, plan, P, s_nr, s_dm, s_row, ids, nb,
+                                                     nb_cnt, goalpref, pv_out, status, failed_at, arrived, fq, fq_state,
+                                                     s0, s1, lrow, fq_cons, fq_perm, s_perm);
+}
+
+// The same for a QUEUE of sorted slots (ORCA_CERT32: the agents k_solve_cert could not certify,
+// cq[0 .. plan->cq_count)): a fixed grid walks the queue, so the launch does not depend on a
+// count only the device knows.
+template <typename S, typename R, int MAXN, int THREADS, int GL, bool PRESH>
+__global__ void __launch_bounds__(THREADS, (GL == 2 ? ORCA_SG_BLOCKS : 8))
+k_solve_group_queue(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ s_nr,
+                    const typename Vec<R>::T4 *__restrict__ s_dm,
+                    const int *__restrict__ s_row, const i64 *__restrict__ ids, const int *__restrict__ nb,
+                    const u8 *__restrict__ nb_cnt, const typename Vec<S>::T4 *__restrict__ goalpref,
+                    typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
+                    i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
+                    typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
+                    typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm,
+                    const uint32_t *__restrict__ s_perm, const int *__restrict__ queue)
+{
+    constexpr int NG = THREADS / GL;
+    const int nq = plan->cq_count;
+    for (int base = blockIdx.x * NG; base < nq; base += gridDim.x * NG) { // uniform trip count per block
+        const int idx = base + threadIdx.x / GL;
+        const bool in_range = idx < nq;
+        solve_group_body<S, R, MAXN, THREADS, GL, PRESH>(idx, in_range, in_range ? queue[idx] : 0, plan, P, s_nr, s_dm,
+                                                         s_row, ids, nb, nb_cnt, goalpref, pv_out, status, failed_at,
+                                                         arrived, fq, fq_state, s0, s1, lrow, fq_cons, fq_perm, s_perm);
+        __syncthreads(); // the block's shared memory is reused by the next queue chunk
+    }
 }
 
 // Least-penetration stage for the agents the solve kernels queued, GL adjacent lanes per

@@ -19,7 +19,7 @@ from enum import Enum
 
 import numpy as np
 
-from ._lib import ORCA_F64, ORCA_MIXED, check, load, precision_code, ptr
+from ._lib import ORCA_CERT32, ORCA_F64, ORCA_MIXED, check, load, precision_code, ptr
 
 __all__ = ["HalfPlaneConstraint", "LpProblem", "LpResult", "LpStatus", "LpBatch",
            "shuffle_order", "solve_range", "solve_batch", "solve_closest_point",
@@ -105,7 +105,7 @@ def _lp_precision(precision) -> int:
     """The LP entry points take arbitrary float64 problems: 'f64' (default, bit-identical
     to the reference) or 'f32'. 'mixed' has no separate meaning here and maps to 'f64'."""
     code = precision_code(precision)
-    return ORCA_F64 if code == ORCA_MIXED else code
+    return ORCA_F64 if code in (ORCA_MIXED, ORCA_CERT32) else code
 
 
 def _prep(coff, cpts, cnrm, tgt, caps, seeds):

@@ -509,7 +509,8 @@ def run_bench(args, rank: int, world: int, local: int):
                 "n_gpus": world, "steps": args.steps, "warmup": warm,
                 "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
                 "vs_baseline": None,
-                "dtype": {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64"}[args.precision],
+                "dtype": {"mixed": "f32 state / f64 arithmetic", "f32": "f32", "f64": "f64",
+                          "cert32": "f32 state / certified f32 solve, f64 result"}[args.precision],
                 "data": "synthetic",
                 "config": {"workload": args.workload, "pedestrians": n_ped, "vehicles": n_veh,
                            "density_per_m2": density, "neighbor_radius": cfg.neighbor_radius,

@@ -39,7 +39,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.OrcaInfo) == 5 * 8 + 8 + 2 * 4 + 8 + 3 * 8
     src = open(HEADER).read()
     assert "#define ORCA_N_STAGES 6" in src and _lib.ORCA_N_STAGES == 6
-    assert "ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2" in src
+    assert "ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2, ORCA_CERT32 = 3" in src
 
 
 def test_no_cpu_fallback_without_a_device():

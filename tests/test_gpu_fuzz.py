@@ -70,7 +70,8 @@ def test_random_step_matches_oracle(seed):
     fs = O.frame_solve(st, cfg, worker_count=4, debug=True)
     assert np.all(fs.err == -1)
     k = max(cfg.max_neighbors, 1)
-    for precision in ("f64", "mixed"):
+    kept = {}
+    for precision in ("f64", "mixed", "cert32"):
         with Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False) as sim:
             sim.load(st)
             sim.step()
@@ -99,3 +100,8 @@ def test_random_step_matches_oracle(seed):
                 assert np.array_equal(pos2, st1.positions + fs1.out_v * cfg.dt)
         else:
             assert np.abs(d["out_v"] - fs.out_v).max() <= 1e-6
+            kept[precision] = (d["out_v"], d2["out_v"], d2["status"])
+    # the certified FP32 solve returns what MIXED returns, bit for bit (random radii, speeds,
+    # responsibility matrices, max_neighbors 0..32, lattices with exact ties)
+    for a, b in zip(kept["mixed"], kept["cert32"]):
+        assert np.array_equal(a, b)
