@@ -503,6 +503,37 @@ template <typename R, int GL> __device__ __forceinline__ R group_min(R v, unsign
     return v;
 }
 
+// First position p in [i, k) at which pred(p) holds, or k. The sequential scans of the stage
+// ("next violated constraint") test ONE position per iteration and every lane of a group repeats
+// the same test; here the group's lanes test GL consecutive positions at once and a group ballot
+// picks the first hit. pred evaluates exactly the expression the sequential loop evaluates at p,
+// against the same (vx, vy), so the position found -- and everything after it -- is unchanged.
+// Must be called by all lanes of the group with the same i and k.
+// Measured: with 16 lanes per problem (k_lp_batch_fallback, k up to 64) the batched LP's
+// infeasible mix went 14.5 -> 11.8 ms; with 2 or 4 lanes per agent (k_solve_group,
+// k_fallback_coop, k <= 16) the ballot per 2-4 positions costs more than the redundant test
+// (1 M plaza 0.845 -> 0.94 ms), so small groups keep the sequential scan.
+#ifndef ORCA_PARALLEL_SCAN_MIN_GL
+#define ORCA_PARALLEL_SCAN_MIN_GL 8
+#endif
+template <int GL, typename F>
+__device__ __forceinline__ int g_find_first(int i, int k, int gl, unsigned gmask, F pred)
+{
+    if constexpr (GL < ORCA_PARALLEL_SCAN_MIN_GL) {
+        for (; i < k; ++i)
+            if (pred(i)) return i;
+        return k;
+    }
+    const int gshift = __ffs((int)gmask) - 1;
+    for (; i < k; i += GL) {
+        const int p = i + gl;
+        const bool hit = p < k && pred(p);
+        const unsigned bits = (__ballot_sync(gmask, hit) & gmask) >> gshift;
+        if (bits) return i + __ffs((int)bits) - 1;
+    }
+    return k;
+}
+
 // K:74-119 with the j loop split over the group
 template <typename R, int GL, bool SHIFT, typename V>
 __device__ __forceinline__ bool g_lp1_target(const V &view, int i_pos, R zz, R cap, R tx, R ty, R &ox,
@@ -563,22 +594,26 @@ __device__ __forceinline__ bool g_lp2_target(const V &view, int k, R zz, R cap, 
         vx = tx;
         vy = ty;
     }
-    for (int i_pos = 0; i_pos < k; ++i_pos) {
-        R px, py, nx, ny;
-        view.get(i_pos, px, py, nx, ny);
-        if (SHIFT) {
-            px = px - zz * nx;
-            py = py - zz * ny;
-        }
-        if ((vx - px) * nx + (vy - py) * ny < R(0)) {
-            R nvx, nvy;
-            if (!g_lp1_target<R, GL, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy, gl, gmask)) {
-                fail_pos = i_pos;
-                return false;
+    int i_pos = 0;
+    while (true) {
+        i_pos = g_find_first<GL>(i_pos, k, gl, gmask, [&](int p) {
+            R px, py, nx, ny;
+            view.get(p, px, py, nx, ny);
+            if (SHIFT) {
+                px = px - zz * nx;
+                py = py - zz * ny;
             }
-            vx = nvx;
-            vy = nvy;
+            return (vx - px) * nx + (vy - py) * ny < R(0);
+        });
+        if (i_pos >= k) break;
+        R nvx, nvy;
+        if (!g_lp1_target<R, GL, SHIFT, V>(view, i_pos, zz, cap, tx, ty, nvx, nvy, gl, gmask)) {
+            fail_pos = i_pos;
+            return false;
         }
+        vx = nvx;
+        vy = nvy;
+        ++i_pos;
     }
     fail_pos = -1;
     return true;
@@ -606,21 +641,17 @@ __device__ __forceinline__ bool g_lp2_target_runahead(const V &view, int k, R zz
     fail_pos = -1;
     while (true) {
         bool found = false;
-        if (!done) {
-            constexpr int kRaScanUnroll = ORCA_RA_SCAN_UNROLL;
-#pragma unroll kRaScanUnroll
-            for (; i_pos < k; ++i_pos) {
+        if (!done) { // (uniform over the group)
+            i_pos = g_find_first<GL>(i_pos, k, gl, gmask, [&](int p) {
                 R px, py, nx, ny;
-                view.get(i_pos, px, py, nx, ny);
+                view.get(p, px, py, nx, ny);
                 if (SHIFT) {
                     px = px - zz * nx;
                     py = py - zz * ny;
                 }
-                if ((vx - px) * nx + (vy - py) * ny < R(0)) {
-                    found = true;
-                    break;
-                }
-            }
+                return (vx - px) * nx + (vy - py) * ny < R(0);
+            });
+            found = i_pos < k;
             done = !found;
         }
         if (!__any_sync(live, found)) break;
@@ -682,19 +713,23 @@ __device__ __forceinline__ bool g_lp2_dir(const P &proj, int m, R cap, R ox, R o
                                           unsigned gmask)
 {
     R vx = cap * ox, vy = cap * oy;
-    for (int i = 0; i < m; ++i) {
-        R px, py, nx, ny;
-        proj.get(i, px, py, nx, ny);
-        if ((vx - px) * nx + (vy - py) * ny < R(0)) {
-            R nvx, nvy;
-            if (!g_lp1_dir<R, GL, P>(proj, i, cap, ox, oy, nvx, nvy, gl, gmask)) {
-                rx = vx;
-                ry = vy;
-                return false;
-            }
-            vx = nvx;
-            vy = nvy;
+    int i = 0;
+    while (true) {
+        i = g_find_first<GL>(i, m, gl, gmask, [&](int p) {
+            R px, py, nx, ny;
+            proj.get(p, px, py, nx, ny);
+            return (vx - px) * nx + (vy - py) * ny < R(0);
+        });
+        if (i >= m) break;
+        R nvx, nvy;
+        if (!g_lp1_dir<R, GL, P>(proj, i, cap, ox, oy, nvx, nvy, gl, gmask)) {
+            rx = vx;
+            ry = vy;
+            return false;
         }
+        vx = nvx;
+        vy = nvy;
+        ++i;
     }
     rx = vx;
     ry = vy;
@@ -708,11 +743,17 @@ __device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int 
                                              R &z, int gl, unsigned gmask, int gshift)
 {
     R dist = R(0);
-    for (int i_pos = begin; i_pos < k; ++i_pos) {
+    int i_pos = begin;
+    while (true) {
+        i_pos = g_find_first<GL>(i_pos, k, gl, gmask, [&](int p) {
+            R qx, qy, mx, my;
+            view.get(p, qx, qy, mx, my);
+            return (qx - vx) * mx + (qy - vy) * my > dist;
+        });
+        if (i_pos >= k) break;
         R cpx, cpy, cnx, cny;
         view.get(i_pos, cpx, cpy, cnx, cny);
-        const R viol = (cpx - vx) * cnx + (cpy - vy) * cny;
-        if (viol > dist) {
+        {
             int m = 0;
             for (int j0 = 0; j0 < i_pos; j0 += GL) {
                 const int j_pos = j0 + gl;
@@ -748,6 +789,7 @@ __device__ __forceinline__ void g_lp3_minmax(const V &view, P &proj, int k, int 
             if (dist < R(0)) dist = R(0);
             __syncwarp(gmask); // everyone is done reading before the next sweep overwrites
         }
+        ++i_pos;
     }
     z = dist;
 }
@@ -803,15 +845,13 @@ __device__ __forceinline__ bool g_lp2_dir_ra(const P &proj, int m, R cap, R ox, 
     bool done = !enabled, ok = true;
     while (true) {
         bool found = false;
-        if (!done) {
-            for (; i < m; ++i) {
+        if (!done) { // (uniform over the group)
+            i = g_find_first<GL>(i, m, gl, gmask, [&](int p) {
                 R px, py, nx, ny;
-                proj.get(i, px, py, nx, ny);
-                if ((vx - px) * nx + (vy - py) * ny < R(0)) {
-                    found = true;
-                    break;
-                }
-            }
+                proj.get(p, px, py, nx, ny);
+                return (vx - px) * nx + (vy - py) * ny < R(0);
+            });
+            found = i < m;
             done = !found;
         }
         if (!__any_sync(live, found)) break;
@@ -843,14 +883,14 @@ __device__ __forceinline__ void g_lp3_minmax_ra(const V &view, P &proj, int k, i
     while (true) {
         bool found = false;
         R cpx = R(0), cpy = R(0), cnx = R(0), cny = R(0);
-        if (!done) {
-            for (; i_pos < k; ++i_pos) {
-                view.get(i_pos, cpx, cpy, cnx, cny);
-                if ((cpx - vx) * cnx + (cpy - vy) * cny > dist) {
-                    found = true;
-                    break;
-                }
-            }
+        if (!done) { // (uniform over the group)
+            i_pos = g_find_first<GL>(i_pos, k, gl, gmask, [&](int p) {
+                R qx, qy, mx, my;
+                view.get(p, qx, qy, mx, my);
+                return (qx - vx) * mx + (qy - vy) * my > dist;
+            });
+            found = i_pos < k;
+            if (found) view.get(i_pos, cpx, cpy, cnx, cny);
             done = !found;
         }
         if (!__any_sync(live, found)) break;
