@@ -301,6 +301,7 @@ def run_ours(args):
         if "MASTER_ADDR" not in os.environ:
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         backend = os.environ.get("ORCA_STRIPS_BACKEND") or ("nccl" if ndev >= world else "gloo")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # stdout carries the ONE JSON line only
         local = local % ndev
         torch.cuda.set_device(local)
         if backend == "nccl":
@@ -457,7 +458,8 @@ def run_ours(args):
             extras["config5_8m_single_gpu"] = other["config5_8m"]
             extras["lp_1m_resident_ms"] = {k: lp_resident(k, "f64", local, stream, 10)
                                            for k in sorted(LP_WORKLOADS)}
-        census = parity_census(state, cfg, [args.precision] + [p for p in ("f32",) if p != args.precision], local)
+        census = parity_census(state, cfg, [args.precision] + [p for p in ("cert32", "f32") if p != args.precision],
+                               local)
         ref_numba = numba_reference(state, cfg)
     else:
         ref_numba = {"skipped": "--no-extras"}

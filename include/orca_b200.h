@@ -390,9 +390,11 @@ ORCA_API int orca_strip_drop_ghosts(orca_sim *sim);
  * small raises a sticky device-side flag reported by the next orca_sync as
  * ORCA_ECAPACITY; nothing is lost silently.
  *
- * Per frame and rank (parallel/strips.py):
- *   orca_strip_pack_halo(left slab, right slab)   -> exchange ->  orca_strip_append_slab(ghost = 1) x2
- *   orca_strip_step(left slab, right slab)        -> exchange ->  orca_strip_append_slab(ghost = 0) x2
+ * Per frame and rank (parallel/strips.py), ONE exchange with each neighbour:
+ *   orca_strip_append_slab(received immigrants, ghost = 0)            from the previous exchange
+ *   orca_strip_append_slab(received halo, 1) + (own emigrants, 2)
+ *   orca_strip_step(emigrant slabs)
+ *   orca_strip_pack_halo(halo slabs)          -> exchange (emigrants + halo) with both neighbours
  * Halo slabs carry orca_halo_record_f32 (32 B; FP32 state: ORCA_MIXED, ORCA_F32) or
  * orca_halo_record_f64 (64 B; ORCA_F64): what a neighbour reads of an agent
  * (_kernels.py:525-541: position, velocity, radius, class) plus the id that orders
@@ -422,18 +424,26 @@ typedef struct orca_halo_record_f64 {
 /* sizeof the halo record this handle's precision uses (32 or 64). */
 ORCA_API int64_t orca_strip_halo_record_bytes(const orca_sim *sim);
 
-/* This handle owns x in [x_lo, x_hi) (+-inf at the ends of the domain). vmax_floor:
- * the largest max_speed of the WHOLE crowd (ghosts travel without theirs; the
- * neighbour search's displacement bound needs it). */
-ORCA_API int orca_strip_configure(orca_sim *sim, double x_lo, double x_hi, double vmax_floor);
+/* After orca_upload: this handle owns x in [x_lo, x_hi) (+-inf at the ends of the domain) and
+ * runs the slab protocol from here on. vmax_floor: the largest max_speed of the WHOLE crowd
+ * (ghosts travel without theirs; the neighbour search's displacement bound needs it).
+ * slack_rows: how many rows (ghosts + immigrants) may be appended on top of the row count the
+ * host last saw before it synchronises again -- the host's launch bound is that count +
+ * slack_rows and stays FIXED between synchronisations, so that one captured CUDA graph serves
+ * every frame in between; appends beyond it raise the sticky overflow flag. */
+ORCA_API int orca_strip_configure(orca_sim *sim, double x_lo, double x_hi, double vmax_floor,
+                                  int64_t slack_rows);
 
 /* Owned rows with x < x_lo + reach -> left slab, x >= x_hi - reach -> right slab
  * (either may be NULL: no neighbour on that side). cap = records per slab. */
 ORCA_API int orca_strip_pack_halo(orca_sim *sim, double reach, void *slab_left, void *slab_right,
                                   int64_t cap);
 
-/* Append the records of a received slab: ghost != 0 -> halo records as ghost rows,
- * ghost == 0 -> orca_agent_record as owned rows (not while ghosts are resident). */
+/* Append the records of a slab: ghost == 0 -> orca_agent_record as owned rows (received
+ * immigrants; not while ghosts are resident), ghost == 1 -> halo records as ghost rows (a
+ * received halo), ghost == 2 -> orca_agent_record as ghost rows (this handle's OWN emigrants of
+ * the last orca_strip_step: an agent that just crossed the edge is within neighbor_radius of it,
+ * so it stays here as a ghost and the neighbour does not have to send it back). */
 ORCA_API int orca_strip_append_slab(orca_sim *sim, const void *slab, int64_t cap, int ghost);
 
 /* orca_step for a strip: the step, then ONE compaction that drops the ghosts, the

@@ -140,7 +140,7 @@ def load():
     L.orca_strip_append.argtypes = [vp, vp, i64, ci]
     L.orca_strip_drop_ghosts.argtypes = [vp]
     L.orca_strip_halo_record_bytes.argtypes = [vp]
-    L.orca_strip_configure.argtypes = [vp, f64, f64, f64]
+    L.orca_strip_configure.argtypes = [vp, f64, f64, f64, i64]
     L.orca_strip_pack_halo.argtypes = [vp, f64, vp, vp, i64]
     L.orca_strip_append_slab.argtypes = [vp, vp, i64, ci]
     L.orca_strip_step.argtypes = [vp, vp, vp, i64]

@@ -69,6 +69,8 @@ struct orca_sim {
     int64_t arr_read = 0;                          // ... of which the host has fetched this many
     // strip decomposition without host round trips (orca_strip_configure / _step)
     bool strip_on = false;
+    int64_t strip_slack = 0;                // rows the host's launch bound keeps above the last known count
+    bool strip_ghosts = false;              // ghost rows are resident (the host does not know how many)
     double strip_lo = -INFINITY, strip_hi = INFINITY;
     void *mig_slab[2] = {nullptr, nullptr}; // migrant slabs of the running orca_strip_step
     int64_t mig_cap = 0;
@@ -123,6 +125,9 @@ struct orca_sim {
         bool had_bins;             // key: sorted arrays already valid (metrics mode)
         int bbox_gap;              // key: which bounding-box path the bin build takes (-1: k_bbox)
         int log_mode;              // key: the frame-log kernels are part of the sequence
+        void *mig0, *mig1;         // key: migrant slabs of orca_strip_step (null outside strips)
+        int64_t mig_cap;
+        bool strip_ghosts;         // key: the compaction that drops ghosts is part of the sequence
         int bbox_rel;              // bbox_frame - frame after the step
         cudaGraphExec_t exec;
         int new_cur, new_acur, new_pre; // host state after the step
@@ -561,17 +566,27 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->n_bound = n;
     sim->n_pre = n;
     sim->ghost_bound = 0;
+    sim->strip_on = false;
+    sim->strip_ghosts = false;
     sim->loaded = true;
     sim->binned_frame = -1;
     sim->bbox_frame = -1;
     return ORCA_OK;
 }
 
+static int fetch_plan(orca_sim *sim);
+
 extern "C" int orca_upload_pv(orca_sim *sim, int64_t n, int64_t frame, const double *positions,
                               const double *velocities)
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_upload_pv: no resident state");
-    if (n != sim->n_bound)
+    if (sim->strip_on) { // the host bound has slack: ask the device
+        int rc = fetch_plan(sim);
+        if (rc) return rc;
+        if (n != sim->h_plan->n_owned || sim->strip_ghosts)
+            return fail(sim, ORCA_EINVAL, "orca_upload_pv: n = %lld but %d owned rows are resident%s", (long long)n,
+                        sim->h_plan->n_owned, sim->strip_ghosts ? " (and ghosts)" : "");
+    } else if (n != sim->n_bound)
         return fail(sim, ORCA_EINVAL, "orca_upload_pv: n = %lld but %lld rows are resident", (long long)n,
                     (long long)sim->n_bound);
     if (n > 0 && (!positions || !velocities)) return fail(sim, ORCA_EINVAL, "orca_upload_pv: NULL array");
@@ -593,7 +608,11 @@ static int fetch_plan(orca_sim *sim)
     CK(sim, cudaMemcpyAsync(sim->h_plan, sim->plan, sizeof(GridPlan), cudaMemcpyDeviceToHost, sim->stream));
     CK(sim, cudaStreamSynchronize(sim->stream));
     const GridPlan &h = *sim->h_plan;
-    sim->n_bound = h.n;
+    // strips: the launch bound stays FIXED between two synchronisations (so one captured graph
+    // serves every frame in between) and therefore keeps room for what may arrive until the next
+    // (rounded up to 32,768 rows so that the bound -- a graph key -- changes rarely)
+    sim->n_bound = sim->strip_on ? std::min<int64_t>(sim->capacity, (((int64_t)h.n + sim->strip_slack + 32767) >> 15) << 15)
+                                 : h.n;
     if (h.err_range) return fail(sim, ORCA_ERANGE, "agent position out of indexable grid range");
     if (h.err_capacity)
         return fail(sim, ORCA_ECAPACITY, "strip exchange: a slab or the handle capacity (%lld rows) overflowed",
@@ -967,7 +986,9 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
     k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums,
                                                        sim->dst_idx);
     const int *lscan = nullptr;
-    if (sim->rows_permuted) {
+    // (a strip's storage order means nothing to the host -- agents come and go with every
+    //  migration -- so there the survivors are simply renumbered in their new physical order)
+    if (sim->rows_permuted && !sim->strip_on) {
         // survivors keep the reference's relative order: new logical row = rank among the
         // surviving logical rows
         k_keep_by_logical<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->keep, sim->lrow[a], sim->lkeep);
@@ -1038,7 +1059,7 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     int rc;
     const int64_t n = sim->n_bound;
     sim->n_pre = n;
-    if (sim->reorder_due && sim->ghost_bound == 0 && n > 1) {
+    if (sim->reorder_due && sim->ghost_bound == 0 && !sim->strip_on && n > 1) { // (strips: the driver reorders)
         rc = reorder_rows<S, R>(sim, P);
         if (rc) return rc;
         sim->reorder_due = false;
@@ -1072,13 +1093,14 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     sim->pre = sim->cur;
     sim->apre = sim->acur;
     if (sim->reorder_every > 0 && ++sim->since_reorder >= sim->reorder_every) sim->reorder_due = true;
-    if (sim->params.remove_arrivals || sim->ghost_bound > 0 || sim->mig_cap > 0) {
+    if (sim->params.remove_arrivals || sim->ghost_bound > 0 || sim->strip_ghosts || sim->mig_cap > 0) {
         const int dst = (sim->cur + 2) % 3;
         rc = compact_stage<S>(sim, out_idx, dst);
         if (rc) return rc;
         sim->cur = dst;
         sim->n_bound -= sim->ghost_bound; // ghosts never survive a step
-        sim->ghost_bound = 0;
+        sim->ghost_bound = 0;             // (strips: the bound is fixed and ghost_bound stays 0)
+        sim->strip_ghosts = false;
     } else {
         sim->cur = out_idx;
     }
@@ -1153,7 +1175,8 @@ static int step_graphed(orca_sim *sim)
     const int bbox_gap = gap64 < 0 || gap64 > 1 ? -1 : (int)gap64;
     for (auto &g : sim->graphs) {
         if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins &&
-            g.bbox_gap == bbox_gap && g.log_mode == sim->log_mode) {
+            g.bbox_gap == bbox_gap && g.log_mode == sim->log_mode && g.mig0 == sim->mig_slab[0] &&
+            g.mig1 == sim->mig_slab[1] && g.mig_cap == sim->mig_cap && g.strip_ghosts == sim->strip_ghosts) {
             CK(sim, cudaGraphLaunch(g.exec, sim->stream));
             sim->n_pre = sim->n_bound;
             sim->apre = g.acur;
@@ -1165,6 +1188,7 @@ static int step_graphed(orca_sim *sim)
             sim->bbox_frame = sim->frame + g.bbox_rel;
             sim->binned_frame = g.leaves_bins ? sim->frame : -1;
             sim->launches += g.launches;
+            sim->strip_ghosts = false;
             return ORCA_OK;
         }
     }
@@ -1176,6 +1200,10 @@ static int step_graphed(orca_sim *sim)
     g.had_bins = had_bins;
     g.bbox_gap = bbox_gap;
     g.log_mode = sim->log_mode;
+    g.mig0 = sim->mig_slab[0];
+    g.mig1 = sim->mig_slab[1];
+    g.mig_cap = sim->mig_cap;
+    g.strip_ghosts = sim->strip_ghosts;
     const int64_t l0 = sim->launches;
     if (cudaStreamBeginCapture(sim->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
         cudaGetLastError();
@@ -1207,15 +1235,23 @@ static int step_graphed(orca_sim *sim)
     return ORCA_OK;
 }
 
+// graph replay whenever the launch sequence is a function of the key (see step_graphed); in a
+// strip the launch bound is fixed between synchronisations and the driver does the reordering,
+// so frames with ghost rows resident replay too
+static int step_dispatch(orca_sim *sim)
+{
+    const bool plain_state = sim->ghost_bound == 0 && (sim->strip_on || !sim->reorder_due);
+    if (sim->use_graph && !sim->profiling && plain_state && sim->n_bound > 0) return step_graphed(sim);
+    return step_plain(sim);
+}
+
 extern "C" int orca_step(orca_sim *sim)
 {
     if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_step: sim is NULL");
     if (!sim->loaded) return fail(sim, ORCA_EINVAL, "orca_step: no state uploaded");
     if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_step: orca_set_params was not called");
     CK(sim, cudaSetDevice(sim->device));
-    if (sim->use_graph && !sim->profiling && sim->ghost_bound == 0 && sim->n_bound > 0 && !sim->reorder_due)
-        return step_graphed(sim);
-    return step_plain(sim);
+    return step_dispatch(sim);
 }
 
 // Lay the resident rows out in cell-sorted order now. orca_step does this by
@@ -1226,7 +1262,7 @@ extern "C" int orca_reorder_rows(orca_sim *sim)
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_reorder_rows: no resident state");
     if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_reorder_rows: orca_set_params was not called");
-    if (sim->ghost_bound > 0)
+    if (sim->ghost_bound > 0 || sim->strip_ghosts)
         return fail(sim, ORCA_EINVAL, "orca_reorder_rows: ghost rows are resident (drop them first)");
     CK(sim, cudaSetDevice(sim->device));
     if (sim->n_bound < 2) return ORCA_OK;
@@ -1292,7 +1328,8 @@ extern "C" int orca_run_logged(orca_sim *sim, int64_t steps, orca_frame_record *
         (traj && (traj_cap_rows < 0 || !traj_rows)) || arr_cap < 0 || (arr_cap > 0 && (!arr_ids || !arr_frames)) ||
         !n_arrivals)
         return fail(sim, ORCA_EINVAL, "orca_run_logged: bad arguments");
-    if (sim->ghost_bound > 0) return fail(sim, ORCA_EINVAL, "orca_run_logged: ghost rows are resident");
+    if (sim->ghost_bound > 0 || sim->strip_on)
+        return fail(sim, ORCA_EINVAL, "orca_run_logged: not available on a strip / with ghost rows resident");
     CK(sim, cudaSetDevice(sim->device));
     *n_records = 0;
     *n_arrivals = 0;
@@ -1408,6 +1445,7 @@ extern "C" int orca_advance_host(orca_sim *sim, int64_t n, int64_t frame, const 
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_advance_host: no resident state");
     if (!sim->have_params) return fail(sim, ORCA_EINVAL, "orca_advance_host: orca_set_params was not called");
+    if (sim->strip_on) return fail(sim, ORCA_EINVAL, "orca_advance_host: not available on a strip");
     if (n != sim->n_bound || sim->ghost_bound != 0)
         return fail(sim, ORCA_EINVAL, "orca_advance_host: n = %lld but %lld rows are resident", (long long)n,
                     (long long)sim->n_bound);
@@ -1499,6 +1537,8 @@ extern "C" int orca_strip_pack(orca_sim *sim, double x_lo, double x_hi, int remo
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_pack: no resident state");
     if (cap < 0 || (cap > 0 && !records)) return fail(sim, ORCA_EINVAL, "orca_strip_pack: bad buffer");
+    if (sim->strip_on)
+        return fail(sim, ORCA_EINVAL, "orca_strip_pack: the handle runs the slab protocol (orca_strip_configure)");
     if (remove && sim->ghost_bound > 0)
         return fail(sim, ORCA_EINVAL, "orca_strip_pack: cannot remove rows while ghosts are resident");
     CK(sim, cudaSetDevice(sim->device));
@@ -1525,6 +1565,8 @@ extern "C" int orca_strip_append(orca_sim *sim, const orca_agent_record *records
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_append: no resident state");
     if (count < 0 || (count > 0 && !records)) return fail(sim, ORCA_EINVAL, "orca_strip_append: bad arguments");
+    if (sim->strip_on)
+        return fail(sim, ORCA_EINVAL, "orca_strip_append: the handle runs the slab protocol (orca_strip_configure)");
     if (!ghost && sim->ghost_bound > 0)
         return fail(sim, ORCA_EINVAL, "orca_strip_append: owned rows cannot follow ghost rows");
     if (sim->n_bound + count > sim->capacity)
@@ -1563,14 +1605,24 @@ extern "C" int64_t orca_strip_halo_record_bytes(const orca_sim *sim)
                                              : (int64_t)sizeof(orca_halo_record_f32);
 }
 
-extern "C" int orca_strip_configure(orca_sim *sim, double x_lo, double x_hi, double vmax_floor)
+extern "C" int orca_strip_configure(orca_sim *sim, double x_lo, double x_hi, double vmax_floor, int64_t slack_rows)
 {
-    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_strip_configure: sim is NULL");
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_configure: no resident state");
+    if (slack_rows < 0) return fail(sim, ORCA_EINVAL, "orca_strip_configure: slack_rows = %lld", (long long)slack_rows);
+    if (sim->ghost_bound > 0) return fail(sim, ORCA_EINVAL, "orca_strip_configure: ghost rows are resident");
     if (!(x_lo < x_hi)) return fail(sim, ORCA_EINVAL, "orca_strip_configure: empty strip [%g, %g)", x_lo, x_hi);
     if (!(vmax_floor >= 0.0) || !std::isfinite(vmax_floor))
         return fail(sim, ORCA_EINVAL, "orca_strip_configure: vmax_floor = %g", vmax_floor);
     CK(sim, cudaSetDevice(sim->device));
+    {   // exact row count now, launch bound = count + slack from here on (see fetch_plan)
+        sim->strip_on = false;
+        int rc = fetch_plan(sim);
+        if (rc) return rc;
+    }
     sim->strip_on = true;
+    sim->strip_slack = slack_rows;
+    sim->n_bound = std::min<int64_t>(sim->capacity, ((sim->n_bound + slack_rows + 32767) >> 15) << 15);
+    sim->drop_graphs();
     sim->strip_lo = x_lo;
     sim->strip_hi = x_hi;
     k_strip_configure<<<1, 1, 0, sim->stream>>>(sim->plan, vmax_floor);
@@ -1584,7 +1636,7 @@ extern "C" int orca_strip_pack_halo(orca_sim *sim, double reach, void *slab_left
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: no resident state");
     if (!sim->strip_on) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: orca_strip_configure was not called");
     if (cap < 0 || cap > 0x7FFFFFFF || !(reach >= 0.0)) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: bad arguments");
-    if (sim->ghost_bound > 0) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: ghost rows are resident");
+    if (sim->strip_ghosts) return fail(sim, ORCA_EINVAL, "orca_strip_pack_halo: ghost rows are resident");
     CK(sim, cudaSetDevice(sim->device));
     cudaStream_t st = sim->stream;
     orca_slab_header *hl = reinterpret_cast<orca_slab_header *>(slab_left);
@@ -1619,19 +1671,20 @@ template <typename S> static int strip_append_slab_impl(orca_sim *sim, const voi
     const int a = sim->acur;
     const orca_slab_header *hdr = reinterpret_cast<const orca_slab_header *>(slab);
     cudaStream_t st = sim->stream;
-    if (ghost)
+    const int cap_rows = (int)sim->n_bound; // the launch bound: rows beyond it would never be visited
+    if (ghost == 1)
         k_strip_append_halo<S><<<grid_for(cap, 256), 256, 0, st>>>(
-            sim->plan, hdr, reinterpret_cast<const HaloRec<S> *>(hdr + 1), (int)cap, (int)sim->capacity,
+            sim->plan, hdr, reinterpret_cast<const HaloRec<S> *>(hdr + 1), (int)cap, cap_rows,
             reinterpret_cast<S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->goalpref[a]),
             reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->status[a], sim->failed[a],
             sim->hint[a], sim->lrow[a], sim->a64[a]);
     else
         k_strip_append_slab<S><<<grid_for(cap, 256), 256, 0, st>>>(
-            sim->plan, hdr, reinterpret_cast<const orca_agent_record *>(hdr + 1), (int)cap, (int)sim->capacity,
+            sim->plan, hdr, reinterpret_cast<const orca_agent_record *>(hdr + 1), (int)cap, cap_rows,
             reinterpret_cast<S4 *>(sim->pv[sim->cur]), reinterpret_cast<S4 *>(sim->goalpref[a]),
             reinterpret_cast<S2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->status[a], sim->failed[a],
             sim->hint[a], sim->lrow[a], sim->a64[a]);
-    k_after_append_slab<<<1, 1, 0, st>>>(sim->plan, hdr, (int)cap, (int)sim->capacity, ghost);
+    k_after_append_slab<<<1, 1, 0, st>>>(sim->plan, hdr, (int)cap, cap_rows, ghost);
     CKL(sim);
     sim->launches += 2;
     return ORCA_OK;
@@ -1640,19 +1693,19 @@ template <typename S> static int strip_append_slab_impl(orca_sim *sim, const voi
 extern "C" int orca_strip_append_slab(orca_sim *sim, const void *slab, int64_t cap, int ghost)
 {
     if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: no resident state");
-    if (!slab || cap < 0 || cap > 0x7FFFFFFF) return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: bad arguments");
-    if (!ghost && sim->ghost_bound > 0)
+    if (!sim->strip_on) return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: orca_strip_configure was not called");
+    if (!slab || cap < 0 || cap > 0x7FFFFFFF || ghost < 0 || ghost > 2)
+        return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: bad arguments");
+    if (!ghost && sim->strip_ghosts)
         return fail(sim, ORCA_EINVAL, "orca_strip_append_slab: owned rows cannot follow ghost rows");
     if (cap == 0) return ORCA_OK;
     CK(sim, cudaSetDevice(sim->device));
     int rc = sim->precision == ORCA_F64 ? strip_append_slab_impl<double>(sim, slab, cap, ghost)
                                         : strip_append_slab_impl<float>(sim, slab, cap, ghost);
     if (rc) return rc;
-    // the host does not know the count: its row bound grows by the slab capacity (the device
-    // clamps at the handle capacity and raises the sticky overflow flag beyond it)
-    const int64_t grown = std::min<int64_t>(sim->capacity, sim->n_bound + cap);
-    if (ghost) sim->ghost_bound += grown - sim->n_bound;
-    sim->n_bound = grown;
+    // the host does not know the count and its launch bound does not move: the device clamps at
+    // that bound and raises the sticky overflow flag beyond it (orca_sync -> ORCA_ECAPACITY)
+    if (ghost) sim->strip_ghosts = true;
     sim->binned_frame = -1;
     sim->bbox_frame = -1; // rows appended from outside
     return ORCA_OK;
@@ -1673,7 +1726,7 @@ extern "C" int orca_strip_step(orca_sim *sim, void *migrants_left, void *migrant
     sim->mig_slab[0] = migrants_left;
     sim->mig_slab[1] = migrants_right;
     sim->mig_cap = cap;
-    const int rc = step_plain(sim);
+    const int rc = step_dispatch(sim);
     sim->mig_slab[0] = sim->mig_slab[1] = nullptr;
     sim->mig_cap = 0;
     return rc;

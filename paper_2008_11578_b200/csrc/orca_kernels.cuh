@@ -1816,7 +1816,7 @@ __global__ void k_after_append_slab(GridPlan *plan, const orca_slab_header *__re
     plan->n += count;
     if (!ghost) plan->n_owned += count;
     plan->n_after = plan->n_owned;
-    plan->strip_recv[ghost ? 0 : 1] += (unsigned long long)count;
+    if (ghost != 2) plan->strip_recv[ghost ? 0 : 1] += (unsigned long long)count; // (2: own emigrants kept as ghosts)
 }
 
 // keep flags of the strip step: owned rows that have not arrived AND whose new x is still

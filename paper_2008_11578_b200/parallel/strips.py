@@ -6,26 +6,30 @@ The reference has no multi-process path at all; what must hold i
 its synchronous-update rule: an agent's new velocity depends
 only on the pre-step snapshot of the agents within neighbor_radius, so a rank that
 sees its owned agents plus every foreign agent within neighbor_radius of its strip
-computes exactly what a single device would. Per step and per rank:
+computes exactly what a single device would. Per frame and per rank, ONE exchange with each
+adjacent strip:
 
-  1. halo     owned agents within neighbor_radius of a strip edge are packed
-              into that side's HALO SLAB (orca_strip_pack_halo: 32-byte records --
-              position, velocity, radius, class, id); the slabs are swapped with
-              the two adjacent strips; what arrives is appended as ghost rows
-              (orca_strip_append_slab, ghost=1)
-  2. step     orca_strip_step solves the owned agents, then ONE compaction drops
-              the ghosts, the arrivals and the owned agents whose new x left the
-              strip -- those go into the MIGRANT SLABS as full 96-byte records
-  3. migrate  the migrant slabs are swapped and appended as owned rows
+  1. append   what the last exchange brought: immigrants as owned rows, the neighbour's halo as
+              ghost rows -- and this rank's OWN emigrants of the last step as ghosts too (an agent
+              that just crossed the edge is still within neighbor_radius of it, so the neighbour
+              never has to send it back)
+  2. step     orca_strip_step solves the owned agents, then ONE compaction drops the ghosts, the
+              arrivals and the owned agents whose new x left the strip -- those go into the
+              EMIGRANT SLABS as full 96-byte records
+  3. halo     the owned agents within neighbor_radius of a strip edge, at their NEW positions, are
+              packed into that side's HALO SLAB (32-byte records: position, velocity, radius,
+              class, id)
+  4. exchange emigrant + halo slab of each side travel together, one grouped send/recv
 
-The host is not in this loop. A slab is a fixed-capacity device buffer whose
-32-byte header carries the record count; the packing kernels count with atomics,
-the whole slab travels (a size both ranks know without asking), the appending
-kernels read the count from the header. Each exchange is one grouped NCCL
-send/recv with the two adjacent strips (no collective on the data path) ordered
-against the handle's stream on the device. The host only keeps an upper bound on
-its row count and re-synchronises every `resync_every` frames (default 16), which
-is also when a slab overflow -- a sticky device-side flag -- surfaces as an error.
+The host is not in this loop. A slab is a fixed-capacity device buffer whose 32-byte header
+carries the record count; the packing kernels count with atomics, the whole slab travels (a
+size both ranks know without asking), the appending kernels read the count from the header.
+The exchange is ordered against the handle's stream on the device (NCCL) and involves the two
+adjacent strips only -- no collective on the data path. The host keeps a launch bound that
+stays FIXED between two synchronisations (row count last seen + slack), so the frames in
+between replay one captured CUDA graph, and re-synchronises every `resync_every` frames
+(default 16), which is also when a slab overflow -- a sticky device-side flag -- surfaces as an
+error.
 
 `StripDriver` holds this protocol and is written against a small ops interface so
 the same code runs on NCCL with the CUDA handle (DeviceStripOps) and, in the CPU
@@ -127,9 +131,9 @@ class DeviceStripOps:
             self.stream = torch.cuda.Stream(dev)   # "the handle's own stream" -- take a real one
         sim.set_stream(self.stream)
 
-    def configure(self, x_lo: float, x_hi: float, vmax_floor: float):
-        check(self._L.orca_strip_configure(self.sim._h, float(x_lo), float(x_hi), float(vmax_floor)),
-              self.sim._h)
+    def configure(self, x_lo: float, x_hi: float, vmax_floor: float, slack_rows: int):
+        check(self._L.orca_strip_configure(self.sim._h, float(x_lo), float(x_hi), float(vmax_floor),
+                                           int(slack_rows)), self.sim._h)
 
     @staticmethod
     def _p(t):
@@ -139,9 +143,10 @@ class DeviceStripOps:
         check(self._L.orca_strip_pack_halo(self.sim._h, float(reach), self._p(slab_left),
                                            self._p(slab_right), int(cap)), self.sim._h)
 
-    def append_slab(self, slab, cap: int, ghost: bool):
-        check(self._L.orca_strip_append_slab(self.sim._h, self._p(slab), int(cap), 1 if ghost else 0),
-              self.sim._h)
+    def append_slab(self, slab, cap: int, kind: int):
+        """kind 0: immigrants (agent records) as owned rows; 1: a received halo as ghosts;
+        2: this handle's own emigrants (agent records) as ghosts."""
+        check(self._L.orca_strip_append_slab(self.sim._h, self._p(slab), int(cap), int(kind)), self.sim._h)
 
     def step(self, mig_left, mig_right, cap: int):
         check(self._L.orca_strip_step(self.sim._h, self._p(mig_left), self._p(mig_right), int(cap)),
@@ -185,38 +190,45 @@ class StripDriver:
         self.mig_cap = int(migrant_capacity if migrant_capacity is not None else halo_capacity)
         hb = SLAB_HEADER_BYTES + self.halo_cap * int(ops.halo_record_bytes)
         mb = SLAB_HEADER_BYTES + self.mig_cap * RECORD_BYTES
-
-        def slabs(nbytes):
-            return {s: (torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        self._mb = mb
+        # per side ONE send and ONE receive buffer: [emigrant slab | halo slab]
+        def buffers():
+            return {s: (torch.zeros(mb + hb, dtype=torch.uint8, device=self.device)
                         if self.peer[s] is not None else None) for s in self.SIDES}
-        self.send_halo, self.recv_halo = slabs(hb), slabs(hb)
-        self.send_mig, self.recv_mig = slabs(mb), slabs(mb)
+        self.send, self.recv = buffers(), buffers()
+        view = lambda d, lo, hi: {s: (t[lo:hi] if t is not None else None) for s, t in d.items()}  # noqa: E731
+        self.send_mig, self.send_halo = view(self.send, 0, mb), view(self.send, mb, mb + hb)
+        self.recv_mig, self.recv_halo = view(self.recv, 0, mb), view(self.recv, mb, mb + hb)
         self.frames = 0
         self.reorder_every = 64          # frames between row reorderings (no ghosts resident then)
         self.resync_every = int(resync_every)
         self.host_syncs = 0
+        self._pending = False            # an exchange has happened and its slabs are not appended yet
         # gloo moves host memory only: device slabs are staged through the host (the 2-process
         # test on one GPU); NCCL sends them as they are
         self._stage = (self.device.type == "cuda" and dist.is_available() and dist.is_initialized()
                        and dist.get_backend(group) == "gloo")
-        ops.configure(self.lo, self.hi, float(vmax))
+        # rows that may be appended on top of the count the host last saw: two halos at any time,
+        # immigrants of every frame until the next synchronisation
+        slack = 2 * self.halo_cap + 2 * self.mig_cap * (max(self.resync_every, 1) + 1)
+        ops.configure(self.lo, self.hi, float(vmax), slack)
 
-    # -- one exchange with both neighbours: fixed-size slabs, one grouped call ----
-    def _swap(self, send: dict, recv: dict):
+    # -- one exchange with both neighbours: fixed-size buffers, one grouped call ----
+    def _swap(self):
         p2p, staged = [], []
         for s in self.SIDES:
             p = self.peer[s]
             if p is None:
                 continue
             if self._stage:
-                out = send[s].cpu()                      # (synchronises: test transport only)
+                out = self.send[s].cpu()                 # (synchronises: test transport only)
                 inn = torch.empty_like(out)
-                staged.append((recv[s], inn))
+                staged.append((self.recv[s], inn))
                 p2p += [dist.P2POp(dist.isend, out, p, group=self.group),
                         dist.P2POp(dist.irecv, inn, p, group=self.group)]
             else:
-                p2p += [dist.P2POp(dist.isend, send[s], p, group=self.group),
-                        dist.P2POp(dist.irecv, recv[s], p, group=self.group)]
+                p2p += [dist.P2POp(dist.isend, self.send[s], p, group=self.group),
+                        dist.P2POp(dist.irecv, self.recv[s], p, group=self.group)]
         if not p2p:
             return
         # NCCL: the grouped send/recv is ordered after the packing kernels through the current
@@ -227,29 +239,49 @@ class StripDriver:
         for dst, src in staged:
             dst.copy_(src)
 
-    def _exchange(self, send: dict, recv: dict):
+    def exchange(self):
         stream = getattr(self.ops, "stream", None)
         if stream is None:
-            return self._swap(send, recv)
-        with torch.cuda.stream(stream):      # the handle's stream is the current one for the transport
-            return self._swap(send, recv)
+            self._swap()
+        else:
+            with torch.cuda.stream(stream):  # the handle's stream is the current one for the transport
+                self._swap()
+        self._pending = True
 
     # -- protocol phases (split so a test can drive several ranks in one process) ------
-    def pack_halo(self):
+    def append_received(self):
+        """Phase 1: immigrants as owned rows, then the ghosts (received halo, own emigrants)."""
+        if not self._pending:
+            return
+        for s in self.SIDES:
+            if self.peer[s] is not None:
+                self.ops.append_slab(self.recv_mig[s], self.mig_cap, 0)
+        for s in self.SIDES:
+            if self.peer[s] is not None:
+                self.ops.append_slab(self.recv_halo[s], self.halo_cap, 1)
+                self.ops.append_slab(self.send_mig[s], self.mig_cap, 2)
+        self._pending = False
+
+    def step_and_pack(self):
+        """Phases 2 and 3: the step with its emigrant slabs, then the halo of the new positions."""
+        self.ops.step(self.send_mig["left"], self.send_mig["right"], self.mig_cap)
         self.ops.pack_halo(self.reach, self.send_halo["left"], self.send_halo["right"], self.halo_cap)
 
-    def unpack_halo(self):
+    def _zero_header(self, slab):
+        stream = getattr(self.ops, "stream", None)
+        if stream is None:
+            slab[:SLAB_HEADER_BYTES].zero_()
+        else:
+            with torch.cuda.stream(stream):      # ordered with the handle's kernels
+                slab[:SLAB_HEADER_BYTES].zero_()
+
+    def prime(self):
+        """Before the first frame: nobody has emigrated yet, the halo of the initial positions
+        goes out (the emigrant slabs travel empty)."""
         for s in self.SIDES:
             if self.peer[s] is not None:
-                self.ops.append_slab(self.recv_halo[s], self.halo_cap, True)
-
-    def step_and_pack_migrants(self):
-        self.ops.step(self.send_mig["left"], self.send_mig["right"], self.mig_cap)
-
-    def unpack_migrants(self):
-        for s in self.SIDES:
-            if self.peer[s] is not None:
-                self.ops.append_slab(self.recv_mig[s], self.mig_cap, False)
+                self._zero_header(self.send_mig[s])
+        self.ops.pack_halo(self.reach, self.send_halo["left"], self.send_halo["right"], self.halo_cap)
 
     def begin_frame(self):
         if self.reorder_every and self.frames % self.reorder_every == 0 and hasattr(self.ops, "reorder"):
@@ -264,15 +296,26 @@ class StripDriver:
         self.host_syncs += 1
         self.ops.resync()
 
+    def flush(self):
+        """Append what the last exchange brought as OWNED rows only (the immigrants), so that
+        the resident state is the strip's agents and nothing else -- before reading it back."""
+        if self._pending:
+            for s in self.SIDES:
+                if self.peer[s] is not None:
+                    self.ops.append_slab(self.recv_mig[s], self.mig_cap, 0)
+                    # (consumed: a later append_received must not add them again)
+                    self._zero_header(self.recv_mig[s])
+        self.resync()
+
     def step(self):
         """One frame of the whole strip-decomposed crowd, as seen by this rank."""
+        if self.frames == 0 and not self._pending:
+            self.prime()
+            self.exchange()
         self.begin_frame()
-        self.pack_halo()
-        self._exchange(self.send_halo, self.recv_halo)
-        self.unpack_halo()
-        self.step_and_pack_migrants()
-        self._exchange(self.send_mig, self.recv_mig)
-        self.unpack_migrants()
+        self.append_received()
+        self.step_and_pack()
+        self.exchange()
         self.end_frame()
 
 
@@ -298,7 +341,7 @@ def _slab_capacities(cfg, n_local: int, height: float, density: float, vmax: flo
 def _strip_sim(cfg, state, args, local, stream, halo_cap, mig_cap, resync_every):
     from .. import Simulation
     n_local = state.active_count
-    capacity = n_local + 2 * halo_cap + 2 * mig_cap * (resync_every + 1) + max(65536, n_local // 8)
+    capacity = n_local + 2 * halo_cap + 2 * mig_cap * (resync_every + 1) + max(131072, n_local // 8)
     sim = Simulation(cfg, capacity=capacity, precision=args.precision, device=local,
                      remove_arrivals=False, compute_metrics=False, stream=stream)
     sim.load(state)
@@ -408,6 +451,7 @@ def run_bench(args, rank: int, world: int, local: int):
     g0, m0 = drv.ops.stats()
     sampler = args.make_sampler() if hasattr(args, "make_sampler") else None
     dev_ms, wall_ms, enq_ms, syncs = _timed(drv, sim, stream, args.steps, device, sampler)
+    drv.flush()
     info = sim.info()
     g1, m1 = drv.ops.stats()
     tot = torch.tensor([float(info.active_agents), float(info.kernel_launches - l0), float(g1 - g0),
@@ -418,6 +462,7 @@ def run_bench(args, rank: int, world: int, local: int):
     # ---- correctness gate: id-keyed digest over all ranks vs the same crowd on ONE device ----
     verify = None
     if not getattr(args, "no_verify", False):
+        drv.flush()
         got_hash, got_n = _gather_hash(sim, device)
         want = torch.zeros(2, dtype=torch.int64, device=rdev)
         if rank == 0:
@@ -465,7 +510,7 @@ def run_bench(args, rank: int, world: int, local: int):
     # ---- e2e: the same step with this rank's positions / velocities going up from pinned host
     # memory and coming back every frame (what a host-side caller of a strip-decomposed crowd pays)
     e2e_steps = max(3, min(args.steps, getattr(args, "e2e_steps", 20)))
-    drv.resync()
+    drv.flush()
     pos, vel = sim.positions_velocities()
     h2d = d2h = 0
     for k in range(2 + e2e_steps):
@@ -477,7 +522,7 @@ def run_bench(args, rank: int, world: int, local: int):
         sim.load_pv(pos, vel, int(sim.info().frame))
         h2d += pos.nbytes + vel.nbytes
         drv.step()
-        drv.resync()
+        drv.flush()
         pos, vel = sim.positions_velocities()
         d2h += pos.nbytes + vel.nbytes
     torch.cuda.synchronize()

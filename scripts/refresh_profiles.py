@@ -12,7 +12,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
-tag = sys.argv[1] if len(sys.argv) > 1 else "g"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 
 
 def summary(kind, src):
@@ -27,32 +27,43 @@ def last_json_line(path):
 
 
 # bench lines
-for name in ("mixed", "f32", "f64", "ref"):
-    with open(os.path.join(P, f"bench_r01_{name}.json"), "w") as f:
+for name in ("mixed", "cert32", "f32", "f64", "ref"):
+    with open(os.path.join(P, f"bench_{tag}_{name}.json"), "w") as f:
         f.write(last_json_line(os.path.join(G, f"g_{name}.json")) + "\n")
-shutil.copy(os.path.join(G, "g_configs.jsonl"), os.path.join(P, "bench_r01_configs.jsonl"))
+for name in ("configs", "lp", "strips"):
+    shutil.copy(os.path.join(G, f"g_{name}.jsonl"), os.path.join(P, f"bench_{tag}_{name}.jsonl"))
 
 # ncu launch list and full captures
-head_l = (f"# Round 1 ({tag}) — ncu launch list, 1,048,576 agents, mixed precision, final state of the round\n\n"
+head_l = (f"# {tag} — ncu launch list, 1,048,576 agents, mixed precision, final state of the round\n\n"
           "Command: `ORCA_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python "
           "bench.py --steps 3 --warmup 3 --resident-only` (per-launch times are cold-cache and serialised: compare "
           "shares; `k_import_*`, `k_iota`, `k_bbox`, `k_begin_bins`, `k_permute_rows` run once after the upload; the "
           "first `k_gather` launch searches for every agent, ~0.9 ms, the others ~25 us).\n\n")
-with open(os.path.join(P, f"r01_{tag}_launches_mixed_1m.md"), "w") as f:
+with open(os.path.join(P, f"{tag}_launches_mixed_1m.md"), "w") as f:
     f.write(head_l + summary("launches", os.path.join(G, "g_launches.csv")))
-head_f = (f"# Round 1 ({tag}) — ncu --set full, kernels of the step, 1,048,576 agents, mixed precision, final state "
+head_f = (f"# {tag} — ncu --set full, kernels of the step, 1,048,576 agents, mixed precision, final state "
           "of the round\n\nCommand: `ORCA_GRAPH=0 ncu --set full --clock-control none --import-source on -k "
           "regex:\"k_solve_group|k_gather_fast32|k_scatter|k_fallback_coop|k_count|k_gather\" -s 40 -c 7 python "
           "bench.py --steps 3 --warmup 4 --resident-only`\n\n")
-with open(os.path.join(P, f"r01_{tag}_full_mixed_1m.md"), "w") as f:
+with open(os.path.join(P, f"{tag}_full_mixed_1m.md"), "w") as f:
     f.write(head_f + summary("full", os.path.join(G, "g_full.ncu-rep")))
-head_d = (f"# Round 1 ({tag}) — ncu --set full, solve and fallback kernels, 266,240 agents at 2.0 /m2 (79 % of the "
+head_d = (f"# {tag} — ncu --set full, solve and fallback kernels, 266,240 agents at 2.0 /m2 (79 % of the "
           "agents in the least-penetration stage), mixed precision\n\nCommand: `ORCA_GRAPH=0 ncu --set full "
           "--clock-control none -k regex:\"k_solve_group|k_fallback_coop\" -s 12 -c 3 python bench.py --steps 3 "
           "--warmup 4 --resident-only --workload config3_262k_d2`\n\n")
-with open(os.path.join(P, f"r01_{tag}_full_mixed_dense2.md"), "w") as f:
+with open(os.path.join(P, f"{tag}_full_mixed_dense2.md"), "w") as f:
     f.write(head_d + summary("full", os.path.join(G, "g_full_d2.ncu-rep")))
 
+
+with open(os.path.join(P, f"{tag}_full_cert32_1m.md"), "w") as f:
+    f.write(f"# {tag} -- ncu --set full, the solve stage of ORCA_CERT32 (k_shuffle, k_solve_cert, k_solve_group_queue), "
+            "1,048,576 agents\n\nCommand: `ORCA_GRAPH=0 ncu --set full --clock-control none -k "
+            "regex:\"k_solve_cert|k_solve_group_queue|k_shuffle\" -s 6 -c 3 python bench.py --steps 3 --warmup 4 "
+            "--resident-only --precision cert32`\n\n" + summary("full", os.path.join(G, "g_full_cert.ncu-rep")))
+with open(os.path.join(P, f"{tag}_full_lp_infeasible.md"), "w") as f:
+    f.write(f"# {tag} -- ncu --set full, batched LP (BASELINE config 4), 1,048,576 problems, infeasible mix, FP64\n\n"
+            "Command: `ncu --set full --clock-control none -k regex:k_lp_batch -s 4 -c 2 python bench.py --workload "
+            "lp_1m_infeasible --steps 2 --warmup 3`\n\n" + summary("full", os.path.join(G, "g_full_lp.ncu-rep")))
 
 # traffic.json: DRAM bytes per launch and issue / pipe utilisation of the 1 M mixed capture
 def raw_rows(rep):
@@ -71,7 +82,7 @@ def val(r, key):
     return v * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}.get(u, 1.0)
 
 
-entry = {"source": f"profiles/r01_{tag}_full_mixed_1m.md", "ncu": {}}
+entry = {"source": f"profiles/{tag}_full_mixed_1m.md", "ncu": {}}
 for r in rows:
     name = r[col["Kernel Name"]]
     short = name.split("<")[0].split()[-1].split("::")[-1]

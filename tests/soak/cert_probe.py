@@ -1,5 +1,5 @@
 import sys, os, numpy as np, time
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from oracle import oracle as O
 from paper_2008_11578_b200 import Simulation
 from paper_2008_11578_b200.synth import make_workload

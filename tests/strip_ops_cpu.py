@@ -76,7 +76,7 @@ class OracleStripOps:
         self.ghosts = self.migrants = 0
         self.overflow = False
 
-    def configure(self, x_lo, x_hi, vmax_floor):
+    def configure(self, x_lo, x_hi, vmax_floor, slack_rows):
         self.lo, self.hi = x_lo, x_hi
 
     def pack_halo(self, reach, slab_left, slab_right, cap):
@@ -96,13 +96,14 @@ class OracleStripOps:
             rec["radius"][:m], rec["id"][:m] = st.radii[mask][:m], st.ids[mask][:m]
             rec["class_code"][:m] = st.class_codes[mask][:m]
 
-    def append_slab(self, slab, cap, ghost):
+    def append_slab(self, slab, cap, kind):
+        """kind 0: immigrants (owned); 1: a received halo (ghosts); 2: own emigrants as ghosts."""
         h = _header(slab)
         count = int(h["count"][0])
         if count > cap or int(h["overflow"][0]):
             self.overflow = True
         count = min(count, cap)
-        if ghost:
+        if kind == 1:
             g = _records(slab, HALO_DTYPE_F64, cap)[:count]
             rec = np.zeros(count, dtype=RECORD_DTYPE)
             for f in ("x", "y", "vx", "vy", "radius", "id", "class_code"):
@@ -110,11 +111,12 @@ class OracleStripOps:
             rec["goal_x"], rec["goal_y"] = g["x"], g["y"]
             self.ghosts += count
         else:
-            assert self.state.ids.shape[0] == self.n_owned
             rec = _records(slab, RECORD_DTYPE, cap)[:count].copy()
-            self.migrants += count
+            if kind == 0:
+                assert self.state.ids.shape[0] == self.n_owned
+                self.migrants += count
         append_records(self.state, rec)
-        if not ghost:
+        if kind == 0:
             self.n_owned += count
 
     def step(self, mig_left, mig_right, cap):
@@ -207,7 +209,7 @@ def gloo_worker(rank, world, port, steps, out_dir):
                           resync_every=4)
         for _ in range(steps):
             drv.step()
-        drv.resync()
+        drv.flush()
         out = ops.state
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=out.ids, positions=out.positions,
                  velocities=out.velocities, frame=out.frame, lo=drv.lo, hi=drv.hi,
@@ -243,7 +245,7 @@ def gpu_gloo_worker(rank, world, port, steps, out_dir, precision):
             assert drv._stage
             for _ in range(steps):
                 drv.step()
-            drv.resync()
+            drv.flush()
             out = sim.state()
             g, m = drv.ops.stats()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=out.ids, positions=out.positions,

@@ -21,34 +21,36 @@ SIDE = {"left": "right", "right": "left"}
 
 
 def lockstep(drivers, steps, reorder_every=3):
-    """Drive all ranks phase by phase; rank r's `right` slab goes to rank r+1's `left`
+    """Drive all ranks phase by phase; rank r's `right` buffer goes to rank r+1's `left`
     (a device-to-device copy on the legacy stream in place of the NCCL send/recv)."""
-    def swap(which):
+    def exchange():
         torch.cuda.synchronize()
-        for r, d in enumerate(drivers):
+        for d in drivers:
             for side in ("left", "right"):
                 if d.peer[side] is not None:
-                    getattr(drivers[d.peer[side]], "recv_" + which)[SIDE[side]].copy_(
-                        getattr(d, "send_" + which)[side])
+                    drivers[d.peer[side]].recv[SIDE[side]].copy_(d.send[side])
         torch.cuda.synchronize()
+        for d in drivers:
+            d._pending = True
 
     for d in drivers:
         d.reorder_every = reorder_every
+    if drivers[0].frames == 0:
+        for d in drivers:
+            d.prime()
+        exchange()
     for _ in range(steps):
         for d in drivers:
             d.begin_frame()
         for d in drivers:
-            d.pack_halo()
-        swap("halo")
+            d.append_received()
         for d in drivers:
-            d.unpack_halo()
-        for d in drivers:
-            d.step_and_pack_migrants()
-        swap("mig")
-        for d in drivers:
-            d.unpack_migrants()
+            d.step_and_pack()
+        exchange()
         for d in drivers:
             d.end_frame()
+    for d in drivers:
+        d.flush()
 
 
 def build_strips(st, cfg, precision, world, halo_cap, mig_cap, resync_every=4, capacity=None):
@@ -79,8 +81,6 @@ def test_strips_on_device_equal_single_handle(precision, world):
     sims, drivers, b = build_strips(st, cfg, precision, world, halo_cap=n, mig_cap=n // 4)
     assert drivers[0].ops.halo_record_bytes == (64 if precision == "f64" else 32)
     lockstep(drivers, steps)
-    for d in drivers:
-        d.resync()
     parts = [s.state() for s in sims]
     for r, p in enumerate(parts):
         assert p.frame == steps
@@ -94,7 +94,7 @@ def test_strips_on_device_equal_single_handle(precision, world):
     stats = [d.ops.stats() for d in drivers]
     assert sum(g for g, _m in stats) > 0 and sum(m for _g, m in stats) > 0     # both paths exercised
     assert sum(int(s.info().lp_fallbacks) for s in sims) == want.lp_fallbacks
-    assert all(d.host_syncs <= steps // 4 + 1 for d in drivers)                # the host is not in the frame loop
+    assert all(d.host_syncs <= steps // 4 + 1 for d in drivers)                # (+1: the final flush)
     # the digest bench.py compares across ranks
     assert sum(state_hash(p.ids, p.positions, p.velocities) for p in parts) % (1 << 64) == \
         state_hash(want.ids, want.positions, want.velocities)
@@ -138,18 +138,15 @@ def test_slab_overflow_is_reported_not_silent():
     st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
     # halo slabs far too small for the ~1,000 agents within neighbor_radius of the edge
     sims, drivers, _b = build_strips(st, cfg, "mixed", 2, halo_cap=16, mig_cap=4096, resync_every=0)
-    lockstep(drivers, 1)
     with pytest.raises(OrcaError) as ei:
-        drivers[0].resync()
+        lockstep(drivers, 1)
     assert ei.value.code == -5 and "overflow" in str(ei.value)
     for s in sims:
         s.close()
-    # migrant slabs too small: the rows that do not fit stay put and the flag is raised
+    # emigrant slabs too small: the rows that do not fit stay put and the flag is raised
     sims, drivers, _b = build_strips(st, cfg, "mixed", 2, halo_cap=8192, mig_cap=1, resync_every=0)
-    lockstep(drivers, 6)
     with pytest.raises(OrcaError) as ei:
-        for d in drivers:
-            d.resync()
+        lockstep(drivers, 6)
     assert ei.value.code == -5
     for s in sims:
         s.close()
@@ -166,7 +163,9 @@ def test_halo_slab_layout_and_refusals():
             assert ops.halo_record_bytes == dtype.itemsize
             with pytest.raises(OrcaError):
                 ops.pack_halo(3.0, None, None, n)                     # not configured yet
-            ops.configure(-np.inf, mid, 2.0)
+            with pytest.raises(OrcaError):
+                ops.append_slab(torch.zeros(64, dtype=torch.uint8, device="cuda"), 1, 1)
+            ops.configure(-np.inf, mid, 2.0, 2 * n)
             slab = torch.zeros(_lib.SLAB_HEADER_BYTES + n * dtype.itemsize, dtype=torch.uint8, device="cuda")
             ops.pack_halo(cfg.neighbor_radius, None, slab, n)
             raw = slab.cpu().numpy()
@@ -184,10 +183,10 @@ def test_halo_slab_layout_and_refusals():
             rec["x"] += 0.37
             rec["id"] += 10**6
             slab.copy_(torch.from_numpy(raw))
-            ops.append_slab(slab, n, True)
+            ops.append_slab(slab, n, 1)
             assert int(sim.info().active_agents) == n
             with pytest.raises(OrcaError):
-                ops.append_slab(slab, n, False)                       # owned rows cannot follow ghosts
+                ops.append_slab(slab, n, 0)                           # owned rows cannot follow ghosts
             sim.set_config(cfg, remove_arrivals=False, compute_metrics=True)
             mig = torch.zeros(_lib.SLAB_HEADER_BYTES + n * RECORD_BYTES, dtype=torch.uint8, device="cuda")
             with pytest.raises(OrcaError) as ei:
@@ -202,6 +201,19 @@ def test_halo_slab_layout_and_refusals():
             assert left.ids.shape[0] + cnt == n                       # every agent is in exactly one place
             assert np.all(left.positions[:, 0] < mid) and np.all(out["x"] >= mid)
             assert np.array_equal(np.sort(np.concatenate([left.ids, out["id"]])), np.sort(st.ids))
+            # own emigrants stay as ghosts (kind 2); immigrants (kind 0) come back as owned rows
+            ops.append_slab(mig, n, 2)
+            assert int(sim.info().active_agents) == n - cnt
+            ops.step(None, mig, n)                                    # drops the ghosts again
+            with Simulation(cfg, capacity=2 * n, precision=precision, remove_arrivals=False) as other:
+                other.load(S.take(st, np.arange(n) < 4))
+                o2 = DeviceStripOps(other)
+                o2.configure(mid, np.inf, 2.0, 2 * n)
+                back = torch.from_numpy(moved).cuda()
+                o2.append_slab(back, n, 0)
+                got = other.state()
+                assert got.ids.shape[0] == 4 + cnt and np.array_equal(got.ids[4:], out["id"])
+                assert np.array_equal(got.goals[4:, 0], out["goal_x"]) and np.array_equal(got.radii[4:], out["radius"])
 
 
 def test_two_processes_one_gpu_over_gloo(tmp_path):
