@@ -12,12 +12,11 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
-import torch  # noqa: E402
 
 import strip_ops_cpu as S  # noqa: E402
-from test_gpu_strips import lockstep  # noqa: E402
+from test_gpu_strips import build_strips, lockstep  # noqa: E402
 from paper_2008_11578_b200 import Simulation  # noqa: E402
-from paper_2008_11578_b200.parallel.strips import DeviceStripOps, StripDriver, strip_bounds  # noqa: E402
+from paper_2008_11578_b200.parallel.strips import strip_bounds  # noqa: E402
 
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 40
@@ -38,15 +37,9 @@ for seed in range(first, first + count):
         bounds = strip_bounds(st.positions[:, 0], world)
         b = [-np.inf] + list(bounds) + [np.inf]
         if min(b[i + 1] - b[i] for i in range(world)) < cfg.neighbor_radius + 1.0:
-            continue                                   # strips must be wider than the halo reach
-        sims, drivers = [], []
-        for r in range(world):
-            mine = (st.positions[:, 0] >= b[r]) & (st.positions[:, 0] < b[r + 1])
-            sim = Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False)
-            sim.load(S.take(st, mine))
-            sims.append(sim)
-            drivers.append(StripDriver(DeviceStripOps(sim), r, world, bounds, cfg.neighbor_radius,
-                                       torch.device("cuda", 0), halo_capacity=n))
+            continue                                   # strips must be wider than the halo reach (StripDriver checks)
+        sims, drivers, _b = build_strips(st, cfg, precision, world, halo_cap=n, mig_cap=n,
+                                         resync_every=int(rng.integers(1, 6)), capacity=5 * n)
         lockstep(drivers, steps)
         ran += 1
         parts = [s.state() for s in sims]
