@@ -301,19 +301,35 @@ def run_ours(args):
         if "MASTER_ADDR" not in os.environ:
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         backend = os.environ.get("ORCA_STRIPS_BACKEND") or ("nccl" if ndev >= world else "gloo")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # stdout carries the ONE JSON line only
         local = local % ndev
         torch.cuda.set_device(local)
+        # NCCL prints its version banner on stdout (at communicator creation): keep file
+        # descriptor 1 for the ONE JSON line
+        sys.stdout.flush()
+        saved_stdout = os.dup(1)
+        os.dup2(2, 1)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
         from paper_2008_11578_b200.parallel import strips
         args.make_sampler = lambda: ClockSampler(local)
+        line = None
         try:
-            return strips.run_bench(args, rank, world, local)
+            line = strips.run_bench(args, rank, world, local)
         finally:
             dist.destroy_process_group()
+            sys.stdout.flush()
+            try:                              # NCCL's banner sits in libc's stdout buffer: flush it to stderr
+                import ctypes
+                ctypes.CDLL(None).fflush(None)
+            except Exception:
+                pass
+            os.dup2(saved_stdout, 1)
+            os.close(saved_stdout)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
     torch.cuda.set_device(local)
 
     state, cfg, wl = build_workload(args.workload)

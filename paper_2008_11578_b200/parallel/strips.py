@@ -402,8 +402,8 @@ def run_bench(args, rank: int, world: int, local: int):
     of (position, velocity) over all ranks is compared with the digest of the same crowd stepped
     the same number of frames on ONE device by rank 0 (SURVEY.md s8(e) correctness gate; the
     multi-rank analogue of pkg/tests/test_engine.py:197). Skipped (null) when the whole crowd
-    does not fit rank 0's GPU next to its strip, or with --no-verify. Prints the JSON line on
-    rank 0."""
+    does not fit rank 0's GPU next to its strip, or with --no-verify. Returns the JSON line (a
+    dict) on rank 0, None elsewhere."""
     from .. import Simulation
     from ..synth import CONFIGS, make_workload
 
@@ -539,6 +539,7 @@ def run_bench(args, rank: int, world: int, local: int):
     sim.profile_stages(False)
     stage_ms = {k: v / max(covered, 1) for k, v in stage_ms.items()}
     dist.barrier()
+    line = None
     if rank == 0:
         hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         pk = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
@@ -590,5 +591,5 @@ def run_bench(args, rank: int, world: int, local: int):
                              "note": "rank 0's dominant kernel; the step is issue/latency bound (DESIGN.md s5)"},
                 "cpu_baseline": None,
                 "note": "multi-GPU line: device-timed max over ranks; cpu_baseline is reported by the N=1 run"}
-        print(json.dumps(line), flush=True)
     sim.close()
+    return line if rank == 0 else None
