@@ -433,7 +433,7 @@ def run_ours(args):
     cpu1_value, _ = cpu_port_rate(state, cfg, max(1024, min(rows, 65536)), 1)
 
     dom_kernel = {"bins": "k_scatter", "gather": "k_gather_fast32",
-                  "solve": "k_solve" if args.precision == "f32" else "k_solve_group",
+                  "solve": {"f32": "k_solve", "cert32": "k_solve_cert"}.get(args.precision, "k_solve_group"),
                   "fallback": "k_fallback_coop"}[dom]
     traffic, traffic_src, ncu_util = load_traffic(args.workload, args.precision, dom_kernel)
     # ---- context lines the driver sees too: the other precision modes on this workload, every
@@ -497,6 +497,9 @@ def run_ours(args):
                                     "h2d_bytes_per_step": 32 * n, "d2h_bytes_per_step": 40 * n}},
         "gpu_launches": launches,
         "stages_ms": stage_ms,
+        "stages_note": "per-stage CUDA events, plain launches, the stages one after the other; the timed step replays "
+                       "a CUDA graph in which gather / solve / fallback run as a two-chunk pipeline on two streams, "
+                       "so the stages add up to more than ms_per_step",
         "extras": extras,
         "roofline": {"bound": "hbm", "kernel": dom_kernel,
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
@@ -653,7 +656,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="plaza_1m", choices=sorted(CONFIGS) + sorted(LP_WORKLOADS))
-    ap.add_argument("--precision", default="mixed", choices=list(PRECISIONS))
+    ap.add_argument("--precision", default="cert32", choices=list(PRECISIONS),
+                    help="cert32 (default): FP32 state, certified FP32 solve with an FP64-evaluated result -- the "
+                         "results of `mixed` bit for bit, checked against the oracle on every agent in the line's "
+                         "`parity`; mixed: FP32 state, FP64 arithmetic; f64: bit-identical to the reference; f32")
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-rows", type=int, default=0,
                     help="agents the CPU port solves per step (0: the whole crowd for cpu_baseline, "

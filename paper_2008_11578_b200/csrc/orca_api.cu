@@ -113,6 +113,10 @@ struct orca_sim {
     bool use_graph = true;     // ORCA_GRAPH=0: launch the step's kernels one by one
     cudaStream_t aux_stream = nullptr; // copy stream of orca_advance_host
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // gather + solve + fallback are issued per CHUNK of sorted slots on two streams (solve_stage)
+    int chunks = 0;                    // 0: chosen from the crowd size; ORCA_CHUNKS forces 1..ORCA_MAX_CHUNKS
+    cudaStream_t chunk_stream = nullptr;
+    cudaEvent_t ev_cfork = nullptr, ev_cjoin = nullptr, ev_patched = nullptr;
     // orca_advance_host: copies overlapped with the step (see there)
     cudaEvent_t ev_vel = nullptr, ev_state = nullptr, ev_dl = nullptr;
     bool split_vel = false;             // velocities arrive on aux_stream; patched in before k_solve
@@ -294,6 +298,10 @@ extern "C" void orca_destroy(orca_sim *sim)
     if (sim->h_plan) cudaFreeHost(sim->h_plan);
     if (sim->own_stream) cudaStreamDestroy(sim->own_stream);
     if (sim->aux_stream) cudaStreamDestroy(sim->aux_stream);
+    if (sim->chunk_stream) cudaStreamDestroy(sim->chunk_stream);
+    if (sim->ev_cfork) cudaEventDestroy(sim->ev_cfork);
+    if (sim->ev_cjoin) cudaEventDestroy(sim->ev_cjoin);
+    if (sim->ev_patched) cudaEventDestroy(sim->ev_patched);
     if (sim->ev_fork) cudaEventDestroy(sim->ev_fork);
     if (sim->ev_join) cudaEventDestroy(sim->ev_join);
     if (sim->ev_vel) cudaEventDestroy(sim->ev_vel);
@@ -328,6 +336,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
     if (const char *re = getenv("ORCA_REORDER_EVERY")) sim->reorder_every = std::max(0, atoi(re));
     if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
+    if (const char *ch = getenv("ORCA_CHUNKS")) sim->chunks = std::min(ORCA_MAX_CHUNKS, std::max(0, atoi(ch)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
     const size_t as = precision == ORCA_F32 ? sizeof(float) : sizeof(double); // arithmetic type R
@@ -346,6 +355,10 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC(cudaStreamCreateWithFlags(&sim->own_stream, cudaStreamNonBlocking));
     sim->stream = sim->own_stream;
     CKC(cudaStreamCreateWithFlags(&sim->aux_stream, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&sim->chunk_stream, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&sim->ev_cfork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&sim->ev_cjoin, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&sim->ev_patched, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&sim->ev_fork, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&sim->ev_join, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&sim->ev_vel, cudaEventDisableTiming));
@@ -638,7 +651,14 @@ extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
     const GridPlan &h = *sim->h_plan;
     info->frame = h.frame;
     info->active_agents = h.n_owned;
-    info->lp_fallbacks = h.fq_count;
+    info->lp_fallbacks = 0;
+    info->gather_queue = 0;
+    info->solve_queue = 0;
+    for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) {
+        info->lp_fallbacks += h.fq_count[c];
+        info->gather_queue += h.gq_count[c];
+        info->solve_queue += h.cq_count[c];
+    }
     info->removed_agents = h.removed;
     info->collision_count = (int64_t)h.collisions;
     info->min_separation = dec_double(h.min_sep_enc);
@@ -646,8 +666,6 @@ extern "C" int orca_get_info(orca_sim *sim, orca_info *info)
     info->grid_ny = h.ny;
     info->grid_cell = h.cell;
     info->kernel_launches = sim->launches;
-    info->gather_queue = h.gq_count;
-    info->solve_queue = h.cq_count;
     return rc;
 }
 
@@ -841,109 +859,104 @@ template <typename S, typename R> static int bin_build(orca_sim *sim, const Step
     return ORCA_OK;
 }
 
-// K2: certified fast pass for everyone, exact ring search for the agents it queued
-template <typename S, int MAXN> static int gather_stage(orca_sim *sim, const StepParams &P)
+// K2 for the sorted slots [s0, s1) = chunk c: certified fast pass for everyone, exact ring
+// search for the agents it queued (queue segment gq + s0, counter gq_count[c])
+template <typename S, int MAXN>
+static int gather_stage(orca_sim *sim, const StepParams &P, cudaStream_t st, int s0, int s1, int c)
 {
     typedef typename Vec<S>::T2 S2;
-    cudaStream_t st = sim->stream;
-    const int64_t n = sim->n_bound;
+    const int64_t m = s1 - s0;
     const int a = sim->acur;
-    k_gather_fast32<S, MAXN, 48><<<grid_for(n, 128), 128, 0, st>>>(
+    k_gather_fast32<S, MAXN, 48><<<grid_for(m, 128), 128, 0, st>>>(
         sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-        reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt, sim->gq, 0, (int)n);
-    const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 127) / 128));
+        reinterpret_cast<const S2 *>(sim->radmax[a]), sim->hint[a], sim->nb, sim->nb_cnt, sim->gq + s0,
+        &sim->plan->gq_count[c], s0, s1);
+    const int gq_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (m + 127) / 128));
     k_gather<S, MAXN><<<gq_blocks, 128, 0, st>>>(
         sim->plan, P, reinterpret_cast<const S2 *>(sim->s_xy), sim->cell_start, sim->s_cell, sim->s_row,
-        sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq);
+        sim->ids[a], sim->hint[a], sim->nb, sim->nb_cnt, sim->gq + s0, &sim->plan->gq_count[c]);
     CKL(sim);
     sim->launches += 2;
     return ORCA_OK;
 }
 
-template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim, const StepParams &P, int out_idx)
+// K3 for chunk c: insertion orders, half-planes + LP (k_solve_group / k_solve / k_solve_cert + the
+// FP64 pass over what it could not certify), least-penetration queue
+template <typename S, typename R, int MAXN>
+static int solve_chunk(orca_sim *sim, const StepParams &P, int out_idx, cudaStream_t st, int s0, int s1, int c,
+                       bool mark)
 {
     typedef typename Vec<S>::T4 S4;
     typedef typename Vec<R>::T4 R4;
     typedef KCfg<R, MAXN> C;
-    cudaStream_t st = sim->stream;
+    const int64_t m = s1 - s0;
     const int64_t n = sim->n_bound;
     const int a = sim->acur;
-    if (sim->spill_maxn < MAXN || !sim->fq_cons || !sim->fq_perm)
-        return fail(sim, ORCA_EINVAL, "solve_stage: no spill buffers for max_neighbors %d", P.max_n);
-    int rc = gather_stage<S, MAXN>(sim, P);
-    if (rc) return rc;
-    sim->mark();
-    if (sim->split_vel) {
-        // the velocities were still in flight while the bins and the neighbour lists
-        // were built from the positions; they are needed from here on
-        CK(sim, cudaStreamWaitEvent(st, sim->ev_vel, 0));
-        k_patch_vel<S><<<grid_for(n, 256), 256, 0, st>>>(
-            sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
-            reinterpret_cast<NbRec<S> *>(sim->s_nr), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
-        sim->launches += 1;
-    }
-    const int s0 = 0, s1 = (int)n;
+    int *fq_cnt = &sim->plan->fq_count[c];
+    // queue segments of this chunk: at most m entries each, so they start at its first slot
+    int *fq = sim->fq + s0;
+    R4 *fq_state = reinterpret_cast<R4 *>(sim->fq_state) + s0;
+    R4 *fq_cons = reinterpret_cast<R4 *>(sim->fq_cons) + (size_t)s0 * MAXN;
+    u8 *fq_perm = sim->fq_perm + (size_t)s0 * MAXN;
 #define ORCA_SOLVE_ARGS                                                                                    \
     sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
         sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
-        sim->status[a], sim->failed[a], sim->arrived, sim->fq, reinterpret_cast<R4 *>(sim->fq_state), s0, s1,  \
-        sim->lrow[a], reinterpret_cast<R4 *>(sim->fq_cons), sim->fq_perm
+        sim->status[a], sim->failed[a], sim->arrived, fq, fq_state, s0, s1, sim->lrow[a], fq_cons, fq_perm
     // below ~64 k agents the step is launch-latency bound and the extra launch costs more than the
     // idle lanes of the in-kernel shuffle (16,640 agents: +1.8 us)
     const bool cert = sim->precision == ORCA_CERT32;
     const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && (cert || n >= ORCA_PRESHUFFLE_MIN_AGENTS);
     const uint32_t *s_perm = preshuffle ? reinterpret_cast<const uint32_t *>(sim->s_perm) : nullptr;
     if (preshuffle) {
-        k_shuffle<MAXN><<<grid_for(n, 128), 128, 0, st>>>(sim->plan, sim->s_row, sim->ids[a], sim->nb_cnt,
+        k_shuffle<MAXN><<<grid_for(m, 128), 128, 0, st>>>(sim->plan, sim->s_row, sim->ids[a], sim->nb_cnt,
                                                          reinterpret_cast<uint4 *>(sim->s_perm), s0, s1);
         sim->launches += 1;
     }
     if (cert) {
         // FP32 solve with a certificate for everyone, the FP64 kernel for the agents it queued
         if constexpr (Fmt<S>::is_f32 && !Fmt<R>::is_f32) {
-            k_solve_cert<MAXN, 128><<<grid_for(n, 128), 128, 21 * MAXN * 128, st>>>(
+            k_solve_cert<MAXN, 128><<<grid_for(m, 128), 128, 21 * MAXN * 128, st>>>(
                 sim->plan, P, reinterpret_cast<const NbRec<float> *>(sim->s_nr),
                 reinterpret_cast<const double4 *>(sim->s_dm), sim->s_row, sim->nb, sim->nb_cnt,
                 reinterpret_cast<const float4 *>(sim->goalpref[a]), reinterpret_cast<float4 *>(sim->pv[out_idx]),
-                sim->status[a], sim->failed[a], sim->arrived, sim->cq, s_perm);
+                sim->status[a], sim->failed[a], sim->arrived, sim->cq + s0, s_perm, &sim->plan->cq_count[c], s0, s1);
             // (4x the resident blocks: a typical queue -- the ~6 % of a sparse crowd -- is ONE chunk per
             //  block, spread over every SM at once; blocks beyond the queue exit at their first test)
-            const int qblocks = (int)std::min<int64_t>(148 * ORCA_SG_BLOCKS * 4, std::max<int64_t>(1, (n + 63) / 64));
+            const int qblocks = (int)std::min<int64_t>(148 * ORCA_SG_BLOCKS * 4, std::max<int64_t>(1, (m + 63) / 64));
             k_solve_group_queue<S, R, MAXN, 128, 2, true><<<qblocks, 128, C::solve_bpt * 64, st>>>(
-                ORCA_SOLVE_ARGS, s_perm, sim->cq);
+                ORCA_SOLVE_ARGS, s_perm, fq_cnt, sim->cq + s0, &sim->plan->cq_count[c]);
             sim->launches += 1;
         }
     } else if (sim->solve_gl == 2 && preshuffle)
-        k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(n, 64), 128, C::solve_bpt * 64, st>>>(
-            ORCA_SOLVE_ARGS, s_perm);
+        k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(m, 64), 128, C::solve_bpt * 64, st>>>(
+            ORCA_SOLVE_ARGS, s_perm, fq_cnt);
     else if (sim->solve_gl == 2)
-        k_solve_group<S, R, MAXN, 128, 2, false><<<grid_for(n, 64), 128, C::solve_bpt * 64, st>>>(
-            ORCA_SOLVE_ARGS, s_perm);
+        k_solve_group<S, R, MAXN, 128, 2, false><<<grid_for(m, 64), 128, C::solve_bpt * 64, st>>>(
+            ORCA_SOLVE_ARGS, s_perm, fq_cnt);
     else
-        k_solve<S, R, MAXN, C::solve_threads><<<grid_for(n, C::solve_threads), C::solve_threads,
-                                                C::solve_bpt * C::solve_threads, st>>>(ORCA_SOLVE_ARGS);
+        k_solve<S, R, MAXN, C::solve_threads><<<grid_for(m, C::solve_threads), C::solve_threads,
+                                                C::solve_bpt * C::solve_threads, st>>>(ORCA_SOLVE_ARGS, fq_cnt);
 #undef ORCA_SOLVE_ARGS
     sim->launches += 1;
-    sim->mark();
+    if (mark) sim->mark();
     {
 #define ORCA_FB_ARGS                                                                                       \
     sim->plan, P, reinterpret_cast<const NbRec<S> *>(sim->s_nr), reinterpret_cast<const R4 *>(sim->s_dm),  \
         sim->s_row, sim->ids[a], sim->nb, sim->nb_cnt,            \
         reinterpret_cast<const S4 *>(sim->goalpref[a]), reinterpret_cast<S4 *>(sim->pv[out_idx]),          \
-        sim->arrived, sim->fq, reinterpret_cast<const R4 *>(sim->fq_state),                               \
-        reinterpret_cast<const R4 *>(sim->fq_cons), sim->fq_perm
+        sim->arrived, fq, fq_state, fq_cons, fq_perm, fq_cnt
         // long-queue and short-queue instance; the device-side queue length decides which one works
         const int ng = C::fb_threads / ORCA_GL; // agents per block and pass
-        const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + ng - 1) / ng));
-        if (ORCA_GL_SHORT == ORCA_GL || n > ORCA_FB_SHORT_QUEUE) { // a queue of <= n entries is never "long"
+        const int fb_blocks = (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (m + ng - 1) / ng));
+        if (ORCA_GL_SHORT == ORCA_GL || m > ORCA_FB_SHORT_QUEUE) { // a queue of <= m entries is never "long"
             k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL><<<fb_blocks, C::fb_threads, C::fb_bpt * ng, st>>>(
                 ORCA_FB_ARGS);
             sim->launches += 1;
         }
         if (ORCA_GL_SHORT != ORCA_GL) {
             const int ngs = C::fb_threads / ORCA_GL_SHORT;
-            const int64_t qmax = std::min<int64_t>(n, ORCA_FB_SHORT_QUEUE);
+            const int64_t qmax = std::min<int64_t>(m, ORCA_FB_SHORT_QUEUE);
             const int sb = (int)std::max<int64_t>(1, (qmax + ngs - 1) / ngs);
             k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL_SHORT><<<sb, C::fb_threads, C::fb_bpt * ngs, st>>>(
                 ORCA_FB_ARGS);
@@ -951,8 +964,75 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
         }
 #undef ORCA_FB_ARGS
     }
-    sim->mark();
     CKL(sim);
+    return ORCA_OK;
+}
+
+// K2 + K3. The stage is a pipeline over CHUNKS of sorted slots on two streams: the exact-search
+// queue, the FP64 pass of ORCA_CERT32 and the least-penetration queue serve a few percent of the
+// agents at a few percent of the machine's warp slots and take as long as one dependent chain;
+// issued per chunk, those latency-bound kernels of one chunk run under the throughput-bound
+// kernels (fast gather, LP) of the next. Chunks own disjoint sorted slots, queue segments and
+// queue counters, and results do not depend on the number of chunks (tests/test_gpu_step.py).
+template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim, const StepParams &P, int out_idx)
+{
+    typedef typename Vec<S>::T4 S4;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur;
+    if (sim->spill_maxn < MAXN || !sim->fq_cons || !sim->fq_perm)
+        return fail(sim, ORCA_EINVAL, "solve_stage: no spill buffers for max_neighbors %d", P.max_n);
+    int chunks = sim->chunks > 0 ? sim->chunks : (n >= ORCA_CHUNK_MIN_AGENTS ? ORCA_CHUNKS_DEFAULT : 1);
+    if (sim->profiling) chunks = 1; // per-stage events need the stages one after the other
+    chunks = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, n / 1024));
+    const int64_t per = ((n + chunks - 1) / chunks + 127) / 128 * 128;
+    if (chunks == 1) {
+        int rc = gather_stage<S, MAXN>(sim, P, st, 0, (int)n, 0);
+        if (rc) return rc;
+        sim->mark();
+        if (sim->split_vel) {
+            // the velocities were still in flight while the bins and the neighbour lists
+            // were built from the positions; they are needed from here on
+            CK(sim, cudaStreamWaitEvent(st, sim->ev_vel, 0));
+            k_patch_vel<S><<<grid_for(n, 256), 256, 0, st>>>(
+                sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
+                reinterpret_cast<NbRec<S> *>(sim->s_nr), sim->cell_of, sim->rank_of, sim->cell_start, sim->lrow[a]);
+            sim->launches += 1;
+        }
+        rc = solve_chunk<S, R, MAXN>(sim, P, out_idx, st, 0, (int)n, 0, true);
+        if (rc) return rc;
+        sim->mark();
+        return ORCA_OK;
+    }
+    // fork: even chunks on the handle's stream, odd chunks on the second one
+    cudaStream_t s2 = sim->chunk_stream;
+    CK(sim, cudaEventRecord(sim->ev_cfork, st));
+    CK(sim, cudaStreamWaitEvent(s2, sim->ev_cfork, 0));
+    for (int c = 0; c < chunks; ++c) {
+        cudaStream_t cs = (c & 1) ? s2 : st;
+        const int s0 = (int)std::min<int64_t>(n, c * per), s1 = (int)std::min<int64_t>(n, (c + 1) * per);
+        if (s1 <= s0) continue;
+        int rc = gather_stage<S, MAXN>(sim, P, cs, s0, s1, c);
+        if (rc) return rc;
+        if (sim->split_vel) {
+            if (c == 0) { // one patch of all rows, after the first chunk's gather; the others wait for it
+                CK(sim, cudaStreamWaitEvent(cs, sim->ev_vel, 0));
+                k_patch_vel<S><<<grid_for(n, 256), 256, 0, cs>>>(
+                    sim->plan, sim->stg + 2 * n, reinterpret_cast<S4 *>(sim->pv[sim->cur]),
+                    reinterpret_cast<NbRec<S> *>(sim->s_nr), sim->cell_of, sim->rank_of, sim->cell_start,
+                    sim->lrow[a]);
+                sim->launches += 1;
+                CK(sim, cudaEventRecord(sim->ev_patched, cs));
+            } else {
+                CK(sim, cudaStreamWaitEvent(cs, sim->ev_patched, 0));
+            }
+        }
+        rc = solve_chunk<S, R, MAXN>(sim, P, out_idx, cs, s0, s1, c, false);
+        if (rc) return rc;
+    }
+    CK(sim, cudaEventRecord(sim->ev_cjoin, s2));
+    CK(sim, cudaStreamWaitEvent(st, sim->ev_cjoin, 0));
+    for (int i = 0; i < 3; ++i) sim->mark(); // (not reached while profiling; keeps the event count per step fixed)
     return ORCA_OK;
 }
 
@@ -2113,7 +2193,9 @@ extern "C" int orca_neighbor_query(int device, int64_t n, const int64_t *ids, co
     if (!rc) {
         const StepParams P = make_params(sim);
         rc = bin_build<double, double>(sim, P);
-        if (!rc) rc = max_count <= 16 ? gather_stage<double, 16>(sim, P) : gather_stage<double, 32>(sim, P);
+        if (!rc)
+            rc = max_count <= 16 ? gather_stage<double, 16>(sim, P, sim->stream, 0, (int)n, 0)
+                                 : gather_stage<double, 32>(sim, P, sim->stream, 0, (int)n, 0);
         sim->pre = sim->cur;
         sim->n_pre = n;
         if (!rc) rc = debug_impl<double, double>(sim, n, nullptr, nullptr, out_rows, out_count, nullptr, nullptr,

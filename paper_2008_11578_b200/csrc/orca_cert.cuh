@@ -247,15 +247,15 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
              const double4 *__restrict__ s_dm, const int *__restrict__ s_row, const int *__restrict__ nb,
              const u8 *__restrict__ nb_cnt, const float4 *__restrict__ goalpref, float4 *__restrict__ pv_out,
              i8 *__restrict__ status, i8 *__restrict__ failed_at, u8 *__restrict__ arrived,
-             int *__restrict__ cq, const uint32_t *__restrict__ s_perm)
+             int *__restrict__ cq, const uint32_t *__restrict__ s_perm, int *__restrict__ cq_cnt, int s0, int s1)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *sm_cons = reinterpret_cast<float4 *>(smem_raw);
     float *sm_err = reinterpret_cast<float *>(sm_cons + MAXN * THREADS);
     u8 *sm_perm = reinterpret_cast<u8 *>(sm_err + MAXN * THREADS);
 
-    const int s = blockIdx.x * THREADS + threadIdx.x;
-    const bool in_range = s < plan->n;
+    const int s = s0 + blockIdx.x * THREADS + threadIdx.x; // this launch covers sorted slots [s0, s1)
+    const bool in_range = s < min(s1, plan->n);
     const int row = in_range ? s_row[s] : 0;
     const bool active = in_range && row < plan->n_owned;
     const unsigned live = __ballot_sync(0xFFFFFFFFu, active);
@@ -384,7 +384,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
         }
     }
     if (!certified) {
-        cq[atomicAdd(&plan->cq_count, 1)] = s;
+        cq[atomicAdd(cq_cnt, 1)] = s;
         return;
     }
     status[row] = 0;

@@ -19,6 +19,9 @@ typedef signed char i8;
 
 #define ORCA_NO_ERR 0xFFFFFFFFFFFFFFFFULL
 
+// gather + solve + fallback are issued per chunk of sorted slots, at most this many
+#define ORCA_MAX_CHUNKS 4
+
 // Device-resident per-step plan and counters. Written by k_plan / k_finish and
 // read by every kernel of the step, so a step needs no host round trip.
 struct GridPlan {
@@ -43,9 +46,12 @@ struct GridPlan {
     int err_capacity; // a strip-exchange slab (or the handle) overflowed: rows were dropped or kept back
     unsigned long long strip_recv[2]; // ghost rows / migrant rows appended from slabs since the upload
     // per-step counters
-    int fq_count;  // agents queued for the least-penetration stage == lp_fallbacks
-    int gq_count;  // agents the certified fast pass queued for the exact ring search (k_gather)
-    int cq_count;   // ORCA_CERT32: agents whose FP32 solve was not certified (redone in FP64)
+    // work queues, one counter per CHUNK of sorted slots (orca_api.cu: the step issues gather, solve
+    // and fallback per chunk on two streams, so that the latency-bound queue kernels of one chunk
+    // overlap the throughput-bound kernels of the other)
+    int fq_count[ORCA_MAX_CHUNKS]; // agents queued for the least-penetration stage; sum == lp_fallbacks
+    int gq_count[ORCA_MAX_CHUNKS]; // agents the certified fast pass queued for the exact ring search (k_gather)
+    int cq_count[ORCA_MAX_CHUNKS]; // ORCA_CERT32: agents whose FP32 solve was not certified (redone in FP64)
     int pack_count; // rows selected by the last orca_strip_pack
     u64 vmax_enc;  // order-preserving encoding of the largest max_speed ever uploaded
     double vmax;

@@ -46,6 +46,12 @@
 #ifndef ORCA_PRESHUFFLE_MIN_AGENTS
 #define ORCA_PRESHUFFLE_MIN_AGENTS 65536
 #endif
+#ifndef ORCA_CHUNKS_DEFAULT
+#define ORCA_CHUNKS_DEFAULT 2          // gather + solve + fallback pipelined over this many chunks of sorted slots ...
+#endif
+#ifndef ORCA_CHUNK_MIN_AGENTS
+#define ORCA_CHUNK_MIN_AGENTS 262144   // ... for crowds of at least this many agents (below: one chunk)
+#endif
 #ifndef ORCA_SG_BLOCKS
 #define ORCA_SG_BLOCKS 6    // resident blocks per SM k_solve_group is compiled for (register cap)
 #endif
@@ -59,11 +65,9 @@ namespace orca {
 // per-step counters (start of every step)
 __global__ void k_begin_step(GridPlan *plan)
 {
-    plan->fq_count = 0;
-    plan->cq_count = 0;
+    for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) plan->fq_count[c] = plan->cq_count[c] = plan->gq_count[c] = 0;
     plan->n_pre = plan->n_owned;
     plan->idle = plan->halt_when_empty && plan->n_owned == 0;
-    plan->gq_count = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
     plan->sep_ub_enc = plan->min_sep_enc;
@@ -542,7 +546,7 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
                 const int *__restrict__ cell_start, const int *__restrict__ s_cell,
                 const int *__restrict__ s_row, const typename Vec<R>::T2 *__restrict__ radmax,
                 float *__restrict__ hint, int *__restrict__ nb, u8 *__restrict__ nb_cnt,
-                int *__restrict__ gq, int s0, int s1)
+                int *__restrict__ gq, int *__restrict__ gq_cnt, int s0, int s1)
 {
     static_assert(CAP <= 64, "slot must fit the 6 cleared mantissa bits");
     __shared__ int buf[CAP * 128];
@@ -690,7 +694,7 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
             return;
         }
     }
-    gq[atomicAdd(&plan->gq_count, 1)] = s;
+    gq[atomicAdd(gq_cnt, 1)] = s;
 }
 
 // Exact ring search for the agents the fast pass queued (all of them on the first step
@@ -704,9 +708,9 @@ k_gather(const GridPlan *__restrict__ plan, StepParams P,
          const typename Vec<R>::T2 *__restrict__ s_xy, const int *__restrict__ cell_start,
          const int *__restrict__ s_cell, const int *__restrict__ s_row,
          const i64 *__restrict__ ids, float *__restrict__ hint, int *__restrict__ nb,
-         u8 *__restrict__ nb_cnt, const int *__restrict__ gq)
+         u8 *__restrict__ nb_cnt, const int *__restrict__ gq, const int *__restrict__ gq_cnt)
 {
-    const int nq = plan->gq_count;
+    const int nq = *gq_cnt;
     const int nx = plan->nx, ny = plan->ny, rmax = plan->rmax;
     const double cell = plan->cell;
     const double rad2 = P.rad2;
@@ -1071,7 +1075,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
         typename Vec<S>::T4 *__restrict__ pv_out, i8 *__restrict__ status,
         i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
         typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
-        typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm)
+        typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm, int *__restrict__ fq_cnt)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typename Vec<R>::T4 *sm_cons = reinterpret_cast<typename Vec<R>::T4 *>(smem_raw);
@@ -1115,7 +1119,7 @@ k_solve(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restrict__ 
     // queue for the least-penetration stage (warp-aggregated by the compiler)
     status[row] = 1;
     failed_at[row] = (i8)perm[fail_pos * THREADS];
-    const int q = atomicAdd(&plan->fq_count, 1);
+    const int q = atomicAdd(fq_cnt, 1);
     fq[q] = s;
     fq_state[q] = mk4(vx, vy, (R)fail_pos, R(0));
     spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + threadIdx.x, perm, THREADS, 0, 1);
@@ -1166,7 +1170,7 @@ solve_group_body(int idx, bool in_range, int s,
               i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
               typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
               typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm,
-              const uint32_t *__restrict__ s_perm)
+              const uint32_t *__restrict__ s_perm, int *__restrict__ fq_cnt)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int NG = THREADS / GL; // agents per block
@@ -1248,7 +1252,7 @@ solve_group_body(int idx, bool in_range, int s,
         cons, cnt, R(0), dm.z, dm.x, dm.y, fail_pos, vx, vy, live, built, gl, gmask);
     int q = 0;
     if (built && !feasible) { // uniform over the group: queue for the least-penetration stage
-        if (gl == 0) q = atomicAdd(&plan->fq_count, 1);
+        if (gl == 0) q = atomicAdd(fq_cnt, 1);
         q = __shfl_sync(gmask, q, gshift);
         spill_constraints<R, MAXN>(fq_cons, fq_perm, q, cnt, sm_cons + g, perm, NG, gl, GL);
     }
@@ -1284,12 +1288,12 @@ k_solve_group(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *__restr
               i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
               typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
               typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm,
-              const uint32_t *__restrict__ s_perm)
+              const uint32_t *__restrict__ s_perm, int *__restrict__ fq_cnt)
 {
     const int idx = s0 + blockIdx.x * (THREADS / GL) + threadIdx.x / GL;
     solve_group_body<S, R, MAXN, THREADS, GL, PRESH>(idx, idx < min(s1, plan->n), idx, plan, P, s_nr, s_dm, s_row, ids, nb,
                                                      nb_cnt, goalpref, pv_out, status, failed_at, arrived, fq, fq_state,
-                                                     s0, s1, lrow, fq_cons, fq_perm, s_perm);
+                                                     s0, s1, lrow, fq_cons, fq_perm, s_perm, fq_cnt);
 }
 
 // The same for a QUEUE of sorted slots (ORCA_CERT32: the agents k_solve_cert could not certify,
@@ -1305,16 +1309,18 @@ k_solve_group_queue(GridPlan *__restrict__ plan, StepParams P, const NbRec<S> *_
                     i8 *__restrict__ failed_at, u8 *__restrict__ arrived, int *__restrict__ fq,
                     typename Vec<R>::T4 *__restrict__ fq_state, int s0, int s1, const int *__restrict__ lrow,
                     typename Vec<R>::T4 *__restrict__ fq_cons, u8 *__restrict__ fq_perm,
-                    const uint32_t *__restrict__ s_perm, const int *__restrict__ queue)
+                    const uint32_t *__restrict__ s_perm, int *__restrict__ fq_cnt,
+                    const int *__restrict__ queue, const int *__restrict__ cq_cnt)
 {
     constexpr int NG = THREADS / GL;
-    const int nq = plan->cq_count;
+    const int nq = *cq_cnt;
     for (int base = blockIdx.x * NG; base < nq; base += gridDim.x * NG) { // uniform trip count per block
         const int idx = base + threadIdx.x / GL;
         const bool in_range = idx < nq;
         solve_group_body<S, R, MAXN, THREADS, GL, PRESH>(idx, in_range, in_range ? queue[idx] : 0, plan, P, s_nr, s_dm,
                                                          s_row, ids, nb, nb_cnt, goalpref, pv_out, status, failed_at,
-                                                         arrived, fq, fq_state, s0, s1, lrow, fq_cons, fq_perm, s_perm);
+                                                         arrived, fq, fq_state, s0, s1, lrow, fq_cons, fq_perm, s_perm,
+                                                         fq_cnt);
         __syncthreads(); // the block's shared memory is reused by the next queue chunk
     }
 }
@@ -1338,12 +1344,13 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
                 const typename Vec<S>::T4 *__restrict__ goalpref, typename Vec<S>::T4 *__restrict__ pv_out,
                 u8 *__restrict__ arrived, const int *__restrict__ fq,
                 const typename Vec<R>::T4 *__restrict__ fq_state,
-                const typename Vec<R>::T4 *__restrict__ fq_cons, const u8 *__restrict__ fq_perm)
+                const typename Vec<R>::T4 *__restrict__ fq_cons, const u8 *__restrict__ fq_perm,
+                const int *__restrict__ fq_cnt)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef typename Vec<R>::T4 R4;
     {   // which instance serves this queue length (both see the same count, exactly one runs)
-        const bool is_short = plan->fq_count <= ORCA_FB_SHORT_QUEUE;
+        const bool is_short = *fq_cnt <= ORCA_FB_SHORT_QUEUE;
         if (ORCA_GL_SHORT != ORCA_GL && is_short != (GL == ORCA_GL_SHORT)) return;
     }
     constexpr int NG = THREADS / GL;                  // agents (groups) per block and pass
@@ -1356,7 +1363,7 @@ k_fallback_coop(const GridPlan *__restrict__ plan, StepParams P,
     u8 *sm_perm = reinterpret_cast<u8 *>(sm_proj + MAXN * NG);
     u8 *sm_inv = sm_perm + MAXN * NG;
 
-    const int nq = plan->fq_count;
+    const int nq = *fq_cnt;
     // every lane makes the same number of passes (a group without an agent rides along
     // disabled), so the run-ahead stage can vote over the whole warp
     for (int base = blockIdx.x * NG; base < nq; base += gridDim.x * NG) {
@@ -1673,7 +1680,8 @@ __global__ void k_log_frame(GridPlan *plan, orca_frame_record *__restrict__ rec,
         r.frame = plan->frame;
         r.active_agents = plan->n_owned;
         r.rows_before = plan->n_pre;
-        r.lp_fallbacks = plan->fq_count;
+        r.lp_fallbacks = 0;
+        for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) r.lp_fallbacks += plan->fq_count[c];
         r.removed_agents = plan->removed;
         r.collision_count = (i64)plan->collisions;
         r.min_separation = dec_double(plan->min_sep_enc);

@@ -72,6 +72,27 @@ def raw_rows(rep):
     return rows[0], rows[1], rows[2:]
 
 
+def traffic_entry(rep, source):
+    global col, units
+    hdr, units, rows = raw_rows(rep)
+    col = {k: i for i, k in enumerate(hdr)}
+    entry = {"source": source, "ncu": {}}
+    for r in rows:
+        name = r[col["Kernel Name"]]
+        short = name.split("<")[0].split()[-1].split("::")[-1]
+        if short in entry:
+            continue
+        if short == "k_fallback_coop" and ", 16>" in name.split("(")[0]:
+            continue          # the short-queue instance exits at once on this workload
+        entry[short] = int(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum"))
+        entry["ncu"][short] = {
+            "ipc": round(val(r, "sm__inst_executed.avg.per_cycle_elapsed"), 3),
+            "fp64_pipe_pct": round(val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"), 1),
+            "lanes": round(val(r, "smsp__thread_inst_executed_per_inst_executed.ratio"), 2),
+            "warps_pct": round(val(r, "sm__warps_active.avg.pct_of_peak_sustained_active"), 1)}
+    return entry
+
+
 hdr, units, rows = raw_rows(os.path.join(G, "g_full.ncu-rep"))
 col = {k: i for i, k in enumerate(hdr)}
 
@@ -100,6 +121,11 @@ tj = os.path.join(P, "traffic.json")
 with open(tj) as f:
     t = json.load(f)
 t["plaza_1m/mixed"] = entry
+cert = traffic_entry(os.path.join(G, "g_full_cert.ncu-rep"), f"profiles/{tag}_full_cert32_1m.md")
+for k in ("k_gather", "k_fallback_coop", "k_count", "k_scatter", "k_gather_fast32"):   # same kernels, same crowd
+    cert.setdefault(k, entry.get(k))
+    cert["ncu"].setdefault(k, entry["ncu"].get(k))
+t["plaza_1m/cert32"] = cert
 with open(tj, "w") as f:
     json.dump(t, f, indent=1)
     f.write("\n")
