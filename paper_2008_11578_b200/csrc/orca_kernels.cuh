@@ -1245,7 +1245,8 @@ solve_group_body(int idx, bool in_range, int s,
             cons.set(pos, mevx + f * ux, mevy + f * uy, nx, ny);
         }
     }
-    const bool built = (__ballot_sync(gmask, !ok_mine) & gmask) == 0u; // also orders the stores
+    __syncwarp(gmask); // the partner's half-planes are read from here on (a vote alone orders no memory)
+    const bool built = (__ballot_sync(gmask, !ok_mine) & gmask) == 0u;
     int fail_pos;
     R vx, vy;
     const bool feasible = g_lp2_target_runahead<R, GL, false, SmemCons<R>>(

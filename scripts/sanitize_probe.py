@@ -9,7 +9,7 @@ sys.path.insert(0, ROOT)
 from paper_2008_11578_b200 import Simulation, LpBatch, step
 from paper_2008_11578_b200.synth import plaza_crowd, lp_batch
 
-for prec in ("mixed", "f32", "f64"):
+for prec in ("mixed", "cert32", "f32", "f64"):
     for dens in (0.3, 2.0):
         st, cfg = plaza_crowd(3000, 100, density=dens, seed=3)
         rng = np.random.default_rng(1)
@@ -39,4 +39,38 @@ for prec in ("f64", "f32"):
     b.solve()
     v, stt, fa = b.results()
     b.close()
-print("probe done", m.active_agents, int(stt.sum()))
+print("lp done", m.active_agents, int(stt.sum()))
+
+# round 2: chunked pipeline on two streams (ORCA_CHUNKS forces it on a small crowd), the device-side
+# frame log, the slab protocol of the strip decomposition (two handles in lock step), the taps
+import torch
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+os.environ["ORCA_CHUNKS"] = "2"
+st, cfg = plaza_crowd(6000, 200, density=0.8, seed=8)
+rng = np.random.default_rng(2)
+close = rng.permutation(st.active_count)[:500]
+st.goals[close] = st.positions[close] + rng.normal(size=(500, 2)) * 0.5
+for prec in ("cert32", "mixed"):
+    with Simulation(cfg, capacity=st.active_count, precision=prec, remove_arrivals=True, compute_metrics=True) as sim:
+        sim.load(st)
+        recs, traj, arr = sim.run_logged(6, st.active_count, with_trajectories=True)
+        kept = sim.last_step_kept(int(recs[-1]["rows_before"]))
+        s2 = sim.state()
+    print("chunks + frame log", prec, len(recs), traj.shape, arr[0].shape, int(kept.sum()), s2.active_count)
+del os.environ["ORCA_CHUNKS"]
+import strip_ops_cpu as S
+from test_gpu_strips import build_strips, lockstep
+st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
+for prec, world in (("mixed", 2), ("f64", 3)):
+    sims, drivers, _b = build_strips(st, cfg, prec, world, halo_cap=st.ids.shape[0], mig_cap=2000, resync_every=3)
+    lockstep(drivers, 7)
+    print("strips", prec, world, [s.state().ids.shape[0] for s in sims], [d.ops.stats() for d in drivers])
+    for s_ in sims:
+        s_.close()
+from paper_2008_11578_b200 import HalfPlaneConstraint, solve_least_penetration
+from paper_2008_11578_b200.grid import neighbor_lists
+rows, cnt = neighbor_lists(st.ids, st.positions, 5.0, 12)
+ang = rng.uniform(0, 6.28, 9)
+v = solve_least_penetration([HalfPlaneConstraint(rng.normal(size=2), (np.cos(a), np.sin(a))) for a in ang], 1.5,
+                            start_index=3, warm_start=(0.1, 0.2))
+print("probe done", rows.shape, int(cnt.sum()), v)
