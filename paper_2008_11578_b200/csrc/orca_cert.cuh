@@ -237,10 +237,18 @@ __device__ __forceinline__ bool halfplane64(int s, int pos, const StepParams &P,
     return ok;
 }
 
-// The solve stage of ORCA_CERT32 (see the header of this file). One thread per agent, FP32
-// half-planes + their error bounds in shared memory ([position][thread]); the insertion
-// order comes from k_shuffle. Certified agents are finished here (status 0, FP64 velocity,
-// integration); the others are appended to cq for k_solve_group<float, double>.
+// The solve stage of ORCA_CERT32 (see the header of this file), FP32 half-planes + their error
+// bounds in shared memory ([position][thread]); the insertion order comes from k_shuffle.
+//
+// Phase A, one thread per agent: build the half-planes and test the (clamped) preferred velocity
+// against them. ~40 % of the agents of a sparse crowd violate nothing by a clear margin: they are
+// finished here. Agents with a clear violation become LP TASKS.
+// Phase B: the tasks of the block are compacted (a shared-memory list), and thread t runs the LP,
+// the FP64 evaluation and the certificate of task t on that agent's shared-memory half-planes --
+// the warps that do run the divergent LP loops are full of agents that need them, instead of
+// every warp dragging its finished lanes through them.
+// Certified agents are finished (status 0, FP64 velocity, integration); the others are appended
+// to cq for the FP64 kernel (k_solve_group_queue).
 template <int MAXN, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__restrict__ s_nr,
@@ -253,84 +261,131 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
     float4 *sm_cons = reinterpret_cast<float4 *>(smem_raw);
     float *sm_err = reinterpret_cast<float *>(sm_cons + MAXN * THREADS);
     u8 *sm_perm = reinterpret_cast<u8 *>(sm_err + MAXN * THREADS);
+    __shared__ int sm_task[THREADS];
+    __shared__ int sm_ntask;
+    if (threadIdx.x == 0) sm_ntask = 0;
+    __syncthreads();
 
-    const int s = s0 + blockIdx.x * THREADS + threadIdx.x; // this launch covers sorted slots [s0, s1)
-    const bool in_range = s < min(s1, plan->n);
-    const int row = in_range ? s_row[s] : 0;
-    const bool active = in_range && row < plan->n_owned;
-    const unsigned live = __ballot_sync(0xFFFFFFFFu, active);
-    if (!active) return;
-
-    const int cnt = nb_cnt[s];
+    const int s_base = s0 + blockIdx.x * THREADS;
+    {   // ---- phase A ----
+        const int s = s_base + threadIdx.x; // this launch covers sorted slots [s0, s1)
+        const bool in_range = s < min(s1, plan->n);
+        const int row = in_range ? s_row[s] : 0;
+        if (in_range && row < plan->n_owned) {
+            const int cnt = nb_cnt[s];
+            const NbRec<float> me_rec = s_nr[s];
+            const float4 me = me_rec.pv;
+            const double4 dm = s_dm[s]; // desired velocity (FP64, k_scatter), max_speed, avoid radius
+            u8 *perm = sm_perm + threadIdx.x;
+            float *cerr = sm_err + threadIdx.x;
+            SmemCons<float> cons{sm_cons + threadIdx.x, THREADS};
+            {
+                const uint32_t *src = s_perm + (size_t)s * (MAXN / 4);
+                for (int t = 0; 4 * t < cnt; ++t) {
+                    const uint32_t w = src[t];
+                    perm[(4 * t) * THREADS] = (u8)(w & 0xFFu);
+                    perm[(4 * t + 1) * THREADS] = (u8)((w >> 8) & 0xFFu);
+                    perm[(4 * t + 2) * THREADS] = (u8)((w >> 16) & 0xFFu);
+                    perm[(4 * t + 3) * THREADS] = (u8)(w >> 24);
+                }
+            }
+            const float cap = (float)dm.z;
+            // the start of the LP (K:129-136) in FP32: the half-planes are tested against it as they are built
+            float v0x = (float)dm.x, v0y = (float)dm.y;
+            {
+                const float t2 = __fmaf_rn(v0x, v0x, v0y * v0y);
+                if (t2 > cap * cap) {
+                    const float sc = cap * rsqrtf(t2);
+                    v0x *= sc;
+                    v0y *= sc;
+                }
+            }
+            bool built = true, violated = false, unclear = false;
+            {   // FP32 half-planes in shuffled order, each with its error bound against |v| <= cap
+                const float ri = (float)((double)me_rec.rc.x + P.half_margin);
+                const int ci = (int)me_rec.rc.y;
+                const float f0 = (float)(ci ? P.fmat[2] : P.fmat[0]), f1 = (float)(ci ? P.fmat[3] : P.fmat[1]);
+                const float inv_tau = __fdividef(1.0f, (float)P.tau), inv_dt = __fdividef(1.0f, (float)P.dt);
+                float4 q_next = me;
+                float2 rc_next = me_rec.rc;
+                if (cnt > 0) {
+                    const NbRec<float> rn = s_nr[nb[(size_t)perm[0] * P.stride + s]];
+                    q_next = rn.pv;
+                    rc_next = rn.rc;
+                }
+                for (int pos = 0; pos < cnt; ++pos) {
+                    const float4 q = q_next;
+                    const float2 rc_j = rc_next;
+                    if (pos + 1 < cnt) {
+                        const NbRec<float> rn = s_nr[nb[(size_t)perm[(pos + 1) * THREADS] * P.stride + s]];
+                        q_next = rn.pv;
+                        rc_next = rn.rc;
+                    }
+                    const float rj = (float)((double)rc_j.x + P.half_margin);
+                    float ux, uy, nx, ny, eu, en;
+                    built &= vo_exit_cond(q.x - me.x, q.y - me.y, me.z - q.z, me.w - q.w, ri + rj, inv_tau, inv_dt,
+                                          ux, uy, nx, ny, eu, en);
+                    const float f = rc_j.y != 0.0f ? f1 : f0;
+                    const float px = __fmaf_rn(f, ux, me.z), py = __fmaf_rn(f, uy, me.w);
+                    cons.set(pos, px, py, nx, ny);
+                    // |(v - p).n evaluated in FP32 - the same in exact arithmetic on the FP64 half-plane|, any |v| <= cap
+                    const float reach = cap + fabsf(px) + fabsf(py);
+                    const float e = f * eu + en * reach + CERT_SAFETY * 4.0f * CERT_EPS * (reach + fabsf(me.z) + fabsf(me.w));
+                    cerr[pos * THREADS] = e;
+                    const float slack = __fmaf_rn(v0x - px, nx, (v0y - py) * ny);
+                    violated = violated || slack < -e;
+                    unclear = unclear || !(fabsf(slack) > e); // (also catches an infinite error bound)
+                }
+            }
+            if (!built || (unclear && !violated)) {
+                // coincident centres (the FP64 kernel reports them) or a half-plane through the start
+                // within its error: nothing to guess, the FP64 kernels decide
+                cq[atomicAdd(cq_cnt, 1)] = s;
+            } else if (!violated) {
+                // the start violates nothing, by margins above every error bound: it is the result (K:137-146
+                // never enters _lp1_target), evaluated in FP64 exactly as the reference does
+                const double tx = dm.x, ty = dm.y, capd = dm.z;
+                double vx = tx, vy = ty;
+                const double t2 = tx * tx + ty * ty;
+                if (t2 > capd * capd) {
+                    const double sc = __ddiv_rn(capd, __dsqrt_rn(t2));
+                    vx = tx * sc;
+                    vy = ty * sc;
+                }
+                status[row] = 0;
+                failed_at[row] = -1;
+                integrate_row<float, double>(row, me, vx, vy, P, goalpref, pv_out, arrived);
+            } else {
+                sm_task[atomicAdd(&sm_ntask, 1)] = threadIdx.x;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- phase B: thread t takes task t ----
+    const int ntask = sm_ntask;
+    if ((int)(threadIdx.x & ~31u) >= ntask) return; // whole warp without a task
+    const bool enabled = (int)threadIdx.x < ntask;
+    const int a = enabled ? sm_task[threadIdx.x] : 0; // the agent's thread slot in shared memory
+    const int s = s_base + a;
+    const int row = s_row[s];
+    const int cnt = enabled ? (int)nb_cnt[s] : 0;
     const NbRec<float> me_rec = s_nr[s];
     const float4 me = me_rec.pv;
-    const double4 dm = s_dm[s]; // desired velocity (FP64, k_scatter), max_speed, avoid radius
-    u8 *perm = sm_perm + threadIdx.x;
-    float *cerr = sm_err + threadIdx.x;
-    SmemCons<float> cons{sm_cons + threadIdx.x, THREADS};
-    {
-        const uint32_t *src = s_perm + (size_t)s * (MAXN / 4);
-        for (int t = 0; 4 * t < cnt; ++t) {
-            const uint32_t w = src[t];
-            perm[(4 * t) * THREADS] = (u8)(w & 0xFFu);
-            perm[(4 * t + 1) * THREADS] = (u8)((w >> 8) & 0xFFu);
-            perm[(4 * t + 2) * THREADS] = (u8)((w >> 16) & 0xFFu);
-            perm[(4 * t + 3) * THREADS] = (u8)(w >> 24);
-        }
-    }
+    const double4 dm = s_dm[s];
+    const u8 *perm = sm_perm + a;
+    const float *cerr = sm_err + a;
+    SmemCons<float> cons{sm_cons + a, THREADS};
     const float cap = (float)dm.z;
-    bool built = true;
-    {   // FP32 half-planes in shuffled order, each with its error bound against |v| <= cap
-        const float ri = (float)((double)me_rec.rc.x + P.half_margin);
-        const int ci = (int)me_rec.rc.y;
-        const float f0 = (float)(ci ? P.fmat[2] : P.fmat[0]), f1 = (float)(ci ? P.fmat[3] : P.fmat[1]);
-        const float inv_tau = __fdividef(1.0f, (float)P.tau), inv_dt = __fdividef(1.0f, (float)P.dt);
-        float4 q_next = me;
-        float2 rc_next = me_rec.rc;
-        if (cnt > 0) {
-            const NbRec<float> rn = s_nr[nb[(size_t)perm[0] * P.stride + s]];
-            q_next = rn.pv;
-            rc_next = rn.rc;
-        }
-        for (int pos = 0; pos < cnt; ++pos) {
-            const float4 q = q_next;
-            const float2 rc_j = rc_next;
-            if (pos + 1 < cnt) {
-                const NbRec<float> rn = s_nr[nb[(size_t)perm[(pos + 1) * THREADS] * P.stride + s]];
-                q_next = rn.pv;
-                rc_next = rn.rc;
-            }
-            const float rj = (float)((double)rc_j.x + P.half_margin);
-            float ux, uy, nx, ny, eu, en;
-            built &= vo_exit_cond(q.x - me.x, q.y - me.y, me.z - q.z, me.w - q.w, ri + rj, inv_tau, inv_dt, ux, uy,
-                                  nx, ny, eu, en);
-            const float f = rc_j.y != 0.0f ? f1 : f0;
-            const float px = __fmaf_rn(f, ux, me.z), py = __fmaf_rn(f, uy, me.w);
-            cons.set(pos, px, py, nx, ny);
-            // |(v - p).n evaluated in FP32 - the same in exact arithmetic on the FP64 half-plane|, any |v| <= cap
-            const float reach = cap + fabsf(px) + fabsf(py);
-            cerr[pos * THREADS] = f * eu + en * reach + CERT_SAFETY * 4.0f * CERT_EPS * (reach + fabsf(me.z) + fabsf(me.w));
-        }
-    }
     float vxf, vyf;
     int c_last, kind, j_sel;
     const bool feasible = lp2_target_runahead_act<SmemCons<float>>(cons, cnt, cap, (float)dm.x, (float)dm.y, vxf, vyf,
-                                                                  c_last, kind, j_sel, live, built);
-    bool certified = built && feasible && kind <= 2;
+                                                                  c_last, kind, j_sel, 0xFFFFFFFFu, enabled);
+    if (!enabled) return;
+    bool certified = feasible && kind <= 2 && c_last >= 0;
     double vx = 0.0, vy = 0.0;
     if (certified) {
-        const double tx = dm.x, ty = dm.y, capd = dm.z;
-        if (c_last < 0) { // K:129-136
-            const double t2 = tx * tx + ty * ty;
-            if (t2 > capd * capd) {
-                const double sc = __ddiv_rn(capd, __dsqrt_rn(t2));
-                vx = tx * sc;
-                vy = ty * sc;
-            } else {
-                vx = tx;
-                vy = ty;
-            }
-        } else { // the closing formula of _lp1_target on line L = c_last, bound B = j_sel (K:98-119)
+        const double tx = dm.x, ty = dm.y;
+        {   // the closing formula of _lp1_target on line L = c_last, bound B = j_sel (K:98-119)
             const double inv_tau = __ddiv_rn(1.0, P.tau), inv_dt = __ddiv_rn(1.0, P.dt);
             double px, py, nx, ny;
             halfplane64(s, c_last, P, s_nr, nb, perm, THREADS, inv_tau, inv_dt, px, py, nx, ny);
@@ -341,9 +396,9 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
             } else {
                 double qx, qy, mx, my;
                 halfplane64(s, j_sel, P, s_nr, nb, perm, THREADS, inv_tau, inv_dt, qx, qy, mx, my);
-                const double a = dx * mx + dy * my;
-                const double b = (qx - px) * mx + (qy - py) * my;
-                t = __ddiv_rn(b, a);
+                const double a_ = dx * mx + dy * my;
+                const double b_ = (qx - px) * mx + (qy - py) * my;
+                t = __ddiv_rn(b_, a_);
             }
             vx = px + t * dx;
             vy = py + t * dy;
@@ -351,8 +406,8 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
         // ---- the certificate, at the FP64 candidate ----
         const float cvx = (float)vx, cvy = (float)vy;
         const float txf = (float)tx, tyf = (float)ty;
-        // strictly inside the speed disc (an active disc is left to FP64); the unclamped start needs none
-        if (c_last >= 0) certified = cvx * cvx + cvy * cvy < cap * cap * (1.0f - 1e-4f);
+        // strictly inside the speed disc (an active disc is left to FP64)
+        certified = cvx * cvx + cvy * cvy < cap * cap * (1.0f - 1e-4f);
         float e_act = 0.0f;
         for (int pos = 0; pos < cnt; ++pos) { // every inactive half-plane holds with a margin above its error
             float px, py, nx, ny;
@@ -363,7 +418,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
             if (act) e_act += e;
             certified = certified && (act ? e < 1.0f : slack > e);
         }
-        if (certified && c_last >= 0) { // optimality: target - v = alpha n_L + beta n_B with alpha, beta < 0
+        if (certified) { // optimality: target - v = alpha n_L + beta n_B with alpha, beta < 0
             float lx, ly, lnx, lny;
             cons.get(c_last, lx, ly, lnx, lny);
             const float gx = txf - cvx, gy = tyf - cvy;
