@@ -474,8 +474,8 @@ def run_ours(args):
             extras["config5_8m_single_gpu"] = other["config5_8m"]
             extras["lp_1m_resident_ms"] = {k: lp_resident(k, "f64", local, stream, 10)
                                            for k in sorted(LP_WORKLOADS)}
-        census = parity_census(state, cfg, [args.precision] + [p for p in ("cert32", "f32") if p != args.precision],
-                               local)
+        census = parity_census(state, cfg, [args.precision] + [p for p in ("mixed", "cert32", "f32")
+                                                               if p != args.precision], local)
         ref_numba = numba_reference(state, cfg)
     else:
         ref_numba = {"skipped": "--no-extras"}

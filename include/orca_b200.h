@@ -52,7 +52,9 @@
  *                   the result itself is evaluated in FP64 on those, and accepted only
  *                   with a certificate (feasibility and optimality margins above the FP32
  *                   error bounds, csrc/orca_cert.cuh). Everything else -- infeasible LPs,
- *                   thin margins -- goes through the FP64 kernels of ORCA_MIXED.
+ *                   thin margins -- goes through the FP64 kernels of ORCA_MIXED, and so do
+ *                   whole crowds for which the certified pass would not pay (fewer than
+ *                   65,536 agents, or a quarter of the LPs infeasible at the last count).
  */
 #ifndef ORCA_B200_H
 #define ORCA_B200_H

@@ -92,6 +92,12 @@ struct orca_sim {
     u8 *s_perm = nullptr; // insertion order per sorted slot (k_shuffle -> k_solve_group), spill_maxn bytes each
     int spill_maxn = 0;
     int *cq = nullptr; // ORCA_CERT32: agents whose FP32 solve was not certified (solved in FP64)
+    // ORCA_CERT32 takes the certified path only where it pays -- large crowds in which most LPs are
+    // feasible (the count is the last one the host saw) -- and the FP64 kernels of ORCA_MIXED
+    // otherwise; the results are the same bits either way, so this is a performance choice only
+    bool cert_active = false;
+    bool cert_force = false;   // ORCA_CERT_FORCE=1: always the certified path (tests: small and jammed crowds)
+    int64_t cert_seen_frame = -1;
     int *gq = nullptr; // agents queued for the exact ring search
     GridPlan *plan = nullptr;
     GridPlan *h_plan = nullptr; // pinned mirror
@@ -132,6 +138,7 @@ struct orca_sim {
         void *mig0, *mig1;         // key: migrant slabs of orca_strip_step (null outside strips)
         int64_t mig_cap;
         bool strip_ghosts;         // key: the compaction that drops ghosts is part of the sequence
+        bool cert_active;          // key: which solve kernels run (ORCA_CERT32)
         int bbox_rel;              // bbox_frame - frame after the step
         cudaGraphExec_t exec;
         int new_cur, new_acur, new_pre; // host state after the step
@@ -336,6 +343,7 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     sim->solve_gl = precision == ORCA_F32 ? 1 : 2;
     if (const char *re = getenv("ORCA_REORDER_EVERY")) sim->reorder_every = std::max(0, atoi(re));
     if (const char *gr = getenv("ORCA_GRAPH")) sim->use_graph = atoi(gr) != 0;
+    if (const char *cf = getenv("ORCA_CERT_FORCE")) sim->cert_force = atoi(cf) != 0;
     if (const char *ch = getenv("ORCA_CHUNKS")) sim->chunks = std::min(ORCA_MAX_CHUNKS, std::max(0, atoi(ch)));
     const size_t cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t rs = precision == ORCA_F64 ? sizeof(double) : sizeof(float); // storage type S
@@ -581,6 +589,8 @@ extern "C" int orca_upload(orca_sim *sim, int64_t n, int64_t frame, const int64_
     sim->ghost_bound = 0;
     sim->strip_on = false;
     sim->strip_ghosts = false;
+    sim->cert_active = sim->precision == ORCA_CERT32 && (sim->cert_force || n >= ORCA_CERT_MIN_AGENTS); // until a fallback count is seen
+    sim->cert_seen_frame = frame;
     sim->loaded = true;
     sim->binned_frame = -1;
     sim->bbox_frame = -1;
@@ -626,6 +636,13 @@ static int fetch_plan(orca_sim *sim)
     // (rounded up to 32,768 rows so that the bound -- a graph key -- changes rarely)
     sim->n_bound = sim->strip_on ? std::min<int64_t>(sim->capacity, (((int64_t)h.n + sim->strip_slack + 32767) >> 15) << 15)
                                  : h.n;
+    if (sim->precision == ORCA_CERT32 && h.frame > sim->cert_seen_frame) {
+        int64_t fb = 0;
+        for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) fb += h.fq_count[c];
+        sim->cert_active = sim->cert_force || (h.n_owned >= ORCA_CERT_MIN_AGENTS &&
+                                               fb * 100 < (int64_t)h.n_owned * ORCA_CERT_MAX_FALLBACK_PCT);
+        sim->cert_seen_frame = h.frame;
+    }
     if (h.err_range) return fail(sim, ORCA_ERANGE, "agent position out of indexable grid range");
     if (h.err_capacity)
         return fail(sim, ORCA_ECAPACITY, "strip exchange: a slab or the handle capacity (%lld rows) overflowed",
@@ -905,7 +922,7 @@ static int solve_chunk(orca_sim *sim, const StepParams &P, int out_idx, cudaStre
         sim->status[a], sim->failed[a], sim->arrived, fq, fq_state, s0, s1, sim->lrow[a], fq_cons, fq_perm
     // below ~64 k agents the step is launch-latency bound and the extra launch costs more than the
     // idle lanes of the in-kernel shuffle (16,640 agents: +1.8 us)
-    const bool cert = sim->precision == ORCA_CERT32;
+    const bool cert = sim->precision == ORCA_CERT32 && sim->cert_active;
     const bool preshuffle = ORCA_PRESHUFFLE && sim->solve_gl >= 2 && (cert || n >= ORCA_PRESHUFFLE_MIN_AGENTS);
     const uint32_t *s_perm = preshuffle ? reinterpret_cast<const uint32_t *>(sim->s_perm) : nullptr;
     if (preshuffle) {
@@ -1256,7 +1273,8 @@ static int step_graphed(orca_sim *sim)
     for (auto &g : sim->graphs) {
         if (g.cur == sim->cur && g.acur == sim->acur && g.n_bound == sim->n_bound && g.had_bins == had_bins &&
             g.bbox_gap == bbox_gap && g.log_mode == sim->log_mode && g.mig0 == sim->mig_slab[0] &&
-            g.mig1 == sim->mig_slab[1] && g.mig_cap == sim->mig_cap && g.strip_ghosts == sim->strip_ghosts) {
+            g.mig1 == sim->mig_slab[1] && g.mig_cap == sim->mig_cap && g.strip_ghosts == sim->strip_ghosts &&
+            g.cert_active == sim->cert_active) {
             CK(sim, cudaGraphLaunch(g.exec, sim->stream));
             sim->n_pre = sim->n_bound;
             sim->apre = g.acur;
@@ -1284,6 +1302,7 @@ static int step_graphed(orca_sim *sim)
     g.mig1 = sim->mig_slab[1];
     g.mig_cap = sim->mig_cap;
     g.strip_ghosts = sim->strip_ghosts;
+    g.cert_active = sim->cert_active;
     const int64_t l0 = sim->launches;
     if (cudaStreamBeginCapture(sim->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
         cudaGetLastError();

@@ -41,6 +41,12 @@ namespace orca {
 #ifndef CERT_SAFETY
 #define CERT_SAFETY 8.0f        // multiplies every first-order error estimate below
 #endif
+#ifndef ORCA_CERT_MIN_AGENTS
+#define ORCA_CERT_MIN_AGENTS 65536        // below: launch-latency bound, the extra kernels cost more than they save
+#endif
+#ifndef ORCA_CERT_MAX_FALLBACK_PCT
+#define ORCA_CERT_MAX_FALLBACK_PCT 25     // above: most agents need the FP64 kernels anyway (measured break-even ~30 %)
+#endif
 #define CERT_CROSS_MIN 0.02f    // |n_L x n_B| below this: the vertex is ill-conditioned, leave it to FP64
 
 // vo_exit<float> (orca_math.cuh) plus a first-order bound on how far the FP32 half-plane can be

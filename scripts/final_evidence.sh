@@ -2,8 +2,8 @@
 #   gpurun -- 'bash scripts/final_evidence.sh'    then    python scripts/refresh_profiles.py r02
 set -x
 mkdir -p gpurun_out
-python bench.py > gpurun_out/g_mixed.json 2> gpurun_out/g_mixed.err
-python bench.py --precision cert32 --no-extras > gpurun_out/g_cert32.json 2>/dev/null
+python bench.py > gpurun_out/g_default.json 2> gpurun_out/g_default.err
+python bench.py --precision mixed --no-extras > gpurun_out/g_mixed.json 2>/dev/null
 python bench.py --precision f32 --no-extras > gpurun_out/g_f32.json 2>/dev/null
 python bench.py --precision f64 --no-extras > gpurun_out/g_f64.json 2>/dev/null
 python bench.py --impl reference > gpurun_out/g_ref.json 2>/dev/null

@@ -27,7 +27,7 @@ def last_json_line(path):
 
 
 # bench lines
-for name in ("mixed", "cert32", "f32", "f64", "ref"):
+for name in ("default", "mixed", "f32", "f64", "ref"):
     with open(os.path.join(P, f"bench_{tag}_{name}.json"), "w") as f:
         f.write(last_json_line(os.path.join(G, f"g_{name}.json")) + "\n")
 for name in ("configs", "lp", "strips"):

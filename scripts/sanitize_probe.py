@@ -4,6 +4,7 @@
 """
 import os, sys
 import numpy as np
+os.environ["ORCA_CERT_FORCE"] = "1"   # the certified kernels on small crowds too
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2008_11578_b200 import Simulation, LpBatch, step

@@ -12,6 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, ROOT)
 
+os.environ["ORCA_CERT_FORCE"] = "1"     # small crowds too
+
 import numpy as np  # noqa: E402
 
 import test_gpu_fuzz as F  # noqa: E402

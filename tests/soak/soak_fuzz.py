@@ -12,6 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("ORCA_REORDER_EVERY", "2")
+os.environ.setdefault("ORCA_CERT_FORCE", "1")     # the certified kernels on small crowds too
 
 import numpy as np  # noqa: E402
 

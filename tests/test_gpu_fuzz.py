@@ -3,6 +3,8 @@
 the CPU oracle. FP64 mode must be bit-exact, MIXED within 1e-6 m/s with identical status;
 bins and ordered neighbour lists exact in both."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -61,6 +63,12 @@ def random_case(seed):
                   radii=radii, pref_speeds=pref, max_speeds=maxs, goals=goals, goal_tols=gtol,
                   class_codes=cls)
     return st, cfg
+
+
+@pytest.fixture(autouse=True)
+def certified_kernels_on_small_crowds(monkeypatch):
+    """cert32 handles take the certified path only for large crowds by themselves; these crowds are small."""
+    monkeypatch.setenv("ORCA_CERT_FORCE", "1")
 
 
 @pytest.mark.parametrize("seed", range(24))
