@@ -1053,6 +1053,36 @@ template <typename S, typename R, int MAXN> static int solve_stage(orca_sim *sim
     return ORCA_OK;
 }
 
+// A strip's removal of rows after a step, in place (k_strip_holes): emigrants into the slabs,
+// arrivals and ghosts dropped, the tail's survivors moved into the holes. pv_idx: the buffer the
+// step wrote (it stays the current one).
+template <typename R> static int strip_fill_stage(orca_sim *sim, int pv_idx)
+{
+    typedef typename Vec<R>::T4 R4;
+    typedef typename Vec<R>::T2 R2;
+    cudaStream_t st = sim->stream;
+    const int64_t n = sim->n_bound;
+    const int a = sim->acur;
+    orca_slab_header *hl = reinterpret_cast<orca_slab_header *>(sim->mig_slab[0]);
+    orca_slab_header *hr = reinterpret_cast<orca_slab_header *>(sim->mig_slab[1]);
+    k_strip_keep_flags<R><<<grid_for(n + 1, 256), 256, 0, st>>>(
+        sim->plan, sim->arrived, sim->keep, sim->params.remove_arrivals, reinterpret_cast<const R4 *>(sim->pv[pv_idx]),
+        reinterpret_cast<const R4 *>(sim->goalpref[a]), reinterpret_cast<const R2 *>(sim->radmax[a]), sim->ids[a],
+        sim->cls[a], sim->strip_lo, sim->strip_hi, hl, hl ? reinterpret_cast<orca_agent_record *>(hl + 1) : nullptr, hr,
+        hr ? reinterpret_cast<orca_agent_record *>(hr + 1) : nullptr, (int)sim->mig_cap, sim->a64[a]);
+    k_strip_holes<<<grid_for(n, 256), 256, 0, st>>>(sim->plan, sim->keep, sim->sel, sim->sel_idx);
+    // (holes are at most the emigrant slabs' capacity plus the arrivals; the grid covers every row
+    //  all the same -- surplus threads leave at once)
+    k_strip_fill<R><<<grid_for(n, 256), 256, 0, st>>>(
+        sim->plan, sim->sel, sim->sel_idx, reinterpret_cast<R4 *>(sim->pv[pv_idx]),
+        reinterpret_cast<R4 *>(sim->goalpref[a]), reinterpret_cast<R2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a],
+        sim->status[a], sim->failed[a], sim->hint[a], sim->lrow[a], sim->a64[a]);
+    k_after_strip_fill<<<1, 1, 0, st>>>(sim->plan);
+    CKL(sim);
+    sim->launches += 4;
+    return ORCA_OK;
+}
+
 // Order-preserving removal of rows: arrivals and ghosts after a step (from_sel == false)
 // or the rows orca_strip_pack selected (from_sel == true).
 template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int dst_pv_idx, bool from_sel = false)
@@ -1064,17 +1094,7 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
     const int a = sim->acur, b = 1 - a;
     if (from_sel)
         k_keep_unselected<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->sel, sim->keep);
-    else if (sim->mig_cap > 0) {
-        // strip step: rows whose new x left the strip go to the migrant slabs and are dropped
-        orca_slab_header *hl = reinterpret_cast<orca_slab_header *>(sim->mig_slab[0]);
-        orca_slab_header *hr = reinterpret_cast<orca_slab_header *>(sim->mig_slab[1]);
-        k_strip_keep_flags<R><<<grid_for(n + 1, 256), 256, 0, st>>>(
-            sim->plan, sim->arrived, sim->keep, sim->params.remove_arrivals,
-            reinterpret_cast<const R4 *>(sim->pv[src_idx]), reinterpret_cast<const R4 *>(sim->goalpref[a]),
-            reinterpret_cast<const R2 *>(sim->radmax[a]), sim->ids[a], sim->cls[a], sim->strip_lo, sim->strip_hi,
-            hl, hl ? reinterpret_cast<orca_agent_record *>(hl + 1) : nullptr, hr,
-            hr ? reinterpret_cast<orca_agent_record *>(hr + 1) : nullptr, (int)sim->mig_cap, sim->a64[a]);
-    } else
+    else
         k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
                                                            sim->params.remove_arrivals);
     const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
@@ -1143,6 +1163,11 @@ template <typename S, typename R> static int reorder_rows(orca_sim *sim, const S
         sim->hint[a], sim->hint[b], sim->lrow[a], sim->lrow[b], sim->a64[a], sim->a64[b]);
     CKL(sim);
     sim->launches += 1;
+    if (sim->strip_on) { // a strip's logical rows are its physical rows (strip_fill_stage relies on it)
+        k_iota<<<grid_for(n, 256), 256, 0, sim->stream>>>((int)n, sim->lrow[b]);
+        CKL(sim);
+        sim->launches += 1;
+    }
     sim->cur = dst;
     sim->acur = b;
     sim->rows_permuted = true;
@@ -1191,10 +1216,16 @@ template <typename S, typename R> static int step_impl(orca_sim *sim)
     sim->apre = sim->acur;
     if (sim->reorder_every > 0 && ++sim->since_reorder >= sim->reorder_every) sim->reorder_due = true;
     if (sim->params.remove_arrivals || sim->ghost_bound > 0 || sim->strip_ghosts || sim->mig_cap > 0) {
-        const int dst = (sim->cur + 2) % 3;
-        rc = compact_stage<S>(sim, out_idx, dst);
-        if (rc) return rc;
-        sim->cur = dst;
+        if (sim->mig_cap > 0) { // a strip: in place
+            rc = strip_fill_stage<S>(sim, out_idx);
+            if (rc) return rc;
+            sim->cur = out_idx;
+        } else {
+            const int dst = (sim->cur + 2) % 3;
+            rc = compact_stage<S>(sim, out_idx, dst);
+            if (rc) return rc;
+            sim->cur = dst;
+        }
         sim->n_bound -= sim->ghost_bound; // ghosts never survive a step
         sim->ghost_bound = 0;             // (strips: the bound is fixed and ghost_bound stays 0)
         sim->strip_ghosts = false;

@@ -68,6 +68,7 @@ __global__ void k_begin_step(GridPlan *plan)
     for (int c = 0; c < ORCA_MAX_CHUNKS; ++c) plan->fq_count[c] = plan->cq_count[c] = plan->gq_count[c] = 0;
     plan->n_pre = plan->n_owned;
     plan->idle = plan->halt_when_empty && plan->n_owned == 0;
+    plan->strip_removed = plan->hole_count = plan->tail_count = 0;
     plan->removed = 0;
     plan->min_sep_enc = enc_double(__longlong_as_double(0x7FF0000000000000LL));
     plan->sep_ub_enc = plan->min_sep_enc;
@@ -1887,6 +1888,62 @@ k_strip_keep_flags(GridPlan *__restrict__ plan, const u8 *__restrict__ arrived, 
         }
     }
     keep[i] = k;
+    // owned rows that go (emigrants, arrivals): counted for the in-place removal that follows
+    const unsigned gone = __ballot_sync(__activemask(), i < plan->n_owned && !k);
+    if (gone && (threadIdx.x & 31) == (unsigned)(__ffs((int)gone) - 1)) atomicAdd(&plan->strip_removed, __popc(gone));
+}
+
+// In-place removal for a strip. The step's result sits in rows [0, n_owned) followed by the ghosts;
+// the rows that go (keep == 0: emigrants, arrivals) are few. Instead of compacting every array into
+// its twin (214 B per agent of traffic, ~60 us per million agents), the survivors of the TAIL
+// [n', n_owned) -- n' = n_owned - removed -- move into the HOLES below n', and the ghosts are
+// dropped by the new row count. The order of a strip's rows means nothing (agents come and go
+// with every exchange): the logical row of a row IS its physical row there.
+__global__ void __launch_bounds__(256)
+k_strip_holes(GridPlan *__restrict__ plan, const int *__restrict__ keep, int *__restrict__ holes,
+              int *__restrict__ tail)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n_o = plan->n_owned;
+    if (i >= n_o) return;
+    const int n_new = n_o - plan->strip_removed;
+    if (i < n_new) {
+        if (!keep[i]) holes[atomicAdd(&plan->hole_count, 1)] = i;
+    } else if (keep[i]) {
+        tail[atomicAdd(&plan->tail_count, 1)] = i;
+    }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_strip_fill(const GridPlan *__restrict__ plan, const int *__restrict__ holes, const int *__restrict__ tail,
+             typename Vec<R>::T4 *__restrict__ pv, typename Vec<R>::T4 *__restrict__ gp,
+             typename Vec<R>::T2 *__restrict__ rm, i64 *__restrict__ ids, u8 *__restrict__ cls,
+             i8 *__restrict__ st, i8 *__restrict__ fa, float *__restrict__ hint, int *__restrict__ lrow,
+             Attr64 *__restrict__ a64)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= plan->hole_count) return; // == tail_count
+    const int d = holes[r], i = tail[r];
+    pv[d] = pv[i];
+    gp[d] = gp[i];
+    rm[d] = rm[i];
+    ids[d] = ids[i];
+    cls[d] = cls[i];
+    st[d] = st[i];
+    fa[d] = fa[i];
+    hint[d] = hint[i];
+    lrow[d] = d;
+    if (a64) a64[d] = a64[i];
+}
+
+__global__ void k_after_strip_fill(GridPlan *plan)
+{
+    const int kept = plan->n_owned - plan->strip_removed;
+    plan->removed = plan->strip_removed;
+    plan->n_after = kept;
+    plan->n = kept;
+    plan->n_owned = kept;
 }
 
 __global__ void k_set_frame(GridPlan *plan, i64 frame) { plan->frame = frame; }
