@@ -69,10 +69,17 @@ def load_traffic(workload, precision, kernel):
 
 
 def load_peaks():
+    """Measured HBM copy bandwidth of this pool's B200s (MEASURED_PEAKS.json, driver-written), else
+    the fallback B200_PROFILING.md states."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
+    try:
         with open(p) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+            peaks = json.load(f)
+        for key in ("hbm_gbs", "hbm_gb_s", "hbm_GBs", "hbm"):
+            if key in peaks and float(peaks[key]) > 0:
+                return float(peaks[key]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 

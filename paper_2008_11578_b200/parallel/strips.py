@@ -544,9 +544,11 @@ def run_bench(args, rank: int, world: int, local: int):
         hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         pk = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
                           "MEASURED_PEAKS.json")
-        if os.path.exists(pk):
+        try:
             with open(pk) as f:
                 hbm_peak, peak_src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
         solve_bytes = (16 + 32 + 1 + 4 * 16 + 1 + 16 + 16 + 2 + 1) * n_local     # bench.py SOLVE_BYTES_PER_AGENT
         achieved = solve_bytes / (max(stage_ms["solve"], 1e-9) * 1e-3) / 1e9
         ms_step = dev_ms / args.steps
