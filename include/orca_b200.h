@@ -293,11 +293,17 @@ ORCA_API int orca_debug_last_step(orca_sim *sim, int64_t n, int64_t *cell_ix, in
 /* Host arrays in the layout of _kernels.py:306-312: coff int64[n+1], cpts/cnrm
  * float64[m,2], tgt float64[n,2], caps float64[n], seeds uint64[n]; outputs
  * out_v float64[n,2], out_status int64[n] (0 feasible, 1 fallback used),
- * out_failed int64[n] (original constraint index or -1). Synchronous. */
+ * out_failed int64[n] (original constraint index or -1). Synchronous. The batch is cut into
+ * chunks of problems that are uploaded, packed and solved on two alternating streams, so with
+ * pinned host arrays the call is bound by the one PCIe crossing of the constraints. */
 ORCA_API int orca_lp_solve_batch(int device, int precision, int64_t n, const int64_t *coff,
                         const double *cpts, const double *cnrm, const double *tgt,
                         const double *caps, const uint64_t *seeds, double *out_v,
                         int64_t *out_status, int64_t *out_failed);
+
+/* orca_lp_solve_batch keeps its device scratch (~3 GB for a million problems) between calls;
+ * this gives it back. */
+ORCA_API int orca_lp_release_scratch(void);
 
 /* Resident variant for benchmarking: build once, solve many times on device. */
 typedef struct orca_lp_batch orca_lp_batch;

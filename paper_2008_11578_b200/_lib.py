@@ -30,7 +30,7 @@ SYMBOLS = [
     "orca_download_last_step_pv", "orca_download_last_step_kept",
     "orca_step", "orca_run", "orca_run_logged", "orca_sync", "orca_get_info", "orca_step_host", "orca_advance_host", "orca_reorder_rows",
     "orca_profile_stages", "orca_get_stage_ms",
-    "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_batch_create",
+    "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_release_scratch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
     "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
     "orca_least_penetration", "orca_neighbor_query",
@@ -125,6 +125,7 @@ def load():
     L.orca_get_stage_ms.argtypes = [vp, P(C.c_double), P(i64)]
     L.orca_debug_last_step.argtypes = [vp, i64] + [vp] * 8
     L.orca_lp_solve_batch.argtypes = [ci, ci, i64] + [vp] * 9
+    L.orca_lp_release_scratch.argtypes = []
     L.orca_lp_batch_create.argtypes = [P(vp), ci, ci, i64] + [vp] * 6
     L.orca_lp_batch_set_stream.argtypes = [vp, vp]
     L.orca_lp_batch_solve.argtypes = [vp]

@@ -127,9 +127,10 @@ def solve_range(coff, cpts, cnrm, tgt, caps, seeds, precision="f64", device: int
     """_kernels.solve_range over the whole batch on the GPU.
     Returns (out_v f64[n,2], status i64[n], failed_at i64[n])."""
     n, coff, cpts, cnrm, tgt, caps, seeds = _prep(coff, cpts, cnrm, tgt, caps, seeds)
-    out_v = np.empty((n, 2))
-    status = np.empty(n, dtype=np.int64)
-    failed = np.empty(n, dtype=np.int64)
+    from .engine import _host_empty          # pinned (pooled) result buffers when torch is there
+    out_v = _host_empty((n, 2))
+    status = _host_empty(n, np.int64)
+    failed = _host_empty(n, np.int64)
     check(load().orca_lp_solve_batch(device, _lp_precision(precision), n, ptr(coff), ptr(cpts),
                                      ptr(cnrm), ptr(tgt), ptr(caps), ptr(seeds), ptr(out_v),
                                      ptr(status), ptr(failed)))
