@@ -15,8 +15,10 @@ ORCA_BENCH_FORCE_STRIPS=1 python bench.py --steps 50 >> gpurun_out/g_strips.json
 python bench.py --gpus 2 --steps 30 >> gpurun_out/g_strips.jsonl 2>/dev/null
 python bench.py --gpus 4 --steps 20 --workload config5_8m --scaling strong >> gpurun_out/g_strips.jsonl 2>/dev/null
 ORCA_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/g_launches.csv python bench.py --steps 3 --warmup 3 --resident-only > gpurun_out/g_l.log 2>&1
-ORCA_GRAPH=0 ncu --set full --clock-control none --import-source on -k regex:"k_solve_group|k_gather_fast32|k_scatter|k_fallback_coop|k_count|k_gather" -s 40 -c 7 -o gpurun_out/g_full python bench.py --steps 3 --warmup 4 --resident-only > gpurun_out/g_f.log 2>&1
-ORCA_GRAPH=0 ncu --set full --clock-control none -k regex:"k_solve_group|k_fallback_coop" -s 12 -c 3 -o gpurun_out/g_full_d2 python bench.py --steps 3 --warmup 4 --resident-only --workload config3_262k_d2 > gpurun_out/g_fd2.log 2>&1
-ORCA_GRAPH=0 ncu --set full --clock-control none -k regex:"k_solve_cert|k_solve_group_queue|k_shuffle" -s 6 -c 3 -o gpurun_out/g_full_cert python bench.py --steps 3 --warmup 4 --resident-only --precision cert32 > gpurun_out/g_fc.log 2>&1
+# (--set full captures with ORCA_CHUNKS=1: one launch per kernel and step, the launches bench.py's per-stage timing and
+#  roofline.traffic refer to; the launch list above shows the real step, two chunks)
+ORCA_CHUNKS=1 ORCA_GRAPH=0 ncu --set full --clock-control none --import-source on -k regex:"k_solve_group|k_gather_fast32|k_scatter|k_fallback_coop|k_count|k_gather" -s 40 -c 7 -o gpurun_out/g_full python bench.py --steps 3 --warmup 4 --resident-only --precision mixed > gpurun_out/g_f.log 2>&1
+ORCA_CHUNKS=1 ORCA_GRAPH=0 ncu --set full --clock-control none -k regex:"k_solve_group|k_fallback_coop" -s 12 -c 3 -o gpurun_out/g_full_d2 python bench.py --steps 3 --warmup 4 --resident-only --workload config3_262k_d2 --precision mixed > gpurun_out/g_fd2.log 2>&1
+ORCA_CHUNKS=1 ORCA_GRAPH=0 ncu --set full --clock-control none -k regex:"k_solve_cert|k_solve_group_queue|k_shuffle" -s 6 -c 3 -o gpurun_out/g_full_cert python bench.py --steps 3 --warmup 4 --resident-only --precision cert32 > gpurun_out/g_fc.log 2>&1
 ncu --set full --clock-control none -k regex:k_lp_batch -s 4 -c 2 -o gpurun_out/g_full_lp python bench.py --workload lp_1m_infeasible --steps 2 --warmup 3 > gpurun_out/g_flp.log 2>&1
 ls -la gpurun_out/g_*
