@@ -678,6 +678,11 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="--gpus N > 1: weak = one `workload` plaza per GPU (default), strong = ONE "
                          "`workload` crowd cut into N strips (BASELINE config 5: --workload config5_8m)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "window", "sendrecv"],
+                    help="--gpus N > 1, how the strips' slabs travel: window = each strip's kernel writes them "
+                         "into its neighbours' memory (CUDA IPC peer mapping, flags; no library call per frame), "
+                         "sendrecv = grouped NCCL send/recv (gloo, staged through the host, when ranks share a "
+                         "GPU); auto = window, send/recv if a neighbour's window cannot be mapped")
     ap.add_argument("--no-verify", action="store_true",
                     help="--gpus N > 1: skip the bit-equality check against the same crowd on one GPU")
     args = ap.parse_args()

@@ -80,7 +80,8 @@ enum {
     ORCA_ECOINCIDENT = -3, /* engine.py:239-245: exactly coincident centres */
     ORCA_ERANGE = -4,      /* engine.py:152-153: position outside the indexable grid */
     ORCA_ECAPACITY = -5,   /* more agents than the handle was created for */
-    ORCA_EUNSUPPORTED = -6 /* e.g. max_neighbors above ORCA_MAX_NEIGHBORS */
+    ORCA_EUNSUPPORTED = -6, /* e.g. max_neighbors above ORCA_MAX_NEIGHBORS */
+    ORCA_ETIMEOUT = -7     /* orca_strip_window_wait: the neighbouring strip's exchange never arrived */
 };
 
 enum { ORCA_F32 = 0, ORCA_F64 = 1, ORCA_MIXED = 2, ORCA_CERT32 = 3 };
@@ -459,6 +460,36 @@ ORCA_API int orca_strip_append_slab(orca_sim *sim, const void *slab, int64_t cap
  * those are written to the migrant slabs (NULL = no neighbour on that side) as
  * orca_agent_record. */
 ORCA_API int orca_strip_step(orca_sim *sim, void *migrants_left, void *migrants_right, int64_t cap);
+
+/* ---- The exchange through peer memory (one node: NVLink / NVSwitch) ----------------------
+ * Instead of handing the slabs to a communication library, a strip WRITES them into its
+ * neighbour's memory. Each handle owns a WINDOW (one device allocation): per side a flag and two
+ * receive buffers of side_bytes = [emigrant slab | halo slab], double-buffered by the parity of
+ * the exchange index. orca_strip_window_push copies the used part of the sender's slabs (the
+ * counts are read from the headers ON THE DEVICE) into the neighbour's window and then raises
+ * the neighbour's flag to exchange + 1; orca_strip_window_wait makes the receiver's stream wait
+ * for its own flag (a one-thread kernel, bounded: ORCA_WINDOW_TIMEOUT_MS, default 20,000 --
+ * after that the sticky error ORCA_ETIMEOUT surfaces at the next orca_sync). Pack, copy, flag,
+ * wait and append are all kernels on the handles' streams: no host call of a library, no host
+ * synchronisation, nothing collective. The neighbour's window is mapped with the CUDA IPC handle
+ * orca_strip_window_create returns (another process, its own or the same GPU) or, for handles
+ * of the SAME process, given by its base address.
+ * Exchange indices count from 0 and must be pushed / waited for in order. */
+#define ORCA_IPC_HANDLE_BYTES 64
+ORCA_API int orca_strip_window_create(orca_sim *sim, int64_t side_bytes, void *ipc_handle_out /* 64 bytes */,
+                                      void **base_out);
+/* side: 0 = the neighbour on the left, 1 = on the right. Exactly one of ipc_handle /
+ * same_process_base is non-NULL. */
+ORCA_API int orca_strip_window_open(orca_sim *sim, int side, const void *ipc_handle, void *same_process_base);
+/* send = [emigrant slab (32 + mig_cap * 96 bytes) | halo slab (32 + halo_cap * record bytes)] */
+ORCA_API int orca_strip_window_push(orca_sim *sim, int side, const void *send, int64_t mig_cap, int64_t halo_cap,
+                                    int64_t exchange);
+/* *slab_out: where exchange `exchange` of that side lands in THIS handle's window (valid for
+ * kernels that follow on the handle's stream). */
+ORCA_API int orca_strip_window_wait(orca_sim *sim, int side, int64_t exchange, void **slab_out);
+/* Unmaps the neighbours' windows and frees this one (every strip must have finished its frames:
+ * synchronise the ranks first). Also done by orca_destroy. */
+ORCA_API int orca_strip_window_close(orca_sim *sim);
 
 /* Rows appended from slabs since the last orca_upload: ghosts, migrants (for
  * benchmarks). Synchronises. */

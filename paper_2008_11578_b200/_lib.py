@@ -21,7 +21,10 @@ ORCA_F32, ORCA_F64, ORCA_MIXED, ORCA_CERT32 = 0, 1, 2, 3
 ORCA_MAX_NEIGHBORS = 32
 ORCA_N_STAGES = 6
 STAGE_NAMES = ["bins", "gather", "solve", "fallback", "finish", "metrics"]
+ORCA_EINVAL, ORCA_ECUDA = -1, -2
 ORCA_ECOINCIDENT, ORCA_ERANGE = -3, -4
+ORCA_ECAPACITY, ORCA_EUNSUPPORTED, ORCA_ETIMEOUT = -5, -6, -7
+ORCA_IPC_HANDLE_BYTES = 64
 
 # every symbol include/orca_b200.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
@@ -37,6 +40,8 @@ SYMBOLS = [
     "orca_strip_pack", "orca_strip_append", "orca_strip_drop_ghosts",
     "orca_strip_halo_record_bytes", "orca_strip_configure", "orca_strip_pack_halo",
     "orca_strip_append_slab", "orca_strip_step", "orca_strip_stats",
+    "orca_strip_window_create", "orca_strip_window_open", "orca_strip_window_push",
+    "orca_strip_window_wait", "orca_strip_window_close",
 ]
 
 RECORD_BYTES = 96   # sizeof(orca_agent_record)
@@ -146,6 +151,11 @@ def load():
     L.orca_strip_append_slab.argtypes = [vp, vp, i64, ci]
     L.orca_strip_step.argtypes = [vp, vp, vp, i64]
     L.orca_strip_stats.argtypes = [vp, P(i64), P(i64)]
+    L.orca_strip_window_create.argtypes = [vp, i64, vp, P(vp)]
+    L.orca_strip_window_open.argtypes = [vp, ci, vp, vp]
+    L.orca_strip_window_push.argtypes = [vp, ci, vp, i64, i64, i64]
+    L.orca_strip_window_wait.argtypes = [vp, ci, i64, P(vp)]
+    L.orca_strip_window_close.argtypes = [vp]
     for name in SYMBOLS:
         fn = getattr(L, name)
         if name == "orca_strip_halo_record_bytes":

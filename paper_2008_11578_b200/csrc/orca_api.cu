@@ -75,6 +75,14 @@ struct orca_sim {
     double strip_lo = -INFINITY, strip_hi = INFINITY;
     void *mig_slab[2] = {nullptr, nullptr}; // migrant slabs of the running orca_strip_step
     int64_t mig_cap = 0;
+    // the exchange through peer memory (orca_strip_window_*)
+    unsigned char *win = nullptr;           // this handle's window: [flag line x 2][side x parity receive buffers]
+    int64_t win_side_bytes = 0, win_stride = 0;
+    unsigned char *win_peer[2] = {nullptr, nullptr}; // the neighbours' windows as mapped here
+    bool win_peer_ipc[2] = {false, false};           // ... through cudaIpcOpenMemHandle (to be closed)
+    unsigned *win_done = nullptr;                    // block counter of k_window_push
+    int64_t win_pushed[2] = {0, 0}, win_waited[2] = {0, 0}; // next exchange index per side
+    unsigned long long win_timeout_ns = 20000000000ULL;
 
     // per-step scratch
     int max_cells = 0;
@@ -253,6 +261,7 @@ extern "C" void orca_destroy(orca_sim *sim)
     if (!sim) return;
     cudaSetDevice(sim->device);
     if (sim->stream) cudaStreamSynchronize(sim->stream);
+    orca_strip_window_close(sim);
     for (int i = 0; i < 3; ++i) cudaFree(sim->pv[i]);
     for (int i = 0; i < 2; ++i) {
         cudaFree(sim->goalpref[i]);
@@ -648,6 +657,9 @@ static int fetch_plan(orca_sim *sim)
     if (h.err_capacity)
         return fail(sim, ORCA_ECAPACITY, "strip exchange: a slab or the handle capacity (%lld rows) overflowed",
                     (long long)sim->capacity);
+    if (h.err_window)
+        return fail(sim, ORCA_ETIMEOUT, "strip exchange: a neighbouring strip's slabs did not arrive within %.1f s",
+                    (double)sim->win_timeout_ns * 1e-9);
     if (h.err_pair != ORCA_NO_ERR)
         return fail(sim, ORCA_ECOINCIDENT,
                     "frame %lld: agents %lld and %lld have exactly coincident centers; "
@@ -1861,6 +1873,152 @@ extern "C" int orca_strip_step(orca_sim *sim, void *migrants_left, void *migrant
     sim->mig_slab[0] = sim->mig_slab[1] = nullptr;
     sim->mig_cap = 0;
     return rc;
+}
+
+// ---- the exchange through peer memory -------------------------------------------------
+static inline int64_t window_slot_offset(const orca_sim *sim, int side, int64_t exchange)
+{
+    return 2 * ORCA_WINDOW_FLAG_BYTES + (int64_t)(side * 2 + (int)(exchange & 1)) * sim->win_stride;
+}
+
+extern "C" int orca_strip_window_close(orca_sim *sim)
+{
+    if (!sim) return fail(nullptr, ORCA_EINVAL, "orca_strip_window_close: sim is NULL");
+    if (!sim->win) return ORCA_OK;
+    cudaSetDevice(sim->device);
+    if (sim->stream) cudaStreamSynchronize(sim->stream);
+    for (int s = 0; s < 2; ++s) {
+        if (sim->win_peer[s] && sim->win_peer_ipc[s]) cudaIpcCloseMemHandle(sim->win_peer[s]);
+        sim->win_peer[s] = nullptr;
+        sim->win_peer_ipc[s] = false;
+        sim->win_pushed[s] = sim->win_waited[s] = 0;
+    }
+    cudaFree(sim->win);
+    cudaFree(sim->win_done);
+    sim->win = nullptr;
+    sim->win_done = nullptr;
+    sim->win_side_bytes = sim->win_stride = 0;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_window_create(orca_sim *sim, int64_t side_bytes, void *ipc_handle_out, void **base_out)
+{
+    if (!sim || !sim->loaded) return fail(sim, ORCA_EINVAL, "orca_strip_window_create: no resident state");
+    if (!sim->strip_on) return fail(sim, ORCA_EINVAL, "orca_strip_window_create: orca_strip_configure was not called");
+    if (side_bytes < 2 * (int64_t)sizeof(orca_slab_header) || side_bytes % 16)
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_create: side_bytes = %lld", (long long)side_bytes);
+    static_assert(sizeof(cudaIpcMemHandle_t) == ORCA_IPC_HANDLE_BYTES, "ORCA_IPC_HANDLE_BYTES");
+    int rc = orca_strip_window_close(sim);
+    if (rc) return rc;
+    CK(sim, cudaSetDevice(sim->device));
+    sim->win_side_bytes = side_bytes;
+    sim->win_stride = (side_bytes + 255) & ~(int64_t)255;
+    const size_t bytes = (size_t)(2 * ORCA_WINDOW_FLAG_BYTES + 4 * sim->win_stride);
+    // (plain cudaMalloc: a pooled / virtual-memory allocation cannot be exported as an IPC handle)
+    CK(sim, cudaMalloc(reinterpret_cast<void **>(&sim->win), bytes));
+    CK(sim, cudaMalloc(reinterpret_cast<void **>(&sim->win_done), sizeof(unsigned)));
+    CK(sim, cudaMemsetAsync(sim->win, 0, bytes, sim->stream));
+    CK(sim, cudaMemsetAsync(sim->win_done, 0, sizeof(unsigned), sim->stream));
+    CK(sim, cudaStreamSynchronize(sim->stream)); // a neighbour may write as soon as it has the handle
+    if (const char *e = getenv("ORCA_WINDOW_TIMEOUT_MS")) {
+        const long long ms = atoll(e);
+        if (ms > 0) sim->win_timeout_ns = (unsigned long long)ms * 1000000ULL;
+    }
+    if (ipc_handle_out) {
+        cudaIpcMemHandle_t h;
+        CK(sim, cudaIpcGetMemHandle(&h, sim->win));
+        memcpy(ipc_handle_out, &h, sizeof(h));
+    }
+    if (base_out) *base_out = sim->win;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_window_open(orca_sim *sim, int side, const void *ipc_handle, void *same_process_base)
+{
+    if (!sim || !sim->win) return fail(sim, ORCA_EINVAL, "orca_strip_window_open: orca_strip_window_create was not called");
+    if (side < 0 || side > 1 || (!ipc_handle) == (!same_process_base))
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_open: bad arguments");
+    if (sim->win_peer[side]) return fail(sim, ORCA_EINVAL, "orca_strip_window_open: side %d is already open", side);
+    CK(sim, cudaSetDevice(sim->device));
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, ipc_handle, sizeof(h));
+        void *p = nullptr;
+        CK(sim, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        sim->win_peer[side] = static_cast<unsigned char *>(p);
+        sim->win_peer_ipc[side] = true;
+    } else {
+        // a handle of this process on another device: its memory must be mapped here
+        cudaPointerAttributes attr;
+        CK(sim, cudaPointerGetAttributes(&attr, same_process_base));
+        if (attr.type != cudaMemoryTypeDevice)
+            return fail(sim, ORCA_EINVAL, "orca_strip_window_open: same_process_base is not device memory");
+        if (attr.device != sim->device) {
+            int can = 0;
+            CK(sim, cudaDeviceCanAccessPeer(&can, sim->device, attr.device));
+            if (!can)
+                return fail(sim, ORCA_EUNSUPPORTED, "orca_strip_window_open: device %d cannot map the memory of device %d",
+                            sim->device, attr.device);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(attr.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(sim, e);
+            (void)cudaGetLastError();
+        }
+        sim->win_peer[side] = static_cast<unsigned char *>(same_process_base);
+        sim->win_peer_ipc[side] = false;
+    }
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_window_push(orca_sim *sim, int side, const void *send, int64_t mig_cap, int64_t halo_cap,
+                                      int64_t exchange)
+{
+    if (!sim || !sim->win) return fail(sim, ORCA_EINVAL, "orca_strip_window_push: no window");
+    if (side < 0 || side > 1 || !sim->win_peer[side])
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_push: side %d is not open", side);
+    if (!send || mig_cap < 0 || halo_cap < 0 || mig_cap > 0x7FFFFFFF || halo_cap > 0x7FFFFFFF)
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_push: bad arguments");
+    const int64_t rec = orca_strip_halo_record_bytes(sim);
+    const int64_t mig_bytes = (int64_t)sizeof(orca_slab_header) + mig_cap * (int64_t)sizeof(orca_agent_record);
+    const int64_t halo_bytes = (int64_t)sizeof(orca_slab_header) + halo_cap * rec;
+    if (mig_bytes + halo_bytes > sim->win_side_bytes)
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_push: slabs of %lld bytes, the windows hold %lld per side",
+                    (long long)(mig_bytes + halo_bytes), (long long)sim->win_side_bytes);
+    if (exchange != sim->win_pushed[side])
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_push: exchange %lld out of order (next is %lld)",
+                    (long long)exchange, (long long)sim->win_pushed[side]);
+    CK(sim, cudaSetDevice(sim->device));
+    // the neighbour sees this strip on its OTHER side
+    unsigned char *peer = sim->win_peer[side];
+    unsigned char *dst = peer + window_slot_offset(sim, 1 - side, exchange);
+    unsigned long long *flag = reinterpret_cast<unsigned long long *>(peer + (1 - side) * ORCA_WINDOW_FLAG_BYTES);
+    const int64_t vec = (mig_bytes + halo_bytes) / 16;
+    const int blocks = (int)std::min<int64_t>(std::max<int64_t>((vec + 1023) / 1024, 1), (int64_t)296); // (at most two blocks per SM of a B200)
+    k_window_push<<<blocks, 256, 0, sim->stream>>>(static_cast<const unsigned char *>(send), dst, (long long)mig_bytes,
+                                                   (int)mig_cap, (int)halo_cap, (int)rec, flag,
+                                                   (unsigned long long)(exchange + 1), sim->win_done);
+    CKL(sim);
+    sim->launches += 1;
+    sim->win_pushed[side] = exchange + 1;
+    return ORCA_OK;
+}
+
+extern "C" int orca_strip_window_wait(orca_sim *sim, int side, int64_t exchange, void **slab_out)
+{
+    if (!sim || !sim->win) return fail(sim, ORCA_EINVAL, "orca_strip_window_wait: no window");
+    if (side < 0 || side > 1 || !slab_out) return fail(sim, ORCA_EINVAL, "orca_strip_window_wait: bad arguments");
+    if (exchange < sim->win_waited[side] - 1 || exchange > sim->win_waited[side])
+        return fail(sim, ORCA_EINVAL, "orca_strip_window_wait: exchange %lld out of order (next is %lld)",
+                    (long long)exchange, (long long)sim->win_waited[side]);
+    CK(sim, cudaSetDevice(sim->device));
+    const unsigned long long *flag = reinterpret_cast<const unsigned long long *>(sim->win + side * ORCA_WINDOW_FLAG_BYTES);
+    if (exchange == sim->win_waited[side]) { // (a repeated wait for the last exchange just returns the address)
+        k_window_wait<<<1, 1, 0, sim->stream>>>(sim->plan, flag, (unsigned long long)(exchange + 1), sim->win_timeout_ns);
+        CKL(sim);
+        sim->launches += 1;
+        sim->win_waited[side] = exchange + 1;
+    }
+    *slab_out = sim->win + window_slot_offset(sim, side, exchange);
+    return ORCA_OK;
 }
 
 extern "C" int orca_strip_stats(orca_sim *sim, int64_t *ghost_rows, int64_t *migrant_rows)

@@ -44,6 +44,7 @@ struct GridPlan {
     i64 err_id_i, err_id_j;
     int err_range;  // a position left the reference's indexable grid range
     int err_capacity; // a strip-exchange slab (or the handle) overflowed: rows were dropped or kept back
+    int err_window;   // k_window_wait gave up: the neighbouring strip's exchange never arrived
     // strip step: rows removed in place (orca_api.cu, strip_fill_stage)
     int strip_removed, hole_count, tail_count;
     unsigned long long strip_recv[2]; // ghost rows / migrant rows appended from slabs since the upload

@@ -1829,6 +1829,71 @@ __global__ void k_after_append_slab(GridPlan *plan, const orca_slab_header *__re
     if (ghost != 2) plan->strip_recv[ghost ? 0 : 1] += (unsigned long long)count; // (2: own emigrants kept as ghosts)
 }
 
+// ---- peer-memory window (orca_strip_window_*): the exchange without a communication library ----
+// A strip's window is one device allocation: a flag line per side, then per side two receive
+// buffers ([emigrant slab | halo slab], double-buffered by the parity of the exchange index).
+// The SENDER writes its slabs straight into the neighbour's window (peer mapping: NVLink) and
+// then raises that window's flag to `exchange + 1`; the RECEIVER's stream waits on its own
+// flag. Double buffering is enough without an acknowledgement: exchange e + 2 (same parity as
+// e) is only pushed after this rank has waited for the neighbour's exchange e + 1, which the
+// neighbour pushed -- in stream order -- after appending what exchange e brought.
+#define ORCA_WINDOW_FLAG_BYTES 128
+
+// copy the USED part of [emigrant slab | halo slab] (the counts are in the headers) to `dst`,
+// then -- once every block's stores are fenced system-wide -- publish the flag
+__global__ void __launch_bounds__(256)
+k_window_push(const unsigned char *__restrict__ send, unsigned char *__restrict__ dst, long long mig_bytes,
+              int mig_cap, int halo_cap, int halo_rec_bytes, unsigned long long *flag, unsigned long long value,
+              unsigned *done)
+{
+    const orca_slab_header *hm = reinterpret_cast<const orca_slab_header *>(send);
+    const orca_slab_header *hh = reinterpret_cast<const orca_slab_header *>(send + mig_bytes);
+    const long long used_m = (long long)sizeof(orca_slab_header) +
+                             (long long)min(max(hm->count, 0), mig_cap) * (long long)sizeof(orca_agent_record);
+    const long long used_h = (long long)sizeof(orca_slab_header) +
+                             (long long)min(max(hh->count, 0), halo_cap) * (long long)halo_rec_bytes;
+    const long long vm = used_m / 16, vh = used_h / 16; // (every size above is a multiple of 16)
+    const uint4 *sm = reinterpret_cast<const uint4 *>(send), *sh = reinterpret_cast<const uint4 *>(send + mig_bytes);
+    uint4 *dm = reinterpret_cast<uint4 *>(dst), *dh = reinterpret_cast<uint4 *>(dst + mig_bytes);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < vm + vh; i += stride) {
+        if (i < vm) dm[i] = sm[i];
+        else dh[i - vm] = sh[i - vm];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atomicAdd(done, 1u);
+        if (ticket == gridDim.x - 1) { // the last block: every other block's stores are fenced
+            *done = 0;
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned long long *>(flag) = value;
+            __threadfence_system();
+        }
+    }
+}
+
+// the receiving stream stalls here until the neighbour's exchange has landed; bounded, so a
+// neighbour that died surfaces as ORCA_ETIMEOUT at the next synchronisation instead of a hang
+__global__ void k_window_wait(GridPlan *plan, const unsigned long long *flag, unsigned long long want,
+                              unsigned long long timeout_ns)
+{
+    if (plan->err_window) return;
+    const volatile unsigned long long *f = flag;
+    unsigned long long t0 = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*f < want) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > timeout_ns) {
+            plan->err_window = 1;
+            break;
+        }
+        __nanosleep(256);
+    }
+    __threadfence_system();
+}
+
 // keep flags of the strip step: owned rows that have not arrived AND whose new x is still
 // inside [lo, hi); the ones that left go into the migrant slab of that side as full records
 // and are removed by the compaction that follows (ghosts are always dropped). A row that does

@@ -54,7 +54,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .._lib import RECORD_BYTES, SLAB_HEADER_BYTES, check, load
+from .._lib import ORCA_IPC_HANDLE_BYTES, RECORD_BYTES, SLAB_HEADER_BYTES, check, load
 
 __all__ = ["DeviceStripOps", "StripDriver", "strip_bounds", "check_strip_widths", "state_hash",
            "run_bench"]
@@ -139,6 +139,32 @@ class DeviceStripOps:
     def _p(t):
         return C.c_void_p(t.data_ptr()) if t is not None else None
 
+    # -- the exchange through peer memory (orca_strip_window_*) --
+    def window_create(self, side_bytes: int):
+        """This handle's window: (CUDA IPC handle as bytes, base address, the window as a uint8
+        tensor view for the slots `window_wait` returns)."""
+        h = (C.c_ubyte * ORCA_IPC_HANDLE_BYTES)()
+        base = C.c_void_p()
+        check(self._L.orca_strip_window_create(self.sim._h, int(side_bytes), h, C.byref(base)), self.sim._h)
+        return bytes(h), int(base.value)
+
+    def window_open(self, side: int, ipc_handle: bytes | None = None, base: int | None = None):
+        buf = (C.c_ubyte * ORCA_IPC_HANDLE_BYTES).from_buffer_copy(ipc_handle) if ipc_handle is not None else None
+        check(self._L.orca_strip_window_open(self.sim._h, int(side), buf,
+                                             C.c_void_p(base) if base is not None else None), self.sim._h)
+
+    def window_push(self, side: int, send, mig_cap: int, halo_cap: int, exchange: int):
+        check(self._L.orca_strip_window_push(self.sim._h, int(side), self._p(send), int(mig_cap), int(halo_cap),
+                                             int(exchange)), self.sim._h)
+
+    def window_wait(self, side: int, exchange: int) -> int:
+        out = C.c_void_p()
+        check(self._L.orca_strip_window_wait(self.sim._h, int(side), int(exchange), C.byref(out)), self.sim._h)
+        return int(out.value)
+
+    def window_close(self):
+        check(self._L.orca_strip_window_close(self.sim._h), self.sim._h)
+
     def pack_halo(self, reach: float, slab_left, slab_right, cap: int):
         check(self._L.orca_strip_pack_halo(self.sim._h, float(reach), self._p(slab_left),
                                            self._p(slab_right), int(cap)), self.sim._h)
@@ -166,6 +192,18 @@ class DeviceStripOps:
         self.sim.reorder_rows()
 
 
+class _DevAddr:
+    """A raw device address where the ops expect a tensor (a slot of the handle's window)."""
+
+    __slots__ = ("addr",)
+
+    def __init__(self, addr: int):
+        self.addr = int(addr)
+
+    def data_ptr(self) -> int:
+        return self.addr
+
+
 class StripDriver:
     """One rank's side of the strip protocol."""
 
@@ -173,8 +211,17 @@ class StripDriver:
 
     def __init__(self, ops, rank: int, world: int, bounds, neighbor_radius: float, device,
                  halo_capacity: int, migrant_capacity: int | None = None, group=None,
-                 vmax: float = 0.0, dt: float = 0.0, resync_every: int = 16):
+                 vmax: float = 0.0, dt: float = 0.0, resync_every: int = 16, transport: str = "sendrecv"):
+        """transport: "sendrecv" -- the slabs travel through torch.distributed (NCCL between GPUs;
+        gloo, staged through the host, when several ranks share one); "window" -- every strip writes
+        its slabs into its neighbours' memory (orca_strip_window_*, CUDA IPC / peer mappings: one
+        node) and the receiving stream waits on a flag: no library call per frame at all. After
+        construction a "window" driver must be connected: connect_windows() (ranks = processes)
+        or connect_local() (several drivers in one process)."""
+        if transport not in ("sendrecv", "window"):
+            raise ValueError(f"transport must be 'sendrecv' or 'window', got {transport!r}")
         self.ops, self.rank, self.world, self.group = ops, rank, world, group
+        self.transport = transport
         b = [-math.inf] + [float(v) for v in bounds] + [math.inf]
         if len(b) != world + 1:
             raise ValueError(f"{world} strips need {world - 1} interior boundaries, got {len(b) - 2}")
@@ -195,10 +242,20 @@ class StripDriver:
         def buffers():
             return {s: (torch.zeros(mb + hb, dtype=torch.uint8, device=self.device)
                         if self.peer[s] is not None else None) for s in self.SIDES}
-        self.send, self.recv = buffers(), buffers()
         view = lambda d, lo, hi: {s: (t[lo:hi] if t is not None else None) for s, t in d.items()}  # noqa: E731
+        self.send = buffers()
         self.send_mig, self.send_halo = view(self.send, 0, mb), view(self.send, mb, mb + hb)
-        self.recv_mig, self.recv_halo = view(self.recv, 0, mb), view(self.recv, mb, mb + hb)
+        if transport == "window":
+            # the receive buffers live in this handle's window, where the neighbours write them;
+            # recv_mig / recv_halo are filled in (as addresses) by the wait of each exchange
+            self.recv = {s: None for s in self.SIDES}
+            self.recv_mig, self.recv_halo = dict(self.recv), dict(self.recv)
+        else:
+            self.recv = buffers()
+            self.recv_mig, self.recv_halo = view(self.recv, 0, mb), view(self.recv, mb, mb + hb)
+        self.exchanges = 0               # exchanges issued so far (the index of the next one)
+        self._connected = transport != "window"
+        self._immigrants_done = False    # flush() has already appended the pending immigrants
         self.frames = 0
         self.reorder_every = 64          # frames between row reorderings (no ghosts resident then)
         self.resync_every = int(resync_every)
@@ -212,6 +269,44 @@ class StripDriver:
         # immigrants of every frame until the next synchronisation
         slack = 2 * self.halo_cap + 2 * self.mig_cap * (max(self.resync_every, 1) + 1)
         ops.configure(self.lo, self.hi, float(vmax), slack)
+        if transport == "window":
+            self.window_handle, self.window_base = ops.window_create(mb + hb)
+
+    # -- "window" transport: map the neighbours' windows ------------------------------
+    def connect_windows(self):
+        """Ranks are processes: every rank publishes (host name, device, IPC handle) and maps the
+        windows of its two neighbours. One all_gather of a few bytes, at set-up only."""
+        import socket
+        mine = (socket.gethostname(), self.window_handle)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=self.group)
+        for k, s in enumerate(self.SIDES):
+            p = self.peer[s]
+            if p is None:
+                continue
+            if everyone[p][0] != mine[0]:
+                raise RuntimeError(f"strip {self.rank} and strip {p} are on different hosts ({mine[0]}, "
+                                   f"{everyone[p][0]}): the window transport maps peer memory and needs one "
+                                   "node; use transport='sendrecv'")
+            self.ops.window_open(k, ipc_handle=everyone[p][1])
+        self._connected = True
+        dist.barrier(group=self.group)      # nobody pushes into a window its owner has not created yet
+
+    def connect_local(self, left=None, right=None):
+        """Several drivers in ONE process (tests, one process driving several GPUs): the
+        neighbours' windows are given by their drivers."""
+        for k, other in enumerate((left, right)):
+            if (other is None) != (self.peer[self.SIDES[k]] is None):
+                raise ValueError(f"strip {self.rank}: neighbour on side {self.SIDES[k]} does not match the layout")
+            if other is not None:
+                self.ops.window_open(k, base=other.window_base)
+        self._connected = True
+
+    def close(self):
+        """Unmap / free the window (after every rank has finished its frames)."""
+        if self.transport == "window" and self._connected:
+            self.ops.window_close()
+            self._connected = False
 
     # -- one exchange with both neighbours: fixed-size buffers, one grouped call ----
     def _swap(self):
@@ -240,22 +335,49 @@ class StripDriver:
             dst.copy_(src)
 
     def exchange(self):
-        stream = getattr(self.ops, "stream", None)
-        if stream is None:
-            self._swap()
+        if self.transport == "window":
+            if not self._connected:
+                raise RuntimeError("window transport: call connect_windows() / connect_local() first")
+            # the used part of [emigrants | halo] goes straight into the neighbour's window, then its flag
+            for k, s in enumerate(self.SIDES):
+                if self.peer[s] is not None:
+                    self.ops.window_push(k, self.send[s], self.mig_cap, self.halo_cap, self.exchanges)
         else:
-            with torch.cuda.stream(stream):  # the handle's stream is the current one for the transport
+            stream = getattr(self.ops, "stream", None)
+            if stream is None:
                 self._swap()
+            else:
+                with torch.cuda.stream(stream):  # the handle's stream is the current one for the transport
+                    self._swap()
+        self.mark_exchanged()
+
+    def mark_exchanged(self):
+        """The slabs of one more exchange are on their way / in place (also called by tests that
+        move the buffers themselves)."""
+        self.exchanges += 1
         self._pending = True
+        self._immigrants_done = False
+
+    def _await_exchange(self):
+        """window transport: the handle's stream waits for the last exchange of both neighbours;
+        the slabs are then where the neighbours wrote them."""
+        if self.transport != "window":
+            return
+        for k, s in enumerate(self.SIDES):
+            if self.peer[s] is not None:
+                addr = self.ops.window_wait(k, self.exchanges - 1)
+                self.recv_mig[s], self.recv_halo[s] = _DevAddr(addr), _DevAddr(addr + self._mb)
 
     # -- protocol phases (split so a test can drive several ranks in one process) ------
     def append_received(self):
         """Phase 1: immigrants as owned rows, then the ghosts (received halo, own emigrants)."""
         if not self._pending:
             return
-        for s in self.SIDES:
-            if self.peer[s] is not None:
-                self.ops.append_slab(self.recv_mig[s], self.mig_cap, 0)
+        self._await_exchange()
+        if not self._immigrants_done:
+            for s in self.SIDES:
+                if self.peer[s] is not None:
+                    self.ops.append_slab(self.recv_mig[s], self.mig_cap, 0)
         for s in self.SIDES:
             if self.peer[s] is not None:
                 self.ops.append_slab(self.recv_halo[s], self.halo_cap, 1)
@@ -299,12 +421,12 @@ class StripDriver:
     def flush(self):
         """Append what the last exchange brought as OWNED rows only (the immigrants), so that
         the resident state is the strip's agents and nothing else -- before reading it back."""
-        if self._pending:
+        if self._pending and not self._immigrants_done:
+            self._await_exchange()
             for s in self.SIDES:
                 if self.peer[s] is not None:
                     self.ops.append_slab(self.recv_mig[s], self.mig_cap, 0)
-                    # (consumed: a later append_received must not add them again)
-                    self._zero_header(self.recv_mig[s])
+            self._immigrants_done = True     # (a later append_received must not add them again)
         self.resync()
 
     def step(self):
@@ -440,8 +562,34 @@ def run_bench(args, rank: int, world: int, local: int):
     resync_every = 16
     halo_cap, mig_cap = _slab_capacities(cfg, n_local, side, density, vmax)
     sim = _strip_sim(cfg, state, args, local, stream, halo_cap, mig_cap, resync_every)
-    drv = StripDriver(DeviceStripOps(sim, stream), rank, world, bounds, cfg.neighbor_radius, device, halo_cap,
-                      mig_cap, vmax=vmax, dt=cfg.dt, resync_every=resync_every)
+    ops = DeviceStripOps(sim, stream)
+
+    def make_driver(transport):
+        return StripDriver(ops, rank, world, bounds, cfg.neighbor_radius, device, halo_cap, mig_cap, vmax=vmax,
+                           dt=cfg.dt, resync_every=resync_every, transport=transport)
+
+    # transport: peer-memory windows by default (one node: every rank maps its neighbours' windows
+    # through CUDA IPC); if ANY rank cannot map its neighbour, all fall back to send/recv together
+    want = getattr(args, "transport", "auto")
+    transport_note = None
+    if want in ("auto", "window") and world > 1:
+        drv = make_driver("window")
+        err = ""
+        try:
+            drv.connect_windows()
+        except Exception as exc:             # noqa: BLE001 -- reported in the line, see below
+            err = f"{type(exc).__name__}: {exc}"
+        bad = torch.tensor([1.0 if err else 0.0], dtype=torch.float64, device=rdev)
+        dist.all_reduce(bad, op=dist.ReduceOp.SUM)
+        if float(bad.item()) > 0:
+            if want == "window":
+                raise RuntimeError(f"--transport window: {int(bad.item())} rank(s) could not map a neighbour's "
+                                   f"window ({err or 'see the other ranks'})")
+            drv.close()
+            transport_note = "peer-memory windows unavailable, send/recv instead" + (f" ({err})" if err else "")
+            drv = make_driver("sendrecv")
+    else:
+        drv = make_driver("sendrecv")
 
     warm = max(args.warmup, 3)
     for _ in range(warm):
@@ -564,10 +712,19 @@ def run_bench(args, rank: int, world: int, local: int):
                            "density_per_m2": density, "neighbor_radius": cfg.neighbor_radius,
                            "max_neighbors": cfg.max_neighbors, "dt": cfg.dt, "tau": cfg.tau},
                 "parallelism": {"layout": f"x-strips={world}", "agents_rank0": n_local, "agents_total": n_total,
-                                "exchange": "fixed-capacity slabs, device-side counts, grouped send/recv "
-                                            "with the adjacent strips; no collective per frame",
-                                "backend": dist.get_backend() + (" (slabs staged through the host: several "
-                                                                 "ranks share a GPU)" if drv._stage else ""),
+                                "transport": drv.transport,
+                                "exchange": ("fixed-capacity slabs with device-side counts; each strip's kernel "
+                                             "writes the used part of its slabs into the adjacent strips' memory "
+                                             "(CUDA IPC peer mapping) and raises a flag the receiving stream waits "
+                                             "on: no library call, no collective per frame"
+                                             if drv.transport == "window" else
+                                             "fixed-capacity slabs, device-side counts, grouped send/recv "
+                                             "with the adjacent strips; no collective per frame"),
+                                "transport_note": transport_note,
+                                "backend": dist.get_backend() + (
+                                    " (set-up and timing reductions only)" if drv.transport == "window" else
+                                    " (slabs staged through the host: several ranks share a GPU)" if drv._stage
+                                    else ""),
                                 "halo_record_bytes": drv.ops.halo_record_bytes, "migrant_record_bytes": RECORD_BYTES,
                                 "halo_slab_records": halo_cap, "migrant_slab_records": mig_cap,
                                 "halo_records_per_step": float(tot[2]) / args.steps,
@@ -593,5 +750,8 @@ def run_bench(args, rank: int, world: int, local: int):
                              "note": "rank 0's dominant kernel; the step is issue/latency bound (DESIGN.md s5)"},
                 "cpu_baseline": None,
                 "note": "multi-GPU line: device-timed max over ranks; cpu_baseline is reported by the N=1 run"}
+    torch.cuda.synchronize()
+    dist.barrier()          # (window transport: nobody frees a window a neighbour may still be writing)
+    drv.close()
     sim.close()
     return line if rank == 0 else None

@@ -10,10 +10,13 @@ python bench.py --impl reference > gpurun_out/g_ref.json 2>/dev/null
 rm -f gpurun_out/g_configs.jsonl gpurun_out/g_lp.jsonl gpurun_out/g_strips.jsonl
 for wl in config1_1k config2_16k config3_262k_d1 config3_262k_d2 config3_262k_d1_nr3 config3_262k_d2_nr3 blobs_1m config5_8m; do python bench.py --workload $wl --no-extras >> gpurun_out/g_configs.jsonl 2>/dev/null; done
 for wl in lp_1m_feasible lp_1m_half lp_1m_infeasible; do for p in f64 f32; do python bench.py --workload $wl --precision $p >> gpurun_out/g_lp.jsonl 2>/dev/null; done; done
-# the multi-rank path on this one-GPU box: one rank over NCCL, then 2 and 4 ranks sharing the GPU (slabs over gloo)
+# the multi-rank path on this one-GPU box: one rank over NCCL, then 2 and 4 ranks (processes) sharing the GPU --
+# through peer-memory windows (CUDA IPC; the default transport) and through send/recv (gloo, staged through the host)
 ORCA_BENCH_FORCE_STRIPS=1 python bench.py --steps 50 >> gpurun_out/g_strips.jsonl 2>/dev/null
 python bench.py --gpus 2 --steps 30 >> gpurun_out/g_strips.jsonl 2>/dev/null
 python bench.py --gpus 4 --steps 20 --workload config5_8m --scaling strong >> gpurun_out/g_strips.jsonl 2>/dev/null
+python bench.py --gpus 2 --steps 30 --transport sendrecv >> gpurun_out/g_strips.jsonl 2>/dev/null
+python bench.py --gpus 4 --steps 20 --workload config5_8m --scaling strong --transport sendrecv >> gpurun_out/g_strips.jsonl 2>/dev/null
 ORCA_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/g_launches.csv python bench.py --steps 3 --warmup 3 --resident-only > gpurun_out/g_l.log 2>&1
 # (--set full captures with ORCA_CHUNKS=1: one launch per kernel and step, the launches bench.py's per-stage timing and
 #  roofline.traffic refer to; the launch list above shows the real step, two chunks)

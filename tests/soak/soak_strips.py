@@ -2,7 +2,9 @@
 adjacent strips with device-to-device buffer swaps in place of NCCL (tests/test_gpu_strips.py),
 random crowds / densities / strip counts, 12 frames with a row reordering every third frame; the
 decomposed crowd must equal the single-handle run bit for bit, keyed by id.
-    python tests/soak/soak_strips.py [first_seed] [count]"""
+    python tests/soak/soak_strips.py [first_seed] [count] [sendrecv|window|both]
+"window": the handles exchange through their peer-memory windows (kernels write the neighbour's
+window and raise its flag) instead of the test's buffer swaps; "both" alternates by seed."""
 import os
 import sys
 import time
@@ -20,6 +22,7 @@ from paper_2008_11578_b200.parallel.strips import strip_bounds  # noqa: E402
 
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+mode = sys.argv[3] if len(sys.argv) > 3 else "sendrecv"
 bad, t0, ran = [], time.time(), 0
 for seed in range(first, first + count):
     rng = np.random.default_rng(seed)
@@ -39,7 +42,8 @@ for seed in range(first, first + count):
         if min(b[i + 1] - b[i] for i in range(world)) < cfg.neighbor_radius + 1.0:
             continue                                   # strips must be wider than the halo reach (StripDriver checks)
         sims, drivers, _b = build_strips(st, cfg, precision, world, halo_cap=n, mig_cap=n,
-                                         resync_every=int(rng.integers(1, 6)), capacity=5 * n)
+                                         resync_every=int(rng.integers(1, 6)), capacity=5 * n,
+                                         transport=mode if mode != "both" else ("window", "sendrecv")[(seed // 2) % 2])
         lockstep(drivers, steps)
         ran += 1
         parts = [s.state() for s in sims]

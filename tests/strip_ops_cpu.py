@@ -219,9 +219,10 @@ def gloo_worker(rank, world, port, steps, out_dir):
         dist.destroy_process_group()
 
 
-def gpu_gloo_worker(rank, world, port, steps, out_dir, precision):
-    """One of several ranks sharing cuda:0: the CUDA handle behind DeviceStripOps, slabs staged
-    through the host and sent over gloo (tests/test_gpu_strips.py)."""
+def gpu_gloo_worker(rank, world, port, steps, out_dir, precision, transport="sendrecv"):
+    """One of several ranks sharing cuda:0: the CUDA handle behind DeviceStripOps; the slabs are
+    staged through the host and sent over gloo ("sendrecv"), or written by each process's kernel
+    into its neighbours' windows through CUDA IPC ("window") (tests/test_gpu_strips.py)."""
     import torch
     import torch.distributed as dist
 
@@ -241,13 +242,19 @@ def gpu_gloo_worker(rank, world, port, steps, out_dir, precision):
             sim.load(take(st, mine))
             drv = StripDriver(DeviceStripOps(sim), rank, world, bounds, cfg.neighbor_radius,
                               torch.device("cuda", 0), halo_capacity=n, migrant_capacity=n // 4,
-                              vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=4)
-            assert drv._stage
+                              vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=4, transport=transport)
+            if transport == "window":
+                drv.connect_windows()
+            else:
+                assert drv._stage
             for _ in range(steps):
                 drv.step()
             drv.flush()
             out = sim.state()
             g, m = drv.ops.stats()
+            torch.cuda.synchronize()
+            dist.barrier()           # nobody frees a window its neighbour may still be writing
+            drv.close()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), ids=out.ids, positions=out.positions,
                  velocities=out.velocities, halo_recv=g, migr_recv=m)
         dist.barrier()

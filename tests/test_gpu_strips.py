@@ -22,8 +22,14 @@ SIDE = {"left": "right", "right": "left"}
 
 def lockstep(drivers, steps, reorder_every=3):
     """Drive all ranks phase by phase; rank r's `right` buffer goes to rank r+1's `left`
-    (a device-to-device copy on the legacy stream in place of the NCCL send/recv)."""
+    (a device-to-device copy on the legacy stream in place of the NCCL send/recv). Drivers on
+    the window transport exchange for real: every handle's kernel writes into its neighbours'
+    windows and their streams wait on the flags -- no synchronisation from here."""
     def exchange():
+        if drivers[0].transport == "window":
+            for d in drivers:
+                d.exchange()
+            return
         torch.cuda.synchronize()
         for d in drivers:
             for side in ("left", "right"):
@@ -31,7 +37,7 @@ def lockstep(drivers, steps, reorder_every=3):
                     drivers[d.peer[side]].recv[SIDE[side]].copy_(d.send[side])
         torch.cuda.synchronize()
         for d in drivers:
-            d._pending = True
+            d.mark_exchanged()
 
     for d in drivers:
         d.reorder_every = reorder_every
@@ -53,7 +59,8 @@ def lockstep(drivers, steps, reorder_every=3):
         d.flush()
 
 
-def build_strips(st, cfg, precision, world, halo_cap, mig_cap, resync_every=4, capacity=None):
+def build_strips(st, cfg, precision, world, halo_cap, mig_cap, resync_every=4, capacity=None,
+                 transport="sendrecv"):
     n = st.ids.shape[0]
     bounds = strip_bounds(st.positions[:, 0], world)
     b = [-np.inf] + list(bounds) + [np.inf]
@@ -65,12 +72,18 @@ def build_strips(st, cfg, precision, world, halo_cap, mig_cap, resync_every=4, c
         sims.append(sim)
         drivers.append(StripDriver(DeviceStripOps(sim), r, world, bounds, cfg.neighbor_radius,
                                    torch.device("cuda", 0), halo_cap, mig_cap,
-                                   vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=resync_every))
+                                   vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=resync_every,
+                                   transport=transport))
+    if transport == "window":
+        for r, d in enumerate(drivers):
+            d.connect_local(drivers[r - 1] if r > 0 else None, drivers[r + 1] if r + 1 < world else None)
     return sims, drivers, b
 
 
-@pytest.mark.parametrize("precision,world", [("f64", 2), ("mixed", 3), ("f32", 2)])
-def test_strips_on_device_equal_single_handle(precision, world):
+@pytest.mark.parametrize("precision,world,transport", [("f64", 2, "sendrecv"), ("mixed", 3, "sendrecv"),
+                                                       ("f32", 2, "sendrecv"), ("f64", 3, "window"),
+                                                       ("mixed", 4, "window"), ("cert32", 2, "window")])
+def test_strips_on_device_equal_single_handle(precision, world, transport):
     st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
     n = st.ids.shape[0]
     steps = 8
@@ -78,7 +91,7 @@ def test_strips_on_device_equal_single_handle(precision, world):
         ref.load(st)
         ref.run(steps)
         want = ref.state()
-    sims, drivers, b = build_strips(st, cfg, precision, world, halo_cap=n, mig_cap=n // 4)
+    sims, drivers, b = build_strips(st, cfg, precision, world, halo_cap=n, mig_cap=n // 4, transport=transport)
     assert drivers[0].ops.halo_record_bytes == (64 if precision == "f64" else 32)
     lockstep(drivers, steps)
     parts = [s.state() for s in sims]
@@ -130,6 +143,34 @@ def test_strips_with_arrival_removal_equal_single_handle():
     assert np.array_equal(ids[order], want.ids[ref_order])
     assert np.array_equal(np.concatenate([p.positions for p in parts])[order], want.positions[ref_order])
     assert np.array_equal(np.concatenate([p.velocities for p in parts])[order], want.velocities[ref_order])
+    for s in sims:
+        s.close()
+
+
+def test_window_wait_gives_up_with_an_error_instead_of_hanging(monkeypatch):
+    """A neighbour that never delivers: the receiving stream's wait is bounded and the failure
+    surfaces as ORCA_ETIMEOUT at the next synchronisation."""
+    monkeypatch.setenv("ORCA_WINDOW_TIMEOUT_MS", "200")
+    st, cfg = S.make_crowd(seed=4, n_ped=2000, n_veh=100, density=0.5)
+    n = st.ids.shape[0]
+    sims, drivers, _b = build_strips(st, cfg, "mixed", 2, halo_cap=n, mig_cap=n // 4, transport="window")
+    d0 = drivers[0]
+    d0.prime()
+    d0.exchange()                    # strip 0 delivers, strip 1 never does
+    d0.begin_frame()
+    d0.append_received()             # waits for strip 1's exchange 0 on the device
+    with pytest.raises(OrcaError) as e:
+        d0.resync()
+    assert e.value.code == _lib.ORCA_ETIMEOUT and "did not arrive" in str(e.value)
+    # refusals of the window calls themselves
+    L = _lib.load()
+    assert L.orca_strip_window_push(sims[1]._h, 0, None, 8, 8, 0) == _lib.ORCA_EINVAL       # no send buffer
+    assert L.orca_strip_window_push(sims[1]._h, 1, C.c_void_p(drivers[1].send["left"].data_ptr()), 8, 8, 0) \
+        == _lib.ORCA_EINVAL                                                                   # no neighbour there
+    assert L.orca_strip_window_push(sims[1]._h, 0, C.c_void_p(drivers[1].send["left"].data_ptr()), 8, 8, 3) \
+        == _lib.ORCA_EINVAL                                                                   # out of order
+    out = C.c_void_p()
+    assert L.orca_strip_window_wait(sims[1]._h, 0, 5, C.byref(out)) == _lib.ORCA_EINVAL      # out of order
     for s in sims:
         s.close()
 
@@ -216,17 +257,22 @@ def test_halo_slab_layout_and_refusals():
                 assert np.array_equal(got.goals[4:, 0], out["goal_x"]) and np.array_equal(got.radii[4:], out["radius"])
 
 
-def test_two_processes_one_gpu_over_gloo(tmp_path):
-    """The real device ops under the real multi-process protocol: two ranks share cuda:0, the
-    slabs are staged through host memory and travel over gloo (NCCL refuses two ranks on one
-    device). Equal to the single-handle run, keyed by id."""
+@pytest.mark.parametrize("world,transport", [(2, "sendrecv"), (2, "window"), (3, "window")])
+def test_processes_sharing_one_gpu(tmp_path, world, transport):
+    """The real device ops under the real multi-process protocol: the ranks are processes that
+    share cuda:0. "sendrecv": the slabs are staged through host memory and travel over gloo (NCCL
+    refuses two ranks on one device). "window": every process maps its neighbours' windows through
+    CUDA IPC handles, its kernels write the slabs there and raise the flags the neighbours'
+    streams wait on (gloo carries the 64-byte handles at set-up, nothing per frame). Equal to
+    the single-handle run, keyed by id."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    world, steps = 2, 6
-    mp.spawn(S.gpu_gloo_worker, args=(world, port, steps, str(tmp_path), "mixed"), nprocs=world, join=True)
+    steps = 6
+    mp.spawn(S.gpu_gloo_worker, args=(world, port, steps, str(tmp_path), "mixed", transport), nprocs=world,
+             join=True)
     st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
     with Simulation(cfg, capacity=st.ids.shape[0], precision="mixed", remove_arrivals=False) as ref:
         ref.load(st)
