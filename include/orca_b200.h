@@ -40,13 +40,14 @@
  *                   contraction for desired velocity, ORCA half-planes, LP and
  *                   integration. For float32-representable inputs the solver
  *                   takes exactly the reference's branches and the results are
- *                   the reference's, rounded once to FP32 on store. Default.
+ *                   the reference's, rounded once to FP32 on store.
  *       ORCA_F32    FP32 state and FP32 arithmetic: fastest; velocities agree
  *                   with the reference to ~1e-7 m/s typically, but ill-conditioned
  *                   LPs (dense crowds in the fallback stage) can differ by more
  *                   than 1e-4 m/s -- counted and reported by the parity tests.
  *       ORCA_F64    FP64 state and arithmetic: bit-identical to the reference on
- *                   any float64 input.
+ *                   any float64 input. What the reference-shaped host entry points
+ *                   (engine.step / run, the CLI) use unless told otherwise.
  *       ORCA_CERT32 the results of ORCA_MIXED, faster: the half-planes and the LP run in
  *                   FP32 only to find which (at most two) half-planes decide the result;
  *                   the result itself is evaluated in FP64 on those, and accepted only
@@ -337,6 +338,14 @@ ORCA_API int orca_least_penetration(int device, int precision, int64_t k, const 
  * int64[n, max_count] (row indices, -1 padded), out_count int64[n]. */
 ORCA_API int orca_neighbor_query(int device, int64_t n, const int64_t *ids, const double *positions,
                                  double radius, int32_t max_count, int64_t *out_rows, int64_t *out_count);
+
+/* grid.query_neighbors with max_count beyond ORCA_MAX_NEIGHBORS ("everyone within the radius",
+ * G:50-83 called with a huge max_count): every agent's complete list, ordered by (d2, id), as
+ * CSR -- out_offsets[n + 1], out_rows[cap]. *total_out = the number of entries; ORCA_ECAPACITY
+ * (offsets and total valid) when they do not fit cap. An object-level operator, not the step. */
+ORCA_API int orca_neighbor_query_all(int device, int64_t n, const int64_t *ids, const double *positions,
+                                     double radius, int64_t cap, int64_t *out_offsets, int64_t *out_rows,
+                                     int64_t *total_out);
 
 /* Fisher-Yates order (_kernels.py:43-54) computed on the device: perm[k]. */
 ORCA_API int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *perm);

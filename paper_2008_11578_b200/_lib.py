@@ -36,7 +36,7 @@ SYMBOLS = [
     "orca_debug_last_step", "orca_lp_solve_batch", "orca_lp_release_scratch", "orca_lp_batch_create",
     "orca_lp_batch_set_stream", "orca_lp_batch_solve", "orca_lp_batch_download",
     "orca_lp_batch_destroy", "orca_vo_exit_batch", "orca_shuffle_order", "orca_problem_seed",
-    "orca_least_penetration", "orca_neighbor_query",
+    "orca_least_penetration", "orca_neighbor_query", "orca_neighbor_query_all",
     "orca_strip_pack", "orca_strip_append", "orca_strip_drop_ghosts",
     "orca_strip_halo_record_bytes", "orca_strip_configure", "orca_strip_pack_halo",
     "orca_strip_append_slab", "orca_strip_step", "orca_strip_stats",
@@ -140,6 +140,7 @@ def load():
     L.orca_vo_exit_batch.argtypes = [ci, ci, i64, vp, vp]
     L.orca_least_penetration.argtypes = [ci, ci, i64, vp, vp, f64, i64, f64, f64, vp]
     L.orca_neighbor_query.argtypes = [ci, i64, vp, vp, f64, C.c_int32, vp, vp]
+    L.orca_neighbor_query_all.argtypes = [ci, i64, vp, vp, f64, i64, vp, vp, P(i64)]
     L.orca_shuffle_order.argtypes = [ci, i64, u64, vp]
     L.orca_problem_seed.argtypes = [ci, i64, i64, P(u64)]
     L.orca_strip_pack.argtypes = [vp, f64, f64, ci, vp, i64, P(i64)]

@@ -2582,6 +2582,87 @@ extern "C" int orca_neighbor_query(int device, int64_t n, const int64_t *ids, co
     return rc;
 }
 
+extern "C" int orca_neighbor_query_all(int device, int64_t n, const int64_t *ids, const double *positions,
+                                       double radius, int64_t cap, int64_t *out_offsets, int64_t *out_rows,
+                                       int64_t *total_out)
+{
+    if (n < 0 || cap < 0 || !total_out || (n > 0 && (!ids || !positions || !out_offsets)) || (cap > 0 && !out_rows))
+        return fail(nullptr, ORCA_EINVAL, "orca_neighbor_query_all: bad arguments");
+    if (!(radius > 0.0) || !std::isfinite(radius))
+        return fail(nullptr, ORCA_EINVAL, "radius must be positive, got %g", radius);
+    *total_out = 0;
+    if (out_offsets) out_offsets[0] = 0;
+    if (n == 0) return ORCA_OK;
+    orca_sim *sim = nullptr;
+    int rc = orca_create(&sim, device, n, ORCA_F64);
+    if (rc) return rc;
+    orca_params p{};
+    p.dt = 1.0;
+    p.tau = 1.0;
+    p.neighbor_radius = radius;
+    p.max_neighbors = 1; // (sizes the search grid only; the lists of this query have no cap)
+    rc = orca_set_params(sim, &p);
+    if (!rc) {
+        std::vector<double> zeros((size_t)2 * n, 0.0), ones((size_t)n, 1.0);
+        std::vector<int64_t> cls((size_t)n, 0);
+        rc = orca_upload(sim, n, 0, ids, positions, zeros.data(), ones.data(), ones.data(), ones.data(), positions,
+                         ones.data(), cls.data());
+        if (!rc) rc = orca_sync(sim);
+    }
+    double *d_keys = nullptr;
+    i64 *d_rows = nullptr;
+    std::vector<int> off;
+    if (!rc) {
+        const StepParams P = make_params(sim);
+        rc = bin_build<double, double>(sim, P);
+        cudaStream_t st = sim->stream;
+        const dim3 blocks = grid_for(n + 1, 128);
+        const double2 *xy = reinterpret_cast<const double2 *>(sim->s_xy);
+        const i64 *d_ids = sim->ids[sim->acur];
+        if (!rc) {
+            k_neighbors_all<0><<<blocks, 128, 0, st>>>(sim->plan, P.rad2, xy, sim->cell_start, sim->s_cell, sim->s_row,
+                                                       d_ids, sim->sel, nullptr, nullptr, nullptr);
+            const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
+            k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->sel, sim->block_sums);
+            k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
+            k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->sel, sim->block_sums, sim->sel_idx);
+            off.resize((size_t)n + 1);
+            cudaError_t e = cudaGetLastError();
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(off.data(), sim->sel_idx, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) rc = fail(sim, ORCA_ECUDA, "orca_neighbor_query_all: %s", cudaGetErrorString(e));
+        }
+        if (!rc) rc = fetch_plan(sim); // range error of a position (engine.py:152-153)
+        if (!rc) {
+            const int64_t total = off[(size_t)n];
+            *total_out = total;
+            for (int64_t i = 0; i <= n; ++i) out_offsets[i] = off[(size_t)i];
+            if (total > cap)
+                rc = fail(sim, ORCA_ECAPACITY, "orca_neighbor_query_all: %lld neighbour entries, the buffer holds %lld",
+                          (long long)total, (long long)cap);
+            else if (total > 0) {
+                cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&d_keys), sizeof(double) * total);
+                if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&d_rows), sizeof(i64) * total);
+                if (e == cudaSuccess) {
+                    k_neighbors_all<1><<<blocks, 128, 0, st>>>(sim->plan, P.rad2, xy, sim->cell_start, sim->s_cell,
+                                                               sim->s_row, d_ids, nullptr, sim->sel_idx, d_keys, d_rows);
+                    e = cudaGetLastError();
+                }
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(out_rows, d_rows, sizeof(i64) * total, cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) rc = fail(sim, ORCA_ECUDA, "orca_neighbor_query_all: %s", cudaGetErrorString(e));
+            }
+        }
+    }
+    cudaFree(d_keys);
+    cudaFree(d_rows);
+    if (rc) memcpy(g_err, sim->err, sizeof(g_err));
+    orca_destroy(sim);
+    return rc;
+}
+
 extern "C" int orca_shuffle_order(int device, int64_t k, uint64_t seed, int64_t *perm)
 {
     if (k < 0 || (k > 0 && !perm)) return fail(nullptr, ORCA_EINVAL, "orca_shuffle_order: bad arguments");

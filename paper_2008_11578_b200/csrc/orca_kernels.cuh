@@ -698,6 +698,59 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
     gq[atomicAdd(gq_cnt, 1)] = s;
 }
 
+// grid.query_neighbors without a cap on the count (orca_neighbor_query_all): EVERY agent within the
+// radius, ordered by (d2, id) (G:60-83). Thread per sorted slot over the search grid of the bin
+// build; pass 0 counts (cnt[row]), pass 1 -- after a scan of the counts -- writes the rows at
+// off[row] and orders its own segment by insertion (the segments of an object-level query are
+// short; the step itself never comes here). Same FP64 operations as the reference: d2 = dx*dx +
+// dy*dy, kept unless d2 > radius*radius.
+template <int PASS>
+__global__ void __launch_bounds__(128)
+k_neighbors_all(const GridPlan *__restrict__ plan, double rad2, const double2 *__restrict__ s_xy,
+                const int *__restrict__ cell_start, const int *__restrict__ s_cell, const int *__restrict__ s_row,
+                const i64 *__restrict__ ids, int *__restrict__ cnt, const int *__restrict__ off,
+                double *__restrict__ keys, i64 *__restrict__ rows)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = plan->n;
+    if (PASS == 0 && s == n) cnt[n] = 0; // (the scan runs over n + 1 entries: off[n] = total)
+    if (s >= n) return;
+    const int nx = plan->nx, ny = plan->ny, r = plan->rmax;
+    const double2 me = s_xy[s];
+    const int row = s_row[s];
+    const int c0 = s_cell[s];
+    const int cx = c0 / ny, cy = c0 - cx * ny;
+    const int y_lo = max(cy - r, 0), y_hi = min(cy + r, ny - 1);
+    const int base = PASS ? off[row] : 0;
+    int m = 0;
+    for (int gx = max(cx - r, 0); gx <= min(cx + r, nx - 1); ++gx) {
+        const int a = cell_start[gx * ny + y_lo], e = cell_start[gx * ny + y_hi + 1];
+        for (int s2 = a; s2 < e; ++s2) {
+            if (s2 == s) continue;
+            const double2 q = s_xy[s2];
+            const double dx = q.x - me.x, dy = q.y - me.y;
+            const double d2 = dx * dx + dy * dy;
+            if (d2 > rad2) continue;
+            if (PASS) {
+                const i64 row2 = (i64)s_row[s2];
+                const i64 id2 = ids[row2];
+                int at = m; // insertion into the ordered prefix [base, base + m)
+                while (at > 0) {
+                    const double kp = keys[base + at - 1];
+                    if (kp < d2 || (kp == d2 && ids[rows[base + at - 1]] < id2)) break;
+                    keys[base + at] = kp;
+                    rows[base + at] = rows[base + at - 1];
+                    --at;
+                }
+                keys[base + at] = d2;
+                rows[base + at] = row2;
+            }
+            ++m;
+        }
+    }
+    if (!PASS) cnt[row] = m;
+}
+
 // Exact ring search for the agents the fast pass queued (all of them on the first step
 // after an upload). The search grid is walked in growing square rings around the
 // agent's cell; it stops as soon as the list is full and every unscanned cell is

@@ -8,8 +8,11 @@ radius; the result -- the up to max_count nearest agents within `radius`, ascend
 (distance, id) -- is defined geometrically and does not depend on the cell size
 (pkg/tests/test_grid.py:101). Here the query runs the step's own neighbour search
 (k_gather_fast32 + k_gather through orca_neighbor_query) for EVERY agent at once and caches
-the lists on the grid object, so a loop over self_id costs one device call. `cells` / `cell_of`
-are provided for inspection with the reference's meaning.
+the lists on the grid object, so a loop over self_id costs one device call. A max_count above
+the step's limit of 32 -- the reference's tests ask for "everyone within the radius" with
+10**9 -- takes the uncapped query (orca_neighbor_query_all: complete lists in CSR form, then
+the first max_count of each). `cells` / `cell_of` are provided for inspection with the
+reference's meaning.
 """
 
 from __future__ import annotations
@@ -19,9 +22,11 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import ORCA_MAX_NEIGHBORS, check, load, ptr
+import ctypes as C
 
-__all__ = ["UniformGrid", "rebuild", "query_neighbors", "neighbor_lists"]
+from ._lib import ORCA_ECAPACITY, ORCA_MAX_NEIGHBORS, check, load, ptr
+
+__all__ = ["UniformGrid", "rebuild", "query_neighbors", "neighbor_lists", "neighbor_lists_all"]
 
 ORIGIN = (0.0, 0.0)
 
@@ -37,6 +42,26 @@ def neighbor_lists(ids, positions, radius: float, max_count: int, device: int = 
     check(load().orca_neighbor_query(device, n, ptr(ids), ptr(pos), float(radius), int(max_count),
                                      ptr(rows), ptr(count)))
     return rows[:, :int(max_count)], count
+
+
+def neighbor_lists_all(ids, positions, radius: float, device: int = 0):
+    """(offsets int64[n + 1], rows int64[total]): EVERY agent within `radius` of each agent,
+    ascending by (distance, id) -- grid.py:50-83 without a cap on the count."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 2)
+    n = ids.shape[0]
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    total = C.c_int64(0)
+    cap = max(64 * n, 1)
+    while True:
+        rows = np.empty(cap, dtype=np.int64)
+        rc = load().orca_neighbor_query_all(device, n, ptr(ids), ptr(pos), float(radius), cap, ptr(offsets),
+                                            ptr(rows), C.byref(total))
+        if rc == ORCA_ECAPACITY and total.value > cap:
+            cap = int(total.value)          # the call reports what it needs: once more with room
+            continue
+        check(rc)
+        return offsets, rows[:int(total.value)]
 
 
 @dataclass
@@ -87,14 +112,18 @@ def query_neighbors(grid: UniformGrid, agents, self_id, radius: float, max_count
         raise KeyError(f"unknown agent id {self_id!r}")
     if max_count == 0:
         return []
-    if max_count > ORCA_MAX_NEIGHBORS:
-        raise ValueError(f"max_count {max_count} exceeds the device limit of {ORCA_MAX_NEIGHBORS} neighbours")
     pos = np.array([a.position for a in agents], dtype=np.float64).reshape(-1, 2)
-    key = (radius, int(max_count), device, pos.tobytes(), tuple(row_of))
+    capped = max_count <= ORCA_MAX_NEIGHBORS
+    key = (radius, int(max_count) if capped else "all", device, pos.tobytes(), tuple(row_of))
     cached = grid._lists.get("key") == key
     if not cached:
         ids = np.array([a.id for a in agents], dtype=np.int64)
-        grid._lists = {"key": key, "lists": neighbor_lists(ids, pos, radius, max_count, device)}
-    rows, count = grid._lists["lists"]
+        lists = (neighbor_lists(ids, pos, radius, max_count, device) if capped
+                 else neighbor_lists_all(ids, pos, radius, device))
+        grid._lists = {"key": key, "lists": lists}
     i = row_of[self_id]
-    return [agents[j] for j in rows[i, :count[i]].tolist()]
+    if capped:
+        rows, count = grid._lists["lists"]
+        return [agents[j] for j in rows[i, :count[i]].tolist()]
+    offsets, rows = grid._lists["lists"]
+    return [agents[j] for j in rows[offsets[i]:offsets[i + 1]][:max_count].tolist()]

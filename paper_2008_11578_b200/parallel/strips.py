@@ -19,12 +19,15 @@ adjacent strip:
   3. halo     the owned agents within neighbor_radius of a strip edge, at their NEW positions, are
               packed into that side's HALO SLAB (32-byte records: position, velocity, radius,
               class, id)
-  4. exchange emigrant + halo slab of each side travel together, one grouped send/recv
+  4. exchange emigrant + halo slab of each side travel together: with transport "window" this
+              strip's kernel copies the used part of them into the neighbour's memory (peer
+              mapping, CUDA IPC) and raises a flag the neighbour's stream waits on; with
+              "sendrecv" the whole buffers go through one grouped send/recv
 
 The host is not in this loop. A slab is a fixed-capacity device buffer whose 32-byte header
-carries the record count; the packing kernels count with atomics, the whole slab travels (a
-size both ranks know without asking), the appending kernels read the count from the header.
-The exchange is ordered against the handle's stream on the device (NCCL) and involves the two
+carries the record count; the packing kernels count with atomics, the receiving side needs no
+size from the host, the appending kernels read the count from the header.
+The exchange is ordered against the handle's stream on the device and involves the two
 adjacent strips only -- no collective on the data path. The host keeps a launch bound that
 stays FIXED between two synchronisations (row count last seen + slack), so the frames in
 between replay one captured CUDA graph, and re-synchronises every `resync_every` frames

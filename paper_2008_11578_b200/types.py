@@ -198,6 +198,16 @@ class SimState:
     def active_count(self) -> int:
         return int(self.ids.shape[0])
 
+    @property
+    def agents(self) -> list:
+        """One orca.AgentState per row, in storage order (engine.py:80-87)."""
+        from .orca import AgentState
+        return [AgentState(id=int(self.ids[i]), position=self.positions[i].copy(),
+                           velocity=self.velocities[i].copy(), radius=float(self.radii[i]),
+                           pref_speed=float(self.pref_speeds[i]), max_speed=float(self.max_speeds[i]),
+                           goal=self.goals[i].copy(), agent_class=AgentClass(int(self.class_codes[i])))
+                for i in range(self.active_count)]
+
 
 @dataclass(eq=False)
 class FrameLog:

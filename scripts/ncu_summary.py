@@ -8,6 +8,7 @@ import collections
 import csv
 import io
 import re
+import os
 import subprocess
 import sys
 
@@ -64,7 +65,11 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    pre = path[:-len(".ncu-rep")] + ".raw.csv" if path.endswith(".ncu-rep") else path
+    if os.path.exists(pre):       # `ncu -i X.ncu-rep --page raw --csv > X.raw.csv` done on the GPU box (reports are big)
+        out = open(pre).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")

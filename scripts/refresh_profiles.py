@@ -67,7 +67,11 @@ with open(os.path.join(P, f"{tag}_full_lp_infeasible.md"), "w") as f:
 
 # traffic.json: DRAM bytes per launch and issue / pipe utilisation of the 1 M mixed capture
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    pre = rep[:-len(".ncu-rep")] + ".raw.csv" if rep.endswith(".ncu-rep") else rep
+    if os.path.exists(pre):       # `ncu -i X.ncu-rep --page raw --csv > X.raw.csv` done on the GPU box (reports are big)
+        out = open(pre).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 

@@ -62,10 +62,12 @@ del os.environ["ORCA_CHUNKS"]
 import strip_ops_cpu as S
 from test_gpu_strips import build_strips, lockstep
 st, cfg = S.make_crowd(seed=4, n_ped=4000, n_veh=200, density=0.5)
-for prec, world in (("mixed", 2), ("f64", 3)):
-    sims, drivers, _b = build_strips(st, cfg, prec, world, halo_cap=st.ids.shape[0], mig_cap=2000, resync_every=3)
+for prec, world, transport in (("mixed", 2, "sendrecv"), ("f64", 3, "sendrecv"), ("mixed", 3, "window"),
+                               ("f64", 2, "window")):
+    sims, drivers, _b = build_strips(st, cfg, prec, world, halo_cap=st.ids.shape[0], mig_cap=2000, resync_every=3,
+                                     transport=transport)
     lockstep(drivers, 7)
-    print("strips", prec, world, [s.state().ids.shape[0] for s in sims], [d.ops.stats() for d in drivers])
+    print("strips", prec, world, transport, [s.state().ids.shape[0] for s in sims], [d.ops.stats() for d in drivers])
     for s_ in sims:
         s_.close()
 from paper_2008_11578_b200 import HalfPlaneConstraint, solve_least_penetration

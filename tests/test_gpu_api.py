@@ -100,3 +100,51 @@ def test_solve_least_penetration_equals_the_reference():
         solve_least_penetration([], 1.0, start_index=1)
     with pytest.raises(ValueError, match="warm_start is non-finite"):
         solve_least_penetration([], 1.0, warm_start=(np.nan, 0.0))
+
+
+def test_query_neighbors_without_a_cap_matches_brute_force():
+    """max_count beyond the step's 32 (the reference's tests ask for 300 and 10**9): complete
+    lists from orca_neighbor_query_all, ordered by (d2, id) with exact ties, against a brute-force
+    scan in the reference's arithmetic (grid.py:60-83)."""
+    from paper_2008_11578_b200.grid import neighbor_lists_all
+    rng = np.random.default_rng(5)
+    n = 700
+    pos = np.round(rng.uniform(-20.0, 20.0, size=(n, 2)) * 4.0) / 4.0     # a 0.25 m lattice: many equal distances
+    _u, first = np.unique(pos, axis=0, return_index=True)
+    pos = pos[np.sort(first)]
+    n = pos.shape[0]
+    ids = rng.permutation(10 * n)[:n].astype(np.int64)
+    for radius in (0.9, 3.0, 7.5):
+        off, rows = neighbor_lists_all(ids, pos, radius)
+        assert off.shape == (n + 1,) and off[0] == 0 and off[-1] == rows.shape[0]
+        for i in range(0, n, 7):
+            d = pos - pos[i]
+            d2 = d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]
+            cand = [j for j in range(n) if j != i and not d2[j] > radius * radius]
+            cand.sort(key=lambda j: (d2[j], ids[j]))
+            assert rows[off[i]:off[i + 1]].tolist() == cand, (radius, i)
+    agents = [AgentState(int(ids[i]), pos[i], (0.0, 0.0), 0.25, 1.4, 2.0, (0.0, 0.0)) for i in range(n)]
+    g = rebuild(agents, 3.0)
+    full = query_neighbors(g, agents, int(ids[3]), 7.5, 10**9)
+    assert len(full) > 32
+    assert [a.id for a in query_neighbors(g, agents, int(ids[3]), 7.5, 40)] == [a.id for a in full[:40]]
+    assert [a.id for a in query_neighbors(g, agents, int(ids[3]), 7.5, 16)] == [a.id for a in full[:16]]
+    # an empty crowd and a crowd nobody is near anybody in
+    off, rows = neighbor_lists_all(np.zeros(0, np.int64), np.zeros((0, 2)), 1.0)
+    assert off.tolist() == [0] and rows.shape == (0,)
+    off, rows = neighbor_lists_all(np.arange(3), np.array([[0.0, 0.0], [50.0, 0.0], [0.0, 50.0]]), 1.0)
+    assert off.tolist() == [0, 0, 0, 0] and rows.shape == (0,)
+
+
+def test_simstate_agents_are_the_rows_as_agent_states():
+    from paper_2008_11578_b200 import crossing_config, init_state
+    cfg = crossing_config("two_way", 6, 0.5, seed=3)
+    st = init_state(cfg)
+    agents = st.agents
+    assert len(agents) == st.active_count
+    for i, a in enumerate(agents):
+        assert a.id == int(st.ids[i]) and np.array_equal(a.position, st.positions[i])
+        assert np.array_equal(a.goal, st.goals[i]) and a.radius == float(st.radii[i])
+        assert int(a.agent_class) == int(st.class_codes[i])
+    agents[0].position[0] += 1.0                     # copies, not views
+    assert agents[0].position[0] != st.positions[0, 0]
