@@ -244,8 +244,8 @@ template <typename S, typename R, int MAXN> static cudaError_t set_smem_attrs()
     e = cudaFuncSetAttribute(k_solve_group<S, R, MAXN, 128, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::solve_bpt * 64);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_solve_group_queue<S, R, MAXN, 128, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::solve_bpt * 64);
+    e = cudaFuncSetAttribute(k_solve_group_queue<S, R, MAXN, 128, ORCA_QUEUE_GL, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::solve_bpt * (128 / ORCA_QUEUE_GL));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_fallback_coop<S, R, MAXN, C::fb_threads, ORCA_GL_SHORT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -953,8 +953,10 @@ static int solve_chunk(orca_sim *sim, const StepParams &P, int out_idx, cudaStre
                 sim->status[a], sim->failed[a], sim->arrived, sim->cq + s0, s_perm, &sim->plan->cq_count[c], s0, s1);
             // (4x the resident blocks: a typical queue -- the ~6 % of a sparse crowd -- is ONE chunk per
             //  block, spread over every SM at once; blocks beyond the queue exit at their first test)
-            const int qblocks = (int)std::min<int64_t>(148 * ORCA_SG_BLOCKS * 4, std::max<int64_t>(1, (m + 63) / 64));
-            k_solve_group_queue<S, R, MAXN, 128, 2, true><<<qblocks, 128, C::solve_bpt * 64, st>>>(
+            constexpr int QNG = 128 / ORCA_QUEUE_GL; // agents per block of the queue pass
+            const int qblocks = (int)std::min<int64_t>(148 * ORCA_SG_BLOCKS * 4 * (ORCA_QUEUE_GL / 2),
+                                                       std::max<int64_t>(1, (m + QNG - 1) / QNG));
+            k_solve_group_queue<S, R, MAXN, 128, ORCA_QUEUE_GL, true><<<qblocks, 128, C::solve_bpt * QNG, st>>>(
                 ORCA_SOLVE_ARGS, s_perm, fq_cnt, sim->cq + s0, &sim->plan->cq_count[c]);
             sim->launches += 1;
         }

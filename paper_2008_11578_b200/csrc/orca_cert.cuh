@@ -48,6 +48,9 @@ namespace orca {
 #define ORCA_CERT_MAX_FALLBACK_PCT 25     // above: most agents need the FP64 kernels anyway (measured break-even ~30 %)
 #endif
 #define CERT_CROSS_MIN 0.02f    // |n_L x n_B| below this: the vertex is ill-conditioned, leave it to FP64
+#ifndef CERT_TASK_BUCKETS
+#define CERT_TASK_BUCKETS 6     // LP tasks of a block are ordered by min(clearly violated half-planes, this)
+#endif
 
 // vo_exit<float> (orca_math.cuh) plus a first-order bound on how far the FP32 half-plane can be
 // from the FP64 one: err_n on the unit normal (radians), err_u on the exit vector. CERT_INF when
@@ -64,48 +67,49 @@ __device__ __forceinline__ bool vo_exit_cond(float rpx, float rpy, float rvx, fl
     const float r2 = comb_r * comb_r;
     const bool overlap = d2 < r2; // K:357
     const float inv = overlap ? inv_dt : inv_tau;
-    const float cx = rpx * inv, cy = rpy * inv;
     const float rr = comb_r * inv;
-    const float wx = rvx - cx, wy = rvy - cy;
+    const float wx = __fmaf_rn(-rpx, inv, rvx), wy = __fmaf_rn(-rpy, inv, rvy); // w = rv - rp / tau
     const float wl2 = __fmaf_rn(wx, wx, wy * wy);
     const float dot_wp = __fmaf_rn(wx, rpx, wy * rpy);
     const bool arc = overlap || (dot_wp < 0.0f && dot_wp * dot_wp > r2 * wl2); // K:395
-    const float arg = arc ? wl2 : d2 - r2;
+    const float dmr = d2 - r2, dpr = d2 + r2;
+    const float arg = arc ? wl2 : dmr;
     const float rsq = rsqrtf(arg);          // 1 / |w|  or  1 / leg
     const float sq = arg * rsq;
-    const float crs = __fmaf_rn(rpx, wy, -(rpy * wx));
+    const float p1 = rpx * wy, p2 = rpy * wx;
+    const float crs = p1 - p2;
     const bool side = crs > 0.0f; // K:404
-    const float a1 = rpx * sq, a2 = rpy * comb_r, b1 = rpx * comb_r, b2 = rpy * sq;
-    const float lx = side ? a1 - a2 : -(a1 + a2);
-    const float ly = side ? b1 + b2 : b1 - b2;
+    // leg direction (K:405-412): (rpx sq -+ rpy R, +-rpy sq + rpx R) with the sign of the side
+    const float ssq = side ? sq : -sq;
+    const float lx = __fmaf_rn(rpx, ssq, -(rpy * comb_r));
+    const float ly = __fmaf_rn(rpy, ssq, rpx * comb_r);
     const float rd2 = __fdividef(1.0f, d2);
     const float iden = arc ? rsq : rd2;
     const float qx = (arc ? wx : lx) * iden;
     const float qy = (arc ? wy : ly) * iden;
     const float s = rr - sq;
     const float t = __fmaf_rn(rvx, qx, rvy * qy);
-    float mx = -qy, my = qx;
-    if (__fmaf_rn(mx, rpx, my * rpy) > 0.0f) {
-        mx = -mx;
-        my = -my;
-    }
-    ux = arc ? s * qx : __fmaf_rn(t, qx, -rvx);
-    uy = arc ? s * qy : __fmaf_rn(t, qy, -rvy);
+    const bool flip = __fmaf_rn(qx, rpy, -(qy * rpx)) > 0.0f; // (m = (-qy, qx); m . rp > 0)
+    const float mx = flip ? qy : -qy, my = flip ? -qx : qx;
+    // u = s q (arc) or t q - rv (leg), as ONE fused form so that no branch splits the loop body
+    const float ut = arc ? s : t, ucx = arc ? 0.0f : -rvx, ucy = arc ? 0.0f : -rvy;
+    ux = __fmaf_rn(ut, qx, ucx);
+    uy = __fmaf_rn(ut, qy, ucy);
     nx = arc ? qx : mx;
     ny = arc ? qy : my;
     // --- conditioning (first order; CERT_SAFETY covers the approximations above) ---
-    const float sw = fabsf(rvx) + fabsf(rvy) + fabsf(cx) + fabsf(cy); // scale of the operands of w
     const float srv = fabsf(rvx) + fabsf(rvy);
+    const float sw = __fmaf_rn(fabsf(rpx) + fabsf(rpy), inv, srv); // scale of the operands of w
     // arc: q = w / |w|, u = (rr - |w|) q.   leg = sqrt(d2 - r2): cancellation when the discs almost touch,
     // kappa = (d2 + r2) / (d2 - r2) = (d2 + r2) * rsq^2, and the direction error is kappa * leg / |rp|
-    const float en_arc = 4.0f * CERT_EPS * (sw * rsq + 1.0f);
-    const float eu_arc = 4.0f * CERT_EPS * (sw + fabsf(rr)) + fabsf(s) * en_arc;
-    const float en_leg = 2.0f * CERT_EPS * ((d2 + r2) * rsq * rsqrtf(d2) + 3.0f);
-    const float eu_leg = srv * (2.0f * en_leg + 4.0f * CERT_EPS);
+    const float en_arc = (4.0f * CERT_EPS) * __fmaf_rn(sw, rsq, 1.0f);
+    const float eu_arc = __fmaf_rn(fabsf(s), en_arc, (4.0f * CERT_EPS) * (sw + fabsf(rr)));
+    const float en_leg = (2.0f * CERT_EPS) * __fmaf_rn(dpr * rsq, rsqrtf(d2), 3.0f);
+    const float eu_leg = srv * __fmaf_rn(2.0f, en_leg, 4.0f * CERT_EPS);
     const float en = arc ? en_arc : en_leg, eu = arc ? eu_arc : eu_leg;
-    bool sure = fabsf(d2 - r2) > 64.0f * CERT_EPS * (d2 + r2);                        // overlap decision
-    sure = sure && wl2 > 1e-9f * (sw * sw) && wl2 > 1e-20f;                            // |w|^2 < 1e-24 branch, q = w/|w|
-    sure = sure && (overlap || fabsf(crs) > 64.0f * CERT_EPS * (fabsf(rpx * wy) + fabsf(rpy * wx))); // leg side
+    bool sure = fabsf(dmr) > (64.0f * CERT_EPS) * dpr;                                  // overlap decision
+    sure = sure && wl2 > 1e-9f * (sw * sw) && wl2 > 1e-20f;                             // |w|^2 < 1e-24 branch, q = w/|w|
+    sure = sure && (overlap || fabsf(crs) > (64.0f * CERT_EPS) * (fabsf(p1) + fabsf(p2))); // leg side
     sure = sure && d2 > 0.0f;
     err_n = sure ? CERT_SAFETY * en : CERT_INF;
     err_u = sure ? CERT_SAFETY * eu : CERT_INF;
@@ -189,10 +193,20 @@ __device__ __forceinline__ bool lp2_target_runahead_act(const V &view, int k, fl
     while (true) {
         bool found = false;
         if (!done) {
-            for (; i_pos < k; ++i_pos) {
-                float px, py, nx, ny;
-                view.get(i_pos, px, py, nx, ny);
-                if (__fmaf_rn(vx - px, nx, (vy - py) * ny) < 0.0f) {
+            // next violated constraint at or after i_pos, four positions per trip: the four shared-memory
+            // loads are in flight together (one at a time, this scan is a chain of exposed load latencies
+            // -- it was 15 % of the kernel's stall samples)
+            for (; i_pos < k; i_pos += 4) {
+                unsigned m = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    float px, py, nx, ny;
+                    view.get(min(i_pos + u, k - 1), px, py, nx, ny);
+                    const bool viol = __fmaf_rn(vx - px, nx, (vy - py) * ny) < 0.0f;
+                    m |= (viol && i_pos + u < k) ? (1u << u) : 0u;
+                }
+                if (m) {
+                    i_pos += __ffs(m) - 1;
                     found = true;
                     break;
                 }
@@ -268,11 +282,12 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
     float *sm_err = reinterpret_cast<float *>(sm_cons + MAXN * THREADS);
     u8 *sm_perm = reinterpret_cast<u8 *>(sm_err + MAXN * THREADS);
     __shared__ int sm_task[THREADS];
-    __shared__ int sm_ntask;
-    if (threadIdx.x == 0) sm_ntask = 0;
+    __shared__ int sm_bcnt[CERT_TASK_BUCKETS];
+    if (threadIdx.x < CERT_TASK_BUCKETS) sm_bcnt[threadIdx.x] = 0;
     __syncthreads();
 
     const int s_base = s0 + blockIdx.x * THREADS;
+    int my_bucket = -1, my_rank = 0; // an LP task: its bucket (by clearly violated half-planes) and rank in it
     {   // ---- phase A ----
         const int s = s_base + threadIdx.x; // this launch covers sorted slots [s0, s1)
         const bool in_range = s < min(s1, plan->n);
@@ -306,28 +321,40 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                     v0y *= sc;
                 }
             }
-            bool built = true, violated = false, unclear = false;
+            bool built = true, unclear = false;
+            int nviol = 0;
             {   // FP32 half-planes in shuffled order, each with its error bound against |v| <= cap
-                const float ri = (float)((double)me_rec.rc.x + P.half_margin);
+                const float hm = (float)P.half_margin;
+                const float ri = me_rec.rc.x + hm;
+                const float mz = fabsf(me.z) + fabsf(me.w);
                 const int ci = (int)me_rec.rc.y;
                 const float f0 = (float)(ci ? P.fmat[2] : P.fmat[0]), f1 = (float)(ci ? P.fmat[3] : P.fmat[1]);
                 const float inv_tau = __fdividef(1.0f, (float)P.tau), inv_dt = __fdividef(1.0f, (float)P.dt);
+                // software pipeline, two deep: a neighbour's record hangs on TWO dependent loads (its
+                // index nb[perm[pos]][s], then s_nr[index]), each a trip to L2 -- the index is requested two
+                // rounds ahead and the record one round ahead, so neither is waited for
                 float4 q_next = me;
                 float2 rc_next = me_rec.rc;
+                int j_next = 0;
+                const int *nbs = nb + s;
                 if (cnt > 0) {
-                    const NbRec<float> rn = s_nr[nb[(size_t)perm[0] * P.stride + s]];
+                    const NbRec<float> rn = s_nr[nbs[(size_t)perm[0] * P.stride]];
                     q_next = rn.pv;
                     rc_next = rn.rc;
+                    j_next = nbs[(size_t)perm[min(1, cnt - 1) * THREADS] * P.stride];
                 }
+#pragma unroll 2
                 for (int pos = 0; pos < cnt; ++pos) {
                     const float4 q = q_next;
                     const float2 rc_j = rc_next;
-                    if (pos + 1 < cnt) {
-                        const NbRec<float> rn = s_nr[nb[(size_t)perm[(pos + 1) * THREADS] * P.stride + s]];
+                    {   // (no branches: the last rounds re-read the last neighbour, and the loop body stays one
+                        //  basic block the scheduler can interleave with the next round's)
+                        const NbRec<float> rn = s_nr[j_next];
                         q_next = rn.pv;
                         rc_next = rn.rc;
+                        j_next = nbs[(size_t)perm[min(pos + 2, cnt - 1) * THREADS] * P.stride];
                     }
-                    const float rj = (float)((double)rc_j.x + P.half_margin);
+                    const float rj = rc_j.x + hm;
                     float ux, uy, nx, ny, eu, en;
                     built &= vo_exit_cond(q.x - me.x, q.y - me.y, me.z - q.z, me.w - q.w, ri + rj, inv_tau, inv_dt,
                                           ux, uy, nx, ny, eu, en);
@@ -336,13 +363,14 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                     cons.set(pos, px, py, nx, ny);
                     // |(v - p).n evaluated in FP32 - the same in exact arithmetic on the FP64 half-plane|, any |v| <= cap
                     const float reach = cap + fabsf(px) + fabsf(py);
-                    const float e = f * eu + en * reach + CERT_SAFETY * 4.0f * CERT_EPS * (reach + fabsf(me.z) + fabsf(me.w));
+                    const float e = __fmaf_rn(f, eu, __fmaf_rn(en, reach, (CERT_SAFETY * 4.0f * CERT_EPS) * (reach + mz)));
                     cerr[pos * THREADS] = e;
                     const float slack = __fmaf_rn(v0x - px, nx, (v0y - py) * ny);
-                    violated = violated || slack < -e;
+                    nviol += slack < -e ? 1 : 0;
                     unclear = unclear || !(fabsf(slack) > e); // (also catches an infinite error bound)
                 }
             }
+            const bool violated = nviol > 0;
             if (!built || (unclear && !violated)) {
                 // coincident centres (the FP64 kernel reports them) or a half-plane through the start
                 // within its error: nothing to guess, the FP64 kernels decide
@@ -362,13 +390,27 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                 failed_at[row] = -1;
                 integrate_row<float, double>(row, me, vx, vy, P, goalpref, pv_out, arrived);
             } else {
-                sm_task[atomicAdd(&sm_ntask, 1)] = threadIdx.x;
+                // the incremental LP re-solves on (roughly) every half-plane its start violates: tasks with
+                // the same count share a warp, so a warp's round count is close to what its lanes need
+                my_bucket = min(nviol, CERT_TASK_BUCKETS) - 1;
+                my_rank = atomicAdd(&sm_bcnt[my_bucket], 1);
             }
         }
     }
     __syncthreads();
+    int ntask = 0;
+    {
+        int before = 0;
+#pragma unroll
+        for (int b = 0; b < CERT_TASK_BUCKETS; ++b) {
+            const int c = sm_bcnt[b];
+            if (b < my_bucket) before += c;
+            ntask += c;
+        }
+        if (my_bucket >= 0) sm_task[before + my_rank] = threadIdx.x;
+    }
+    __syncthreads();
     // ---- phase B: thread t takes task t ----
-    const int ntask = sm_ntask;
     if ((int)(threadIdx.x & ~31u) >= ntask) return; // whole warp without a task
     const bool enabled = (int)threadIdx.x < ntask;
     const int a = enabled ? sm_task[threadIdx.x] : 0; // the agent's thread slot in shared memory

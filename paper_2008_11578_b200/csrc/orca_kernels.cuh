@@ -47,6 +47,11 @@
 #define ORCA_PRESHUFFLE_MIN_AGENTS 65536
 #endif
 #ifndef ORCA_CHUNKS_DEFAULT
+#ifndef ORCA_QUEUE_GL
+#define ORCA_QUEUE_GL 4 // lanes per agent in the FP64 pass over the agents ORCA_CERT32 could not certify: a few
+                        // percent of the crowd, i.e. one wave whose time is ONE agent's chain of sixteen FP64
+                        // half-planes -- four lanes build four each (2 lanes: solve stage 0.422 ms, 4: 0.394, 8: 0.403)
+#endif
 #define ORCA_CHUNKS_DEFAULT 2          // gather + solve + fallback pipelined over this many chunks of sorted slots ...
 #endif
 #ifndef ORCA_CHUNK_MIN_AGENTS
