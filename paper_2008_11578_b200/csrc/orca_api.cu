@@ -433,8 +433,8 @@ extern "C" int orca_create(orca_sim **out, int device, int64_t capacity, int pre
     CKC((set_smem_attrs<float, double, 32>()));
     CKC((set_smem_attrs<double, double, 16>()));
     CKC((set_smem_attrs<double, double, 32>()));
-    CKC(cudaFuncSetAttribute(k_solve_cert<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 16 * 128));
-    CKC(cudaFuncSetAttribute(k_solve_cert<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 128));
+    CKC(cudaFuncSetAttribute(k_solve_cert<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 18 * 16 * 128));
+    CKC(cudaFuncSetAttribute(k_solve_cert<32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 18 * 32 * 128));
 #undef CKC
     *out = sim;
     return ORCA_OK;
@@ -946,7 +946,7 @@ static int solve_chunk(orca_sim *sim, const StepParams &P, int out_idx, cudaStre
     if (cert) {
         // FP32 solve with a certificate for everyone, the FP64 kernel for the agents it queued
         if constexpr (Fmt<S>::is_f32 && !Fmt<R>::is_f32) {
-            k_solve_cert<MAXN, 128><<<grid_for(m, 128), 128, 21 * MAXN * 128, st>>>(
+            k_solve_cert<MAXN, 128><<<grid_for(m, 128), 128, 18 * MAXN * 128, st>>>(
                 sim->plan, P, reinterpret_cast<const NbRec<float> *>(sim->s_nr),
                 reinterpret_cast<const double4 *>(sim->s_dm), sim->s_row, sim->nb, sim->nb_cnt,
                 reinterpret_cast<const float4 *>(sim->goalpref[a]), reinterpret_cast<float4 *>(sim->pv[out_idx]),

@@ -32,6 +32,8 @@
 // BASELINE crowd against the oracle).
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "orca_kernels.cuh"
 
 namespace orca {
@@ -279,8 +281,9 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *sm_cons = reinterpret_cast<float4 *>(smem_raw);
-    float *sm_err = reinterpret_cast<float *>(sm_cons + MAXN * THREADS);
-    u8 *sm_perm = reinterpret_cast<u8 *>(sm_err + MAXN * THREADS);
+    // (error bounds as halves rounded UP, insertion order in registers: 18 bytes per half-plane, so that
+    //  SIX blocks of 128 agents fit an SM's shared memory -- with 21 bytes it was five)
+    __half *sm_err = reinterpret_cast<__half *>(sm_cons + MAXN * THREADS);
     __shared__ int sm_task[THREADS];
     __shared__ int sm_bcnt[CERT_TASK_BUCKETS];
     if (threadIdx.x < CERT_TASK_BUCKETS) sm_bcnt[threadIdx.x] = 0;
@@ -297,19 +300,21 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
             const NbRec<float> me_rec = s_nr[s];
             const float4 me = me_rec.pv;
             const double4 dm = s_dm[s]; // desired velocity (FP64, k_scatter), max_speed, avoid radius
-            u8 *perm = sm_perm + threadIdx.x;
-            float *cerr = sm_err + threadIdx.x;
+            __half *cerr = sm_err + threadIdx.x;
             SmemCons<float> cons{sm_cons + threadIdx.x, THREADS};
+            // the order k_shuffle drew, four positions per word, kept in registers
+            uint32_t pw[MAXN / 4];
             {
                 const uint32_t *src = s_perm + (size_t)s * (MAXN / 4);
-                for (int t = 0; 4 * t < cnt; ++t) {
-                    const uint32_t w = src[t];
-                    perm[(4 * t) * THREADS] = (u8)(w & 0xFFu);
-                    perm[(4 * t + 1) * THREADS] = (u8)((w >> 8) & 0xFFu);
-                    perm[(4 * t + 2) * THREADS] = (u8)((w >> 16) & 0xFFu);
-                    perm[(4 * t + 3) * THREADS] = (u8)(w >> 24);
-                }
+#pragma unroll
+                for (int t = 0; t < MAXN / 4; ++t) pw[t] = 4 * t < cnt ? src[t] : 0u;
             }
+            auto perm_at = [&](int pos) -> int { // (static register indices only: a select tree)
+                uint32_t w = pw[0];
+#pragma unroll
+                for (int t = 1; t < MAXN / 4; ++t) w = (pos >> 2) == t ? pw[t] : w;
+                return (int)((w >> ((pos & 3) * 8)) & 0xFFu);
+            };
             const float cap = (float)dm.z;
             // the start of the LP (K:129-136) in FP32: the half-planes are tested against it as they are built
             float v0x = (float)dm.x, v0y = (float)dm.y;
@@ -338,10 +343,10 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                 int j_next = 0;
                 const int *nbs = nb + s;
                 if (cnt > 0) {
-                    const NbRec<float> rn = s_nr[nbs[(size_t)perm[0] * P.stride]];
+                    const NbRec<float> rn = s_nr[nbs[(size_t)perm_at(0) * P.stride]];
                     q_next = rn.pv;
                     rc_next = rn.rc;
-                    j_next = nbs[(size_t)perm[min(1, cnt - 1) * THREADS] * P.stride];
+                    j_next = nbs[(size_t)perm_at(min(1, cnt - 1)) * P.stride];
                 }
 #pragma unroll 2
                 for (int pos = 0; pos < cnt; ++pos) {
@@ -352,7 +357,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                         const NbRec<float> rn = s_nr[j_next];
                         q_next = rn.pv;
                         rc_next = rn.rc;
-                        j_next = nbs[(size_t)perm[min(pos + 2, cnt - 1) * THREADS] * P.stride];
+                        j_next = nbs[(size_t)perm_at(min(pos + 2, cnt - 1)) * P.stride];
                     }
                     const float rj = rc_j.x + hm;
                     float ux, uy, nx, ny, eu, en;
@@ -364,7 +369,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                     // |(v - p).n evaluated in FP32 - the same in exact arithmetic on the FP64 half-plane|, any |v| <= cap
                     const float reach = cap + fabsf(px) + fabsf(py);
                     const float e = __fmaf_rn(f, eu, __fmaf_rn(en, reach, (CERT_SAFETY * 4.0f * CERT_EPS) * (reach + mz)));
-                    cerr[pos * THREADS] = e;
+                    cerr[pos * THREADS] = __float2half_ru(e); // (an infinite bound stays infinite)
                     const float slack = __fmaf_rn(v0x - px, nx, (v0y - py) * ny);
                     nviol += slack < -e ? 1 : 0;
                     unclear = unclear || !(fabsf(slack) > e); // (also catches an infinite error bound)
@@ -420,8 +425,8 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
     const NbRec<float> me_rec = s_nr[s];
     const float4 me = me_rec.pv;
     const double4 dm = s_dm[s];
-    const u8 *perm = sm_perm + a;
-    const float *cerr = sm_err + a;
+    const u8 *perm = reinterpret_cast<const u8 *>(s_perm) + (size_t)s * MAXN; // (position p of the order: byte p)
+    const __half *cerr = sm_err + a;
     SmemCons<float> cons{sm_cons + a, THREADS};
     const float cap = (float)dm.z;
     float vxf, vyf;
@@ -436,14 +441,14 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
         {   // the closing formula of _lp1_target on line L = c_last, bound B = j_sel (K:98-119)
             const double inv_tau = __ddiv_rn(1.0, P.tau), inv_dt = __ddiv_rn(1.0, P.dt);
             double px, py, nx, ny;
-            halfplane64(s, c_last, P, s_nr, nb, perm, THREADS, inv_tau, inv_dt, px, py, nx, ny);
+            halfplane64(s, c_last, P, s_nr, nb, perm, 1, inv_tau, inv_dt, px, py, nx, ny);
             const double dx = -ny, dy = nx;
             double t;
             if (kind == 0) {
                 t = (tx - px) * dx + (ty - py) * dy;
             } else {
                 double qx, qy, mx, my;
-                halfplane64(s, j_sel, P, s_nr, nb, perm, THREADS, inv_tau, inv_dt, qx, qy, mx, my);
+                halfplane64(s, j_sel, P, s_nr, nb, perm, 1, inv_tau, inv_dt, qx, qy, mx, my);
                 const double a_ = dx * mx + dy * my;
                 const double b_ = (qx - px) * mx + (qy - py) * my;
                 t = __ddiv_rn(b_, a_);
@@ -460,7 +465,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
         for (int pos = 0; pos < cnt; ++pos) { // every inactive half-plane holds with a margin above its error
             float px, py, nx, ny;
             cons.get(pos, px, py, nx, ny);
-            const float e = cerr[pos * THREADS];
+            const float e = __half2float(cerr[pos * THREADS]);
             const bool act = pos == c_last || (kind != 0 && pos == j_sel);
             const float slack = __fmaf_rn(cvx - px, nx, (cvy - py) * ny);
             if (act) e_act += e;
