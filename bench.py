@@ -219,6 +219,44 @@ def numba_reference(state, cfg, budget_s: float = 40.0):
         return {"unavailable": f"{type(e).__name__}: {e}"}
 
 
+def paper_scale_run(device):
+    """The paper's own experiment: a 4-way crossing of 2,500 agents
+    (10 % vehicles) from spawn to the last arrival through `run(config)` -- spawn sampling, every
+    frame with arrival removal and metrics, trajectories recorded -- in this package (f64: the
+    reference's bits, tests/test_gpu_run.py) and, where baseline/_ref is installed, in the
+    unmodified reference with all host cores. Wall-clock, the whole call."""
+    from paper_2008_11578_b200 import crossing_config, run
+    out = {"scenario": "four_way crossing, 625 agents per arm, vehicle fraction 0.1, seed 11; run to termination"}
+    cfg = crossing_config("four_way", 625, 0.1, seed=11)
+    run(crossing_config("four_way", 8, 0.1, seed=1), device=device)          # (library / context warm-up)
+    t0 = time.perf_counter()
+    res = run(cfg, record_trajectories=True, device=device)
+    t = time.perf_counter() - t0
+    out["ours_f64"] = {"frames": res.summary.frames, "arrived": res.summary.arrived, "wall_s": t,
+                       "ms_per_frame": t / max(res.summary.frames, 1) * 1e3}
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "orcasim")):
+        try:
+            if ref_dir not in sys.path:
+                sys.path.insert(0, ref_dir)
+            from orcasim import bench as rbench
+            from orcasim import crossings as rcross
+            from orcasim import engine as rengine
+            rbench.warmup()
+            rcfg = rcross.crossing_config("four_way", 625, 0.1, seed=11)
+            threads = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            rres = rengine.run(rcfg, worker_count=threads, record_trajectories=True)
+            t = time.perf_counter() - t0
+            out["reference_numba"] = {"frames": rres.summary.frames, "arrived": rres.summary.arrived, "wall_s": t,
+                                      "ms_per_frame": t / max(rres.summary.frames, 1) * 1e3, "workers": threads}
+            out["same_frames_and_arrivals"] = bool(rres.summary.frames == res.summary.frames
+                                                   and rres.summary.arrived == res.summary.arrived)
+        except Exception as e:      # noqa: BLE001 -- context only, never takes the line down
+            out["reference_numba"] = {"unavailable": f"{type(e).__name__}: {e}"}
+    return out
+
+
 def parity_census(state, cfg, precisions, device):
     """One frame of the benchmarked crowd from its initial state in each precision mode against
     the CPU oracle on EVERY agent (run after the timed region; the oracle is the checker only):
@@ -481,6 +519,7 @@ def run_ours(args):
             extras["config5_8m_single_gpu"] = other["config5_8m"]
             extras["lp_1m_resident_ms"] = {k: lp_resident(k, "f64", local, stream, 10)
                                            for k in sorted(LP_WORKLOADS)}
+            extras["paper_scale_run"] = paper_scale_run(local)
         census = parity_census(state, cfg, [args.precision] + [p for p in ("mixed", "cert32", "f32")
                                                                if p != args.precision], local)
         ref_numba = numba_reference(state, cfg)

@@ -518,6 +518,8 @@ def main():
         return gen_api()
     if os.environ.get("GEN_ONLY_RUN"):
         return gen_run()
+    if os.environ.get("GEN_ONLY_PAPER"):
+        return gen_run_paper()
     if os.environ.get("GEN_ONLY_SCENARIO"):
         return gen_scenarios()
     gen_kat()
@@ -525,6 +527,7 @@ def main():
     gen_frames()
     gen_chain()
     gen_run()
+    gen_run_paper()
     gen_scenarios()
     gen_api()
 
@@ -581,6 +584,62 @@ def gen_run():
             arrival=arrival, sample_frames=np.array(sample, dtype=np.int64), traj=traj,
             final_ids=res.final_state.ids)
         print(f"run_{name}.npz agents={n0} frames={s.frames} terminated={s.terminated} "
+              f"arrived={s.arrived} collisions={s.total_collisions} fallbacks={s.total_fallbacks}")
+
+
+def _mix64(z):
+    z = z.astype(np.uint64, copy=True)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def frame_digest(ids, positions, velocities) -> int:
+    """Order-independent 64-bit digest of {id: (position bits, velocity bits)} -- the function of
+    paper_2008_11578_b200.parallel.strips.state_hash, restated here so that the generator needs
+    nothing but the reference."""
+    mix = np.uint64(0x9E3779B97F4A7C15)
+    ids = np.ascontiguousarray(ids, dtype=np.int64).view(np.uint64)
+    p = np.ascontiguousarray(positions, dtype=np.float64).view(np.uint64).reshape(-1, 2)
+    v = np.ascontiguousarray(velocities, dtype=np.float64).view(np.uint64).reshape(-1, 2)
+    with np.errstate(over="ignore"):
+        h = _mix64(ids * mix + np.uint64(1))
+        for col in (p[:, 0], p[:, 1], v[:, 0], v[:, 1]):
+            h = _mix64(h ^ (col + mix))
+        return int(h.sum(dtype=np.uint64))
+
+
+def gen_run_paper():
+    """The paper's own experiment scale: 2- and 4-way crossings of
+    2,500 agents, run to termination by the reference. Too long for per-frame trajectories in a
+    fixture: every frame is pinned by an id-keyed 64-bit digest of (position, velocity) of the agents
+    active in it, plus the per-frame metrics and the run summary."""
+    from orcasim.crossings import crossing_config
+    for name, kind, per_arm, vf, seed in (("paper_four_way_2500", "four_way", 625, 0.1, 11),
+                                          ("paper_two_way_2500", "two_way", 1250, 0.1, 12)):
+        cfg = crossing_config(kind, per_arm, vf, seed)
+        st = E.init_state(cfg)
+        res = E.run(cfg, worker_count=os.cpu_count() or 1, record_trajectories=True)
+        s = res.summary
+        digests = np.array([frame_digest(l.ids, l.positions, l.velocities) for l in res.frame_logs], dtype=np.uint64)
+        np.savez_compressed(
+            os.path.join(OUT, f"run_{name}.npz"),
+            ids=st.ids, positions=st.positions, velocities=st.velocities, radii=st.radii,
+            pref_speeds=st.pref_speeds, max_speeds=st.max_speeds, goals=st.goals,
+            goal_tols=st.goal_tols, class_codes=st.class_codes.astype(np.int8),
+            dt=cfg.dt, tau=cfg.tau, neighbor_radius=cfg.neighbor_radius,
+            max_neighbors=np.int64(cfg.max_neighbors), avoidance_margin=cfg.avoidance_margin,
+            fmat=cfg.responsibility.as_array(), guard=np.int64(cfg.frame_guard()), seed=np.int64(cfg.seed),
+            frames=np.int64(s.frames), terminated=np.bool_(s.terminated), arrived=np.int64(s.arrived),
+            total_collisions=np.int64(s.total_collisions), min_separation=np.float64(s.min_separation),
+            total_fallbacks=np.int64(s.total_fallbacks),
+            travel_ped=np.float64(s.mean_travel_time.get(E.AgentClass.PEDESTRIAN, np.nan)),
+            travel_veh=np.float64(s.mean_travel_time.get(E.AgentClass.VEHICLE, np.nan)),
+            m_min_sep=np.array([m.min_separation for m in res.frame_metrics]),
+            m_coll=np.array([m.collision_count for m in res.frame_metrics], dtype=np.int64),
+            m_active=np.array([m.active_agents for m in res.frame_metrics], dtype=np.int64),
+            digests=digests, final_ids=res.final_state.ids)
+        print(f"run_{name}.npz agents={st.active_count} frames={s.frames} terminated={s.terminated} "
               f"arrived={s.arrived} collisions={s.total_collisions} fallbacks={s.total_fallbacks}")
 
 

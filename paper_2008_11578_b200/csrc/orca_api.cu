@@ -1107,29 +1107,39 @@ template <typename R> static int compact_stage(orca_sim *sim, int src_idx, int d
     cudaStream_t st = sim->stream;
     const int64_t n = sim->n_bound;
     const int a = sim->acur, b = 1 - a;
-    if (from_sel)
-        k_keep_unselected<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->sel, sim->keep);
-    else
-        k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
-                                                           sim->params.remove_arrivals);
-    const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
-    k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums);
-    k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
-    k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums,
-                                                       sim->dst_idx);
     const int *lscan = nullptr;
     // (a strip's storage order means nothing to the host -- agents come and go with every
     //  migration -- so there the survivors are simply renumbered in their new physical order)
-    if (sim->rows_permuted && !sim->strip_on) {
-        // survivors keep the reference's relative order: new logical row = rank among the
-        // surviving logical rows
-        k_keep_by_logical<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->keep, sim->lrow[a], sim->lkeep);
-        k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->lkeep, sim->block_sums);
+    const bool logical = sim->rows_permuted && !sim->strip_on;
+    if (!from_sel && n + 1 <= ORCA_SMALL_ROWS) {
+        // a small crowd's frame is a chain of dependent launches: all four passes in one block
+        k_removal_scans_small<<<1, SCAN_THREADS, 0, st>>>(sim->plan, sim->arrived, sim->params.remove_arrivals, sim->keep,
+                                                          sim->dst_idx, logical ? sim->lrow[a] : nullptr, sim->lkeep,
+                                                          sim->lscan);
+        sim->launches -= 3;
+        if (logical) lscan = sim->lscan;
+    } else {
+        if (from_sel)
+            k_keep_unselected<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->sel, sim->keep);
+        else
+            k_keep_flags<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->arrived, sim->keep,
+                                                               sim->params.remove_arrivals);
+        const int scan_blocks = (int)((n + 1 + SCAN_TILE - 1) / SCAN_TILE);
+        k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums);
         k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
-        k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->lkeep, sim->block_sums,
-                                                           sim->lscan);
-        sim->launches += 4;
-        lscan = sim->lscan;
+        k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->keep, sim->block_sums,
+                                                           sim->dst_idx);
+        if (logical) {
+            // survivors keep the reference's relative order: new logical row = rank among the
+            // surviving logical rows
+            k_keep_by_logical<<<grid_for(n + 1, 256), 256, 0, st>>>(sim->plan, sim->keep, sim->lrow[a], sim->lkeep);
+            k_scan_reduce<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->lkeep, sim->block_sums);
+            k_scan_top<<<1, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->block_sums);
+            k_scan_apply<<<scan_blocks, SCAN_THREADS, 0, st>>>(&sim->plan->n, 1, sim->lkeep, sim->block_sums,
+                                                               sim->lscan);
+            sim->launches += 4;
+            lscan = sim->lscan;
+        }
     }
     k_compact<R><<<grid_for(n, 256), 256, 0, st>>>(
         sim->plan, sim->keep, sim->dst_idx, reinterpret_cast<const R4 *>(sim->pv[src_idx]),

@@ -399,6 +399,55 @@ k_scan_small(const int *__restrict__ len_ptr, int len_extra, const int *__restri
     }
 }
 
+// Everything the removal of arrivals needs before the rows move, for a SMALL crowd, by one block
+// (k_keep_flags + scan, k_keep_by_logical + scan: eight launches of a few microseconds each --
+// a 2,500-agent frame is a chain of ~26 dependent launches and nothing else).
+#ifndef ORCA_SMALL_ROWS
+#define ORCA_SMALL_ROWS 16384
+#endif
+__device__ __forceinline__ void block_scan_tiles(int len, const int *in, int *out, int *sm)
+{
+    int carry = 0;
+    for (int base = 0; base < len; base += SCAN_TILE) {
+        const int first = base + threadIdx.x * SCAN_ITEMS;
+        int v[SCAN_ITEMS];
+        int s = 0;
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) {
+            v[k] = (first + k) < len ? in[first + k] : 0;
+            s += v[k];
+        }
+        int total;
+        int run = carry + block_exclusive_scan(s, sm, total);
+#pragma unroll
+        for (int k = 0; k < SCAN_ITEMS; ++k) {
+            if ((first + k) < len) out[first + k] = run;
+            run += v[k];
+        }
+        carry += total;
+        __syncthreads(); // sm is reused by the next tile
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_removal_scans_small(const GridPlan *__restrict__ plan, const u8 *__restrict__ arrived, int remove_arrivals,
+                      int *keep, int *dst_idx, const int *__restrict__ lrow, int *lkeep, int *lscan)
+{
+    __shared__ int sm[64];
+    const int n = plan->n, n_owned = plan->n_owned;
+    for (int i = threadIdx.x; i <= n; i += SCAN_THREADS)
+        keep[i] = (i < n_owned && !(remove_arrivals && arrived[i])) ? 1 : 0; // (k_keep_flags)
+    __syncthreads();
+    block_scan_tiles(n + 1, keep, dst_idx, sm);
+    if (!lrow) return;
+    for (int i = threadIdx.x; i <= n; i += SCAN_THREADS) { // (k_keep_by_logical)
+        if (i == n) lkeep[n] = 0;
+        else lkeep[lrow[i]] = keep[i];
+    }
+    __syncthreads();
+    block_scan_tiles(n + 1, lkeep, lscan, sm);
+}
+
 // Scatter into cell-sorted order. Writes, per sorted slot s:
 //   s_xy  (x, y)                         candidate stream of the neighbour search
 //   s_nr  (x, y, vx, vy | radius, class code | pad)   pre-step snapshot, one 32 B record (NbRec):

@@ -149,7 +149,8 @@ def test_grid_range_error():
         O.grid_arrays(np.array([[1e12, 0.0]]), 1.0)
 
 
-@pytest.mark.parametrize("name", ["run_two_way_80.npz", "run_four_way_96.npz"])
+@pytest.mark.parametrize("name", ["run_two_way_80.npz", "run_four_way_96.npz", "run_paper_four_way_2500.npz",
+                                  "run_paper_two_way_2500.npz"])
 def test_whole_run_bitwise(name):
     """The oracle stepped in a loop reproduces the reference's engine.run of the built-in
     crossing scenarios (spawned crowd taken from the fixture): frames, arrivals, metrics."""
