@@ -24,6 +24,8 @@ ORCA_CHUNKS=1 ORCA_GRAPH=0 ncu --set full --clock-control none --import-source o
 ORCA_CHUNKS=1 ORCA_GRAPH=0 ncu --set full --clock-control none -k regex:"k_solve_group|k_fallback_coop" -s 12 -c 3 -o gpurun_out/g_full_d2 python bench.py --steps 3 --warmup 4 --resident-only --workload config3_262k_d2 --precision mixed > gpurun_out/g_fd2.log 2>&1
 ORCA_CHUNKS=1 ORCA_GRAPH=0 ncu --set full --clock-control none -k regex:"k_solve_cert|k_solve_group_queue|k_shuffle" -s 6 -c 3 -o gpurun_out/g_full_cert python bench.py --steps 3 --warmup 4 --resident-only --precision cert32 > gpurun_out/g_fc.log 2>&1
 ncu --set full --clock-control none -k regex:k_lp_batch -s 4 -c 2 -o gpurun_out/g_full_lp python bench.py --workload lp_1m_infeasible --steps 2 --warmup 3 > gpurun_out/g_flp.log 2>&1
+# the reference's own test-suite against this package (tests/test_gpu_refsuite.py runs the same command)
+PYTHONPATH=tests/refsuite:$PWD python -m pytest baseline/_ref/_tests -v -p no:cacheprovider > gpurun_out/g_refsuite.log 2>&1
 # the reports are ~15 MB each and gpurun_out/ travels back only below 64 MiB: keep their raw pages instead
 for f in g_full g_full_d2 g_full_cert g_full_lp; do ncu -i gpurun_out/$f.ncu-rep --page raw --csv > gpurun_out/$f.raw.csv 2>/dev/null && rm -f gpurun_out/$f.ncu-rep; done
 ls -la gpurun_out/g_*

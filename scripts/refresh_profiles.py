@@ -33,6 +33,18 @@ for name in ("default", "mixed", "f32", "f64", "ref"):
 for name in ("configs", "lp", "strips"):
     shutil.copy(os.path.join(G, f"g_{name}.jsonl"), os.path.join(P, f"bench_{tag}_{name}.jsonl"))
 
+# the reference's own suite against this package: the verbose pytest listing as it came
+rs = os.path.join(G, "g_refsuite.log")
+if os.path.exists(rs):
+    with open(rs) as f:
+        lines = [l.rstrip() for l in f.read().splitlines()]
+    keep = [l for l in lines if "::" in l or " passed" in l or " failed" in l or "error" in l.lower()]
+    with open(os.path.join(P, f"{tag}_refsuite.txt"), "w") as f:
+        f.write("# The reference's own test-suite (pkg/tests, unmodified, staged into baseline/_ref/_tests) with the name\n"
+                "# `orcasim` bound to paper_2008_11578_b200 (tests/refsuite/orcasim), on one B200:\n"
+                "#   PYTHONPATH=tests/refsuite:$PWD python -m pytest baseline/_ref/_tests -v -p no:cacheprovider\n\n")
+        f.write("\n".join(keep) + "\n")
+
 # ncu launch list and full captures
 head_l = (f"# {tag} — ncu launch list, 1,048,576 agents, mixed precision, final state of the round\n\n"
           "Command: `ORCA_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python "
