@@ -963,6 +963,11 @@ static int solve_chunk(orca_sim *sim, const StepParams &P, int out_idx, cudaStre
     } else if (sim->solve_gl == 2 && preshuffle)
         k_solve_group<S, R, MAXN, 128, 2, true><<<grid_for(m, 64), 128, C::solve_bpt * 64, st>>>(
             ORCA_SOLVE_ARGS, s_perm, fq_cnt);
+    else if (sim->solve_gl == 2 && ORCA_SMALL_SOLVE_GL != 2 && n <= ORCA_SMALL_SOLVE_AGENTS)
+        // a small crowd is one wave whose time is ONE agent's chain of half-planes: more lanes per agent
+        k_solve_group<S, R, MAXN, 128, ORCA_SMALL_SOLVE_GL, false>
+            <<<grid_for(m, 128 / ORCA_SMALL_SOLVE_GL), 128, C::solve_bpt * (128 / ORCA_SMALL_SOLVE_GL), st>>>(
+                ORCA_SOLVE_ARGS, s_perm, fq_cnt);
     else if (sim->solve_gl == 2)
         k_solve_group<S, R, MAXN, 128, 2, false><<<grid_for(m, 64), 128, C::solve_bpt * 64, st>>>(
             ORCA_SOLVE_ARGS, s_perm, fq_cnt);

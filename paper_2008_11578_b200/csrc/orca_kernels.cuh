@@ -47,6 +47,12 @@
 #define ORCA_PRESHUFFLE_MIN_AGENTS 65536
 #endif
 #ifndef ORCA_CHUNKS_DEFAULT
+#ifndef ORCA_SMALL_SOLVE_GL
+#define ORCA_SMALL_SOLVE_GL 8      // lanes per agent in the FP64 solve kernel for crowds of <= ORCA_SMALL_SOLVE_AGENTS:
+#endif                             // one wave whose time is one agent's chain (1,024 agents: solve 27 -> 20 us; 4 lanes: 23)
+#ifndef ORCA_SMALL_SOLVE_AGENTS
+#define ORCA_SMALL_SOLVE_AGENTS 8192
+#endif
 #ifndef ORCA_QUEUE_GL
 #define ORCA_QUEUE_GL 4 // lanes per agent in the FP64 pass over the agents ORCA_CERT32 could not certify: a few
                         // percent of the crowd, i.e. one wave whose time is ONE agent's chain of sixteen FP64
