@@ -144,8 +144,9 @@ class DeviceStripOps:
 
     # -- the exchange through peer memory (orca_strip_window_*) --
     def window_create(self, side_bytes: int):
-        """This handle's window: (CUDA IPC handle as bytes, base address, the window as a uint8
-        tensor view for the slots `window_wait` returns)."""
+        """Allocate this handle's window (two receive buffers of side_bytes per side + flags):
+        (CUDA IPC handle as 64 bytes -- for neighbours in other processes --, base address -- for
+        neighbours in this process)."""
         h = (C.c_ubyte * ORCA_IPC_HANDLE_BYTES)()
         base = C.c_void_p()
         check(self._L.orca_strip_window_create(self.sim._h, int(side_bytes), h, C.byref(base)), self.sim._h)
