@@ -388,6 +388,11 @@ def run_ours(args):
     sim.load(state)
     sim.run(max(args.warmup, 3))
     sim.sync()
+    # (the handle adapts at a synchronisation -- ORCA_CERT32 picks its path from the fallback count it
+    #  sees there -- and a changed path means a new graph capture and first launches of other kernels:
+    #  a second, short warm-up keeps those one-off costs out of the timed region)
+    sim.run(2)
+    sim.sync()
     l0 = sim.info().kernel_launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -491,6 +496,8 @@ def run_ours(args):
                             remove_arrivals=False, compute_metrics=False, stream=stream) as sm:
                 sm.load(st)
                 sm.run(warm)
+                sm.sync()
+                sm.run(2)          # (see run_ours: adaptation happens at a synchronisation)
                 sm.sync()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
