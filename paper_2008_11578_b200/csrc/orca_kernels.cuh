@@ -671,10 +671,11 @@ k_gather_fast32(GridPlan *__restrict__ plan, StepParams P, const typename Vec<R>
         constexpr int kScanUnroll = ORCA_SCAN_UNROLL;
 #pragma unroll kScanUnroll
         for (int s2 = a0; s2 < e; ++s2) {
-            if (d2_f32(s_xy[s2]) <= T_f && s2 != s) {
-                if (nbuf < CAP) my_buf[nbuf * 128] = s2;
-                ++nbuf;
-            }
+            // (one predicated store, no branch: past CAP the last slot is overwritten, and the
+            //  count alone sends the agent to the exact search)
+            const bool pass = d2_f32(s_xy[s2]) <= T_f && s2 != s;
+            if (pass) my_buf[min(nbuf, CAP - 1) * 128] = s2;
+            nbuf += pass ? 1 : 0;
         }
     }
     bool ok = nbuf <= CAP;
