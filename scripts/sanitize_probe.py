@@ -71,8 +71,10 @@ for prec, world, transport in (("mixed", 2, "sendrecv"), ("f64", 3, "sendrecv"),
     for s_ in sims:
         s_.close()
 from paper_2008_11578_b200 import HalfPlaneConstraint, solve_least_penetration
-from paper_2008_11578_b200.grid import neighbor_lists
+from paper_2008_11578_b200.grid import neighbor_lists, neighbor_lists_all
 rows, cnt = neighbor_lists(st.ids, st.positions, 5.0, 12)
+off, allrows = neighbor_lists_all(st.ids, st.positions, 6.0)          # the uncapped query (CSR)
+print("neighbor_lists_all", off[-1], allrows.shape)
 ang = rng.uniform(0, 6.28, 9)
 v = solve_least_penetration([HalfPlaneConstraint(rng.normal(size=2), (np.cos(a), np.sin(a))) for a in ang], 1.5,
                             start_index=3, warm_start=(0.1, 0.2))
