@@ -345,3 +345,25 @@ def test_pack_record_layout_and_errors():
         ops.append(buf, c, False)
         back = sim.state()
         assert np.array_equal(np.sort(back.ids), np.sort(st.ids))
+
+
+def test_bench_gpus_2_launches_its_ranks_and_verifies_against_one_gpu():
+    """`python bench.py --gpus 2` outside torchrun: it starts its own two ranks (they share this
+    box's GPU, so the set-up runs over gloo), the strips exchange through peer-memory windows, and
+    the one JSON line on stdout carries the digest check against the same crowd on one GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "6", "--warmup", "3",
+                          "--workload", "config2_16k"], capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, out.stdout[-2000:]          # stdout carries the line and nothing else
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["metric"] == "agent_steps_per_s"
+    assert line["parallelism"]["transport"] == "window"
+    assert line["verify"]["bit_equal_vs_1gpu"] is True and line["verify"]["agents"] == 2 * 16640
+    assert line["parallelism"]["host_syncs_per_step"] <= 0.5 and line["gpu_launches"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
