@@ -148,3 +148,31 @@ def test_simstate_agents_are_the_rows_as_agent_states():
         assert int(a.agent_class) == int(st.class_codes[i])
     agents[0].position[0] += 1.0                     # copies, not views
     assert agents[0].position[0] != st.positions[0, 0]
+
+
+def test_neighbor_query_all_reports_the_capacity_it_needs():
+    """The C entry point with a buffer that is too small: ORCA_ECAPACITY, with the offsets and the
+    total already valid, so that one retry with `total` entries succeeds (grid.neighbor_lists_all)."""
+    import ctypes as C
+    from paper_2008_11578_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(9)
+    n = 300
+    pos = rng.uniform(0.0, 12.0, size=(n, 2))
+    ids = np.arange(n, dtype=np.int64)
+    off = np.zeros(n + 1, dtype=np.int64)
+    total = C.c_int64(-1)
+    rc = L.orca_neighbor_query_all(0, n, _lib.ptr(ids), _lib.ptr(pos), 2.0, 0, _lib.ptr(off), None, C.byref(total))
+    assert rc == _lib.ORCA_ECAPACITY and total.value > 0 and off[-1] == total.value
+    rows = np.empty(total.value, dtype=np.int64)
+    rc = L.orca_neighbor_query_all(0, n, _lib.ptr(ids), _lib.ptr(pos), 2.0, total.value, _lib.ptr(off),
+                                   _lib.ptr(rows), C.byref(total))
+    assert rc == 0
+    d = pos[:, None, :] - pos[None, :, :]
+    within = (d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1] <= 4.0) & ~np.eye(n, dtype=bool)
+    assert np.array_equal(np.diff(off), within.sum(axis=1))
+    # bad arguments are refused, not dereferenced
+    assert L.orca_neighbor_query_all(0, n, _lib.ptr(ids), _lib.ptr(pos), -1.0, 0, _lib.ptr(off), None,
+                                     C.byref(total)) == _lib.ORCA_EINVAL
+    assert L.orca_neighbor_query_all(0, n, _lib.ptr(ids), _lib.ptr(pos), 2.0, 0, _lib.ptr(off), None, None) \
+        == _lib.ORCA_EINVAL
