@@ -77,64 +77,69 @@ def adversarial(seed):
     return st, cfg
 
 
-first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-count = int(sys.argv[2]) if len(sys.argv) > 2 else 200
-bad, t0, agents, queued, ran = [], time.time(), 0, 0, 0
-if len(sys.argv) > 3 and sys.argv[3] == "oracle":
-    from oracle import oracle as O
+def main():
+    first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    count = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+    bad, t0, agents, queued, ran = [], time.time(), 0, 0, 0
+    if len(sys.argv) > 3 and sys.argv[3] == "oracle":
+        from oracle import oracle as O
+        for seed in range(first, first + count):
+            st, cfg = adversarial(seed)
+            n = st.active_count
+            try:
+                ref = O.frame_solve(st, cfg, debug=True)
+            except ValueError:
+                continue                                   # coincident centres in the initial crowd
+            with Simulation(cfg, capacity=n, precision="f64", remove_arrivals=False) as sim:
+                sim.load(st)
+                sim.step()
+                sim.sync()
+                d = sim.debug_last_step(n, cfg.max_neighbors)
+            ran += 1
+            ok = (np.array_equal(d["out_v"], ref.out_v) and np.array_equal(d["status"], ref.status)
+                  and np.array_equal(d["failed_at"], ref.failed_at) and np.array_equal(d["nb_count"], ref.nb_count))
+            for i in range(n):
+                ok = ok and np.array_equal(d["nb_rows"][i, :d["nb_count"][i]], ref.nb_rows[i, :ref.nb_count[i]])
+            if not ok:
+                bad.append(seed)
+                print("FAIL", seed, n, flush=True)
+            agents += n
+        print("adversarial f64-vs-oracle soak done:", count, "seeds from", first, f"({ran} ran)", "- failures:", len(bad),
+              "in", round(time.time() - t0), "s;", agents, "agents")
+        sys.exit(1 if bad else 0)
     for seed in range(first, first + count):
         st, cfg = adversarial(seed)
         n = st.active_count
         try:
-            ref = O.frame_solve(st, cfg, debug=True)
-        except ValueError:
-            continue                                   # coincident centres in the initial crowd
-        with Simulation(cfg, capacity=n, precision="f64", remove_arrivals=False) as sim:
-            sim.load(st)
-            sim.step()
-            sim.sync()
-            d = sim.debug_last_step(n, cfg.max_neighbors)
-        ran += 1
-        ok = (np.array_equal(d["out_v"], ref.out_v) and np.array_equal(d["status"], ref.status)
-              and np.array_equal(d["failed_at"], ref.failed_at) and np.array_equal(d["nb_count"], ref.nb_count))
-        for i in range(n):
-            ok = ok and np.array_equal(d["nb_rows"][i, :d["nb_count"][i]], ref.nb_rows[i, :ref.nb_count[i]])
-        if not ok:
-            bad.append(seed)
-            print("FAIL", seed, n, flush=True)
-        agents += n
-    print("adversarial f64-vs-oracle soak done:", count, "seeds from", first, f"({ran} ran)", "- failures:", len(bad),
-          "in", round(time.time() - t0), "s;", agents, "agents")
-    sys.exit(1 if bad else 0)
-for seed in range(first, first + count):
-    st, cfg = adversarial(seed)
-    n = st.active_count
-    try:
-        out = {}
-        for precision in ("mixed", "cert32"):
-            rows = []
-            with Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False) as sim:
-                sim.load(st)
-                for _ in range(3):
-                    sim.step()
-                    sim.sync()
-                    d = sim.debug_last_step(n, cfg.max_neighbors)
-                    info = sim.info()
-                    rows.append((d["out_v"], d["status"], d["failed_at"], int(info.lp_fallbacks), int(info.solve_queue)))
-            out[precision] = rows
-        ran += 1
-        for k, (a, b) in enumerate(zip(out["mixed"], out["cert32"])):
-            assert np.array_equal(a[0], b[0]), f"velocities, frame {k}: {int((a[0] != b[0]).any(axis=1).sum())} agents"
-            assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3], f"status, frame {k}"
-            agents += n
-            queued += b[4]
-    except ValueError as e:       # the reference's own error (coincident centres after a frame)
-        if "coincident" not in str(e):
+            out = {}
+            for precision in ("mixed", "cert32"):
+                rows = []
+                with Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False) as sim:
+                    sim.load(st)
+                    for _ in range(3):
+                        sim.step()
+                        sim.sync()
+                        d = sim.debug_last_step(n, cfg.max_neighbors)
+                        info = sim.info()
+                        rows.append((d["out_v"], d["status"], d["failed_at"], int(info.lp_fallbacks), int(info.solve_queue)))
+                out[precision] = rows
+            ran += 1
+            for k, (a, b) in enumerate(zip(out["mixed"], out["cert32"])):
+                assert np.array_equal(a[0], b[0]), f"velocities, frame {k}: {int((a[0] != b[0]).any(axis=1).sum())} agents"
+                assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and a[3] == b[3], f"status, frame {k}"
+                agents += n
+                queued += b[4]
+        except ValueError as e:       # the reference's own error (coincident centres after a frame)
+            if "coincident" not in str(e):
+                bad.append((seed, repr(e)[:160]))
+                print("FAIL", seed, repr(e)[:160], flush=True)
+        except AssertionError as e:
             bad.append((seed, repr(e)[:160]))
-            print("FAIL", seed, repr(e)[:160], flush=True)
-    except AssertionError as e:
-        bad.append((seed, repr(e)[:160]))
-        print("FAIL", seed, n, repr(e)[:160], flush=True)
-print("adversarial cert32 soak done:", count, "seeds from", first, f"({ran} ran to the end)", "- failures:", len(bad),
-      "in", round(time.time() - t0), "s;",
-      f"{agents} agent-frames, {queued} ({queued / max(agents, 1):.1%}) went through the FP64 kernels")
+            print("FAIL", seed, n, repr(e)[:160], flush=True)
+    print("adversarial cert32 soak done:", count, "seeds from", first, f"({ran} ran to the end)", "- failures:", len(bad),
+          "in", round(time.time() - t0), "s;",
+          f"{agents} agent-frames, {queued} ({queued / max(agents, 1):.1%}) went through the FP64 kernels")
+
+
+if __name__ == "__main__":
+    main()

@@ -113,3 +113,37 @@ def test_random_step_matches_oracle(seed):
     # responsibility matrices, max_neighbors 0..32, lattices with exact ties)
     for a, b in zip(kept["mixed"], kept["cert32"]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 5, 8, 13, 21])
+def test_certificate_refuses_what_it_cannot_decide(seed):
+    """Crowds that sit ON the decisions of the certified FP32 solve (tests/soak/soak_cert_adversarial.py:
+    exact lattices, discs exactly touching, identical / mirrored / zero velocities, agents at their
+    goal): cert32 == mixed bit for bit over three frames, and f64 == the oracle on the first."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "soak"))
+    from soak_cert_adversarial import adversarial
+    st, cfg = adversarial(seed)
+    n = st.active_count
+    out = {}
+    for precision in ("mixed", "cert32"):
+        rows = []
+        with Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False) as sim:
+            sim.load(st)
+            for _ in range(3):
+                sim.step()
+                sim.sync()
+                d = sim.debug_last_step(n, cfg.max_neighbors)
+                rows.append((d["out_v"], d["status"], d["failed_at"]))
+        out[precision] = rows
+    for a, b in zip(out["mixed"], out["cert32"]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    ref = O.frame_solve(st, cfg, debug=True)
+    with Simulation(cfg, capacity=n, precision="f64", remove_arrivals=False) as sim:
+        sim.load(st)
+        sim.step()
+        sim.sync()
+        d = sim.debug_last_step(n, cfg.max_neighbors)
+    assert np.array_equal(d["out_v"], ref.out_v) and np.array_equal(d["status"], ref.status)
+    assert np.array_equal(d["failed_at"], ref.failed_at) and np.array_equal(d["nb_count"], ref.nb_count)
