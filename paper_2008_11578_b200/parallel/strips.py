@@ -284,17 +284,25 @@ class StripDriver:
         mine = (socket.gethostname(), self.window_handle)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine, group=self.group)
-        for k, s in enumerate(self.SIDES):
-            p = self.peer[s]
-            if p is None:
-                continue
-            if everyone[p][0] != mine[0]:
-                raise RuntimeError(f"strip {self.rank} and strip {p} are on different hosts ({mine[0]}, "
-                                   f"{everyone[p][0]}): the window transport maps peer memory and needs one "
-                                   "node; use transport='sendrecv'")
-            self.ops.window_open(k, ipc_handle=everyone[p][1])
-        self._connected = True
+        failure = None
+        try:
+            for k, s in enumerate(self.SIDES):
+                p = self.peer[s]
+                if p is None:
+                    continue
+                if everyone[p][0] != mine[0]:
+                    raise RuntimeError(f"strip {self.rank} and strip {p} are on different hosts ({mine[0]}, "
+                                       f"{everyone[p][0]}): the window transport maps peer memory and needs one "
+                                       "node; use transport='sendrecv'")
+                self.ops.window_open(k, ipc_handle=everyone[p][1])
+        except Exception as exc:            # noqa: BLE001 -- re-raised below, after the collective
+            failure = exc
+        # (every rank reaches this barrier whether or not its own mapping worked: a rank that raised
+        #  before it would leave the others waiting in a collective it never joins)
         dist.barrier(group=self.group)      # nobody pushes into a window its owner has not created yet
+        if failure is not None:
+            raise failure
+        self._connected = True
 
     def connect_local(self, left=None, right=None):
         """Several drivers in ONE process (tests, one process driving several GPUs): the

@@ -242,8 +242,34 @@ def gpu_gloo_worker(rank, world, port, steps, out_dir, precision, transport="sen
             sim.load(take(st, mine))
             drv = StripDriver(DeviceStripOps(sim), rank, world, bounds, cfg.neighbor_radius,
                               torch.device("cuda", 0), halo_capacity=n, migrant_capacity=n // 4,
-                              vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=4, transport=transport)
-            if transport == "window":
+                              vmax=float(st.max_speeds.max()), dt=cfg.dt, resync_every=4,
+                              transport="sendrecv" if transport == "window_fail" else transport)
+            if transport == "window_fail":
+                # rank 1 cannot map its neighbour's window: connect_windows must raise THERE, return on the
+                # other ranks, and leave nobody behind in a collective; everyone then falls back to send/recv
+                # together, the way bench.py --transport auto does
+                def make(tr):
+                    return StripDriver(drv.ops, rank, world, bounds, cfg.neighbor_radius, torch.device("cuda", 0),
+                                       halo_capacity=n, migrant_capacity=n // 4, vmax=float(st.max_speeds.max()),
+                                       dt=cfg.dt, resync_every=4, transport=tr)
+                drv = make("window")
+                if rank == 1:
+                    def refuse(*_a, **_k):
+                        raise RuntimeError("no peer access (simulated)")
+                    drv.ops.window_open = refuse
+                failed = 0.0
+                try:
+                    drv.connect_windows()
+                except RuntimeError as exc:
+                    assert rank == 1 and "simulated" in str(exc)
+                    failed = 1.0
+                bad = torch.tensor([failed], dtype=torch.float64)
+                dist.all_reduce(bad)
+                assert float(bad.item()) == 1.0
+                drv.close()
+                drv = make("sendrecv")
+                assert drv._stage
+            elif transport == "window":
                 drv.connect_windows()
             else:
                 assert drv._stage

@@ -257,14 +257,15 @@ def test_halo_slab_layout_and_refusals():
                 assert np.array_equal(got.goals[4:, 0], out["goal_x"]) and np.array_equal(got.radii[4:], out["radius"])
 
 
-@pytest.mark.parametrize("world,transport", [(2, "sendrecv"), (2, "window"), (3, "window")])
+@pytest.mark.parametrize("world,transport", [(2, "sendrecv"), (2, "window"), (3, "window"), (2, "window_fail")])
 def test_processes_sharing_one_gpu(tmp_path, world, transport):
     """The real device ops under the real multi-process protocol: the ranks are processes that
     share cuda:0. "sendrecv": the slabs are staged through host memory and travel over gloo (NCCL
     refuses two ranks on one device). "window": every process maps its neighbours' windows through
     CUDA IPC handles, its kernels write the slabs there and raise the flags the neighbours'
     streams wait on (gloo carries the 64-byte handles at set-up, nothing per frame). Equal to
-    the single-handle run, keyed by id."""
+    the single-handle run, keyed by id. "window_fail": one rank cannot map its neighbour's window --
+    it raises, nobody hangs, and all ranks fall back to send/recv together."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as sk:
