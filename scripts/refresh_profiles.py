@@ -46,12 +46,12 @@ if os.path.exists(rs):
         f.write("\n".join(keep) + "\n")
 
 # ncu launch list and full captures
-head_l = (f"# {tag} — ncu launch list, 1,048,576 agents, mixed precision, final state of the round\n\n"
+head_l = (f"# {tag} — ncu launch list of the default bench command (1,048,576 agents, `cert32`), final state of the round\n\n"
           "Command: `ORCA_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python "
           "bench.py --steps 3 --warmup 3 --resident-only` (per-launch times are cold-cache and serialised: compare "
           "shares; `k_import_*`, `k_iota`, `k_bbox`, `k_begin_bins`, `k_permute_rows` run once after the upload; the "
           "first `k_gather` launch searches for every agent, ~0.9 ms, the others ~25 us).\n\n")
-with open(os.path.join(P, f"{tag}_launches_mixed_1m.md"), "w") as f:
+with open(os.path.join(P, f"{tag}_launches_default_1m.md"), "w") as f:
     f.write(head_l + summary("launches", os.path.join(G, "g_launches.csv")))
 head_f = (f"# {tag} — ncu --set full, kernels of the step, 1,048,576 agents, mixed precision, final state "
           "of the round\n\nCommand: `ORCA_GRAPH=0 ncu --set full --clock-control none --import-source on -k "
