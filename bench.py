@@ -559,6 +559,12 @@ def run_ours(args):
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "ncu": ncu_util,   # what actually bounds it: issue slots (ipc of 4), FP64 pipe, lanes, warps
                      "algorithmic_bytes_per_launch": dom_bytes,
+                     "duration_ms": stage_ms[dom],
+                     "duration_source": f"CUDA events on the handle's stream around the '{dom}' stage in this run "
+                                        "(plain launches, one chunk: ONE launch of the kernel per step"
+                                        + (", plus k_shuffle and the FP64 pass over the few percent it queues -- "
+                                           "the stage's time is charged to the kernel whole)" if dom == "solve"
+                                           else ")"),
                      "step_frac": STEP_BYTES_PER_AGENT * n / (ms_step * 1e-3) / 1e9 / hbm_peak,
                      "note": "the step is issue/latency bound, not HBM bound (DESIGN.md s5); "
                              "fractions are reported against the HBM roofline as the contract asks"},
