@@ -22,6 +22,18 @@
 //      on the later-inserted active constraint bounded by the earlier one -- i.e. the value
 //      computed in step 2, bit for bit. (The FP32 run only GUESSES the active set; nothing it
 //      decides is trusted.)
+//   4. and it checks the WAY there. The reference does not only return the optimum, it reports
+//      whether its incremental LP got there (status / failed_at), and that LP gives up on yes / no
+//      tests of its own -- a (nearly) parallel earlier constraint with the line outside it
+//      (K:100-103), an interval that closed (K:112), a line missing the speed disc (K:86). On
+//      duplicated half-planes (symmetric crowds) or three lines through one point those tests hang
+//      on FP64 rounding and can declare a feasible LP infeasible. The intermediate optima the
+//      incremental LP visits (of the first 1, 2, ... constraints in insertion order) do not depend
+//      on who computes them, so the FP32 run sees the same situations: every scan decision must be
+//      clear of the half-plane's error bound plus the current vertex's, every 1-D solve clear of a
+//      parallel-and-not-inside constraint, of a closing interval, of a grazed disc and of an
+//      ill-conditioned vertex (lp1_target_act: `shaky`). Found by the adversarial soak
+//      (tests/soak/soak_cert_adversarial.py, one status mismatch in 2,300 lattice crowds before).
 //
 // An agent that is not certified -- infeasible LP (the least-penetration stage needs FP64
 // half-planes anyway), an active speed disc, near-parallel active lines, a margin too small, an
@@ -50,6 +62,8 @@ namespace orca {
 #define ORCA_CERT_MAX_FALLBACK_PCT 25     // above: most agents need the FP64 kernels anyway (measured break-even ~30 %)
 #endif
 #define CERT_CROSS_MIN 0.02f    // |n_L x n_B| below this: the vertex is ill-conditioned, leave it to FP64
+#define CERT_PAR_BAND 1e-4f     // |d_i . n_j| below this: "parallel" as far as FP32 can tell (the reference: 1e-12 in FP64)
+#define CERT_VERR_MAX 1e-2f     // an intermediate vertex whose error bound exceeds this is not followed
 #ifndef CERT_TASK_BUCKETS
 #define CERT_TASK_BUCKETS 6     // LP tasks of a block are ordered by min(clearly violated half-planes, this)
 #endif
@@ -120,63 +134,92 @@ __device__ __forceinline__ bool vo_exit_cond(float rpx, float rpy, float rvx, fl
 
 // _lp1_target (K:74-119) in FP32 that also reports WHICH bound closed the interval:
 // kind 0 = the projection of the target itself, 1 / 2 = an earlier constraint (position j_sel)
-// from the left / right, 3 / 4 = the speed disc.
+// from the left / right, 3 / 4 = the speed disc -- and how far the point it returns can be from
+// the exact one (verr), and whether any of the reference's own yes / no decisions in this 1-D solve
+// sits within the FP32 error of flipping (shaky): a (nearly) parallel earlier constraint that the
+// line is not clearly inside (K:100-103 declares the LP infeasible there), an interval about to
+// close (K:112), a line grazing the speed disc (K:86), an ill-conditioned binding vertex. The
+// reference takes those decisions in FP64 on ITS half-planes; where they hang on rounding --
+// duplicated half-planes of a symmetric crowd, three lines through one point -- its result is
+// whatever its rounding says, and only the FP64 kernels can reproduce that.
 template <typename V>
-__device__ __forceinline__ bool lp1_target_act(const V &view, int i_pos, float cap, float tx, float ty,
-                                               float &ox, float &oy, int &kind, int &j_sel)
+__device__ __forceinline__ bool lp1_target_act(const V &view, const __half *cerr, int estride, int i_pos, float cap,
+                                               float tx, float ty, float &ox, float &oy, int &kind, int &j_sel,
+                                               float &verr, bool &shaky)
 {
     float px, py, nx, ny;
     view.get(i_pos, px, py, nx, ny);
+    const float ei = __half2float(cerr[i_pos * estride]);
     const float dx = -ny, dy = nx;
     const float pd = __fmaf_rn(px, dx, py * dy);
     const float disc = __fmaf_rn(pd, pd, cap * cap) - __fmaf_rn(px, px, py * py);
     if (disc < 0.0f) return false;
     const float sq = disc * rsqrtf(fmaxf(disc, 1e-30f));
+    shaky = shaky || sq < CERT_CROSS_MIN * cap; // the line grazes the disc: K:86 within rounding, end points ill-conditioned
+    const float ed = ei * cap * __fdividef(1.0f, fmaxf(sq, 1e-20f)); // error of a disc end point
     float t_left = -pd - sq, t_right = -pd + sq;
+    float el = ed, er = ed; // error bounds of the two ends as they stand
     int jl = -1, jr = -1;
     bool bad = false;
 #pragma unroll 4
     for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
         float qx, qy, mx, my;
         view.get(j_pos, qx, qy, mx, my);
+        const float eij = ei + __half2float(cerr[j_pos * estride]);
         const float a = __fmaf_rn(dx, mx, dy * my);
         const float b = __fmaf_rn(qx - px, mx, (qy - py) * my);
         const bool par = fabsf(a) <= 1e-6f;
         bad = bad || (par && b > 0.0f);
-        const float t = __fdividef(b, a);
+        // (nearly) parallel and the line not clearly inside: the reference's "parallel and outside" test
+        // (|a| <= 1e-12 and b > 0 in FP64) cannot be told from here
+        shaky = shaky || (fabsf(a) <= CERT_PAR_BAND && b > -4.0f * eij);
+        const float ra = __fdividef(1.0f, a);
+        const float t = b * ra;
+        const float et = eij * fabsf(ra);
         if (!par && a > 0.0f && t > t_left) {
             t_left = t;
             jl = j_pos;
+            el = et;
         }
         if (!par && !(a > 0.0f) && t < t_right) {
             t_right = t;
             jr = j_pos;
+            er = et;
         }
     }
     if (bad || t_left > t_right) return false;
+    shaky = shaky || !(t_right - t_left > 2.0f * (el + er)); // the interval is about to close (K:112)
     float t = __fmaf_rn(tx - px, dx, (ty - py) * dy);
     kind = 0;
     j_sel = -1;
+    verr = ei;
     if (t < t_left) {
         t = t_left;
         kind = jl >= 0 ? 1 : 3;
         j_sel = jl;
+        verr = el + ei;
     } else if (t > t_right) {
         t = t_right;
         kind = jr >= 0 ? 2 : 4;
         j_sel = jr;
+        verr = er + ei;
     }
+    shaky = shaky || !(verr < CERT_VERR_MAX); // an ill-conditioned vertex: later decisions would be taken at a wrong point
     ox = __fmaf_rn(t, dx, px);
     oy = __fmaf_rn(t, dy, py);
     return true;
 }
 
 // lp2_target_runahead (orca_math.cuh) in FP32, reporting the active set of the LAST 1-D solve
-// (c_last = -1: the clamped target violated nothing).
+// (c_last = -1: the clamped target violated nothing) and whether every decision on the way was clear
+// of its error band (shaky, see lp1_target_act): the incremental LP visits the optima of the first 1, 2,
+// ... constraints, which do not depend on who computes them, so a scan or a 1-D solve that is clear here
+// is decided the same way by the reference.
 template <typename V>
-__device__ __forceinline__ bool lp2_target_runahead_act(const V &view, int k, float cap, float tx, float ty,
-                                                        float &vx, float &vy, int &c_last, int &kind,
-                                                        int &j_sel, unsigned live, bool enabled)
+__device__ __forceinline__ bool lp2_target_runahead_act(const V &view, const __half *cerr, int estride, int k,
+                                                        float cap, float tx, float ty, float &vx, float &vy,
+                                                        int &c_last, int &kind, int &j_sel, bool &shaky,
+                                                        unsigned live, bool enabled)
 {
     const float t2 = __fmaf_rn(tx, tx, ty * ty);
     if (t2 > cap * cap) {
@@ -189,6 +232,7 @@ __device__ __forceinline__ bool lp2_target_runahead_act(const V &view, int k, fl
     }
     int i_pos = 0;
     bool done = !enabled, ok = true;
+    float verr = 0.0f; // how far (vx, vy) can be from the exact intermediate optimum
     c_last = -1;
     kind = 0;
     j_sel = -1;
@@ -199,14 +243,20 @@ __device__ __forceinline__ bool lp2_target_runahead_act(const V &view, int k, fl
             // loads are in flight together (one at a time, this scan is a chain of exposed load latencies
             // -- it was 15 % of the kernel's stall samples)
             for (; i_pos < k; i_pos += 4) {
-                unsigned m = 0;
+                unsigned m = 0, amb = 0;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
+                    const int p = min(i_pos + u, k - 1);
                     float px, py, nx, ny;
-                    view.get(min(i_pos + u, k - 1), px, py, nx, ny);
-                    const bool viol = __fmaf_rn(vx - px, nx, (vy - py) * ny) < 0.0f;
-                    m |= (viol && i_pos + u < k) ? (1u << u) : 0u;
+                    view.get(p, px, py, nx, ny);
+                    const float slack = __fmaf_rn(vx - px, nx, (vy - py) * ny);
+                    const bool valid = i_pos + u < k;
+                    m |= (slack < 0.0f && valid) ? (1u << u) : 0u;
+                    amb |= (!(fabsf(slack) > __half2float(cerr[p * estride]) + verr) && valid) ? (1u << u) : 0u;
                 }
+                // the reference examines the positions up to and including the first violated one at this v
+                const unsigned seen = m ? ((2u << (__ffs(m) - 1)) - 1u) : 0xFu;
+                shaky = shaky || (amb & seen) != 0u;
                 if (m) {
                     i_pos += __ffs(m) - 1;
                     found = true;
@@ -217,11 +267,12 @@ __device__ __forceinline__ bool lp2_target_runahead_act(const V &view, int k, fl
         }
         if (!__any_sync(live, found)) break;
         if (found) {
-            float nvx, nvy;
+            float nvx, nvy, ve = 0.0f;
             int kd, js;
-            if (lp1_target_act<V>(view, i_pos, cap, tx, ty, nvx, nvy, kd, js)) {
+            if (lp1_target_act<V>(view, cerr, estride, i_pos, cap, tx, ty, nvx, nvy, kd, js, ve, shaky)) {
                 vx = nvx;
                 vy = nvy;
+                verr = ve;
                 c_last = i_pos;
                 kind = kd;
                 j_sel = js;
@@ -431,10 +482,12 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
     const float cap = (float)dm.z;
     float vxf, vyf;
     int c_last, kind, j_sel;
-    const bool feasible = lp2_target_runahead_act<SmemCons<float>>(cons, cnt, cap, (float)dm.x, (float)dm.y, vxf, vyf,
-                                                                  c_last, kind, j_sel, 0xFFFFFFFFu, enabled);
+    bool shaky = false;
+    const bool feasible = lp2_target_runahead_act<SmemCons<float>>(cons, cerr, THREADS, cnt, cap, (float)dm.x,
+                                                                  (float)dm.y, vxf, vyf, c_last, kind, j_sel, shaky,
+                                                                  0xFFFFFFFFu, enabled);
     if (!enabled) return;
-    bool certified = feasible && kind <= 2 && c_last >= 0;
+    bool certified = feasible && !shaky && kind <= 2 && c_last >= 0;
     double vx = 0.0, vy = 0.0;
     if (certified) {
         const double tx = dm.x, ty = dm.y;

@@ -115,11 +115,13 @@ def test_random_step_matches_oracle(seed):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2, 3, 5, 8, 13, 21])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 5, 8, 13, 21, 1399])
 def test_certificate_refuses_what_it_cannot_decide(seed):
     """Crowds that sit ON the decisions of the certified FP32 solve (tests/soak/soak_cert_adversarial.py:
     exact lattices, discs exactly touching, identical / mirrored / zero velocities, agents at their
-    goal): cert32 == mixed bit for bit over three frames, and f64 == the oracle on the first."""
+    goal): cert32 == mixed bit for bit over three frames, and f64 == the oracle on the first. (Seed 1399:
+    duplicated half-planes on which the reference's incremental LP gives up by FP64 rounding although
+    the LP is feasible -- the case that made the certificate check the path, not only the result.)"""
     import os
     import sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "soak"))
