@@ -143,13 +143,13 @@ __device__ __forceinline__ bool vo_exit_cond(float rpx, float rpy, float rvx, fl
 // duplicated half-planes of a symmetric crowd, three lines through one point -- its result is
 // whatever its rounding says, and only the FP64 kernels can reproduce that.
 template <typename V>
-__device__ __forceinline__ bool lp1_target_act(const V &view, const __half *cerr, int estride, int i_pos, float cap,
-                                               float tx, float ty, float &ox, float &oy, int &kind, int &j_sel,
-                                               float &verr, bool &shaky)
+__device__ __forceinline__ bool lp1_target_act(const V &view, float emax, int i_pos, float cap, float tx, float ty,
+                                               float &ox, float &oy, int &kind, int &j_sel, float &verr,
+                                               bool &shaky)
 {
     float px, py, nx, ny;
     view.get(i_pos, px, py, nx, ny);
-    const float ei = __half2float(cerr[i_pos * estride]);
+    const float ei = emax; // (the agent's LARGEST half-plane error bound stands in for each one's own: no loads here)
     const float dx = -ny, dy = nx;
     const float pd = __fmaf_rn(px, dx, py * dy);
     const float disc = __fmaf_rn(pd, pd, cap * cap) - __fmaf_rn(px, px, py * py);
@@ -157,6 +157,7 @@ __device__ __forceinline__ bool lp1_target_act(const V &view, const __half *cerr
     const float sq = disc * rsqrtf(fmaxf(disc, 1e-30f));
     shaky = shaky || sq < CERT_CROSS_MIN * cap; // the line grazes the disc: K:86 within rounding, end points ill-conditioned
     const float ed = ei * cap * __fdividef(1.0f, fmaxf(sq, 1e-20f)); // error of a disc end point
+    const float eij = 2.0f * emax;
     float t_left = -pd - sq, t_right = -pd + sq;
     float el = ed, er = ed; // error bounds of the two ends as they stand
     int jl = -1, jr = -1;
@@ -165,7 +166,6 @@ __device__ __forceinline__ bool lp1_target_act(const V &view, const __half *cerr
     for (int j_pos = 0; j_pos < i_pos; ++j_pos) {
         float qx, qy, mx, my;
         view.get(j_pos, qx, qy, mx, my);
-        const float eij = ei + __half2float(cerr[j_pos * estride]);
         const float a = __fmaf_rn(dx, mx, dy * my);
         const float b = __fmaf_rn(qx - px, mx, (qy - py) * my);
         const bool par = fabsf(a) <= 1e-6f;
@@ -216,10 +216,9 @@ __device__ __forceinline__ bool lp1_target_act(const V &view, const __half *cerr
 // ... constraints, which do not depend on who computes them, so a scan or a 1-D solve that is clear here
 // is decided the same way by the reference.
 template <typename V>
-__device__ __forceinline__ bool lp2_target_runahead_act(const V &view, const __half *cerr, int estride, int k,
-                                                        float cap, float tx, float ty, float &vx, float &vy,
-                                                        int &c_last, int &kind, int &j_sel, bool &shaky,
-                                                        unsigned live, bool enabled)
+__device__ __forceinline__ bool lp2_target_runahead_act(const V &view, float emax, int k, float cap, float tx,
+                                                        float ty, float &vx, float &vy, int &c_last, int &kind,
+                                                        int &j_sel, bool &shaky, unsigned live, bool enabled)
 {
     const float t2 = __fmaf_rn(tx, tx, ty * ty);
     if (t2 > cap * cap) {
@@ -252,7 +251,7 @@ __device__ __forceinline__ bool lp2_target_runahead_act(const V &view, const __h
                     const float slack = __fmaf_rn(vx - px, nx, (vy - py) * ny);
                     const bool valid = i_pos + u < k;
                     m |= (slack < 0.0f && valid) ? (1u << u) : 0u;
-                    amb |= (!(fabsf(slack) > __half2float(cerr[p * estride]) + verr) && valid) ? (1u << u) : 0u;
+                    amb |= (!(fabsf(slack) > emax + verr) && valid) ? (1u << u) : 0u;
                 }
                 // the reference examines the positions up to and including the first violated one at this v
                 const unsigned seen = m ? ((2u << (__ffs(m) - 1)) - 1u) : 0xFu;
@@ -269,7 +268,7 @@ __device__ __forceinline__ bool lp2_target_runahead_act(const V &view, const __h
         if (found) {
             float nvx, nvy, ve = 0.0f;
             int kd, js;
-            if (lp1_target_act<V>(view, cerr, estride, i_pos, cap, tx, ty, nvx, nvy, kd, js, ve, shaky)) {
+            if (lp1_target_act<V>(view, emax, i_pos, cap, tx, ty, nvx, nvy, kd, js, ve, shaky)) {
                 vx = nvx;
                 vy = nvy;
                 verr = ve;
@@ -335,7 +334,8 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
     // (error bounds as halves rounded UP, insertion order in registers: 18 bytes per half-plane, so that
     //  SIX blocks of 128 agents fit an SM's shared memory -- with 21 bytes it was five)
     __half *sm_err = reinterpret_cast<__half *>(sm_cons + MAXN * THREADS);
-    __shared__ int sm_task[THREADS];
+    __shared__ u8 sm_task[THREADS];     // (THREADS <= 256)
+    __shared__ float sm_emax[THREADS];  // each agent's largest half-plane error bound, for its LP task
     __shared__ int sm_bcnt[CERT_TASK_BUCKETS];
     if (threadIdx.x < CERT_TASK_BUCKETS) sm_bcnt[threadIdx.x] = 0;
     __syncthreads();
@@ -379,6 +379,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
             }
             bool built = true, unclear = false;
             int nviol = 0;
+            float emax = 0.0f;
             {   // FP32 half-planes in shuffled order, each with its error bound against |v| <= cap
                 const float hm = (float)P.half_margin;
                 const float ri = me_rec.rc.x + hm;
@@ -421,6 +422,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                     const float reach = cap + fabsf(px) + fabsf(py);
                     const float e = __fmaf_rn(f, eu, __fmaf_rn(en, reach, (CERT_SAFETY * 4.0f * CERT_EPS) * (reach + mz)));
                     cerr[pos * THREADS] = __float2half_ru(e); // (an infinite bound stays infinite)
+                    emax = fmaxf(emax, e);
                     const float slack = __fmaf_rn(v0x - px, nx, (v0y - py) * ny);
                     nviol += slack < -e ? 1 : 0;
                     unclear = unclear || !(fabsf(slack) > e); // (also catches an infinite error bound)
@@ -450,6 +452,7 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
                 // the same count share a warp, so a warp's round count is close to what its lanes need
                 my_bucket = min(nviol, CERT_TASK_BUCKETS) - 1;
                 my_rank = atomicAdd(&sm_bcnt[my_bucket], 1);
+                sm_emax[threadIdx.x] = emax;
             }
         }
     }
@@ -463,13 +466,13 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
             if (b < my_bucket) before += c;
             ntask += c;
         }
-        if (my_bucket >= 0) sm_task[before + my_rank] = threadIdx.x;
+        if (my_bucket >= 0) sm_task[before + my_rank] = (u8)threadIdx.x;
     }
     __syncthreads();
     // ---- phase B: thread t takes task t ----
     if ((int)(threadIdx.x & ~31u) >= ntask) return; // whole warp without a task
     const bool enabled = (int)threadIdx.x < ntask;
-    const int a = enabled ? sm_task[threadIdx.x] : 0; // the agent's thread slot in shared memory
+    const int a = enabled ? (int)sm_task[threadIdx.x] : 0; // the agent's thread slot in shared memory
     const int s = s_base + a;
     const int row = s_row[s];
     const int cnt = enabled ? (int)nb_cnt[s] : 0;
@@ -483,9 +486,9 @@ k_solve_cert(GridPlan *__restrict__ plan, StepParams P, const NbRec<float> *__re
     float vxf, vyf;
     int c_last, kind, j_sel;
     bool shaky = false;
-    const bool feasible = lp2_target_runahead_act<SmemCons<float>>(cons, cerr, THREADS, cnt, cap, (float)dm.x,
-                                                                  (float)dm.y, vxf, vyf, c_last, kind, j_sel, shaky,
-                                                                  0xFFFFFFFFu, enabled);
+    const bool feasible = lp2_target_runahead_act<SmemCons<float>>(cons, sm_emax[a], cnt, cap, (float)dm.x, (float)dm.y,
+                                                                  vxf, vyf, c_last, kind, j_sel, shaky, 0xFFFFFFFFu,
+                                                                  enabled);
     if (!enabled) return;
     bool certified = feasible && !shaky && kind <= 2 && c_last >= 0;
     double vx = 0.0, vy = 0.0;
