@@ -1,9 +1,11 @@
 """Soak of the randomised parity tests over many more seeds than the test-suite runs
 (development tooling; imports the tests, which use the oracle):
-    python tests/soak/soak_fuzz.py [first_seed] [count]
+    python tests/soak/soak_fuzz.py [first_seed] [count] [adversarial]
 Per seed: tests/test_gpu_fuzz.py::test_random_step_matches_oracle, then five resident frames
 (radius-hint fast pass, exact-search queue, row reordering every 2 frames) of the same random
-crowd in f64 and mixed, every frame against the oracle fed the device's own state."""
+crowd in f64 and mixed, every frame against the oracle fed the device's own state. With
+"adversarial" the crowds are those of soak_cert_adversarial.py (exact lattices, touching discs,
+identical / mirrored velocities) instead of the random ones."""
 import os
 import sys
 import time
@@ -22,11 +24,18 @@ from paper_2008_11578_b200 import SimState, Simulation  # noqa: E402
 
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 400
+adv = len(sys.argv) > 3 and sys.argv[3] == "adversarial"
+if adv:
+    sys.path.insert(0, os.path.join(ROOT, "tests", "soak"))
+    from soak_cert_adversarial import adversarial  # noqa: E402
 bad, t0 = [], time.time()
 for seed in range(first, first + count):
     try:
-        F.test_random_step_matches_oracle(seed)
-        st, cfg = F.random_case(seed)
+        if adv:
+            st, cfg = adversarial(seed)
+        else:
+            F.test_random_step_matches_oracle(seed)
+            st, cfg = F.random_case(seed)
         n = st.active_count
         for precision in ("f64", "mixed"):
             with Simulation(cfg, capacity=n, precision=precision, remove_arrivals=False) as sim:
