@@ -23,7 +23,11 @@ from paper_2008_11578_b200.synth import blobs_crowd, plaza_crowd  # noqa: E402
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 bad, t0, agents, queued = [], time.time(), 0, 0
+BUDGET = float(os.environ.get("ORCA_SOAK_SECONDS", "0"))
 for seed in range(first, first + count):
+    if BUDGET and time.time() - t0 > BUDGET:     # ORCA_SOAK_SECONDS: stop here, report what ran
+        count = seed - first
+        break
     rng = np.random.default_rng(10_000 + seed)
     kind = seed % 4
     if kind == 3:

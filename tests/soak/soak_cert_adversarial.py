@@ -81,9 +81,13 @@ def main():
     first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
     count = int(sys.argv[2]) if len(sys.argv) > 2 else 200
     bad, t0, agents, queued, ran = [], time.time(), 0, 0, 0
+    budget = float(os.environ.get("ORCA_SOAK_SECONDS", "0"))   # stop after this many seconds, report what ran
     if len(sys.argv) > 3 and sys.argv[3] == "oracle":
         from oracle import oracle as O
         for seed in range(first, first + count):
+            if budget and time.time() - t0 > budget:
+                count = seed - first
+                break
             st, cfg = adversarial(seed)
             n = st.active_count
             try:
@@ -108,6 +112,9 @@ def main():
               "in", round(time.time() - t0), "s;", agents, "agents")
         sys.exit(1 if bad else 0)
     for seed in range(first, first + count):
+        if budget and time.time() - t0 > budget:
+            count = seed - first
+            break
         st, cfg = adversarial(seed)
         n = st.active_count
         try:

@@ -29,7 +29,11 @@ if adv:
     sys.path.insert(0, os.path.join(ROOT, "tests", "soak"))
     from soak_cert_adversarial import adversarial  # noqa: E402
 bad, t0 = [], time.time()
+BUDGET = float(os.environ.get("ORCA_SOAK_SECONDS", "0"))
 for seed in range(first, first + count):
+    if BUDGET and time.time() - t0 > BUDGET:     # ORCA_SOAK_SECONDS: stop here, report what ran
+        count = seed - first
+        break
     try:
         if adv:
             st, cfg = adversarial(seed)

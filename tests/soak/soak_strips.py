@@ -24,7 +24,11 @@ first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 mode = sys.argv[3] if len(sys.argv) > 3 else "sendrecv"
 bad, t0, ran = [], time.time(), 0
+BUDGET = float(os.environ.get("ORCA_SOAK_SECONDS", "0"))
 for seed in range(first, first + count):
+    if BUDGET and time.time() - t0 > BUDGET:     # ORCA_SOAK_SECONDS: stop here, report what ran
+        count = seed - first
+        break
     rng = np.random.default_rng(seed)
     world = int(rng.integers(2, 5))
     precision = ["f64", "mixed"][seed % 2]
