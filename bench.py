@@ -412,6 +412,11 @@ def run_ours(args):
     sim.run(args.steps)
     stage_ms, covered = sim.stage_ms()
     sim.profile_stages(False)
+    stage_pass_error = None
+    try:                 # a sticky device-side error of the second pass (e.g. the reference's coincident-centres
+        sim.sync()       # error deep into a jammed FP32-state run) is reported, not hidden
+    except Exception as e:
+        stage_pass_error = str(e)[:200]
     stage_ms = {k: v / max(covered, 1) for k, v in stage_ms.items()}
     stage_bytes = {"bins": BINS_BYTES_PER_AGENT, "gather": GATHER_BYTES_PER_AGENT,
                    "solve": SOLVE_BYTES_PER_AGENT}
@@ -423,7 +428,8 @@ def run_ours(args):
     if args.resident_only:
         print(json.dumps({"metric": "agent_steps_per_s", "value": value, "ms_per_step": ms_step,
                           "stages_ms": stage_ms, "gpu_launches": launches, "n": n,
-                          "precision": args.precision, "note": "resident-only run"}), flush=True)
+                          "precision": args.precision, "note": "resident-only run",
+                          **({"stages_error": stage_pass_error} if stage_pass_error else {})}), flush=True)
         return
 
     # ---- e2e: engine.step(state, config), host in / host out -------------------
@@ -553,6 +559,7 @@ def run_ours(args):
         "stages_note": "per-stage CUDA events, plain launches, the stages one after the other; the timed step replays "
                        "a CUDA graph in which gather / solve / fallback run as a two-chunk pipeline on two streams, "
                        "so the stages add up to more than ms_per_step",
+        **({"stages_error": stage_pass_error} if stage_pass_error else {}),
         "extras": extras,
         "roofline": {"bound": "hbm", "kernel": dom_kernel,
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
