@@ -20,7 +20,11 @@ from paper_2008_11578_b200.synth import plaza_crowd  # noqa: E402
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 60
 bad, t0 = [], time.time()
+BUDGET = float(os.environ.get("ORCA_SOAK_SECONDS", "0"))
 for seed in range(first, first + count):
+    if BUDGET and time.time() - t0 > BUDGET:     # ORCA_SOAK_SECONDS: stop here, report what ran
+        count = seed - first
+        break
     rng = np.random.default_rng(seed)
     n_ped = int(rng.integers(5000, 60000))
     n_veh = int(rng.integers(0, n_ped // 8))

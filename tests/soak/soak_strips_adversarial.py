@@ -24,7 +24,11 @@ def main():
     first = int(sys.argv[1]) if len(sys.argv) > 1 else 0
     count = int(sys.argv[2]) if len(sys.argv) > 2 else 100
     bad, t0, ran = [], time.time(), 0
+    budget = float(os.environ.get("ORCA_SOAK_SECONDS", "0"))   # stop after this many seconds, report what ran
     for seed in range(first, first + count):
+        if budget and time.time() - t0 > budget:
+            count = seed - first
+            break
         st, cfg = adversarial(seed)
         st.goal_tols[:] = 0.25
         n, steps = st.active_count, 8
